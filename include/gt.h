@@ -1,0 +1,146 @@
+/*
+ * gt.h — C ABI of the B200-native CSR->CSC graph transposition library
+ * (paper_2501_06872_b200/libgt.so).
+ *
+ * The reference (arxiv 2501.06872, package `potra`) exposes this path as
+ * Python functions over numpy arrays; there is no FFI in the reference.  The
+ * entry points below are what a reference-side binding (ctypes stub shown in
+ * INTEGRATION.md) would call in place of the numba kernels:
+ *
+ *   gt_transpose         replaces transpose_atomic / transpose_potra steps 1-3
+ *                        + sort_neighbor_lists  (baselines.py:168-209,
+ *                        hlh.py:441-588, baselines.py:457-475); output equals
+ *                        transpose_oracle (graph.py:136-148) bit for bit.
+ *   gt_transpose_host    same, host buffers in and out (H2D + kernels + D2H).
+ *   gt_prefix_sum        prefix_sum_parallel (baselines.py:116-127).
+ *   gt_edge_balanced_bounds  edge_balanced_vertex_bounds (_nb.py:118-132),
+ *                        the source-range sharding rule for multi-GPU runs.
+ *   gt_shard_*           multi-GPU building blocks (sender-side stable partition
+ *                        by destination owner, receiver-side transpose of the
+ *                        received records); the exchange itself is NCCL.
+ *
+ * Array conventions (graph.py:34-36, 59-80): offsets are uint64[V+1] with
+ * offsets[0]=0 and offsets[V]=E; neighbour IDs are uint32[E] (V <= 2^32).
+ * Every neighbour list of the output is ascending by source ID.
+ *
+ * Return codes mirror the reference's exceptions:
+ *   GT_OK (0); GT_EINVAL (ValueError: bad arguments, _nb.py:112-113);
+ *   GT_EOVERFLOW (CounterOverflowError: an in-degree >= 2^32,
+ *   baselines.py:189-192); GT_ENOMEM (MemoryError / FootprintError precheck,
+ *   errors.py:17-26); GT_ECUDA (a CUDA runtime failure); GT_ENODEV (no GPU).
+ * gt_last_error() returns a thread-local message for the last failure.
+ *
+ * Device pointers are CUDA global-memory pointers; `stream` is a cudaStream_t
+ * (NULL = legacy default stream).  All calls are stream-ordered; the caller
+ * owns every buffer.  No torch types cross this boundary.
+ */
+#ifndef GT_H_
+#define GT_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GT_OK 0
+#define GT_EINVAL (-1)
+#define GT_EOVERFLOW (-2)
+#define GT_ENOMEM (-3)
+#define GT_ECUDA (-4)
+#define GT_ENODEV (-5)
+
+#define GT_ABI_VERSION 1
+
+/* Per-call accounting; mirrors TransposeOutput.phase_times / aux_footprint_bytes
+ * (baselines.py:39-53).  Times are device time from CUDA events, in ms, filled
+ * only when stats != NULL (timing adds event records to the stream). */
+typedef struct gt_stats {
+    double ms_total;       /* whole transpose                                  */
+    double ms_step1;       /* level-1 count + partition (source-ordered pass)  */
+    double ms_step2;       /* level-2 chunk sort by middle digit               */
+    double ms_step3;       /* final per-bucket sort + CSC offsets              */
+    uint64_t workspace_bytes; /* aux device memory used (aux_footprint_bytes)  */
+    int32_t bits[3];       /* destination-ID digit split per level             */
+    int32_t rank_mode;     /* 0 = lane-ordered smem atomics, 1 = safe OR-mask  */
+    uint64_t n_big_buckets;/* final buckets that took the multi-CTA path       */
+    uint64_t n_launches;   /* kernels this call launched                       */
+} gt_stats;
+
+/* Library / device info. */
+int gt_abi_version(void);
+const char *gt_last_error(void);
+
+/* Workspace bytes gt_transpose needs for a graph of this size (0 allowed). */
+int gt_workspace_size(uint64_t num_vertices, uint64_t num_edges, uint64_t *bytes);
+
+/* Device-resident CSR -> CSC.  `workspace` may be NULL: the library then uses
+ * an internal cached device allocation (reported in stats->workspace_bytes). */
+int gt_transpose(const uint64_t *offsets, const uint32_t *edges,
+                 uint64_t num_vertices, uint64_t num_edges,
+                 uint64_t *t_offsets, uint32_t *t_edges,
+                 void *workspace, uint64_t workspace_bytes,
+                 void *stream, gt_stats *stats);
+
+/* Host-resident CSR -> CSC on `device` (H2D copy, transpose, D2H copy).  Host
+ * buffers may be pageable or pinned. */
+int gt_transpose_host(const uint64_t *h_offsets, const uint32_t *h_edges,
+                      uint64_t num_vertices, uint64_t num_edges,
+                      uint64_t *h_t_offsets, uint32_t *h_t_edges,
+                      int device, gt_stats *stats);
+
+/* Exclusive prefix sum of uint32 counts into uint64[n+1] (out[n] = total). */
+int gt_prefix_sum(const uint32_t *counts, uint64_t n, uint64_t *out, void *stream);
+
+/* Host helper: edge_balanced_vertex_bounds (_nb.py:118-132) on host offsets. */
+int gt_edge_balanced_bounds(const uint64_t *h_offsets, uint64_t num_vertices,
+                            int64_t parts, int64_t *h_bounds);
+
+/* Smem-atomic lane-order self-test.  Runs `trials`
+ * randomized warp-instructions on the current device; *violations = count of
+ * returns that were not lane-ascending.  gt_transpose runs it once per device
+ * and falls back to the OR-mask ranking when it fails. */
+int gt_selftest_rank_order(uint64_t trials, uint64_t *violations);
+
+/* Force the ranking mode: -1 auto (self-test), 0 atomics, 1 safe OR-mask. */
+int gt_set_rank_mode(int mode);
+
+/* ---- multi-GPU building blocks (one process per GPU; NCCL moves records) --
+ * Sender: stable partition of this rank's source shard (sources
+ * [src_begin, src_end), i.e. edges [offsets[src_begin], offsets[src_end])) into
+ * `parts` destination-owner ranges dst_bounds[0..parts] (vertex IDs).  Writes
+ * records (src, dst) as uint32 pairs grouped by owner, each group in CSR
+ * order, and counts[p] = records for owner p.  `offsets`/`edges` are the
+ * rank's device copies of the full offsets and its edge slice. */
+int gt_shard_partition(const uint64_t *offsets, const uint32_t *edges_slice,
+                       uint64_t num_vertices, uint64_t src_begin, uint64_t src_end,
+                       const uint64_t *h_dst_bounds, int parts,
+                       uint32_t *records_out /* 2 * slice edges */,
+                       uint64_t *h_counts_out /* parts */,
+                       void *stream);
+
+/* Receiver: records (src, dst) for destinations [dst_begin, dst_end), already
+ * concatenated in sender-rank order (= ascending source order), transposed
+ * into the local CSC slice: t_offsets_local[0..n_local] (global positions
+ * start at `global_base`) and t_edges_local[0..num_records). */
+int gt_shard_transpose(const uint32_t *records, uint64_t num_records,
+                       uint64_t dst_begin, uint64_t dst_end, uint64_t global_base,
+                       uint64_t *t_offsets_local, uint32_t *t_edges_local,
+                       void *stream, gt_stats *stats);
+
+/* ---- seeded synthetic inputs (BASELINE.json configs), generated on device --
+ * Deterministic counter-based generators; identical to the numpy versions in
+ * paper_2501_06872_b200/gen.py.  Pairs are written as src[i], dst[i]. */
+int gt_gen_rmat(uint64_t scale, uint64_t num_edges, uint64_t seed, int permute,
+                uint32_t *src, uint32_t *dst, void *stream);
+int gt_gen_er(uint64_t num_vertices, uint64_t num_edges, uint64_t seed,
+              uint32_t *src, uint32_t *dst, void *stream);
+/* COO pairs -> CSR with every list ascending by destination (duplicates kept).
+ * Consumes src/dst (they are overwritten as scratch). */
+int gt_build_csr(uint32_t *src, uint32_t *dst, uint64_t num_vertices, uint64_t num_edges,
+                 uint64_t *offsets, uint32_t *edges, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GT_H_ */

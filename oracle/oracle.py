@@ -1,0 +1,162 @@
+"""TEST INFRASTRUCTURE ONLY — CPU oracle for the transposition path.
+
+Imported by tests/, __graft_entry__.smoke() and bench.py's CPU-baseline leg;
+never by the product package.  Two restatements of the reference algorithm:
+
+* ``transpose_np`` — numpy restatement of ``transpose_oracle``
+  (pkg/src/potra/graph.py:136-148, via from_edge_pairs graph.py:104-122 and
+  _owners graph.py:125-129): owners = repeat(arange(V), degrees); a *stable*
+  argsort by endpoint of the CSR-ordered stream equals the reference's
+  lexsort((owner, endpoint)) because owners are non-decreasing in CSR order;
+  offsets = bincount + cumsum.
+* ``libgt_oracle.so`` (gt_oracle.c, built by oracle/Makefile): serial stable
+  counting sort (same order, 64-bit cursors) plus OpenMP ports of the
+  reference's parallel CPU algorithms used as the CPU baseline:
+  transpose_scantrans (baselines.py:265-312), transpose_atomic
+  (baselines.py:168-209) and sort_neighbor_lists (baselines.py:457-475).
+
+Pinned against the reference: tests/golden/ holds outputs of the real
+``potra.transpose_oracle`` (made by tests/golden/make_golden.py, which imports
+/root/reference); tests/test_oracle.py checks both restatements against them.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+LIB = HERE / "libgt_oracle.so"
+
+GTO_OK, GTO_EINVAL, GTO_EOVERFLOW, GTO_ENOMEM = 0, -1, -2, -3
+
+
+def transpose_np(offsets: np.ndarray, edges: np.ndarray, num_vertices: int):
+    """numpy restatement of transpose_oracle -> (t_offsets uint64, t_edges uint32)."""
+    offsets = np.asarray(offsets, dtype=np.uint64)
+    edges = np.asarray(edges)
+    deg = np.diff(offsets.view(np.int64))
+    owners = np.repeat(np.arange(num_vertices, dtype=np.uint32), deg)
+    order = np.argsort(edges, kind="stable")
+    t_edges = np.ascontiguousarray(owners[order].astype(np.uint32))
+    counts = np.bincount(edges.astype(np.int64), minlength=num_vertices)
+    t_offsets = np.zeros(num_vertices + 1, dtype=np.uint64)
+    np.cumsum(counts, out=t_offsets[1:])
+    return t_offsets, t_edges
+
+
+_lib = None
+
+
+def build():
+    """Compile gt_oracle.c into oracle/libgt_oracle.so (gcc, OpenMP)."""
+    subprocess.run(["make", "-s", "-C", str(HERE)], check=True)
+
+
+def load():
+    global _lib
+    if _lib is None:
+        if not LIB.exists():
+            build()
+        lib = ctypes.CDLL(str(LIB))
+        vp, u64, i = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int
+        lib.gto_transpose_serial.argtypes = [vp, vp, u64, u64, vp, vp]
+        lib.gto_transpose_scantrans.argtypes = [vp, vp, u64, u64, vp, vp, i]
+        lib.gto_transpose_atomic.argtypes = [vp, vp, u64, u64, vp, vp, i, u64]
+        lib.gto_sort_lists.argtypes = [vp, u64, vp, i]
+        lib.gto_scan_exclusive.argtypes = [vp, u64, vp, i]
+        lib.gto_edge_balanced_bounds.argtypes = [vp, u64, ctypes.c_int64, vp]
+        lib.gto_edge_balanced_bounds.restype = None
+        for f in ("gto_transpose_serial", "gto_transpose_scantrans", "gto_transpose_atomic", "gto_sort_lists",
+                  "gto_scan_exclusive", "gto_max_threads"):
+            getattr(lib, f).restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _check(rc: int, what: str):
+    if rc == GTO_OK:
+        return
+    if rc == GTO_EOVERFLOW:
+        raise OverflowError(f"{what}: 32-bit counter overflow")
+    if rc == GTO_EINVAL:
+        raise ValueError(what)
+    raise MemoryError(what)
+
+
+def transpose_c(offsets, edges, num_vertices: int):
+    """Serial stable counting sort in C (the checker for large sizes)."""
+    lib = load()
+    off = np.ascontiguousarray(offsets, dtype=np.uint64)
+    e = np.ascontiguousarray(edges, dtype=np.uint32)
+    t_off = np.empty(num_vertices + 1, dtype=np.uint64)
+    t_e = np.empty(e.shape[0], dtype=np.uint32)
+    _check(lib.gto_transpose_serial(_p(off), _p(e), num_vertices, e.shape[0], _p(t_off), _p(t_e)),
+           "gto_transpose_serial")
+    return t_off, t_e
+
+
+def transpose_scantrans_c(offsets, edges, num_vertices: int, threads: int):
+    """OpenMP port of transpose_scantrans (sorted by construction)."""
+    lib = load()
+    off = np.ascontiguousarray(offsets, dtype=np.uint64)
+    e = np.ascontiguousarray(edges, dtype=np.uint32)
+    t_off = np.empty(num_vertices + 1, dtype=np.uint64)
+    t_e = np.empty(e.shape[0], dtype=np.uint32)
+    _check(lib.gto_transpose_scantrans(_p(off), _p(e), num_vertices, e.shape[0], _p(t_off), _p(t_e), threads),
+           "gto_transpose_scantrans")
+    return t_off, t_e
+
+
+def transpose_atomic_sorted_c(offsets, edges, num_vertices: int, threads: int, partition_edges: int = 1 << 18):
+    """OpenMP port of transpose_atomic followed by sort_neighbor_lists."""
+    lib = load()
+    off = np.ascontiguousarray(offsets, dtype=np.uint64)
+    e = np.ascontiguousarray(edges, dtype=np.uint32)
+    t_off = np.empty(num_vertices + 1, dtype=np.uint64)
+    t_e = np.empty(e.shape[0], dtype=np.uint32)
+    _check(lib.gto_transpose_atomic(_p(off), _p(e), num_vertices, e.shape[0], _p(t_off), _p(t_e), threads,
+                                    partition_edges), "gto_transpose_atomic")
+    _check(lib.gto_sort_lists(_p(t_off), num_vertices, _p(t_e), threads), "gto_sort_lists")
+    return t_off, t_e
+
+
+def edge_balanced_bounds_c(offsets, parts: int):
+    lib = load()
+    off = np.ascontiguousarray(offsets, dtype=np.uint64)
+    parts = max(1, int(parts))
+    out = np.empty(parts + 1, dtype=np.int64)
+    lib.gto_edge_balanced_bounds(_p(off), off.shape[0] - 1, parts, _p(out))
+    return out
+
+
+def edge_balanced_bounds_np(offsets, parts: int):
+    """Restates edge_balanced_vertex_bounds (_nb.py:118-132)."""
+    offsets = np.asarray(offsets, dtype=np.uint64)
+    nv = offsets.shape[0] - 1
+    ne = int(offsets[-1])
+    parts = max(1, parts)
+    targets = (np.arange(parts + 1, dtype=np.int64) * ne) // parts
+    bounds = np.searchsorted(offsets, targets.astype(np.uint64), side="left").astype(np.int64)
+    bounds[0] = 0
+    bounds[-1] = nv
+    return bounds
+
+
+def max_threads() -> int:
+    return int(load().gto_max_threads())
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1

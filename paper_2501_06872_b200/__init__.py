@@ -1,0 +1,40 @@
+"""B200-native CSR->CSC graph transposition (the hot path of arxiv 2501.06872, PoTra).
+
+Public API mirrors the reference package ``potra`` for this path:
+``CsrGraph``, ``TransposeOutput``, the error types, and ``transpose_gpu`` — a
+drop-in for ``transpose_atomic``/``transpose_potra`` + ``sort_neighbor_lists``
+whose output equals ``transpose_oracle``.
+"""
+
+from .errors import CounterOverflowError, FootprintError, GpuUnavailableError, GraphFormatError
+from .graph import CsrGraph, edge_id_dtype, flip_orientation, lists_are_sorted
+from .transpose import (
+    TransposeOutput,
+    edge_balanced_vertex_bounds,
+    prefix_sum_gpu,
+    selftest_rank_order,
+    set_rank_mode,
+    transpose_device,
+    transpose_gpu,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "CsrGraph",
+    "TransposeOutput",
+    "transpose_gpu",
+    "transpose_device",
+    "prefix_sum_gpu",
+    "edge_balanced_vertex_bounds",
+    "selftest_rank_order",
+    "set_rank_mode",
+    "edge_id_dtype",
+    "flip_orientation",
+    "lists_are_sorted",
+    "CounterOverflowError",
+    "FootprintError",
+    "GraphFormatError",
+    "GpuUnavailableError",
+    "__version__",
+]

@@ -1,0 +1,112 @@
+"""ctypes binding of libgt.so (the C ABI declared in include/gt.h).
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (or
+``make -C paper_2501_06872_b200/csrc``).  There is no fallback: if the library
+cannot be loaded every GPU entry point raises :class:`GpuUnavailableError`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from pathlib import Path
+
+from .errors import CounterOverflowError, FootprintError, GpuUnavailableError
+
+__all__ = ["lib", "GtStats", "check", "LIB_PATH", "SYMBOLS", "load"]
+
+LIB_PATH = Path(__file__).resolve().parent / "libgt.so"
+
+GT_OK, GT_EINVAL, GT_EOVERFLOW, GT_ENOMEM, GT_ECUDA, GT_ENODEV = 0, -1, -2, -3, -4, -5
+
+
+class GtStats(ctypes.Structure):
+    _fields_ = [
+        ("ms_total", ctypes.c_double),
+        ("ms_step1", ctypes.c_double),
+        ("ms_step2", ctypes.c_double),
+        ("ms_step3", ctypes.c_double),
+        ("workspace_bytes", ctypes.c_uint64),
+        ("bits", ctypes.c_int32 * 3),
+        ("rank_mode", ctypes.c_int32),
+        ("n_big_buckets", ctypes.c_uint64),
+        ("n_launches", ctypes.c_uint64),
+    ]
+
+
+_u64, _i64, _int, _vp = ctypes.c_uint64, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
+_stats_p = ctypes.POINTER(GtStats)
+
+# name -> (restype, argtypes); must match include/gt.h exactly
+SYMBOLS = {
+    "gt_abi_version": (_int, []),
+    "gt_last_error": (ctypes.c_char_p, []),
+    "gt_workspace_size": (_int, [_u64, _u64, ctypes.POINTER(_u64)]),
+    "gt_transpose": (_int, [_vp, _vp, _u64, _u64, _vp, _vp, _vp, _u64, _vp, _stats_p]),
+    "gt_transpose_host": (_int, [_vp, _vp, _u64, _u64, _vp, _vp, _int, _stats_p]),
+    "gt_prefix_sum": (_int, [_vp, _u64, _vp, _vp]),
+    "gt_edge_balanced_bounds": (_int, [_vp, _u64, _i64, _vp]),
+    "gt_selftest_rank_order": (_int, [_u64, ctypes.POINTER(_u64)]),
+    "gt_set_rank_mode": (_int, [_int]),
+    "gt_shard_partition": (_int, [_vp, _vp, _u64, _u64, _u64, _vp, _int, _vp, _vp, _vp]),
+    "gt_shard_transpose": (_int, [_vp, _u64, _u64, _u64, _u64, _vp, _vp, _vp, _stats_p]),
+    "gt_gen_rmat": (_int, [_u64, _u64, _u64, _int, _vp, _vp, _vp]),
+    "gt_gen_er": (_int, [_u64, _u64, _u64, _vp, _vp, _vp]),
+    "gt_build_csr": (_int, [_vp, _vp, _u64, _u64, _vp, _vp, _vp]),
+}
+
+_lock = threading.Lock()
+_lib = None
+_load_error: str | None = None
+
+
+def load():
+    """Load libgt.so once; raise GpuUnavailableError when it is missing."""
+    global _lib, _load_error
+    with _lock:
+        if _lib is not None:
+            return _lib
+        path = os.environ.get("GT_LIBRARY", str(LIB_PATH))
+        try:
+            handle = ctypes.CDLL(path, mode=ctypes.RTLD_GLOBAL)
+        except OSError as exc:
+            _load_error = f"cannot load {path}: {exc} (run __graft_entry__.build())"
+            raise GpuUnavailableError(_load_error) from None
+        for name, (res, args) in SYMBOLS.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        if handle.gt_abi_version() != 1:
+            raise GpuUnavailableError("libgt.so ABI version mismatch")
+        _lib = handle
+        return _lib
+
+
+class _LazyLib:
+    def __getattr__(self, name):
+        return getattr(load(), name)
+
+
+lib = _LazyLib()
+
+
+def check(rc: int, what: str) -> None:
+    """Map a GT_* return code to the reference's exception types."""
+    if rc == GT_OK:
+        return
+    msg = lib.gt_last_error().decode(errors="replace")
+    text = f"{what}: {msg}"
+    if rc == GT_EINVAL:
+        raise ValueError(text)
+    if rc == GT_EOVERFLOW:
+        raise CounterOverflowError(msg)
+    if rc == GT_ENOMEM:
+        raise MemoryError(text)
+    if rc == GT_ENODEV:
+        raise GpuUnavailableError(text)
+    raise RuntimeError(text)
+
+
+def footprint_error(required: int, limit: int) -> FootprintError:
+    return FootprintError(required, limit)

@@ -1,0 +1,695 @@
+// gt_api.cu — host orchestration and the extern "C" boundary of libgt.so.
+// See include/gt.h for the contract and the reference functions each entry
+// point replaces.  No torch types cross this boundary.
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/gt.h"
+#include "gt_kernels.cuh"
+
+using namespace gt;
+
+namespace {
+
+thread_local std::string g_err;
+int g_forced_rank_mode = -1;           // -1 auto
+int g_dev_rank_mode[64];               // per device: -1 unknown, 0/1 decided
+std::once_flag g_init_flag;
+std::mutex g_mu;
+
+int set_err(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int set_err(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define GT_CUDA(call)                                                                          \
+  do {                                                                                         \
+    cudaError_t e_ = (call);                                                                   \
+    if (e_ != cudaSuccess) {                                                                   \
+      if (e_ == cudaErrorMemoryAllocation)                                                      \
+        return set_err(GT_ENOMEM, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+      return set_err(GT_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+    }                                                                                          \
+  } while (0)
+
+#define GT_LAUNCH_CHECK() GT_CUDA(cudaGetLastError())
+
+inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+inline int bits_for(uint64_t V) {  // bits to address IDs 0..V-1 (>= 1)
+  if (V <= 2) return 1;
+  return 64 - __builtin_clzll(V - 1);
+}
+
+struct Plan {
+  uint64_t V = 0, E = 0;
+  int nb = 0, a = 0, b = 0, c = 0;
+  int D1 = 1, Db = 1, Dc = 1;
+  uint64_t CT = 65536, ntiles = 0, max_chunks = 0;
+  // workspace offsets
+  uint64_t o_rec, o_tcnt, o_tbase, o_tsrc, o_cstart, o_cfirst, o_cbucket, o_segoff, o_fhist, o_fbase,
+      o_status, o_ctr, o_big, o_bigcnt, o_err, total;
+};
+
+int make_plan(uint64_t V, uint64_t E, Plan& p) {
+  p.V = V;
+  p.E = E;
+  p.nb = bits_for(V);
+  if (p.nb > 30) return set_err(GT_EINVAL, "num_vertices > 2^30 is not supported by this build");
+  const double avg = V ? (double)E / (double)V : 1.0;
+  int c = 0;
+  const double target = (double)kFCap / 3.0;
+  while (c < 8 && (double)(1u << (c + 1)) * std::max(avg, 1.0) <= target) ++c;
+  c = std::min(c, p.nb);
+  const int rem = p.nb - c;
+  int a, b;
+  if (rem <= 11) {
+    a = rem;
+    b = 0;
+  } else {
+    a = rem - rem / 2;
+    b = rem / 2;
+  }
+  if (a > 11 || b > 11) return set_err(GT_EINVAL, "digit split out of range (nb=%d)", p.nb);
+  p.a = a;
+  p.b = b;
+  p.c = c;
+  p.D1 = 1 << a;
+  p.Db = 1 << b;
+  p.Dc = 1 << c;
+  p.CT = 65536;
+  p.ntiles = (E + p.CT - 1) / p.CT;
+  while ((uint64_t)p.D1 * p.ntiles > (1ull << 24)) {
+    p.CT *= 2;
+    p.ntiles = (E + p.CT - 1) / p.CT;
+  }
+  p.max_chunks = (E + kChunk - 1) / kChunk + (uint64_t)p.D1;
+  const uint64_t nfine = (uint64_t)p.D1 * p.Db;
+  uint64_t off = 0;
+  auto take = [&](uint64_t bytes) {
+    const uint64_t o = off;
+    off = align_up(off + std::max<uint64_t>(bytes, 1), 256);
+    return o;
+  };
+  p.o_rec = take(E * 8);
+  p.o_tcnt = take((uint64_t)p.D1 * p.ntiles * 4);
+  p.o_tbase = take(((uint64_t)p.D1 * p.ntiles + 1) * 8);
+  p.o_tsrc = take(p.ntiles * 4);
+  p.o_cstart = take((uint64_t)(p.D1 + 1) * 8);
+  p.o_cfirst = take((uint64_t)(p.D1 + 1) * 4);
+  p.o_cbucket = take(p.max_chunks * 4);
+  p.o_segoff = take(p.b ? p.max_chunks * (uint64_t)(p.Db + 1) * 4 : 0);
+  p.o_fhist = take(nfine * 8);
+  p.o_fbase = take((nfine + 1) * 8);
+  const uint64_t max_scan = std::max<uint64_t>((uint64_t)p.D1 * p.ntiles, nfine) + 1;
+  p.o_status = take(((max_scan + kScanTile - 1) / kScanTile + 1) * 8);
+  p.o_ctr = take(64);
+  p.o_big = take(nfine * 4);
+  p.o_bigcnt = take(4);
+  p.o_err = take(4);
+  p.total = off;
+  return GT_OK;
+}
+
+// ---- cached device memory (workspace when the caller passes none; big-path
+// job tables).  One cache per device, grown on demand, never shrunk.
+struct Cache {
+  void* ptr = nullptr;
+  uint64_t bytes = 0;
+};
+Cache g_ws[64], g_aux[64];
+
+int cache_get(Cache& c, uint64_t bytes, void** out) {
+  if (c.bytes < bytes) {
+    if (c.ptr) cudaFree(c.ptr);
+    c.ptr = nullptr;
+    c.bytes = 0;
+    GT_CUDA(cudaMalloc(&c.ptr, bytes));
+    c.bytes = bytes;
+  }
+  *out = c.ptr;
+  return GT_OK;
+}
+
+int current_device(int* dev) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) return set_err(GT_ENODEV, "no CUDA device: %s", cudaGetErrorString(e));
+  GT_CUDA(cudaGetDevice(dev));
+  if (*dev < 0 || *dev >= 64) return set_err(GT_EINVAL, "device index out of range");
+  return GT_OK;
+}
+
+int run_selftest(uint64_t trials, uint64_t* violations, cudaStream_t st) {
+  unsigned long long* d_bad = nullptr;
+  GT_CUDA(cudaMallocAsync(&d_bad, 8, st));
+  GT_CUDA(cudaMemsetAsync(d_bad, 0, 8, st));
+  const int blocks = 148 * 2, threads = 1024;
+  const uint64_t per_launch = (uint64_t)blocks * threads * 64;
+  const uint64_t launches = std::max<uint64_t>(1, (trials + per_launch - 1) / per_launch);
+  for (uint64_t l = 0; l < launches; ++l) {
+    k_selftest_rank<<<blocks, threads, 0, st>>>(d_bad, (uint32_t)(0x9E3779B9u * (l + 1)), 64);
+    GT_LAUNCH_CHECK();
+  }
+  unsigned long long h = 0;
+  GT_CUDA(cudaMemcpyAsync(&h, d_bad, 8, cudaMemcpyDeviceToHost, st));
+  GT_CUDA(cudaFreeAsync(d_bad, st));
+  GT_CUDA(cudaStreamSynchronize(st));
+  *violations = h;
+  return GT_OK;
+}
+
+int rank_mode_for(int dev, cudaStream_t st, int* mode) {
+  if (g_forced_rank_mode >= 0) {
+    *mode = g_forced_rank_mode;
+    return GT_OK;
+  }
+  std::lock_guard<std::mutex> lk(g_mu);
+  static bool init = false;
+  if (!init) {
+    for (int i = 0; i < 64; ++i) g_dev_rank_mode[i] = -1;
+    init = true;
+  }
+  if (g_dev_rank_mode[dev] < 0) {
+    uint64_t bad = 0;
+    int rc = run_selftest(1ull << 26, &bad, st);
+    if (rc != GT_OK) return rc;
+    g_dev_rank_mode[dev] = bad ? kRankSafe : kRankAtomic;
+  }
+  *mode = g_dev_rank_mode[dev];
+  return GT_OK;
+}
+
+size_t smem_l1_place(int D, int mode) {
+  const int W = kL1Warps;
+  return (size_t)kPlaceTile * 8 + (size_t)D * 8 + (size_t)kPlaceTile * 4 + (size_t)W * D * 4 +
+         (mode == kRankSafe ? (size_t)W * D * 4 : 0) + (size_t)D * 8 + 40 * 4;
+}
+size_t smem_b1(const Plan& p, int mode) {
+  const int W = kB1Warps, D = p.Db;
+  return (size_t)kChunk * 8 + (size_t)W * D * 4 + (mode == kRankSafe ? (size_t)W * D * 4 : 0) + (size_t)D * 8 +
+         40 * 4;
+}
+size_t smem_final(const Plan& p, int mode) {
+  const int W = kFWarps, D = p.Dc;
+  return (size_t)kSegCap * 8 + (size_t)(kSegCap + 4) * 4 + (size_t)kFCap * 4 * 2 + (size_t)W * D * 4 +
+         (mode == kRankSafe ? (size_t)W * D * 4 : 0) + (size_t)D * 8 + 40 * 4 + kFCap + (size_t)D * 8 + 64;
+}
+
+template <typename K>
+int set_smem(K kernel, size_t bytes) {
+  GT_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  return GT_OK;
+}
+
+int scan_u32_to_u64(const uint32_t* in, uint64_t n, uint64_t* out, uint64_t init, bool total,
+                    uint64_t* status, unsigned int* ctr, cudaStream_t st) {
+  const uint64_t tiles = std::max<uint64_t>(1, (n + kScanTile - 1) / kScanTile);
+  GT_CUDA(cudaMemsetAsync(status, 0, tiles * 8, st));
+  GT_CUDA(cudaMemsetAsync(ctr, 0, 4, st));
+  k_scan_lookback<uint32_t><<<(unsigned)tiles, kScanThreads, 0, st>>>(in, n, out, init, total ? 1 : 0, status, ctr);
+  GT_LAUNCH_CHECK();
+  return GT_OK;
+}
+int scan_u64_to_u64(const unsigned long long* in, uint64_t n, uint64_t* out, uint64_t init, bool total,
+                    uint64_t* status, unsigned int* ctr, cudaStream_t st) {
+  const uint64_t tiles = std::max<uint64_t>(1, (n + kScanTile - 1) / kScanTile);
+  GT_CUDA(cudaMemsetAsync(status, 0, tiles * 8, st));
+  GT_CUDA(cudaMemsetAsync(ctr, 0, 4, st));
+  k_scan_lookback<unsigned long long><<<(unsigned)tiles, kScanThreads, 0, st>>>(in, n, out, init, total ? 1 : 0,
+                                                                                  status, ctr);
+  GT_LAUNCH_CHECK();
+  return GT_OK;
+}
+
+struct Timer {
+  bool on = false;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev[5] = {};
+  int n = 0;
+  int init(bool enable, cudaStream_t s) {
+    on = enable;
+    st = s;
+    if (!on) return GT_OK;
+    for (auto& e : ev) GT_CUDA(cudaEventCreate(&e));
+    return GT_OK;
+  }
+  int mark() {
+    if (on) GT_CUDA(cudaEventRecord(ev[n++], st));
+    return GT_OK;
+  }
+  ~Timer() {
+    if (on)
+      for (auto& e : ev) cudaEventDestroy(e);
+  }
+};
+
+// Core pipeline over an input stream `in` of p.E edges whose destinations are
+// local IDs in [0, p.V).  Workspace already sized by make_plan.
+template <int kMode, class In>
+int transpose_core(const Plan& p, In in, uint64_t* t_offsets, uint32_t* t_edges, unsigned char* ws, cudaStream_t st,
+                   gt_stats* stats, Timer& tm) {
+  const uint64_t V = p.V, E = p.E;
+  uint2* rec = reinterpret_cast<uint2*>(ws + p.o_rec);
+  uint32_t* tcnt = reinterpret_cast<uint32_t*>(ws + p.o_tcnt);
+  uint64_t* tbase = reinterpret_cast<uint64_t*>(ws + p.o_tbase);
+  uint32_t* tsrc = reinterpret_cast<uint32_t*>(ws + p.o_tsrc);
+  uint64_t* cstart = reinterpret_cast<uint64_t*>(ws + p.o_cstart);
+  uint32_t* cfirst = reinterpret_cast<uint32_t*>(ws + p.o_cfirst);
+  uint32_t* cbucket = reinterpret_cast<uint32_t*>(ws + p.o_cbucket);
+  uint32_t* segoff = p.b ? reinterpret_cast<uint32_t*>(ws + p.o_segoff) : nullptr;
+  unsigned long long* fhist = reinterpret_cast<unsigned long long*>(ws + p.o_fhist);
+  uint64_t* fbase = reinterpret_cast<uint64_t*>(ws + p.o_fbase);
+  uint64_t* status = reinterpret_cast<uint64_t*>(ws + p.o_status);
+  unsigned int* ctr = reinterpret_cast<unsigned int*>(ws + p.o_ctr);
+  uint32_t* big = reinterpret_cast<uint32_t*>(ws + p.o_big);
+  uint32_t* bigcnt = reinterpret_cast<uint32_t*>(ws + p.o_bigcnt);
+  unsigned int* err = reinterpret_cast<unsigned int*>(ws + p.o_err);
+  const uint64_t nfine = (uint64_t)p.D1 * p.Db;
+  const DigShift dig1{p.b + p.c};
+  int rc;
+
+  GT_CUDA(cudaMemsetAsync(bigcnt, 0, 4, st));
+  GT_CUDA(cudaMemsetAsync(err, 0, 4, st));
+  if ((rc = tm.mark())) return rc;
+  // ---- step 1: level-1 partition (source-ordered pass over the edge stream)
+  if constexpr (!In::kRecords) {
+    k_tile_src<<<(unsigned)((p.ntiles + 255) / 256), 256, 0, st>>>(in, p.CT, p.ntiles, tsrc);
+    GT_LAUNCH_CHECK();
+  }
+  k_l1_count<In, DigShift><<<(unsigned)p.ntiles, 512, p.D1 * 4, st>>>(in, dig1, E, p.CT, p.ntiles, p.D1, tcnt);
+  GT_LAUNCH_CHECK();
+  if ((rc = scan_u32_to_u64(tcnt, (uint64_t)p.D1 * p.ntiles, tbase, 0, true, status, ctr, st))) return rc;
+  {
+    const size_t sm = smem_l1_place(p.D1, kMode);
+    if ((rc = set_smem(k_l1_place<kMode, In, DigShift>, sm))) return rc;
+    k_l1_place<kMode, In, DigShift><<<(unsigned)p.ntiles, kL1Warps * 32, sm, st>>>(in, dig1, E, p.CT, p.ntiles, p.D1,
+                                                                                   tbase, tsrc, rec);
+    GT_LAUNCH_CHECK();
+  }
+  k_coarse_info<<<1, 1024, (p.D1 + 1) * 4, st>>>(tbase, p.ntiles, p.D1, E, cstart, cfirst,
+                                                 p.b ? nullptr : fhist);
+  GT_LAUNCH_CHECK();
+  k_chunk_map<<<p.D1, 128, 0, st>>>(cfirst, p.D1, cbucket);
+  GT_LAUNCH_CHECK();
+  if ((rc = tm.mark())) return rc;
+  // ---- step 2: level-2 chunk sort by the middle digit
+  const uint64_t* fine_base_ptr = cstart;
+  if (p.b) {
+    GT_CUDA(cudaMemsetAsync(fhist, 0, nfine * 8, st));
+    const size_t sm = smem_b1(p, kMode);
+    if ((rc = set_smem(k_b1<kMode>, sm))) return rc;
+    k_b1<kMode><<<(unsigned)p.max_chunks, kB1Warps * 32, sm, st>>>(rec, cstart, cfirst, cbucket, p.D1, p.c,
+                                                                    (uint32_t)(p.Db - 1), p.Db, segoff, fhist);
+    GT_LAUNCH_CHECK();
+    if ((rc = scan_u64_to_u64(fhist, nfine, fbase, 0, true, status, ctr, st))) return rc;
+    fine_base_ptr = fbase;
+  }
+  if ((rc = tm.mark())) return rc;
+  // ---- step 3: final per-bucket sort, CSC offsets
+  FineCtx fx;
+  fx.rec = rec;
+  fx.cstart = cstart;
+  fx.chunk_first = cfirst;
+  fx.segoff = segoff;
+  fx.Db = p.Db;
+  fx.bits_c = p.c;
+  fx.mask_c = (uint32_t)(p.Dc - 1);
+  fx.V = V;
+  {
+    const size_t sm = smem_final(p, kMode);
+    if ((rc = set_smem(k_final_small<kMode>, sm))) return rc;
+    k_final_small<kMode><<<(unsigned)nfine, kFWarps * 32, sm, st>>>(fx, fhist, fine_base_ptr, t_offsets, t_edges,
+                                                                     big, bigcnt);
+    GT_LAUNCH_CHECK();
+  }
+  k_set_u64<<<1, 1, 0, st>>>(t_offsets + V, E);
+  GT_LAUNCH_CHECK();
+  uint32_t h_big = 0;
+  GT_CUDA(cudaMemcpyAsync(&h_big, bigcnt, 4, cudaMemcpyDeviceToHost, st));
+  GT_CUDA(cudaStreamSynchronize(st));
+  if (stats) stats->n_big_buckets = h_big;
+  if (h_big) {
+    std::vector<uint32_t> blist(h_big), cf(p.D1 + 1);
+    GT_CUDA(cudaMemcpyAsync(blist.data(), big, h_big * 4, cudaMemcpyDeviceToHost, st));
+    GT_CUDA(cudaMemcpyAsync(cf.data(), cfirst, (p.D1 + 1) * 4, cudaMemcpyDeviceToHost, st));
+    GT_CUDA(cudaStreamSynchronize(st));
+    std::sort(blist.begin(), blist.end());
+    std::vector<BigJob> jobs;
+    std::vector<uint32_t> jfirst;
+    for (uint32_t bi = 0; bi < h_big; ++bi) {
+      const uint32_t fid = blist[bi];
+      const uint32_t c = fid / p.Db;
+      jfirst.push_back((uint32_t)jobs.size());
+      for (uint32_t g = cf[c]; g < cf[c + 1]; g += kJobChunks)
+        jobs.push_back(BigJob{fid, g, std::min<uint32_t>(g + kJobChunks, cf[c + 1]), bi});
+    }
+    jfirst.push_back((uint32_t)jobs.size());
+    const uint64_t nj = jobs.size();
+    const uint64_t need = align_up(nj * sizeof(BigJob), 256) + align_up(jfirst.size() * 4, 256) +
+                          align_up(h_big * 4, 256) + align_up(nj * p.Dc * 4, 256) + align_up(nj * p.Dc * 8, 256);
+    int dev;
+    if ((rc = current_device(&dev))) return rc;
+    void* aux = nullptr;
+    if ((rc = cache_get(g_aux[dev], need, &aux))) return rc;
+    unsigned char* a = static_cast<unsigned char*>(aux);
+    BigJob* d_jobs = reinterpret_cast<BigJob*>(a);
+    a += align_up(nj * sizeof(BigJob), 256);
+    uint32_t* d_jfirst = reinterpret_cast<uint32_t*>(a);
+    a += align_up(jfirst.size() * 4, 256);
+    uint32_t* d_blist = reinterpret_cast<uint32_t*>(a);
+    a += align_up(h_big * 4, 256);
+    uint32_t* d_jobcnt = reinterpret_cast<uint32_t*>(a);
+    a += align_up(nj * p.Dc * 4, 256);
+    uint64_t* d_jobbase = reinterpret_cast<uint64_t*>(a);
+    GT_CUDA(cudaMemcpyAsync(d_jobs, jobs.data(), nj * sizeof(BigJob), cudaMemcpyHostToDevice, st));
+    GT_CUDA(cudaMemcpyAsync(d_jfirst, jfirst.data(), jfirst.size() * 4, cudaMemcpyHostToDevice, st));
+    GT_CUDA(cudaMemcpyAsync(d_blist, blist.data(), h_big * 4, cudaMemcpyHostToDevice, st));
+    k_big_count<<<(unsigned)nj, 256, p.Dc * 4, st>>>(fx, d_jobs, d_jobcnt);
+    GT_LAUNCH_CHECK();
+    k_big_scan<<<h_big, 256, p.Dc * 8, st>>>(fx, d_blist, d_jfirst, fine_base_ptr, d_jobcnt, d_jobbase, t_offsets,
+                                             err);
+    GT_LAUNCH_CHECK();
+    const size_t sm = smem_final(p, kMode);
+    if ((rc = set_smem(k_big_place<kMode>, sm))) return rc;
+    k_big_place<kMode><<<(unsigned)nj, kFWarps * 32, sm, st>>>(fx, d_jobs, d_jobbase, t_edges);
+    GT_LAUNCH_CHECK();
+    unsigned int h_err = 0;
+    GT_CUDA(cudaMemcpyAsync(&h_err, err, 4, cudaMemcpyDeviceToHost, st));
+    GT_CUDA(cudaStreamSynchronize(st));
+    if (h_err) return set_err(GT_EOVERFLOW, "32-bit degree counter overflowed (a transposed degree >= 2^32)");
+  }
+  if ((rc = tm.mark())) return rc;
+  return GT_OK;
+}
+
+int fill_stats(const Plan& p, int mode, Timer& tm, gt_stats* stats) {
+  const uint64_t big = stats->n_big_buckets;
+  float a = 0, b = 0, c = 0, t = 0;
+  GT_CUDA(cudaEventElapsedTime(&a, tm.ev[0], tm.ev[1]));
+  GT_CUDA(cudaEventElapsedTime(&b, tm.ev[1], tm.ev[2]));
+  GT_CUDA(cudaEventElapsedTime(&c, tm.ev[2], tm.ev[3]));
+  GT_CUDA(cudaEventElapsedTime(&t, tm.ev[0], tm.ev[3]));
+  stats->ms_step1 = a;
+  stats->ms_step2 = b;
+  stats->ms_step3 = c;
+  stats->ms_total = t;
+  stats->workspace_bytes = p.total;
+  stats->bits[0] = p.a;
+  stats->bits[1] = p.b;
+  stats->bits[2] = p.c;
+  stats->rank_mode = mode;
+  stats->n_big_buckets = big;
+  // kernels of transpose_core: tile_src (CSR input), l1_count, scan, l1_place, coarse_info,
+  // chunk_map, [b1, scan], final_small, set_u64, [big_count, big_scan, big_place]
+  stats->n_launches = 8 + (p.b ? 2 : 0) + (big ? 3 : 0);
+  return GT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gt_abi_version(void) { return GT_ABI_VERSION; }
+const char* gt_last_error(void) { return g_err.c_str(); }
+
+int gt_workspace_size(uint64_t V, uint64_t E, uint64_t* bytes) {
+  if (!bytes) return set_err(GT_EINVAL, "bytes is NULL");
+  if (E == 0 || V == 0) {
+    *bytes = 0;
+    return GT_OK;
+  }
+  Plan p;
+  int rc = make_plan(V, E, p);
+  if (rc) return rc;
+  *bytes = p.total;
+  return GT_OK;
+}
+
+int gt_set_rank_mode(int mode) {
+  if (mode < -1 || mode > 1) return set_err(GT_EINVAL, "rank mode must be -1, 0 or 1");
+  g_forced_rank_mode = mode;
+  return GT_OK;
+}
+
+int gt_selftest_rank_order(uint64_t trials, uint64_t* violations) {
+  if (!violations) return set_err(GT_EINVAL, "violations is NULL");
+  int dev;
+  int rc = current_device(&dev);
+  if (rc) return rc;
+  return run_selftest(trials, violations, nullptr);
+}
+
+int gt_transpose(const uint64_t* offsets, const uint32_t* edges, uint64_t V, uint64_t E, uint64_t* t_offsets,
+                 uint32_t* t_edges, void* workspace, uint64_t workspace_bytes, void* stream, gt_stats* stats) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (stats) std::memset(stats, 0, sizeof(*stats));
+  if (!t_offsets) return set_err(GT_EINVAL, "t_offsets is NULL");
+  if (E && (!offsets || !edges || !t_edges)) return set_err(GT_EINVAL, "NULL array with num_edges > 0");
+  if (V > (1ull << 32)) return set_err(GT_EINVAL, "num_vertices > 2^32 needs 64-bit edge IDs");
+  if (E && V == 0) return set_err(GT_EINVAL, "edges present but num_vertices == 0");
+  int dev;
+  int rc = current_device(&dev);
+  if (rc) return rc;
+  if (E == 0) {
+    GT_CUDA(cudaMemsetAsync(t_offsets, 0, (V + 1) * 8, st));
+    if (stats) GT_CUDA(cudaStreamSynchronize(st));
+    return GT_OK;
+  }
+  Plan p;
+  if ((rc = make_plan(V, E, p))) return rc;
+  unsigned char* ws = static_cast<unsigned char*>(workspace);
+  if (!ws) {
+    void* w = nullptr;
+    if ((rc = cache_get(g_ws[dev], p.total, &w))) return rc;
+    ws = static_cast<unsigned char*>(w);
+  } else if (workspace_bytes < p.total) {
+    return set_err(GT_ENOMEM, "workspace too small: need %llu bytes, got %llu", (unsigned long long)p.total,
+                   (unsigned long long)workspace_bytes);
+  }
+  int mode;
+  if ((rc = rank_mode_for(dev, st, &mode))) return rc;
+  Timer tm;
+  if ((rc = tm.init(stats != nullptr, st))) return rc;
+  const InCsr in{offsets, edges, 0, V};
+  rc = (mode == kRankAtomic) ? transpose_core<kRankAtomic>(p, in, t_offsets, t_edges, ws, st, stats, tm)
+                             : transpose_core<kRankSafe>(p, in, t_offsets, t_edges, ws, st, stats, tm);
+  if (rc) return rc;
+  if (stats) {
+    GT_CUDA(cudaEventSynchronize(tm.ev[tm.n - 1]));
+    if ((rc = fill_stats(p, mode, tm, stats))) return rc;
+  }
+  return GT_OK;
+}
+
+int gt_transpose_host(const uint64_t* h_offsets, const uint32_t* h_edges, uint64_t V, uint64_t E,
+                      uint64_t* h_t_offsets, uint32_t* h_t_edges, int device, gt_stats* stats) {
+  if (!h_offsets || !h_t_offsets || (E && (!h_edges || !h_t_edges)))
+    return set_err(GT_EINVAL, "NULL host array");
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) return set_err(GT_ENODEV, "no CUDA device");
+  if (device < 0 || device >= n) return set_err(GT_EINVAL, "bad device %d", device);
+  GT_CUDA(cudaSetDevice(device));
+  cudaStream_t st;
+  GT_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  uint64_t *d_off = nullptr, *d_toff = nullptr;
+  uint32_t *d_e = nullptr, *d_te = nullptr;
+  int rc = GT_OK;
+  auto cleanup = [&]() {
+    cudaFreeAsync(d_off, st);
+    cudaFreeAsync(d_toff, st);
+    if (d_e) cudaFreeAsync(d_e, st);
+    if (d_te) cudaFreeAsync(d_te, st);
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+  };
+  do {
+    cudaError_t ce;
+    if ((ce = cudaMallocAsync(&d_off, (V + 1) * 8, st)) != cudaSuccess ||
+        (ce = cudaMallocAsync(&d_toff, (V + 1) * 8, st)) != cudaSuccess ||
+        (E && (ce = cudaMallocAsync(&d_e, E * 4, st)) != cudaSuccess) ||
+        (E && (ce = cudaMallocAsync(&d_te, E * 4, st)) != cudaSuccess)) {
+      rc = set_err(ce == cudaErrorMemoryAllocation ? GT_ENOMEM : GT_ECUDA, "device allocation: %s",
+                   cudaGetErrorString(ce));
+      break;
+    }
+    if ((ce = cudaMemcpyAsync(d_off, h_offsets, (V + 1) * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+        (E && (ce = cudaMemcpyAsync(d_e, h_edges, E * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess)) {
+      rc = set_err(GT_ECUDA, "H2D: %s", cudaGetErrorString(ce));
+      break;
+    }
+    rc = gt_transpose(d_off, d_e, V, E, d_toff, d_te, nullptr, 0, st, stats);
+    if (rc) break;
+    if ((ce = cudaMemcpyAsync(h_t_offsets, d_toff, (V + 1) * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (E && (ce = cudaMemcpyAsync(h_t_edges, d_te, E * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) ||
+        (ce = cudaStreamSynchronize(st)) != cudaSuccess) {
+      rc = set_err(GT_ECUDA, "D2H: %s", cudaGetErrorString(ce));
+      break;
+    }
+  } while (0);
+  cleanup();
+  return rc;
+}
+
+int gt_prefix_sum(const uint32_t* counts, uint64_t n, uint64_t* out, void* stream) {
+  if (!out || (n && !counts)) return set_err(GT_EINVAL, "NULL array");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int dev;
+  int rc = current_device(&dev);
+  if (rc) return rc;
+  const uint64_t tiles = std::max<uint64_t>(1, (n + kScanTile - 1) / kScanTile);
+  void* w = nullptr;
+  // use the tail of the aux cache (status words + counter)
+  if ((rc = cache_get(g_aux[dev], std::max<uint64_t>(g_aux[dev].bytes, tiles * 8 + 256), &w))) return rc;
+  uint64_t* status = static_cast<uint64_t*>(w);
+  unsigned int* ctr = reinterpret_cast<unsigned int*>(static_cast<unsigned char*>(w) + align_up(tiles * 8, 128));
+  return scan_u32_to_u64(counts, n, out, 0, true, status, ctr, st);
+}
+
+__global__ void k_add_base(uint64_t* a, uint64_t n, uint64_t base) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    a[i] += base;
+}
+
+int gt_shard_partition(const uint64_t* offsets, const uint32_t* edges_slice, uint64_t V, uint64_t src_begin,
+                       uint64_t src_end, const uint64_t* h_dst_bounds, int parts, uint32_t* records_out,
+                       uint64_t* h_counts_out, void* stream) {
+  if (!offsets || !h_dst_bounds || !h_counts_out || parts < 1 || parts > kMaxParts || src_begin > src_end ||
+      src_end > V)
+    return set_err(GT_EINVAL, "gt_shard_partition: bad arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int dev;
+  int rc = current_device(&dev);
+  if (rc) return rc;
+  uint64_t e_rng[2];
+  GT_CUDA(cudaMemcpyAsync(&e_rng[0], offsets + src_begin, 8, cudaMemcpyDeviceToHost, st));
+  GT_CUDA(cudaMemcpyAsync(&e_rng[1], offsets + src_end, 8, cudaMemcpyDeviceToHost, st));
+  GT_CUDA(cudaStreamSynchronize(st));
+  const uint64_t E = e_rng[1] - e_rng[0];
+  for (int q = 0; q < parts; ++q) h_counts_out[q] = 0;
+  if (E == 0) return GT_OK;
+  if (!edges_slice || !records_out) return set_err(GT_EINVAL, "gt_shard_partition: NULL edge/record buffer");
+  DigBounds dig{};
+  dig.parts = parts;
+  for (int q = 0; q <= parts; ++q) {
+    if (h_dst_bounds[q] > V || (q && h_dst_bounds[q] < h_dst_bounds[q - 1]))
+      return set_err(GT_EINVAL, "gt_shard_partition: destination bounds not monotone in [0, V]");
+    dig.lo[q] = (uint32_t)std::min<uint64_t>(h_dst_bounds[q], 0xffffffffull);
+  }
+  uint64_t CT = 65536, ntiles = (E + CT - 1) / CT;
+  uint64_t off = 0;
+  const uint64_t o_tcnt = off;
+  off = align_up(off + ntiles * parts * 4, 256);
+  const uint64_t o_tbase = off;
+  off = align_up(off + (ntiles * parts + 1) * 8, 256);
+  const uint64_t o_tsrc = off;
+  off = align_up(off + ntiles * 4, 256);
+  const uint64_t o_status = off;
+  off = align_up(off + ((ntiles * parts + kScanTile) / kScanTile + 1) * 8, 256);
+  const uint64_t o_ctr = off;
+  off += 256;
+  void* w = nullptr;
+  if ((rc = cache_get(g_aux[dev], off, &w))) return rc;
+  unsigned char* ws = static_cast<unsigned char*>(w);
+  uint32_t* tcnt = reinterpret_cast<uint32_t*>(ws + o_tcnt);
+  uint64_t* tbase = reinterpret_cast<uint64_t*>(ws + o_tbase);
+  uint32_t* tsrc = reinterpret_cast<uint32_t*>(ws + o_tsrc);
+  uint64_t* status = reinterpret_cast<uint64_t*>(ws + o_status);
+  unsigned int* ctr = reinterpret_cast<unsigned int*>(ws + o_ctr);
+  int mode;
+  if ((rc = rank_mode_for(dev, st, &mode))) return rc;
+  const InCsr in{offsets, edges_slice, e_rng[0], V};
+  k_tile_src<<<(unsigned)((ntiles + 255) / 256), 256, 0, st>>>(in, CT, ntiles, tsrc);
+  GT_LAUNCH_CHECK();
+  k_l1_count<InCsr, DigBounds><<<(unsigned)ntiles, 512, parts * 4, st>>>(in, dig, E, CT, ntiles, parts, tcnt);
+  GT_LAUNCH_CHECK();
+  if ((rc = scan_u32_to_u64(tcnt, ntiles * parts, tbase, 0, true, status, ctr, st))) return rc;
+  uint2* out = reinterpret_cast<uint2*>(records_out);
+  const size_t sm = smem_l1_place(parts, mode);
+  if (mode == kRankAtomic) {
+    if ((rc = set_smem(k_l1_place<kRankAtomic, InCsr, DigBounds>, sm))) return rc;
+    k_l1_place<kRankAtomic, InCsr, DigBounds><<<(unsigned)ntiles, kL1Warps * 32, sm, st>>>(in, dig, E, CT, ntiles, parts,
+                                                                                         tbase, tsrc, out);
+  } else {
+    if ((rc = set_smem(k_l1_place<kRankSafe, InCsr, DigBounds>, sm))) return rc;
+    k_l1_place<kRankSafe, InCsr, DigBounds><<<(unsigned)ntiles, kL1Warps * 32, sm, st>>>(in, dig, E, CT, ntiles, parts,
+                                                                                       tbase, tsrc, out);
+  }
+  GT_LAUNCH_CHECK();
+  std::vector<uint64_t> starts(parts + 1);
+  for (int q = 0; q < parts; ++q)
+    GT_CUDA(cudaMemcpyAsync(&starts[q], tbase + (uint64_t)q * ntiles, 8, cudaMemcpyDeviceToHost, st));
+  GT_CUDA(cudaStreamSynchronize(st));
+  starts[parts] = E;
+  for (int q = 0; q < parts; ++q) h_counts_out[q] = starts[q + 1] - starts[q];
+  return GT_OK;
+}
+
+int gt_shard_transpose(const uint32_t* records, uint64_t R, uint64_t dst_begin, uint64_t dst_end, uint64_t global_base,
+                       uint64_t* t_offsets_local, uint32_t* t_edges_local, void* stream, gt_stats* stats) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (stats) std::memset(stats, 0, sizeof(*stats));
+  if (dst_end < dst_begin || !t_offsets_local || (R && (!records || !t_edges_local)))
+    return set_err(GT_EINVAL, "gt_shard_transpose: bad arguments");
+  const uint64_t V = dst_end - dst_begin;
+  int dev;
+  int rc = current_device(&dev);
+  if (rc) return rc;
+  if (R == 0) {
+    GT_CUDA(cudaMemsetAsync(t_offsets_local, 0, (V + 1) * 8, st));
+    k_add_base<<<1, 256, 0, st>>>(t_offsets_local, V + 1, global_base);
+    GT_LAUNCH_CHECK();
+    return GT_OK;
+  }
+  if (V == 0) return set_err(GT_EINVAL, "gt_shard_transpose: records for an empty destination range");
+  Plan p;
+  if ((rc = make_plan(V, R, p))) return rc;
+  void* w = nullptr;
+  if ((rc = cache_get(g_ws[dev], p.total, &w))) return rc;
+  unsigned char* ws = static_cast<unsigned char*>(w);
+  int mode;
+  if ((rc = rank_mode_for(dev, st, &mode))) return rc;
+  Timer tm;
+  if ((rc = tm.init(stats != nullptr, st))) return rc;
+  const InRec in{reinterpret_cast<const uint2*>(records), (uint32_t)dst_begin};
+  rc = (mode == kRankAtomic) ? transpose_core<kRankAtomic>(p, in, t_offsets_local, t_edges_local, ws, st, stats, tm)
+                             : transpose_core<kRankSafe>(p, in, t_offsets_local, t_edges_local, ws, st, stats, tm);
+  if (rc) return rc;
+  if (global_base) {
+    k_add_base<<<148, 256, 0, st>>>(t_offsets_local, V + 1, global_base);
+    GT_LAUNCH_CHECK();
+  }
+  if (stats) {
+    GT_CUDA(cudaStreamSynchronize(st));
+    fill_stats(p, mode, tm, stats);
+  }
+  return GT_OK;
+}
+
+int gt_edge_balanced_bounds(const uint64_t* h_offsets, uint64_t V, int64_t parts, int64_t* h_bounds) {
+  if (!h_offsets || !h_bounds) return set_err(GT_EINVAL, "NULL array");
+  if (parts < 1) parts = 1;  // _nb.py:127
+  const uint64_t E = h_offsets[V];
+  for (int64_t q = 0; q <= parts; ++q) {
+    const unsigned __int128 t = (unsigned __int128)E * (uint64_t)q / (uint64_t)parts;
+    const uint64_t target = (uint64_t)t;
+    const uint64_t* it = std::lower_bound(h_offsets, h_offsets + V + 1, target);  // searchsorted 'left'
+    h_bounds[q] = (int64_t)(it - h_offsets);
+  }
+  h_bounds[0] = 0;
+  h_bounds[parts] = (int64_t)V;
+  return GT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,147 @@
+// gt_common.cuh — shared device helpers for the B200 transposition kernels.
+//
+// Ranking model: a warp processes its contiguous item
+// range in slots of 32 consecutive items (lane l holds item 32*s + l), so the
+// warp's program order equals item order.  Each warp owns a private counter
+// array in shared memory.  kRankAtomic: one shared-memory atomicAdd per item;
+// B200 returns the old values of same-address lanes of one instruction in
+// ascending lane order (gt_selftest_rank_order checks this on the device before
+// it is used).  kRankSafe: architecture-guaranteed fallback that builds the
+// peer mask with a shared atomicOr and lets the lowest peer advance the count.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gt {
+
+constexpr uint32_t kFull = 0xffffffffu;
+
+enum RankMode : int { kRankAtomic = 0, kRankSafe = 1 };
+
+__host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ uint32_t warp_id() { return threadIdx.x >> 5; }
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Count-only increment (order irrelevant).
+__device__ __forceinline__ void smem_inc(uint32_t* p) { atomicAdd(p, 1u); }
+
+// Stable rank of this lane's item among same-digit items of the warp's stream.
+// cnt[d] holds the running count (or running position after the base pass) of
+// digit d for this warp; scratch[d] must be zero between calls (safe mode).
+// All 32 lanes must call; invalid lanes pass valid=false.
+template <int kMode>
+__device__ __forceinline__ uint32_t warp_rank(uint32_t* cnt, uint32_t* scratch, uint32_t d,
+                                              bool valid) {
+  if constexpr (kMode == kRankAtomic) {
+    (void)scratch;
+    uint32_t r = 0;
+    if (valid) r = atomicAdd(&cnt[d], 1u);
+    return r;
+  } else {
+    const uint32_t lane = lane_id();
+    if (valid) atomicOr(&scratch[d], 1u << lane);
+    __syncwarp();
+    uint32_t peers = 0, c = 0;
+    if (valid) {
+      peers = scratch[d];
+      c = cnt[d];
+    }
+    __syncwarp();
+    const uint32_t lt = peers & lanemask_lt();
+    if (valid && lt == 0) {
+      cnt[d] = c + __popc(peers);
+      scratch[d] = 0;
+    }
+    __syncwarp();
+    return c + __popc(lt);
+  }
+}
+
+// Block-wide exclusive scan of a shared uint32 array a[0..n) in place; returns
+// the total to all threads.  n may exceed blockDim.x.  Uses `tmp` (>= 33 words).
+__device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t* a, int n, uint32_t* tmp) {
+  const int T = blockDim.x, t = threadIdx.x;
+  const int per = (n + T - 1) / T;
+  const int lo = t * per, hi = min(n, lo + per);
+  uint32_t s = 0;
+  for (int i = lo; i < hi; ++i) s += a[i];
+  // warp inclusive scan of s
+  uint32_t x = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(kFull, x, o);
+    if ((t & 31) >= o) x += y;
+  }
+  if ((t & 31) == 31) tmp[t >> 5] = x;
+  __syncthreads();
+  if (t < 32) {
+    const int nw = (T + 31) >> 5;
+    uint32_t w = (t < nw) ? tmp[t] : 0;
+    uint32_t v = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(kFull, v, o);
+      if (t >= o) v += y;
+    }
+    if (t < nw) tmp[t] = v - w;  // exclusive warp offsets
+    if (t == 31) tmp[32] = v;    // total
+  }
+  __syncthreads();
+  uint32_t run = tmp[t >> 5] + x - s;
+  for (int i = lo; i < hi; ++i) {
+    uint32_t v = a[i];
+    a[i] = run;
+    run += v;
+  }
+  const uint32_t total = tmp[32];
+  __syncthreads();
+  return total;
+}
+
+// Per-warp counters cnt[W][D] (row per warp).  After counting, turn them into
+// tile-local bases: base[w][d] = digit_start[d] + sum_{w'<w} cnt[w'][d].
+// digit_start (size D, optional) receives the tile-local start of each digit,
+// digit_total (size D, optional) the per-digit totals.  Returns the tile total.
+template <int W>
+__device__ __forceinline__ uint32_t warp_counts_to_bases(uint32_t* cnt, int D, uint32_t* dstart,
+                                                         uint32_t* dtotal, uint32_t* tmp) {
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      uint32_t c = cnt[w * D + d];
+      cnt[w * D + d] = run;
+      run += c;
+    }
+    dstart[d] = run;
+    if (dtotal) dtotal[d] = run;
+  }
+  __syncthreads();
+  uint32_t total = block_excl_scan_u32(dstart, D, tmp);
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    const uint32_t b = dstart[d];
+#pragma unroll
+    for (int w = 0; w < W; ++w) cnt[w * D + d] += b;
+  }
+  __syncthreads();
+  return total;
+}
+
+// 64-bit global loads/stores with streaming hints.
+__device__ __forceinline__ uint2 ldg_stream(const uint2* p) {
+  uint2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t ldg_stream(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+}  // namespace gt

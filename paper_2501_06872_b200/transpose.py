@@ -1,0 +1,197 @@
+"""Drop-in GPU transposition with the reference's operator contract.
+
+Mirrors the reference entry points of the hot path
+(``transpose_atomic(g, threads, ...)`` baselines.py:168-209 and
+``transpose_potra(g, threads, ...)`` hlh.py:441-588, each followed by
+``sort_neighbor_lists`` baselines.py:457-475): a ``CsrGraph`` in, a
+``TransposeOutput`` out whose graph is bit-identical to
+``transpose_oracle(g)`` (graph.py:136-148) — uint64 offsets, uint32 neighbour
+IDs, orientation flipped, every list ascending by source — with
+``sorted=True`` and no sort pass.
+
+The work runs in libgt.so (hand-written sm_100a kernels behind a C ABI).
+torch is used only for device memory and streams.  There is no CPU fallback:
+missing library or device raises :class:`GpuUnavailableError`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .errors import GpuUnavailableError
+from .graph import CsrGraph, flip_orientation
+
+__all__ = [
+    "TransposeOutput",
+    "transpose_gpu",
+    "transpose_device",
+    "prefix_sum_gpu",
+    "edge_balanced_vertex_bounds",
+    "selftest_rank_order",
+    "set_rank_mode",
+]
+
+
+@dataclass
+class TransposeOutput:
+    """Result of one transposition run plus its cost accounting
+    (baselines.py:39-53, same fields)."""
+
+    graph: object
+    phase_times: dict
+    aux_footprint_bytes: int
+    method: str
+    sorted: bool
+    details: dict = field(default_factory=dict)
+
+
+def _torch():
+    try:
+        import torch
+    except ImportError as exc:  # pragma: no cover - torch is in the image
+        raise GpuUnavailableError(f"torch is required for device memory: {exc}") from None
+    if not torch.cuda.is_available():
+        raise GpuUnavailableError("no CUDA device visible (transpose_gpu has no CPU path)")
+    return torch
+
+
+def _stream_handle(torch, stream):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def transpose_device(offsets, edges, num_vertices: int, *, t_offsets=None, t_edges=None, stream=None,
+                     want_stats: bool = False):
+    """Device-resident CSR -> CSC on torch CUDA tensors.
+
+    ``offsets`` int64[V+1] (uint64 bits) and ``edges`` int32[E] (uint32 bits)
+    on the same device.  Returns ``(t_offsets, t_edges, stats_or_None)``.
+    """
+    torch = _torch()
+    V = int(num_vertices)
+    E = int(edges.numel())
+    if offsets.dtype != torch.int64 or edges.dtype != torch.int32:
+        raise ValueError("offsets must be int64 (uint64 bits) and edges int32 (uint32 bits)")
+    if offsets.numel() != V + 1:
+        raise ValueError(f"offsets must have exactly {V + 1} entries")
+    dev = offsets.device
+    if t_offsets is None:
+        t_offsets = torch.empty(V + 1, dtype=torch.int64, device=dev)
+    if t_edges is None:
+        t_edges = torch.empty(E, dtype=torch.int32, device=dev)
+    st = _lib.GtStats() if want_stats else None
+    with torch.cuda.device(dev):
+        rc = _lib.lib.gt_transpose(
+            ctypes.c_void_p(offsets.data_ptr()),
+            ctypes.c_void_p(edges.data_ptr()),
+            V,
+            E,
+            ctypes.c_void_p(t_offsets.data_ptr()),
+            ctypes.c_void_p(t_edges.data_ptr()),
+            None,
+            0,
+            _stream_handle(torch, stream),
+            ctypes.byref(st) if st is not None else None,
+        )
+    _lib.check(rc, "gt_transpose")
+    return t_offsets, t_edges, st
+
+
+def transpose_gpu(g, devices: int = 1, *, device=None, stream=None) -> TransposeOutput:
+    """Transpose a CsrGraph on the GPU; same contract as transpose_atomic +
+    sort_neighbor_lists, output equal to transpose_oracle(g).
+
+    ``devices`` plays the role of the reference's ``threads`` (must be >= 1,
+    _nb.py:112-113).  ``devices > 1`` needs an initialised torch.distributed
+    process group with that many ranks (one process per GPU) and dispatches to
+    :func:`paper_2501_06872_b200.multi.transpose_distributed`.
+    """
+    if devices < 1:
+        raise ValueError(f"device count must be >= 1, got {devices}")
+    if devices > 1:
+        from .multi import transpose_distributed
+
+        return transpose_distributed(g, devices=devices, device=device)
+    torch = _torch()
+    nv, ne = int(g.num_vertices), int(g.num_edges)
+    if g.edges.dtype != np.uint32:
+        raise ValueError("only 32-bit neighbour IDs (num_vertices <= 2^32) are supported")
+    if g.offsets.dtype != np.uint64:
+        raise ValueError("offsets must be uint64")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    t0 = time.perf_counter()
+    off_d = torch.from_numpy(np.ascontiguousarray(g.offsets).view(np.int64)).to(dev, non_blocking=False)
+    edg_d = torch.from_numpy(np.ascontiguousarray(g.edges).view(np.int32)).to(dev, non_blocking=False)
+    t1 = time.perf_counter()
+    t_off, t_edg, st = transpose_device(off_d, edg_d, nv, stream=stream, want_stats=True)
+    t2 = time.perf_counter()
+    t_offsets = t_off.cpu().numpy().view(np.uint64)
+    t_edges = t_edg.cpu().numpy().view(np.uint32)
+    t3 = time.perf_counter()
+    out_graph = type(g)(nv, ne, t_offsets, t_edges, flip_orientation(g.orientation))
+    return TransposeOutput(
+        graph=out_graph,
+        phase_times={
+            "h2d": t1 - t0,
+            "step1": st.ms_step1 / 1e3,
+            "step2": st.ms_step2 / 1e3,
+            "step3": st.ms_step3 / 1e3,
+            "d2h": t3 - t2,
+        },
+        aux_footprint_bytes=int(st.workspace_bytes),
+        method="gpu",
+        sorted=True,
+        details={
+            "device_ms": st.ms_total,
+            "digit_bits": tuple(st.bits),
+            "rank_mode": "smem-atomic" if st.rank_mode == 0 else "or-mask",
+            "big_buckets": int(st.n_big_buckets),
+            "devices": 1,
+        },
+    )
+
+
+def prefix_sum_gpu(counts: np.ndarray) -> np.ndarray:
+    """Exclusive prefix sum with the total appended, uint64 (mirrors
+    prefix_sum_parallel, baselines.py:116-127)."""
+    torch = _torch()
+    c = np.ascontiguousarray(counts)
+    if c.size and (c.min() < 0 or c.max() >= 2**32):
+        raise ValueError("counts must fit in uint32")
+    c32 = torch.from_numpy(c.astype(np.uint32).view(np.int32)).cuda()
+    out = torch.empty(c.size + 1, dtype=torch.int64, device=c32.device)
+    rc = _lib.lib.gt_prefix_sum(ctypes.c_void_p(c32.data_ptr()), c.size, ctypes.c_void_p(out.data_ptr()),
+                                _stream_handle(torch, None))
+    _lib.check(rc, "gt_prefix_sum")
+    return out.cpu().numpy().view(np.uint64)
+
+
+def edge_balanced_vertex_bounds(offsets: np.ndarray, parts: int) -> np.ndarray:
+    """Source-range sharding rule (_nb.py:118-132), computed by libgt.so."""
+    off = np.ascontiguousarray(offsets, dtype=np.uint64)
+    nv = off.shape[0] - 1
+    parts = max(1, int(parts))
+    out = np.empty(parts + 1, dtype=np.int64)
+    rc = _lib.lib.gt_edge_balanced_bounds(off.ctypes.data_as(ctypes.c_void_p), nv, parts,
+                                         out.ctypes.data_as(ctypes.c_void_p))
+    _lib.check(rc, "gt_edge_balanced_bounds")
+    return out
+
+
+def selftest_rank_order(trials: int = 1 << 26) -> int:
+    """Run the device self-test of lane-ordered shared-memory atomics; returns
+    the number of violations (0 means the fast ranking mode is used)."""
+    _torch()
+    v = ctypes.c_uint64(0)
+    _lib.check(_lib.lib.gt_selftest_rank_order(trials, ctypes.byref(v)), "gt_selftest_rank_order")
+    return int(v.value)
+
+
+def set_rank_mode(mode: int) -> None:
+    """-1 auto (self-test), 0 smem-atomic ranking, 1 safe OR-mask ranking."""
+    _lib.check(_lib.lib.gt_set_rank_mode(int(mode)), "gt_set_rank_mode")

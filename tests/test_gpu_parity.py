@@ -1,0 +1,229 @@
+"""GPU parity: libgt.so (through the C ABI / transpose_gpu) against the CPU
+oracle and the reference's golden outputs.  Bit-exact: identical CSC offsets
+(uint64) and identical neighbour arrays (uint32), lists ascending by source."""
+
+import ctypes
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, random_graph, sha
+
+sys.path.insert(0, str(ROOT))
+from oracle import oracle  # noqa: E402  (test infrastructure)
+
+pytestmark = pytest.mark.gpu
+
+RANK_MODES = [0, 1]  # 0 = smem-atomic ranking (default when the self-test passes), 1 = safe OR-mask
+
+
+@pytest.fixture(params=RANK_MODES, ids=["atomic-rank", "safe-rank"])
+def rank_mode(request):
+    from paper_2501_06872_b200 import set_rank_mode
+
+    set_rank_mode(request.param)
+    yield request.param
+    set_rank_mode(-1)
+
+
+def _graph(nv, off, edg):
+    from paper_2501_06872_b200 import CsrGraph
+
+    return CsrGraph(nv, int(edg.shape[0]), off.astype(np.uint64), edg.astype(np.uint32))
+
+
+def test_selftest_lane_order():
+    from paper_2501_06872_b200 import selftest_rank_order
+
+    assert selftest_rank_order(1 << 24) == 0
+
+
+def test_golden_cases(golden_cases, rank_mode):
+    from paper_2501_06872_b200 import transpose_gpu
+
+    for name, c in golden_cases.items():
+        g = _graph(c["nv"], c["off"], c["edg"])
+        out = transpose_gpu(g)
+        assert out.sorted and out.method == "gpu"
+        assert out.graph.orientation == "CSC"
+        assert out.graph.offsets.dtype == np.uint64 and out.graph.edges.dtype == np.uint32
+        assert np.array_equal(out.graph.offsets, c["toff"]), name
+        assert np.array_equal(out.graph.edges, c["tedg"]), name
+
+
+def test_random_suite_vs_oracle(rank_mode):
+    from paper_2501_06872_b200 import lists_are_sorted, transpose_gpu
+
+    rng = np.random.default_rng(2024 + rank_mode)
+    for i in range(60):
+        g = random_graph(rng, max_vertices=3000, max_edges=40_000)
+        toff, tedg = oracle.transpose_c(g.offsets, g.edges, g.num_vertices)
+        out = transpose_gpu(g)
+        assert np.array_equal(out.graph.offsets, toff), i
+        assert np.array_equal(out.graph.edges, tedg), i
+        assert lists_are_sorted(out.graph)
+
+
+def test_involution():
+    from paper_2501_06872_b200 import transpose_gpu
+
+    rng = np.random.default_rng(7)
+    for _ in range(10):
+        g = random_graph(rng, max_vertices=500, max_edges=5000)
+        back = transpose_gpu(transpose_gpu(g).graph).graph
+        # transposing twice gives the canonical (sorted-list) form of g
+        co, ce = oracle.transpose_c(*oracle.transpose_c(g.offsets, g.edges, g.num_vertices), g.num_vertices)
+        assert np.array_equal(back.offsets, co) and np.array_equal(back.edges, ce)
+        assert back.orientation == "CSR"
+
+
+def test_c1_matches_reference_hash(golden_hashes, rank_mode):
+    from paper_2501_06872_b200 import gen, transpose_gpu
+
+    cfg = gen.CONFIGS["C1"]
+    off, edg = gen.generate_np(cfg)
+    out = transpose_gpu(_graph(cfg.num_vertices, off, edg))
+    assert sha(out.graph.offsets, out.graph.edges) == golden_hashes["C1"]["oracle"]
+
+
+def test_device_generator_matches_numpy(golden_hashes):
+    import torch
+
+    from paper_2501_06872_b200 import gen
+
+    cfg = gen.CONFIGS["C1"]
+    off_d, edg_d = gen.generate_device(cfg)
+    torch.cuda.synchronize()
+    off = off_d.cpu().numpy().view(np.uint64)
+    edg = edg_d.cpu().numpy().view(np.uint32)
+    assert sha(off, edg) == golden_hashes["C1"]["input"]
+    # permuted RMAT and ER at a reduced edge count: device == numpy
+    for kind_cfg, E in ((gen.GraphConfig("p", "rmat", 1 << 13, 1 << 17, scale=13, permute=True, seed=9), 1 << 17),
+                        (gen.GraphConfig("q", "rmat", 1 << 12, 1 << 16, scale=12, permute=True, seed=3), 1 << 16),
+                        (gen.GraphConfig("e", "er", 100_003, 1 << 18, seed=11), 1 << 18)):
+        o_d, e_d = gen.generate_device(kind_cfg, num_edges=E)
+        o_n, e_n = gen.generate_np(kind_cfg)
+        assert np.array_equal(o_d.cpu().numpy().view(np.uint64), o_n)
+        assert np.array_equal(e_d.cpu().numpy().view(np.uint32), e_n)
+
+
+def test_edge_cases():
+    from paper_2501_06872_b200 import CsrGraph, transpose_gpu
+
+    # no edges, several vertex counts (test_baselines.py:151-160, test_io.py:31-37)
+    for nv in (0, 1, 17, 70_000):
+        g = CsrGraph(nv, 0, np.zeros(nv + 1, np.uint64), np.empty(0, np.uint32))
+        out = transpose_gpu(g)
+        assert np.array_equal(out.graph.offsets, np.zeros(nv + 1, np.uint64)) and out.graph.num_edges == 0
+    # every edge to one vertex, large (multi-job big-bucket path)
+    rng = np.random.default_rng(3)
+    for nv, ne in ((50, 2_000_000), (1 << 20, 3_000_000)):
+        src = np.sort(rng.integers(0, nv, ne))
+        g = CsrGraph.from_edge_pairs(src, np.full(ne, nv // 3), nv)
+        out = transpose_gpu(g)
+        toff, tedg = oracle.transpose_c(g.offsets, g.edges, nv)
+        assert np.array_equal(out.graph.offsets, toff) and np.array_equal(out.graph.edges, tedg)
+    # one source with all edges (a single out-list spanning many tiles)
+    g = CsrGraph.from_edge_pairs(np.full(1_000_000, 5), rng.integers(0, 1 << 18, 1_000_000), 1 << 18)
+    out = transpose_gpu(g)
+    toff, tedg = oracle.transpose_c(g.offsets, g.edges, g.num_vertices)
+    assert np.array_equal(out.graph.offsets, toff) and np.array_equal(out.graph.edges, tedg)
+    # many isolated sources between edges (long zero-degree runs)
+    nv = 3_000_000
+    src = rng.choice(nv, 5000, replace=False)
+    g = CsrGraph.from_edge_pairs(np.repeat(src, 40), rng.integers(0, nv, 200_000), nv)
+    out = transpose_gpu(g)
+    toff, tedg = oracle.transpose_c(g.offsets, g.edges, nv)
+    assert np.array_equal(out.graph.offsets, toff) and np.array_equal(out.graph.edges, tedg)
+
+
+@pytest.mark.parametrize("nv,ne,skew", [(1 << 16, 1 << 22, 3.0), (1_000_003, 1 << 23, 1.0), (1 << 21, 1 << 24, 6.0)])
+def test_medium_graphs(nv, ne, skew, rank_mode):
+    from paper_2501_06872_b200 import CsrGraph, transpose_gpu
+
+    rng = np.random.default_rng(nv ^ ne)
+    src = rng.integers(0, nv, ne)
+    dst = np.minimum((nv * rng.random(ne) ** skew).astype(np.int64), nv - 1)
+    perm = rng.permutation(nv)
+    g = CsrGraph.from_edge_pairs(src, perm[dst], nv)
+    out = transpose_gpu(g)
+    toff, tedg = oracle.transpose_c(g.offsets, g.edges, nv)
+    assert np.array_equal(out.graph.offsets, toff)
+    assert np.array_equal(out.graph.edges, tedg)
+    assert out.details["big_buckets"] >= 0
+
+
+def test_prefix_sum_gpu(golden_hashes):
+    from paper_2501_06872_b200 import prefix_sum_gpu
+
+    counts = np.random.default_rng(19).integers(0, 1000, size=100_000)
+    assert sha(prefix_sum_gpu(counts)) == golden_hashes["prefix_sum_100k_seed19"]
+    assert prefix_sum_gpu(np.array([2, 0, 3])).tolist() == [0, 2, 2, 5]  # test_baselines.py:19-21
+    assert prefix_sum_gpu(np.zeros(0, np.int64)).tolist() == [0]
+    big = np.random.default_rng(1).integers(0, 1 << 31, size=3_000_000)
+    assert np.array_equal(prefix_sum_gpu(big).astype(np.int64), np.concatenate([[0], np.cumsum(big)]))
+
+
+def test_host_entry_point_e2e():
+    """gt_transpose_host: host buffers in/out through the C ABI."""
+    from paper_2501_06872_b200 import _lib
+
+    rng = np.random.default_rng(11)
+    g = random_graph(rng, max_vertices=20_000, max_edges=300_000)
+    toff = np.empty(g.num_vertices + 1, np.uint64)
+    tedg = np.empty(g.num_edges, np.uint32)
+    st = _lib.GtStats()
+    rc = _lib.lib.gt_transpose_host(g.offsets.ctypes.data_as(ctypes.c_void_p), g.edges.ctypes.data_as(ctypes.c_void_p),
+                                    g.num_vertices, g.num_edges, toff.ctypes.data_as(ctypes.c_void_p),
+                                    tedg.ctypes.data_as(ctypes.c_void_p), 0, ctypes.byref(st))
+    _lib.check(rc, "gt_transpose_host")
+    o, e = oracle.transpose_c(g.offsets, g.edges, g.num_vertices)
+    assert np.array_equal(toff, o) and np.array_equal(tedg, e)
+
+
+@pytest.mark.parametrize("parts", [1, 2, 3, 8])
+def test_shard_pipeline_single_gpu(parts):
+    """The multi-GPU building blocks, run for every rank on one GPU in sequence
+    (no kernel waits on another): sender partitions + receiver transposes."""
+    from paper_2501_06872_b200.multi import GpuShardBackend, plan_shards, transpose_sharded_local
+
+    rng = np.random.default_rng(parts)
+    nv, ne = 200_003, 2_000_000
+    src = rng.integers(0, nv, ne)
+    dst = np.minimum((nv * rng.random(ne) ** 2).astype(np.int64), nv - 1)
+    from paper_2501_06872_b200 import CsrGraph
+
+    g = CsrGraph.from_edge_pairs(src, dst, nv)
+    plan = plan_shards(g.offsets, parts)
+    toff, tedg = transpose_sharded_local(g, plan, GpuShardBackend())
+    o, e = oracle.transpose_c(g.offsets, g.edges, nv)
+    assert np.array_equal(toff, o) and np.array_equal(tedg, e)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg_name", ["C2", "C3"])
+def test_full_size_configs(cfg_name):
+    """Full BASELINE sizes: generated on device, checked against the C oracle
+    bit for bit, plus size-independent properties."""
+    import torch
+
+    from paper_2501_06872_b200 import gen, transpose_device
+
+    if os.environ.get("GT_SKIP_FULL") == "1":
+        pytest.skip("GT_SKIP_FULL=1")
+    cfg = gen.CONFIGS[cfg_name]
+    off_d, edg_d = gen.generate_device(cfg)
+    t_off, t_edg, st = transpose_device(off_d, edg_d, cfg.num_vertices, want_stats=True)
+    torch.cuda.synchronize()
+    off = off_d.cpu().numpy().view(np.uint64)
+    edg = edg_d.cpu().numpy().view(np.uint32)
+    got_off = t_off.cpu().numpy().view(np.uint64)
+    got_edg = t_edg.cpu().numpy().view(np.uint32)
+    del off_d, edg_d, t_off, t_edg
+    torch.cuda.empty_cache()
+    assert got_off[-1] == cfg.num_edges
+    o, e = oracle.transpose_c(off, edg, cfg.num_vertices)
+    assert np.array_equal(got_off, o)
+    assert np.array_equal(got_edg, e)
