@@ -55,10 +55,10 @@ struct Plan {
   uint64_t V = 0, E = 0;
   int nb = 0, a = 0, b = 0, c = 0;
   int D1 = 1, Db = 1, Dc = 1;
-  uint64_t CT = 65536, ntiles = 0, max_chunks = 0;
+  uint64_t CT = 65536, ntiles = 0, nplace = 0, max_chunks = 0, max_items_s = 0, max_items_b = 0;
   // workspace offsets
-  uint64_t o_rec, o_tcnt, o_tbase, o_tsrc, o_cstart, o_cfirst, o_cbucket, o_segoff, o_fhist, o_fbase,
-      o_status, o_ctr, o_big, o_bigcnt, o_err, total;
+  uint64_t o_rec, o_tcnt, o_tbase, o_psrc, o_cstart, o_cfirst, o_cbucket, o_segoff, o_items_s, o_items_b, o_bigb,
+      o_bigbase, o_cnttab, o_curtab, o_status, o_ctr, o_counters, o_err, total;
 };
 
 int make_plan(uint64_t V, uint64_t E, Plan& p) {
@@ -67,13 +67,13 @@ int make_plan(uint64_t V, uint64_t E, Plan& p) {
   p.nb = bits_for(V);
   if (p.nb > 30) return set_err(GT_EINVAL, "num_vertices > 2^30 is not supported by this build");
   const double avg = V ? (double)E / (double)V : 1.0;
+  // final digit: fine buckets of 2^c vertices averaging <= kFCap/2 records
   int c = 0;
-  const double target = (double)kFCap / 3.0;
-  while (c < 8 && (double)(1u << (c + 1)) * std::max(avg, 1.0) <= target) ++c;
+  while (c < 8 && (double)(1u << (c + 1)) * std::max(avg, 1.0) <= (double)kFCap / 2.0) ++c;
   c = std::min(c, p.nb);
   const int rem = p.nb - c;
   int a, b;
-  if (rem <= 11) {
+  if (rem <= 10) {
     a = rem;
     b = 0;
   } else {
@@ -93,8 +93,11 @@ int make_plan(uint64_t V, uint64_t E, Plan& p) {
     p.CT *= 2;
     p.ntiles = (E + p.CT - 1) / p.CT;
   }
+  p.nplace = (E + kPlaceTile - 1) / kPlaceTile;
   p.max_chunks = (E + kChunk - 1) / kChunk + (uint64_t)p.D1;
   const uint64_t nfine = (uint64_t)p.D1 * p.Db;
+  p.max_items_s = nfine;
+  p.max_items_b = E / kFCap + nfine;
   uint64_t off = 0;
   auto take = [&](uint64_t bytes) {
     const uint64_t o = off;
@@ -104,18 +107,21 @@ int make_plan(uint64_t V, uint64_t E, Plan& p) {
   p.o_rec = take(E * 8);
   p.o_tcnt = take((uint64_t)p.D1 * p.ntiles * 4);
   p.o_tbase = take(((uint64_t)p.D1 * p.ntiles + 1) * 8);
-  p.o_tsrc = take(p.ntiles * 4);
+  p.o_psrc = take((p.nplace + 2) * 4);
   p.o_cstart = take((uint64_t)(p.D1 + 1) * 8);
   p.o_cfirst = take((uint64_t)(p.D1 + 1) * 4);
   p.o_cbucket = take(p.max_chunks * 4);
-  p.o_segoff = take(p.b ? p.max_chunks * (uint64_t)(p.Db + 1) * 4 : 0);
-  p.o_fhist = take(nfine * 8);
-  p.o_fbase = take((nfine + 1) * 8);
-  const uint64_t max_scan = std::max<uint64_t>((uint64_t)p.D1 * p.ntiles, nfine) + 1;
+  p.o_segoff = take(p.b ? p.max_chunks * (uint64_t)(p.Db + 1) * 2 : 0);
+  p.o_items_s = take(p.max_items_s * sizeof(FItem));
+  p.o_items_b = take(p.max_items_b * sizeof(FItem));
+  p.o_bigb = take(nfine * 3 * 4);
+  p.o_bigbase = take(nfine * 8);
+  p.o_cnttab = take(p.max_items_b * p.Dc * 4);
+  p.o_curtab = take(p.max_items_b * p.Dc * 8);
+  const uint64_t max_scan = (uint64_t)p.D1 * p.ntiles + 1;
   p.o_status = take(((max_scan + kScanTile - 1) / kScanTile + 1) * 8);
   p.o_ctr = take(64);
-  p.o_big = take(nfine * 4);
-  p.o_bigcnt = take(4);
+  p.o_counters = take(64);  // n_items_s, n_items_b, n_big
   p.o_err = take(4);
   p.total = off;
   return GT_OK;
@@ -190,20 +196,40 @@ int rank_mode_for(int dev, cudaStream_t st, int* mode) {
   return GT_OK;
 }
 
-size_t smem_l1_place(int D, int mode) {
-  const int W = kL1Warps;
-  return (size_t)kPlaceTile * 8 + (size_t)D * 8 + (size_t)kPlaceTile * 4 + (size_t)W * D * 4 +
-         (mode == kRankSafe ? (size_t)W * D * 4 : 0) + (size_t)D * 8 + 40 * 4;
+size_t smem_l1_place(int D, int mode, bool records, uint64_t CT) {
+  const int W = kL1Warps, PT = kPlaceTile;
+  const size_t in = records ? (size_t)2 * PT * 8 : (size_t)2 * PT * 4 + (size_t)2 * kWinCap * 8;
+  return in + (size_t)PT * 8 + (size_t)D * 8 + (records ? 0 : (size_t)PT * 4) + (size_t)W * D * 4 +
+         (mode == kRankSafe ? (size_t)W * D * 4 : 0) + (size_t)D * 8 + 40 * 4 + (CT / PT + 4) * 4;
 }
 size_t smem_b1(const Plan& p, int mode) {
   const int W = kB1Warps, D = p.Db;
-  return (size_t)kChunk * 8 + (size_t)W * D * 4 + (mode == kRankSafe ? (size_t)W * D * 4 : 0) + (size_t)D * 8 +
+  return (size_t)2 * kChunk * 8 + (size_t)W * D * 4 + (mode == kRankSafe ? (size_t)W * D * 4 : 0) + (size_t)D * 8 +
          40 * 4;
 }
-size_t smem_final(const Plan& p, int mode) {
-  const int W = kFWarps, D = p.Dc;
-  return (size_t)kSegCap * 8 + (size_t)(kSegCap + 4) * 4 + (size_t)kFCap * 4 * 2 + (size_t)W * D * 4 +
-         (mode == kRankSafe ? (size_t)W * D * 4 : 0) + (size_t)D * 8 + 40 * 4 + kFCap + (size_t)D * 8 + 64;
+size_t smem_final(int mode) {
+  const int W = kFWarps;
+  return (size_t)2 * kFCap * 8 + (size_t)kSegCap * 8 + (size_t)(kSegCap + 4) * 4 + (size_t)W * kFMaxLocal * 4 +
+         (mode == kRankSafe ? (size_t)W * kFMaxLocal * 4 : 0) + (size_t)kFMaxLocal * 8 + 40 * 4 +
+         (size_t)kFMaxLocal * 8 + 64;
+}
+
+int g_num_sms = 0;
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+template <typename Kern>
+unsigned persistent_grid(Kern kernel, int threads, size_t smem, uint64_t work) {
+  int occ = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem) != cudaSuccess || occ < 1) occ = 1;
+  const uint64_t g = (uint64_t)num_sms() * occ;
+  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g, std::max<uint64_t>(work, 1)));
 }
 
 template <typename K>
@@ -255,7 +281,8 @@ struct Timer {
 };
 
 // Core pipeline over an input stream `in` of p.E edges whose destinations are
-// local IDs in [0, p.V).  Workspace already sized by make_plan.
+// local IDs in [0, p.V).  Workspace already sized by make_plan.  No host
+// synchronisation until the final overflow check.
 template <int kMode, class In>
 int transpose_core(const Plan& p, In in, uint64_t* t_offsets, uint32_t* t_edges, unsigned char* ws, cudaStream_t st,
                    gt_stats* stats, Timer& tm) {
@@ -263,60 +290,63 @@ int transpose_core(const Plan& p, In in, uint64_t* t_offsets, uint32_t* t_edges,
   uint2* rec = reinterpret_cast<uint2*>(ws + p.o_rec);
   uint32_t* tcnt = reinterpret_cast<uint32_t*>(ws + p.o_tcnt);
   uint64_t* tbase = reinterpret_cast<uint64_t*>(ws + p.o_tbase);
-  uint32_t* tsrc = reinterpret_cast<uint32_t*>(ws + p.o_tsrc);
+  uint32_t* psrc = reinterpret_cast<uint32_t*>(ws + p.o_psrc);
   uint64_t* cstart = reinterpret_cast<uint64_t*>(ws + p.o_cstart);
   uint32_t* cfirst = reinterpret_cast<uint32_t*>(ws + p.o_cfirst);
   uint32_t* cbucket = reinterpret_cast<uint32_t*>(ws + p.o_cbucket);
-  uint32_t* segoff = p.b ? reinterpret_cast<uint32_t*>(ws + p.o_segoff) : nullptr;
-  unsigned long long* fhist = reinterpret_cast<unsigned long long*>(ws + p.o_fhist);
-  uint64_t* fbase = reinterpret_cast<uint64_t*>(ws + p.o_fbase);
+  uint16_t* segoff = p.b ? reinterpret_cast<uint16_t*>(ws + p.o_segoff) : nullptr;
+  FItem* items_s = reinterpret_cast<FItem*>(ws + p.o_items_s);
+  FItem* items_b = reinterpret_cast<FItem*>(ws + p.o_items_b);
+  uint32_t* bigb = reinterpret_cast<uint32_t*>(ws + p.o_bigb);
+  uint64_t* bigbase = reinterpret_cast<uint64_t*>(ws + p.o_bigbase);
+  uint32_t* cnttab = reinterpret_cast<uint32_t*>(ws + p.o_cnttab);
+  uint64_t* curtab = reinterpret_cast<uint64_t*>(ws + p.o_curtab);
   uint64_t* status = reinterpret_cast<uint64_t*>(ws + p.o_status);
   unsigned int* ctr = reinterpret_cast<unsigned int*>(ws + p.o_ctr);
-  uint32_t* big = reinterpret_cast<uint32_t*>(ws + p.o_big);
-  uint32_t* bigcnt = reinterpret_cast<uint32_t*>(ws + p.o_bigcnt);
+  uint32_t* counters = reinterpret_cast<uint32_t*>(ws + p.o_counters);
+  uint32_t *n_s = counters, *n_b = counters + 1, *n_big = counters + 2;
   unsigned int* err = reinterpret_cast<unsigned int*>(ws + p.o_err);
-  const uint64_t nfine = (uint64_t)p.D1 * p.Db;
   const DigShift dig1{p.b + p.c};
   int rc;
+  int launches = 0;
 
-  GT_CUDA(cudaMemsetAsync(bigcnt, 0, 4, st));
+  GT_CUDA(cudaMemsetAsync(counters, 0, 64, st));
   GT_CUDA(cudaMemsetAsync(err, 0, 4, st));
   if ((rc = tm.mark())) return rc;
   // ---- step 1: level-1 partition (source-ordered pass over the edge stream)
   if constexpr (!In::kRecords) {
-    k_tile_src<<<(unsigned)((p.ntiles + 255) / 256), 256, 0, st>>>(in, p.CT, p.ntiles, tsrc);
+    k_tile_src<<<(unsigned)((p.nplace + 1 + 255) / 256), 256, 0, st>>>(in, E, kPlaceTile, p.nplace + 1, psrc);
     GT_LAUNCH_CHECK();
+    ++launches;
   }
   k_l1_count<In, DigShift><<<(unsigned)p.ntiles, 512, p.D1 * 4, st>>>(in, dig1, E, p.CT, p.ntiles, p.D1, tcnt);
   GT_LAUNCH_CHECK();
   if ((rc = scan_u32_to_u64(tcnt, (uint64_t)p.D1 * p.ntiles, tbase, 0, true, status, ctr, st))) return rc;
   {
-    const size_t sm = smem_l1_place(p.D1, kMode);
+    const size_t sm = smem_l1_place(p.D1, kMode, In::kRecords, p.CT);
     if ((rc = set_smem(k_l1_place<kMode, In, DigShift>, sm))) return rc;
     k_l1_place<kMode, In, DigShift><<<(unsigned)p.ntiles, kL1Warps * 32, sm, st>>>(in, dig1, E, p.CT, p.ntiles, p.D1,
-                                                                                   tbase, tsrc, rec);
+                                                                                   tbase, psrc, rec);
     GT_LAUNCH_CHECK();
   }
-  k_coarse_info<<<1, 1024, (p.D1 + 1) * 4, st>>>(tbase, p.ntiles, p.D1, E, cstart, cfirst,
-                                                 p.b ? nullptr : fhist);
+  k_coarse_info<<<1, 1024, (p.D1 + 1) * 4, st>>>(tbase, p.ntiles, p.D1, E, cstart, cfirst, nullptr);
   GT_LAUNCH_CHECK();
   k_chunk_map<<<p.D1, 128, 0, st>>>(cfirst, p.D1, cbucket);
   GT_LAUNCH_CHECK();
+  launches += 5;
   if ((rc = tm.mark())) return rc;
-  // ---- step 2: level-2 chunk sort by the middle digit
-  const uint64_t* fine_base_ptr = cstart;
+  // ---- step 2: level-2 chunk sort by the middle digit (persistent, prefetching)
   if (p.b) {
-    GT_CUDA(cudaMemsetAsync(fhist, 0, nfine * 8, st));
     const size_t sm = smem_b1(p, kMode);
     if ((rc = set_smem(k_b1<kMode>, sm))) return rc;
-    k_b1<kMode><<<(unsigned)p.max_chunks, kB1Warps * 32, sm, st>>>(rec, cstart, cfirst, cbucket, p.D1, p.c,
-                                                                    (uint32_t)(p.Db - 1), p.Db, segoff, fhist);
+    const unsigned grid = persistent_grid(k_b1<kMode>, kB1Warps * 32, sm, p.max_chunks);
+    k_b1<kMode><<<grid, kB1Warps * 32, sm, st>>>(rec, cstart, cfirst, cbucket, p.D1, p.c, (uint32_t)(p.Db - 1), p.Db,
+                                                  segoff);
     GT_LAUNCH_CHECK();
-    if ((rc = scan_u64_to_u64(fhist, nfine, fbase, 0, true, status, ctr, st))) return rc;
-    fine_base_ptr = fbase;
+    ++launches;
   }
   if ((rc = tm.mark())) return rc;
-  // ---- step 3: final per-bucket sort, CSC offsets
+  // ---- step 3: plan, big-bucket counts/cursors, final per-item sort + CSC offsets
   FineCtx fx;
   fx.rec = rec;
   fx.cstart = cstart;
@@ -326,75 +356,46 @@ int transpose_core(const Plan& p, In in, uint64_t* t_offsets, uint32_t* t_edges,
   fx.bits_c = p.c;
   fx.mask_c = (uint32_t)(p.Dc - 1);
   fx.V = V;
+  k_f_plan<<<p.D1, 256, (3 * p.Db + 256) * 4, st>>>(fx, items_s, n_s, items_b, n_b, bigb, n_big, bigbase, t_offsets);
+  GT_LAUNCH_CHECK();
   {
-    const size_t sm = smem_final(p, kMode);
-    if ((rc = set_smem(k_final_small<kMode>, sm))) return rc;
-    k_final_small<kMode><<<(unsigned)nfine, kFWarps * 32, sm, st>>>(fx, fhist, fine_base_ptr, t_offsets, t_edges,
-                                                                     big, bigcnt);
+    const size_t sm = smem_final(kMode);
+    if ((rc = set_smem(k_final<kMode, true>, sm))) return rc;
+    if ((rc = set_smem(k_final<kMode, false>, sm))) return rc;
+    const unsigned gb = persistent_grid(k_final<kMode, true>, kFWarps * 32, sm, p.max_items_b);
+    k_final<kMode, true><<<gb, kFWarps * 32, sm, st>>>(fx, items_b, n_b, cnttab, curtab, t_offsets, t_edges);
+    GT_LAUNCH_CHECK();
+    const unsigned gs = persistent_grid(k_big_scan, 256, 0, (uint64_t)p.D1 * p.Db);
+    k_big_scan<<<gs, 256, 0, st>>>(fx, bigb, n_big, bigbase, cnttab, curtab, t_offsets, err);
+    GT_LAUNCH_CHECK();
+    const unsigned gf = persistent_grid(k_final<kMode, false>, kFWarps * 32, sm, p.max_items_s + p.max_items_b);
+    k_final<kMode, false><<<gf, kFWarps * 32, sm, st>>>(fx, items_s, n_s, cnttab, curtab, t_offsets, t_edges);
+    GT_LAUNCH_CHECK();
+    k_final<kMode, false><<<gf, kFWarps * 32, sm, st>>>(fx, items_b, n_b, cnttab, curtab, t_offsets, t_edges);
     GT_LAUNCH_CHECK();
   }
   k_set_u64<<<1, 1, 0, st>>>(t_offsets + V, E);
   GT_LAUNCH_CHECK();
-  uint32_t h_big = 0;
-  GT_CUDA(cudaMemcpyAsync(&h_big, bigcnt, 4, cudaMemcpyDeviceToHost, st));
-  GT_CUDA(cudaStreamSynchronize(st));
-  if (stats) stats->n_big_buckets = h_big;
-  if (h_big) {
-    std::vector<uint32_t> blist(h_big), cf(p.D1 + 1);
-    GT_CUDA(cudaMemcpyAsync(blist.data(), big, h_big * 4, cudaMemcpyDeviceToHost, st));
-    GT_CUDA(cudaMemcpyAsync(cf.data(), cfirst, (p.D1 + 1) * 4, cudaMemcpyDeviceToHost, st));
-    GT_CUDA(cudaStreamSynchronize(st));
-    std::sort(blist.begin(), blist.end());
-    std::vector<BigJob> jobs;
-    std::vector<uint32_t> jfirst;
-    for (uint32_t bi = 0; bi < h_big; ++bi) {
-      const uint32_t fid = blist[bi];
-      const uint32_t c = fid / p.Db;
-      jfirst.push_back((uint32_t)jobs.size());
-      for (uint32_t g = cf[c]; g < cf[c + 1]; g += kJobChunks)
-        jobs.push_back(BigJob{fid, g, std::min<uint32_t>(g + kJobChunks, cf[c + 1]), bi});
-    }
-    jfirst.push_back((uint32_t)jobs.size());
-    const uint64_t nj = jobs.size();
-    const uint64_t need = align_up(nj * sizeof(BigJob), 256) + align_up(jfirst.size() * 4, 256) +
-                          align_up(h_big * 4, 256) + align_up(nj * p.Dc * 4, 256) + align_up(nj * p.Dc * 8, 256);
-    int dev;
-    if ((rc = current_device(&dev))) return rc;
-    void* aux = nullptr;
-    if ((rc = cache_get(g_aux[dev], need, &aux))) return rc;
-    unsigned char* a = static_cast<unsigned char*>(aux);
-    BigJob* d_jobs = reinterpret_cast<BigJob*>(a);
-    a += align_up(nj * sizeof(BigJob), 256);
-    uint32_t* d_jfirst = reinterpret_cast<uint32_t*>(a);
-    a += align_up(jfirst.size() * 4, 256);
-    uint32_t* d_blist = reinterpret_cast<uint32_t*>(a);
-    a += align_up(h_big * 4, 256);
-    uint32_t* d_jobcnt = reinterpret_cast<uint32_t*>(a);
-    a += align_up(nj * p.Dc * 4, 256);
-    uint64_t* d_jobbase = reinterpret_cast<uint64_t*>(a);
-    GT_CUDA(cudaMemcpyAsync(d_jobs, jobs.data(), nj * sizeof(BigJob), cudaMemcpyHostToDevice, st));
-    GT_CUDA(cudaMemcpyAsync(d_jfirst, jfirst.data(), jfirst.size() * 4, cudaMemcpyHostToDevice, st));
-    GT_CUDA(cudaMemcpyAsync(d_blist, blist.data(), h_big * 4, cudaMemcpyHostToDevice, st));
-    k_big_count<<<(unsigned)nj, 256, p.Dc * 4, st>>>(fx, d_jobs, d_jobcnt);
-    GT_LAUNCH_CHECK();
-    k_big_scan<<<h_big, 256, p.Dc * 8, st>>>(fx, d_blist, d_jfirst, fine_base_ptr, d_jobcnt, d_jobbase, t_offsets,
-                                             err);
-    GT_LAUNCH_CHECK();
-    const size_t sm = smem_final(p, kMode);
-    if ((rc = set_smem(k_big_place<kMode>, sm))) return rc;
-    k_big_place<kMode><<<(unsigned)nj, kFWarps * 32, sm, st>>>(fx, d_jobs, d_jobbase, t_edges);
-    GT_LAUNCH_CHECK();
-    unsigned int h_err = 0;
-    GT_CUDA(cudaMemcpyAsync(&h_err, err, 4, cudaMemcpyDeviceToHost, st));
-    GT_CUDA(cudaStreamSynchronize(st));
-    if (h_err) return set_err(GT_EOVERFLOW, "32-bit degree counter overflowed (a transposed degree >= 2^32)");
-  }
+  launches += 6;
   if ((rc = tm.mark())) return rc;
+  uint32_t h_cnt[3] = {0, 0, 0};
+  unsigned int h_err = 0;
+  GT_CUDA(cudaMemcpyAsync(h_cnt, counters, 12, cudaMemcpyDeviceToHost, st));
+  GT_CUDA(cudaMemcpyAsync(&h_err, err, 4, cudaMemcpyDeviceToHost, st));
+  GT_CUDA(cudaStreamSynchronize(st));
+  if (stats) {
+    stats->n_big_buckets = h_cnt[2];
+    stats->n_launches = launches + 1 /* scan */;
+  }
+  if (h_err) return set_err(GT_EOVERFLOW, "32-bit degree counter overflowed (a transposed degree >= 2^32)");
   return GT_OK;
 }
 
+}  // namespace
+
+namespace {
 int fill_stats(const Plan& p, int mode, Timer& tm, gt_stats* stats) {
-  const uint64_t big = stats->n_big_buckets;
+  const uint64_t big = stats->n_big_buckets, launches = stats->n_launches;
   float a = 0, b = 0, c = 0, t = 0;
   GT_CUDA(cudaEventElapsedTime(&a, tm.ev[0], tm.ev[1]));
   GT_CUDA(cudaEventElapsedTime(&b, tm.ev[1], tm.ev[2]));
@@ -410,9 +411,7 @@ int fill_stats(const Plan& p, int mode, Timer& tm, gt_stats* stats) {
   stats->bits[2] = p.c;
   stats->rank_mode = mode;
   stats->n_big_buckets = big;
-  // kernels of transpose_core: tile_src (CSR input), l1_count, scan, l1_place, coarse_info,
-  // chunk_map, [b1, scan], final_small, set_u64, [big_count, big_scan, big_place]
-  stats->n_launches = 8 + (p.b ? 2 : 0) + (big ? 3 : 0);
+  stats->n_launches = launches;
   return GT_OK;
 }
 
@@ -588,13 +587,14 @@ int gt_shard_partition(const uint64_t* offsets, const uint32_t* edges_slice, uin
     dig.lo[q] = (uint32_t)std::min<uint64_t>(h_dst_bounds[q], 0xffffffffull);
   }
   uint64_t CT = 65536, ntiles = (E + CT - 1) / CT;
+  const uint64_t nplace = (E + kPlaceTile - 1) / kPlaceTile;
   uint64_t off = 0;
   const uint64_t o_tcnt = off;
   off = align_up(off + ntiles * parts * 4, 256);
   const uint64_t o_tbase = off;
   off = align_up(off + (ntiles * parts + 1) * 8, 256);
   const uint64_t o_tsrc = off;
-  off = align_up(off + ntiles * 4, 256);
+  off = align_up(off + (nplace + 2) * 4, 256);
   const uint64_t o_status = off;
   off = align_up(off + ((ntiles * parts + kScanTile) / kScanTile + 1) * 8, 256);
   const uint64_t o_ctr = off;
@@ -610,13 +610,13 @@ int gt_shard_partition(const uint64_t* offsets, const uint32_t* edges_slice, uin
   int mode;
   if ((rc = rank_mode_for(dev, st, &mode))) return rc;
   const InCsr in{offsets, edges_slice, e_rng[0], V};
-  k_tile_src<<<(unsigned)((ntiles + 255) / 256), 256, 0, st>>>(in, CT, ntiles, tsrc);
+  k_tile_src<<<(unsigned)((nplace + 1 + 255) / 256), 256, 0, st>>>(in, E, kPlaceTile, nplace + 1, tsrc);
   GT_LAUNCH_CHECK();
   k_l1_count<InCsr, DigBounds><<<(unsigned)ntiles, 512, parts * 4, st>>>(in, dig, E, CT, ntiles, parts, tcnt);
   GT_LAUNCH_CHECK();
   if ((rc = scan_u32_to_u64(tcnt, ntiles * parts, tbase, 0, true, status, ctr, st))) return rc;
   uint2* out = reinterpret_cast<uint2*>(records_out);
-  const size_t sm = smem_l1_place(parts, mode);
+  const size_t sm = smem_l1_place(parts, mode, false, CT);
   if (mode == kRankAtomic) {
     if ((rc = set_smem(k_l1_place<kRankAtomic, InCsr, DigBounds>, sm))) return rc;
     k_l1_place<kRankAtomic, InCsr, DigBounds><<<(unsigned)ntiles, kL1Warps * 32, sm, st>>>(in, dig, E, CT, ntiles, parts,

@@ -31,14 +31,16 @@ namespace gt {
 // ---------------------------------------------------------------- constants
 constexpr int kL1Warps = 8;
 constexpr int kL1Slots = 16;
-constexpr int kPlaceTile = kL1Warps * kL1Slots * 32;  // 4096 edges
+constexpr int kPlaceTile = kL1Warps * kL1Slots * 32;  // 4096 edges per place tile
+constexpr int kWinCap = 1024;                         // prefetched offsets per place tile
 constexpr int kB1Warps = 8;
-constexpr int kB1Slots = 32;
-constexpr int kChunk = kB1Warps * kB1Slots * 32;  // 8192 records
+constexpr int kB1Slots = 16;
+constexpr int kChunk = kB1Warps * kB1Slots * 32;  // 4096 records per level-2 chunk
 constexpr int kFWarps = 8;
-constexpr int kFCap = 8192;
-constexpr int kSegCap = 1024;
-constexpr int kJobChunks = 64;  // chunks per big-bucket job
+constexpr int kFSlots = 16;
+constexpr int kFCap = kFWarps * kFSlots * 32;  // 4096 records per final work item
+constexpr int kFMaxLocal = 256;                // local vertices per final work item
+constexpr int kSegCap = 1024;                  // chunks per coarse bucket held in smem
 
 // ------------------------------------------------------------ small kernels
 __global__ void k_set_u64(uint64_t* p, uint64_t v) { *p = v; }
@@ -79,12 +81,12 @@ struct DigBounds {
   }
 };
 
-// Owner (source) of the first edge of each count tile: largest v with
-// offsets[v] <= e_begin + k*CT, by binary search.
-__global__ void k_tile_src(InCsr in, uint64_t CT, uint64_t ntiles, uint32_t* __restrict__ tile_src) {
+// Owner (source) of edge min(k*CT, E-1) of the stream (global edge
+// e_begin + ...): largest v with offsets[v] <= that position, by binary search.
+__global__ void k_tile_src(InCsr in, uint64_t E, uint64_t CT, uint64_t ntiles, uint32_t* __restrict__ tile_src) {
   const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (k >= ntiles) return;
-  const uint64_t pos = in.e_begin + k * CT;
+  const uint64_t pos = in.e_begin + umin64(k * CT, E - 1);
   uint64_t lo = 0, hi = in.V;  // answer in [0, V-1]; offsets[0] = 0 <= pos
   while (hi - lo > 1) {
     const uint64_t mid = lo + (hi - lo) / 2;
@@ -130,78 +132,107 @@ __global__ void __launch_bounds__(512) k_l1_count(In in, Dig dig, uint64_t E, ui
 }
 
 // L1 place.  One CTA per count tile; its place tiles (4096 edges) are processed
-// in order with running global cursors per digit.  Writes records (src, dst)
-// grouped by digit, each group in stream order.
+// in order with running global cursors per digit, and the next place tile's
+// neighbour IDs and offsets window are prefetched with cp.async while the
+// current one is ranked.  Writes records (src, dst) grouped by digit, each
+// group in stream order.
+// place_src[t] = owner of edge min(t*kPlaceTile, E-1) (global place index t).
 template <int kMode, class In, class Dig>
 __global__ void __launch_bounds__(kL1Warps * 32) k_l1_place(In in, Dig dig, uint64_t E, uint64_t CT, uint64_t ntiles,
                                                            int D, const uint64_t* __restrict__ tbase,
-                                                           const uint32_t* __restrict__ tile_src,
+                                                           const uint32_t* __restrict__ place_src,
                                                            uint2* __restrict__ rec_out) {
-  constexpr int W = kL1Warps, K = kL1Slots, T = W * 32;
+  constexpr int W = kL1Warps, K = kL1Slots, T = W * 32, PT = kPlaceTile;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint2* s_stage = reinterpret_cast<uint2*>(smem_raw);                  // kPlaceTile
-  uint64_t* s_gcur = reinterpret_cast<uint64_t*>(s_stage + kPlaceTile);  // D
-  uint32_t* s_mark = reinterpret_cast<uint32_t*>(s_gcur + D);            // kPlaceTile
-  uint32_t* s_cnt = s_mark + kPlaceTile;                                 // W * D
-  uint32_t* s_scr = s_cnt + W * D;                                       // W * D (safe mode)
-  uint32_t* s_dstart = s_scr + (kMode == kRankSafe ? W * D : 0);         // D
-  uint32_t* s_dtot = s_dstart + D;                                       // D
-  uint32_t* s_tmp = s_dtot + D;                                          // 40
+  // input staging: CSR -> dst u32[2][PT] + offsets window u64[2][kWinCap]; records -> uint2[2][PT]
+  constexpr size_t kInBytes = In::kRecords ? 2 * PT * 8 : 2 * PT * 4 + 2 * kWinCap * 8;
+  unsigned char* s_in = smem_raw;
+  uint2* s_stage = reinterpret_cast<uint2*>(smem_raw + kInBytes);     // PT
+  uint64_t* s_gcur = reinterpret_cast<uint64_t*>(s_stage + PT);       // D
+  uint32_t* s_mark = reinterpret_cast<uint32_t*>(s_gcur + D);         // PT (CSR only)
+  uint32_t* s_cnt = s_mark + (In::kRecords ? 0 : PT);                 // W * D
+  uint32_t* s_scr = s_cnt + W * D;                                    // W * D (safe mode)
+  uint32_t* s_dstart = s_scr + (kMode == kRankSafe ? W * D : 0);      // D
+  uint32_t* s_dtot = s_dstart + D;                                    // D
+  uint32_t* s_tmp = s_dtot + D;                                       // 40
+  uint32_t* s_psrc = s_tmp + 40;                                      // CT/PT + 2 (CSR only)
   __shared__ uint32_t s_wmax[W];
-  __shared__ uint32_t s_next_src;
 
   const uint64_t k = blockIdx.x;
   const uint64_t tb = k * CT, te = umin64(E, tb + CT);
+  const int nplace = (int)((te - tb + PT - 1) / PT);
+  const uint64_t gp0 = tb / PT;  // global index of the first place tile
   for (int d = threadIdx.x; d < D; d += T) s_gcur[d] = tbase[(uint64_t)d * ntiles + k];
+  if constexpr (!In::kRecords) {
+    for (int j = threadIdx.x; j <= nplace; j += T) s_psrc[j] = place_src[gp0 + j];
+    for (int i = threadIdx.x; i < PT; i += T) s_mark[i] = 0;
+  }
   if (kMode == kRankSafe)
     for (int i = threadIdx.x; i < W * D; i += T) s_scr[i] = 0;
-  uint32_t s_cur = 0;
-  if constexpr (!In::kRecords) s_cur = tile_src[k];
+  __syncthreads();
   const uint32_t lane = lane_id(), w = warp_id();
   uint32_t* cnt_w = s_cnt + w * D;
   uint32_t* scr_w = s_scr + (kMode == kRankSafe ? w * D : 0);
   const uint32_t seg0 = w * (K * 32);
 
-  for (uint64_t pt = tb; pt < te; pt += kPlaceTile) {
-    const uint64_t pe = umin64(te, pt + (uint64_t)kPlaceTile);
+  auto issue = [&](int j) {
+    const int b = j & 1;
+    const uint64_t pt = tb + (uint64_t)j * PT;
+    const uint32_t n = (uint32_t)(umin64(te, pt + PT) - pt);
+    if constexpr (In::kRecords) {
+      uint2* dst = reinterpret_cast<uint2*>(s_in) + b * PT;
+      for (uint32_t i = threadIdx.x; i < n; i += T) cp_async8(dst + i, in.rec + pt + i);
+    } else {
+      uint32_t* dst = reinterpret_cast<uint32_t*>(s_in) + b * PT;
+      for (uint32_t i = threadIdx.x; i < n; i += T) cp_async4(dst + i, in.edges + pt + i);
+      uint64_t* win = reinterpret_cast<uint64_t*>(s_in + 2 * PT * 4) + b * kWinCap;
+      const uint32_t s0 = s_psrc[j], s1 = s_psrc[j + 1];
+      const uint32_t wn = min(s1 - s0, (uint32_t)kWinCap);
+      for (uint32_t i = threadIdx.x; i < wn; i += T) cp_async8(win + i, in.offsets + s0 + 1 + i);
+    }
+    cp_commit();
+  };
+
+  if (nplace > 0) issue(0);
+  for (int j = 0; j < nplace; ++j) {
+    const int b = j & 1;
+    const uint64_t pt = tb + (uint64_t)j * PT;
+    const uint64_t pe = umin64(te, pt + PT);
     const uint32_t n = (uint32_t)(pe - pt);
+    if (j + 1 < nplace) {
+      issue(j + 1);
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
     for (int i = threadIdx.x; i < W * D; i += T) s_cnt[i] = 0;
+    __syncthreads();
     uint32_t r_src[K], r_dst[K];
     if constexpr (!In::kRecords) {
-      for (int i = threadIdx.x; i < kPlaceTile; i += T) s_mark[i] = 0;
-      if (threadIdx.x == 0) s_next_src = s_cur;
-      __syncthreads();
-      // owners: mark every source boundary inside the place tile
+      // owners: mark every source boundary inside the place tile (window in smem;
+      // the rare overflow beyond kWinCap is read directly)
       const uint64_t gpt = in.e_begin + pt, gpe = in.e_begin + pe;
-      uint64_t vb = (uint64_t)s_cur + 1;
-      while (true) {
-        const uint64_t v = vb + threadIdx.x;
-        bool inside = false;
-        if (v < in.V) {
-          const uint64_t o = in.offsets[v];
-          if (o < gpe) {
-            atomicMax(&s_mark[o - gpt], (uint32_t)v);
-            inside = true;
-          }
-          if (o <= gpe) atomicMax(&s_next_src, (uint32_t)v);
-        }
-        if (!__syncthreads_and(inside)) break;
-        vb += T;
+      const uint32_t s0 = s_psrc[j], s1 = s_psrc[j + 1];
+      const uint64_t* win = reinterpret_cast<const uint64_t*>(s_in + 2 * PT * 4) + b * kWinCap;
+      for (uint32_t i = threadIdx.x; i < s1 - s0; i += T) {
+        const uint64_t o = (i < (uint32_t)kWinCap) ? win[i] : in.offsets[s0 + 1 + i];
+        if (o < gpe) atomicMax(&s_mark[o - gpt], s0 + 1 + i);
       }
-      // per-warp max of marks -> starting owner of each warp segment
+      __syncthreads();
       uint32_t wm = 0;
 #pragma unroll
       for (int s = 0; s < K; ++s) wm = max(wm, s_mark[seg0 + s * 32 + lane]);
       wm = __reduce_max_sync(kFull, wm);
       if (lane == 0) s_wmax[w] = wm;
       __syncthreads();
-      uint32_t carry = s_cur;
+      uint32_t carry = s0;
       for (int ww = 0; ww < (int)w; ++ww) carry = max(carry, s_wmax[ww]);
+      const uint32_t* dbuf = reinterpret_cast<const uint32_t*>(s_in) + b * PT;
 #pragma unroll
       for (int s = 0; s < K; ++s) {
         const uint32_t i = seg0 + s * 32 + lane;
         const bool valid = i < n;
-        r_dst[s] = valid ? in.dst(pt + i) : 0u;
+        r_dst[s] = valid ? dbuf[i] : 0u;
         uint32_t m = s_mark[i];
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -214,14 +245,14 @@ __global__ void __launch_bounds__(kL1Warps * 32) k_l1_place(In in, Dig dig, uint
         if (valid) smem_inc(&cnt_w[dig(r_dst[s])]);
       }
     } else {
-      __syncthreads();
+      const uint2* rbuf = reinterpret_cast<const uint2*>(s_in) + b * PT;
 #pragma unroll
       for (int s = 0; s < K; ++s) {
         const uint32_t i = seg0 + s * 32 + lane;
         const bool valid = i < n;
         uint2 r = make_uint2(0, 0);
         if (valid) {
-          r = ldg_stream(in.rec + pt + i);
+          r = rbuf[i];
           r.y -= in.dst_base;
           smem_inc(&cnt_w[dig(r.y)]);
         }
@@ -231,7 +262,6 @@ __global__ void __launch_bounds__(kL1Warps * 32) k_l1_place(In in, Dig dig, uint
     }
     __syncthreads();
     warp_counts_to_bases<W>(s_cnt, D, s_dstart, s_dtot, s_tmp);
-    // round 2: final tile-local positions; stage records in digit order
 #pragma unroll
     for (int s = 0; s < K; ++s) {
       const uint32_t i = seg0 + s * 32 + lane;
@@ -240,16 +270,15 @@ __global__ void __launch_bounds__(kL1Warps * 32) k_l1_place(In in, Dig dig, uint
       if (valid) s_stage[pos] = make_uint2(r_src[s], r_dst[s]);
     }
     __syncthreads();
-    // write out: consecutive staged records of a digit are consecutive in rec_out
     for (uint32_t i = threadIdx.x; i < n; i += T) {
       const uint2 r = s_stage[i];
       const uint32_t d = dig(r.y);
       rec_out[s_gcur[d] + (i - s_dstart[d])] = r;
     }
+    if constexpr (!In::kRecords)
+      for (int i = threadIdx.x; i < PT; i += T) s_mark[i] = 0;
     __syncthreads();
     for (int d = threadIdx.x; d < D; d += T) s_gcur[d] += s_dtot[d];
-    if constexpr (!In::kRecords) s_cur = s_next_src;
-    __syncthreads();
   }
 }
 
@@ -284,62 +313,91 @@ __global__ void k_chunk_map(const uint32_t* __restrict__ chunk_first, int D1, ui
   for (uint32_t g = chunk_first[c] + threadIdx.x; g < chunk_first[c + 1]; g += blockDim.x) chunk_bucket[g] = c;
 }
 
-// B1: in-place stable sort of each chunk by the middle digit.
+
+
+// B1: stable sort of each chunk by the middle digit, in place.  Persistent
+// CTAs stride over the chunks; the next chunk is prefetched with cp.async
+// while the current one is ranked.  segoff[g][f] (u16) = start of fine digit f
+// inside chunk g.
 template <int kMode>
-__global__ void __launch_bounds__(kB1Warps * 32) k_b1(
-    uint2* __restrict__ rec, const uint64_t* __restrict__ cstart, const uint32_t* __restrict__ chunk_first,
-    const uint32_t* __restrict__ chunk_bucket, int D1, int shift_b, uint32_t mask_b, int Db,
-    uint32_t* __restrict__ segoff, unsigned long long* __restrict__ fine_hist) {
-  constexpr int W = kB1Warps, K = kB1Slots, T = W * 32;
+__global__ void __launch_bounds__(kB1Warps * 32) k_b1(uint2* __restrict__ rec, const uint64_t* __restrict__ cstart,
+                                                     const uint32_t* __restrict__ chunk_first,
+                                                     const uint32_t* __restrict__ chunk_bucket, int D1, int shift_b,
+                                                     uint32_t mask_b, int Db, uint16_t* __restrict__ segoff) {
+  constexpr int W = kB1Warps, K = kB1Slots, T = W * 32, CH = kChunk;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint2* s_stage = reinterpret_cast<uint2*>(smem_raw);  // kChunk
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_stage + kChunk);
+  uint2* s_buf = reinterpret_cast<uint2*>(smem_raw);  // 2 * CH (the current buffer doubles as staging)
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_buf + 2 * CH);
   uint32_t* s_scr = s_cnt + W * Db;
   uint32_t* s_dstart = s_scr + (kMode == kRankSafe ? W * Db : 0);
   uint32_t* s_dtot = s_dstart + Db;
   uint32_t* s_tmp = s_dtot + Db;
-  const uint32_t g = blockIdx.x;
-  if (g >= chunk_first[D1]) return;  // grid is an upper bound on the chunk count
-  const uint32_t c = chunk_bucket[g];
-  const uint64_t start = cstart[c] + (uint64_t)(g - chunk_first[c]) * kChunk;
-  const uint32_t n = (uint32_t)umin64(kChunk, cstart[c + 1] - start);
-  for (int i = threadIdx.x; i < W * Db; i += T) {
-    s_cnt[i] = 0;
-    if (kMode == kRankSafe) s_scr[i] = 0;
-  }
-  __syncthreads();
+  const uint32_t nchunks = chunk_first[D1];
   const uint32_t lane = lane_id(), w = warp_id();
   uint32_t* cnt_w = s_cnt + w * Db;
   uint32_t* scr_w = s_scr + (kMode == kRankSafe ? w * Db : 0);
   const uint32_t seg0 = w * (K * 32);
-  uint2 r[K];
-#pragma unroll
-  for (int s = 0; s < K; ++s) {
-    const uint32_t i = seg0 + s * 32 + lane;
-    if (i < n) {
-      r[s] = rec[start + i];  // plain load: this chunk is rewritten in place below
-      smem_inc(&cnt_w[(r[s].y >> shift_b) & mask_b]);
+  if (kMode == kRankSafe)
+    for (int i = threadIdx.x; i < W * Db; i += T) s_scr[i] = 0;
+
+  auto chunk_range = [&](uint32_t g, uint64_t& start, uint32_t& n) {
+    const uint32_t c = chunk_bucket[g];
+    start = cstart[c] + (uint64_t)(g - chunk_first[c]) * CH;
+    n = (uint32_t)umin64(CH, cstart[c + 1] - start);
+  };
+  auto issue = [&](uint32_t g, int b) {
+    uint64_t st;
+    uint32_t n;
+    chunk_range(g, st, n);
+    uint2* dst = s_buf + b * CH;
+    for (uint32_t i = threadIdx.x; i < n; i += T) cp_async8(dst + i, rec + st + i);
+    cp_commit();
+  };
+
+  uint32_t g = blockIdx.x;
+  if (g < nchunks) issue(g, 0);
+  for (int it = 0; g < nchunks; ++it, g += gridDim.x) {
+    const int b = it & 1;
+    const uint32_t gn = g + gridDim.x;
+    if (gn < nchunks) {
+      issue(gn, b ^ 1);
+      cp_wait<1>();
     } else {
-      r[s] = make_uint2(0, 0);
+      cp_wait<0>();
     }
-  }
-  __syncthreads();
-  warp_counts_to_bases<W>(s_cnt, Db, s_dstart, s_dtot, s_tmp);
+    uint64_t start;
+    uint32_t n;
+    chunk_range(g, start, n);
+    for (int i = threadIdx.x; i < W * Db; i += T) s_cnt[i] = 0;
+    __syncthreads();
+    uint2* buf = s_buf + b * CH;
 #pragma unroll
-  for (int s = 0; s < K; ++s) {
-    const uint32_t i = seg0 + s * 32 + lane;
-    const bool valid = i < n;
-    const uint32_t pos = warp_rank<kMode>(cnt_w, scr_w, (r[s].y >> shift_b) & mask_b, valid);
-    if (valid) s_stage[pos] = r[s];
+    for (int s = 0; s < K; ++s) {
+      const uint32_t i = seg0 + s * 32 + lane;
+      if (i < n) smem_inc(&cnt_w[(buf[i].y >> shift_b) & mask_b]);
+    }
+    __syncthreads();
+    warp_counts_to_bases<W>(s_cnt, Db, s_dstart, s_dtot, s_tmp);
+    uint2 rr[K];
+    uint32_t pp[K];
+#pragma unroll
+    for (int s = 0; s < K; ++s) {
+      const uint32_t i = seg0 + s * 32 + lane;
+      const bool valid = i < n;
+      rr[s] = valid ? buf[i] : make_uint2(0, 0);
+      pp[s] = warp_rank<kMode>(cnt_w, scr_w, (rr[s].y >> shift_b) & mask_b, valid);
+    }
+    __syncthreads();  // every record of the chunk is in registers: stage in place
+#pragma unroll
+    for (int s = 0; s < K; ++s)
+      if (seg0 + s * 32 + lane < n) buf[pp[s]] = rr[s];
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < n; i += T) rec[start + i] = buf[i];
+    uint16_t* so = segoff + (uint64_t)g * (Db + 1);
+    for (int f = threadIdx.x; f < Db; f += T) so[f] = (uint16_t)s_dstart[f];
+    if (threadIdx.x == 0) so[Db] = (uint16_t)n;
+    // buf / s_dstart are reused only after the next iteration's barriers
   }
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < n; i += T) rec[start + i] = s_stage[i];
-  uint32_t* so = segoff + (uint64_t)g * (Db + 1);
-  for (int f = threadIdx.x; f < Db; f += T) {
-    so[f] = s_dstart[f];
-    if (s_dtot[f]) atomicAdd(&fine_hist[(uint64_t)c * Db + f], (unsigned long long)s_dtot[f]);
-  }
-  if (threadIdx.x == 0) so[Db] = n;
 }
 
 // ------------------------------------------------------------------ final
@@ -347,268 +405,337 @@ struct FineCtx {
   const uint2* rec;
   const uint64_t* cstart;
   const uint32_t* chunk_first;
-  const uint32_t* segoff;  // nullptr when b == 0
+  const uint16_t* segoff;  // nullptr when b == 0 (each chunk is one segment)
   int Db;
   int bits_c;
   uint32_t mask_c;
   uint64_t V;
 };
 
-// Segment of fine bucket f inside chunk g (of coarse bucket c).
-__device__ __forceinline__ void fine_segment(const FineCtx& x, uint32_t c, uint32_t f, uint32_t g,
-                                             uint64_t& start, uint32_t& len) {
-  const uint64_t cpos = x.cstart[c] + (uint64_t)(g - x.chunk_first[c]) * kChunk;
-  if (x.segoff) {
-    const uint32_t* so = x.segoff + (uint64_t)g * (x.Db + 1);
-    const uint32_t a = so[f], b = so[f + 1];
-    start = cpos + a;
-    len = b - a;
-  } else {
-    start = cpos;
-    len = (uint32_t)umin64(kChunk, x.cstart[c + 1] - cpos);
-  }
-}
-
-// Shared batch engine: gather `n` records (the concatenation of nseg segments
-// described in s_seg_start/s_seg_pos) into smem, stable-rank them by digit c,
-// and stage their sources in (vertex, rank) order.  On return s_dstart[v] is the
-// batch-local start of vertex v and s_dtot[v] its count in this batch.
-template <int kMode>
-__device__ __forceinline__ void fine_batch(const FineCtx& x, uint32_t n, int nseg, const uint64_t* s_seg_start,
-                                           const uint32_t* s_seg_pos, uint32_t* s_src, uint8_t* s_dig,
-                                           uint32_t* s_out, uint32_t* s_cnt, uint32_t* s_scr, uint32_t* s_dstart,
-                                           uint32_t* s_dtot, uint32_t* s_tmp) {
-  constexpr int W = kFWarps, T = W * 32;
-  const int Dc = 1 << x.bits_c;
-  const uint32_t lane = lane_id(), w = warp_id();
-  // gather: warp w copies segments w, w+W, ...
-  for (int j = w; j < nseg; j += W) {
-    const uint64_t st = s_seg_start[j];
-    const uint32_t p0 = s_seg_pos[j], len = s_seg_pos[j + 1] - p0;
-    for (uint32_t q = lane; q < len; q += 32) {
-      const uint2 r = ldg_stream(x.rec + st + q);
-      s_src[p0 + q] = r.x;
-      s_dig[p0 + q] = (uint8_t)(r.y & x.mask_c);
-    }
-  }
-  for (int i = threadIdx.x; i < W * Dc; i += T) {
-    s_cnt[i] = 0;
-    if (kMode == kRankSafe) s_scr[i] = 0;
-  }
-  __syncthreads();
-  uint32_t* cnt_w = s_cnt + w * Dc;
-  uint32_t* scr_w = s_scr + (kMode == kRankSafe ? w * Dc : 0);
-  const uint32_t lo = (uint32_t)(((uint64_t)n * w) / W), hi = (uint32_t)(((uint64_t)n * (w + 1)) / W);
-  for (uint32_t b = lo; b < hi; b += 32) {
-    const uint32_t i = b + lane;
-    if (i < hi) smem_inc(&cnt_w[s_dig[i]]);
-  }
-  __syncthreads();
-  warp_counts_to_bases<W>(s_cnt, Dc, s_dstart, s_dtot, s_tmp);
-  for (uint32_t b = lo; b < hi; b += 32) {
-    const uint32_t i = b + lane;
-    const bool valid = i < hi;
-    const uint32_t d = valid ? s_dig[i] : 0u;
-    const uint32_t pos = warp_rank<kMode>(cnt_w, scr_w, d, valid);
-    if (valid) s_out[pos] = s_src[i];
-  }
-  __syncthreads();
-}
-
-template <int kMode>
-__global__ void __launch_bounds__(kFWarps * 32) k_final_small(FineCtx x, const unsigned long long* __restrict__ fine_hist,
-                                                             const uint64_t* __restrict__ fine_base,
-                                                             uint64_t* __restrict__ t_offsets, uint32_t* __restrict__ t_edges,
-                                                             uint32_t* __restrict__ big_list, uint32_t* __restrict__ big_count) {
-  constexpr int W = kFWarps, T = W * 32;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int Dc = 1 << x.bits_c;
-  uint64_t* s_seg_start = reinterpret_cast<uint64_t*>(smem_raw);    // kSegCap
-  uint32_t* s_seg_pos = reinterpret_cast<uint32_t*>(s_seg_start + kSegCap);  // kSegCap + 1
-  uint32_t* s_src = s_seg_pos + kSegCap + 4;                        // kFCap
-  uint32_t* s_out = s_src + kFCap;                                  // kFCap
-  uint32_t* s_cnt = s_out + kFCap;                                  // W * Dc
-  uint32_t* s_scr = s_cnt + W * Dc;                                 // W * Dc (safe)
-  uint32_t* s_dstart = s_scr + (kMode == kRankSafe ? W * Dc : 0);   // Dc
-  uint32_t* s_dtot = s_dstart + Dc;                                 // Dc
-  uint32_t* s_tmp = s_dtot + Dc;                                    // 40
-  uint8_t* s_dig = reinterpret_cast<uint8_t*>(s_tmp + 40);          // kFCap
-
-  const uint32_t fid = blockIdx.x;
-  const uint64_t v0 = (uint64_t)fid << x.bits_c;
-  if (v0 >= x.V) return;
-  const uint32_t nv = (uint32_t)umin64((uint64_t)Dc, x.V - v0);
-  const uint64_t n64 = fine_hist[fid];
-  const uint64_t base = fine_base[fid];
-  if (n64 == 0) {
-    for (uint32_t v = threadIdx.x; v < nv; v += T) t_offsets[v0 + v] = base;
-    return;
-  }
-  const uint32_t c = fid / x.Db, f = fid % x.Db;
-  const uint32_t g0 = x.chunk_first[c], g1 = x.chunk_first[c + 1];
-  const int nch = (int)(g1 - g0);
-  if (n64 > (uint64_t)kFCap || nch > kSegCap) {
-    if (threadIdx.x == 0) big_list[atomicAdd(big_count, 1u)] = fid;
-    return;
-  }
-  const uint32_t n = (uint32_t)n64;
-  for (int j = threadIdx.x; j < nch; j += T) {
-    uint64_t st;
-    uint32_t len;
-    fine_segment(x, c, f, g0 + j, st, len);
-    s_seg_start[j] = st;
-    s_seg_pos[j] = len;
-  }
-  __syncthreads();
-  block_excl_scan_u32(s_seg_pos, nch, s_tmp);
-  if (threadIdx.x == 0) s_seg_pos[nch] = n;
-  __syncthreads();
-  fine_batch<kMode>(x, n, nch, s_seg_start, s_seg_pos, s_src, s_dig, s_out, s_cnt, s_scr, s_dstart, s_dtot, s_tmp);
-  for (uint32_t v = threadIdx.x; v < nv; v += T) t_offsets[v0 + v] = base + s_dstart[v];
-  for (uint32_t i = threadIdx.x; i < n; i += T) t_edges[base + i] = s_out[i];
-}
-
-// Big fine buckets.  A job = (fid, first chunk, last chunk).
-struct BigJob {
-  uint32_t fid;
-  uint32_t g0, g1;   // chunk range (absolute chunk ids)
-  uint32_t bucket;   // index into the big-bucket list
+// Final work item: a group of consecutive fine buckets [f0, f1) of coarse
+// bucket c holding n <= kFCap records (kind 0), or one kFCap batch of a big
+// fine bucket f0 (kind 1).  The item's records are gathered by walking chunks
+// from g_start (absolute chunk id), taking the slice of fine digits [f0, f1) of
+// each chunk, after skipping `skip` records, until n records are collected.
+struct FItem {
+  uint32_t c;
+  uint32_t f0, f1;
+  uint32_t kind;
+  uint32_t n;
+  uint32_t g_start;
+  uint32_t skip;
+  uint32_t pad;
+  uint64_t base;  // kind 0: CSC position of the group's first record
 };
 
-// Count per vertex over the job's segments -> jobcnt[job][Dc].
-__global__ void __launch_bounds__(256) k_big_count(FineCtx x, const BigJob* __restrict__ jobs,
-                                                   uint32_t* __restrict__ jobcnt) {
-  extern __shared__ uint32_t s_h[];
-  const int Dc = 1 << x.bits_c;
-  const BigJob jb = jobs[blockIdx.x];
-  for (int i = threadIdx.x; i < Dc; i += blockDim.x) s_h[i] = 0;
-  __syncthreads();
-  const uint32_t c = jb.fid / x.Db, f = jb.fid % x.Db;
+// Issue cp.async copies of item `it`'s records into dst.  All threads; uses the
+// segment scratch s_st / s_pos (kSegCap entries) block by block.
+__device__ __forceinline__ void item_gather(const FineCtx& x, const FItem& it, uint64_t* s_st, uint32_t* s_pos,
+                                            uint32_t* s_tmp, uint2* dst) {
+  const uint32_t g_end = x.chunk_first[it.c + 1];
+  const uint64_t cs = x.cstart[it.c], ce = x.cstart[it.c + 1];
+  const uint32_t g_first = x.chunk_first[it.c];
   const uint32_t lane = lane_id(), w = warp_id(), nw = blockDim.x >> 5;
-  for (uint32_t g = jb.g0 + w; g < jb.g1; g += nw) {
-    uint64_t st;
-    uint32_t len;
-    fine_segment(x, c, f, g, st, len);
-    for (uint32_t q = lane; q < len; q += 32) smem_inc(&s_h[ldg_stream(x.rec + st + q).y & x.mask_c]);
+  uint32_t got = 0;       // records collected (uniform)
+  uint32_t skip = it.skip;
+  for (uint32_t gb = it.g_start; gb < g_end && got < it.n; gb += kSegCap) {
+    const int nch = (int)min((uint32_t)kSegCap, g_end - gb);
+    for (int j = threadIdx.x; j < nch; j += blockDim.x) {
+      const uint64_t cpos = cs + (uint64_t)(gb + j - g_first) * kChunk;
+      uint32_t a, e;
+      if (x.segoff) {
+        const uint16_t* so = x.segoff + (uint64_t)(gb + j) * (x.Db + 1);
+        a = so[it.f0];
+        e = so[it.f1];
+      } else {
+        a = 0;
+        e = (uint32_t)umin64(kChunk, ce - cpos);
+      }
+      s_st[j] = cpos + a;
+      s_pos[j] = e - a;
+    }
+    __syncthreads();
+    const uint32_t tot = block_excl_scan_u32(s_pos, nch, s_tmp);
+    if (threadIdx.x == 0) s_pos[nch] = tot;
+    __syncthreads();
+    // this block's records [skip, tot) map to item positions starting at `got`
+    const uint32_t lo = skip, hi = min(tot, skip + (it.n - got));
+    for (int j = w; j < nch; j += nw) {
+      const uint32_t a = max(s_pos[j], lo), e = min(s_pos[j + 1], hi);
+      if (a >= e) continue;
+      const uint64_t src = s_st[j] + (a - s_pos[j]);
+      uint2* d = dst + got + (a - lo);
+      for (uint32_t q = lane; q < e - a; q += 32) cp_async8(d + q, x.rec + src + q);
+    }
+    got += (hi > lo) ? hi - lo : 0;
+    skip = (tot > skip) ? 0 : skip - tot;
+    __syncthreads();
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < Dc; i += blockDim.x) jobcnt[(uint64_t)blockIdx.x * Dc + i] = s_h[i];
 }
 
-// Per big bucket: CSC offsets of its vertices and per-job vertex cursors.
-__global__ void k_big_scan(FineCtx x, const uint32_t* __restrict__ big_list, const uint32_t* __restrict__ job_first,
-                           const uint64_t* __restrict__ fine_base, const uint32_t* __restrict__ jobcnt,
-                           uint64_t* __restrict__ jobbase, uint64_t* __restrict__ t_offsets,
-                           unsigned int* __restrict__ err_overflow) {
-  extern __shared__ uint64_t s_tot[];  // Dc
+// Persistent final stage over planned items, the next item's records gathered
+// with cp.async while the current one is ranked.  kCount: count records per
+// local vertex of big-batch items into cnt_tab[item][Dc] (no output).
+// Big-batch item i uses cursor row i of cur_tab.
+template <int kMode, bool kCount>
+__global__ void __launch_bounds__(kFWarps * 32) k_final(FineCtx x, const FItem* __restrict__ items,
+                                                       const uint32_t* __restrict__ n_items_ptr,
+                                                       uint32_t* __restrict__ cnt_tab,
+                                                       const uint64_t* __restrict__ cur_tab,
+                                                       uint64_t* __restrict__ t_offsets, uint32_t* __restrict__ t_edges) {
+  constexpr int W = kFWarps, K = kFSlots, T = W * 32, CAP = kFCap;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint2* s_buf = reinterpret_cast<uint2*>(smem_raw);                       // 2 * CAP (staging in place)
+  uint64_t* s_st = reinterpret_cast<uint64_t*>(s_buf + 2 * CAP);           // kSegCap
+  uint32_t* s_pos = reinterpret_cast<uint32_t*>(s_st + kSegCap);           // kSegCap + 4
+  uint32_t* s_cnt = s_pos + kSegCap + 4;                                   // W * kFMaxLocal
+  uint32_t* s_scr = s_cnt + W * kFMaxLocal;                                // (safe)
+  uint32_t* s_dstart = s_scr + (kMode == kRankSafe ? W * kFMaxLocal : 0);  // kFMaxLocal
+  uint32_t* s_dtot = s_dstart + kFMaxLocal;                                // kFMaxLocal
+  uint32_t* s_tmp = s_dtot + kFMaxLocal;                                   // 40
+  uint64_t* s_cur = reinterpret_cast<uint64_t*>(s_tmp + 40);               // kFMaxLocal
+  __shared__ FItem s_item[2];
+
+  const uint32_t n_items = *n_items_ptr;
+  const uint32_t lane = lane_id(), w = warp_id();
   const int Dc = 1 << x.bits_c;
-  const uint32_t bk = blockIdx.x;
-  const uint32_t fid = big_list[bk];
-  const uint32_t j0 = job_first[bk], j1 = job_first[bk + 1];
+  if (kMode == kRankSafe)
+    for (int i = threadIdx.x; i < W * kFMaxLocal; i += T) s_scr[i] = 0;
+
+  auto prepare = [&](uint32_t idx, int b) {
+    if (threadIdx.x == 0) s_item[b] = items[idx];
+    __syncthreads();
+    const FItem it = s_item[b];
+    item_gather(x, it, s_st, s_pos, s_tmp, s_buf + b * CAP);
+    cp_commit();
+  };
+
+  uint32_t idx = blockIdx.x;
+  if (idx < n_items) prepare(idx, 0);
+  for (int itn = 0; idx < n_items; ++itn, idx += gridDim.x) {
+    const int b = itn & 1;
+    const uint32_t nidx = idx + gridDim.x;
+    if (nidx < n_items) {
+      prepare(nidx, b ^ 1);
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    const FItem it = s_item[b];
+    const uint32_t n = it.n;
+    const uint32_t f0 = it.f0;
+    const uint32_t nloc = (it.f1 - it.f0) << x.bits_c;
+    for (int i = threadIdx.x; i < W * kFMaxLocal; i += T) s_cnt[i] = 0;
+    __syncthreads();
+    uint2* buf = s_buf + b * CAP;
+    const uint32_t shift_f = x.bits_c;
+    const uint32_t mask_f = (uint32_t)x.Db - 1;
+    auto local_of = [&](uint32_t dst) -> uint32_t {
+      return ((((dst >> shift_f) & mask_f) - f0) << shift_f) | (dst & x.mask_c);
+    };
+    // per-warp counter rows use stride nloc (the layout warp_counts_to_bases expects)
+    uint32_t* cnt_w = s_cnt + w * nloc;
+    uint32_t* scr_w = s_scr + (kMode == kRankSafe ? w * nloc : 0);
+    const uint32_t seg0 = w * (K * 32);
+#pragma unroll
+    for (int s = 0; s < K; ++s) {
+      const uint32_t i = seg0 + s * 32 + lane;
+      if (i < n) smem_inc(&cnt_w[local_of(buf[i].y)]);
+    }
+    __syncthreads();
+    if constexpr (kCount) {
+      for (int v = threadIdx.x; v < Dc; v += T) {
+        uint32_t sum = 0;
+        for (int ww = 0; ww < W; ++ww) sum += s_cnt[ww * nloc + v];
+        cnt_tab[(uint64_t)idx * Dc + v] = sum;
+      }
+      __syncthreads();
+      continue;
+    }
+    warp_counts_to_bases<W>(s_cnt, (int)nloc, s_dstart, s_dtot, s_tmp);
+    if (it.kind == 0) {
+      const uint64_t v0 = ((uint64_t)it.c * x.Db + it.f0) << x.bits_c;
+      for (uint32_t v = threadIdx.x; v < nloc; v += T)
+        if (v0 + v < x.V) t_offsets[v0 + v] = it.base + s_dstart[v];
+    } else {
+      for (int v = threadIdx.x; v < Dc; v += T) s_cur[v] = cur_tab[(uint64_t)idx * Dc + v];
+    }
+    uint2 rr[K];
+    uint32_t pp[K];
+#pragma unroll
+    for (int s = 0; s < K; ++s) {
+      const uint32_t i = seg0 + s * 32 + lane;
+      const bool valid = i < n;
+      const uint2 r = valid ? buf[i] : make_uint2(0, 0);
+      const uint32_t lv = valid ? local_of(r.y) : 0u;
+      pp[s] = warp_rank<kMode>(cnt_w, scr_w, lv, valid);
+      rr[s] = make_uint2(r.x, lv);
+    }
+    __syncthreads();  // all records are in registers: stage (src, local vertex) in place
+#pragma unroll
+    for (int s = 0; s < K; ++s)
+      if (seg0 + s * 32 + lane < n) buf[pp[s]] = rr[s];
+    __syncthreads();
+    if (it.kind == 0) {
+      for (uint32_t i = threadIdx.x; i < n; i += T) t_edges[it.base + i] = buf[i].x;
+    } else {
+      for (uint32_t i = threadIdx.x; i < n; i += T) {
+        const uint2 r = buf[i];
+        t_edges[s_cur[r.y] + (i - s_dstart[r.y])] = r.x;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Plan the final stage: one CTA per coarse bucket.  Fine-bucket sizes from the
+// chunk segment tables, CSC bases, greedy groups of consecutive fine buckets
+// (<= kFCap records, <= kFMaxLocal local vertices) and big fine buckets split
+// into kFCap batches (with their starting chunk / skip); t_offsets of empty
+// fine buckets.  big_buckets[bi] = {fid, first big item, batches}.
+__global__ void k_f_plan(FineCtx x, FItem* __restrict__ items_s, uint32_t* __restrict__ n_s,
+                         FItem* __restrict__ items_b, uint32_t* __restrict__ n_b,
+                         uint32_t* __restrict__ big_buckets, uint32_t* __restrict__ n_big,
+                         uint64_t* __restrict__ big_base, uint64_t* __restrict__ t_offsets) {
+  extern __shared__ uint32_t s_dyn[];
+  uint32_t* s_sz = s_dyn;              // Db
+  uint32_t* s_base = s_sz + x.Db;      // Db
+  uint32_t* s_bigf = s_base + x.Db;    // Db
+  uint32_t* s_len = s_bigf + x.Db;     // blockDim
+  __shared__ uint32_t s_tmp[40];
+  __shared__ uint32_t s_nbig;
+  const uint32_t c = blockIdx.x;
+  const int Db = x.Db, Dc = 1 << x.bits_c;
+  const uint32_t g0 = x.chunk_first[c], g1 = x.chunk_first[c + 1];
+  const uint64_t cs = x.cstart[c];
+  for (int f = threadIdx.x; f < Db; f += blockDim.x) {
+    uint32_t sum = 0;
+    if (x.segoff) {
+      for (uint32_t g = g0; g < g1; ++g) {
+        const uint16_t* so = x.segoff + (uint64_t)g * (Db + 1);
+        sum += (uint32_t)so[f + 1] - so[f];
+      }
+    } else {
+      sum = (uint32_t)(x.cstart[c + 1] - cs);
+    }
+    s_sz[f] = sum;
+    s_base[f] = sum;
+  }
+  __syncthreads();
+  block_excl_scan_u32(s_base, Db, s_tmp);
+  for (int f = 0; f < Db; ++f) {  // t_offsets of empty fine buckets
+    if (s_sz[f]) continue;
+    const uint64_t v0 = ((uint64_t)c * Db + f) << x.bits_c;
+    for (int v = threadIdx.x; v < Dc; v += blockDim.x)
+      if (v0 + v < x.V) t_offsets[v0 + v] = cs + s_base[f];
+  }
+  if (threadIdx.x == 0) {
+    const uint32_t maxf = (uint32_t)max(1, kFMaxLocal >> x.bits_c);
+    uint32_t nbig = 0;
+    int f = 0;
+    while (f < Db) {
+      if (s_sz[f] == 0) { ++f; continue; }
+      if (s_sz[f] > (uint32_t)kFCap) { s_bigf[nbig++] = f; ++f; continue; }
+      uint32_t total = 0;
+      int e = f;
+      while (e < Db && (uint32_t)(e - f) < maxf && s_sz[e] <= (uint32_t)kFCap && total + s_sz[e] <= (uint32_t)kFCap) {
+        total += s_sz[e];
+        ++e;
+      }
+      FItem it{};
+      it.c = c; it.f0 = f; it.f1 = e; it.kind = 0; it.n = total;
+      it.g_start = g0; it.skip = 0; it.base = cs + s_base[f];
+      items_s[atomicAdd(n_s, 1u)] = it;
+      f = e;
+    }
+    s_nbig = nbig;
+  }
+  __syncthreads();
+  const uint32_t nbig = s_nbig;
+  for (uint32_t q = 0; q < nbig; ++q) {
+    const uint32_t f = s_bigf[q];
+    const uint32_t nb = (s_sz[f] + kFCap - 1) / kFCap;
+    __shared__ uint32_t s_i0;
+    if (threadIdx.x == 0) {
+      const uint32_t bi = atomicAdd(n_big, 1u);
+      const uint32_t i0 = atomicAdd(n_b, nb);
+      big_buckets[3 * bi + 0] = c * Db + f;
+      big_buckets[3 * bi + 1] = i0;
+      big_buckets[3 * bi + 2] = nb;
+      big_base[bi] = cs + s_base[f];
+      s_i0 = i0;
+    }
+    __syncthreads();
+    const uint32_t i0 = s_i0;
+    // batch k starts at record k*kFCap of the bucket's stream: locate its chunk
+    uint32_t run = 0;
+    for (uint32_t gb = g0; gb < g1; gb += blockDim.x) {
+      const uint32_t g = gb + threadIdx.x;
+      uint32_t len = 0;
+      if (g < g1) {
+        if (x.segoff) {
+          const uint16_t* so = x.segoff + (uint64_t)g * (Db + 1);
+          len = (uint32_t)so[f + 1] - so[f];
+        } else {
+          len = (uint32_t)umin64(kChunk, x.cstart[c + 1] - (cs + (uint64_t)(g - g0) * kChunk));
+        }
+      }
+      s_len[threadIdx.x] = len;
+      __syncthreads();
+      const uint32_t tot = block_excl_scan_u32(s_len, blockDim.x, s_tmp);
+      if (g < g1 && len) {
+        const uint32_t a = run + s_len[threadIdx.x], e = a + len;
+        // batches whose first record lies in [a, e)
+        for (uint32_t k = (a + kFCap - 1) / kFCap; k * kFCap < e && k < nb; ++k) {
+          FItem it{};
+          it.c = c; it.f0 = f; it.f1 = f + 1; it.kind = 1;
+          it.n = min((uint32_t)kFCap, s_sz[f] - k * kFCap);
+          it.g_start = g; it.skip = k * kFCap - a; it.base = cs + s_base[f];
+          items_b[i0 + k] = it;
+        }
+      }
+      run += tot;
+      __syncthreads();
+    }
+  }
+}
+
+// Big fine buckets: CSC offsets of their vertices and the per-batch cursors.
+__global__ void k_big_scan(FineCtx x, const uint32_t* __restrict__ big_buckets, const uint32_t* __restrict__ n_big,
+                           const uint64_t* __restrict__ big_base, const uint32_t* __restrict__ cnt_tab,
+                           uint64_t* __restrict__ cur_tab, uint64_t* __restrict__ t_offsets,
+                           unsigned int* __restrict__ err_overflow) {
+  const int Dc = 1 << x.bits_c;
+  const uint32_t nbk = *n_big;
+  for (uint32_t bk = blockIdx.x; bk < nbk; bk += gridDim.x) {
+  const uint32_t fid = big_buckets[3 * bk], i0 = big_buckets[3 * bk + 1], nb = big_buckets[3 * bk + 2];
   const uint64_t v0 = (uint64_t)fid << x.bits_c;
+  __shared__ uint64_t s_tot[kFMaxLocal];
+  __shared__ uint64_t s_ex[kFMaxLocal];
   for (int v = threadIdx.x; v < Dc; v += blockDim.x) {
     uint64_t run = 0;
-    for (uint32_t j = j0; j < j1; ++j) run += jobcnt[(uint64_t)j * Dc + v];
+    for (uint32_t j = 0; j < nb; ++j) run += cnt_tab[(uint64_t)(i0 + j) * Dc + v];
     s_tot[v] = run;
     if (run >= (1ull << 32)) atomicExch(err_overflow, 1u);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {  // Dc <= 256: serial exclusive scan is cheap
-    uint64_t run = fine_base[fid];
+  if (threadIdx.x == 0) {
+    uint64_t run = big_base[bk];
     for (int v = 0; v < Dc; ++v) {
-      const uint64_t t = s_tot[v];
-      s_tot[v] = run;
-      run += t;
+      s_ex[v] = run;
+      run += s_tot[v];
     }
   }
   __syncthreads();
   for (int v = threadIdx.x; v < Dc; v += blockDim.x) {
-    uint64_t run = s_tot[v];
+    uint64_t run = s_ex[v];
     if (v0 + v < x.V) t_offsets[v0 + v] = run;
-    for (uint32_t j = j0; j < j1; ++j) {
-      jobbase[(uint64_t)j * Dc + v] = run;
-      run += jobcnt[(uint64_t)j * Dc + v];
+    for (uint32_t j = 0; j < nb; ++j) {
+      cur_tab[(uint64_t)(i0 + j) * Dc + v] = run;
+      run += cnt_tab[(uint64_t)(i0 + j) * Dc + v];
     }
   }
-}
-
-// Place a big job: batches of whole segments (a segment longer than kFCap is
-// cut into kFCap pieces), staged in (vertex, rank) order, written as runs.
-template <int kMode>
-__global__ void __launch_bounds__(kFWarps * 32) k_big_place(FineCtx x, const BigJob* __restrict__ jobs,
-                                                           const uint64_t* __restrict__ jobbase,
-                                                           uint32_t* __restrict__ t_edges) {
-  constexpr int W = kFWarps, T = W * 32;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int Dc = 1 << x.bits_c;
-  uint64_t* s_seg_start = reinterpret_cast<uint64_t*>(smem_raw);
-  uint32_t* s_seg_pos = reinterpret_cast<uint32_t*>(s_seg_start + kSegCap);
-  uint32_t* s_src = s_seg_pos + kSegCap + 4;
-  uint32_t* s_out = s_src + kFCap;
-  uint32_t* s_cnt = s_out + kFCap;
-  uint32_t* s_scr = s_cnt + W * Dc;
-  uint32_t* s_dstart = s_scr + (kMode == kRankSafe ? W * Dc : 0);
-  uint32_t* s_dtot = s_dstart + Dc;
-  uint32_t* s_tmp = s_dtot + Dc;
-  uint8_t* s_dig = reinterpret_cast<uint8_t*>(s_tmp + 40);
-  uint64_t* s_cur = reinterpret_cast<uint64_t*>(s_dig + kFCap);  // Dc
-  __shared__ uint32_t s_nseg, s_n;
-
-  const BigJob jb = jobs[blockIdx.x];
-  const uint32_t c = jb.fid / x.Db, f = jb.fid % x.Db;
-  for (int v = threadIdx.x; v < Dc; v += T) s_cur[v] = jobbase[(uint64_t)blockIdx.x * Dc + v];
-  uint32_t g = jb.g0;
-  uint32_t g_off = 0;  // records of chunk g's segment already consumed
   __syncthreads();
-  while (g < jb.g1) {
-    // build a batch (single thread; segment lists are short)
-    if (threadIdx.x == 0) {
-      uint32_t n = 0;
-      int ns = 0;
-      while (g < jb.g1 && ns < kSegCap) {
-        uint64_t st;
-        uint32_t len;
-        fine_segment(x, c, f, g, st, len);
-        len -= g_off;
-        st += g_off;
-        if (len == 0) { ++g; g_off = 0; continue; }
-        const uint32_t take = min(len, (uint32_t)kFCap - n);
-        if (take == 0) break;
-        s_seg_start[ns] = st;
-        s_seg_pos[ns] = n;
-        ++ns;
-        n += take;
-        if (take == len) { ++g; g_off = 0; } else { g_off += take; break; }
-      }
-      s_seg_pos[ns] = n;
-      s_nseg = ns;
-      s_n = n;
-      // publish loop state through smem for the other threads
-      s_tmp[36] = g;
-      s_tmp[37] = g_off;
-    }
-    __syncthreads();
-    const uint32_t n = s_n;
-    const int ns = (int)s_nseg;
-    g = s_tmp[36];
-    g_off = s_tmp[37];
-    __syncthreads();
-    if (n == 0) break;
-    fine_batch<kMode>(x, n, ns, s_seg_start, s_seg_pos, s_src, s_dig, s_out, s_cnt, s_scr, s_dstart, s_dtot, s_tmp);
-    // staged run of vertex v: s_out[dstart[v] .. dstart[v]+dtot[v]) -> t_edges[cur[v] ..)
-    for (uint32_t i = threadIdx.x; i < n; i += T) {
-      // vertex of staged slot i: binary search in dstart (Dc <= 256)
-      int lo = 0, hi = Dc - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (s_dstart[mid] <= i) lo = mid; else hi = mid - 1;
-      }
-      // skip empty vertices that share the same start: take the last v with dstart<=i and dtot>0
-      t_edges[s_cur[lo] + (i - s_dstart[lo])] = s_out[i];
-    }
-    __syncthreads();
-    for (int v = threadIdx.x; v < Dc; v += T) s_cur[v] += s_dtot[v];
-    __syncthreads();
   }
 }
 
