@@ -122,8 +122,10 @@ int gt_shard_partition(const uint64_t *offsets, const uint32_t *edges_slice,
 /* Receiver: records (src, dst) for destinations [dst_begin, dst_end), already
  * concatenated in sender-rank order (= ascending source order), transposed
  * into the local CSC slice: t_offsets_local[0..n_local] (global positions
- * start at `global_base`) and t_edges_local[0..num_records). */
+ * start at `global_base`) and t_edges_local[0..num_records).  Sources are
+ * global IDs < src_num_vertices. */
 int gt_shard_transpose(const uint32_t *records, uint64_t num_records,
+                       uint64_t src_num_vertices,
                        uint64_t dst_begin, uint64_t dst_end, uint64_t global_base,
                        uint64_t *t_offsets_local, uint32_t *t_edges_local,
                        void *stream, gt_stats *stats);

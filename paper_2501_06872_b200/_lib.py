@@ -50,7 +50,7 @@ SYMBOLS = {
     "gt_selftest_rank_order": (_int, [_u64, ctypes.POINTER(_u64)]),
     "gt_set_rank_mode": (_int, [_int]),
     "gt_shard_partition": (_int, [_vp, _vp, _u64, _u64, _u64, _vp, _int, _vp, _vp, _vp]),
-    "gt_shard_transpose": (_int, [_vp, _u64, _u64, _u64, _u64, _vp, _vp, _vp, _stats_p]),
+    "gt_shard_transpose": (_int, [_vp, _u64, _u64, _u64, _u64, _u64, _vp, _vp, _vp, _stats_p]),
     "gt_gen_rmat": (_int, [_u64, _u64, _u64, _int, _vp, _vp, _vp]),
     "gt_gen_er": (_int, [_u64, _u64, _u64, _vp, _vp, _vp]),
     "gt_build_csr": (_int, [_vp, _vp, _u64, _u64, _vp, _vp, _vp]),

@@ -5,6 +5,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -53,32 +54,60 @@ inline int bits_for(uint64_t V) {  // bits to address IDs 0..V-1 (>= 1)
 
 struct Plan {
   uint64_t V = 0, E = 0;
-  int nb = 0, a = 0, b = 0, c = 0;
+  bool compact = false;  // 4-byte records (R1/R2), see gt_kernels.cuh
+  int L = 0, nsh = 0;    // compact R1: source low bits, source high bits
+  int nb = 0, nbs = 0, a = 0, b = 0, c = 0;
   int D1 = 1, Db = 1, Dc = 1;
   uint64_t CT = 65536, ntiles = 0, nplace = 0, max_chunks = 0, max_items_s = 0, max_items_b = 0;
   // workspace offsets
-  uint64_t o_rec, o_tcnt, o_tbase, o_psrc, o_cstart, o_cfirst, o_cbucket, o_segoff, o_items_s, o_items_b, o_bigb,
-      o_bigbase, o_cnttab, o_curtab, o_status, o_ctr, o_counters, o_err, total;
+  uint64_t o_rec, o_tcnt, o_tbase, o_psrc, o_cstart, o_cfirst, o_cbucket, o_segoff, o_fsize, o_fbase, o_ranges,
+      o_status, o_ctr, o_counters, o_err, o_seghi, o_prev, total;
 };
 
-int make_plan(uint64_t V, uint64_t E, Plan& p) {
+int make_plan(uint64_t V, uint64_t E, Plan& p, uint64_t Vsrc = 0) {
   p.V = V;
   p.E = E;
   p.nb = bits_for(V);
+  p.nbs = bits_for(Vsrc ? Vsrc : V);  // source ID bits (differs on the multi-GPU receiver side)
   if (p.nb > 30) return set_err(GT_EINVAL, "num_vertices > 2^30 is not supported by this build");
   const double avg = V ? (double)E / (double)V : 1.0;
-  // final digit: fine buckets of 2^c vertices averaging <= kFCap/2 records
-  int c = 0;
-  while (c < 8 && (double)(1u << (c + 1)) * std::max(avg, 1.0) <= (double)kFCap / 2.0) ++c;
-  c = std::min(c, p.nb);
-  const int rem = p.nb - c;
-  int a, b;
-  if (rem <= 10) {
-    a = rem;
-    b = 0;
-  } else {
-    a = rem - rem / 2;
-    b = rem / 2;
+  int a = 0, b = 0, c = 0;
+  // compact path: 4-byte records; fine buckets average ~kFCapC/2 records
+  {
+    int cc = 1;
+    while (cc < 8 && (double)(1u << (cc + 1)) * std::max(avg, 1.0) <= (double)kFCapC / 2.0) ++cc;
+    cc = std::min(cc, 32 - p.nbs);
+    cc = std::min(cc, p.nb);
+    const int rem = p.nb - cc;
+    int ca = rem, cb = 0;
+    if (rem > 9) {
+      cb = std::min(9, rem / 2);
+      ca = rem - cb;
+    }
+    const int L = 32 - (cb + cc);
+    const int nsh = std::max(0, p.nbs - L);
+    p.compact = (cc >= 1 && p.nbs + cc <= 32 && ca <= 10 && cb <= 9 && nsh <= 12 &&
+                 getenv("GT_FORCE_FULL") == nullptr);
+    if (p.compact) {
+      a = ca;
+      b = cb;
+      c = cc;
+      p.L = L;
+      p.nsh = nsh;
+    }
+  }
+  if (!p.compact) {
+    // final digit: fine buckets of 2^c vertices averaging <= kFCap/2 records
+    while (c < 8 && (double)(1u << (c + 1)) * std::max(avg, 1.0) <= (double)kFCap / 2.0) ++c;
+    c = std::min(c, p.nb);
+    const int rem = p.nb - c;
+    if (rem <= 10) {
+      a = rem;
+      b = 0;
+    } else {
+      a = rem - rem / 2;
+      b = rem / 2;
+    }
   }
   if (a > 11 || b > 11) return set_err(GT_EINVAL, "digit split out of range (nb=%d)", p.nb);
   p.a = a;
@@ -94,7 +123,8 @@ int make_plan(uint64_t V, uint64_t E, Plan& p) {
     p.ntiles = (E + p.CT - 1) / p.CT;
   }
   p.nplace = (E + kPlaceTile - 1) / kPlaceTile;
-  p.max_chunks = (E + kChunk - 1) / kChunk + (uint64_t)p.D1;
+  const uint64_t chunk = p.compact ? kChunkC : kChunk;
+  p.max_chunks = (E + chunk - 1) / chunk + (uint64_t)p.D1;
   const uint64_t nfine = (uint64_t)p.D1 * p.Db;
   p.max_items_s = nfine;
   p.max_items_b = E / kFCap + nfine;
@@ -104,25 +134,24 @@ int make_plan(uint64_t V, uint64_t E, Plan& p) {
     off = align_up(off + std::max<uint64_t>(bytes, 1), 256);
     return o;
   };
-  p.o_rec = take(E * 8);
+  p.o_rec = take(E * (p.compact ? 4 : 8));
   p.o_tcnt = take((uint64_t)p.D1 * p.ntiles * 4);
   p.o_tbase = take(((uint64_t)p.D1 * p.ntiles + 1) * 8);
   p.o_psrc = take((p.nplace + 2) * 4);
   p.o_cstart = take((uint64_t)(p.D1 + 1) * 8);
   p.o_cfirst = take((uint64_t)(p.D1 + 1) * 4);
   p.o_cbucket = take(p.max_chunks * 4);
-  p.o_segoff = take(p.b ? p.max_chunks * (uint64_t)(p.Db + 1) * 2 : 0);
-  p.o_items_s = take(p.max_items_s * sizeof(FItem));
-  p.o_items_b = take(p.max_items_b * sizeof(FItem));
-  p.o_bigb = take(nfine * 3 * 4);
-  p.o_bigbase = take(nfine * 8);
-  p.o_cnttab = take(p.max_items_b * p.Dc * 4);
-  p.o_curtab = take(p.max_items_b * p.Dc * 8);
+  p.o_segoff = take((p.b || p.compact) ? p.max_chunks * (uint64_t)(p.Db + 1) * 2 : 0);
+  p.o_fsize = take(nfine * 4);
+  p.o_fbase = take(nfine * 8);
+  p.o_ranges = take(nfine * sizeof(FRange));
   const uint64_t max_scan = (uint64_t)p.D1 * p.ntiles + 1;
   p.o_status = take(((max_scan + kScanTile - 1) / kScanTile + 1) * 8);
   p.o_ctr = take(64);
   p.o_counters = take(64);  // n_items_s, n_items_b, n_big
   p.o_err = take(4);
+  p.o_seghi = take(p.compact ? (uint64_t)p.D1 * ((1ull << p.nsh) + 1) * 8 : 0);
+  p.o_prev = take(p.compact ? (p.ntiles + 1) * 4 : 0);
   p.total = off;
   return GT_OK;
 }
@@ -196,11 +225,23 @@ int rank_mode_for(int dev, cudaStream_t st, int* mode) {
   return GT_OK;
 }
 
-size_t smem_l1_place(int D, int mode, bool records, uint64_t CT) {
+size_t smem_l1_place(int D, int mode, bool records, uint64_t CT, bool compact = false) {
   const int W = kL1Warps, PT = kPlaceTile;
   const size_t in = records ? (size_t)2 * PT * 8 : (size_t)2 * PT * 4 + (size_t)2 * kWinCap * 8;
-  return in + (size_t)PT * 8 + (size_t)D * 8 + (records ? 0 : (size_t)PT * 4) + (size_t)W * D * 4 +
-         (mode == kRankSafe ? (size_t)W * D * 4 : 0) + (size_t)D * 8 + 40 * 4 + (CT / PT + 4) * 4;
+  return in + (size_t)PT * (compact ? 4 : 8) + (size_t)D * 8 + (records ? 0 : (size_t)PT * 4) + (size_t)W * D * 4 +
+         (mode == kRankSafe ? (size_t)W * D * 4 : 0) + (size_t)D * 8 + 40 * 4 + (CT / PT + 4) * 4 +
+         (compact ? (size_t)D * 4 + (size_t)PT * 2 : 0) + 16;
+}
+size_t smem_b1c(int Db, int mode) {
+  const int W = kB1cWarps;
+  return (size_t)2 * kChunkC * 4 + (size_t)W * Db * 4 + (mode == kRankSafe ? (size_t)W * Db * 4 : 0) +
+         (size_t)Db * 8 + 40 * 4 + kMaxBnd * 8 + 16;
+}
+size_t smem_final_c(int mode) {
+  const int W = kFcWarps, ML = kFMaxLocal;
+  return (size_t)2 * kFCapC * 4 + (size_t)kSegCapC * 8 + (size_t)(kSegCapC + 4) * 4 + (size_t)W * ML * 4 +
+         (mode == kRankSafe ? (size_t)W * ML * 4 : 0) + (size_t)ML * 8 + 40 * 4 + (size_t)ML * 8 + (size_t)ML * 4 +
+         (size_t)kMaxRange * 12 + 64;
 }
 size_t smem_b1(const Plan& p, int mode) {
   const int W = kB1Warps, D = p.Db;
@@ -211,7 +252,7 @@ size_t smem_final(int mode) {
   const int W = kFWarps;
   return (size_t)2 * kFCap * 8 + (size_t)kSegCap * 8 + (size_t)(kSegCap + 4) * 4 + (size_t)W * kFMaxLocal * 4 +
          (mode == kRankSafe ? (size_t)W * kFMaxLocal * 4 : 0) + (size_t)kFMaxLocal * 8 + 40 * 4 +
-         (size_t)kFMaxLocal * 8 + 64;
+         (size_t)kFMaxLocal * 8 + (size_t)kFMaxLocal * 4 + (size_t)kMaxRange * 12 + (size_t)(kFCap + 4) * 4 + 64;
 }
 
 int g_num_sms = 0;
@@ -295,16 +336,14 @@ int transpose_core(const Plan& p, In in, uint64_t* t_offsets, uint32_t* t_edges,
   uint32_t* cfirst = reinterpret_cast<uint32_t*>(ws + p.o_cfirst);
   uint32_t* cbucket = reinterpret_cast<uint32_t*>(ws + p.o_cbucket);
   uint16_t* segoff = p.b ? reinterpret_cast<uint16_t*>(ws + p.o_segoff) : nullptr;
-  FItem* items_s = reinterpret_cast<FItem*>(ws + p.o_items_s);
-  FItem* items_b = reinterpret_cast<FItem*>(ws + p.o_items_b);
-  uint32_t* bigb = reinterpret_cast<uint32_t*>(ws + p.o_bigb);
-  uint64_t* bigbase = reinterpret_cast<uint64_t*>(ws + p.o_bigbase);
-  uint32_t* cnttab = reinterpret_cast<uint32_t*>(ws + p.o_cnttab);
-  uint64_t* curtab = reinterpret_cast<uint64_t*>(ws + p.o_curtab);
+  uint32_t* fsize = reinterpret_cast<uint32_t*>(ws + p.o_fsize);
+  uint64_t* fbase = reinterpret_cast<uint64_t*>(ws + p.o_fbase);
+  FRange* ranges = reinterpret_cast<FRange*>(ws + p.o_ranges);
   uint64_t* status = reinterpret_cast<uint64_t*>(ws + p.o_status);
   unsigned int* ctr = reinterpret_cast<unsigned int*>(ws + p.o_ctr);
   uint32_t* counters = reinterpret_cast<uint32_t*>(ws + p.o_counters);
-  uint32_t *n_s = counters, *n_b = counters + 1, *n_big = counters + 2;
+  uint32_t* n_ranges = counters;
+  unsigned int* range_ctr = counters + 1;
   unsigned int* err = reinterpret_cast<unsigned int*>(ws + p.o_err);
   const DigShift dig1{p.b + p.c};
   int rc;
@@ -324,9 +363,9 @@ int transpose_core(const Plan& p, In in, uint64_t* t_offsets, uint32_t* t_edges,
   if ((rc = scan_u32_to_u64(tcnt, (uint64_t)p.D1 * p.ntiles, tbase, 0, true, status, ctr, st))) return rc;
   {
     const size_t sm = smem_l1_place(p.D1, kMode, In::kRecords, p.CT);
-    if ((rc = set_smem(k_l1_place<kMode, In, DigShift>, sm))) return rc;
-    k_l1_place<kMode, In, DigShift><<<(unsigned)p.ntiles, kL1Warps * 32, sm, st>>>(in, dig1, E, p.CT, p.ntiles, p.D1,
-                                                                                   tbase, psrc, rec);
+    if ((rc = set_smem(k_l1_place<kMode, In, DigShift, OutFull>, sm))) return rc;
+    k_l1_place<kMode, In, DigShift, OutFull><<<(unsigned)p.ntiles, kL1Warps * 32, sm, st>>>(
+        in, dig1, E, p.CT, p.ntiles, p.D1, tbase, psrc, OutFull{rec});
     GT_LAUNCH_CHECK();
   }
   k_coarse_info<<<1, 1024, (p.D1 + 1) * 4, st>>>(tbase, p.ntiles, p.D1, E, cstart, cfirst, nullptr);
@@ -356,27 +395,35 @@ int transpose_core(const Plan& p, In in, uint64_t* t_offsets, uint32_t* t_edges,
   fx.bits_c = p.c;
   fx.mask_c = (uint32_t)(p.Dc - 1);
   fx.V = V;
-  k_f_plan<<<p.D1, 256, (3 * p.Db + 256) * 4, st>>>(fx, items_s, n_s, items_b, n_b, bigb, n_big, bigbase, t_offsets);
-  GT_LAUNCH_CHECK();
   {
+    const uint32_t target = (uint32_t)std::min<uint64_t>(
+        1u << 20, std::max<uint64_t>(4 * kFCap, E / ((uint64_t)num_sms() * 2 * 6)));
+    k_f_plan<<<p.D1, 256, 2 * p.Db * 4, st>>>(fx, target, fsize, fbase, ranges, n_ranges, t_offsets, err);
+    GT_LAUNCH_CHECK();
     const size_t sm = smem_final(kMode);
-    if ((rc = set_smem(k_final<kMode, true>, sm))) return rc;
-    if ((rc = set_smem(k_final<kMode, false>, sm))) return rc;
-    const unsigned gb = persistent_grid(k_final<kMode, true>, kFWarps * 32, sm, p.max_items_b);
-    k_final<kMode, true><<<gb, kFWarps * 32, sm, st>>>(fx, items_b, n_b, cnttab, curtab, t_offsets, t_edges);
+    if ((rc = set_smem(k_final<kMode>, sm))) return rc;
+    const unsigned gf = persistent_grid(k_final<kMode>, kFWarps * 32, sm, (uint64_t)p.D1 * p.Db);
+    unsigned long long* prof = nullptr;
+    if (getenv("GT_FPROF")) {
+      GT_CUDA(cudaMallocAsync(&prof, 10 * 8, st));
+      GT_CUDA(cudaMemsetAsync(prof, 0, 10 * 8, st));
+    }
+    k_final<kMode><<<gf, kFWarps * 32, sm, st>>>(fx, ranges, n_ranges, range_ctr, fsize, fbase, t_offsets, t_edges, err,
+                                                 prof);
     GT_LAUNCH_CHECK();
-    const unsigned gs = persistent_grid(k_big_scan, 256, 0, (uint64_t)p.D1 * p.Db);
-    k_big_scan<<<gs, 256, 0, st>>>(fx, bigb, n_big, bigbase, cnttab, curtab, t_offsets, err);
-    GT_LAUNCH_CHECK();
-    const unsigned gf = persistent_grid(k_final<kMode, false>, kFWarps * 32, sm, p.max_items_s + p.max_items_b);
-    k_final<kMode, false><<<gf, kFWarps * 32, sm, st>>>(fx, items_s, n_s, cnttab, curtab, t_offsets, t_edges);
-    GT_LAUNCH_CHECK();
-    k_final<kMode, false><<<gf, kFWarps * 32, sm, st>>>(fx, items_b, n_b, cnttab, curtab, t_offsets, t_edges);
-    GT_LAUNCH_CHECK();
+    if (prof) {
+      unsigned long long h[10];
+      GT_CUDA(cudaMemcpyAsync(h, prof, 80, cudaMemcpyDeviceToHost, st));
+      GT_CUDA(cudaStreamSynchronize(st));
+      fprintf(stderr, "[gt_fprof] grid=%u gen=%.3g issue=%.3g wait=%.3g count=%.3g bases=%.3g rank=%.3g write=%.3g loop=%.3g units0=%llu units12=%llu (cycles summed over CTAs)\n",
+              gf, (double)h[0], (double)h[1], (double)h[2], (double)h[3], (double)h[4], (double)h[5], (double)h[6],
+              (double)h[9], h[7], h[8]);
+      cudaFreeAsync(prof, st);
+    }
   }
   k_set_u64<<<1, 1, 0, st>>>(t_offsets + V, E);
   GT_LAUNCH_CHECK();
-  launches += 6;
+  launches += 3;
   if ((rc = tm.mark())) return rc;
   uint32_t h_cnt[3] = {0, 0, 0};
   unsigned int h_err = 0;
@@ -384,7 +431,7 @@ int transpose_core(const Plan& p, In in, uint64_t* t_offsets, uint32_t* t_edges,
   GT_CUDA(cudaMemcpyAsync(&h_err, err, 4, cudaMemcpyDeviceToHost, st));
   GT_CUDA(cudaStreamSynchronize(st));
   if (stats) {
-    stats->n_big_buckets = h_cnt[2];
+    stats->n_big_buckets = h_cnt[0];  /* reports the number of final ranges */
     stats->n_launches = launches + 1 /* scan */;
   }
   if (h_err) return set_err(GT_EOVERFLOW, "32-bit degree counter overflowed (a transposed degree >= 2^32)");
@@ -394,6 +441,157 @@ int transpose_core(const Plan& p, In in, uint64_t* t_offsets, uint32_t* t_edges,
 }  // namespace
 
 namespace {
+// Compact (4-byte record) pipeline: L1 -> R1 (with the source-high boundary
+// table), level 2 re-encodes to R2 in 16K-record chunks, level 3 per fine unit.
+template <int kMode, class In>
+int transpose_core_c(const Plan& p, In in, uint64_t* t_offsets, uint32_t* t_edges, unsigned char* ws, cudaStream_t st,
+                     gt_stats* stats, Timer& tm) {
+  const uint64_t V = p.V, E = p.E;
+  uint32_t* rec = reinterpret_cast<uint32_t*>(ws + p.o_rec);
+  uint32_t* tcnt = reinterpret_cast<uint32_t*>(ws + p.o_tcnt);
+  uint64_t* tbase = reinterpret_cast<uint64_t*>(ws + p.o_tbase);
+  uint32_t* psrc = reinterpret_cast<uint32_t*>(ws + p.o_psrc);
+  uint64_t* cstart = reinterpret_cast<uint64_t*>(ws + p.o_cstart);
+  uint32_t* cfirst = reinterpret_cast<uint32_t*>(ws + p.o_cfirst);
+  uint32_t* cbucket = reinterpret_cast<uint32_t*>(ws + p.o_cbucket);
+  uint16_t* segoff = reinterpret_cast<uint16_t*>(ws + p.o_segoff);
+  uint32_t* fsize = reinterpret_cast<uint32_t*>(ws + p.o_fsize);
+  uint64_t* fbase = reinterpret_cast<uint64_t*>(ws + p.o_fbase);
+  FRange* ranges = reinterpret_cast<FRange*>(ws + p.o_ranges);
+  uint64_t* status = reinterpret_cast<uint64_t*>(ws + p.o_status);
+  unsigned int* ctr = reinterpret_cast<unsigned int*>(ws + p.o_ctr);
+  uint32_t* counters = reinterpret_cast<uint32_t*>(ws + p.o_counters);
+  uint32_t* n_ranges = counters;
+  unsigned int* range_ctr = counters + 1;
+  unsigned int* err = reinterpret_cast<unsigned int*>(ws + p.o_err);
+  uint64_t* seghi = reinterpret_cast<uint64_t*>(ws + p.o_seghi);
+  uint32_t* prev = reinterpret_cast<uint32_t*>(ws + p.o_prev);
+  const DigShift dig1{p.b + p.c};
+  const uint32_t nh = 1u << p.nsh;
+  int rc;
+  int launches = 0;
+
+  GT_CUDA(cudaMemsetAsync(counters, 0, 64, st));
+  GT_CUDA(cudaMemsetAsync(err, 0, 4, st));
+  GT_CUDA(cudaMemsetAsync(seghi, 0xff, (uint64_t)p.D1 * (nh + 1) * 8, st));
+  if ((rc = tm.mark())) return rc;
+  if constexpr (!In::kRecords) {
+    k_tile_src<<<(unsigned)((p.nplace + 1 + 255) / 256), 256, 0, st>>>(in, E, kPlaceTile, p.nplace + 1, psrc);
+    GT_LAUNCH_CHECK();
+    k_prev_src<<<(unsigned)((p.ntiles + 255) / 256), 256, 0, st>>>(in, E, p.CT, p.ntiles, prev);
+    GT_LAUNCH_CHECK();
+    launches += 2;
+  }
+  k_l1_count<In, DigShift><<<(unsigned)p.ntiles, 512, p.D1 * 4, st>>>(in, dig1, E, p.CT, p.ntiles, p.D1, tcnt);
+  GT_LAUNCH_CHECK();
+  if ((rc = scan_u32_to_u64(tcnt, (uint64_t)p.D1 * p.ntiles, tbase, 0, true, status, ctr, st))) return rc;
+  {
+    OutCompact oc;
+    oc.rec = rec;
+    oc.low_mask = (uint32_t)((1ull << (p.b + p.c)) - 1);
+    oc.L = p.L;
+    oc.src_mask = (uint32_t)((1ull << p.L) - 1);
+    oc.nh = nh;
+    oc.seg_hi = seghi;
+    oc.prev_src = prev;
+    const size_t sm = smem_l1_place(p.D1, kMode, In::kRecords, p.CT, true);
+    if ((rc = set_smem(k_l1_place<kMode, In, DigShift, OutCompact>, sm))) return rc;
+    k_l1_place<kMode, In, DigShift, OutCompact><<<(unsigned)p.ntiles, kL1Warps * 32, sm, st>>>(
+        in, dig1, E, p.CT, p.ntiles, p.D1, tbase, psrc, oc);
+    GT_LAUNCH_CHECK();
+  }
+  k_coarse_info_c<<<1, 1024, (p.D1 + 1) * 4, st>>>(tbase, p.ntiles, p.D1, E, cstart, cfirst);
+  GT_LAUNCH_CHECK();
+  k_chunk_map<<<p.D1, 128, 0, st>>>(cfirst, p.D1, cbucket);
+  GT_LAUNCH_CHECK();
+  launches += 5;
+  if ((rc = tm.mark())) return rc;
+  {
+    DecodeC dc;
+    dc.L = p.L;
+    dc.src_mask = (uint32_t)((1ull << p.L) - 1);
+    dc.nh = nh;
+    dc.seg_hi = seghi;
+    dc.bits_c = p.c;
+    dc.nb = p.nbs;
+    const size_t sm = smem_b1c(p.Db, kMode);
+    if ((rc = set_smem(k_b1c<kMode>, sm))) return rc;
+    const unsigned grid = persistent_grid(k_b1c<kMode>, kB1cWarps * 32, sm, p.max_chunks);
+    k_b1c<kMode><<<grid, kB1cWarps * 32, sm, st>>>(rec, rec, cstart, cfirst, cbucket, p.D1, dc, p.Db, segoff);
+    GT_LAUNCH_CHECK();
+    ++launches;
+  }
+  if ((rc = tm.mark())) return rc;
+  {
+    FineCtx fx{};
+    fx.rec = nullptr;
+    fx.cstart = cstart;
+    fx.chunk_first = cfirst;
+    fx.segoff = segoff;
+    fx.Db = p.Db;
+    fx.bits_c = p.c;
+    fx.mask_c = (uint32_t)(p.Dc - 1);
+    fx.V = V;
+    const uint32_t target = (uint32_t)std::min<uint64_t>(
+        1u << 20, std::max<uint64_t>(4 * kFCapC, E / ((uint64_t)num_sms() * 2 * 6)));
+    k_f_plan<<<p.D1, 256, 2 * p.Db * 4, st>>>(fx, target, fsize, fbase, ranges, n_ranges, t_offsets, err);
+    GT_LAUNCH_CHECK();
+    FineCtxC xc;
+    xc.rec = rec;
+    xc.cstart = cstart;
+    xc.chunk_first = cfirst;
+    xc.segoff = segoff;
+    xc.Db = p.Db;
+    xc.bits_c = p.c;
+    xc.nb = p.nbs;
+    xc.V = V;
+    unsigned long long* prof = nullptr;
+    if (getenv("GT_FPROF")) {
+      GT_CUDA(cudaMallocAsync(&prof, 10 * 8, st));
+      GT_CUDA(cudaMemsetAsync(prof, 0, 10 * 8, st));
+    }
+    const size_t sm = smem_final_c(kMode);
+    if ((rc = set_smem(k_final_c<kMode>, sm))) return rc;
+    const unsigned gf = persistent_grid(k_final_c<kMode>, kFcWarps * 32, sm, (uint64_t)p.D1 * p.Db);
+    k_final_c<kMode><<<gf, kFcWarps * 32, sm, st>>>(xc, ranges, n_ranges, range_ctr, fsize, fbase, t_offsets, t_edges,
+                                                    prof);
+    GT_LAUNCH_CHECK();
+    if (prof) {
+      unsigned long long h[10];
+      GT_CUDA(cudaMemcpyAsync(h, prof, 80, cudaMemcpyDeviceToHost, st));
+      GT_CUDA(cudaStreamSynchronize(st));
+      fprintf(stderr,
+              "[gt_fprof-c] grid=%u gen=%.3g issue=%.3g wait=%.3g count=%.3g bases=%.3g rank=%.3g write=%.3g "
+              "loop=%.3g units0=%llu units12=%llu\\n",
+              gf, (double)h[0], (double)h[1], (double)h[2], (double)h[3], (double)h[4], (double)h[5], (double)h[6],
+              (double)h[9], h[7], h[8]);
+      cudaFreeAsync(prof, st);
+    }
+  }
+  k_set_u64<<<1, 1, 0, st>>>(t_offsets + V, E);
+  GT_LAUNCH_CHECK();
+  launches += 3;
+  if ((rc = tm.mark())) return rc;
+  uint32_t h_cnt[3] = {0, 0, 0};
+  unsigned int h_err = 0;
+  GT_CUDA(cudaMemcpyAsync(h_cnt, counters, 12, cudaMemcpyDeviceToHost, st));
+  GT_CUDA(cudaMemcpyAsync(&h_err, err, 4, cudaMemcpyDeviceToHost, st));
+  GT_CUDA(cudaStreamSynchronize(st));
+  if (stats) {
+    stats->n_big_buckets = h_cnt[0];
+    stats->n_launches = launches + 1;
+  }
+  if (h_err) return set_err(GT_EOVERFLOW, "32-bit degree counter overflowed (a transposed degree >= 2^32)");
+  return GT_OK;
+}
+
+template <int kMode, class In>
+int transpose_any(const Plan& p, In in, uint64_t* t_offsets, uint32_t* t_edges, unsigned char* ws, cudaStream_t st,
+                  gt_stats* stats, Timer& tm) {
+  if (p.compact) return transpose_core_c<kMode, In>(p, in, t_offsets, t_edges, ws, st, stats, tm);
+  return transpose_core<kMode, In>(p, in, t_offsets, t_edges, ws, st, stats, tm);
+}
+
 int fill_stats(const Plan& p, int mode, Timer& tm, gt_stats* stats) {
   const uint64_t big = stats->n_big_buckets, launches = stats->n_launches;
   float a = 0, b = 0, c = 0, t = 0;
@@ -481,8 +679,8 @@ int gt_transpose(const uint64_t* offsets, const uint32_t* edges, uint64_t V, uin
   Timer tm;
   if ((rc = tm.init(stats != nullptr, st))) return rc;
   const InCsr in{offsets, edges, 0, V};
-  rc = (mode == kRankAtomic) ? transpose_core<kRankAtomic>(p, in, t_offsets, t_edges, ws, st, stats, tm)
-                             : transpose_core<kRankSafe>(p, in, t_offsets, t_edges, ws, st, stats, tm);
+  rc = (mode == kRankAtomic) ? transpose_any<kRankAtomic>(p, in, t_offsets, t_edges, ws, st, stats, tm)
+                             : transpose_any<kRankSafe>(p, in, t_offsets, t_edges, ws, st, stats, tm);
   if (rc) return rc;
   if (stats) {
     GT_CUDA(cudaEventSynchronize(tm.ev[tm.n - 1]));
@@ -618,13 +816,13 @@ int gt_shard_partition(const uint64_t* offsets, const uint32_t* edges_slice, uin
   uint2* out = reinterpret_cast<uint2*>(records_out);
   const size_t sm = smem_l1_place(parts, mode, false, CT);
   if (mode == kRankAtomic) {
-    if ((rc = set_smem(k_l1_place<kRankAtomic, InCsr, DigBounds>, sm))) return rc;
-    k_l1_place<kRankAtomic, InCsr, DigBounds><<<(unsigned)ntiles, kL1Warps * 32, sm, st>>>(in, dig, E, CT, ntiles, parts,
-                                                                                         tbase, tsrc, out);
+    if ((rc = set_smem(k_l1_place<kRankAtomic, InCsr, DigBounds, OutFull>, sm))) return rc;
+    k_l1_place<kRankAtomic, InCsr, DigBounds, OutFull><<<(unsigned)ntiles, kL1Warps * 32, sm, st>>>(
+        in, dig, E, CT, ntiles, parts, tbase, tsrc, OutFull{out});
   } else {
-    if ((rc = set_smem(k_l1_place<kRankSafe, InCsr, DigBounds>, sm))) return rc;
-    k_l1_place<kRankSafe, InCsr, DigBounds><<<(unsigned)ntiles, kL1Warps * 32, sm, st>>>(in, dig, E, CT, ntiles, parts,
-                                                                                       tbase, tsrc, out);
+    if ((rc = set_smem(k_l1_place<kRankSafe, InCsr, DigBounds, OutFull>, sm))) return rc;
+    k_l1_place<kRankSafe, InCsr, DigBounds, OutFull><<<(unsigned)ntiles, kL1Warps * 32, sm, st>>>(
+        in, dig, E, CT, ntiles, parts, tbase, tsrc, OutFull{out});
   }
   GT_LAUNCH_CHECK();
   std::vector<uint64_t> starts(parts + 1);
@@ -636,8 +834,9 @@ int gt_shard_partition(const uint64_t* offsets, const uint32_t* edges_slice, uin
   return GT_OK;
 }
 
-int gt_shard_transpose(const uint32_t* records, uint64_t R, uint64_t dst_begin, uint64_t dst_end, uint64_t global_base,
-                       uint64_t* t_offsets_local, uint32_t* t_edges_local, void* stream, gt_stats* stats) {
+int gt_shard_transpose(const uint32_t* records, uint64_t R, uint64_t src_num_vertices, uint64_t dst_begin,
+                       uint64_t dst_end, uint64_t global_base, uint64_t* t_offsets_local, uint32_t* t_edges_local,
+                       void* stream, gt_stats* stats) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (stats) std::memset(stats, 0, sizeof(*stats));
   if (dst_end < dst_begin || !t_offsets_local || (R && (!records || !t_edges_local)))
@@ -654,7 +853,9 @@ int gt_shard_transpose(const uint32_t* records, uint64_t R, uint64_t dst_begin, 
   }
   if (V == 0) return set_err(GT_EINVAL, "gt_shard_transpose: records for an empty destination range");
   Plan p;
-  if ((rc = make_plan(V, R, p))) return rc;
+  if (src_num_vertices == 0 || src_num_vertices > (1ull << 32))
+    return set_err(GT_EINVAL, "gt_shard_transpose: bad src_num_vertices");
+  if ((rc = make_plan(V, R, p, src_num_vertices))) return rc;
   void* w = nullptr;
   if ((rc = cache_get(g_ws[dev], p.total, &w))) return rc;
   unsigned char* ws = static_cast<unsigned char*>(w);
@@ -663,8 +864,8 @@ int gt_shard_transpose(const uint32_t* records, uint64_t R, uint64_t dst_begin, 
   Timer tm;
   if ((rc = tm.init(stats != nullptr, st))) return rc;
   const InRec in{reinterpret_cast<const uint2*>(records), (uint32_t)dst_begin};
-  rc = (mode == kRankAtomic) ? transpose_core<kRankAtomic>(p, in, t_offsets_local, t_edges_local, ws, st, stats, tm)
-                             : transpose_core<kRankSafe>(p, in, t_offsets_local, t_edges_local, ws, st, stats, tm);
+  rc = (mode == kRankAtomic) ? transpose_any<kRankAtomic>(p, in, t_offsets_local, t_edges_local, ws, st, stats, tm)
+                             : transpose_any<kRankSafe>(p, in, t_offsets_local, t_edges_local, ws, st, stats, tm);
   if (rc) return rc;
   if (global_base) {
     k_add_base<<<148, 256, 0, st>>>(t_offsets_local, V + 1, global_base);

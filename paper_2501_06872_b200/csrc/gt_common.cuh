@@ -64,39 +64,43 @@ __device__ __forceinline__ uint32_t warp_rank(uint32_t* cnt, uint32_t* scratch, 
 
 // Block-wide exclusive scan of a shared uint32 array a[0..n) in place; returns
 // the total to all threads.  n may exceed blockDim.x.  Uses `tmp` (>= 33 words).
+// Warp w owns a contiguous slice; lanes touch consecutive words (no bank
+// conflicts) and a shuffle scan carries 32 elements per step.
 __device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t* a, int n, uint32_t* tmp) {
   const int T = blockDim.x, t = threadIdx.x;
-  const int per = (n + T - 1) / T;
-  const int lo = t * per, hi = min(n, lo + per);
+  const int nw = (T + 31) >> 5, w = t >> 5, lane = t & 31;
+  const int per = ((n + nw - 1) / nw + 31) & ~31;  // slice per warp, multiple of 32
+  const int lo = w * per, hi = min(n, lo + per);
   uint32_t s = 0;
-  for (int i = lo; i < hi; ++i) s += a[i];
-  // warp inclusive scan of s
-  uint32_t x = s;
+  for (int i = lo + lane; i < hi; i += 32) s += a[i];
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    uint32_t y = __shfl_up_sync(kFull, x, o);
-    if ((t & 31) >= o) x += y;
-  }
-  if ((t & 31) == 31) tmp[t >> 5] = x;
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  if (lane == 0) tmp[w] = s;
   __syncthreads();
   if (t < 32) {
-    const int nw = (T + 31) >> 5;
-    uint32_t w = (t < nw) ? tmp[t] : 0;
-    uint32_t v = w;
+    uint32_t v0 = (t < nw) ? tmp[t] : 0;
+    uint32_t v = v0;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      uint32_t y = __shfl_up_sync(kFull, v, o);
+      const uint32_t y = __shfl_up_sync(kFull, v, o);
       if (t >= o) v += y;
     }
-    if (t < nw) tmp[t] = v - w;  // exclusive warp offsets
-    if (t == 31) tmp[32] = v;    // total
+    if (t < nw) tmp[t] = v - v0;  // exclusive warp offsets
+    if (t == 31) tmp[32] = v;     // total
   }
   __syncthreads();
-  uint32_t run = tmp[t >> 5] + x - s;
-  for (int i = lo; i < hi; ++i) {
-    uint32_t v = a[i];
-    a[i] = run;
-    run += v;
+  uint32_t carry = tmp[w];
+  for (int base = lo; base < hi; base += 32) {
+    const int i = base + lane;
+    const uint32_t x = (i < hi) ? a[i] : 0u;
+    uint32_t y = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t z = __shfl_up_sync(kFull, y, o);
+      if (lane >= o) y += z;
+    }
+    if (i < hi) a[i] = carry + y - x;
+    carry += __shfl_sync(kFull, y, 31);
   }
   const uint32_t total = tmp[32];
   __syncthreads();

@@ -25,6 +25,7 @@
 #pragma once
 #include "gt_common.cuh"
 #include "gt_scan.cuh"
+#include <type_traits>
 
 namespace gt {
 
@@ -41,6 +42,16 @@ constexpr int kFSlots = 16;
 constexpr int kFCap = kFWarps * kFSlots * 32;  // 4096 records per final work item
 constexpr int kFMaxLocal = 256;                // local vertices per final work item
 constexpr int kSegCap = 1024;                  // chunks per coarse bucket held in smem
+constexpr int kMaxRange = 256;                 // fine buckets per final-stage range
+// compact (4-byte record) path
+constexpr int kB1cWarps = 16;
+constexpr int kB1cSlots = 32;
+constexpr int kChunkC = kB1cWarps * kB1cSlots * 32;  // 16384 records per chunk
+constexpr int kFcWarps = 8;
+constexpr int kFcSlots = 16;
+constexpr int kFCapC = kFcWarps * kFcSlots * 32;  // 4096 records per final unit
+constexpr int kSegCapC = 512;
+constexpr int kMaxBnd = 64;
 
 // ------------------------------------------------------------ small kernels
 __global__ void k_set_u64(uint64_t* p, uint64_t v) { *p = v; }
@@ -95,6 +106,24 @@ __global__ void k_tile_src(InCsr in, uint64_t E, uint64_t CT, uint64_t ntiles, u
   tile_src[k] = (uint32_t)lo;
 }
 
+// Source of the edge just before each count tile (compact path): owner of
+// edge k*CT - 1 for k >= 1, ~0u for k = 0.
+__global__ void k_prev_src(InCsr in, uint64_t E, uint64_t CT, uint64_t ntiles, uint32_t* __restrict__ prev) {
+  const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (k >= ntiles) return;
+  if (k == 0) {
+    prev[0] = 0xffffffffu;
+    return;
+  }
+  const uint64_t pos = in.e_begin + umin64(k * CT, E) - 1;
+  uint64_t lo = 0, hi = in.V;
+  while (hi - lo > 1) {
+    const uint64_t mid = lo + (hi - lo) / 2;
+    if (in.offsets[mid] <= pos) lo = mid; else hi = mid;
+  }
+  prev[k] = (uint32_t)lo;
+}
+
 // L1 count: histogram of the level-1 digit over each count tile.  tcnt is
 // digit-major: tcnt[d * ntiles + k].
 template <class In, class Dig>
@@ -131,23 +160,43 @@ __global__ void __launch_bounds__(512) k_l1_count(In in, Dig dig, uint64_t E, ui
   for (int d = threadIdx.x; d < D; d += blockDim.x) tcnt[(uint64_t)d * ntiles + k] = s_hist[d];
 }
 
+// Level-1 output encoders.
+// OutFull: (src, dst) uint2 records.
+// OutCompact: one u32 per record = (dst_low << L) | src_low with dst_low the
+// b+c low destination bits and src_low the L low source bits; the src high
+// bits are recovered from the record's position: seg_hi[d][h] = first position
+// (in rec_out) of coarse bucket d whose source has src >> L >= h.
+struct OutFull {
+  static constexpr bool kCompact = false;
+  uint2* rec;
+};
+struct OutCompact {
+  static constexpr bool kCompact = true;
+  uint32_t* rec;
+  uint32_t low_mask;  // (1 << (b + c)) - 1
+  int L;              // source low bits kept in the record
+  uint32_t src_mask;  // (1 << L) - 1
+  uint32_t nh;        // number of src_high values; table rows have nh + 1 entries
+  uint64_t* seg_hi;   // [D][nh + 1], pre-filled with ~0
+  const uint32_t* prev_src;  // per count tile: source of the element before it (~0u: none)
+};
+
 // L1 place.  One CTA per count tile; its place tiles (4096 edges) are processed
 // in order with running global cursors per digit, and the next place tile's
 // neighbour IDs and offsets window are prefetched with cp.async while the
-// current one is ranked.  Writes records (src, dst) grouped by digit, each
-// group in stream order.
-// place_src[t] = owner of edge min(t*kPlaceTile, E-1) (global place index t).
-template <int kMode, class In, class Dig>
+// current one is ranked.  Writes records grouped by digit, each group in
+// stream order.  place_src[t] = owner of edge min(t*kPlaceTile, E-1).
+template <int kMode, class In, class Dig, class Out>
 __global__ void __launch_bounds__(kL1Warps * 32) k_l1_place(In in, Dig dig, uint64_t E, uint64_t CT, uint64_t ntiles,
                                                            int D, const uint64_t* __restrict__ tbase,
-                                                           const uint32_t* __restrict__ place_src,
-                                                           uint2* __restrict__ rec_out) {
+                                                           const uint32_t* __restrict__ place_src, Out out) {
   constexpr int W = kL1Warps, K = kL1Slots, T = W * 32, PT = kPlaceTile;
+  using StageT = typename std::conditional<Out::kCompact, uint32_t, uint2>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // input staging: CSR -> dst u32[2][PT] + offsets window u64[2][kWinCap]; records -> uint2[2][PT]
   constexpr size_t kInBytes = In::kRecords ? 2 * PT * 8 : 2 * PT * 4 + 2 * kWinCap * 8;
   unsigned char* s_in = smem_raw;
-  uint2* s_stage = reinterpret_cast<uint2*>(smem_raw + kInBytes);     // PT
+  StageT* s_stage = reinterpret_cast<StageT*>(smem_raw + kInBytes);   // PT
   uint64_t* s_gcur = reinterpret_cast<uint64_t*>(s_stage + PT);       // D
   uint32_t* s_mark = reinterpret_cast<uint32_t*>(s_gcur + D);         // PT (CSR only)
   uint32_t* s_cnt = s_mark + (In::kRecords ? 0 : PT);                 // W * D
@@ -156,7 +205,10 @@ __global__ void __launch_bounds__(kL1Warps * 32) k_l1_place(In in, Dig dig, uint
   uint32_t* s_dtot = s_dstart + D;                                    // D
   uint32_t* s_tmp = s_dtot + D;                                       // 40
   uint32_t* s_psrc = s_tmp + 40;                                      // CT/PT + 2 (CSR only)
+  uint32_t* s_bh = s_psrc + (CT / PT + 4);                            // D (compact)
+  uint16_t* s_sdig = reinterpret_cast<uint16_t*>(s_bh + (Out::kCompact ? D : 0));  // PT (compact)
   __shared__ uint32_t s_wmax[W];
+  __shared__ uint32_t s_last_src;
 
   const uint64_t k = blockIdx.x;
   const uint64_t tb = k * CT, te = umin64(E, tb + CT);
@@ -169,6 +221,15 @@ __global__ void __launch_bounds__(kL1Warps * 32) k_l1_place(In in, Dig dig, uint
   }
   if (kMode == kRankSafe)
     for (int i = threadIdx.x; i < W * D; i += T) s_scr[i] = 0;
+  uint32_t h_prev = 0xffffffffu;  // src_high of the element before the current place tile
+  if constexpr (Out::kCompact) {
+    uint32_t ps = 0xffffffffu;
+    if (k > 0) {
+      if constexpr (In::kRecords) ps = in.rec[tb - 1].x;
+      else ps = out.prev_src[k];
+    }
+    h_prev = (ps == 0xffffffffu) ? 0xffffffffu : (ps >> out.L);
+  }
   __syncthreads();
   const uint32_t lane = lane_id(), w = warp_id();
   uint32_t* cnt_w = s_cnt + w * D;
@@ -260,20 +321,52 @@ __global__ void __launch_bounds__(kL1Warps * 32) k_l1_place(In in, Dig dig, uint
         r_dst[s] = r.y;
       }
     }
+    if constexpr (Out::kCompact) {
+      // record the src_high boundaries that fall in this tile: h in (h_prev, h_last]
+#pragma unroll
+      for (int s = 0; s < K; ++s)
+        if (seg0 + s * 32 + lane == n - 1) s_last_src = r_src[s];
+      __syncthreads();
+      const uint32_t h_last = s_last_src >> out.L;
+      for (uint32_t h = (h_prev == 0xffffffffu) ? 0u : h_prev + 1; h <= h_last; ++h) {
+        for (int d = threadIdx.x; d < D; d += T) s_bh[d] = 0;
+        __syncthreads();
+        const uint64_t bsrc = (uint64_t)h << out.L;
+#pragma unroll
+        for (int s = 0; s < K; ++s) {
+          const uint32_t i = seg0 + s * 32 + lane;
+          if (i < n && (uint64_t)r_src[s] < bsrc) smem_inc(&s_bh[dig(r_dst[s])]);
+        }
+        __syncthreads();
+        for (int d = threadIdx.x; d < D; d += T) out.seg_hi[(uint64_t)d * (out.nh + 1) + h] = s_gcur[d] + s_bh[d];
+        __syncthreads();
+      }
+      h_prev = h_last;
+    }
     __syncthreads();
     warp_counts_to_bases<W>(s_cnt, D, s_dstart, s_dtot, s_tmp);
 #pragma unroll
     for (int s = 0; s < K; ++s) {
       const uint32_t i = seg0 + s * 32 + lane;
       const bool valid = i < n;
-      const uint32_t pos = warp_rank<kMode>(cnt_w, scr_w, valid ? dig(r_dst[s]) : 0u, valid);
-      if (valid) s_stage[pos] = make_uint2(r_src[s], r_dst[s]);
+      const uint32_t d = valid ? dig(r_dst[s]) : 0u;
+      const uint32_t pos = warp_rank<kMode>(cnt_w, scr_w, d, valid);
+      if (valid) {
+        if constexpr (Out::kCompact) {
+          s_stage[pos] = ((r_dst[s] & out.low_mask) << out.L) | (r_src[s] & out.src_mask);
+          s_sdig[pos] = (uint16_t)d;
+        } else {
+          s_stage[pos] = make_uint2(r_src[s], r_dst[s]);
+        }
+      }
     }
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < n; i += T) {
-      const uint2 r = s_stage[i];
-      const uint32_t d = dig(r.y);
-      rec_out[s_gcur[d] + (i - s_dstart[d])] = r;
+      const StageT r = s_stage[i];
+      uint32_t d;
+      if constexpr (Out::kCompact) d = s_sdig[i];
+      else d = dig(r.y);
+      out.rec[s_gcur[d] + (i - s_dstart[d])] = r;
     }
     if constexpr (!In::kRecords)
       for (int i = threadIdx.x; i < PT; i += T) s_mark[i] = 0;
@@ -299,6 +392,23 @@ __global__ void k_coarse_info(const uint64_t* __restrict__ tbase, uint64_t ntile
     const uint64_t sz = cstart[c + 1] - cstart[c];
     s_nch[c] = (uint32_t)((sz + kChunk - 1) / kChunk);
     if (fine_hist_b0) fine_hist_b0[c] = sz;
+  }
+  __syncthreads();
+  const uint32_t total = block_excl_scan_u32(s_nch, D1, s_tmp);
+  for (int c = threadIdx.x; c < D1; c += blockDim.x) chunk_first[c] = s_nch[c];
+  if (threadIdx.x == 0) chunk_first[D1] = total;
+}
+
+// Same for the compact path's 16K-record chunks.
+__global__ void k_coarse_info_c(const uint64_t* __restrict__ tbase, uint64_t ntiles, int D1, uint64_t E,
+                                uint64_t* __restrict__ cstart, uint32_t* __restrict__ chunk_first) {
+  extern __shared__ uint32_t s_nch[];
+  __shared__ uint32_t s_tmp[40];
+  for (int c = threadIdx.x; c <= D1; c += blockDim.x) cstart[c] = (c < D1) ? tbase[(uint64_t)c * ntiles] : E;
+  __syncthreads();
+  for (int c = threadIdx.x; c < D1; c += blockDim.x) {
+    const uint64_t sz = cstart[c + 1] - cstart[c];
+    s_nch[c] = (uint32_t)((sz + kChunkC - 1) / kChunkC);
   }
   __syncthreads();
   const uint32_t total = block_excl_scan_u32(s_nch, D1, s_tmp);
@@ -412,41 +522,57 @@ struct FineCtx {
   uint64_t V;
 };
 
-// Final work item: a group of consecutive fine buckets [f0, f1) of coarse
-// bucket c holding n <= kFCap records (kind 0), or one kFCap batch of a big
-// fine bucket f0 (kind 1).  The item's records are gathered by walking chunks
-// from g_start (absolute chunk id), taking the slice of fine digits [f0, f1) of
-// each chunk, after skipping `skip` records, until n records are collected.
-struct FItem {
-  uint32_t c;
-  uint32_t f0, f1;
-  uint32_t kind;
-  uint32_t n;
-  uint32_t g_start;
-  uint32_t skip;
-  uint32_t pad;
-  uint64_t base;  // kind 0: CSC position of the group's first record
+// ---- final stage: per coarse-bucket fine ranges, one CTA per range --------
+// A range = fine buckets [f0, f1) of coarse bucket c.  The CTA walks it as a
+// pipeline of units, gathering unit k+1 with cp.async while ranking unit k:
+//   kind 0  group of consecutive small fine buckets (<= kFCap records,
+//           <= kFMaxLocal local vertices): one pass, contiguous CSC slice;
+//   kind 1  count batch of a big fine bucket (per-vertex counts);
+//   kind 2  place batch of a big fine bucket (runs at per-vertex cursors).
+// Walking the fine buckets of a coarse bucket in order keeps the chunk segment
+// tables in L1 and a big bucket's second (place) read in L2.
+struct FRange {
+  uint32_t c, f0, f1, prio;
 };
 
-// Issue cp.async copies of item `it`'s records into dst.  All threads; uses the
-// segment scratch s_st / s_pos (kSegCap entries) block by block.
-__device__ __forceinline__ void item_gather(const FineCtx& x, const FItem& it, uint64_t* s_st, uint32_t* s_pos,
-                                            uint32_t* s_tmp, uint2* dst) {
-  const uint32_t g_end = x.chunk_first[it.c + 1];
-  const uint64_t cs = x.cstart[it.c], ce = x.cstart[it.c + 1];
-  const uint32_t g_first = x.chunk_first[it.c];
-  const uint32_t lane = lane_id(), w = warp_id(), nw = blockDim.x >> 5;
-  uint32_t got = 0;       // records collected (uniform)
-  uint32_t skip = it.skip;
-  for (uint32_t gb = it.g_start; gb < g_end && got < it.n; gb += kSegCap) {
+struct FUnit {
+  uint32_t kind;
+  uint32_t f0, f1;
+  uint32_t n;
+  uint32_t g, skip;  // gather start: absolute chunk id, records to skip there
+  uint32_t last;     // kind 1: last count batch of its bucket
+  uint32_t first;    // kind 1: first count batch of its bucket
+  uint64_t base;     // CSC position of f0's first record
+};
+
+// Gather `n` records of fine digits [f0, f1) of coarse bucket c, starting at
+// chunk g (skipping `skip` records of that chunk's slice), into dst with
+// cp.async.  All threads.  Returns the position after the last record
+// (g_out, skip_out).
+struct CoarseInfo {
+  uint32_t g_first, g_end;  // chunk ids of the coarse bucket
+  uint64_t cs, ce;          // record range of the coarse bucket
+};
+
+__device__ __forceinline__ void gather_unit(const FineCtx& x, const CoarseInfo& ci, uint32_t f0, uint32_t f1,
+                                            uint32_t n, uint32_t g, uint32_t skip, uint2* dst, uint64_t* s_st,
+                                            uint32_t* s_pos, uint32_t* s_seg, uint32_t* s_tmp, uint32_t& g_out,
+                                            uint32_t& skip_out) {
+  const uint32_t g_first = ci.g_first, g_end = ci.g_end;
+  const uint64_t cs = ci.cs, ce = ci.ce;
+  uint32_t got = 0;
+  g_out = g;
+  skip_out = skip;
+  uint32_t gb = g;
+  while (gb < g_end && got < n) {
     const int nch = (int)min((uint32_t)kSegCap, g_end - gb);
     for (int j = threadIdx.x; j < nch; j += blockDim.x) {
       const uint64_t cpos = cs + (uint64_t)(gb + j - g_first) * kChunk;
       uint32_t a, e;
       if (x.segoff) {
         const uint16_t* so = x.segoff + (uint64_t)(gb + j) * (x.Db + 1);
-        a = so[it.f0];
-        e = so[it.f1];
+        a = so[f0];
+        e = so[f1];
       } else {
         a = 0;
         e = (uint32_t)umin64(kChunk, ce - cpos);
@@ -458,31 +584,64 @@ __device__ __forceinline__ void item_gather(const FineCtx& x, const FItem& it, u
     const uint32_t tot = block_excl_scan_u32(s_pos, nch, s_tmp);
     if (threadIdx.x == 0) s_pos[nch] = tot;
     __syncthreads();
-    // this block's records [skip, tot) map to item positions starting at `got`
-    const uint32_t lo = skip, hi = min(tot, skip + (it.n - got));
-    for (int j = w; j < nch; j += nw) {
-      const uint32_t a = max(s_pos[j], lo), e = min(s_pos[j + 1], hi);
-      if (a >= e) continue;
-      const uint64_t src = s_st[j] + (a - s_pos[j]);
-      uint2* d = dst + got + (a - lo);
-      for (uint32_t q = lane; q < e - a; q += 32) cp_async8(d + q, x.rec + src + q);
+    const uint32_t lo = skip, want = n - got;
+    const uint32_t hi = (tot > lo) ? min(tot, lo + want) : lo;
+    // thread-per-record: segment of record i = (#segment starts <= i) - 1, from
+    // a per-position count of segment starts and a block prefix sum
+    if (hi > lo) {
+      const uint32_t m = hi - lo;
+      for (uint32_t p = threadIdx.x; p <= m; p += blockDim.x) s_seg[p] = 0;
+      __syncthreads();
+      uint32_t below = 0;  // segment starts at or before lo (this thread's share)
+      for (int j = threadIdx.x; j < nch; j += blockDim.x) {
+        const uint32_t a = s_pos[j];
+        if (a <= lo) ++below;
+        else if (a < hi) atomicAdd(&s_seg[a - lo], 1u);
+      }
+      below = __reduce_add_sync(kFull, below);
+      if (lane_id() == 0) atomicAdd(&s_tmp[36], below);
+      __syncthreads();
+      const uint32_t base = s_tmp[36];
+      block_excl_scan_u32(s_seg, (int)m + 1, s_tmp);  // s_seg[m] must be 0 (zeroed below)
+      for (uint32_t p = threadIdx.x; p < m; p += blockDim.x) {
+        const uint32_t j = base - 1 + s_seg[p + 1];  // inclusive count at p
+        const uint32_t i = lo + p;
+        cp_async8(dst + got + p, x.rec + s_st[j] + (i - s_pos[j]));
+      }
+      if (threadIdx.x == 0) s_tmp[36] = 0;
     }
-    got += (hi > lo) ? hi - lo : 0;
+    if (hi > lo) {
+      got += hi - lo;
+      if (got >= n) {
+        // position after the last record: chunk containing index hi-1 (+1 past it)
+        int lo_j = 0, hi_j = nch - 1;  // last j with s_pos[j] < hi
+        while (lo_j < hi_j) {
+          const int mid = (lo_j + hi_j + 1) >> 1;
+          if (s_pos[mid] < hi) lo_j = mid; else hi_j = mid - 1;
+        }
+        g_out = gb + lo_j;
+        skip_out = hi - s_pos[lo_j];
+        __syncthreads();
+        return;
+      }
+    }
     skip = (tot > skip) ? 0 : skip - tot;
+    gb += nch;
     __syncthreads();
   }
+  g_out = gb;
+  skip_out = skip;
 }
 
-// Persistent final stage over planned items, the next item's records gathered
-// with cp.async while the current one is ranked.  kCount: count records per
-// local vertex of big-batch items into cnt_tab[item][Dc] (no output).
-// Big-batch item i uses cursor row i of cur_tab.
-template <int kMode, bool kCount>
-__global__ void __launch_bounds__(kFWarps * 32) k_final(FineCtx x, const FItem* __restrict__ items,
-                                                       const uint32_t* __restrict__ n_items_ptr,
-                                                       uint32_t* __restrict__ cnt_tab,
-                                                       const uint64_t* __restrict__ cur_tab,
-                                                       uint64_t* __restrict__ t_offsets, uint32_t* __restrict__ t_edges) {
+template <int kMode>
+__global__ void __launch_bounds__(kFWarps * 32) k_final(FineCtx x, const FRange* __restrict__ ranges,
+                                                       const uint32_t* __restrict__ n_ranges_ptr,
+                                                       unsigned int* __restrict__ range_ctr,
+                                                       const uint32_t* __restrict__ fine_size,
+                                                       const uint64_t* __restrict__ fine_base,
+                                                       uint64_t* __restrict__ t_offsets, uint32_t* __restrict__ t_edges,
+                                                       unsigned int* __restrict__ err_overflow,
+                                                       unsigned long long* __restrict__ prof) {
   constexpr int W = kFWarps, K = kFSlots, T = W * 32, CAP = kFCap;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint2* s_buf = reinterpret_cast<uint2*>(smem_raw);                       // 2 * CAP (staging in place)
@@ -493,250 +652,770 @@ __global__ void __launch_bounds__(kFWarps * 32) k_final(FineCtx x, const FItem* 
   uint32_t* s_dstart = s_scr + (kMode == kRankSafe ? W * kFMaxLocal : 0);  // kFMaxLocal
   uint32_t* s_dtot = s_dstart + kFMaxLocal;                                // kFMaxLocal
   uint32_t* s_tmp = s_dtot + kFMaxLocal;                                   // 40
-  uint64_t* s_cur = reinterpret_cast<uint64_t*>(s_tmp + 40);               // kFMaxLocal
-  __shared__ FItem s_item[2];
+  uint64_t* s_cur = reinterpret_cast<uint64_t*>(s_tmp + 40);               // kFMaxLocal (big cursors)
+  uint32_t* s_bcnt = reinterpret_cast<uint32_t*>(s_cur + kFMaxLocal);      // kFMaxLocal (big counts)
+  __shared__ uint32_t s_range;
 
-  const uint32_t n_items = *n_items_ptr;
+  const uint32_t n_ranges = *n_ranges_ptr;
   const uint32_t lane = lane_id(), w = warp_id();
   const int Dc = 1 << x.bits_c;
+  const uint32_t maxf = (uint32_t)max(1, kFMaxLocal >> x.bits_c);
   if (kMode == kRankSafe)
     for (int i = threadIdx.x; i < W * kFMaxLocal; i += T) s_scr[i] = 0;
 
-  auto prepare = [&](uint32_t idx, int b) {
-    if (threadIdx.x == 0) s_item[b] = items[idx];
+  // ---- unit generator (uniform across threads); range sizes/bases live in smem
+  uint32_t* s_rsz = s_bcnt + kFMaxLocal;                              // kMaxRange
+  uint64_t* s_rbase = reinterpret_cast<uint64_t*>(s_rsz + kMaxRange);  // kMaxRange
+  uint32_t* s_seg = reinterpret_cast<uint32_t*>(s_rbase + kMaxRange);   // kFCap + 4 (gather scratch)
+  if (threadIdx.x == 0) s_tmp[36] = 0;
+  struct Gen {
+    uint32_t c, f, f0, f1;     // current range (f relative to the coarse bucket)
+    uint32_t big_f, big_left;  // big bucket in progress
+    uint32_t phase;            // 1 = counting, 2 = placing
+    uint32_t g, skip;          // gather position inside the big bucket
+    uint64_t big_base;
+    uint32_t big_size;
+    bool live;
+    CoarseInfo ci;
+  } gen;
+  gen.live = false;
+  gen.big_left = 0;
+  gen.phase = 0;
+  auto fetch_range = [&]() -> bool {
+    __syncthreads();  // previous range's smem arrays are no longer read
+    if (threadIdx.x == 0) s_range = atomicAdd(range_ctr, 1u);
     __syncthreads();
-    const FItem it = s_item[b];
-    item_gather(x, it, s_st, s_pos, s_tmp, s_buf + b * CAP);
+    const uint32_t r = s_range;
+    if (r >= n_ranges) return false;
+    const FRange R = ranges[r];
+    gen.c = R.c;
+    gen.f0 = R.f0;
+    gen.f = R.f0;
+    gen.f1 = R.f1;
+    gen.live = true;
+    gen.ci.g_first = x.chunk_first[R.c];
+    gen.ci.g_end = x.chunk_first[R.c + 1];
+    gen.ci.cs = x.cstart[R.c];
+    gen.ci.ce = x.cstart[R.c + 1];
+    const uint64_t fb = (uint64_t)R.c * x.Db + R.f0;
+    for (uint32_t i = threadIdx.x; i < R.f1 - R.f0; i += blockDim.x) {
+      s_rsz[i] = fine_size[fb + i];
+      s_rbase[i] = fine_base[fb + i];
+    }
+    __syncthreads();
+    return true;
+  };
+  // next unit; returns false when all work is exhausted
+  auto next_unit = [&](FUnit& u) -> bool {
+    while (true) {
+      if (gen.big_left) {
+        u.kind = gen.phase;
+        u.f0 = gen.big_f;
+        u.f1 = gen.big_f + 1;
+        u.n = min((uint32_t)CAP, gen.big_left);
+        u.g = gen.g;
+        u.skip = gen.skip;
+        u.base = gen.big_base;
+        gen.big_left -= u.n;
+        u.last = (gen.big_left == 0);
+        u.first = (gen.phase == 1 && gen.big_left + u.n == gen.big_size);
+        if (gen.big_left == 0 && gen.phase == 1) {  // counting done: place pass next
+          gen.phase = 2;
+          gen.big_left = gen.big_size;
+          gen.g = gen.ci.g_first;
+          gen.skip = 0;
+          u.last = 1;
+          return true;
+        }
+        if (gen.big_left == 0) gen.phase = 0;
+        return true;
+      }
+      if (!gen.live || gen.f >= gen.f1) {
+        if (!fetch_range()) return false;
+        continue;
+      }
+      const uint32_t sz = s_rsz[gen.f - gen.f0];
+      if (sz == 0) { ++gen.f; continue; }
+      if (sz > (uint32_t)CAP) {
+        gen.big_f = gen.f;
+        gen.big_size = sz;
+        gen.big_left = sz;
+        gen.big_base = s_rbase[gen.f - gen.f0];
+        gen.phase = 1;
+        gen.g = gen.ci.g_first;
+        gen.skip = 0;
+        ++gen.f;
+        continue;
+      }
+      uint32_t total = sz, e = gen.f + 1;
+      while (e < gen.f1 && e - gen.f < maxf) {
+        const uint32_t z = s_rsz[e - gen.f0];
+        if (z > (uint32_t)CAP || total + z > (uint32_t)CAP) break;
+        total += z;
+        ++e;
+      }
+      u.kind = 0;
+      u.f0 = gen.f;
+      u.f1 = e;
+      u.n = total;
+      u.g = gen.ci.g_first;
+      u.skip = 0;
+      u.last = 0;
+      u.first = 0;
+      u.base = s_rbase[gen.f - gen.f0];
+      gen.f = e;
+      return true;
+    }
+  };
+  auto issue = [&](const FUnit& u, int b) {
+    uint32_t go, so;
+    gather_unit(x, gen.ci, u.f0, u.f1, u.n, u.g, u.skip, s_buf + b * CAP, s_st, s_pos, s_seg, s_tmp, go, so);
+    if (u.kind != 0 && !(u.kind == 1 && u.last)) {  // continue the big bucket walk
+      gen.g = go;
+      gen.skip = so;
+    }
     cp_commit();
   };
 
-  uint32_t idx = blockIdx.x;
-  if (idx < n_items) prepare(idx, 0);
-  for (int itn = 0; idx < n_items; ++itn, idx += gridDim.x) {
-    const int b = itn & 1;
-    const uint32_t nidx = idx + gridDim.x;
-    if (nidx < n_items) {
-      prepare(nidx, b ^ 1);
+  FUnit u0, u1;
+  uint32_t c0 = 0, c1 = 0, cur_c = 0;
+  __shared__ unsigned long long pacc[10];  // profiling accumulators (thread 0)
+  __shared__ long long tprev;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 10; ++i) pacc[i] = 0;
+    tprev = clock64();
+  }
+  auto ptick = [&](int ph) {
+    if (prof && threadIdx.x == 0) {
+      const long long tn = clock64();
+      pacc[ph] += (unsigned long long)(tn - tprev);
+      tprev = tn;
+    }
+  };
+  if (!next_unit(u0)) return;
+  c0 = gen.c;
+  issue(u0, 0);
+  for (int it = 0;; ++it) {
+    const int b = it & 1;
+    ptick(9);
+    const bool more = next_unit(u1);
+    c1 = gen.c;
+    ptick(0);
+    if (more) {
+      issue(u1, b ^ 1);
+      ptick(1);
       cp_wait<1>();
     } else {
       cp_wait<0>();
     }
-    const FItem it = s_item[b];
-    const uint32_t n = it.n;
-    const uint32_t f0 = it.f0;
-    const uint32_t nloc = (it.f1 - it.f0) << x.bits_c;
+    // ---- process u0 (coarse bucket c0) from buffer b
+    cur_c = c0;
+    const FUnit u = u0;
+    const uint32_t n = u.n, f0 = u.f0;
+    const uint32_t nloc = (u.f1 - u.f0) << x.bits_c;
+    uint32_t* cnt_w = s_cnt + w * nloc;
+    uint32_t* scr_w = s_scr + (kMode == kRankSafe ? w * nloc : 0);
     for (int i = threadIdx.x; i < W * kFMaxLocal; i += T) s_cnt[i] = 0;
+    if (u.kind == 1 && u.first)
+      for (int v = threadIdx.x; v < Dc; v += T) s_bcnt[v] = 0;  // first count batch of a big bucket
     __syncthreads();
+    ptick(2);
+    if (prof && threadIdx.x == 0) pacc[7 + (u.kind == 0 ? 0 : 1)] += 1;
     uint2* buf = s_buf + b * CAP;
-    const uint32_t shift_f = x.bits_c;
-    const uint32_t mask_f = (uint32_t)x.Db - 1;
+    const uint32_t shift_f = x.bits_c, mask_f = (uint32_t)x.Db - 1;
     auto local_of = [&](uint32_t dst) -> uint32_t {
       return ((((dst >> shift_f) & mask_f) - f0) << shift_f) | (dst & x.mask_c);
     };
-    // per-warp counter rows use stride nloc (the layout warp_counts_to_bases expects)
-    uint32_t* cnt_w = s_cnt + w * nloc;
-    uint32_t* scr_w = s_scr + (kMode == kRankSafe ? w * nloc : 0);
     const uint32_t seg0 = w * (K * 32);
+    if (u.kind == 1) {
 #pragma unroll
-    for (int s = 0; s < K; ++s) {
-      const uint32_t i = seg0 + s * 32 + lane;
-      if (i < n) smem_inc(&cnt_w[local_of(buf[i].y)]);
-    }
-    __syncthreads();
-    if constexpr (kCount) {
-      for (int v = threadIdx.x; v < Dc; v += T) {
-        uint32_t sum = 0;
-        for (int ww = 0; ww < W; ++ww) sum += s_cnt[ww * nloc + v];
-        cnt_tab[(uint64_t)idx * Dc + v] = sum;
+      for (int s = 0; s < K; ++s) {
+        const uint32_t i = seg0 + s * 32 + lane;
+        if (i < n) smem_inc(&s_bcnt[buf[i].y & x.mask_c]);
       }
       __syncthreads();
-      continue;
-    }
-    warp_counts_to_bases<W>(s_cnt, (int)nloc, s_dstart, s_dtot, s_tmp);
-    if (it.kind == 0) {
-      const uint64_t v0 = ((uint64_t)it.c * x.Db + it.f0) << x.bits_c;
-      for (uint32_t v = threadIdx.x; v < nloc; v += T)
-        if (v0 + v < x.V) t_offsets[v0 + v] = it.base + s_dstart[v];
+      if (u.last) {  // CSC offsets of the big bucket's vertices and place cursors
+        if (threadIdx.x == 0) {
+          uint64_t run = u.base;
+          for (int v = 0; v < Dc; ++v) {
+            s_cur[v] = run;
+            run += s_bcnt[v];
+          }
+        }
+        __syncthreads();
+        const uint64_t v0 = ((uint64_t)cur_c * x.Db + u.f0) << x.bits_c;
+        for (int v = threadIdx.x; v < Dc; v += T)
+          if (v0 + v < x.V) t_offsets[v0 + v] = s_cur[v];
+        __syncthreads();
+      }
     } else {
-      for (int v = threadIdx.x; v < Dc; v += T) s_cur[v] = cur_tab[(uint64_t)idx * Dc + v];
-    }
-    uint2 rr[K];
-    uint32_t pp[K];
 #pragma unroll
-    for (int s = 0; s < K; ++s) {
-      const uint32_t i = seg0 + s * 32 + lane;
-      const bool valid = i < n;
-      const uint2 r = valid ? buf[i] : make_uint2(0, 0);
-      const uint32_t lv = valid ? local_of(r.y) : 0u;
-      pp[s] = warp_rank<kMode>(cnt_w, scr_w, lv, valid);
-      rr[s] = make_uint2(r.x, lv);
-    }
-    __syncthreads();  // all records are in registers: stage (src, local vertex) in place
+      for (int s = 0; s < K; ++s) {
+        const uint32_t i = seg0 + s * 32 + lane;
+        if (i < n) smem_inc(&cnt_w[local_of(buf[i].y)]);
+      }
+      __syncthreads();
+      ptick(3);
+      warp_counts_to_bases<W>(s_cnt, (int)nloc, s_dstart, s_dtot, s_tmp);
+      ptick(4);
+      if (u.kind == 0) {
+        const uint64_t v0 = ((uint64_t)cur_c * x.Db + u.f0) << x.bits_c;
+        for (uint32_t v = threadIdx.x; v < nloc; v += T)
+          if (v0 + v < x.V) t_offsets[v0 + v] = u.base + s_dstart[v];
+      }
+      uint2 rr[K];
+      uint32_t pp[K];
 #pragma unroll
-    for (int s = 0; s < K; ++s)
-      if (seg0 + s * 32 + lane < n) buf[pp[s]] = rr[s];
-    __syncthreads();
-    if (it.kind == 0) {
-      for (uint32_t i = threadIdx.x; i < n; i += T) t_edges[it.base + i] = buf[i].x;
-    } else {
-      for (uint32_t i = threadIdx.x; i < n; i += T) {
-        const uint2 r = buf[i];
-        t_edges[s_cur[r.y] + (i - s_dstart[r.y])] = r.x;
+      for (int s = 0; s < K; ++s) {
+        const uint32_t i = seg0 + s * 32 + lane;
+        const bool valid = i < n;
+        const uint2 r = valid ? buf[i] : make_uint2(0, 0);
+        const uint32_t lv = valid ? local_of(r.y) : 0u;
+        pp[s] = warp_rank<kMode>(cnt_w, scr_w, lv, valid);
+        rr[s] = make_uint2(r.x, lv);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int s = 0; s < K; ++s)
+        if (seg0 + s * 32 + lane < n) buf[pp[s]] = rr[s];
+      __syncthreads();
+      ptick(5);
+      if (u.kind == 0) {
+        for (uint32_t i = threadIdx.x; i < n; i += T) t_edges[u.base + i] = buf[i].x;
+      } else {
+        for (uint32_t i = threadIdx.x; i < n; i += T) {
+          const uint2 r = buf[i];
+          t_edges[s_cur[r.y] + (i - s_dstart[r.y])] = r.x;
+        }
+        __syncthreads();
+        for (int v = threadIdx.x; v < Dc; v += T) s_cur[v] += s_dtot[v];
       }
     }
     __syncthreads();
+    ptick(6);
+    if (!more) break;
+    u0 = u1;
+    c0 = c1;
   }
+  if (prof && threadIdx.x == 0)
+    for (int i = 0; i < 10; ++i) atomicAdd(&prof[i], pacc[i]);
+  (void)err_overflow;
 }
 
-// Plan the final stage: one CTA per coarse bucket.  Fine-bucket sizes from the
-// chunk segment tables, CSC bases, greedy groups of consecutive fine buckets
-// (<= kFCap records, <= kFMaxLocal local vertices) and big fine buckets split
-// into kFCap batches (with their starting chunk / skip); t_offsets of empty
-// fine buckets.  big_buckets[bi] = {fid, first big item, batches}.
-__global__ void k_f_plan(FineCtx x, FItem* __restrict__ items_s, uint32_t* __restrict__ n_s,
-                         FItem* __restrict__ items_b, uint32_t* __restrict__ n_b,
-                         uint32_t* __restrict__ big_buckets, uint32_t* __restrict__ n_big,
-                         uint64_t* __restrict__ big_base, uint64_t* __restrict__ t_offsets) {
+// Plan the final stage: one CTA per coarse bucket.  Fine-bucket sizes (sum of
+// the chunk segment tables) and CSC bases; t_offsets of empty fine buckets;
+// fine ranges of ~`target` records (a range never splits a fine bucket).
+__global__ void k_f_plan(FineCtx x, uint32_t target, uint32_t* __restrict__ fine_size, uint64_t* __restrict__ fine_base,
+                         FRange* __restrict__ ranges, uint32_t* __restrict__ n_ranges, uint64_t* __restrict__ t_offsets,
+                         unsigned int* __restrict__ err_overflow) {
   extern __shared__ uint32_t s_dyn[];
-  uint32_t* s_sz = s_dyn;              // Db
-  uint32_t* s_base = s_sz + x.Db;      // Db
-  uint32_t* s_bigf = s_base + x.Db;    // Db
-  uint32_t* s_len = s_bigf + x.Db;     // blockDim
+  uint32_t* s_sz = s_dyn;          // Db
+  uint32_t* s_base = s_sz + x.Db;  // Db
   __shared__ uint32_t s_tmp[40];
-  __shared__ uint32_t s_nbig;
   const uint32_t c = blockIdx.x;
   const int Db = x.Db, Dc = 1 << x.bits_c;
   const uint32_t g0 = x.chunk_first[c], g1 = x.chunk_first[c + 1];
   const uint64_t cs = x.cstart[c];
   for (int f = threadIdx.x; f < Db; f += blockDim.x) {
-    uint32_t sum = 0;
+    uint64_t sum = 0;
     if (x.segoff) {
       for (uint32_t g = g0; g < g1; ++g) {
         const uint16_t* so = x.segoff + (uint64_t)g * (Db + 1);
         sum += (uint32_t)so[f + 1] - so[f];
       }
     } else {
-      sum = (uint32_t)(x.cstart[c + 1] - cs);
+      sum = x.cstart[c + 1] - cs;
     }
-    s_sz[f] = sum;
-    s_base[f] = sum;
+    if (sum >= (1ull << 32)) atomicExch(err_overflow, 1u);
+    s_sz[f] = (uint32_t)sum;
+    s_base[f] = (uint32_t)sum;
   }
   __syncthreads();
-  block_excl_scan_u32(s_base, Db, s_tmp);
+  // bases relative to cs fit 32 bits unless the coarse bucket holds >= 2^32 records
+  const uint64_t nc = x.cstart[c + 1] - cs;
+  if (nc >= (1ull << 32)) {
+    if (threadIdx.x == 0) {
+      uint64_t run = cs;
+      for (int f = 0; f < Db; ++f) {
+        fine_base[(uint64_t)c * Db + f] = run;
+        run += s_sz[f];
+      }
+    }
+    __syncthreads();
+  } else {
+    block_excl_scan_u32(s_base, Db, s_tmp);
+    for (int f = threadIdx.x; f < Db; f += blockDim.x) fine_base[(uint64_t)c * Db + f] = cs + s_base[f];
+  }
+  for (int f = threadIdx.x; f < Db; f += blockDim.x) fine_size[(uint64_t)c * Db + f] = s_sz[f];
+  __syncthreads();
   for (int f = 0; f < Db; ++f) {  // t_offsets of empty fine buckets
     if (s_sz[f]) continue;
     const uint64_t v0 = ((uint64_t)c * Db + f) << x.bits_c;
+    const uint64_t val = fine_base[(uint64_t)c * Db + f];
     for (int v = threadIdx.x; v < Dc; v += blockDim.x)
-      if (v0 + v < x.V) t_offsets[v0 + v] = cs + s_base[f];
+      if (v0 + v < x.V) t_offsets[v0 + v] = val;
   }
-  if (threadIdx.x == 0) {
-    const uint32_t maxf = (uint32_t)max(1, kFMaxLocal >> x.bits_c);
-    uint32_t nbig = 0;
-    int f = 0;
-    while (f < Db) {
-      if (s_sz[f] == 0) { ++f; continue; }
-      if (s_sz[f] > (uint32_t)kFCap) { s_bigf[nbig++] = f; ++f; continue; }
-      uint32_t total = 0;
-      int e = f;
-      while (e < Db && (uint32_t)(e - f) < maxf && s_sz[e] <= (uint32_t)kFCap && total + s_sz[e] <= (uint32_t)kFCap) {
-        total += s_sz[e];
-        ++e;
-      }
-      FItem it{};
-      it.c = c; it.f0 = f; it.f1 = e; it.kind = 0; it.n = total;
-      it.g_start = g0; it.skip = 0; it.base = cs + s_base[f];
-      items_s[atomicAdd(n_s, 1u)] = it;
-      f = e;
-    }
-    s_nbig = nbig;
-  }
-  __syncthreads();
-  const uint32_t nbig = s_nbig;
-  for (uint32_t q = 0; q < nbig; ++q) {
-    const uint32_t f = s_bigf[q];
-    const uint32_t nb = (s_sz[f] + kFCap - 1) / kFCap;
-    __shared__ uint32_t s_i0;
-    if (threadIdx.x == 0) {
-      const uint32_t bi = atomicAdd(n_big, 1u);
-      const uint32_t i0 = atomicAdd(n_b, nb);
-      big_buckets[3 * bi + 0] = c * Db + f;
-      big_buckets[3 * bi + 1] = i0;
-      big_buckets[3 * bi + 2] = nb;
-      big_base[bi] = cs + s_base[f];
-      s_i0 = i0;
-    }
-    __syncthreads();
-    const uint32_t i0 = s_i0;
-    // batch k starts at record k*kFCap of the bucket's stream: locate its chunk
-    uint32_t run = 0;
-    for (uint32_t gb = g0; gb < g1; gb += blockDim.x) {
-      const uint32_t g = gb + threadIdx.x;
-      uint32_t len = 0;
-      if (g < g1) {
-        if (x.segoff) {
-          const uint16_t* so = x.segoff + (uint64_t)g * (Db + 1);
-          len = (uint32_t)so[f + 1] - so[f];
-        } else {
-          len = (uint32_t)umin64(kChunk, x.cstart[c + 1] - (cs + (uint64_t)(g - g0) * kChunk));
-        }
-      }
-      s_len[threadIdx.x] = len;
-      __syncthreads();
-      const uint32_t tot = block_excl_scan_u32(s_len, blockDim.x, s_tmp);
-      if (g < g1 && len) {
-        const uint32_t a = run + s_len[threadIdx.x], e = a + len;
-        // batches whose first record lies in [a, e)
-        for (uint32_t k = (a + kFCap - 1) / kFCap; k * kFCap < e && k < nb; ++k) {
-          FItem it{};
-          it.c = c; it.f0 = f; it.f1 = f + 1; it.kind = 1;
-          it.n = min((uint32_t)kFCap, s_sz[f] - k * kFCap);
-          it.g_start = g; it.skip = k * kFCap - a; it.base = cs + s_base[f];
-          items_b[i0 + k] = it;
-        }
-      }
-      run += tot;
-      __syncthreads();
+  if (threadIdx.x != 0 || nc == 0) return;
+  uint64_t acc = 0;
+  uint32_t f0 = 0;
+  for (uint32_t f = 0; f < (uint32_t)Db; ++f) {
+    acc += s_sz[f];
+    if (acc >= target || f + 1 == (uint32_t)Db || f + 1 - f0 >= (uint32_t)kMaxRange) {
+      FRange r;
+      r.c = c;
+      r.f0 = f0;
+      r.f1 = f + 1;
+      r.prio = 0;
+      ranges[atomicAdd(n_ranges, 1u)] = r;
+      f0 = f + 1;
+      acc = 0;
     }
   }
 }
 
-// Big fine buckets: CSC offsets of their vertices and the per-batch cursors.
-__global__ void k_big_scan(FineCtx x, const uint32_t* __restrict__ big_buckets, const uint32_t* __restrict__ n_big,
-                           const uint64_t* __restrict__ big_base, const uint32_t* __restrict__ cnt_tab,
-                           uint64_t* __restrict__ cur_tab, uint64_t* __restrict__ t_offsets,
-                           unsigned int* __restrict__ err_overflow) {
+// ===================== compact (4-byte record) levels 2 and 3 =====================
+// R1 (level-1 output): (dst_low << L) | src_low, src_high from seg_hi (see OutCompact).
+// R2 (level-2 output): (d << nb) | src, d = the c low destination bits.
+
+struct DecodeC {
+  int L;              // source low bits in R1
+  uint32_t src_mask;  // (1 << L) - 1
+  uint32_t nh;        // src_high values; seg_hi rows have nh + 1 entries
+  const uint64_t* seg_hi;
+  int bits_c;         // low destination digit bits
+  int nb;             // source bits in R2
+};
+
+// Level 2, compact: stable sort of each 16K-record chunk by the middle digit,
+// re-encoding R1 -> R2 (source high bits from the chunk's boundary list).
+template <int kMode>
+__global__ void __launch_bounds__(kB1cWarps * 32) k_b1c(const uint32_t* __restrict__ rin, uint32_t* __restrict__ rout,
+                                                       const uint64_t* __restrict__ cstart,
+                                                       const uint32_t* __restrict__ chunk_first,
+                                                       const uint32_t* __restrict__ chunk_bucket, int D1, DecodeC dc,
+                                                       int Db, uint16_t* __restrict__ segoff) {
+  constexpr int W = kB1cWarps, K = kB1cSlots, T = W * 32, CH = kChunkC;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem_raw);  // 2 * CH
+  uint32_t* s_cnt = s_buf + 2 * CH;                         // W * Db
+  uint32_t* s_scr = s_cnt + W * Db;
+  uint32_t* s_dstart = s_scr + (kMode == kRankSafe ? W * Db : 0);
+  uint32_t* s_dtot = s_dstart + Db;
+  uint32_t* s_tmp = s_dtot + Db;                                        // 40
+  uint64_t* s_bnd = reinterpret_cast<uint64_t*>(s_tmp + 40);            // kMaxBnd
+  __shared__ uint32_t s_h0, s_nbnd;
+  const uint32_t nchunks = chunk_first[D1];
+  const uint32_t lane = lane_id(), w = warp_id();
+  uint32_t* cnt_w = s_cnt + w * Db;
+  uint32_t* scr_w = s_scr + (kMode == kRankSafe ? w * Db : 0);
+  const uint32_t seg0 = w * (K * 32);
+  const uint32_t shift_f = dc.L + dc.bits_c, mask_f = (uint32_t)Db - 1;
+  const uint32_t mask_c = (1u << dc.bits_c) - 1;
+  if (kMode == kRankSafe)
+    for (int i = threadIdx.x; i < W * Db; i += T) s_scr[i] = 0;
+
+  auto chunk_range = [&](uint32_t g, uint32_t& c, uint64_t& start, uint32_t& n) {
+    c = chunk_bucket[g];
+    start = cstart[c] + (uint64_t)(g - chunk_first[c]) * CH;
+    n = (uint32_t)umin64(CH, cstart[c + 1] - start);
+  };
+  auto issue = [&](uint32_t g, int b) {
+    uint32_t c;
+    uint64_t st;
+    uint32_t n;
+    chunk_range(g, c, st, n);
+    uint32_t* dst = s_buf + b * CH;
+    for (uint32_t i = threadIdx.x; i < n; i += T) cp_async4(dst + i, rin + st + i);
+    cp_commit();
+  };
+
+  uint32_t g = blockIdx.x;
+  if (g < nchunks) issue(g, 0);
+  for (int it = 0; g < nchunks; ++it, g += gridDim.x) {
+    const int b = it & 1;
+    const uint32_t gn = g + gridDim.x;
+    if (gn < nchunks) {
+      issue(gn, b ^ 1);
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    uint32_t c;
+    uint64_t start;
+    uint32_t n;
+    chunk_range(g, c, start, n);
+    for (int i = threadIdx.x; i < W * Db; i += T) s_cnt[i] = 0;
+    // source-high boundaries covering this chunk (all threads, one round trip):
+    // h0 = #{h >= 1 : row[h] <= start}; boundaries inside (start, start+n)
+    if (threadIdx.x == 0) {
+      s_h0 = 0;
+      s_nbnd = 0;
+    }
+    __syncthreads();
+    {
+      const uint64_t* row = dc.seg_hi + (uint64_t)c * (dc.nh + 1);
+      uint32_t below = 0;
+      for (uint32_t h = 1 + threadIdx.x; h <= dc.nh; h += T) {
+        const uint64_t v = row[h];
+        if (v <= start) ++below;
+        else if (v < start + n) {
+          const uint32_t k = atomicAdd(&s_nbnd, 1u);
+          if (k < (uint32_t)kMaxBnd) s_bnd[k] = v;
+        }
+      }
+      below = __reduce_add_sync(kFull, below);
+      if (lane == 0 && below) atomicAdd(&s_h0, below);
+    }
+    __syncthreads();
+    const uint32_t* buf = s_buf + b * CH;
+#pragma unroll
+    for (int s = 0; s < K; ++s) {
+      const uint32_t i = seg0 + s * 32 + lane;
+      if (i < n) smem_inc(&cnt_w[(buf[i] >> shift_f) & mask_f]);
+    }
+    __syncthreads();
+    warp_counts_to_bases<W>(s_cnt, Db, s_dstart, s_dtot, s_tmp);
+    const uint32_t h0 = s_h0, nbnd = min(s_nbnd, (uint32_t)kMaxBnd);
+    uint32_t rr[K], pp[K];
+#pragma unroll
+    for (int s = 0; s < K; ++s) {
+      const uint32_t i = seg0 + s * 32 + lane;
+      const bool valid = i < n;
+      const uint32_t r = valid ? buf[i] : 0u;
+      uint32_t h = h0;
+      const uint64_t p = start + i;
+      for (uint32_t q = 0; q < nbnd; ++q) h += (s_bnd[q] <= p) ? 1u : 0u;
+      const uint32_t src = (h << dc.L) | (r & dc.src_mask);
+      const uint32_t d = (r >> dc.L) & mask_c;
+      rr[s] = (d << dc.nb) | src;
+      pp[s] = warp_rank<kMode>(cnt_w, scr_w, (r >> shift_f) & mask_f, valid);
+    }
+    __syncthreads();
+    uint32_t* wbuf = s_buf + b * CH;
+#pragma unroll
+    for (int s = 0; s < K; ++s)
+      if (seg0 + s * 32 + lane < n) wbuf[pp[s]] = rr[s];
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < n; i += T) rout[start + i] = wbuf[i];
+    uint16_t* so = segoff + (uint64_t)g * (Db + 1);
+    for (int f = threadIdx.x; f < Db; f += T) so[f] = (uint16_t)s_dstart[f];
+    if (threadIdx.x == 0) so[Db] = (uint16_t)n;
+  }
+}
+
+// Level 3, compact: fine ranges of a coarse bucket walked as units of one
+// fine bucket (<= kFCapC records) or batches of a big fine bucket (count pass
+// then place pass), with the next unit gathered by cp.async while the current
+// one is ranked.
+struct FineCtxC {
+  const uint32_t* rec;  // R2 records, chunk-major (each chunk sorted by fine digit)
+  const uint64_t* cstart;
+  const uint32_t* chunk_first;
+  const uint16_t* segoff;
+  int Db;
+  int bits_c;
+  int nb;
+  uint64_t V;
+};
+
+// Gather n records of fine digit f of the coarse bucket, starting at chunk g
+// after skipping `skip` records of its slice (warp per segment, cp.async).
+__device__ __forceinline__ void gather_unit_c(const FineCtxC& x, const CoarseInfo& ci, uint32_t f, uint32_t n,
+                                              uint32_t g, uint32_t skip, uint32_t* dst, uint64_t* s_st,
+                                              uint32_t* s_pos, uint32_t* s_tmp, uint32_t& g_out,
+                                              uint32_t& skip_out) {
+  const uint32_t lane = lane_id(), w = warp_id(), nw = blockDim.x >> 5;
+  uint32_t got = 0;
+  g_out = g;
+  skip_out = skip;
+  uint32_t gb = g;
+  while (gb < ci.g_end && got < n) {
+    const int nch = (int)min((uint32_t)kSegCapC, ci.g_end - gb);
+    for (int j = threadIdx.x; j < nch; j += blockDim.x) {
+      const uint64_t cpos = ci.cs + (uint64_t)(gb + j - ci.g_first) * kChunkC;
+      const uint16_t* so = x.segoff + (uint64_t)(gb + j) * (x.Db + 1);
+      const uint32_t a = so[f], e = so[f + 1];
+      s_st[j] = cpos + a;
+      s_pos[j] = e - a;
+    }
+    __syncthreads();
+    const uint32_t tot = block_excl_scan_u32(s_pos, nch, s_tmp);
+    if (threadIdx.x == 0) s_pos[nch] = tot;
+    __syncthreads();
+    const uint32_t lo = skip, want = n - got;
+    const uint32_t hi = (tot > lo) ? min(tot, lo + want) : lo;
+    for (int j = w; j < nch; j += nw) {
+      const uint32_t a = max(s_pos[j], lo), e = min(s_pos[j + 1], hi);
+      if (a >= e) continue;
+      const uint64_t src = s_st[j] + (a - s_pos[j]);
+      uint32_t* d = dst + got + (a - lo);
+      for (uint32_t q = lane; q < e - a; q += 32) cp_async4(d + q, x.rec + src + q);
+    }
+    if (hi > lo) {
+      got += hi - lo;
+      if (got >= n) {
+        int lo_j = 0, hi_j = nch - 1;  // last j with s_pos[j] < hi
+        while (lo_j < hi_j) {
+          const int mid = (lo_j + hi_j + 1) >> 1;
+          if (s_pos[mid] < hi) lo_j = mid; else hi_j = mid - 1;
+        }
+        g_out = gb + lo_j;
+        skip_out = hi - s_pos[lo_j];
+        __syncthreads();
+        return;
+      }
+    }
+    skip = (tot > skip) ? 0 : skip - tot;
+    gb += nch;
+    __syncthreads();
+  }
+  g_out = gb;
+  skip_out = skip;
+}
+
+template <int kMode>
+__global__ void __launch_bounds__(kFcWarps * 32, 3) k_final_c(FineCtxC x, const FRange* __restrict__ ranges,
+                                                          const uint32_t* __restrict__ n_ranges_ptr,
+                                                          unsigned int* __restrict__ range_ctr,
+                                                          const uint32_t* __restrict__ fine_size,
+                                                          const uint64_t* __restrict__ fine_base,
+                                                          uint64_t* __restrict__ t_offsets,
+                                                          uint32_t* __restrict__ t_edges,
+                                                          unsigned long long* __restrict__ prof) {
+  constexpr int W = kFcWarps, K = kFcSlots, T = W * 32, CAP = kFCapC, ML = kFMaxLocal;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem_raw);              // 2 * CAP (staging in place)
+  uint64_t* s_st = reinterpret_cast<uint64_t*>(s_buf + 2 * CAP);        // kSegCapC
+  uint32_t* s_pos = reinterpret_cast<uint32_t*>(s_st + kSegCapC);       // kSegCapC + 4
+  uint32_t* s_cnt = s_pos + kSegCapC + 4;                               // W * ML
+  uint32_t* s_scr = s_cnt + W * ML;                                     // (safe)
+  uint32_t* s_dstart = s_scr + (kMode == kRankSafe ? W * ML : 0);       // ML
+  uint32_t* s_dtot = s_dstart + ML;                                     // ML
+  uint32_t* s_tmp = s_dtot + ML;                                        // 40
+  uint64_t* s_cur = reinterpret_cast<uint64_t*>(s_tmp + 40);            // ML
+  uint32_t* s_bcnt = reinterpret_cast<uint32_t*>(s_cur + ML);           // ML
+  uint32_t* s_rsz = s_bcnt + ML;                                        // kMaxRange
+  uint64_t* s_rbase = reinterpret_cast<uint64_t*>(s_rsz + kMaxRange);   // kMaxRange
+  __shared__ uint32_t s_range;
+
+  const uint32_t n_ranges = *n_ranges_ptr;
+  const uint32_t lane = lane_id(), w = warp_id();
   const int Dc = 1 << x.bits_c;
-  const uint32_t nbk = *n_big;
-  for (uint32_t bk = blockIdx.x; bk < nbk; bk += gridDim.x) {
-  const uint32_t fid = big_buckets[3 * bk], i0 = big_buckets[3 * bk + 1], nb = big_buckets[3 * bk + 2];
-  const uint64_t v0 = (uint64_t)fid << x.bits_c;
-  __shared__ uint64_t s_tot[kFMaxLocal];
-  __shared__ uint64_t s_ex[kFMaxLocal];
-  for (int v = threadIdx.x; v < Dc; v += blockDim.x) {
-    uint64_t run = 0;
-    for (uint32_t j = 0; j < nb; ++j) run += cnt_tab[(uint64_t)(i0 + j) * Dc + v];
-    s_tot[v] = run;
-    if (run >= (1ull << 32)) atomicExch(err_overflow, 1u);
-  }
-  __syncthreads();
+  const uint32_t nbmask = (x.nb >= 32) ? 0xffffffffu : ((1u << x.nb) - 1);
+  if (kMode == kRankSafe)
+    for (int i = threadIdx.x; i < W * ML; i += T) s_scr[i] = 0;
+
+  struct Gen {
+    uint32_t c, f, f0, f1;
+    uint32_t big_f, big_left, phase, g, skip, big_size;
+    uint64_t big_base;
+    bool live;
+    CoarseInfo ci;
+  } gen;
+  gen.live = false;
+  gen.big_left = 0;
+  gen.phase = 0;
+  auto fetch_range = [&]() -> bool {
+    __syncthreads();
+    if (threadIdx.x == 0) s_range = atomicAdd(range_ctr, 1u);
+    __syncthreads();
+    const uint32_t r = s_range;
+    if (r >= n_ranges) return false;
+    const FRange R = ranges[r];
+    gen.c = R.c;
+    gen.f0 = R.f0;
+    gen.f = R.f0;
+    gen.f1 = R.f1;
+    gen.live = true;
+    gen.ci.g_first = x.chunk_first[R.c];
+    gen.ci.g_end = x.chunk_first[R.c + 1];
+    gen.ci.cs = x.cstart[R.c];
+    gen.ci.ce = x.cstart[R.c + 1];
+    const uint64_t fb = (uint64_t)R.c * x.Db + R.f0;
+    for (uint32_t i = threadIdx.x; i < R.f1 - R.f0; i += blockDim.x) {
+      s_rsz[i] = fine_size[fb + i];
+      s_rbase[i] = fine_base[fb + i];
+    }
+    __syncthreads();
+    return true;
+  };
+  auto next_unit = [&](FUnit& u) -> bool {
+    while (true) {
+      if (gen.big_left) {
+        u.kind = gen.phase;
+        u.f0 = gen.big_f;
+        u.f1 = gen.big_f + 1;
+        u.n = min((uint32_t)CAP, gen.big_left);
+        u.g = gen.g;
+        u.skip = gen.skip;
+        u.base = gen.big_base;
+        gen.big_left -= u.n;
+        u.last = (gen.big_left == 0);
+        u.first = (gen.phase == 1 && gen.big_left + u.n == gen.big_size);
+        if (gen.big_left == 0 && gen.phase == 1) {
+          gen.phase = 2;
+          gen.big_left = gen.big_size;
+          gen.g = gen.ci.g_first;
+          gen.skip = 0;
+          u.last = 1;
+          return true;
+        }
+        if (gen.big_left == 0) gen.phase = 0;
+        return true;
+      }
+      if (!gen.live || gen.f >= gen.f1) {
+        if (!fetch_range()) return false;
+        continue;
+      }
+      const uint32_t sz = s_rsz[gen.f - gen.f0];
+      if (sz == 0) { ++gen.f; continue; }
+      if (sz > (uint32_t)CAP) {
+        gen.big_f = gen.f;
+        gen.big_size = sz;
+        gen.big_left = sz;
+        gen.big_base = s_rbase[gen.f - gen.f0];
+        gen.phase = 1;
+        gen.g = gen.ci.g_first;
+        gen.skip = 0;
+        ++gen.f;
+        continue;
+      }
+      u.kind = 0;
+      u.f0 = gen.f;
+      u.f1 = gen.f + 1;
+      u.n = sz;
+      u.g = gen.ci.g_first;
+      u.skip = 0;
+      u.last = 0;
+      u.first = 0;
+      u.base = s_rbase[gen.f - gen.f0];
+      ++gen.f;
+      return true;
+    }
+  };
+  auto issue = [&](const FUnit& u, int b) {
+    uint32_t go, so;
+    gather_unit_c(x, gen.ci, u.f0, u.n, u.g, u.skip, s_buf + b * CAP, s_st, s_pos, s_tmp, go, so);
+    if (u.kind != 0 && !(u.kind == 1 && u.last)) {
+      gen.g = go;
+      gen.skip = so;
+    }
+    cp_commit();
+  };
+
+  __shared__ unsigned long long pacc[10];  // profiling accumulators (thread 0)
+  __shared__ long long tprev;
   if (threadIdx.x == 0) {
-    uint64_t run = big_base[bk];
-    for (int v = 0; v < Dc; ++v) {
-      s_ex[v] = run;
-      run += s_tot[v];
+    for (int i = 0; i < 10; ++i) pacc[i] = 0;
+    tprev = clock64();
+  }
+  auto ptick = [&](int ph) {
+    if (prof && threadIdx.x == 0) {
+      const long long tn = clock64();
+      pacc[ph] += (unsigned long long)(tn - tprev);
+      tprev = tn;
     }
-  }
-  __syncthreads();
-  for (int v = threadIdx.x; v < Dc; v += blockDim.x) {
-    uint64_t run = s_ex[v];
-    if (v0 + v < x.V) t_offsets[v0 + v] = run;
-    for (uint32_t j = 0; j < nb; ++j) {
-      cur_tab[(uint64_t)(i0 + j) * Dc + v] = run;
-      run += cnt_tab[(uint64_t)(i0 + j) * Dc + v];
+  };
+  FUnit u0, u1;
+  uint32_t c0 = 0, c1 = 0;
+  if (!next_unit(u0)) return;
+  c0 = gen.c;
+  issue(u0, 0);
+  for (int it = 0;; ++it) {
+    const int b = it & 1;
+    ptick(9);
+    const bool more = next_unit(u1);
+    c1 = gen.c;
+    ptick(0);
+    if (more) {
+      issue(u1, b ^ 1);
+      ptick(1);
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
     }
+    const uint32_t cur_c = c0;
+    const FUnit u = u0;
+    const uint32_t n = u.n;
+    uint32_t* cnt_w = s_cnt + w * Dc;
+    uint32_t* scr_w = s_scr + (kMode == kRankSafe ? w * Dc : 0);
+    for (int i = threadIdx.x; i < W * Dc; i += T) s_cnt[i] = 0;
+    if (u.kind == 1 && u.first)
+      for (int v = threadIdx.x; v < Dc; v += T) s_bcnt[v] = 0;
+    __syncthreads();
+    ptick(2);
+    if (prof && threadIdx.x == 0) pacc[7 + (u.kind == 0 ? 0 : 1)] += 1;
+    uint32_t* buf = s_buf + b * CAP;
+    const uint32_t seg0 = w * (K * 32);
+    if (u.kind == 1) {
+#pragma unroll
+      for (int s = 0; s < K; ++s) {
+        const uint32_t i = seg0 + s * 32 + lane;
+        if (i < n) smem_inc(&s_bcnt[buf[i] >> x.nb]);
+      }
+      __syncthreads();
+      if (u.last) {
+        if (threadIdx.x == 0) {
+          uint64_t run = u.base;
+          for (int v = 0; v < Dc; ++v) {
+            s_cur[v] = run;
+            run += s_bcnt[v];
+          }
+        }
+        __syncthreads();
+        const uint64_t v0 = ((uint64_t)cur_c * x.Db + u.f0) << x.bits_c;
+        for (int v = threadIdx.x; v < Dc; v += T)
+          if (v0 + v < x.V) t_offsets[v0 + v] = s_cur[v];
+        __syncthreads();
+      }
+    } else {
+#pragma unroll
+      for (int s = 0; s < K; ++s) {
+        const uint32_t i = seg0 + s * 32 + lane;
+        if (i < n) smem_inc(&cnt_w[buf[i] >> x.nb]);
+      }
+      __syncthreads();
+      ptick(3);
+      warp_counts_to_bases<W>(s_cnt, Dc, s_dstart, s_dtot, s_tmp);
+      ptick(4);
+      if (u.kind == 0) {
+        const uint64_t v0 = ((uint64_t)cur_c * x.Db + u.f0) << x.bits_c;
+        for (int v = threadIdx.x; v < Dc; v += T)
+          if (v0 + v < x.V) t_offsets[v0 + v] = u.base + s_dstart[v];
+      }
+      uint32_t rr[K], pp[K];
+#pragma unroll
+      for (int s = 0; s < K; ++s) {
+        const uint32_t i = seg0 + s * 32 + lane;
+        const bool valid = i < n;
+        rr[s] = valid ? buf[i] : 0u;
+        pp[s] = warp_rank<kMode>(cnt_w, scr_w, rr[s] >> x.nb, valid);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int s = 0; s < K; ++s)
+        if (seg0 + s * 32 + lane < n) buf[pp[s]] = rr[s];
+      __syncthreads();
+      ptick(5);
+      if (u.kind == 0) {
+        for (uint32_t i = threadIdx.x; i < n; i += T) t_edges[u.base + i] = buf[i] & nbmask;
+      } else {
+        for (uint32_t i = threadIdx.x; i < n; i += T) {
+          const uint32_t r = buf[i], d = r >> x.nb;
+          t_edges[s_cur[d] + (i - s_dstart[d])] = r & nbmask;
+        }
+        __syncthreads();
+        for (int v = threadIdx.x; v < Dc; v += T) s_cur[v] += s_dtot[v];
+      }
+    }
+    __syncthreads();
+    ptick(6);
+    if (!more) break;
+    u0 = u1;
+    c0 = c1;
   }
-  __syncthreads();
-  }
+  if (prof && threadIdx.x == 0)
+    for (int i = 0; i < 10; ++i) atomicAdd(&prof[i], pacc[i]);
 }
 
 // ----------------------------------------------------------- self test

@@ -109,7 +109,8 @@ class GpuShardBackend:
         _lib.check(rc, "gt_shard_partition")
         return records[:n], counts.astype(np.int64)
 
-    def transpose_received(self, records, dst_lo: int, dst_hi: int, global_base: int, want_stats=False):
+    def transpose_received(self, records, dst_lo: int, dst_hi: int, global_base: int, want_stats=False,
+                           src_num_vertices: int = 1 << 32):
         """-> (t_offsets int64[n_local+1] with global positions, t_edges int32[R], stats)."""
         torch = self.torch
         R = int(records.shape[0])
@@ -119,7 +120,7 @@ class GpuShardBackend:
         st = _lib.GtStats() if want_stats else None
         with torch.cuda.device(self.device):
             rc = _lib.lib.gt_shard_transpose(
-                ctypes.c_void_p(records.data_ptr()) if R else None, R, dst_lo, dst_hi, global_base,
+                ctypes.c_void_p(records.data_ptr()) if R else None, R, src_num_vertices, dst_lo, dst_hi, global_base,
                 ctypes.c_void_p(t_off.data_ptr()), ctypes.c_void_p(t_edg.data_ptr()), self._stream(),
                 ctypes.byref(st) if st is not None else None)
         _lib.check(rc, "gt_shard_transpose")
@@ -153,7 +154,7 @@ def transpose_sharded_local(g, plan: ShardPlan, backend):
         torch = backend.torch
         recv = torch.cat(pieces, dim=0) if pieces else None
         lo_v, hi_v = int(plan.dst_bounds[q]), int(plan.dst_bounds[q + 1])
-        t_off, t_edg, _ = backend.transpose_received(recv, lo_v, hi_v, base)
+        t_off, t_edg, _ = backend.transpose_received(recv, lo_v, hi_v, base, src_num_vertices=nv)
         t_offsets[lo_v : hi_v + 1] = t_off.cpu().numpy().view(np.uint64)
         n = int(recv.shape[0])
         t_edges[base : base + n] = t_edg.cpu().numpy().view(np.uint32)
@@ -207,7 +208,7 @@ def distributed_step(offsets_d, edges_slice_d, num_vertices: int, plan: ShardPla
     recv, C = exchange_records(rec, cnt, group=group)
     base = int(C[:, :rank].sum())
     t_off, t_edg, _ = backend.transpose_received(recv, int(plan.dst_bounds[rank]), int(plan.dst_bounds[rank + 1]),
-                                                 base)
+                                                 base, src_num_vertices=num_vertices)
     return t_off, t_edg, base
 
 

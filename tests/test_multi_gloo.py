@@ -41,7 +41,7 @@ class CpuShardBackend:
         counts = np.bincount(owner_rank, minlength=len(dst_bounds) - 1).astype(np.int64)
         return torch.from_numpy(rec.view(np.int32)), counts
 
-    def transpose_received(self, records, dst_lo, dst_hi, global_base, want_stats=False):
+    def transpose_received(self, records, dst_lo, dst_hi, global_base, want_stats=False, src_num_vertices=None):
         rec = records.numpy().view(np.uint32).reshape(-1, 2)
         d = rec[:, 1].astype(np.int64) - dst_lo
         order = np.argsort(d, kind="stable")
