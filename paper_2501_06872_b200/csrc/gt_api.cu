@@ -228,9 +228,9 @@ int rank_mode_for(int dev, cudaStream_t st, int* mode) {
 size_t smem_l1_place(int D, int mode, bool records, uint64_t CT, bool compact = false) {
   const int W = kL1Warps, PT = kPlaceTile;
   const size_t in = records ? (size_t)2 * PT * 8 : (size_t)2 * PT * 4 + (size_t)2 * kWinCap * 8;
-  return in + (size_t)PT * (compact ? 4 : 8) + (size_t)D * 8 + (records ? 0 : (size_t)PT * 4) + (size_t)W * D * 4 +
+  return in + (size_t)PT * (compact ? 4 : 8) + (size_t)D * 16 + (size_t)W * D * 4 +
          (mode == kRankSafe ? (size_t)W * D * 4 : 0) + (size_t)D * 8 + 40 * 4 + (CT / PT + 4) * 4 +
-         (compact ? (size_t)D * 4 + (size_t)PT * 2 : 0) + 16;
+         (compact ? (size_t)D * 4 : 0) + 16;
 }
 size_t smem_b1c(int Db, int mode) {
   const int W = kB1cWarps;

@@ -196,17 +196,19 @@ __global__ void __launch_bounds__(kL1Warps * 32) k_l1_place(In in, Dig dig, uint
   // input staging: CSR -> dst u32[2][PT] + offsets window u64[2][kWinCap]; records -> uint2[2][PT]
   constexpr size_t kInBytes = In::kRecords ? 2 * PT * 8 : 2 * PT * 4 + 2 * kWinCap * 8;
   unsigned char* s_in = smem_raw;
+  // the owner marks (round 1) and the staged records (round 2) share storage;
+  // compact digit tags reuse the consumed input buffer of the current tile
   StageT* s_stage = reinterpret_cast<StageT*>(smem_raw + kInBytes);   // PT
+  uint32_t* s_mark = reinterpret_cast<uint32_t*>(s_stage);            // PT (CSR only, aliases s_stage)
   uint64_t* s_gcur = reinterpret_cast<uint64_t*>(s_stage + PT);       // D
-  uint32_t* s_mark = reinterpret_cast<uint32_t*>(s_gcur + D);         // PT (CSR only)
-  uint32_t* s_cnt = s_mark + (In::kRecords ? 0 : PT);                 // W * D
+  uint64_t* s_delta = s_gcur + D;                                     // D: gcur - dstart
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_delta + D);         // W * D
   uint32_t* s_scr = s_cnt + W * D;                                    // W * D (safe mode)
   uint32_t* s_dstart = s_scr + (kMode == kRankSafe ? W * D : 0);      // D
   uint32_t* s_dtot = s_dstart + D;                                    // D
   uint32_t* s_tmp = s_dtot + D;                                       // 40
   uint32_t* s_psrc = s_tmp + 40;                                      // CT/PT + 2 (CSR only)
   uint32_t* s_bh = s_psrc + (CT / PT + 4);                            // D (compact)
-  uint16_t* s_sdig = reinterpret_cast<uint16_t*>(s_bh + (Out::kCompact ? D : 0));  // PT (compact)
   __shared__ uint32_t s_wmax[W];
   __shared__ uint32_t s_last_src;
 
@@ -280,31 +282,38 @@ __global__ void __launch_bounds__(kL1Warps * 32) k_l1_place(In in, Dig dig, uint
         if (o < gpe) atomicMax(&s_mark[o - gpt], s0 + 1 + i);
       }
       __syncthreads();
+      // per-slot maxima -> per-slot carries (no loop-carried shuffle chain)
+      uint32_t sm[K];
       uint32_t wm = 0;
 #pragma unroll
-      for (int s = 0; s < K; ++s) wm = max(wm, s_mark[seg0 + s * 32 + lane]);
-      wm = __reduce_max_sync(kFull, wm);
+      for (int s = 0; s < K; ++s) {
+        sm[s] = s_mark[seg0 + s * 32 + lane];
+        const uint32_t smax = __reduce_max_sync(kFull, sm[s]);
+        wm = max(wm, smax);
+        r_src[s] = wm;  // inclusive max through slot s (temporarily)
+      }
       if (lane == 0) s_wmax[w] = wm;
       __syncthreads();
       uint32_t carry = s0;
       for (int ww = 0; ww < (int)w; ++ww) carry = max(carry, s_wmax[ww]);
       const uint32_t* dbuf = reinterpret_cast<const uint32_t*>(s_in) + b * PT;
 #pragma unroll
-      for (int s = 0; s < K; ++s) {
+      for (int s = K - 1; s >= 0; --s) {  // carry into slot s = max over earlier slots
+        const uint32_t cin = max(carry, s > 0 ? r_src[s - 1] : 0u);
         const uint32_t i = seg0 + s * 32 + lane;
         const bool valid = i < n;
         r_dst[s] = valid ? dbuf[i] : 0u;
-        uint32_t m = s_mark[i];
+        uint32_t m = sm[s];
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const uint32_t y = __shfl_up_sync(kFull, m, o);
           if (lane >= (uint32_t)o) m = max(m, y);
         }
-        m = max(m, carry);
-        r_src[s] = m;
-        carry = __shfl_sync(kFull, m, 31);
-        if (valid) smem_inc(&cnt_w[dig(r_dst[s])]);
+        r_src[s] = max(m, cin);
       }
+#pragma unroll
+      for (int s = 0; s < K; ++s)
+        if (seg0 + s * 32 + lane < n) smem_inc(&cnt_w[dig(r_dst[s])]);
     } else {
       const uint2* rbuf = reinterpret_cast<const uint2*>(s_in) + b * PT;
 #pragma unroll
@@ -343,8 +352,11 @@ __global__ void __launch_bounds__(kL1Warps * 32) k_l1_place(In in, Dig dig, uint
       }
       h_prev = h_last;
     }
-    __syncthreads();
+    __syncthreads();  // marks consumed: s_stage may be overwritten from here on
     warp_counts_to_bases<W>(s_cnt, D, s_dstart, s_dtot, s_tmp);
+    for (int d = threadIdx.x; d < D; d += T) s_delta[d] = s_gcur[d] - s_dstart[d];
+    // digit tags (compact) live in the consumed input buffer of this tile
+    uint16_t* s_sdig = reinterpret_cast<uint16_t*>(s_in + (size_t)b * PT * (In::kRecords ? 8 : 4));
 #pragma unroll
     for (int s = 0; s < K; ++s) {
       const uint32_t i = seg0 + s * 32 + lane;
@@ -366,11 +378,11 @@ __global__ void __launch_bounds__(kL1Warps * 32) k_l1_place(In in, Dig dig, uint
       uint32_t d;
       if constexpr (Out::kCompact) d = s_sdig[i];
       else d = dig(r.y);
-      out.rec[s_gcur[d] + (i - s_dstart[d])] = r;
+      out.rec[s_delta[d] + i] = r;
     }
+    __syncthreads();
     if constexpr (!In::kRecords)
       for (int i = threadIdx.x; i < PT; i += T) s_mark[i] = 0;
-    __syncthreads();
     for (int d = threadIdx.x; d < D; d += T) s_gcur[d] += s_dtot[d];
   }
 }
