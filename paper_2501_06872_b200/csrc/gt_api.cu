@@ -56,6 +56,7 @@ struct Plan {
   uint64_t V = 0, E = 0;
   bool compact = false;  // 4-byte records (R1/R2), see gt_kernels.cuh
   int L = 0, nsh = 0;    // compact R1: source low bits, source high bits
+  int gbits = 0;         // compact R2: fine-digit bits kept (final units = aligned groups of 2^gbits)
   int nb = 0, nbs = 0, a = 0, b = 0, c = 0;
   int D1 = 1, Db = 1, Dc = 1;
   uint64_t CT = 65536, ntiles = 0, nplace = 0, max_chunks = 0, max_items_s = 0, max_items_b = 0;
@@ -75,7 +76,7 @@ int make_plan(uint64_t V, uint64_t E, Plan& p, uint64_t Vsrc = 0) {
   // compact path: 4-byte records; fine buckets average ~kFCapC/2 records
   {
     int cc = 1;
-    while (cc < 8 && (double)(1u << (cc + 1)) * std::max(avg, 1.0) <= (double)kFCapC / 2.0) ++cc;
+    while (cc < 8 && (double)(1u << (cc + 1)) * std::max(avg, 1.0) <= (double)kFCapC / 4.0) ++cc;
     cc = std::min(cc, 32 - p.nbs);
     cc = std::min(cc, p.nb);
     const int rem = p.nb - cc;
@@ -94,6 +95,9 @@ int make_plan(uint64_t V, uint64_t E, Plan& p, uint64_t Vsrc = 0) {
       c = cc;
       p.L = L;
       p.nsh = nsh;
+      int gb = std::min(32 - p.nbs - cc, cb);
+      while (gb > 0 && (1 << (gb + cc)) > kFMaxLocal) --gb;
+      p.gbits = std::max(0, gb);
     }
   }
   if (!p.compact) {
@@ -514,6 +518,7 @@ int transpose_core_c(const Plan& p, In in, uint64_t* t_offsets, uint32_t* t_edge
     dc.seg_hi = seghi;
     dc.bits_c = p.c;
     dc.nb = p.nbs;
+    dc.gbits = p.gbits;
     const size_t sm = smem_b1c(p.Db, kMode);
     if ((rc = set_smem(k_b1c<kMode>, sm))) return rc;
     const unsigned grid = persistent_grid(k_b1c<kMode>, kB1cWarps * 32, sm, p.max_chunks);
@@ -544,6 +549,7 @@ int transpose_core_c(const Plan& p, In in, uint64_t* t_offsets, uint32_t* t_edge
     xc.Db = p.Db;
     xc.bits_c = p.c;
     xc.nb = p.nbs;
+    xc.gbits = p.gbits;
     xc.V = V;
     unsigned long long* prof = nullptr;
     if (getenv("GT_FPROF")) {

@@ -48,8 +48,8 @@ constexpr int kB1cWarps = 16;
 constexpr int kB1cSlots = 32;
 constexpr int kChunkC = kB1cWarps * kB1cSlots * 32;  // 16384 records per chunk
 constexpr int kFcWarps = 8;
-constexpr int kFcSlots = 16;
-constexpr int kFCapC = kFcWarps * kFcSlots * 32;  // 4096 records per final unit
+constexpr int kFcSlots = 32;
+constexpr int kFCapC = kFcWarps * kFcSlots * 32;  // 8192 records per final unit
 constexpr int kSegCapC = 512;
 constexpr int kMaxBnd = 64;
 
@@ -996,6 +996,7 @@ struct DecodeC {
   const uint64_t* seg_hi;
   int bits_c;         // low destination digit bits
   int nb;             // source bits in R2
+  int gbits;          // low fine-digit bits kept in R2 (final units span aligned groups of 2^gbits)
 };
 
 // Level 2, compact: stable sort of each 16K-record chunk by the middle digit,
@@ -1022,7 +1023,7 @@ __global__ void __launch_bounds__(kB1cWarps * 32) k_b1c(const uint32_t* __restri
   uint32_t* scr_w = s_scr + (kMode == kRankSafe ? w * Db : 0);
   const uint32_t seg0 = w * (K * 32);
   const uint32_t shift_f = dc.L + dc.bits_c, mask_f = (uint32_t)Db - 1;
-  const uint32_t mask_c = (1u << dc.bits_c) - 1;
+  const uint32_t gmask = (1u << (dc.bits_c + dc.gbits)) - 1;
   if (kMode == kRankSafe)
     for (int i = threadIdx.x; i < W * Db; i += T) s_scr[i] = 0;
 
@@ -1098,8 +1099,8 @@ __global__ void __launch_bounds__(kB1cWarps * 32) k_b1c(const uint32_t* __restri
       const uint64_t p = start + i;
       for (uint32_t q = 0; q < nbnd; ++q) h += (s_bnd[q] <= p) ? 1u : 0u;
       const uint32_t src = (h << dc.L) | (r & dc.src_mask);
-      const uint32_t d = (r >> dc.L) & mask_c;
-      rr[s] = (d << dc.nb) | src;
+      const uint32_t lv = (r >> dc.L) & gmask;  // (fine & (G-1)) << c | d
+      rr[s] = (lv << dc.nb) | src;
       pp[s] = warp_rank<kMode>(cnt_w, scr_w, (r >> shift_f) & mask_f, valid);
     }
     __syncthreads();
@@ -1127,13 +1128,14 @@ struct FineCtxC {
   int Db;
   int bits_c;
   int nb;
+  int gbits;  // fine-digit bits in R2: units are runs of an aligned group of 2^gbits fine buckets
   uint64_t V;
 };
 
 // Gather n records of fine digit f of the coarse bucket, starting at chunk g
 // after skipping `skip` records of its slice (warp per segment, cp.async).
-__device__ __forceinline__ void gather_unit_c(const FineCtxC& x, const CoarseInfo& ci, uint32_t f, uint32_t n,
-                                              uint32_t g, uint32_t skip, uint32_t* dst, uint64_t* s_st,
+__device__ __forceinline__ void gather_unit_c(const FineCtxC& x, const CoarseInfo& ci, uint32_t f, uint32_t f_end,
+                                              uint32_t n, uint32_t g, uint32_t skip, uint32_t* dst, uint64_t* s_st,
                                               uint32_t* s_pos, uint32_t* s_tmp, uint32_t& g_out,
                                               uint32_t& skip_out) {
   const uint32_t lane = lane_id(), w = warp_id(), nw = blockDim.x >> 5;
@@ -1146,7 +1148,7 @@ __device__ __forceinline__ void gather_unit_c(const FineCtxC& x, const CoarseInf
     for (int j = threadIdx.x; j < nch; j += blockDim.x) {
       const uint64_t cpos = ci.cs + (uint64_t)(gb + j - ci.g_first) * kChunkC;
       const uint16_t* so = x.segoff + (uint64_t)(gb + j) * (x.Db + 1);
-      const uint32_t a = so[f], e = so[f + 1];
+      const uint32_t a = so[f], e = so[f_end];
       s_st[j] = cpos + a;
       s_pos[j] = e - a;
     }
@@ -1186,7 +1188,7 @@ __device__ __forceinline__ void gather_unit_c(const FineCtxC& x, const CoarseInf
 }
 
 template <int kMode>
-__global__ void __launch_bounds__(kFcWarps * 32, 3) k_final_c(FineCtxC x, const FRange* __restrict__ ranges,
+__global__ void __launch_bounds__(kFcWarps * 32, 2) k_final_c(FineCtxC x, const FRange* __restrict__ ranges,
                                                           const uint32_t* __restrict__ n_ranges_ptr,
                                                           unsigned int* __restrict__ range_ctr,
                                                           const uint32_t* __restrict__ fine_size,
@@ -1213,6 +1215,8 @@ __global__ void __launch_bounds__(kFcWarps * 32, 3) k_final_c(FineCtxC x, const 
   const uint32_t n_ranges = *n_ranges_ptr;
   const uint32_t lane = lane_id(), w = warp_id();
   const int Dc = 1 << x.bits_c;
+  const uint32_t G = 1u << x.gbits;
+  const uint32_t lvmask = (1u << (x.bits_c + x.gbits)) - 1;
   const uint32_t nbmask = (x.nb >= 32) ? 0xffffffffu : ((1u << x.nb) - 1);
   if (kMode == kRankSafe)
     for (int i = threadIdx.x; i < W * ML; i += T) s_scr[i] = 0;
@@ -1292,22 +1296,30 @@ __global__ void __launch_bounds__(kFcWarps * 32, 3) k_final_c(FineCtxC x, const 
         ++gen.f;
         continue;
       }
+      const uint32_t blk_end = min(gen.f1, (gen.f | (G - 1)) + 1);  // end of the aligned group
+      uint32_t total = sz, e = gen.f + 1;
+      while (e < blk_end) {
+        const uint32_t z = s_rsz[e - gen.f0];
+        if (z > (uint32_t)CAP || total + z > (uint32_t)CAP) break;
+        total += z;
+        ++e;
+      }
       u.kind = 0;
       u.f0 = gen.f;
-      u.f1 = gen.f + 1;
-      u.n = sz;
+      u.f1 = e;
+      u.n = total;
       u.g = gen.ci.g_first;
       u.skip = 0;
       u.last = 0;
       u.first = 0;
       u.base = s_rbase[gen.f - gen.f0];
-      ++gen.f;
+      gen.f = e;
       return true;
     }
   };
   auto issue = [&](const FUnit& u, int b) {
     uint32_t go, so;
-    gather_unit_c(x, gen.ci, u.f0, u.n, u.g, u.skip, s_buf + b * CAP, s_st, s_pos, s_tmp, go, so);
+    gather_unit_c(x, gen.ci, u.f0, u.f1, u.n, u.g, u.skip, s_buf + b * CAP, s_st, s_pos, s_tmp, go, so);
     if (u.kind != 0 && !(u.kind == 1 && u.last)) {
       gen.g = go;
       gen.skip = so;
@@ -1349,9 +1361,12 @@ __global__ void __launch_bounds__(kFcWarps * 32, 3) k_final_c(FineCtxC x, const 
     const uint32_t cur_c = c0;
     const FUnit u = u0;
     const uint32_t n = u.n;
-    uint32_t* cnt_w = s_cnt + w * Dc;
-    uint32_t* scr_w = s_scr + (kMode == kRankSafe ? w * Dc : 0);
-    for (int i = threadIdx.x; i < W * Dc; i += T) s_cnt[i] = 0;
+    const uint32_t nloc = (u.f1 - u.f0) << x.bits_c;               // local vertices of the unit
+    const uint32_t lvoff = (u.f0 & (G - 1)) << x.bits_c;            // first local vertex in R2's field
+    auto lv_of = [&](uint32_t r) -> uint32_t { return ((r >> x.nb) & lvmask) - lvoff; };
+    uint32_t* cnt_w = s_cnt + w * nloc;
+    uint32_t* scr_w = s_scr + (kMode == kRankSafe ? w * nloc : 0);
+    for (int i = threadIdx.x; i < W * ML; i += T) s_cnt[i] = 0;
     if (u.kind == 1 && u.first)
       for (int v = threadIdx.x; v < Dc; v += T) s_bcnt[v] = 0;
     __syncthreads();
@@ -1363,7 +1378,7 @@ __global__ void __launch_bounds__(kFcWarps * 32, 3) k_final_c(FineCtxC x, const 
 #pragma unroll
       for (int s = 0; s < K; ++s) {
         const uint32_t i = seg0 + s * 32 + lane;
-        if (i < n) smem_inc(&s_bcnt[buf[i] >> x.nb]);
+        if (i < n) smem_inc(&s_bcnt[lv_of(buf[i])]);
       }
       __syncthreads();
       if (u.last) {
@@ -1384,15 +1399,15 @@ __global__ void __launch_bounds__(kFcWarps * 32, 3) k_final_c(FineCtxC x, const 
 #pragma unroll
       for (int s = 0; s < K; ++s) {
         const uint32_t i = seg0 + s * 32 + lane;
-        if (i < n) smem_inc(&cnt_w[buf[i] >> x.nb]);
+        if (i < n) smem_inc(&cnt_w[lv_of(buf[i])]);
       }
       __syncthreads();
       ptick(3);
-      warp_counts_to_bases<W>(s_cnt, Dc, s_dstart, s_dtot, s_tmp);
+      warp_counts_to_bases<W>(s_cnt, (int)nloc, s_dstart, s_dtot, s_tmp);
       ptick(4);
       if (u.kind == 0) {
         const uint64_t v0 = ((uint64_t)cur_c * x.Db + u.f0) << x.bits_c;
-        for (int v = threadIdx.x; v < Dc; v += T)
+        for (uint32_t v = threadIdx.x; v < nloc; v += T)
           if (v0 + v < x.V) t_offsets[v0 + v] = u.base + s_dstart[v];
       }
       uint32_t rr[K], pp[K];
@@ -1401,7 +1416,7 @@ __global__ void __launch_bounds__(kFcWarps * 32, 3) k_final_c(FineCtxC x, const 
         const uint32_t i = seg0 + s * 32 + lane;
         const bool valid = i < n;
         rr[s] = valid ? buf[i] : 0u;
-        pp[s] = warp_rank<kMode>(cnt_w, scr_w, rr[s] >> x.nb, valid);
+        pp[s] = warp_rank<kMode>(cnt_w, scr_w, valid ? lv_of(rr[s]) : 0u, valid);
       }
       __syncthreads();
 #pragma unroll
@@ -1413,7 +1428,7 @@ __global__ void __launch_bounds__(kFcWarps * 32, 3) k_final_c(FineCtxC x, const 
         for (uint32_t i = threadIdx.x; i < n; i += T) t_edges[u.base + i] = buf[i] & nbmask;
       } else {
         for (uint32_t i = threadIdx.x; i < n; i += T) {
-          const uint32_t r = buf[i], d = r >> x.nb;
+          const uint32_t r = buf[i], d = lv_of(r);
           t_edges[s_cur[d] + (i - s_dstart[d])] = r & nbmask;
         }
         __syncthreads();
