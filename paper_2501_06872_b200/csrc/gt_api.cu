@@ -138,7 +138,7 @@ int make_plan(uint64_t V, uint64_t E, Plan& p, uint64_t Vsrc = 0) {
     off = align_up(off + std::max<uint64_t>(bytes, 1), 256);
     return o;
   };
-  p.o_rec = take(E * (p.compact ? 4 : 8));
+  p.o_rec = take(E * (p.compact ? 4 : 8) + 64);  // + padding for 16B-aligned bulk loads
   p.o_tcnt = take((uint64_t)p.D1 * p.ntiles * 4);
   p.o_tbase = take(((uint64_t)p.D1 * p.ntiles + 1) * 8);
   p.o_psrc = take((p.nplace + 2) * 4);
@@ -238,7 +238,7 @@ size_t smem_l1_place(int D, int mode, bool records, uint64_t CT, bool compact = 
 }
 size_t smem_b1c(int Db, int mode) {
   const int W = kB1cWarps;
-  return (size_t)2 * kChunkC * 4 + (size_t)W * Db * 4 + (mode == kRankSafe ? (size_t)W * Db * 4 : 0) +
+  return (size_t)2 * (kChunkC + 8) * 4 + (size_t)W * Db * 4 + (mode == kRankSafe ? (size_t)W * Db * 4 : 0) +
          (size_t)Db * 8 + 40 * 4 + kMaxBnd * 8 + 16;
 }
 size_t smem_final_c(int mode) {

@@ -1001,22 +1001,27 @@ struct DecodeC {
 
 // Level 2, compact: stable sort of each 16K-record chunk by the middle digit,
 // re-encoding R1 -> R2 (source high bits from the chunk's boundary list).
+// Chunks move with TMA bulk copies: the 16B-aligned span [start & ~3, ...)
+// lands in smem at record offset `off = start & 3`, is ranked and staged in
+// place (same offset), and leaves with one bulk store (unaligned head/tail
+// records by plain stores).  Needs 3 records of readable padding after rin.
 template <int kMode>
 __global__ void __launch_bounds__(kB1cWarps * 32) k_b1c(const uint32_t* __restrict__ rin, uint32_t* __restrict__ rout,
                                                        const uint64_t* __restrict__ cstart,
                                                        const uint32_t* __restrict__ chunk_first,
                                                        const uint32_t* __restrict__ chunk_bucket, int D1, DecodeC dc,
                                                        int Db, uint16_t* __restrict__ segoff) {
-  constexpr int W = kB1cWarps, K = kB1cSlots, T = W * 32, CH = kChunkC;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem_raw);  // 2 * CH
-  uint32_t* s_cnt = s_buf + 2 * CH;                         // W * Db
+  constexpr int W = kB1cWarps, K = kB1cSlots, T = W * 32, CH = kChunkC, CHP = kChunkC + 8;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem_raw);  // 2 * CHP
+  uint32_t* s_cnt = s_buf + 2 * CHP;                        // W * Db
   uint32_t* s_scr = s_cnt + W * Db;
   uint32_t* s_dstart = s_scr + (kMode == kRankSafe ? W * Db : 0);
   uint32_t* s_dtot = s_dstart + Db;
   uint32_t* s_tmp = s_dtot + Db;                                        // 40
   uint64_t* s_bnd = reinterpret_cast<uint64_t*>(s_tmp + 40);            // kMaxBnd
   __shared__ uint32_t s_h0, s_nbnd;
+  __shared__ __align__(8) uint64_t s_bar[2];
   const uint32_t nchunks = chunk_first[D1];
   const uint32_t lane = lane_id(), w = warp_id();
   uint32_t* cnt_w = s_cnt + w * Db;
@@ -1026,46 +1031,52 @@ __global__ void __launch_bounds__(kB1cWarps * 32) k_b1c(const uint32_t* __restri
   const uint32_t gmask = (1u << (dc.bits_c + dc.gbits)) - 1;
   if (kMode == kRankSafe)
     for (int i = threadIdx.x; i < W * Db; i += T) s_scr[i] = 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
 
   auto chunk_range = [&](uint32_t g, uint32_t& c, uint64_t& start, uint32_t& n) {
     c = chunk_bucket[g];
     start = cstart[c] + (uint64_t)(g - chunk_first[c]) * CH;
     n = (uint32_t)umin64(CH, cstart[c + 1] - start);
   };
-  auto issue = [&](uint32_t g, int b) {
-    uint32_t c;
-    uint64_t st;
-    uint32_t n;
-    chunk_range(g, c, st, n);
-    uint32_t* dst = s_buf + b * CH;
-    for (uint32_t i = threadIdx.x; i < n; i += T) cp_async4(dst + i, rin + st + i);
-    cp_commit();
+  uint32_t nx_c = 0, nx_n = 0;
+  uint64_t nx_start = 0;
+  auto issue = [&](uint32_t g, int b) {  // all threads compute the range; thread 0 issues the bulk load
+    chunk_range(g, nx_c, nx_start, nx_n);
+    if (threadIdx.x == 0) {
+      const uint64_t a0 = nx_start & ~3ull, a1 = (nx_start + nx_n + 3) & ~3ull;
+      const uint32_t bytes = (uint32_t)(a1 - a0) * 4;
+      mbar_arrive_expect_tx(&s_bar[b], bytes);
+      bulk_g2s(s_buf + b * CHP, rin + a0, bytes, &s_bar[b]);
+    }
   };
 
   uint32_t g = blockIdx.x;
+  uint32_t phase[2] = {0, 0};
   if (g < nchunks) issue(g, 0);
   for (int it = 0; g < nchunks; ++it, g += gridDim.x) {
     const int b = it & 1;
     const uint32_t gn = g + gridDim.x;
+    const uint32_t c = nx_c, n = nx_n;
+    const uint64_t start = nx_start;
+    const uint32_t off = (uint32_t)(start & 3);
     if (gn < nchunks) {
+      // buffer b^1 was last stored from two iterations ago: its bulk store must have read it
+      if (threadIdx.x == 0) bulk_wait_read<0>();
+      __syncthreads();
       issue(gn, b ^ 1);
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
     }
-    uint32_t c;
-    uint64_t start;
-    uint32_t n;
-    chunk_range(g, c, start, n);
     for (int i = threadIdx.x; i < W * Db; i += T) s_cnt[i] = 0;
-    // source-high boundaries covering this chunk (all threads, one round trip):
-    // h0 = #{h >= 1 : row[h] <= start}; boundaries inside (start, start+n)
     if (threadIdx.x == 0) {
       s_h0 = 0;
       s_nbnd = 0;
     }
     __syncthreads();
-    {
+    {  // source-high boundaries covering this chunk (overlaps the bulk load)
       const uint64_t* row = dc.seg_hi + (uint64_t)c * (dc.nh + 1);
       uint32_t below = 0;
       for (uint32_t h = 1 + threadIdx.x; h <= dc.nh; h += T) {
@@ -1079,8 +1090,10 @@ __global__ void __launch_bounds__(kB1cWarps * 32) k_b1c(const uint32_t* __restri
       below = __reduce_add_sync(kFull, below);
       if (lane == 0 && below) atomicAdd(&s_h0, below);
     }
+    mbar_wait_parity(&s_bar[b], phase[b]);
+    phase[b] ^= 1;
     __syncthreads();
-    const uint32_t* buf = s_buf + b * CH;
+    uint32_t* buf = s_buf + b * CHP + off;
 #pragma unroll
     for (int s = 0; s < K; ++s) {
       const uint32_t i = seg0 + s * 32 + lane;
@@ -1089,31 +1102,56 @@ __global__ void __launch_bounds__(kB1cWarps * 32) k_b1c(const uint32_t* __restri
     __syncthreads();
     warp_counts_to_bases<W>(s_cnt, Db, s_dstart, s_dtot, s_tmp);
     const uint32_t h0 = s_h0, nbnd = min(s_nbnd, (uint32_t)kMaxBnd);
+    // lane q holds boundary q as an index relative to the chunk start
+    const uint32_t my_b = (lane < nbnd) ? (uint32_t)(s_bnd[lane] - start) : 0xffffffffu;
     uint32_t rr[K], pp[K];
 #pragma unroll
     for (int s = 0; s < K; ++s) {
-      const uint32_t i = seg0 + s * 32 + lane;
+      const uint32_t i0 = seg0 + s * 32;
+      const uint32_t i = i0 + lane;
       const bool valid = i < n;
       const uint32_t r = valid ? buf[i] : 0u;
       uint32_t h = h0;
-      const uint64_t p = start + i;
-      for (uint32_t q = 0; q < nbnd; ++q) h += (s_bnd[q] <= p) ? 1u : 0u;
+      if (nbnd) {  // source-high of record i = h0 + #{boundaries <= i}
+        h += __popc(__ballot_sync(kFull, my_b <= i0));
+        uint32_t inslot = __ballot_sync(kFull, my_b > i0 && my_b <= i0 + 31);
+        while (inslot) {
+          const int q = __ffs(inslot) - 1;
+          inslot &= inslot - 1;
+          h += (__shfl_sync(kFull, my_b, q) <= i) ? 1u : 0u;
+        }
+        if (nbnd > 32)
+          for (uint32_t q = 32; q < nbnd; ++q) h += ((uint32_t)(s_bnd[q] - start) <= i) ? 1u : 0u;
+      }
       const uint32_t src = (h << dc.L) | (r & dc.src_mask);
       const uint32_t lv = (r >> dc.L) & gmask;  // (fine & (G-1)) << c | d
       rr[s] = (lv << dc.nb) | src;
       pp[s] = warp_rank<kMode>(cnt_w, scr_w, (r >> shift_f) & mask_f, valid);
     }
-    __syncthreads();
-    uint32_t* wbuf = s_buf + b * CH;
+    __syncthreads();  // every record of the chunk is in registers: stage in place
 #pragma unroll
     for (int s = 0; s < K; ++s)
-      if (seg0 + s * 32 + lane < n) wbuf[pp[s]] = rr[s];
+      if (seg0 + s * 32 + lane < n) buf[pp[s]] = rr[s];
+    fence_proxy_async_smem();
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < n; i += T) rout[start + i] = wbuf[i];
+    {  // write-out: aligned middle by one bulk store, head/tail records by plain stores
+      const uint64_t a = (start + 3) & ~3ull, e = (start + n) & ~3ull;
+      if (a < e) {
+        if (threadIdx.x == 0) {
+          bulk_s2g(rout + a, buf + (a - start), (uint32_t)(e - a) * 4);
+          bulk_commit();
+        }
+        for (uint32_t i = threadIdx.x; i < (uint32_t)(a - start); i += T) rout[start + i] = buf[i];
+        for (uint32_t i = (uint32_t)(e - start) + threadIdx.x; i < n; i += T) rout[start + i] = buf[i];
+      } else {
+        for (uint32_t i = threadIdx.x; i < n; i += T) rout[start + i] = buf[i];
+      }
+    }
     uint16_t* so = segoff + (uint64_t)g * (Db + 1);
     for (int f = threadIdx.x; f < Db; f += T) so[f] = (uint16_t)s_dstart[f];
     if (threadIdx.x == 0) so[Db] = (uint16_t)n;
   }
+  if (threadIdx.x == 0) bulk_wait_read<0>();
 }
 
 // Level 3, compact: fine ranges of a coarse bucket walked as units of one
