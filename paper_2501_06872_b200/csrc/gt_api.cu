@@ -62,7 +62,7 @@ struct Plan {
   uint64_t CT = 65536, ntiles = 0, nplace = 0, max_chunks = 0, max_items_s = 0, max_items_b = 0;
   // workspace offsets
   uint64_t o_rec, o_tcnt, o_tbase, o_psrc, o_cstart, o_cfirst, o_cbucket, o_segoff, o_fsize, o_fbase, o_ranges,
-      o_status, o_ctr, o_counters, o_err, o_seghi, o_prev, total;
+      o_status, o_ctr, o_counters, o_err, o_seghi, o_prev, o_cinfo, total;
 };
 
 int make_plan(uint64_t V, uint64_t E, Plan& p, uint64_t Vsrc = 0) {
@@ -156,6 +156,7 @@ int make_plan(uint64_t V, uint64_t E, Plan& p, uint64_t Vsrc = 0) {
   p.o_err = take(4);
   p.o_seghi = take(p.compact ? (uint64_t)p.D1 * ((1ull << p.nsh) + 1) * 8 : 0);
   p.o_prev = take(p.compact ? (p.ntiles + 1) * 4 : 0);
+  p.o_cinfo = take(p.compact ? p.max_chunks * sizeof(ChunkInfo) : 0);
   p.total = off;
   return GT_OK;
 }
@@ -508,7 +509,11 @@ int transpose_core_c(const Plan& p, In in, uint64_t* t_offsets, uint32_t* t_edge
   GT_LAUNCH_CHECK();
   k_chunk_map<<<p.D1, 128, 0, st>>>(cfirst, p.D1, cbucket);
   GT_LAUNCH_CHECK();
-  launches += 5;
+  ChunkInfo* cinfo = reinterpret_cast<ChunkInfo*>(ws + p.o_cinfo);
+  k_chunk_info<<<(unsigned)std::min<uint64_t>(4096, (p.max_chunks + 7) / 8), 256, 0, st>>>(cstart, cfirst, p.D1,
+                                                                                             cbucket, seghi, nh, cinfo);
+  GT_LAUNCH_CHECK();
+  launches += 6;
   if ((rc = tm.mark())) return rc;
   {
     DecodeC dc;
@@ -522,8 +527,22 @@ int transpose_core_c(const Plan& p, In in, uint64_t* t_offsets, uint32_t* t_edge
     const size_t sm = smem_b1c(p.Db, kMode);
     if ((rc = set_smem(k_b1c<kMode>, sm))) return rc;
     const unsigned grid = persistent_grid(k_b1c<kMode>, kB1cWarps * 32, sm, p.max_chunks);
-    k_b1c<kMode><<<grid, kB1cWarps * 32, sm, st>>>(rec, rec, cstart, cfirst, cbucket, p.D1, dc, p.Db, segoff);
+    unsigned long long* bprof = nullptr;
+    if (getenv("GT_FPROF")) {
+      GT_CUDA(cudaMallocAsync(&bprof, 64, st));
+      GT_CUDA(cudaMemsetAsync(bprof, 0, 64, st));
+    }
+    k_b1c<kMode><<<grid, kB1cWarps * 32, sm, st>>>(rec, rec, cinfo, cfirst, p.D1, dc, p.Db, segoff, bprof);
     GT_LAUNCH_CHECK();
+    if (bprof) {
+      unsigned long long h[8];
+      GT_CUDA(cudaMemcpyAsync(h, bprof, 64, cudaMemcpyDeviceToHost, st));
+      GT_CUDA(cudaStreamSynchronize(st));
+      fprintf(stderr, "[gt_bprof] grid=%u issue=%.3g prep=%.3g wait=%.3g pass1=%.3g bases=%.3g stage=%.3g write=%.3g loop=%.3g\n",
+              grid, (double)h[0], (double)h[1], (double)h[2], (double)h[3], (double)h[4], (double)h[5], (double)h[6],
+              (double)h[7]);
+      cudaFreeAsync(bprof, st);
+    }
     ++launches;
   }
   if ((rc = tm.mark())) return rc;

@@ -53,6 +53,22 @@ constexpr int kFCapC = kFcWarps * kFcSlots * 32;  // 8192 records per final unit
 constexpr int kSegCapC = 512;
 constexpr int kMaxBnd = 64;
 
+// Per-chunk descriptor for level 2 (compact): record range, coarse bucket, and
+// the source-high decode state (h0 = source-high of the first record, up to
+// kChunkBnd boundary offsets inside the chunk; nbnd > kChunkBnd means "read
+// the seg_hi row").  Built once by k_chunk_info so level 2 issues no dependent
+// global loads per chunk.
+constexpr int kChunkBnd = 10;
+struct __align__(16) ChunkInfo {
+  uint64_t start;
+  uint32_t n;
+  uint32_t c;
+  uint32_t h0;
+  uint32_t nbnd;
+  uint16_t bnd[kChunkBnd];  // boundary offsets relative to start (< kChunkC)
+};
+static_assert(sizeof(ChunkInfo) == 48, "ChunkInfo layout");
+
 // ------------------------------------------------------------ small kernels
 __global__ void k_set_u64(uint64_t* p, uint64_t v) { *p = v; }
 
@@ -270,7 +286,7 @@ __global__ void __launch_bounds__(kL1Warps * 32) k_l1_place(In in, Dig dig, uint
     }
     for (int i = threadIdx.x; i < W * D; i += T) s_cnt[i] = 0;
     __syncthreads();
-    uint32_t r_src[K], r_dst[K];
+    uint32_t r_src[K], r_dst[K], r_rank[K];
     if constexpr (!In::kRecords) {
       // owners: mark every source boundary inside the place tile (window in smem;
       // the rare overflow beyond kWinCap is read directly)
@@ -312,8 +328,10 @@ __global__ void __launch_bounds__(kL1Warps * 32) k_l1_place(In in, Dig dig, uint
         r_src[s] = max(m, cin);
       }
 #pragma unroll
-      for (int s = 0; s < K; ++s)
-        if (seg0 + s * 32 + lane < n) smem_inc(&cnt_w[dig(r_dst[s])]);
+      for (int s = 0; s < K; ++s) {
+        const bool valid = seg0 + s * 32 + lane < n;
+        r_rank[s] = warp_rank<kMode>(cnt_w, scr_w, valid ? dig(r_dst[s]) : 0u, valid);
+      }
     } else {
       const uint2* rbuf = reinterpret_cast<const uint2*>(s_in) + b * PT;
 #pragma unroll
@@ -324,10 +342,10 @@ __global__ void __launch_bounds__(kL1Warps * 32) k_l1_place(In in, Dig dig, uint
         if (valid) {
           r = rbuf[i];
           r.y -= in.dst_base;
-          smem_inc(&cnt_w[dig(r.y)]);
         }
         r_src[s] = r.x;
         r_dst[s] = r.y;
+        r_rank[s] = warp_rank<kMode>(cnt_w, scr_w, valid ? dig(r.y) : 0u, valid);
       }
     }
     if constexpr (Out::kCompact) {
@@ -362,7 +380,7 @@ __global__ void __launch_bounds__(kL1Warps * 32) k_l1_place(In in, Dig dig, uint
       const uint32_t i = seg0 + s * 32 + lane;
       const bool valid = i < n;
       const uint32_t d = valid ? dig(r_dst[s]) : 0u;
-      const uint32_t pos = warp_rank<kMode>(cnt_w, scr_w, d, valid);
+      const uint32_t pos = valid ? cnt_w[d] + r_rank[s] : 0u;  // base of (warp, digit) + warp-local rank
       if (valid) {
         if constexpr (Out::kCompact) {
           s_stage[pos] = ((r_dst[s] & out.low_mask) << out.L) | (r_src[s] & out.src_mask);
@@ -426,6 +444,46 @@ __global__ void k_coarse_info_c(const uint64_t* __restrict__ tbase, uint64_t nti
   const uint32_t total = block_excl_scan_u32(s_nch, D1, s_tmp);
   for (int c = threadIdx.x; c < D1; c += blockDim.x) chunk_first[c] = s_nch[c];
   if (threadIdx.x == 0) chunk_first[D1] = total;
+}
+
+// Per-chunk descriptors for the compact level 2 (one warp per chunk).
+__global__ void k_chunk_info(const uint64_t* __restrict__ cstart, const uint32_t* __restrict__ chunk_first, int D1,
+                             const uint32_t* __restrict__ chunk_bucket, const uint64_t* __restrict__ seg_hi,
+                             uint32_t nh, ChunkInfo* __restrict__ info) {
+  const uint32_t nchunks = chunk_first[D1];
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < nchunks; g += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t c = chunk_bucket[g];
+    const uint64_t start = cstart[c] + (uint64_t)(g - chunk_first[c]) * kChunkC;
+    const uint32_t n = (uint32_t)umin64(kChunkC, cstart[c + 1] - start);
+    const uint64_t* row = seg_hi + (uint64_t)c * (nh + 1);
+    uint32_t below = 0, inside = 0;
+    uint16_t mine[kChunkBnd];
+    for (uint32_t h0 = 1; h0 <= nh; h0 += 32) {  // ordered scan: boundaries in increasing h
+      const uint32_t h = h0 + lane;
+      const uint64_t v = (h <= nh) ? row[h] : ~0ull;
+      below += __popc(__ballot_sync(kFull, v <= start));
+      const uint32_t in = __ballot_sync(kFull, v > start && v < start + n);
+      uint32_t m = in;
+      while (m) {
+        const int q = __ffs(m) - 1;
+        m &= m - 1;
+        const uint64_t bv = __shfl_sync(kFull, v, q);
+        if (inside < (uint32_t)kChunkBnd) mine[inside] = (uint16_t)(bv - start);
+        ++inside;
+      }
+    }
+    if (lane == 0) {
+      ChunkInfo ci;
+      ci.start = start;
+      ci.n = n;
+      ci.c = c;
+      ci.h0 = below;
+      ci.nbnd = inside;
+      for (int k = 0; k < kChunkBnd; ++k) ci.bnd[k] = (k < (int)inside) ? mine[k] : (uint16_t)0xffff;
+      info[g] = ci;
+    }
+  }
 }
 
 // chunk -> coarse bucket map.
@@ -1007,11 +1065,24 @@ struct DecodeC {
 // records by plain stores).  Needs 3 records of readable padding after rin.
 template <int kMode>
 __global__ void __launch_bounds__(kB1cWarps * 32) k_b1c(const uint32_t* __restrict__ rin, uint32_t* __restrict__ rout,
-                                                       const uint64_t* __restrict__ cstart,
-                                                       const uint32_t* __restrict__ chunk_first,
-                                                       const uint32_t* __restrict__ chunk_bucket, int D1, DecodeC dc,
-                                                       int Db, uint16_t* __restrict__ segoff) {
+                                                       const ChunkInfo* __restrict__ cinfo,
+                                                       const uint32_t* __restrict__ chunk_first, int D1, DecodeC dc,
+                                                       int Db, uint16_t* __restrict__ segoff,
+                                                       unsigned long long* __restrict__ prof) {
   constexpr int W = kB1cWarps, K = kB1cSlots, T = W * 32, CH = kChunkC, CHP = kChunkC + 8;
+  __shared__ unsigned long long pacc[8];
+  __shared__ long long tprev;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 8; ++i) pacc[i] = 0;
+    tprev = clock64();
+  }
+  auto ptick = [&](int ph) {
+    if (prof && threadIdx.x == 0) {
+      const long long tn = clock64();
+      pacc[ph] += (unsigned long long)(tn - tprev);
+      tprev = tn;
+    }
+  };
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem_raw);  // 2 * CHP
   uint32_t* s_cnt = s_buf + 2 * CHP;                        // W * Db
@@ -1038,17 +1109,13 @@ __global__ void __launch_bounds__(kB1cWarps * 32) k_b1c(const uint32_t* __restri
   }
   __syncthreads();
 
-  auto chunk_range = [&](uint32_t g, uint32_t& c, uint64_t& start, uint32_t& n) {
-    c = chunk_bucket[g];
-    start = cstart[c] + (uint64_t)(g - chunk_first[c]) * CH;
-    n = (uint32_t)umin64(CH, cstart[c + 1] - start);
-  };
-  uint32_t nx_c = 0, nx_n = 0;
-  uint64_t nx_start = 0;
-  auto issue = [&](uint32_t g, int b) {  // all threads compute the range; thread 0 issues the bulk load
-    chunk_range(g, nx_c, nx_start, nx_n);
+  // chunk g's descriptor comes from `cinfo` (built by k_chunk_info); the next
+  // chunk's descriptor is read one iteration ahead (plain loads, used a whole
+  // iteration later) so no global round trip is exposed
+  ChunkInfo nx = cinfo[min(blockIdx.x, nchunks ? nchunks - 1 : 0)];
+  auto issue = [&](const ChunkInfo& ci, int b) {  // thread 0 issues the bulk load
     if (threadIdx.x == 0) {
-      const uint64_t a0 = nx_start & ~3ull, a1 = (nx_start + nx_n + 3) & ~3ull;
+      const uint64_t a0 = ci.start & ~3ull, a1 = (ci.start + ci.n + 3) & ~3ull;
       const uint32_t bytes = (uint32_t)(a1 - a0) * 4;
       mbar_arrive_expect_tx(&s_bar[b], bytes);
       bulk_g2s(s_buf + b * CHP, rin + a0, bytes, &s_bar[b]);
@@ -1057,54 +1124,54 @@ __global__ void __launch_bounds__(kB1cWarps * 32) k_b1c(const uint32_t* __restri
 
   uint32_t g = blockIdx.x;
   uint32_t phase[2] = {0, 0};
-  if (g < nchunks) issue(g, 0);
+  if (g < nchunks) issue(nx, 0);
   for (int it = 0; g < nchunks; ++it, g += gridDim.x) {
     const int b = it & 1;
     const uint32_t gn = g + gridDim.x;
-    const uint32_t c = nx_c, n = nx_n;
-    const uint64_t start = nx_start;
+    const ChunkInfo cur = nx;
+    const uint32_t c = cur.c, n = cur.n;
+    const uint64_t start = cur.start;
     const uint32_t off = (uint32_t)(start & 3);
+    ptick(7);
     if (gn < nchunks) {
+      nx = cinfo[gn];
       // buffer b^1 was last stored from two iterations ago: its bulk store must have read it
       if (threadIdx.x == 0) bulk_wait_read<0>();
       __syncthreads();
-      issue(gn, b ^ 1);
+      issue(nx, b ^ 1);
     }
+    ptick(0);
     for (int i = threadIdx.x; i < W * Db; i += T) s_cnt[i] = 0;
-    if (threadIdx.x == 0) {
-      s_h0 = 0;
-      s_nbnd = 0;
-    }
-    __syncthreads();
-    {  // source-high boundaries covering this chunk (overlaps the bulk load)
+    if (cur.nbnd > (uint32_t)kChunkBnd) {  // many source-high boundaries: read the row
+      if (threadIdx.x == 0) {
+        s_h0 = 0;
+        s_nbnd = 0;
+      }
+      __syncthreads();
       const uint64_t* row = dc.seg_hi + (uint64_t)c * (dc.nh + 1);
-      uint32_t below = 0;
       for (uint32_t h = 1 + threadIdx.x; h <= dc.nh; h += T) {
         const uint64_t v = row[h];
-        if (v <= start) ++below;
-        else if (v < start + n) {
+        if (v > start && v < start + n) {
           const uint32_t k = atomicAdd(&s_nbnd, 1u);
           if (k < (uint32_t)kMaxBnd) s_bnd[k] = v;
         }
       }
-      below = __reduce_add_sync(kFull, below);
-      if (lane == 0 && below) atomicAdd(&s_h0, below);
+    } else if (threadIdx.x < (uint32_t)kChunkBnd) {
+      s_bnd[threadIdx.x] = start + cur.bnd[threadIdx.x];
+      if (threadIdx.x == 0) s_nbnd = cur.nbnd;
     }
+    __syncthreads();
+    ptick(1);
     mbar_wait_parity(&s_bar[b], phase[b]);
     phase[b] ^= 1;
     __syncthreads();
+    ptick(2);
     uint32_t* buf = s_buf + b * CHP + off;
-#pragma unroll
-    for (int s = 0; s < K; ++s) {
-      const uint32_t i = seg0 + s * 32 + lane;
-      if (i < n) smem_inc(&cnt_w[(buf[i] >> shift_f) & mask_f]);
-    }
-    __syncthreads();
-    warp_counts_to_bases<W>(s_cnt, Db, s_dstart, s_dtot, s_tmp);
-    const uint32_t h0 = s_h0, nbnd = min(s_nbnd, (uint32_t)kMaxBnd);
+    const uint32_t h0 = cur.h0, nbnd = min(s_nbnd, (uint32_t)kMaxBnd);
     // lane q holds boundary q as an index relative to the chunk start
     const uint32_t my_b = (lane < nbnd) ? (uint32_t)(s_bnd[lane] - start) : 0xffffffffu;
-    uint32_t rr[K], pp[K];
+    // single pass: decode, warp-local rank (per-warp counters start at 0)
+    uint32_t rr[K], pk[K];
 #pragma unroll
     for (int s = 0; s < K; ++s) {
       const uint32_t i0 = seg0 + s * 32;
@@ -1126,14 +1193,19 @@ __global__ void __launch_bounds__(kB1cWarps * 32) k_b1c(const uint32_t* __restri
       const uint32_t src = (h << dc.L) | (r & dc.src_mask);
       const uint32_t lv = (r >> dc.L) & gmask;  // (fine & (G-1)) << c | d
       rr[s] = (lv << dc.nb) | src;
-      pp[s] = warp_rank<kMode>(cnt_w, scr_w, (r >> shift_f) & mask_f, valid);
+      const uint32_t f = (r >> shift_f) & mask_f;
+      pk[s] = (f << 16) | warp_rank<kMode>(cnt_w, scr_w, f, valid);
     }
-    __syncthreads();  // every record of the chunk is in registers: stage in place
+    __syncthreads();
+    ptick(3);
+    warp_counts_to_bases<W>(s_cnt, Db, s_dstart, s_dtot, s_tmp);  // syncs; all reads of buf are done
+    ptick(4);
 #pragma unroll
     for (int s = 0; s < K; ++s)
-      if (seg0 + s * 32 + lane < n) buf[pp[s]] = rr[s];
+      if (seg0 + s * 32 + lane < n) buf[cnt_w[pk[s] >> 16] + (pk[s] & 0xffffu)] = rr[s];
     fence_proxy_async_smem();
     __syncthreads();
+    ptick(5);
     {  // write-out: aligned middle by one bulk store, head/tail records by plain stores
       const uint64_t a = (start + 3) & ~3ull, e = (start + n) & ~3ull;
       if (a < e) {
@@ -1150,8 +1222,11 @@ __global__ void __launch_bounds__(kB1cWarps * 32) k_b1c(const uint32_t* __restri
     uint16_t* so = segoff + (uint64_t)g * (Db + 1);
     for (int f = threadIdx.x; f < Db; f += T) so[f] = (uint16_t)s_dstart[f];
     if (threadIdx.x == 0) so[Db] = (uint16_t)n;
+    ptick(6);
   }
   if (threadIdx.x == 0) bulk_wait_read<0>();
+  if (prof && threadIdx.x == 0)
+    for (int i = 0; i < 8; ++i) atomicAdd(&prof[i], pacc[i]);
 }
 
 // Level 3, compact: fine ranges of a coarse bucket walked as units of one
@@ -1434,10 +1509,15 @@ __global__ void __launch_bounds__(kFcWarps * 32, 2) k_final_c(FineCtxC x, const 
         __syncthreads();
       }
     } else {
+      // single pass: warp-local rank (per-warp counters start at 0), then bases
+      uint32_t rr[K], pk[K];
 #pragma unroll
       for (int s = 0; s < K; ++s) {
         const uint32_t i = seg0 + s * 32 + lane;
-        if (i < n) smem_inc(&cnt_w[lv_of(buf[i])]);
+        const bool valid = i < n;
+        rr[s] = valid ? buf[i] : 0u;
+        const uint32_t lv = valid ? lv_of(rr[s]) : 0u;
+        pk[s] = (lv << 16) | warp_rank<kMode>(cnt_w, scr_w, lv, valid);
       }
       __syncthreads();
       ptick(3);
@@ -1448,18 +1528,9 @@ __global__ void __launch_bounds__(kFcWarps * 32, 2) k_final_c(FineCtxC x, const 
         for (uint32_t v = threadIdx.x; v < nloc; v += T)
           if (v0 + v < x.V) t_offsets[v0 + v] = u.base + s_dstart[v];
       }
-      uint32_t rr[K], pp[K];
-#pragma unroll
-      for (int s = 0; s < K; ++s) {
-        const uint32_t i = seg0 + s * 32 + lane;
-        const bool valid = i < n;
-        rr[s] = valid ? buf[i] : 0u;
-        pp[s] = warp_rank<kMode>(cnt_w, scr_w, valid ? lv_of(rr[s]) : 0u, valid);
-      }
-      __syncthreads();
 #pragma unroll
       for (int s = 0; s < K; ++s)
-        if (seg0 + s * 32 + lane < n) buf[pp[s]] = rr[s];
+        if (seg0 + s * 32 + lane < n) buf[cnt_w[pk[s] >> 16] + (pk[s] & 0xffffu)] = rr[s];
       __syncthreads();
       ptick(5);
       if (u.kind == 0) {
