@@ -246,7 +246,7 @@ size_t smem_final_c(int mode) {
   const int W = kFcWarps, ML = kFMaxLocal;
   return (size_t)2 * kFCapC * 4 + (size_t)kSegCapC * 8 + (size_t)(kSegCapC + 4) * 4 + (size_t)W * ML * 4 +
          (mode == kRankSafe ? (size_t)W * ML * 4 : 0) + (size_t)ML * 8 + 40 * 4 + (size_t)ML * 8 + (size_t)ML * 4 +
-         (size_t)kMaxRange * 12 + 64;
+         (size_t)kMaxRange * 12 + (size_t)kTabCap * 2 + 64;
 }
 size_t smem_b1(const Plan& p, int mode) {
   const int W = kB1Warps, D = p.Db;
@@ -405,6 +405,8 @@ int transpose_core(const Plan& p, In in, uint64_t* t_offsets, uint32_t* t_edges,
         1u << 20, std::max<uint64_t>(4 * kFCap, E / ((uint64_t)num_sms() * 2 * 6)));
     k_f_plan<<<p.D1, 256, 2 * p.Db * 4, st>>>(fx, target, fsize, fbase, ranges, n_ranges, t_offsets, err);
     GT_LAUNCH_CHECK();
+    k_range_sort<<<1, 1024, 0, st>>>(ranges, n_ranges);
+    GT_LAUNCH_CHECK();
     const size_t sm = smem_final(kMode);
     if ((rc = set_smem(k_final<kMode>, sm))) return rc;
     const unsigned gf = persistent_grid(k_final<kMode>, kFWarps * 32, sm, (uint64_t)p.D1 * p.Db);
@@ -428,7 +430,7 @@ int transpose_core(const Plan& p, In in, uint64_t* t_offsets, uint32_t* t_edges,
   }
   k_set_u64<<<1, 1, 0, st>>>(t_offsets + V, E);
   GT_LAUNCH_CHECK();
-  launches += 3;
+  launches += 4;
   if ((rc = tm.mark())) return rc;
   uint32_t h_cnt[3] = {0, 0, 0};
   unsigned int h_err = 0;
@@ -560,6 +562,8 @@ int transpose_core_c(const Plan& p, In in, uint64_t* t_offsets, uint32_t* t_edge
         1u << 20, std::max<uint64_t>(4 * kFCapC, E / ((uint64_t)num_sms() * 2 * 6)));
     k_f_plan<<<p.D1, 256, 2 * p.Db * 4, st>>>(fx, target, fsize, fbase, ranges, n_ranges, t_offsets, err);
     GT_LAUNCH_CHECK();
+    k_range_sort<<<1, 1024, 0, st>>>(ranges, n_ranges);
+    GT_LAUNCH_CHECK();
     FineCtxC xc;
     xc.rec = rec;
     xc.cstart = cstart;
@@ -572,8 +576,8 @@ int transpose_core_c(const Plan& p, In in, uint64_t* t_offsets, uint32_t* t_edge
     xc.V = V;
     unsigned long long* prof = nullptr;
     if (getenv("GT_FPROF")) {
-      GT_CUDA(cudaMallocAsync(&prof, 10 * 8, st));
-      GT_CUDA(cudaMemsetAsync(prof, 0, 10 * 8, st));
+      GT_CUDA(cudaMallocAsync(&prof, 14 * 8, st));
+      GT_CUDA(cudaMemsetAsync(prof, 0, 14 * 8, st));
     }
     const size_t sm = smem_final_c(kMode);
     if ((rc = set_smem(k_final_c<kMode>, sm))) return rc;
@@ -582,20 +586,20 @@ int transpose_core_c(const Plan& p, In in, uint64_t* t_offsets, uint32_t* t_edge
                                                     prof);
     GT_LAUNCH_CHECK();
     if (prof) {
-      unsigned long long h[10];
-      GT_CUDA(cudaMemcpyAsync(h, prof, 80, cudaMemcpyDeviceToHost, st));
+      unsigned long long h[14];
+      GT_CUDA(cudaMemcpyAsync(h, prof, 14 * 8, cudaMemcpyDeviceToHost, st));
       GT_CUDA(cudaStreamSynchronize(st));
       fprintf(stderr,
-              "[gt_fprof-c] grid=%u gen=%.3g issue=%.3g wait=%.3g count=%.3g bases=%.3g rank=%.3g write=%.3g "
-              "loop=%.3g units0=%llu units12=%llu\\n",
-              gf, (double)h[0], (double)h[1], (double)h[2], (double)h[3], (double)h[4], (double)h[5], (double)h[6],
-              (double)h[9], h[7], h[8]);
+              "[gt_fprof-c] grid=%u gen=%.3g issue=%.3g (table=%.3g copy=%.3g) wait=%.3g count=%.3g bases=%.3g "
+              "rank=%.3g write=%.3g (bigcount=%.3g) loop=%.3g units0=%llu units12=%llu cta_max=%.3g\n",
+              gf, (double)h[0], (double)h[1], (double)h[10], (double)h[11], (double)h[2], (double)h[3], (double)h[4],
+              (double)h[5], (double)h[6], (double)h[12], (double)h[9], h[7], h[8], (double)h[13]);
       cudaFreeAsync(prof, st);
     }
   }
   k_set_u64<<<1, 1, 0, st>>>(t_offsets + V, E);
   GT_LAUNCH_CHECK();
-  launches += 3;
+  launches += 4;
   if ((rc = tm.mark())) return rc;
   uint32_t h_cnt[3] = {0, 0, 0};
   unsigned int h_err = 0;

@@ -51,6 +51,7 @@ constexpr int kFcWarps = 8;
 constexpr int kFcSlots = 32;
 constexpr int kFCapC = kFcWarps * kFcSlots * 32;  // 8192 records per final unit
 constexpr int kSegCapC = 512;
+constexpr int kTabCap = 8192;  // u16 entries of a fine range's per-chunk segment table in shared memory
 constexpr int kMaxBnd = 64;
 
 // Per-chunk descriptor for level 2 (compact): record range, coarse bucket, and
@@ -1028,18 +1029,65 @@ __global__ void k_f_plan(FineCtx x, uint32_t target, uint32_t* __restrict__ fine
   if (threadIdx.x != 0 || nc == 0) return;
   uint64_t acc = 0;
   uint32_t f0 = 0;
+  // ranges narrow enough for their segment table (nch x (width+1) u16) to sit in shared memory
+  const uint32_t nch = g1 - g0;
+  const uint32_t wcap = (nch * 2 <= (uint32_t)kTabCap) ? min((uint32_t)kMaxRange, (uint32_t)kTabCap / nch - 1)
+                                                       : (uint32_t)kMaxRange;
   for (uint32_t f = 0; f < (uint32_t)Db; ++f) {
     acc += s_sz[f];
-    if (acc >= target || f + 1 == (uint32_t)Db || f + 1 - f0 >= (uint32_t)kMaxRange) {
+    if (acc >= target || f + 1 == (uint32_t)Db || f + 1 - f0 >= wcap) {
       FRange r;
       r.c = c;
       r.f0 = f0;
       r.f1 = f + 1;
-      r.prio = 0;
+      r.prio = (uint32_t)umin64(acc, 0xffffffffull);  // records in the range
       ranges[atomicAdd(n_ranges, 1u)] = r;
       f0 = f + 1;
       acc = 0;
     }
+  }
+}
+
+// Order the fine ranges largest first (longest-processing-time-first), so the
+// ranges holding the heaviest vertices start early instead of forming the tail.
+// One CTA, bitonic sort of (size desc, index) keys; lists longer than
+// kRangeSortCap keep their order (scheduling only, results do not depend on it).
+constexpr int kRangeSortCap = 4096;
+__global__ void __launch_bounds__(1024) k_range_sort(FRange* __restrict__ ranges, const uint32_t* __restrict__ n_ranges) {
+  __shared__ unsigned long long key[kRangeSortCap];
+  const uint32_t n = *n_ranges;
+  if (n < 2 || n > (uint32_t)kRangeSortCap) return;
+  uint32_t np = 1;
+  while (np < n) np <<= 1;
+  for (uint32_t i = threadIdx.x; i < np; i += blockDim.x)
+    key[i] = (i < n) ? (((unsigned long long)(~ranges[i].prio) << 32) | i) : ~0ull;
+  __syncthreads();
+  for (uint32_t k = 2; k <= np; k <<= 1)
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = threadIdx.x; i < np; i += blockDim.x) {
+        const uint32_t l = i ^ j;
+        if (l > i) {
+          const unsigned long long a = key[i], b = key[l];
+          const bool up = (i & k) == 0;
+          if ((a > b) == up) {
+            key[i] = b;
+            key[l] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  FRange tmp[kRangeSortCap / 1024];
+#pragma unroll
+  for (int t = 0; t < kRangeSortCap / 1024; ++t) {
+    const uint32_t i = threadIdx.x + t * 1024;
+    if (i < n) tmp[t] = ranges[(uint32_t)key[i]];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int t = 0; t < kRangeSortCap / 1024; ++t) {
+    const uint32_t i = threadIdx.x + t * 1024;
+    if (i < n) ranges[i] = tmp[t];
   }
 }
 
@@ -1250,7 +1298,9 @@ struct FineCtxC {
 __device__ __forceinline__ void gather_unit_c(const FineCtxC& x, const CoarseInfo& ci, uint32_t f, uint32_t f_end,
                                               uint32_t n, uint32_t g, uint32_t skip, uint32_t* dst, uint64_t* s_st,
                                               uint32_t* s_pos, uint32_t* s_tmp, uint32_t& g_out,
-                                              uint32_t& skip_out) {
+                                              uint32_t& skip_out, const uint16_t* tab, uint32_t tw1, uint32_t tf0,
+                                              unsigned long long* pa = nullptr) {
+  long long t0 = (pa && threadIdx.x == 0) ? clock64() : 0;
   const uint32_t lane = lane_id(), w = warp_id(), nw = blockDim.x >> 5;
   uint32_t got = 0;
   g_out = g;
@@ -1259,9 +1309,17 @@ __device__ __forceinline__ void gather_unit_c(const FineCtxC& x, const CoarseInf
   while (gb < ci.g_end && got < n) {
     const int nch = (int)min((uint32_t)kSegCapC, ci.g_end - gb);
     for (int j = threadIdx.x; j < nch; j += blockDim.x) {
-      const uint64_t cpos = ci.cs + (uint64_t)(gb + j - ci.g_first) * kChunkC;
-      const uint16_t* so = x.segoff + (uint64_t)(gb + j) * (x.Db + 1);
-      const uint32_t a = so[f], e = so[f_end];
+      const uint32_t jr = gb + j - ci.g_first;
+      const uint64_t cpos = ci.cs + (uint64_t)jr * kChunkC;
+      uint32_t a, e;
+      if (tab) {  // range table in shared memory
+        a = tab[jr * tw1 + (f - tf0)];
+        e = tab[jr * tw1 + (f_end - tf0)];
+      } else {
+        const uint16_t* so = x.segoff + (uint64_t)(gb + j) * (x.Db + 1);
+        a = so[f];
+        e = so[f_end];
+      }
       s_st[j] = cpos + a;
       s_pos[j] = e - a;
     }
@@ -1269,6 +1327,11 @@ __device__ __forceinline__ void gather_unit_c(const FineCtxC& x, const CoarseInf
     const uint32_t tot = block_excl_scan_u32(s_pos, nch, s_tmp);
     if (threadIdx.x == 0) s_pos[nch] = tot;
     __syncthreads();
+    if (pa && threadIdx.x == 0) {
+      const long long t1 = clock64();
+      pa[10] += (unsigned long long)(t1 - t0);
+      t0 = t1;
+    }
     const uint32_t lo = skip, want = n - got;
     const uint32_t hi = (tot > lo) ? min(tot, lo + want) : lo;
     for (int j = w; j < nch; j += nw) {
@@ -1277,6 +1340,11 @@ __device__ __forceinline__ void gather_unit_c(const FineCtxC& x, const CoarseInf
       const uint64_t src = s_st[j] + (a - s_pos[j]);
       uint32_t* d = dst + got + (a - lo);
       for (uint32_t q = lane; q < e - a; q += 32) cp_async4(d + q, x.rec + src + q);
+    }
+    if (pa && threadIdx.x == 0) {
+      const long long t1 = clock64();
+      pa[11] += (unsigned long long)(t1 - t0);
+      t0 = t1;
     }
     if (hi > lo) {
       got += hi - lo;
@@ -1323,7 +1391,14 @@ __global__ void __launch_bounds__(kFcWarps * 32, 2) k_final_c(FineCtxC x, const 
   uint32_t* s_bcnt = reinterpret_cast<uint32_t*>(s_cur + ML);           // ML
   uint32_t* s_rsz = s_bcnt + ML;                                        // kMaxRange
   uint64_t* s_rbase = reinterpret_cast<uint64_t*>(s_rsz + kMaxRange);   // kMaxRange
+  uint16_t* s_tab = reinterpret_cast<uint16_t*>(s_rbase + kMaxRange);   // kTabCap
   __shared__ uint32_t s_range;
+  __shared__ unsigned long long pacc[14];  // profiling accumulators (thread 0)
+  __shared__ long long tprev, tstart;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 14; ++i) pacc[i] = 0;
+    tprev = tstart = clock64();
+  }
 
   const uint32_t n_ranges = *n_ranges_ptr;
   const uint32_t lane = lane_id(), w = warp_id();
@@ -1338,7 +1413,8 @@ __global__ void __launch_bounds__(kFcWarps * 32, 2) k_final_c(FineCtxC x, const 
     uint32_t c, f, f0, f1;
     uint32_t big_f, big_left, phase, g, skip, big_size;
     uint64_t big_base;
-    bool live;
+    uint32_t tw1;
+    bool live, tab_ok;
     CoarseInfo ci;
   } gen;
   gen.live = false;
@@ -1365,13 +1441,21 @@ __global__ void __launch_bounds__(kFcWarps * 32, 2) k_final_c(FineCtxC x, const 
       s_rsz[i] = fine_size[fb + i];
       s_rbase[i] = fine_base[fb + i];
     }
+    gen.tw1 = R.f1 - R.f0 + 1;
+    const uint32_t nchr = gen.ci.g_end - gen.ci.g_first;
+    gen.tab_ok = (uint64_t)nchr * gen.tw1 <= (uint64_t)kTabCap;
+    if (gen.tab_ok)  // the range's segment offsets for every chunk of the coarse bucket, one coalesced pass
+      for (uint32_t i = threadIdx.x; i < nchr * gen.tw1; i += blockDim.x) {
+        const uint32_t j = i / gen.tw1, t = i - j * gen.tw1;
+        s_tab[i] = x.segoff[(uint64_t)(gen.ci.g_first + j) * (x.Db + 1) + R.f0 + t];
+      }
     __syncthreads();
     return true;
   };
   auto next_unit = [&](FUnit& u) -> bool {
     while (true) {
-      if (gen.big_left) {
-        u.kind = gen.phase;
+      if (gen.big_left) {  // place batches of a big fine bucket
+        u.kind = 2;
         u.f0 = gen.big_f;
         u.f1 = gen.big_f + 1;
         u.n = min((uint32_t)CAP, gen.big_left);
@@ -1380,16 +1464,7 @@ __global__ void __launch_bounds__(kFcWarps * 32, 2) k_final_c(FineCtxC x, const 
         u.base = gen.big_base;
         gen.big_left -= u.n;
         u.last = (gen.big_left == 0);
-        u.first = (gen.phase == 1 && gen.big_left + u.n == gen.big_size);
-        if (gen.big_left == 0 && gen.phase == 1) {
-          gen.phase = 2;
-          gen.big_left = gen.big_size;
-          gen.g = gen.ci.g_first;
-          gen.skip = 0;
-          u.last = 1;
-          return true;
-        }
-        if (gen.big_left == 0) gen.phase = 0;
+        u.first = 0;
         return true;
       }
       if (!gen.live || gen.f >= gen.f1) {
@@ -1398,16 +1473,24 @@ __global__ void __launch_bounds__(kFcWarps * 32, 2) k_final_c(FineCtxC x, const 
       }
       const uint32_t sz = s_rsz[gen.f - gen.f0];
       if (sz == 0) { ++gen.f; continue; }
-      if (sz > (uint32_t)CAP) {
+      if (sz > (uint32_t)CAP) {  // big fine bucket: a streaming count unit (no gather), then batches
         gen.big_f = gen.f;
         gen.big_size = sz;
         gen.big_left = sz;
         gen.big_base = s_rbase[gen.f - gen.f0];
-        gen.phase = 1;
         gen.g = gen.ci.g_first;
         gen.skip = 0;
         ++gen.f;
-        continue;
+        u.kind = 1;
+        u.f0 = gen.big_f;
+        u.f1 = gen.big_f + 1;
+        u.n = 0;
+        u.g = gen.ci.g_first;
+        u.skip = 0;
+        u.last = 1;
+        u.first = 1;
+        u.base = gen.big_base;
+        return true;
       }
       const uint32_t blk_end = min(gen.f1, (gen.f | (G - 1)) + 1);  // end of the aligned group
       uint32_t total = sz, e = gen.f + 1;
@@ -1432,20 +1515,15 @@ __global__ void __launch_bounds__(kFcWarps * 32, 2) k_final_c(FineCtxC x, const 
   };
   auto issue = [&](const FUnit& u, int b) {
     uint32_t go, so;
-    gather_unit_c(x, gen.ci, u.f0, u.f1, u.n, u.g, u.skip, s_buf + b * CAP, s_st, s_pos, s_tmp, go, so);
-    if (u.kind != 0 && !(u.kind == 1 && u.last)) {
+    gather_unit_c(x, gen.ci, u.f0, u.f1, u.n, u.g, u.skip, s_buf + b * CAP, s_st, s_pos, s_tmp, go, so,
+                  gen.tab_ok ? s_tab : nullptr, gen.tw1, gen.f0, prof ? pacc : nullptr);
+    if (u.kind == 2) {
       gen.g = go;
       gen.skip = so;
     }
     cp_commit();
   };
 
-  __shared__ unsigned long long pacc[10];  // profiling accumulators (thread 0)
-  __shared__ long long tprev;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < 10; ++i) pacc[i] = 0;
-    tprev = clock64();
-  }
   auto ptick = [&](int ph) {
     if (prof && threadIdx.x == 0) {
       const long long tn = clock64();
@@ -1455,14 +1533,17 @@ __global__ void __launch_bounds__(kFcWarps * 32, 2) k_final_c(FineCtxC x, const 
   };
   FUnit u0, u1;
   uint32_t c0 = 0, c1 = 0;
+  CoarseInfo ci0, ci1;
   if (!next_unit(u0)) return;
   c0 = gen.c;
+  ci0 = gen.ci;
   issue(u0, 0);
   for (int it = 0;; ++it) {
     const int b = it & 1;
     ptick(9);
     const bool more = next_unit(u1);
     c1 = gen.c;
+    ci1 = gen.ci;
     ptick(0);
     if (more) {
       issue(u1, b ^ 1);
@@ -1472,6 +1553,7 @@ __global__ void __launch_bounds__(kFcWarps * 32, 2) k_final_c(FineCtxC x, const 
       cp_wait<0>();
     }
     const uint32_t cur_c = c0;
+    const CoarseInfo cur_ci = ci0;
     const FUnit u = u0;
     const uint32_t n = u.n;
     const uint32_t nloc = (u.f1 - u.f0) << x.bits_c;               // local vertices of the unit
@@ -1480,34 +1562,79 @@ __global__ void __launch_bounds__(kFcWarps * 32, 2) k_final_c(FineCtxC x, const 
     uint32_t* cnt_w = s_cnt + w * nloc;
     uint32_t* scr_w = s_scr + (kMode == kRankSafe ? w * nloc : 0);
     for (int i = threadIdx.x; i < W * ML; i += T) s_cnt[i] = 0;
-    if (u.kind == 1 && u.first)
+    if (u.kind == 1) {
       for (int v = threadIdx.x; v < Dc; v += T) s_bcnt[v] = 0;
+      for (int i = threadIdx.x; i < CAP; i += T) s_buf[b * CAP + i] = 0;
+    }
     __syncthreads();
     ptick(2);
     if (prof && threadIdx.x == 0) pacc[7 + (u.kind == 0 ? 0 : 1)] += 1;
     uint32_t* buf = s_buf + b * CAP;
     const uint32_t seg0 = w * (K * 32);
     if (u.kind == 1) {
+      // Streaming count of the whole big bucket straight from its chunk
+      // segments (16-byte loads) into per-warp counters [lv][lane & 15] in the
+      // idle staging buffer; the adds are fire-and-forget shared atomics (no
+      // read-modify-write chains), folded into s_bcnt at the end.
+      const int cw = min(W, (CAP * 4) / (Dc * 16 * 4));  // counting warps that fit the buffer
+      uint32_t* c32 = buf + w * Dc * 16 + (lane & 15);
+      const long long tk0 = (prof && threadIdx.x == 0) ? clock64() : 0;
+      if (w < cw) {
+        const uint32_t f = u.f0;
+        auto bump = [&](uint32_t r) { atomicAdd(c32 + lv_of(r) * 16, 1u); };
+        for (uint32_t j = cur_ci.g_first + w; j < cur_ci.g_end; j += cw) {
+          const uint32_t jr = j - cur_ci.g_first;
+          uint32_t a, e;
+          if (gen.tab_ok) {
+            a = s_tab[jr * gen.tw1 + (f - gen.f0)];
+            e = s_tab[jr * gen.tw1 + (f + 1 - gen.f0)];
+          } else {
+            const uint16_t* so = x.segoff + (uint64_t)j * (x.Db + 1);
+            a = so[f];
+            e = so[f + 1];
+          }
+          const uint64_t base = cur_ci.cs + (uint64_t)jr * kChunkC;
+          // unaligned head/tail by scalar loads, 16-byte aligned body by uint4
+          const uint64_t ga = base + a, ge = base + e;
+          const uint64_t va = umin64((ga + 3) & ~3ull, ge), ve = (ge & ~3ull) > va ? (ge & ~3ull) : va;
+          if (ga + lane < va) bump(__ldg(x.rec + ga + lane));
+          if (ve + lane < ge) bump(__ldg(x.rec + ve + lane));
+          const uint4* p4 = reinterpret_cast<const uint4*>(x.rec + va);
+          const uint32_t n4 = (uint32_t)((ve - va) >> 2);
+          for (uint32_t q = lane; q < n4; q += 256) {
+            uint4 r[8];
 #pragma unroll
-      for (int s = 0; s < K; ++s) {
-        const uint32_t i = seg0 + s * 32 + lane;
-        if (i < n) smem_inc(&s_bcnt[lv_of(buf[i])]);
-      }
-      __syncthreads();
-      if (u.last) {
-        if (threadIdx.x == 0) {
-          uint64_t run = u.base;
-          for (int v = 0; v < Dc; ++v) {
-            s_cur[v] = run;
-            run += s_bcnt[v];
+            for (int k = 0; k < 8; ++k) r[k] = (q + 32 * k < n4) ? __ldg(p4 + q + 32 * k) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (q + 32 * k < n4) {
+                bump(r[k].x);
+                bump(r[k].y);
+                bump(r[k].z);
+                bump(r[k].w);
+              }
           }
         }
-        __syncthreads();
-        const uint64_t v0 = ((uint64_t)cur_c * x.Db + u.f0) << x.bits_c;
-        for (int v = threadIdx.x; v < Dc; v += T)
-          if (v0 + v < x.V) t_offsets[v0 + v] = s_cur[v];
-        __syncthreads();
+        __syncwarp();
+        for (int v = 0; v < Dc; ++v) {
+          const uint32_t c = (lane < 16) ? c32[v * 16] : 0u;
+          const uint32_t t = __reduce_add_sync(kFull, c);
+          if (lane == 0 && t) atomicAdd(&s_bcnt[v], t);
+        }
       }
+      __syncthreads();
+      if (prof && threadIdx.x == 0) pacc[12] += (unsigned long long)(clock64() - tk0);
+      if (threadIdx.x == 0) {
+        uint64_t run = u.base;
+        for (int v = 0; v < Dc; ++v) {
+          s_cur[v] = run;
+          run += s_bcnt[v];
+        }
+      }
+      __syncthreads();
+      const uint64_t v0 = ((uint64_t)cur_c * x.Db + u.f0) << x.bits_c;
+      for (int v = threadIdx.x; v < Dc; v += T)
+        if (v0 + v < x.V) t_offsets[v0 + v] = s_cur[v];
     } else {
       // single pass: warp-local rank (per-warp counters start at 0), then bases
       uint32_t rr[K], pk[K];
@@ -1549,9 +1676,13 @@ __global__ void __launch_bounds__(kFcWarps * 32, 2) k_final_c(FineCtxC x, const 
     if (!more) break;
     u0 = u1;
     c0 = c1;
+    ci0 = ci1;
   }
-  if (prof && threadIdx.x == 0)
-    for (int i = 0; i < 10; ++i) atomicAdd(&prof[i], pacc[i]);
+  if (prof && threadIdx.x == 0) {
+    pacc[13] = (unsigned long long)(clock64() - tstart);
+    for (int i = 0; i < 13; ++i) atomicAdd(&prof[i], pacc[i]);
+    atomicMax(&prof[13], pacc[13]);
+  }
 }
 
 // ----------------------------------------------------------- self test
