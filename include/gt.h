@@ -49,6 +49,8 @@ extern "C" {
 #define GT_ENOMEM (-3)
 #define GT_ECUDA (-4)
 #define GT_ENODEV (-5)
+#define GT_EFORMAT (-6) /* GraphFormatError (errors.py:4-14): a POTG file violates the format */
+#define GT_EIO (-7)     /* OSError: a file could not be opened, read or written */
 
 #define GT_ABI_VERSION 1
 
@@ -141,6 +143,44 @@ int gt_gen_er(uint64_t num_vertices, uint64_t num_edges, uint64_t seed,
  * Consumes src/dst (they are overwritten as scratch). */
 int gt_build_csr(uint32_t *src, uint32_t *dst, uint64_t num_vertices, uint64_t num_edges,
                  uint64_t *offsets, uint32_t *edges, void *stream);
+
+/* ---- canonicalisation and verification on the device (bench.py:84-170) ----
+ * gt_sort_lists: out_edges = every list of (offsets, edges) sorted ascending
+ * (sort_neighbor_lists, baselines.py:457-475); the offsets are unchanged.
+ * gt_first_diff_u64/_u32: *first = the first i < n with a[i] != b[i], else n.
+ * gt_in_degree_offsets: offsets[V+1] = exclusive scan of the in-degrees of
+ * edges (bincount + cumsum, bench.py:140-142).
+ * gt_first_diff_lists: *first = the first j < n_vertices whose list
+ * vertices[j] differs between (off_a, edges_a) and (off_b, edges_b), else
+ * n_vertices (the per-vertex multiset check of bench.py:150-170 on
+ * canonical lists). */
+int gt_sort_lists(const uint64_t *offsets, const uint32_t *edges, uint64_t num_vertices, uint64_t num_edges,
+                  uint32_t *out_edges, void *stream);
+int gt_first_diff_u64(const uint64_t *a, const uint64_t *b, uint64_t n, uint64_t *first, void *stream);
+int gt_first_diff_u32(const uint32_t *a, const uint32_t *b, uint64_t n, uint64_t *first, void *stream);
+int gt_in_degree_offsets(const uint32_t *edges, uint64_t num_edges, uint64_t num_vertices, uint64_t *offsets,
+                         void *stream);
+int gt_first_diff_lists(const uint64_t *off_a, const uint32_t *edges_a, const uint64_t *off_b,
+                        const uint32_t *edges_b, const uint32_t *vertices, uint64_t n_vertices, uint64_t *first,
+                        void *stream);
+
+/* ---- POTG files straight to / from device memory (io.py:24-114) ----------
+ * gt_potg_read_header replaces the header half of _load_binary (io.py:54-84):
+ * same checks, same order; on GT_EFORMAT gt_last_error() is the reference's
+ * GraphFormatError message and *err_byte_offset its byte_offset.
+ * gt_potg_read streams offsets and edges into caller device buffers
+ * ((V+1)*8 and E*id_width bytes) and checks them on the device in the order
+ * of io.py:86-109 (offsets[0], monotone, offsets[-1] == E, edge IDs < V).
+ * gt_potg_write replaces store_graph (io.py:28-38) from device buffers. */
+typedef struct gt_potg_header {
+  uint32_t version, id_width, orientation, pad;
+  uint64_t num_vertices, num_edges;
+} gt_potg_header;
+int gt_potg_read_header(const char *path, gt_potg_header *header, uint64_t *err_byte_offset);
+int gt_potg_read(const char *path, const gt_potg_header *header, uint64_t *offsets, void *edges,
+                 void *stream, uint64_t *err_byte_offset);
+int gt_potg_write(const char *path, const uint64_t *offsets, const void *edges, uint64_t num_vertices,
+                  uint64_t num_edges, int orientation, int id_width, void *stream);
 
 #ifdef __cplusplus
 }

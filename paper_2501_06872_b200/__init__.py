@@ -14,9 +14,13 @@ from .transpose import (
     prefix_sum_gpu,
     selftest_rank_order,
     set_rank_mode,
+    transpose_atomic,
     transpose_device,
     transpose_gpu,
+    transpose_potra,
 )
+from .verify import VerifyReport, sort_neighbor_lists, verify_output
+from .io import DeviceGraph, load_graph, load_graph_device, store_graph, store_graph_device, transpose_file
 
 __version__ = "0.1.0"
 
@@ -24,7 +28,18 @@ __all__ = [
     "CsrGraph",
     "TransposeOutput",
     "transpose_gpu",
+    "transpose_potra",
+    "transpose_atomic",
     "transpose_device",
+    "sort_neighbor_lists",
+    "verify_output",
+    "VerifyReport",
+    "load_graph",
+    "load_graph_device",
+    "store_graph",
+    "store_graph_device",
+    "transpose_file",
+    "DeviceGraph",
     "prefix_sum_gpu",
     "edge_balanced_vertex_bounds",
     "selftest_rank_order",

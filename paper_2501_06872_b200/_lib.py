@@ -14,11 +14,12 @@ from pathlib import Path
 
 from .errors import CounterOverflowError, FootprintError, GpuUnavailableError
 
-__all__ = ["lib", "GtStats", "check", "LIB_PATH", "SYMBOLS", "load"]
+__all__ = ["lib", "GtStats", "PotgHeader", "check", "LIB_PATH", "SYMBOLS", "load"]
 
 LIB_PATH = Path(__file__).resolve().parent / "libgt.so"
 
 GT_OK, GT_EINVAL, GT_EOVERFLOW, GT_ENOMEM, GT_ECUDA, GT_ENODEV = 0, -1, -2, -3, -4, -5
+GT_EFORMAT, GT_EIO = -6, -7
 
 
 class GtStats(ctypes.Structure):
@@ -35,8 +36,21 @@ class GtStats(ctypes.Structure):
     ]
 
 
+class PotgHeader(ctypes.Structure):
+    _fields_ = [
+        ("version", ctypes.c_uint32),
+        ("id_width", ctypes.c_uint32),
+        ("orientation", ctypes.c_uint32),
+        ("pad", ctypes.c_uint32),
+        ("num_vertices", ctypes.c_uint64),
+        ("num_edges", ctypes.c_uint64),
+    ]
+
+
 _u64, _i64, _int, _vp = ctypes.c_uint64, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
 _stats_p = ctypes.POINTER(GtStats)
+_hdr_p = ctypes.POINTER(PotgHeader)
+_u64p = ctypes.POINTER(_u64)
 
 # name -> (restype, argtypes); must match include/gt.h exactly
 SYMBOLS = {
@@ -54,6 +68,14 @@ SYMBOLS = {
     "gt_gen_rmat": (_int, [_u64, _u64, _u64, _int, _vp, _vp, _vp]),
     "gt_gen_er": (_int, [_u64, _u64, _u64, _vp, _vp, _vp]),
     "gt_build_csr": (_int, [_vp, _vp, _u64, _u64, _vp, _vp, _vp]),
+    "gt_sort_lists": (_int, [_vp, _vp, _u64, _u64, _vp, _vp]),
+    "gt_first_diff_u64": (_int, [_vp, _vp, _u64, _u64p, _vp]),
+    "gt_first_diff_u32": (_int, [_vp, _vp, _u64, _u64p, _vp]),
+    "gt_in_degree_offsets": (_int, [_vp, _u64, _u64, _vp, _vp]),
+    "gt_first_diff_lists": (_int, [_vp, _vp, _vp, _vp, _vp, _u64, _u64p, _vp]),
+    "gt_potg_read_header": (_int, [ctypes.c_char_p, _hdr_p, _u64p]),
+    "gt_potg_read": (_int, [ctypes.c_char_p, _hdr_p, _vp, _vp, _vp, _u64p]),
+    "gt_potg_write": (_int, [ctypes.c_char_p, _vp, _vp, _u64, _u64, _int, _int, _vp]),
 }
 
 _lock = threading.Lock()
@@ -105,6 +127,8 @@ def check(rc: int, what: str) -> None:
         raise MemoryError(text)
     if rc == GT_ENODEV:
         raise GpuUnavailableError(text)
+    if rc == GT_EIO:
+        raise OSError(msg)
     raise RuntimeError(text)
 
 

@@ -34,6 +34,15 @@ int set_err(int code, const char* fmt, ...) {
   return code;
 }
 
+}  // namespace
+
+int gt_internal_set_err(int code, const char* msg) {  // for the other translation units
+  g_err = msg;
+  return code;
+}
+
+namespace {
+
 #define GT_CUDA(call)                                                                          \
   do {                                                                                         \
     cudaError_t e_ = (call);                                                                   \

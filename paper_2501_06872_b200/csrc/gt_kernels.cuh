@@ -1444,11 +1444,21 @@ __global__ void __launch_bounds__(kFcWarps * 32, 2) k_final_c(FineCtxC x, const 
     gen.tw1 = R.f1 - R.f0 + 1;
     const uint32_t nchr = gen.ci.g_end - gen.ci.g_first;
     gen.tab_ok = (uint64_t)nchr * gen.tw1 <= (uint64_t)kTabCap;
-    if (gen.tab_ok)  // the range's segment offsets for every chunk of the coarse bucket, one coalesced pass
-      for (uint32_t i = threadIdx.x; i < nchr * gen.tw1; i += blockDim.x) {
-        const uint32_t j = i / gen.tw1, t = i - j * gen.tw1;
-        s_tab[i] = x.segoff[(uint64_t)(gen.ci.g_first + j) * (x.Db + 1) + R.f0 + t];
+    if (gen.tab_ok) {  // the range's segment offsets for every chunk of the coarse bucket, one coalesced pass
+      const uint32_t tn = nchr * gen.tw1;
+      for (uint32_t i0 = threadIdx.x; i0 < tn; i0 += 4 * blockDim.x) {
+        uint16_t v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {  // four independent loads in flight per thread
+          const uint32_t i = i0 + q * blockDim.x;
+          const uint32_t jj = i / gen.tw1, t = i - jj * gen.tw1;
+          v[q] = (i < tn) ? x.segoff[(uint64_t)(gen.ci.g_first + jj) * (x.Db + 1) + R.f0 + t] : (uint16_t)0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (i0 + q * blockDim.x < tn) s_tab[i0 + q * blockDim.x] = v[q];
       }
+    }
     __syncthreads();
     return true;
   };

@@ -1,0 +1,151 @@
+// gt_verify.cu — GPU canonicalisation and output verification.
+//
+// * gt_sort_lists replaces sort_neighbor_lists / _sort_segments
+//   (baselines.py:448-475): every list ascending.  It is the transpose applied
+//   twice: T(g) lists sources ascending per destination, and T(T(g)) lists,
+//   for every vertex, its neighbours ascending with multiplicity — the same
+//   offsets as g and each list sorted, by the stable kernels of gt_api.cu.
+// * gt_first_diff_* / gt_in_degree_offsets / gt_first_diff_lists are the
+//   device halves of verify_output (bench.py:91-170): first differing offset
+//   or edge index (_first_mismatch_vertex, bench.py:91-99), the exact
+//   t_offsets = bincount + cumsum of the input's edges (bench.py:140-148), and
+//   the first sampled vertex whose (canonical) neighbour list differs
+//   (bench.py:150-170).  First-index reductions use atomicMin, so the reported
+//   index equals np.nonzero(...)[0][0].
+#include <algorithm>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "../../include/gt.h"
+
+int gt_internal_set_err(int code, const char* msg);  // gt_api.cu
+
+namespace {
+
+template <typename T>
+__global__ void k_first_diff(const T* __restrict__ a, const T* __restrict__ b, uint64_t n,
+                             unsigned long long* first) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    if (a[i] != b[i]) {
+      atomicMin(first, (unsigned long long)i);
+      return;  // later indices of this thread are larger
+    }
+}
+
+__global__ void k_degree_hist(const uint32_t* __restrict__ e, uint64_t E, uint32_t* __restrict__ cnt) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < E; i += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(&cnt[e[i]], 1u);
+}
+
+// warp per listed vertex: does list a[v] differ from list b[v]?
+__global__ void k_first_diff_lists(const uint64_t* __restrict__ oa, const uint32_t* __restrict__ ea,
+                                   const uint64_t* __restrict__ ob, const uint32_t* __restrict__ eb,
+                                   const uint32_t* __restrict__ verts, uint64_t nv, unsigned long long* first) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t j = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); j < nv; j += warps) {
+    const uint32_t v = verts[j];
+    const uint64_t a0 = oa[v], a1 = oa[v + 1], b0 = ob[v], b1 = ob[v + 1];
+    bool diff = (a1 - a0) != (b1 - b0);
+    for (uint64_t q = lane; !diff && q < a1 - a0; q += 32) diff = ea[a0 + q] != eb[b0 + q];
+    if (__any_sync(0xffffffffu, diff)) {
+      if (lane == 0) atomicMin(first, (unsigned long long)j);
+    }
+  }
+}
+
+int cuda_fail(cudaError_t e) {
+  return gt_internal_set_err(e == cudaErrorMemoryAllocation ? GT_ENOMEM : GT_ECUDA, cudaGetErrorString(e));
+}
+
+template <typename T>
+int first_diff(const T* a, const T* b, uint64_t n, uint64_t* first, void* stream) {
+  if (!first || (n && (!a || !b))) return gt_internal_set_err(GT_EINVAL, "null argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned long long* d = nullptr;
+  cudaError_t e = cudaMallocAsync(&d, 8, st);
+  if (e != cudaSuccess) return cuda_fail(e);
+  cudaMemsetAsync(d, 0xff, 8, st);
+  if (n) k_first_diff<T><<<148 * 8, 256, 0, st>>>(a, b, n, d);
+  unsigned long long h = ~0ull;
+  cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, st);
+  e = cudaStreamSynchronize(st);
+  cudaFreeAsync(d, st);
+  if (e != cudaSuccess) return cuda_fail(e);
+  *first = (h == ~0ull) ? n : (uint64_t)h;
+  return GT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gt_sort_lists(const uint64_t* offsets, const uint32_t* edges, uint64_t V, uint64_t E, uint32_t* out_edges,
+                  void* stream) {
+  if (!offsets || (E && (!edges || !out_edges))) return gt_internal_set_err(GT_EINVAL, "null argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint64_t* t_off = nullptr;
+  uint32_t* t_edg = nullptr;
+  uint64_t* tt_off = nullptr;
+  cudaError_t e;
+  if ((e = cudaMallocAsync(&t_off, (V + 1) * 8, st)) != cudaSuccess ||
+      (e = cudaMallocAsync(&t_edg, std::max<uint64_t>(E, 1) * 4, st)) != cudaSuccess ||
+      (e = cudaMallocAsync(&tt_off, (V + 1) * 8, st)) != cudaSuccess) {
+    cudaFreeAsync(t_off, st);
+    cudaFreeAsync(t_edg, st);
+    return cuda_fail(e);
+  }
+  int rc = gt_transpose(offsets, edges, V, E, t_off, t_edg, nullptr, 0, st, nullptr);
+  if (rc == GT_OK) rc = gt_transpose(t_off, t_edg, V, E, tt_off, out_edges, nullptr, 0, st, nullptr);
+  cudaFreeAsync(t_off, st);
+  cudaFreeAsync(t_edg, st);
+  cudaFreeAsync(tt_off, st);
+  if (rc == GT_OK && (e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e);
+  return rc;
+}
+
+int gt_first_diff_u64(const uint64_t* a, const uint64_t* b, uint64_t n, uint64_t* first, void* stream) {
+  return first_diff<uint64_t>(a, b, n, first, stream);
+}
+
+int gt_first_diff_u32(const uint32_t* a, const uint32_t* b, uint64_t n, uint64_t* first, void* stream) {
+  return first_diff<uint32_t>(a, b, n, first, stream);
+}
+
+int gt_in_degree_offsets(const uint32_t* edges, uint64_t E, uint64_t V, uint64_t* offsets, void* stream) {
+  if (!offsets || (E && !edges)) return gt_internal_set_err(GT_EINVAL, "null argument");
+  if (V >= (1ull << 32)) return gt_internal_set_err(GT_EINVAL, "num_vertices must be < 2^32");
+  if (E >= (1ull << 32)) return gt_internal_set_err(GT_EOVERFLOW, "in-degree counters are 32-bit (E >= 2^32)");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint32_t* cnt = nullptr;
+  cudaError_t e = cudaMallocAsync(&cnt, std::max<uint64_t>(V, 1) * 4, st);
+  if (e != cudaSuccess) return cuda_fail(e);
+  cudaMemsetAsync(cnt, 0, std::max<uint64_t>(V, 1) * 4, st);
+  if (E) k_degree_hist<<<148 * 16, 256, 0, st>>>(edges, E, cnt);
+  int rc = gt_prefix_sum(cnt, V, offsets, st);
+  cudaFreeAsync(cnt, st);
+  if (rc == GT_OK && (e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e);
+  return rc;
+}
+
+int gt_first_diff_lists(const uint64_t* off_a, const uint32_t* edges_a, const uint64_t* off_b,
+                        const uint32_t* edges_b, const uint32_t* vertices, uint64_t n_vertices, uint64_t* first,
+                        void* stream) {
+  if (!first || (n_vertices && (!off_a || !off_b || !vertices))) return gt_internal_set_err(GT_EINVAL, "null argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned long long* d = nullptr;
+  cudaError_t e = cudaMallocAsync(&d, 8, st);
+  if (e != cudaSuccess) return cuda_fail(e);
+  cudaMemsetAsync(d, 0xff, 8, st);
+  if (n_vertices) k_first_diff_lists<<<148 * 4, 256, 0, st>>>(off_a, edges_a, off_b, edges_b, vertices, n_vertices, d);
+  unsigned long long h = ~0ull;
+  cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, st);
+  e = cudaStreamSynchronize(st);
+  cudaFreeAsync(d, st);
+  if (e != cudaSuccess) return cuda_fail(e);
+  *first = (h == ~0ull) ? n_vertices : (uint64_t)h;
+  return GT_OK;
+}
+
+}  // extern "C"

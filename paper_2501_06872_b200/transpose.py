@@ -29,6 +29,8 @@ from .graph import CsrGraph, flip_orientation
 __all__ = [
     "TransposeOutput",
     "transpose_gpu",
+    "transpose_potra",
+    "transpose_atomic",
     "transpose_device",
     "prefix_sum_gpu",
     "edge_balanced_vertex_bounds",
@@ -154,6 +156,53 @@ def transpose_gpu(g, devices: int = 1, *, device=None, stream=None) -> Transpose
             "devices": 1,
         },
     )
+
+
+def transpose_potra(g, threads: int, budget=None, *, force_method=None, sample_fraction: float = 0.01,
+                    probe_edges=None, seed: int = 0, partition_edges: int = 1 << 18,
+                    debug: bool = False) -> TransposeOutput:
+    """Signature of the reference's ``transpose_potra`` (hlh.py:441-452) on the GPU.
+
+    Argument checks are the reference's (``threads >= 1``, _nb.py:112-113;
+    ``force_method`` in {None, "atomic", "hlh"}, hlh.py:462-463).  The GPU
+    path has no degree-dependent branch: high- and low-degree destinations go
+    through the same stable partition kernels, so the probe, the HDV sample
+    and the cache budget have nothing to choose; ``details`` reports
+    ``method_chosen="gpu"``, ``k=0`` and the GPU accounting.  The output is
+    sorted (``sorted=True``) and equals ``transpose_oracle(g)``.
+    """
+    if force_method not in (None, "atomic", "hlh"):
+        raise ValueError(f"force_method must be 'atomic' or 'hlh', got {force_method!r}")
+    if threads < 1:
+        raise ValueError(f"thread count must be >= 1, got {threads}")
+    out = transpose_gpu(g)
+    details = {
+        "method_chosen": "gpu",
+        "k": 0,
+        "coverage_estimate": 0.0,
+        "sample_size": 0,
+        "probe": None,
+        "hdv_aux_bytes": 0,
+        "shared_aux_bytes": out.aux_footprint_bytes,
+        "partitions": out.details.get("big_buckets", 0),
+        "step3_imbalance": None,
+    }
+    details.update(out.details)
+    return TransposeOutput(graph=out.graph, phase_times={"step0": 0.0, **out.phase_times},
+                           aux_footprint_bytes=out.aux_footprint_bytes, method="potra-gpu", sorted=True,
+                           details=details)
+
+
+def transpose_atomic(g, threads: int, partition_edges: int = 1 << 18) -> TransposeOutput:
+    """Signature of the reference's ``transpose_atomic`` (baselines.py:168-170)
+    on the GPU.  Unlike the reference the result is already sorted
+    (``sorted=True``), so a following ``sort_neighbor_lists`` is a no-op in
+    effect."""
+    if threads < 1:
+        raise ValueError(f"thread count must be >= 1, got {threads}")
+    if partition_edges < 1:
+        raise ValueError("partition_edges must be >= 1")
+    return transpose_gpu(g)
 
 
 def prefix_sum_gpu(counts: np.ndarray) -> np.ndarray:

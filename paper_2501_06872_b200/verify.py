@@ -1,0 +1,172 @@
+"""GPU canonicalisation and verification with the reference's API.
+
+* ``sort_neighbor_lists(t, threads)`` mirrors baselines.py:457-475: returns a
+  new ``TransposeOutput`` whose lists are ascending, ``sorted=True``, the sort
+  time added to ``phase_times["sort"]``.  The sort is ``gt_sort_lists`` (the
+  stable transpose applied twice), so it is exact for any producer.
+* ``verify_output(input_graph, output, mode, seed, sample_vertices)`` mirrors
+  bench.py:102-170 and returns the same ``VerifyReport``.  The expected CSC
+  is this package's transpose (pinned bit-exact to ``transpose_oracle`` by the
+  test suite) and every comparison runs on the device; the messages and the
+  mismatch vertex follow ``_first_mismatch_vertex`` (bench.py:91-99) and the
+  multiset-sample branch (same seeded sample: numpy ``default_rng(seed)``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .transpose import TransposeOutput, _stream_handle, _torch, transpose_device
+
+__all__ = ["VerifyReport", "verify_output", "sort_neighbor_lists", "sort_lists_device",
+           "FULL_ORACLE_MAX_EDGES", "SAMPLE_VERTICES"]
+
+FULL_ORACLE_MAX_EDGES = 10**8  # bench.py:41
+SAMPLE_VERTICES = 100_000  # bench.py:42
+
+
+@dataclass
+class VerifyReport:
+    """bench.py:77-81."""
+
+    passed: bool
+    mode: str
+    mismatch_vertex: int | None = None
+    message: str = ""
+
+
+def _vp(t):
+    return ctypes.c_void_p(t.data_ptr() if t.numel() else 0)
+
+
+def sort_lists_device(offsets, edges, num_vertices: int, stream=None):
+    """Device lists sorted ascending (offsets unchanged); returns new edges."""
+    torch = _torch()
+    out = torch.empty_like(edges)
+    with torch.cuda.device(offsets.device):
+        rc = _lib.lib.gt_sort_lists(_vp(offsets), _vp(edges), int(num_vertices), int(edges.numel()), _vp(out),
+                                    _stream_handle(torch, stream))
+    _lib.check(rc, "gt_sort_lists")
+    return out
+
+
+def _to_device(g, torch, dev):
+    off = torch.from_numpy(np.ascontiguousarray(g.offsets, dtype=np.uint64).view(np.int64)).to(dev)
+    if g.edges.dtype != np.uint32:
+        raise ValueError("only 32-bit neighbour IDs (num_vertices <= 2^32) are supported")
+    edg = torch.from_numpy(np.ascontiguousarray(g.edges).view(np.int32)).to(dev)
+    return off, edg
+
+
+def sort_neighbor_lists(t: TransposeOutput, threads: int = 1) -> TransposeOutput:
+    """GPU sort_neighbor_lists (baselines.py:457-475)."""
+    if threads < 1:
+        raise ValueError(f"thread count must be >= 1, got {threads}")
+    torch = _torch()
+    g = t.graph
+    dev = torch.device("cuda", torch.cuda.current_device())
+    t0 = time.perf_counter()
+    off, edg = _to_device(g, torch, dev)
+    sorted_edges = sort_lists_device(off, edg, g.num_vertices).cpu().numpy().view(np.uint32)
+    dt = time.perf_counter() - t0
+    phase_times = dict(t.phase_times)
+    phase_times["sort"] = phase_times.get("sort", 0.0) + dt
+    return TransposeOutput(
+        graph=type(g)(g.num_vertices, g.num_edges, g.offsets.copy(), sorted_edges, g.orientation),
+        phase_times=phase_times,
+        aux_footprint_bytes=t.aux_footprint_bytes,
+        method=t.method,
+        sorted=True,
+        details=dict(t.details),
+    )
+
+
+def _first_diff(a, b, kind: str) -> int:
+    torch = _torch()
+    first = ctypes.c_uint64(0)
+    fn = _lib.lib.gt_first_diff_u64 if kind == "u64" else _lib.lib.gt_first_diff_u32
+    with torch.cuda.device(a.device):
+        rc = fn(_vp(a), _vp(b), int(a.numel()), ctypes.byref(first), _stream_handle(torch, None))
+    _lib.check(rc, "gt_first_diff")
+    return int(first.value)
+
+
+def verify_output(input_graph, output: TransposeOutput, mode: str = "full-oracle", seed: int = 0,
+                  sample_vertices: int = SAMPLE_VERTICES) -> VerifyReport:
+    """Check a transposition output against its input graph on the GPU."""
+    if mode not in ("full-oracle", "multiset-sample"):
+        raise ValueError(f"unknown verify mode {mode!r}")
+    torch = _torch()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    g, out = input_graph, output.graph
+    nv = int(g.num_vertices)
+    in_off, in_edg = _to_device(g, torch, dev)
+    got_off, got_edg = _to_device(out, torch, dev)
+
+    if mode == "full-oracle":
+        exp_off, exp_edg, _ = transpose_device(in_off, in_edg, nv)
+        if not output.sorted:
+            got_edg = sort_lists_device(got_off, got_edg, out.num_vertices)
+        same_shape = exp_off.numel() == got_off.numel() and exp_edg.numel() == got_edg.numel()
+        if same_shape:
+            i_off = _first_diff(exp_off, got_off, "u64")
+            if i_off == exp_off.numel():
+                i_e = _first_diff(exp_edg, got_edg, "u32")
+                if i_e == exp_edg.numel():
+                    flip = {"CSR": "CSC", "CSC": "CSR"}[g.orientation]
+                    if out.orientation == flip and out.edges.dtype == np.uint32:
+                        return VerifyReport(passed=True, mode=mode)
+                    return VerifyReport(passed=False, mode=mode, mismatch_vertex=0,
+                                        message="orientation or dtype differs")
+                off_h = exp_off.cpu().numpy().view(np.uint64)
+                v = int(np.searchsorted(off_h, i_e, side="right")) - 1
+                return VerifyReport(passed=False, mode=mode, mismatch_vertex=v,
+                                    message=f"neighbor lists differ at vertex {v} (edge index {i_e})")
+            v = max(i_off - 1, 0)
+            return VerifyReport(passed=False, mode=mode, mismatch_vertex=v, message=f"t_offsets differ at vertex {v}")
+        # different sizes: the first differing offset on the common prefix (or its end)
+        n = min(exp_off.numel(), got_off.numel())
+        i_off = _first_diff(exp_off[:n], got_off[:n], "u64")
+        v = max(i_off - 1, 0)
+        return VerifyReport(passed=False, mode=mode, mismatch_vertex=v, message=f"t_offsets differ at vertex {v}")
+
+    # multiset-sample (bench.py:137-170): exact offsets, then per-vertex multisets on a seeded sample
+    exp_off = torch.empty(nv + 1, dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        rc = _lib.lib.gt_in_degree_offsets(_vp(in_edg), int(in_edg.numel()), nv, _vp(exp_off),
+                                           _stream_handle(torch, None))
+    _lib.check(rc, "gt_in_degree_offsets")
+    if got_off.numel() != exp_off.numel():
+        n = min(exp_off.numel(), got_off.numel())
+        i_off = _first_diff(exp_off[:n], got_off[:n], "u64")
+        v = max(i_off - 1, 0)
+        return VerifyReport(passed=False, mode=mode, mismatch_vertex=v, message=f"t_offsets differ at vertex {v}")
+    i_off = _first_diff(exp_off, got_off, "u64")
+    if i_off != exp_off.numel():
+        v = max(i_off - 1, 0)
+        return VerifyReport(passed=False, mode=mode, mismatch_vertex=v, message=f"t_offsets differ at vertex {v}")
+    rng = np.random.default_rng(seed)
+    n_sample = min(sample_vertices, nv)
+    sample = np.sort(rng.choice(nv, size=n_sample, replace=False)) if n_sample else np.empty(0, np.int64)
+    if not n_sample:
+        return VerifyReport(passed=True, mode=mode)
+    exp_t_off, exp_t_edg, _ = transpose_device(in_off, in_edg, nv)  # canonical (ascending) expected lists
+    # each sampled list is sorted whatever output.sorted claims (np.sort(seg), bench.py:158-160)
+    got_sorted = sort_lists_device(got_off, got_edg, out.num_vertices)
+    verts = torch.from_numpy(sample.astype(np.uint32).view(np.int32)).to(dev)
+    first = ctypes.c_uint64(0)
+    with torch.cuda.device(dev):
+        rc = _lib.lib.gt_first_diff_lists(_vp(exp_t_off), _vp(exp_t_edg), _vp(got_off), _vp(got_sorted), _vp(verts),
+                                          n_sample, ctypes.byref(first), _stream_handle(torch, None))
+    _lib.check(rc, "gt_first_diff_lists")
+    j = int(first.value)
+    if j == n_sample:
+        return VerifyReport(passed=True, mode=mode)
+    v = int(sample[j])
+    return VerifyReport(passed=False, mode=mode, mismatch_vertex=v,
+                        message=f"sampled neighbor multisets differ at vertex {v}")
