@@ -12,6 +12,7 @@
 
 #include "../../include/gt.h"
 #include "gt_kernels.cuh"
+#include "gt_v3.cuh"
 
 using namespace gt;
 
@@ -623,11 +624,245 @@ int transpose_core_c(const Plan& p, In in, uint64_t* t_offsets, uint32_t* t_edge
   return GT_OK;
 }
 
+// ---------------------------------------------------------------- v3 path
+// Workspace layout of the lean pipeline (gt_v3.cuh).  R1 lives in t_edges.
+struct Plan3 {
+  uint64_t ntiles1 = 0, nplace = 0, nh = 0, max_t2 = 0, nfine = 0, max_big = 0, max_t3 = 0;
+  uint64_t o_r2, o_tcnt, o_tbase, o_status, o_ctr, o_psrc, o_prev, o_seghi, o_cstart, o_cfirst, o_tiles2, o_cnt2,
+      o_base2, o_seg2, o_fbase, o_units, o_bigs, o_tiles3, o_cnt3, o_base3, o_seg3, o_cnt, o_err, total;
+};
+
+bool use_v3(const Plan& p) { return p.compact && p.E < (1ull << 32) && getenv("GT_V2") == nullptr; }
+
+void make_plan3(const Plan& p, Plan3& q) {
+  const uint64_t E = p.E;
+  q.ntiles1 = (E + v3::CT1 - 1) / v3::CT1;
+  q.nplace = (E + v3::PT - 1) / v3::PT;
+  q.nh = 1ull << p.nsh;
+  q.max_t2 = (E + v3::CT2 - 1) / v3::CT2 + (uint64_t)p.D1;
+  q.nfine = (uint64_t)p.D1 * p.Db;
+  q.max_big = std::min<uint64_t>(q.nfine, E / v3::CAP3 + 1);
+  q.max_t3 = (E + v3::CT2 - 1) / v3::CT2 + q.max_big;
+  uint64_t off = 0;
+  auto take = [&](uint64_t bytes) {
+    const uint64_t o = off;
+    off = align_up(off + std::max<uint64_t>(bytes, 1), 256);
+    return o;
+  };
+  const uint64_t n1 = (uint64_t)p.D1 * q.ntiles1;
+  q.o_r2 = take(E * 4 + 64);
+  q.o_tcnt = take(n1 * 4);
+  q.o_tbase = take((n1 + 1) * 8);
+  q.o_status = take(((n1 + 1 + kScanTile - 1) / kScanTile + 1) * 8);
+  q.o_ctr = take(64);
+  q.o_psrc = take((q.nplace + 2) * 4);
+  q.o_prev = take((q.ntiles1 + 1) * 4);
+  q.o_seghi = take((uint64_t)p.D1 * (q.nh + 1) * 8);
+  q.o_cstart = take((uint64_t)(p.D1 + 1) * 8);
+  q.o_cfirst = take((uint64_t)(p.D1 + 1) * 4);
+  q.o_tiles2 = take(q.max_t2 * sizeof(v3::RTile));
+  q.o_cnt2 = take(q.max_t2 * (uint64_t)p.Db * 4);
+  q.o_base2 = take(q.max_t2 * (uint64_t)p.Db * 8);
+  q.o_seg2 = take((uint64_t)p.D1 * sizeof(v3::SegDesc));
+  q.o_fbase = take((q.nfine + 1) * 8);
+  q.o_units = take(q.nfine * sizeof(v3::Unit3));
+  q.o_bigs = take(q.max_big * sizeof(v3::Big3));
+  q.o_tiles3 = take(q.max_t3 * sizeof(v3::RTile));
+  q.o_cnt3 = take(q.max_t3 * (uint64_t)p.Dc * 4);
+  q.o_base3 = take(q.max_t3 * (uint64_t)p.Dc * 8);
+  q.o_seg3 = take(q.max_big * sizeof(v3::SegDesc));
+  q.o_cnt = take(64);
+  q.o_err = take(4);
+  q.total = off;
+}
+
+__global__ void k_set_u32(uint32_t* p, uint32_t v) { *p = v; }
+
+template <int kMode>
+int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges, unsigned char* ws, cudaStream_t st,
+                 gt_stats* stats, Timer& tm) {
+  using namespace v3;
+  Plan3 q;
+  make_plan3(p, q);
+  const uint64_t V = p.V, E = p.E;
+  const int D1 = p.D1, Db = p.Db, Dc = p.Dc;
+  uint32_t* r2 = reinterpret_cast<uint32_t*>(ws + q.o_r2);
+  uint32_t* tcnt = reinterpret_cast<uint32_t*>(ws + q.o_tcnt);
+  uint64_t* tbase = reinterpret_cast<uint64_t*>(ws + q.o_tbase);
+  uint64_t* status = reinterpret_cast<uint64_t*>(ws + q.o_status);
+  unsigned int* ctr = reinterpret_cast<unsigned int*>(ws + q.o_ctr);
+  uint32_t* psrc = reinterpret_cast<uint32_t*>(ws + q.o_psrc);
+  uint32_t* prev = reinterpret_cast<uint32_t*>(ws + q.o_prev);
+  uint64_t* seghi = reinterpret_cast<uint64_t*>(ws + q.o_seghi);
+  uint64_t* cstart = reinterpret_cast<uint64_t*>(ws + q.o_cstart);
+  uint32_t* cfirst = reinterpret_cast<uint32_t*>(ws + q.o_cfirst);
+  RTile* tiles2 = reinterpret_cast<RTile*>(ws + q.o_tiles2);
+  uint32_t* cnt2 = reinterpret_cast<uint32_t*>(ws + q.o_cnt2);
+  uint64_t* base2 = reinterpret_cast<uint64_t*>(ws + q.o_base2);
+  SegDesc* seg2 = reinterpret_cast<SegDesc*>(ws + q.o_seg2);
+  uint64_t* fbase = reinterpret_cast<uint64_t*>(ws + q.o_fbase);
+  Unit3* units = reinterpret_cast<Unit3*>(ws + q.o_units);
+  Big3* bigs = reinterpret_cast<Big3*>(ws + q.o_bigs);
+  RTile* tiles3 = reinterpret_cast<RTile*>(ws + q.o_tiles3);
+  uint32_t* cnt3 = reinterpret_cast<uint32_t*>(ws + q.o_cnt3);
+  uint64_t* base3 = reinterpret_cast<uint64_t*>(ws + q.o_base3);
+  SegDesc* seg3 = reinterpret_cast<SegDesc*>(ws + q.o_seg3);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(ws + q.o_cnt);  // [0] units [1] big [2] tiles3 [3] unit ctr [4] D1
+  unsigned int* err = reinterpret_cast<unsigned int*>(ws + q.o_err);
+  const uint32_t nh = (uint32_t)q.nh;
+  int rc;
+  int launches = 0;
+  const int sms = num_sms();
+
+  GT_CUDA(cudaMemsetAsync(cnt, 0, 64, st));
+  GT_CUDA(cudaMemsetAsync(err, 0, 4, st));
+  GT_CUDA(cudaMemsetAsync(seghi, 0xff, (uint64_t)D1 * (nh + 1) * 8, st));
+  k_set_u32<<<1, 1, 0, st>>>(cnt + 4, (uint32_t)D1);
+  GT_LAUNCH_CHECK();
+  if ((rc = tm.mark())) return rc;
+  // ---- step 1: level-1 partition of the CSR stream into R1 (in t_edges)
+  k_tile_src<<<(unsigned)((q.nplace + 1 + 255) / 256), 256, 0, st>>>(in, E, PT, q.nplace + 1, psrc);
+  GT_LAUNCH_CHECK();
+  k_prev_src<<<(unsigned)((q.ntiles1 + 255) / 256), 256, 0, st>>>(in, E, CT1, q.ntiles1, prev);
+  GT_LAUNCH_CHECK();
+  k_c1<<<(unsigned)((q.ntiles1 + G1 - 1) / G1), 512, (size_t)G1 * D1 * 4, st>>>(in.edges, E, q.ntiles1, D1,
+                                                                                p.b + p.c, tcnt);
+  GT_LAUNCH_CHECK();
+  if ((rc = scan_u32_to_u64(tcnt, (uint64_t)D1 * q.ntiles1, tbase, 0, true, status, ctr, st))) return rc;
+  {
+    P1Args a;
+    a.offsets = in.offsets;
+    a.edges = in.edges;
+    a.e_begin = in.e_begin;
+    a.V = V;
+    a.E = E;
+    a.ntiles = q.ntiles1;
+    a.D = D1;
+    a.shift = p.b + p.c;
+    a.L = p.L;
+    a.low_mask = (uint32_t)((1ull << (p.b + p.c)) - 1);
+    a.src_mask = (uint32_t)((1ull << p.L) - 1);
+    a.tbase = tbase;
+    a.psrc = psrc;
+    a.prev_src = prev;
+    a.nh = nh;
+    a.seg_hi = seghi;
+    a.out = t_edges;
+    const size_t sm = smem_p1(D1, kMode);
+    if ((rc = set_smem(k_p1<kMode>, sm))) return rc;
+    k_p1<kMode><<<(unsigned)q.ntiles1, T, sm, st>>>(a);
+    GT_LAUNCH_CHECK();
+  }
+  launches += 6;
+  if ((rc = tm.mark())) return rc;
+  // ---- step 2: level 2 (count, per-bucket column scan, place fine-bucket-major into R2)
+  k_coarse_tiles<<<1, 1024, (size_t)(D1 + 1) * 4, st>>>(tbase, q.ntiles1, D1, E, cstart, cfirst);
+  GT_LAUNCH_CHECK();
+  k_l2_tiles<<<D1, 128, 0, st>>>(cstart, cfirst, Db, seghi, nh, tiles2, seg2);
+  GT_LAUNCH_CHECK();
+  const unsigned gt2 = (unsigned)std::min<uint64_t>(q.max_t2, (uint64_t)sms * 8);
+  k_cnt_rec<<<gt2, 512, (size_t)Db * 4, st>>>(t_edges, tiles2, cfirst + D1, Db, DigSM{p.L + p.c, (uint32_t)(Db - 1)},
+                                              cnt2);
+  GT_LAUNCH_CHECK();
+  k_segscan<<<(unsigned)D1, 512, (size_t)Db * 8, st>>>(seg2, cnt + 4, Db, cnt2, base2, fbase, q.nfine, err);
+  GT_LAUNCH_CHECK();
+  {
+    DecR1 dec;
+    dec.L = p.L;
+    dec.src_mask = (uint32_t)((1ull << p.L) - 1);
+    dec.shB = p.L + p.c;
+    dec.maskB = (uint32_t)(Db - 1);
+    dec.lvmask = (uint32_t)((1ull << (p.c + p.gbits)) - 1);
+    dec.nbs = p.nbs;
+    dec.nh = nh;
+    dec.seg_hi = seghi;
+    const size_t sm = smem_p2(Db, kMode);
+    if ((rc = set_smem(k_p2<kMode, DecR1>, sm))) return rc;
+    const unsigned g = persistent_grid(k_p2<kMode, DecR1>, T, sm, q.max_t2);
+    k_p2<kMode, DecR1><<<g, T, sm, st>>>(t_edges, tiles2, cfirst + D1, Db, dec, base2, r2);
+    GT_LAUNCH_CHECK();
+  }
+  launches += 5;
+  if ((rc = tm.mark())) return rc;
+  // ---- step 3: level 3 (units of small fine buckets; tiled count/scan/place for big ones)
+  k_set_u64<<<1, 1, 0, st>>>(fbase + q.nfine, E);
+  GT_LAUNCH_CHECK();
+  k_plan3<<<(unsigned)((q.nfine / (1u << p.gbits) + 255) / 256 + 1), 256, 0, st>>>(fbase, (uint32_t)q.nfine, p.gbits,
+                                                                                   units, cnt + 0, bigs, cnt + 1);
+  GT_LAUNCH_CHECK();
+  k_big_tiles<<<1, 1024, 0, st>>>(bigs, cnt + 1, p.c, tiles3, cnt + 2, seg3);
+  GT_LAUNCH_CHECK();
+  {
+    const unsigned gt3 = (unsigned)std::min<uint64_t>(q.max_t3, (uint64_t)sms * 8);
+    k_cnt_rec<<<gt3, 512, (size_t)Dc * 4, st>>>(r2, tiles3, cnt + 2, Dc, DigSM{p.nbs, (uint32_t)(Dc - 1)}, cnt3);
+    GT_LAUNCH_CHECK();
+    k_segscan<<<(unsigned)std::min<uint64_t>(q.max_big, (uint64_t)sms * 4), 512, (size_t)Dc * 8, st>>>(
+        seg3, cnt + 1, Dc, cnt3, base3, t_offsets, V, err);
+    GT_LAUNCH_CHECK();
+    DecR2 dec;
+    dec.nbs = p.nbs;
+    dec.src_mask = (p.nbs >= 32) ? 0xffffffffu : (uint32_t)((1ull << p.nbs) - 1);
+    dec.maskC = (uint32_t)(Dc - 1);
+    const size_t sm = smem_p2(Dc, kMode);
+    if ((rc = set_smem(k_p2<kMode, DecR2>, sm))) return rc;
+    const unsigned g = persistent_grid(k_p2<kMode, DecR2>, T, sm, q.max_t3);
+    k_p2<kMode, DecR2><<<g, T, sm, st>>>(r2, tiles3, cnt + 2, Dc, dec, base3, t_edges);
+    GT_LAUNCH_CHECK();
+  }
+  {
+    P3Args a;
+    a.rec = r2;
+    a.units = units;
+    a.n_units = cnt + 0;
+    a.ctr = cnt + 3;
+    a.c = p.c;
+    a.nbs = p.nbs;
+    a.gbits = p.gbits;
+    a.src_mask = (p.nbs >= 32) ? 0xffffffffu : (uint32_t)((1ull << p.nbs) - 1);
+    a.lvmask = (uint32_t)((1ull << (p.c + p.gbits)) - 1);
+    a.V = V;
+    a.t_offsets = t_offsets;
+    a.t_edges = t_edges;
+    const size_t sm = smem_p3(kMode);
+    if ((rc = set_smem(k_p3<kMode>, sm))) return rc;
+    const unsigned g = persistent_grid(k_p3<kMode>, W3 * 32, sm, q.nfine);
+    k_p3<kMode><<<g, W3 * 32, sm, st>>>(a);
+    GT_LAUNCH_CHECK();
+  }
+  k_set_u64<<<1, 1, 0, st>>>(t_offsets + V, E);
+  GT_LAUNCH_CHECK();
+  launches += 8;
+  if ((rc = tm.mark())) return rc;
+  uint32_t h_cnt[3] = {0, 0, 0};
+  unsigned int h_err = 0;
+  GT_CUDA(cudaMemcpyAsync(h_cnt, cnt, 12, cudaMemcpyDeviceToHost, st));
+  GT_CUDA(cudaMemcpyAsync(&h_err, err, 4, cudaMemcpyDeviceToHost, st));
+  GT_CUDA(cudaStreamSynchronize(st));
+  if (stats) {
+    stats->n_big_buckets = h_cnt[1];
+    stats->n_launches = launches + 1;
+  }
+  if (h_err) return set_err(GT_EOVERFLOW, "32-bit degree counter overflowed (a transposed degree >= 2^32)");
+  return GT_OK;
+}
+
 template <int kMode, class In>
 int transpose_any(const Plan& p, In in, uint64_t* t_offsets, uint32_t* t_edges, unsigned char* ws, cudaStream_t st,
                   gt_stats* stats, Timer& tm) {
+  if constexpr (!In::kRecords) {
+    if (use_v3(p)) return transpose_v3<kMode>(p, in, t_offsets, t_edges, ws, st, stats, tm);
+  }
   if (p.compact) return transpose_core_c<kMode, In>(p, in, t_offsets, t_edges, ws, st, stats, tm);
   return transpose_core<kMode, In>(p, in, t_offsets, t_edges, ws, st, stats, tm);
+}
+
+uint64_t workspace_bytes(const Plan& p, bool records) {
+  if (!records && use_v3(p)) {
+    Plan3 q;
+    make_plan3(p, q);
+    return q.total;
+  }
+  return p.total;
 }
 
 int fill_stats(const Plan& p, int mode, Timer& tm, gt_stats* stats) {
@@ -667,7 +902,7 @@ int gt_workspace_size(uint64_t V, uint64_t E, uint64_t* bytes) {
   Plan p;
   int rc = make_plan(V, E, p);
   if (rc) return rc;
-  *bytes = p.total;
+  *bytes = workspace_bytes(p, false);
   return GT_OK;
 }
 
@@ -686,7 +921,7 @@ int gt_selftest_rank_order(uint64_t trials, uint64_t* violations) {
 }
 
 int gt_transpose(const uint64_t* offsets, const uint32_t* edges, uint64_t V, uint64_t E, uint64_t* t_offsets,
-                 uint32_t* t_edges, void* workspace, uint64_t workspace_bytes, void* stream, gt_stats* stats) {
+                 uint32_t* t_edges, void* workspace, uint64_t ws_bytes, void* stream, gt_stats* stats) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (stats) std::memset(stats, 0, sizeof(*stats));
   if (!t_offsets) return set_err(GT_EINVAL, "t_offsets is NULL");
@@ -704,13 +939,14 @@ int gt_transpose(const uint64_t* offsets, const uint32_t* edges, uint64_t V, uin
   Plan p;
   if ((rc = make_plan(V, E, p))) return rc;
   unsigned char* ws = static_cast<unsigned char*>(workspace);
+  const uint64_t need = workspace_bytes(p, false);
   if (!ws) {
     void* w = nullptr;
-    if ((rc = cache_get(g_ws[dev], p.total, &w))) return rc;
+    if ((rc = cache_get(g_ws[dev], need, &w))) return rc;
     ws = static_cast<unsigned char*>(w);
-  } else if (workspace_bytes < p.total) {
-    return set_err(GT_ENOMEM, "workspace too small: need %llu bytes, got %llu", (unsigned long long)p.total,
-                   (unsigned long long)workspace_bytes);
+  } else if (ws_bytes < need) {
+    return set_err(GT_ENOMEM, "workspace too small: need %llu bytes, got %llu", (unsigned long long)need,
+                   (unsigned long long)ws_bytes);
   }
   int mode;
   if ((rc = rank_mode_for(dev, st, &mode))) return rc;
@@ -723,6 +959,7 @@ int gt_transpose(const uint64_t* offsets, const uint32_t* edges, uint64_t V, uin
   if (stats) {
     GT_CUDA(cudaEventSynchronize(tm.ev[tm.n - 1]));
     if ((rc = fill_stats(p, mode, tm, stats))) return rc;
+    stats->workspace_bytes = need;
   }
   return GT_OK;
 }

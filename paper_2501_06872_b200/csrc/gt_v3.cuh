@@ -1,0 +1,1108 @@
+// gt_v3.cuh — lean three-level stable partition (compact 4-byte records).
+//
+// Same contract as gt_kernels.cuh (CSR -> CSC, every list ascending by source =
+// transpose_oracle, graph.py:136-148 = a stable counting sort of the CSR edge
+// stream by destination), re-planned so that every level is one streaming
+// partition pass with a short instruction path per record:
+//
+//   L1  k_c1 count  -> lookback scan -> k_p1 place
+//         CSR edges -> R1 = (dst_low << L | src_low) grouped by coarse digit A,
+//         written into t_edges (the output buffer doubles as R1 storage).
+//         Sources come from per-tile boundary marks (one per source that starts
+//         in the tile) resolved with one ballot per 32-edge slot.
+//   L2  k_cnt_rec count -> k_segscan -> k_p2 place
+//         each coarse bucket is cut into count tiles; a per-bucket column scan
+//         gives every (tile, fine digit B) its final CSC position, so L2 writes
+//         R2 = (lv << nbs | src) fine-bucket-major into the workspace: a fine
+//         bucket's records are contiguous and already sit at their CSC range.
+//   L3  k_p3 units (runs of small fine buckets, TMA in, rank by local vertex,
+//         stage in place, TMA out to t_edges, CSC offsets) and, for fine
+//         buckets above the unit capacity, the same count/scan/place trio as L2
+//         with the low digit C (k_cnt_rec / k_segscan / k_p2<DecR2>).
+//
+// Ranking is the one of gt_common.cuh (warp-private counters, lane-ordered
+// shared atomics or the safe OR-mask mode); stability composes over levels, so
+// each CSC list ends in CSR order = ascending source.
+#pragma once
+#include "gt_common.cuh"
+#include "gt_scan.cuh"
+
+namespace gt {
+namespace v3 {
+
+constexpr int W = 8;             // warps per partition CTA
+constexpr int T = W * 32;
+constexpr int K = 16;            // items per thread per place tile
+constexpr int PT = W * K * 32;   // 4096 records per place tile
+constexpr int PTP = PT + 8;      // landing buffer (alignment slack)
+constexpr int CT1 = 32768;       // L1 count tile (edges)
+constexpr int G1 = 8;            // count tiles per k_c1 CTA
+constexpr int CT2 = 32768;       // L2 / L3-big count tile (records of one segment)
+constexpr int kWin = 1024;       // offsets window (entries) per L1 place tile
+constexpr int kMaxBnd = 512;     // source-high boundaries of an L2 tile held in smem
+constexpr int W3 = 8, K3 = 32;
+constexpr int CAP3 = W3 * K3 * 32;  // 8192 records per L3 unit
+constexpr int CAP3P = CAP3 + 8;
+constexpr int ML3 = 256;            // local vertices per L3 unit
+
+// One count tile of a record pass (L2: a chunk of a coarse bucket; L3-big: a
+// chunk of a big fine bucket).
+struct RTile {
+  uint64_t start;  // first record (absolute index)
+  uint32_t n;      // records
+  uint32_t seg;    // segment (coarse bucket / big-bucket index)
+  uint32_t j, nt;  // tile index inside the segment, tiles in the segment
+  uint32_t h0;     // R1 decode: source-high of the first record
+  uint32_t nbnd;   // R1 decode: source-high boundaries strictly inside the tile
+};
+static_assert(sizeof(RTile) == 32, "RTile layout");
+
+// One segment of a record pass: its count/base table rows are
+// [g0 * D + d * nt + j] (digit-major inside the segment), its records go to
+// positions base + ..., and its per-digit starts to out[out_off + d].
+struct SegDesc {
+  uint64_t base;
+  uint64_t out_off;
+  uint32_t g0, nt;
+};
+
+struct Unit3 {
+  uint64_t start;  // CSC position of the first record
+  uint32_t n;      // records (<= CAP3)
+  uint32_t f0;     // first fine bucket (global index A * Db + B)
+  uint32_t nf;     // fine buckets
+  uint32_t pad;
+};
+
+struct DigSM {  // (r >> shift) & mask
+  int shift;
+  uint32_t mask;
+  __device__ __forceinline__ uint32_t operator()(uint32_t r) const { return (r >> shift) & mask; }
+};
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ uint32_t align_items_u32(const void* p) {
+  return (uint32_t)((reinterpret_cast<uintptr_t>(p) & 15) >> 2);
+}
+__device__ __forceinline__ uint32_t ldg_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+// Number of lanes' positions: for lane l, #{j in [0,32) : rel_j <= l}, rel
+// non-decreasing across lanes (a shuffle binary search, 6 rounds).
+__device__ __forceinline__ uint32_t count_le_lane(uint32_t rel, uint32_t lane) {
+  uint32_t c = 0;
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const uint32_t x = __shfl_sync(kFull, rel, c + s - 1);
+    if (x <= lane) c += s;
+  }
+  const uint32_t x = __shfl_sync(kFull, rel, c);
+  return c + ((x <= lane) ? 1u : 0u);
+}
+
+// Owner of each lane's position in a slot of 32 consecutive positions
+// p0..p0+31 over a non-decreasing boundary sequence b(k): the result for lane l
+// is the largest k in [cur, upper] with k == cur or b(k) <= p0 + l.  `cur` must
+// satisfy "the owner of p0 is >= cur" and nb == b(cur + 1).  Both are advanced
+// to the state of the next slot.  Warp-uniform control flow.
+template <class F>
+__device__ __forceinline__ uint32_t slot_owner(uint32_t& cur, uint64_t& nb, uint64_t p0, uint32_t upper, F bnd_at) {
+  if (nb > p0 + 31) return cur;  // no boundary inside this slot
+  const uint32_t lane = lane_id();
+  uint32_t res;
+  uint32_t base = cur, acc = 0;
+  int rounds = 0;
+  while (true) {
+    const uint64_t k = (uint64_t)base + 1 + lane;
+    const uint64_t bj = (k <= upper) ? bnd_at(k) : ~0ull;
+    const uint32_t rel = (bj <= p0 + 31) ? (uint32_t)(bj - p0) : 32u;
+    acc += count_le_lane(rel, lane);
+    if (__shfl_sync(kFull, rel, 31) >= 32) {
+      res = cur + acc;
+      break;
+    }
+    base += 32;
+    if (++rounds == 3) {  // long run of boundaries at few positions: binary search per lane
+      const uint64_t p = p0 + lane;
+      uint32_t lo = cur, hi = max(upper, cur);
+      while (lo < hi) {
+        const uint32_t mid = lo + (hi - lo + 1) / 2;
+        if (bnd_at(mid) <= p) lo = mid; else hi = mid - 1;
+      }
+      res = lo;
+      break;
+    }
+  }
+  cur = __shfl_sync(kFull, res, 31);
+  nb = ((uint64_t)cur + 1 <= upper) ? bnd_at((uint64_t)cur + 1) : ~0ull;
+  return res;
+}
+
+// Largest k in [lo, hi] with k == lo or b(k) <= p (uniform binary search).
+template <class F>
+__device__ __forceinline__ uint32_t owner_search(uint32_t lo, uint32_t hi, uint64_t p, F bnd_at) {
+  while (lo < hi) {
+    const uint32_t mid = lo + (hi - lo + 1) / 2;
+    if (bnd_at(mid) <= p) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ void zero_u32(uint32_t* p, int n) {  // n multiple of 4, p 16B aligned
+  uint4* q = reinterpret_cast<uint4*>(p);
+  for (int i = threadIdx.x; i < (n >> 2); i += blockDim.x) q[i] = make_uint4(0, 0, 0, 0);
+}
+
+constexpr int WP = W + 1;    // counter table row: digit-major [d][W + 1] (padding keeps rank atomics conflict-free)
+constexpr int W3P = W3 + 1;
+__host__ __device__ constexpr int round4(int x) { return (x + 3) & ~3; }
+
+// Stable rank through the counter at `c` (this warp's entry of the digit);
+// kRankSafe: the OR-mask protocol of gt_common.cuh on the scratch entry `sc`.
+template <int kMode>
+__device__ __forceinline__ uint32_t rank_at(uint32_t* c, uint32_t* sc, bool valid) {
+  if constexpr (kMode == kRankAtomic) {
+    (void)sc;
+    return valid ? atomicAdd(c, 1u) : 0u;
+  } else {
+    const uint32_t lane = lane_id();
+    if (valid) atomicOr(sc, 1u << lane);
+    __syncwarp();
+    uint32_t peers = 0, v = 0;
+    if (valid) {
+      peers = *sc;
+      v = *c;
+    }
+    __syncwarp();
+    const uint32_t lt = peers & lanemask_lt();
+    if (valid && lt == 0) {
+      *c = v + __popc(peers);
+      *sc = 0;
+    }
+    __syncwarp();
+    return v + __popc(lt);
+  }
+}
+
+// In-place exclusive scan of a[0..n) (thread-contiguous chunks, one block scan).
+__device__ __forceinline__ void flat_excl_scan(uint32_t* a, int n, uint32_t* tmp /* >= 33 */) {
+  const int Tn = blockDim.x, t = threadIdx.x, lane = t & 31, w = t >> 5, nw = (Tn + 31) >> 5;
+  const int per = (n + Tn - 1) / Tn;
+  const int lo = min(n, t * per), hi = min(n, lo + per);
+  uint32_t s = 0;
+  for (int i = lo; i < hi; ++i) s += a[i];
+  uint32_t x = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) tmp[w] = x;
+  __syncthreads();
+  if (t < 32) {
+    const uint32_t v0 = (t < nw) ? tmp[t] : 0u;
+    uint32_t v = v0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, v, o);
+      if (t >= o) v += y;
+    }
+    if (t < nw) tmp[t] = v - v0;
+  }
+  __syncthreads();
+  uint32_t run = tmp[w] + x - s;
+  for (int i = lo; i < hi; ++i) {
+    const uint32_t v = a[i];
+    a[i] = run;
+    run += v;
+  }
+  __syncthreads();
+}
+
+// After ranking: cnt[d * (WW+1) + w] becomes the tile position of warp w's
+// first digit-d item; dstart/dtot per digit; delta[d] = gcur[d] - dstart[d]
+// when gcur is given (global index = tile position + delta).
+template <int WW>
+__device__ __forceinline__ void flat_bases(uint32_t* cnt, int D, const uint32_t* gcur, uint32_t* dstart, uint32_t* dtot,
+                                           uint32_t* delta, uint32_t* tmp) {
+  flat_excl_scan(cnt, D * (WW + 1), tmp);
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    const uint32_t b = cnt[d * (WW + 1)];
+    dstart[d] = b;
+    dtot[d] = cnt[d * (WW + 1) + WW] - b;
+    if (gcur) delta[d] = gcur[d] - b;
+  }
+  __syncthreads();
+}
+
+// Block-wide exclusive scan of u64 a[0..n) in place; returns the total.
+__device__ __forceinline__ uint64_t block_excl_scan_u64(uint64_t* a, int n, uint64_t* tmp /* >= 33 */) {
+  const int Tn = blockDim.x, t = threadIdx.x;
+  const int nw = (Tn + 31) >> 5, w = t >> 5, lane = t & 31;
+  const int per = ((n + nw - 1) / nw + 31) & ~31;
+  const int lo = w * per, hi = min(n, lo + per);
+  uint64_t s = 0;
+  for (int i = lo + lane; i < hi; i += 32) s += a[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  if (lane == 0) tmp[w] = s;
+  __syncthreads();
+  if (t < 32) {
+    const uint64_t v0 = (t < nw) ? tmp[t] : 0;
+    uint64_t v = v0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(kFull, v, o);
+      if (t >= o) v += y;
+    }
+    if (t < nw) tmp[t] = v - v0;
+    if (t == 31) tmp[32] = v;
+  }
+  __syncthreads();
+  uint64_t carry = tmp[w];
+  for (int b = lo; b < hi; b += 32) {
+    const int i = b + lane;
+    const uint64_t x = (i < hi) ? a[i] : 0;
+    uint64_t y = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t z = __shfl_up_sync(kFull, y, o);
+      if (lane >= o) y += z;
+    }
+    if (i < hi) a[i] = carry + y - x;
+    carry += __shfl_sync(kFull, y, 31);
+  }
+  const uint64_t total = tmp[32];
+  __syncthreads();
+  return total;
+}
+
+// ------------------------------------------------------------- L1: count
+// Histogram of the coarse digit per count tile (CT1 edges); G1 tiles per CTA.
+// tcnt is digit-major: tcnt[d * ntiles + k] (consecutive tiles of one digit are
+// written together: full 32-byte sectors).
+__global__ void __launch_bounds__(512) k_c1(const uint32_t* __restrict__ edges, uint64_t E, uint64_t ntiles, int D,
+                                            int shift, uint32_t* __restrict__ tcnt) {
+  extern __shared__ __align__(16) uint32_t s_h[];  // G1 * D
+  const uint64_t k0 = (uint64_t)blockIdx.x * G1;
+  const int nt = (int)umin64(G1, ntiles - k0);
+  for (int i = threadIdx.x; i < G1 * D; i += blockDim.x) s_h[i] = 0;
+  __syncthreads();
+  const uint64_t b = k0 * CT1, n = umin64(E, b + (uint64_t)nt * CT1) - b;
+  const uint32_t* p = edges + b;
+  const uint32_t head = (uint32_t)umin64(n, (4 - align_items_u32(p)) & 3);
+  for (uint32_t i = threadIdx.x; i < head; i += blockDim.x) smem_inc(&s_h[(i >> 15) * D + (p[i] >> shift)]);
+  const uint4* p4 = reinterpret_cast<const uint4*>(p + head);
+  const uint64_t n4 = (n - head) >> 2;
+  for (uint64_t q = threadIdx.x; q < n4; q += blockDim.x) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p4 + q));
+    const uint32_t i = head + (uint32_t)q * 4;
+    smem_inc(&s_h[(i >> 15) * D + (v.x >> shift)]);
+    smem_inc(&s_h[((i + 1) >> 15) * D + (v.y >> shift)]);
+    smem_inc(&s_h[((i + 2) >> 15) * D + (v.z >> shift)]);
+    smem_inc(&s_h[((i + 3) >> 15) * D + (v.w >> shift)]);
+  }
+  for (uint64_t i = head + n4 * 4 + threadIdx.x; i < n; i += blockDim.x)
+    smem_inc(&s_h[((uint32_t)i >> 15) * D + (p[i] >> shift)]);
+  __syncthreads();
+  for (int i = threadIdx.x; i < G1 * D; i += blockDim.x) {
+    const int d = i / G1, t = i - d * G1;
+    if (t < nt) tcnt[(uint64_t)d * ntiles + k0 + t] = s_h[t * D + d];
+  }
+}
+
+// ------------------------------------------------------------- L1: place
+struct P1Args {
+  const uint64_t* offsets;
+  const uint32_t* edges;  // stream item 0 = global edge e_begin
+  uint64_t e_begin, V, E;
+  uint64_t ntiles;        // count tiles (CT1)
+  int D, shift, L;
+  uint32_t low_mask, src_mask;
+  const uint64_t* tbase;   // [d * ntiles + k]
+  const uint32_t* psrc;    // owner of the first item of each place tile; [nplace] = owner of item E-1
+  const uint32_t* prev_src;// per count tile: owner of the item before it (~0u: none)
+  uint32_t nh;             // source-high values; seg_hi rows have nh + 1 entries
+  uint64_t* seg_hi;
+  uint32_t* out;           // R1
+};
+
+inline size_t smem_p1(int D, int mode) {
+  return (size_t)PTP * 4 + (size_t)kWin * 8 + (size_t)PT * 6 + (size_t)round4(D * WP) * 4 * (mode == kRankSafe ? 2 : 1) +
+         (size_t)D * 4 * 5 + 40 * 4 + (CT1 / PT + 4) * 4;
+}
+
+__device__ __forceinline__ void bulk_prefetch_l2(const void* g, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ uint32_t lanemask_le() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_le;" : "=r"(m));
+  return m;
+}
+
+// Per-warp tile-local bases and global index offsets: cnt[w][d] becomes the
+// tile position of warp w's first digit-d item, delta[d] = gcur[d] - dstart[d]
+// (global R1 index = tile position + delta[d]), dtot[d] = digit total.
+template <int WW>
+__device__ __forceinline__ void bases_delta(uint32_t* cnt, int D, const uint32_t* gcur, uint32_t* dstart,
+                                            uint32_t* dtot, uint32_t* delta, uint32_t* tmp) {
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < WW; ++w) {
+      const uint32_t c = cnt[w * D + d];
+      cnt[w * D + d] = run;
+      run += c;
+    }
+    dstart[d] = run;
+    dtot[d] = run;
+  }
+  __syncthreads();
+  block_excl_scan_u32(dstart, D, tmp);
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    const uint32_t b = dstart[d];
+#pragma unroll
+    for (int w = 0; w < WW; ++w) cnt[w * D + d] += b;
+    delta[d] = gcur[d] - b;
+  }
+  __syncthreads();
+}
+
+// Write-out of a staged tile: slot i holds payload buf[i] of digit tag[i],
+// global index delta[tag] + i.  Consecutive lanes take consecutive slots, so a
+// warp store covers a few digit runs (coalesced sectors).
+__device__ __forceinline__ void writeout_tag(uint32_t* __restrict__ out, const uint32_t* buf, const uint16_t* tag,
+                                             const uint32_t* delta, uint32_t n) {
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) out[delta[tag[i]] + i] = buf[i];
+}
+
+// L1 place.  One CTA per count tile (CT1 edges), place tiles of PT edges in
+// order with running per-digit cursors.  Per place tile: TMA bulk load of the
+// edges and of the offsets window; every source boundary inside the tile is
+// marked (mark[p] = v + 1 for the source v whose list starts at item p); each
+// 32-edge slot finds its owners with one ballot over the marks (the last mark
+// at or before the lane, else the carry from the previous slot); stable rank
+// by the coarse digit; stage payload + global index by digit; vectorised
+// write-out of the runs.  Requires E < 2^32 (u32 indices).
+template <int kMode>
+__global__ void __launch_bounds__(T, 3) k_p1(const P1Args a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int D = a.D;
+  uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem);                         // PTP (landing, then stage)
+  uint64_t* s_win = reinterpret_cast<uint64_t*>(s_buf + PTP);                  // kWin
+  uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_win + kWin);                 // PT (source-boundary marks)
+  uint16_t* s_tag = reinterpret_cast<uint16_t*>(s_idx + PT);                   // PT (digit of each staged slot)
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_tag + PT);                   // D * WP (digit-major)
+  uint32_t* s_scr = s_cnt + round4(D * WP);                                    // (safe)
+  uint32_t* s_gcur = s_scr + (kMode == kRankSafe ? round4(D * WP) : 0);        // D
+  uint32_t* s_delta = s_gcur + D;                                              // D
+  uint32_t* s_dstart = s_delta + D;                                            // D
+  uint32_t* s_dtot = s_dstart + D;                                             // D
+  uint32_t* s_bh = s_dtot + D;                                                 // D
+  uint32_t* s_tmp = s_bh + D;                                                  // 40
+  uint32_t* s_psrc = s_tmp + 40;                                               // CT1/PT + 2
+  __shared__ __align__(8) uint64_t s_bar;
+  __shared__ uint64_t s_wlo;
+  __shared__ uint32_t s_wn;
+  __shared__ uint32_t s_last_src;
+
+  const uint32_t tid = threadIdx.x, lane = lane_id(), w = warp_id();
+  const uint64_t k = blockIdx.x;
+  const uint64_t tb = k * CT1, te = umin64(a.E, tb + CT1);
+  const int nplace = (int)((te - tb + PT - 1) / PT);
+  const uint64_t gp0 = tb / PT;
+  for (int d = tid; d < D; d += T) s_gcur[d] = (uint32_t)a.tbase[(uint64_t)d * a.ntiles + k];
+  for (int j = tid; j <= nplace; j += T) s_psrc[j] = a.psrc[gp0 + j];
+  zero_u32(s_cnt, round4(D * WP) * (kMode == kRankSafe ? 2 : 1));
+  zero_u32(s_idx, PT);
+  if (tid == 0) {
+    mbar_init(&s_bar, 1);
+    fence_mbar_init();
+  }
+  uint32_t h_prev;
+  {
+    const uint32_t ps = (k > 0) ? a.prev_src[k] : 0xffffffffu;
+    h_prev = (ps == 0xffffffffu) ? 0xffffffffu : (ps >> a.L);
+  }
+  __syncthreads();
+
+  auto issue = [&](int j) {  // thread 0
+    const uint64_t pt = tb + (uint64_t)j * PT;
+    const uint32_t n = (uint32_t)umin64(PT, te - pt);
+    const uint32_t* gp = a.edges + pt;
+    const uint32_t o = align_items_u32(gp);
+    const uint32_t full = (o + n) & ~3u;
+    const uint32_t s0 = s_psrc[j], s1 = s_psrc[j + 1];
+    const uint64_t* wp = a.offsets + s0 + 1;
+    const uint32_t ow = (uint32_t)((reinterpret_cast<uintptr_t>(wp) & 15) >> 3);
+    const uint64_t ws = (uint64_t)s0 + 1 - ow;
+    const uint64_t need = (uint64_t)s1 + 2 - ws, avail = a.V + 1 - ws;
+    const uint32_t nw = (uint32_t)umin64(umin64(need, avail), kWin) & ~1u;
+    s_wlo = ws;
+    s_wn = nw;
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&s_bar, full * 4 + nw * 8);
+    if (full) bulk_g2s(s_buf, gp - o, full * 4, &s_bar);
+    if (nw) bulk_g2s(s_win, a.offsets + ws, nw * 8, &s_bar);
+    if (j + 1 < nplace) {  // warm L2 with the next place tile's edges
+      const uint32_t* gn = gp + PT;
+      const uint32_t on = align_items_u32(gn);
+      const uint32_t nn = (uint32_t)umin64(PT, te - pt - PT);
+      const uint32_t fn = (on + nn) & ~3u;
+      if (fn) bulk_prefetch_l2(gn - on, fn * 4);
+    }
+  };
+
+  uint32_t ph = 0;
+  if (tid == 0 && nplace > 0) issue(0);
+  for (int j = 0; j < nplace; ++j) {
+    const uint64_t pt = tb + (uint64_t)j * PT;
+    const uint32_t n = (uint32_t)umin64(PT, te - pt);
+    const uint32_t* gp = a.edges + pt;
+    const uint32_t o = align_items_u32(gp);
+    const uint32_t full = (o + n) & ~3u;
+    const uint32_t ti = full + tid;
+    const bool tail = tid < 4 && ti < o + n;
+    uint32_t tv = 0;
+    if (tail) tv = ldg_u32(gp - o + ti);
+    mbar_wait_parity(&s_bar, ph);
+    ph ^= 1;
+    if (tail) s_buf[ti] = tv;
+    const uint64_t gi0 = a.e_begin + pt;
+    const uint64_t ws = s_wlo;
+    const uint32_t nw = s_wn;
+    const uint64_t* offs = a.offsets;
+    auto off_at = [&](uint64_t v) -> uint64_t {
+      const uint64_t q = v - ws;
+      return (q < nw) ? s_win[q] : __ldg(offs + v);
+    };
+    const uint32_t s0 = s_psrc[j], s1 = max(s_psrc[j + 1], s0);
+    // mark the first item of every source that starts inside the tile
+    for (uint32_t v = s0 + 1 + tid; v <= s1; v += T) {
+      const uint64_t p = off_at(v) - gi0;
+      if (p < n) atomicMax(&s_idx[p], v + 1);
+    }
+    __syncthreads();  // (A) tile landed, marks placed
+
+    const uint32_t iw = w * (K * 32);
+    uint32_t carry = owner_search(s0, s1, gi0 + iw, off_at);
+    const uint32_t le = lanemask_le();
+    uint32_t pay[K], pk[K];
+    auto slot = [&](int s, bool valid) {
+      const uint32_t i = iw + s * 32 + lane;
+      const uint32_t dst = valid ? s_buf[o + i] : 0u;
+      const uint32_t m = s_idx[i];
+      const uint32_t bal = __ballot_sync(kFull, m != 0);
+      uint32_t src = carry;
+      if (bal) {  // a source starts inside this slot (warp-uniform)
+        const uint32_t bm = bal & le;
+        const uint32_t ms = __shfl_sync(kFull, m, 31 - __clz(bm | 1u));
+        src = bm ? ms - 1 : carry;
+        carry = __shfl_sync(kFull, src, 31);
+      }
+      if (valid && i == n - 1) s_last_src = src;
+      const uint32_t d = dst >> a.shift;
+      pk[s] = (d << 16) | rank_at<kMode>(s_cnt + d * WP + w, s_scr + d * WP + w, valid);
+      pay[s] = ((dst & a.low_mask) << a.L) | (src & a.src_mask);
+    };
+    if (n == (uint32_t)PT) {
+#pragma unroll
+      for (int s = 0; s < K; ++s) slot(s, true);
+    } else {
+#pragma unroll
+      for (int s = 0; s < K; ++s) slot(s, iw + s * 32 + lane < n);
+    }
+    __syncthreads();  // (B) ranks done; landing buffer and marks consumed
+    flat_bases<W>(s_cnt, D, s_gcur, s_dstart, s_dtot, s_delta, s_tmp);
+    // source-high boundaries inside this tile (compact R1 decode table)
+    const uint32_t h_last = s_last_src >> a.L;
+    for (uint32_t h = (h_prev == 0xffffffffu) ? 0u : h_prev + 1; h <= h_last; ++h) {
+      const uint64_t q = __ldg(offs + ((uint64_t)h << a.L)) - gi0;  // first item with src >= h << L
+      for (int d = tid; d < D; d += T) s_bh[d] = 0;
+      __syncthreads();
+#pragma unroll
+      for (int s = 0; s < K; ++s) {
+        const uint32_t i = iw + s * 32 + lane;
+        if (i < n && i < q) smem_inc(&s_bh[pk[s] >> 16]);
+      }
+      __syncthreads();
+      for (int d = tid; d < D; d += T) a.seg_hi[(uint64_t)d * (a.nh + 1) + h] = (uint64_t)s_gcur[d] + s_bh[d];
+      __syncthreads();
+    }
+    h_prev = h_last;
+    // stage payloads and global indices by digit
+#pragma unroll
+    for (int s = 0; s < K; ++s) {
+      if (n == (uint32_t)PT || iw + s * 32 + lane < n) {
+        const uint32_t d = pk[s] >> 16;
+        const uint32_t pos = s_cnt[d * WP + w] + (pk[s] & 0xffffu);
+        s_buf[pos] = pay[s];
+        s_tag[pos] = (uint16_t)d;
+      }
+    }
+    __syncthreads();  // (C)
+    writeout_tag(a.out, s_buf, s_tag, s_delta, n);
+    zero_u32(s_idx, PT);
+    zero_u32(s_cnt, round4(D * WP));
+    for (int d = tid; d < D; d += T) s_gcur[d] += s_dtot[d];
+    fence_proxy_async_smem();
+    __syncthreads();  // (D)
+    if (tid == 0 && j + 1 < nplace) issue(j + 1);
+  }
+}
+
+// -------------------------------------------------- record passes (L2, L3-big)
+// Count: histogram of the digit over each tile -> cnt[(g - j) * D + d * nt + j].
+// Persistent (grid-stride over *n_tiles).
+__global__ void __launch_bounds__(512) k_cnt_rec(const uint32_t* __restrict__ rec, const RTile* __restrict__ tiles,
+                                                 const uint32_t* __restrict__ n_tiles, int D, DigSM dig,
+                                                 uint32_t* __restrict__ cnt) {
+  extern __shared__ __align__(16) uint32_t s_h[];
+  const uint32_t nt_all = *n_tiles;
+  for (uint32_t g = blockIdx.x; g < nt_all; g += gridDim.x) {
+    const RTile t = tiles[g];
+    for (int d = threadIdx.x; d < D; d += blockDim.x) s_h[d] = 0;
+    __syncthreads();
+    const uint32_t* p = rec + t.start;
+    const uint32_t n = t.n;
+    const uint32_t head = min(n, (4 - align_items_u32(p)) & 3);
+    for (uint32_t i = threadIdx.x; i < head; i += blockDim.x) smem_inc(&s_h[dig(p[i])]);
+    const uint4* p4 = reinterpret_cast<const uint4*>(p + head);
+    const uint32_t n4 = (n - head) >> 2;
+    for (uint32_t q = threadIdx.x; q < n4; q += blockDim.x) {
+      uint4 v;
+      asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p4 + q));
+      smem_inc(&s_h[dig(v.x)]);
+      smem_inc(&s_h[dig(v.y)]);
+      smem_inc(&s_h[dig(v.z)]);
+      smem_inc(&s_h[dig(v.w)]);
+    }
+    for (uint32_t i = head + n4 * 4 + threadIdx.x; i < n; i += blockDim.x) smem_inc(&s_h[dig(p[i])]);
+    __syncthreads();
+    const uint64_t row0 = (uint64_t)(g - t.j) * D + t.j;
+    for (int d = threadIdx.x; d < D; d += blockDim.x) cnt[row0 + (uint64_t)d * t.nt] = s_h[d];
+    __syncthreads();
+  }
+}
+
+// Column scan of each segment's count table: totals per digit over the tiles,
+// digit starts (out[out_off + d] = base + start_d when out_off + d < out_limit),
+// and per-(tile, digit) bases.  One CTA per segment (grid-stride over *n_segs).
+// Sets *err when a digit total reaches 2^32 (a transposed degree >= 2^32).
+__global__ void __launch_bounds__(512) k_segscan(const SegDesc* __restrict__ segs, const uint32_t* __restrict__ n_segs,
+                                                 int D, const uint32_t* __restrict__ cnt, uint64_t* __restrict__ base,
+                                                 uint64_t* __restrict__ out, uint64_t out_limit,
+                                                 unsigned int* __restrict__ err) {
+  extern __shared__ __align__(16) uint64_t s_tot[];  // D
+  __shared__ uint64_t s_tmp[40];
+  const uint32_t ns = *n_segs;
+  const uint32_t lane = lane_id(), w = warp_id(), nw = blockDim.x >> 5;
+  for (uint32_t sg = blockIdx.x; sg < ns; sg += gridDim.x) {
+    const SegDesc S = segs[sg];
+    const uint64_t t0 = (uint64_t)S.g0 * D;
+    for (int d = w; d < D; d += nw) {
+      const uint32_t* row = cnt + t0 + (uint64_t)d * S.nt;
+      uint64_t s = 0;
+      for (uint32_t j = lane; j < S.nt; j += 32) s += row[j];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+      if (lane == 0) {
+        s_tot[d] = s;
+        if (s >= (1ull << 32)) atomicExch(err, 1u);
+      }
+    }
+    __syncthreads();
+    block_excl_scan_u64(s_tot, D, s_tmp);
+    for (int d = threadIdx.x; d < D; d += blockDim.x)
+      if (S.out_off + d < out_limit) out[S.out_off + d] = S.base + s_tot[d];
+    for (int d = w; d < D; d += nw) {
+      const uint32_t* row = cnt + t0 + (uint64_t)d * S.nt;
+      uint64_t* brow = base + t0 + (uint64_t)d * S.nt;
+      uint64_t carry = S.base + s_tot[d];
+      for (uint32_t j0 = 0; j0 < S.nt; j0 += 32) {
+        const uint32_t j = j0 + lane;
+        const uint64_t x = (j < S.nt) ? row[j] : 0;
+        uint64_t y = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint64_t z = __shfl_up_sync(kFull, y, o);
+          if (lane >= (uint32_t)o) y += z;
+        }
+        if (j < S.nt) brow[j] = carry + y - x;
+        carry += __shfl_sync(kFull, y, 31);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Record decoders for k_p2.
+// DecR1 (level 2): R1 -> R2; digit = fine digit B; source high bits from the
+// coarse bucket's seg_hi row (h = h0 + #boundaries <= position).
+struct DecR1 {
+  int L;
+  uint32_t src_mask;
+  int shB;
+  uint32_t maskB;
+  uint32_t lvmask;  // (1 << (c + gbits)) - 1
+  int nbs;
+  uint32_t nh;
+  const uint64_t* seg_hi;
+  static constexpr bool kSrcHigh = true;
+  __device__ __forceinline__ uint32_t digit(uint32_t r) const { return (r >> shB) & maskB; }
+  __device__ __forceinline__ uint32_t payload(uint32_t r, uint32_t h) const {
+    return (((r >> L) & lvmask) << nbs) | (h << L) | (r & src_mask);
+  }
+};
+// DecR2 (level 3, big fine buckets): R2 -> source; digit = low digit C.
+struct DecR2 {
+  int nbs;
+  uint32_t src_mask;
+  uint32_t maskC;
+  static constexpr bool kSrcHigh = false;
+  __device__ __forceinline__ uint32_t digit(uint32_t r) const { return (r >> nbs) & maskC; }
+  __device__ __forceinline__ uint32_t payload(uint32_t r, uint32_t) const { return r & src_mask; }
+};
+
+inline size_t smem_p2(int D, int mode) {
+  return (size_t)PTP * 4 + (size_t)PT * 2 + (size_t)round4(D * WP) * 4 * (mode == kRankSafe ? 2 : 1) +
+         (size_t)D * 4 * 4 + 40 * 4 + (size_t)kMaxBnd * 4;
+}
+
+// Owner search over a u32 boundary list (positions relative to the tile):
+// result for lane l = largest k in [cur, upper] with k == cur or b(k) <= p0 + l.
+template <class F>
+__device__ __forceinline__ uint32_t slot_owner32(uint32_t& cur, uint32_t& nb, uint32_t p0, uint32_t upper, F bnd_at) {
+  if (nb > p0 + 31) return cur;
+  const uint32_t lane = lane_id();
+  uint32_t base = cur, acc = 0, res;
+  while (true) {
+    const uint32_t kk = base + 1 + lane;
+    const uint32_t bj = (kk <= upper) ? bnd_at(kk) : 0xffffffffu;
+    const uint32_t rel = (bj <= p0 + 31) ? bj - p0 : 32u;
+    acc += count_le_lane(rel, lane);
+    if (__shfl_sync(kFull, rel, 31) >= 32) break;
+    base += 32;
+  }
+  res = cur + acc;
+  cur = __shfl_sync(kFull, res, 31);
+  nb = (cur + 1 <= upper) ? bnd_at(cur + 1) : 0xffffffffu;
+  return res;
+}
+
+// Place: per tile, place tiles of PT records are ranked by digit, staged with
+// their global indices, and written out (persistent, grid-stride over tiles).
+template <int kMode, class Dec>
+__global__ void __launch_bounds__(T, 3) k_p2(const uint32_t* __restrict__ rec, const RTile* __restrict__ tiles,
+                                             const uint32_t* __restrict__ n_tiles, int D, Dec dec,
+                                             const uint64_t* __restrict__ base, uint32_t* __restrict__ out) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem);                         // PTP
+  uint16_t* s_tag = reinterpret_cast<uint16_t*>(s_buf + PTP);                 // PT (digit of each staged slot)
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_tag + PT);                   // D * WP (digit-major)
+  uint32_t* s_scr = s_cnt + round4(D * WP);
+  uint32_t* s_gcur = s_scr + (kMode == kRankSafe ? round4(D * WP) : 0);        // D
+  uint32_t* s_delta = s_gcur + D;                                              // D
+  uint32_t* s_dstart = s_delta + D;                                            // D
+  uint32_t* s_dtot = s_dstart + D;                                             // D
+  uint32_t* s_tmp = s_dtot + D;                                                // 40
+  uint32_t* s_bnd = s_tmp + 40;                                                // kMaxBnd
+  __shared__ __align__(8) uint64_t s_bar;
+
+  const uint32_t tid = threadIdx.x, lane = lane_id(), w = warp_id();
+  const uint32_t ntall = *n_tiles;
+  zero_u32(s_cnt, round4(D * WP) * (kMode == kRankSafe ? 2 : 1));
+  if (tid == 0) {
+    mbar_init(&s_bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t ph = 0;
+
+  for (uint32_t g = blockIdx.x; g < ntall; g += gridDim.x) {
+    const RTile t = tiles[g];
+    const uint64_t row0 = (uint64_t)(g - t.j) * D + t.j;
+    for (int d = tid; d < D; d += T) s_gcur[d] = (uint32_t)base[row0 + (uint64_t)d * t.nt];
+    const uint32_t nbt = Dec::kSrcHigh ? t.nbnd : 0u;
+    const uint64_t* hrow = nullptr;
+    if constexpr (Dec::kSrcHigh) {
+      hrow = dec.seg_hi + (uint64_t)t.seg * (dec.nh + 1) + t.h0 + 1;  // boundary k (1-based) = hrow[k - 1]
+      if (nbt <= (uint32_t)kMaxBnd)
+        for (uint32_t q = tid; q < nbt; q += T) s_bnd[q] = (uint32_t)(hrow[q] - t.start);
+    }
+    const int nplace = (int)((t.n + PT - 1) / PT);
+    auto issue = [&](int jj) {  // thread 0
+      const uint64_t pt = t.start + (uint64_t)jj * PT;
+      const uint32_t n = min((uint32_t)PT, t.n - jj * PT);
+      const uint32_t* gp = rec + pt;
+      const uint32_t o = align_items_u32(gp);
+      const uint32_t full = (o + n) & ~3u;
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&s_bar, full * 4);
+      if (full) bulk_g2s(s_buf, gp - o, full * 4, &s_bar);
+      if (jj + 1 < nplace) {
+        const uint32_t* gn = gp + PT;
+        const uint32_t on = align_items_u32(gn);
+        const uint32_t nn = min((uint32_t)PT, t.n - (jj + 1) * PT);
+        const uint32_t fn = (on + nn) & ~3u;
+        if (fn) bulk_prefetch_l2(gn - on, fn * 4);
+      }
+    };
+    __syncthreads();  // s_gcur / s_bnd visible; the previous tile's buffers are free
+    if (tid == 0 && nplace > 0) issue(0);
+    for (int jj = 0; jj < nplace; ++jj) {
+      const uint64_t pt = t.start + (uint64_t)jj * PT;
+      const uint32_t n = min((uint32_t)PT, t.n - jj * PT);
+      const uint32_t* gp = rec + pt;
+      const uint32_t o = align_items_u32(gp);
+      const uint32_t full = (o + n) & ~3u;
+      const uint32_t ti = full + tid;
+      const bool tail = tid < 4 && ti < o + n;
+      uint32_t tv = 0;
+      if (tail) tv = ldg_u32(gp - o + ti);
+      mbar_wait_parity(&s_bar, ph);
+      ph ^= 1;
+      if (tail) s_buf[ti] = tv;
+      __syncthreads();  // (A)
+
+      const uint32_t iw = w * (K * 32);
+      const uint32_t rel0 = (uint32_t)jj * PT;  // tile-relative position of item 0
+      uint32_t cur = 0, nb = 0xffffffffu;
+      auto bnd_at = [&](uint32_t kk) -> uint32_t {  // kk in [1, nbt]
+        return (nbt <= (uint32_t)kMaxBnd) ? s_bnd[kk - 1] : (uint32_t)(hrow[kk - 1] - t.start);
+      };
+      if constexpr (Dec::kSrcHigh) {
+        if (nbt) {
+          cur = owner_search(0u, nbt, (uint64_t)rel0 + iw, [&](uint64_t kk) -> uint64_t { return bnd_at((uint32_t)kk); });
+          nb = (cur + 1 <= nbt) ? bnd_at(cur + 1) : 0xffffffffu;
+        }
+      }
+      // warps whose 512 items hold no source-high boundary keep h constant
+      const bool wbnd = nb <= rel0 + iw + (K * 32 - 1);
+      uint32_t pay[K], pk[K];
+      auto slot = [&](int s, bool valid) {
+        const uint32_t i0 = iw + s * 32, i = i0 + lane;
+        const uint32_t r = valid ? s_buf[o + i] : 0u;
+        uint32_t h = t.h0;
+        if constexpr (Dec::kSrcHigh) h += wbnd ? slot_owner32(cur, nb, rel0 + i0, nbt, bnd_at) : cur;
+        const uint32_t d = dec.digit(r);
+        pk[s] = (d << 16) | rank_at<kMode>(s_cnt + d * WP + w, s_scr + d * WP + w, valid);
+        pay[s] = dec.payload(r, h);
+      };
+      if (n == (uint32_t)PT) {
+#pragma unroll
+        for (int s = 0; s < K; ++s) slot(s, true);
+      } else {
+#pragma unroll
+        for (int s = 0; s < K; ++s) slot(s, iw + s * 32 + lane < n);
+      }
+      __syncthreads();  // (B)
+      flat_bases<W>(s_cnt, D, s_gcur, s_dstart, s_dtot, s_delta, s_tmp);
+#pragma unroll
+      for (int s = 0; s < K; ++s) {
+        if (n == (uint32_t)PT || iw + s * 32 + lane < n) {
+          const uint32_t d = pk[s] >> 16;
+          const uint32_t pos = s_cnt[d * WP + w] + (pk[s] & 0xffffu);
+          s_buf[pos] = pay[s];
+          s_tag[pos] = (uint16_t)d;
+        }
+      }
+      __syncthreads();  // (C)
+      writeout_tag(out, s_buf, s_tag, s_delta, n);
+      zero_u32(s_cnt, round4(D * WP));
+      for (int d = tid; d < D; d += T) s_gcur[d] += s_dtot[d];
+      fence_proxy_async_smem();
+      __syncthreads();  // (D)
+      if (tid == 0 && jj + 1 < nplace) issue(jj + 1);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- L3 units
+struct P3Args {
+  const uint32_t* rec;  // R2 at CSC positions
+  const Unit3* units;
+  const uint32_t* n_units;
+  unsigned int* ctr;
+  int c, nbs, gbits;
+  uint32_t src_mask, lvmask;
+  uint64_t V;
+  uint64_t* t_offsets;
+  uint32_t* t_edges;
+};
+
+inline size_t smem_p3(int mode) {
+  return (size_t)2 * CAP3P * 4 + (size_t)round4(ML3 * W3P) * 4 * (mode == kRankSafe ? 2 : 1) + (size_t)ML3 * 8 + 40 * 4;
+}
+
+template <int kMode>
+__global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
+  constexpr int TT = W3 * 32;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem);       // 2 * CAP3P
+  uint32_t* s_cnt = s_buf + 2 * CAP3P;                       // ML3 * W3P (digit-major)
+  uint32_t* s_scr = s_cnt + round4(ML3 * W3P);               // (safe)
+  uint32_t* s_dstart = s_scr + (kMode == kRankSafe ? round4(ML3 * W3P) : 0);
+  uint32_t* s_dtot = s_dstart + ML3;
+  uint32_t* s_tmp = s_dtot + ML3;
+  __shared__ __align__(8) uint64_t s_bar[2];
+  __shared__ uint32_t s_uidx[2];
+
+  const uint32_t tid = threadIdx.x, lane = lane_id(), w = warp_id();
+  const uint32_t nun = *a.n_units;
+  zero_u32(s_cnt, round4(ML3 * W3P) * (kMode == kRankSafe ? 2 : 1));
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    fence_mbar_init();
+  }
+  auto issue = [&](uint32_t ui, int b) {  // thread 0
+    const Unit3 u = a.units[ui];
+    const uint32_t* gp = a.rec + u.start;
+    const uint32_t o = align_items_u32(gp);
+    const uint32_t full = (o + u.n) & ~3u;
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&s_bar[b], full * 4);
+    if (full) bulk_g2s(s_buf + b * CAP3P, gp - o, full * 4, &s_bar[b]);
+  };
+  if (tid == 0) {
+    const uint32_t u0 = atomicAdd(a.ctr, 1u);
+    s_uidx[0] = u0;
+    if (u0 < nun) issue(u0, 0);
+  }
+  __syncthreads();
+  const uint32_t lvoff_mask = (1u << a.gbits) - 1;
+  uint32_t ph0 = 0, ph1 = 0;
+  for (int it = 0;; ++it) {
+    const int b = it & 1;
+    const uint32_t ui = s_uidx[b];
+    if (ui >= nun) break;
+    if (tid == 0) {  // prefetch the next unit into the other buffer (its last bulk store must have read it)
+      const uint32_t un = atomicAdd(a.ctr, 1u);
+      s_uidx[b ^ 1] = un;
+      bulk_wait_read<0>();
+      if (un < nun) issue(un, b ^ 1);
+    }
+    const Unit3 u = a.units[ui];
+    const uint32_t n = u.n;
+    const uint32_t* gp = a.rec + u.start;
+    const uint32_t o = align_items_u32(gp);
+    const uint32_t full = (o + n) & ~3u;
+    uint32_t* buf = s_buf + b * CAP3P;
+    const uint32_t ti = full + tid;
+    const bool tail = tid < 4 && ti < o + n;
+    uint32_t tv = 0;
+    if (tail) tv = ldg_u32(gp - o + ti);
+    if (b == 0) { mbar_wait_parity(&s_bar[0], ph0); ph0 ^= 1; }
+    else { mbar_wait_parity(&s_bar[1], ph1); ph1 ^= 1; }
+    if (tail) buf[ti] = tv;
+    __syncthreads();  // (A)
+    const uint32_t nloc = u.nf << a.c;
+    const uint32_t lvoff = (u.f0 & lvoff_mask) << a.c;
+    const uint32_t seg0 = w * (K3 * 32);
+    uint32_t rr[K3], pk[K3];
+#pragma unroll
+    for (int s = 0; s < K3; ++s) {
+      const uint32_t i = seg0 + s * 32 + lane;
+      const bool valid = i < n;
+      const uint32_t r = valid ? buf[o + i] : 0u;
+      const uint32_t lv = valid ? (((r >> a.nbs) & a.lvmask) - lvoff) : 0u;
+      pk[s] = (lv << 16) | rank_at<kMode>(s_cnt + lv * W3P + w, s_scr + lv * W3P + w, valid);
+      rr[s] = r & a.src_mask;
+    }
+    __syncthreads();  // (B)
+    flat_bases<W3>(s_cnt, (int)nloc, nullptr, s_dstart, s_dtot, nullptr, s_tmp);
+    {
+      const uint64_t v0 = (uint64_t)u.f0 << a.c;
+      for (uint32_t v = tid; v < nloc; v += TT)
+        if (v0 + v < a.V) a.t_offsets[v0 + v] = u.start + s_dstart[v];
+    }
+    uint32_t* t_e = a.t_edges + u.start;
+    const uint32_t oo = align_items_u32(t_e);  // staging offset matching the output's 16B alignment
+#pragma unroll
+    for (int s = 0; s < K3; ++s)
+      if (seg0 + s * 32 + lane < n) buf[oo + s_cnt[(pk[s] >> 16) * W3P + w] + (pk[s] & 0xffffu)] = rr[s];
+    fence_proxy_async_smem();
+    __syncthreads();  // (C)
+    {
+      const uint32_t head = min(n, (4 - oo) & 3);
+      const uint32_t mid = (n - head) & ~3u;
+      if (mid && tid == 0) {
+        bulk_s2g(t_e + head, buf + oo + head, mid * 4);
+        bulk_commit();
+      }
+      if (tid < head) t_e[tid] = buf[oo + tid];
+      const uint32_t tl = head + mid + tid;
+      if (tl < n && tid < 4) t_e[tl] = buf[oo + tl];
+    }
+    zero_u32(s_cnt, round4(ML3 * W3P));
+    __syncthreads();  // (D)
+  }
+  if (tid == 0) bulk_wait_read<0>();
+}
+
+// ---------------------------------------------------------------- planning
+// Coarse buckets -> L2 tiles: cstart[c] (c <= D1), cfirst[c] = first tile of
+// bucket c (exclusive prefix of ceil(size / CT2)), cfirst[D1] = tile count.
+__global__ void k_coarse_tiles(const uint64_t* __restrict__ tbase, uint64_t ntiles1, int D1, uint64_t E,
+                               uint64_t* __restrict__ cstart, uint32_t* __restrict__ cfirst) {
+  extern __shared__ uint32_t s_n[];
+  __shared__ uint32_t s_tmp[40];
+  for (int c = threadIdx.x; c <= D1; c += blockDim.x) cstart[c] = (c < D1) ? tbase[(uint64_t)c * ntiles1] : E;
+  __syncthreads();
+  for (int c = threadIdx.x; c < D1; c += blockDim.x) {
+    const uint64_t sz = cstart[c + 1] - cstart[c];
+    s_n[c] = (uint32_t)((sz + CT2 - 1) / CT2);
+  }
+  __syncthreads();
+  const uint32_t total = block_excl_scan_u32(s_n, D1, s_tmp);
+  for (int c = threadIdx.x; c < D1; c += blockDim.x) cfirst[c] = s_n[c];
+  if (threadIdx.x == 0) cfirst[D1] = total;
+}
+
+// One CTA per coarse bucket: its tiles (with the R1 source-high decode state)
+// and its segment descriptor.
+__global__ void k_l2_tiles(const uint64_t* __restrict__ cstart, const uint32_t* __restrict__ cfirst, int Db,
+                           const uint64_t* __restrict__ seg_hi, uint32_t nh, RTile* __restrict__ tiles,
+                           SegDesc* __restrict__ segs) {
+  const uint32_t c = blockIdx.x;
+  const uint32_t g0 = cfirst[c], nt = cfirst[c + 1] - g0;
+  const uint64_t cs = cstart[c], ce = cstart[c + 1];
+  if (threadIdx.x == 0) {
+    SegDesc S;
+    S.base = cs;
+    S.out_off = (uint64_t)c * Db;
+    S.g0 = g0;
+    S.nt = nt;
+    segs[c] = S;
+  }
+  const uint64_t* row = seg_hi + (uint64_t)c * (nh + 1);
+  for (uint32_t j = threadIdx.x; j < nt; j += blockDim.x) {
+    const uint64_t st = cs + (uint64_t)j * CT2;
+    const uint32_t n = (uint32_t)umin64(CT2, ce - st);
+    // h0 = #{h in [1, nh] : row[h] <= st}; hi = #{h : row[h] <= st + n - 1}
+    auto cnt_le = [&](uint64_t x) -> uint32_t {
+      uint32_t lo = 0, hi = nh;  // answer in [0, nh]
+      while (lo < hi) {
+        const uint32_t mid = lo + (hi - lo + 1) / 2;
+        if (row[mid] <= x) lo = mid; else hi = mid - 1;
+      }
+      return lo;
+    };
+    RTile t;
+    t.start = st;
+    t.n = n;
+    t.seg = c;
+    t.j = j;
+    t.nt = nt;
+    t.h0 = cnt_le(st);
+    t.nbnd = cnt_le(st + n - 1) - t.h0;
+    tiles[g0 + j] = t;
+  }
+}
+
+// L3 plan: one thread per aligned group of G fine buckets.  Small fine
+// buckets are packed into units (<= CAP3 records, one group); fine buckets
+// above CAP3 become big buckets.  fbase[f] = CSC start of fine bucket f,
+// fbase[nfine] = E.
+struct Big3 {
+  uint64_t start;
+  uint64_t n;
+  uint32_t f;
+  uint32_t pad;
+};
+__global__ void k_plan3(const uint64_t* __restrict__ fbase, uint32_t nfine, int gbits, Unit3* __restrict__ units,
+                        uint32_t* __restrict__ n_units, Big3* __restrict__ bigs, uint32_t* __restrict__ n_big) {
+  const uint32_t G = 1u << gbits;
+  const uint32_t grp = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t f_begin = grp * G;
+  if (f_begin >= nfine) return;
+  const uint32_t f_end = min(nfine, f_begin + G);
+  uint32_t f = f_begin;
+  while (f < f_end) {
+    const uint64_t s = fbase[f], sz = fbase[f + 1] - s;
+    if (sz > (uint64_t)CAP3) {
+      const uint32_t q = atomicAdd(n_big, 1u);
+      Big3 bg;
+      bg.start = s;
+      bg.n = sz;
+      bg.f = f;
+      bg.pad = 0;
+      bigs[q] = bg;
+      ++f;
+      continue;
+    }
+    uint64_t tot = sz;
+    uint32_t e = f + 1;
+    while (e < f_end) {
+      const uint64_t z = fbase[e + 1] - fbase[e];
+      if (z > (uint64_t)CAP3 || tot + z > (uint64_t)CAP3) break;
+      tot += z;
+      ++e;
+    }
+    Unit3 u;
+    u.start = s;
+    u.n = (uint32_t)tot;
+    u.f0 = f;
+    u.nf = e - f;
+    u.pad = 0;
+    units[atomicAdd(n_units, 1u)] = u;
+    f = e;
+  }
+}
+
+// Big fine buckets -> L3 tiles and segments (one CTA).  The biggest buckets go
+// first in the tile order (persistent CTAs then start on them).
+__global__ void __launch_bounds__(1024) k_big_tiles(const Big3* __restrict__ bigs, const uint32_t* __restrict__ n_big,
+                                                    int c, RTile* __restrict__ tiles, uint32_t* __restrict__ n_tiles,
+                                                    SegDesc* __restrict__ segs) {
+  __shared__ uint32_t s_tmp[40];
+  __shared__ uint32_t s_cnt[1024];
+  const uint32_t nb = *n_big;
+  uint32_t carry = 0;
+  for (uint32_t q0 = 0; q0 < nb; q0 += blockDim.x) {
+    const uint32_t q = q0 + threadIdx.x;
+    Big3 bg{};
+    uint32_t nt = 0;
+    if (q < nb) {
+      bg = bigs[q];
+      nt = (uint32_t)((bg.n + CT2 - 1) / CT2);
+    }
+    s_cnt[threadIdx.x] = nt;
+    __syncthreads();
+    const uint32_t tot = block_excl_scan_u32(s_cnt, blockDim.x, s_tmp);
+    const uint32_t g0 = carry + s_cnt[threadIdx.x];
+    if (q < nb) {
+      SegDesc S;
+      S.base = bg.start;
+      S.out_off = (uint64_t)bg.f << c;
+      S.g0 = g0;
+      S.nt = nt;
+      segs[q] = S;
+      for (uint32_t j = 0; j < nt; ++j) {
+        RTile t;
+        t.start = bg.start + (uint64_t)j * CT2;
+        t.n = (uint32_t)umin64(CT2, bg.n - (uint64_t)j * CT2);
+        t.seg = q;
+        t.j = j;
+        t.nt = nt;
+        t.h0 = 0;
+        t.nbnd = 0;
+        tiles[g0 + j] = t;
+      }
+    }
+    carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *n_tiles = carry;
+}
+
+}  // namespace v3
+}  // namespace gt
