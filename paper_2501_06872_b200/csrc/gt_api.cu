@@ -677,6 +677,10 @@ void make_plan3(const Plan& p, Plan3& q) {
 }
 
 __global__ void k_set_u32(uint32_t* p, uint32_t v) { *p = v; }
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
 
 template <int kMode>
 int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges, unsigned char* ws, cudaStream_t st,
@@ -776,10 +780,17 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
     dec.nbs = p.nbs;
     dec.nh = nh;
     dec.seg_hi = seghi;
-    const size_t sm = smem_p2(Db, kMode);
-    if ((rc = set_smem(k_p2<kMode, DecR1>, sm))) return rc;
-    const unsigned g = persistent_grid(k_p2<kMode, DecR1>, T, sm, q.max_t2);
-    k_p2<kMode, DecR1><<<g, T, sm, st>>>(t_edges, tiles2, cfirst + D1, Db, dec, base2, r2);
+    if (env_int("GT_K2", 32) == 32) {
+      const size_t sm = smem_p2(Db, kMode, 32);
+      if ((rc = set_smem(k_p2<kMode, DecR1, 32>, sm))) return rc;
+      const unsigned g = persistent_grid(k_p2<kMode, DecR1, 32>, T, sm, q.max_t2);
+      k_p2<kMode, DecR1, 32><<<g, T, sm, st>>>(t_edges, tiles2, cfirst + D1, Db, dec, base2, r2);
+    } else {
+      const size_t sm = smem_p2(Db, kMode, 16);
+      if ((rc = set_smem(k_p2<kMode, DecR1, 16>, sm))) return rc;
+      const unsigned g = persistent_grid(k_p2<kMode, DecR1, 16>, T, sm, q.max_t2);
+      k_p2<kMode, DecR1, 16><<<g, T, sm, st>>>(t_edges, tiles2, cfirst + D1, Db, dec, base2, r2);
+    }
     GT_LAUNCH_CHECK();
   }
   launches += 5;
@@ -803,10 +814,10 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
     dec.nbs = p.nbs;
     dec.src_mask = (p.nbs >= 32) ? 0xffffffffu : (uint32_t)((1ull << p.nbs) - 1);
     dec.maskC = (uint32_t)(Dc - 1);
-    const size_t sm = smem_p2(Dc, kMode);
-    if ((rc = set_smem(k_p2<kMode, DecR2>, sm))) return rc;
-    const unsigned g = persistent_grid(k_p2<kMode, DecR2>, T, sm, q.max_t3);
-    k_p2<kMode, DecR2><<<g, T, sm, st>>>(r2, tiles3, cnt + 2, Dc, dec, base3, t_edges);
+    const size_t sm = smem_p2(Dc, kMode, 16);
+    if ((rc = set_smem(k_p2<kMode, DecR2, 16>, sm))) return rc;
+    const unsigned g = persistent_grid(k_p2<kMode, DecR2, 16>, T, sm, q.max_t3);
+    k_p2<kMode, DecR2, 16><<<g, T, sm, st>>>(r2, tiles3, cnt + 2, Dc, dec, base3, t_edges);
     GT_LAUNCH_CHECK();
   }
   {

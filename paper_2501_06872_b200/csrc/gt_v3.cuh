@@ -187,6 +187,19 @@ __device__ __forceinline__ uint32_t rank_at(uint32_t* c, uint32_t* sc, bool vali
   }
 }
 
+// Rank with peers from match.any: one atomic per distinct digit (leader), no
+// reliance on the order of same-address lanes.  Cheaper than per-lane atomics
+// when few distinct digits share a warp instruction (hub-dominated buckets).
+__device__ __forceinline__ uint32_t rank_match(uint32_t* cnt, int stride, uint32_t d, bool valid) {
+  const uint32_t lane = lane_id();
+  const uint32_t m = __match_any_sync(kFull, valid ? d : 0xffffffffu);
+  const uint32_t ld = __ffs(m) - 1;
+  uint32_t base = 0;
+  if (valid && lane == ld) base = atomicAdd(cnt + d * stride, (uint32_t)__popc(m));
+  base = __shfl_sync(kFull, base, ld);
+  return base + __popc(m & lanemask_lt());
+}
+
 // In-place exclusive scan of a[0..n) (thread-contiguous chunks, one block scan).
 __device__ __forceinline__ void flat_excl_scan(uint32_t* a, int n, uint32_t* tmp /* >= 33 */) {
   const int Tn = blockDim.x, t = threadIdx.x, lane = t & 31, w = t >> 5, nw = (Tn + 31) >> 5;
@@ -333,7 +346,7 @@ struct P1Args {
 };
 
 inline size_t smem_p1(int D, int mode) {
-  return (size_t)PTP * 4 + (size_t)kWin * 8 + (size_t)PT * 6 + (size_t)round4(D * WP) * 4 * (mode == kRankSafe ? 2 : 1) +
+  return (size_t)PTP * 4 + (size_t)kWin * 8 + (size_t)PT * 4 + (size_t)round4(D * WP) * 4 * (mode == kRankSafe ? 2 : 1) +
          (size_t)D * 4 * 5 + 40 * 4 + (CT1 / PT + 4) * 4;
 }
 
@@ -397,8 +410,11 @@ __global__ void __launch_bounds__(T, 3) k_p1(const P1Args a) {
   uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem);                         // PTP (landing, then stage)
   uint64_t* s_win = reinterpret_cast<uint64_t*>(s_buf + PTP);                  // kWin
   uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_win + kWin);                 // PT (source-boundary marks)
-  uint16_t* s_tag = reinterpret_cast<uint16_t*>(s_idx + PT);                   // PT (digit of each staged slot)
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_tag + PT);                   // D * WP (digit-major)
+  // digit of each staged slot: aliases the offsets window (dead after ranking;
+  // the next window lands by TMA after the end-of-tile barrier + proxy fence)
+  static_assert(kWin * 8 >= PT * 2, "tag array must fit in the window");
+  uint16_t* s_tag = reinterpret_cast<uint16_t*>(s_win);
+  uint32_t* s_cnt = s_idx + PT;                                                // D * WP (digit-major)
   uint32_t* s_scr = s_cnt + round4(D * WP);                                    // (safe)
   uint32_t* s_gcur = s_scr + (kMode == kRankSafe ? round4(D * WP) : 0);        // D
   uint32_t* s_delta = s_gcur + D;                                              // D
@@ -656,6 +672,7 @@ struct DecR1 {
   uint32_t nh;
   const uint64_t* seg_hi;
   static constexpr bool kSrcHigh = true;
+  static constexpr bool kMatchRank = false;  // fine digits are spread: lane-ordered atomics
   __device__ __forceinline__ uint32_t digit(uint32_t r) const { return (r >> shB) & maskB; }
   __device__ __forceinline__ uint32_t payload(uint32_t r, uint32_t h) const {
     return (((r >> L) & lvmask) << nbs) | (h << L) | (r & src_mask);
@@ -667,13 +684,15 @@ struct DecR2 {
   uint32_t src_mask;
   uint32_t maskC;
   static constexpr bool kSrcHigh = false;
+  static constexpr bool kMatchRank = true;  // big buckets are dominated by a few hub vertices
   __device__ __forceinline__ uint32_t digit(uint32_t r) const { return (r >> nbs) & maskC; }
   __device__ __forceinline__ uint32_t payload(uint32_t r, uint32_t) const { return r & src_mask; }
 };
 
-inline size_t smem_p2(int D, int mode) {
-  return (size_t)PTP * 4 + (size_t)PT * 2 + (size_t)round4(D * WP) * 4 * (mode == kRankSafe ? 2 : 1) +
-         (size_t)D * 4 * 4 + 40 * 4 + (size_t)kMaxBnd * 4;
+inline size_t smem_p2(int D, int mode, int KK = K) {
+  const size_t pt = (size_t)W * KK * 32;
+  return (pt + 8) * 4 + pt * 2 + (size_t)round4(D * WP) * 4 * (mode == kRankSafe ? 2 : 1) + (size_t)D * 4 * 4 +
+         40 * 4 + (size_t)kMaxBnd * 4;
 }
 
 // Owner search over a u32 boundary list (positions relative to the tile):
@@ -699,10 +718,11 @@ __device__ __forceinline__ uint32_t slot_owner32(uint32_t& cur, uint32_t& nb, ui
 
 // Place: per tile, place tiles of PT records are ranked by digit, staged with
 // their global indices, and written out (persistent, grid-stride over tiles).
-template <int kMode, class Dec>
-__global__ void __launch_bounds__(T, 3) k_p2(const uint32_t* __restrict__ rec, const RTile* __restrict__ tiles,
+template <int kMode, class Dec, int KK>
+__global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __restrict__ rec, const RTile* __restrict__ tiles,
                                              const uint32_t* __restrict__ n_tiles, int D, Dec dec,
                                              const uint64_t* __restrict__ base, uint32_t* __restrict__ out) {
+  constexpr int PT = W * KK * 32, PTP = PT + 8, K = KK;
   extern __shared__ __align__(128) unsigned char smem[];
   uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem);                         // PTP
   uint16_t* s_tag = reinterpret_cast<uint16_t*>(s_buf + PTP);                 // PT (digit of each staged slot)
@@ -793,7 +813,10 @@ __global__ void __launch_bounds__(T, 3) k_p2(const uint32_t* __restrict__ rec, c
         uint32_t h = t.h0;
         if constexpr (Dec::kSrcHigh) h += wbnd ? slot_owner32(cur, nb, rel0 + i0, nbt, bnd_at) : cur;
         const uint32_t d = dec.digit(r);
-        pk[s] = (d << 16) | rank_at<kMode>(s_cnt + d * WP + w, s_scr + d * WP + w, valid);
+        uint32_t rk;
+        if constexpr (Dec::kMatchRank) rk = rank_match(s_cnt + w, WP, d, valid);
+        else rk = rank_at<kMode>(s_cnt + d * WP + w, s_scr + d * WP + w, valid);
+        pk[s] = (d << 16) | rk;
         pay[s] = dec.payload(r, h);
       };
       if (n == (uint32_t)PT) {
