@@ -190,14 +190,92 @@ __device__ __forceinline__ uint32_t rank_at(uint32_t* c, uint32_t* sc, bool vali
 // Rank with peers from match.any: one atomic per distinct digit (leader), no
 // reliance on the order of same-address lanes.  Cheaper than per-lane atomics
 // when few distinct digits share a warp instruction (hub-dominated buckets).
-__device__ __forceinline__ uint32_t rank_match(uint32_t* cnt, int stride, uint32_t d, bool valid) {
+__device__ __forceinline__ uint32_t rank_match(uint32_t* word, uint32_t sh, uint32_t d, bool valid) {
   const uint32_t lane = lane_id();
   const uint32_t m = __match_any_sync(kFull, valid ? d : 0xffffffffu);
   const uint32_t ld = __ffs(m) - 1;
   uint32_t base = 0;
-  if (valid && lane == ld) base = atomicAdd(cnt + d * stride, (uint32_t)__popc(m));
+  if (valid && lane == ld) base = (atomicAdd(word, (uint32_t)__popc(m) << sh) >> sh) & 0xffffu;
   base = __shfl_sync(kFull, base, ld);
   return base + __popc(m & lanemask_lt());
+}
+
+// Packed counter tables: digit-major, two warps per 32-bit word (u16 fields:
+// per-warp counts <= 1024 and tile positions <= 8192 fit), one pad word per
+// digit (odd row stride: random digits spread over banks).
+constexpr int WH = W / 2 + 1;
+constexpr int WH3 = W3 / 2 + 1;
+// Rank through the packed counter word `c` (field at bit `sh` = 16 * (w & 1)).
+// kRankSafe: peers from the OR-mask scratch entry `sc`, one leader per digit
+// adds the group size, so no same-address ordering is assumed.
+template <int kMode>
+__device__ __forceinline__ uint32_t rank_pk(uint32_t* c, uint32_t* sc, uint32_t sh, bool valid) {
+  if constexpr (kMode == kRankAtomic) {
+    (void)sc;
+    return valid ? ((atomicAdd(c, 1u << sh) >> sh) & 0xffffu) : 0u;
+  } else {
+    const uint32_t lane = lane_id();
+    if (valid) atomicOr(sc, 1u << lane);
+    __syncwarp();
+    const uint32_t peers = valid ? *sc : 0u;
+    __syncwarp();
+    const uint32_t ld = peers ? (uint32_t)(__ffs(peers) - 1) : 0u;
+    uint32_t old = 0;
+    if (valid && lane == ld) {
+      old = atomicAdd(c, (uint32_t)__popc(peers) << sh);
+      *sc = 0;
+    }
+    old = __shfl_sync(kFull, old, ld);
+    __syncwarp();
+    return ((old >> sh) & 0xffffu) + __popc(peers & lanemask_lt());
+  }
+}
+// After ranking: tab[d * WHN + k] holds (warp 2k, warp 2k+1) tile positions of
+// their first digit-d item; dtot per digit; delta[d] = gcur[d] - digit start.
+template <int WHN>
+__device__ __forceinline__ void flat_bases_pk(uint32_t* tab, int D, const uint32_t* gcur, uint32_t* dtot,
+                                              uint32_t* delta, uint32_t* tmp) {
+  const int n = D * WHN;
+  const int Tn = blockDim.x, t = threadIdx.x, lane = t & 31, w = t >> 5, nw = (Tn + 31) >> 5;
+  const int per = (n + Tn - 1) / Tn;
+  const int lo = min(n, t * per), hi = min(n, lo + per);
+  uint32_t s = 0;
+  for (int i = lo; i < hi; ++i) {
+    const uint32_t v = tab[i];
+    s += (v & 0xffffu) + (v >> 16);
+  }
+  uint32_t x = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) tmp[w] = x;
+  __syncthreads();
+  if (t < 32) {
+    const uint32_t v0 = (t < nw) ? tmp[t] : 0u;
+    uint32_t v = v0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, v, o);
+      if (t >= o) v += y;
+    }
+    if (t < nw) tmp[t] = v - v0;
+  }
+  __syncthreads();
+  uint32_t run = tmp[w] + x - s;
+  for (int i = lo; i < hi; ++i) {
+    const uint32_t v = tab[i], l = v & 0xffffu;
+    tab[i] = run | ((run + l) << 16);
+    run += l + (v >> 16);
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    const uint32_t b = tab[d * WHN] & 0xffffu;
+    if (dtot) dtot[d] = (tab[d * WHN + WHN - 1] & 0xffffu) - b;
+    if (gcur) delta[d] = gcur[d] - b;
+  }
+  __syncthreads();
 }
 
 // In-place exclusive scan of a[0..n) (thread-contiguous chunks, one block scan).
@@ -346,7 +424,7 @@ struct P1Args {
 };
 
 inline size_t smem_p1(int D, int mode) {
-  return (size_t)PTP * 4 + (size_t)kWin * 8 + (size_t)PT * 4 + (size_t)round4(D * WP) * 4 * (mode == kRankSafe ? 2 : 1) +
+  return (size_t)PTP * 4 + (size_t)kWin * 8 + (size_t)PT * 4 + ((size_t)round4(D * WH) + (mode == kRankSafe ? (size_t)round4(D * WP) : 0)) * 4 +
          (size_t)D * 4 * 5 + 40 * 4 + (CT1 / PT + 4) * 4;
 }
 
@@ -414,8 +492,8 @@ __global__ void __launch_bounds__(T, 3) k_p1(const P1Args a) {
   // the next window lands by TMA after the end-of-tile barrier + proxy fence)
   static_assert(kWin * 8 >= PT * 2, "tag array must fit in the window");
   uint16_t* s_tag = reinterpret_cast<uint16_t*>(s_win);
-  uint32_t* s_cnt = s_idx + PT;                                                // D * WP (digit-major)
-  uint32_t* s_scr = s_cnt + round4(D * WP);                                    // (safe)
+  uint32_t* s_cnt = s_idx + PT;                                                // D * WH (packed, digit-major)
+  uint32_t* s_scr = s_cnt + round4(D * WH);                                    // D * WP (safe)
   uint32_t* s_gcur = s_scr + (kMode == kRankSafe ? round4(D * WP) : 0);        // D
   uint32_t* s_delta = s_gcur + D;                                              // D
   uint32_t* s_dstart = s_delta + D;                                            // D
@@ -429,13 +507,14 @@ __global__ void __launch_bounds__(T, 3) k_p1(const P1Args a) {
   __shared__ uint32_t s_last_src;
 
   const uint32_t tid = threadIdx.x, lane = lane_id(), w = warp_id();
+  const uint32_t sh = (w & 1) << 4;
   const uint64_t k = blockIdx.x;
   const uint64_t tb = k * CT1, te = umin64(a.E, tb + CT1);
   const int nplace = (int)((te - tb + PT - 1) / PT);
   const uint64_t gp0 = tb / PT;
   for (int d = tid; d < D; d += T) s_gcur[d] = (uint32_t)a.tbase[(uint64_t)d * a.ntiles + k];
   for (int j = tid; j <= nplace; j += T) s_psrc[j] = a.psrc[gp0 + j];
-  zero_u32(s_cnt, round4(D * WP) * (kMode == kRankSafe ? 2 : 1));
+  zero_u32(s_cnt, round4(D * WH) + (kMode == kRankSafe ? round4(D * WP) : 0));
   zero_u32(s_idx, PT);
   if (tid == 0) {
     mbar_init(&s_bar, 1);
@@ -524,7 +603,7 @@ __global__ void __launch_bounds__(T, 3) k_p1(const P1Args a) {
       }
       if (valid && i == n - 1) s_last_src = src;
       const uint32_t d = dst >> a.shift;
-      pk[s] = (d << 16) | rank_at<kMode>(s_cnt + d * WP + w, s_scr + d * WP + w, valid);
+      pk[s] = (d << 16) | rank_pk<kMode>(s_cnt + d * WH + (w >> 1), s_scr + d * WP + w, sh, valid);
       pay[s] = ((dst & a.low_mask) << a.L) | (src & a.src_mask);
     };
     if (n == (uint32_t)PT) {
@@ -535,7 +614,7 @@ __global__ void __launch_bounds__(T, 3) k_p1(const P1Args a) {
       for (int s = 0; s < K; ++s) slot(s, iw + s * 32 + lane < n);
     }
     __syncthreads();  // (B) ranks done; landing buffer and marks consumed
-    flat_bases<W>(s_cnt, D, s_gcur, s_dstart, s_dtot, s_delta, s_tmp);
+    flat_bases_pk<WH>(s_cnt, D, s_gcur, s_dtot, s_delta, s_tmp);
     // source-high boundaries inside this tile (compact R1 decode table)
     const uint32_t h_last = s_last_src >> a.L;
     for (uint32_t h = (h_prev == 0xffffffffu) ? 0u : h_prev + 1; h <= h_last; ++h) {
@@ -557,7 +636,7 @@ __global__ void __launch_bounds__(T, 3) k_p1(const P1Args a) {
     for (int s = 0; s < K; ++s) {
       if (n == (uint32_t)PT || iw + s * 32 + lane < n) {
         const uint32_t d = pk[s] >> 16;
-        const uint32_t pos = s_cnt[d * WP + w] + (pk[s] & 0xffffu);
+        const uint32_t pos = ((s_cnt[d * WH + (w >> 1)] >> sh) & 0xffffu) + (pk[s] & 0xffffu);
         s_buf[pos] = pay[s];
         s_tag[pos] = (uint16_t)d;
       }
@@ -565,7 +644,7 @@ __global__ void __launch_bounds__(T, 3) k_p1(const P1Args a) {
     __syncthreads();  // (C)
     writeout_tag(a.out, s_buf, s_tag, s_delta, n);
     zero_u32(s_idx, PT);
-    zero_u32(s_cnt, round4(D * WP));
+    zero_u32(s_cnt, round4(D * WH));
     for (int d = tid; d < D; d += T) s_gcur[d] += s_dtot[d];
     fence_proxy_async_smem();
     __syncthreads();  // (D)
@@ -691,7 +770,7 @@ struct DecR2 {
 
 inline size_t smem_p2(int D, int mode, int KK = K) {
   const size_t pt = (size_t)W * KK * 32;
-  return (pt + 8) * 4 + pt * 2 + (size_t)round4(D * WP) * 4 * (mode == kRankSafe ? 2 : 1) + (size_t)D * 4 * 4 +
+  return (pt + 8) * 4 + pt * 2 + ((size_t)round4(D * WH) + (mode == kRankSafe ? (size_t)round4(D * WP) : 0)) * 4 + (size_t)D * 4 * 4 +
          40 * 4 + (size_t)kMaxBnd * 4;
 }
 
@@ -726,8 +805,8 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __r
   extern __shared__ __align__(128) unsigned char smem[];
   uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem);                         // PTP
   uint16_t* s_tag = reinterpret_cast<uint16_t*>(s_buf + PTP);                 // PT (digit of each staged slot)
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_tag + PT);                   // D * WP (digit-major)
-  uint32_t* s_scr = s_cnt + round4(D * WP);
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_tag + PT);                   // D * WH (packed, digit-major)
+  uint32_t* s_scr = s_cnt + round4(D * WH);                                    // D * WP (safe)
   uint32_t* s_gcur = s_scr + (kMode == kRankSafe ? round4(D * WP) : 0);        // D
   uint32_t* s_delta = s_gcur + D;                                              // D
   uint32_t* s_dstart = s_delta + D;                                            // D
@@ -737,8 +816,9 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __r
   __shared__ __align__(8) uint64_t s_bar;
 
   const uint32_t tid = threadIdx.x, lane = lane_id(), w = warp_id();
+  const uint32_t sh = (w & 1) << 4;
   const uint32_t ntall = *n_tiles;
-  zero_u32(s_cnt, round4(D * WP) * (kMode == kRankSafe ? 2 : 1));
+  zero_u32(s_cnt, round4(D * WH) + (kMode == kRankSafe ? round4(D * WP) : 0));
   if (tid == 0) {
     mbar_init(&s_bar, 1);
     fence_mbar_init();
@@ -814,8 +894,8 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __r
         if constexpr (Dec::kSrcHigh) h += wbnd ? slot_owner32(cur, nb, rel0 + i0, nbt, bnd_at) : cur;
         const uint32_t d = dec.digit(r);
         uint32_t rk;
-        if constexpr (Dec::kMatchRank) rk = rank_match(s_cnt + w, WP, d, valid);
-        else rk = rank_at<kMode>(s_cnt + d * WP + w, s_scr + d * WP + w, valid);
+        if constexpr (Dec::kMatchRank) rk = rank_match(s_cnt + d * WH + (w >> 1), sh, d, valid);
+        else rk = rank_pk<kMode>(s_cnt + d * WH + (w >> 1), s_scr + d * WP + w, sh, valid);
         pk[s] = (d << 16) | rk;
         pay[s] = dec.payload(r, h);
       };
@@ -827,19 +907,19 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __r
         for (int s = 0; s < K; ++s) slot(s, iw + s * 32 + lane < n);
       }
       __syncthreads();  // (B)
-      flat_bases<W>(s_cnt, D, s_gcur, s_dstart, s_dtot, s_delta, s_tmp);
+      flat_bases_pk<WH>(s_cnt, D, s_gcur, s_dtot, s_delta, s_tmp);
 #pragma unroll
       for (int s = 0; s < K; ++s) {
         if (n == (uint32_t)PT || iw + s * 32 + lane < n) {
           const uint32_t d = pk[s] >> 16;
-          const uint32_t pos = s_cnt[d * WP + w] + (pk[s] & 0xffffu);
+          const uint32_t pos = ((s_cnt[d * WH + (w >> 1)] >> sh) & 0xffffu) + (pk[s] & 0xffffu);
           s_buf[pos] = pay[s];
           s_tag[pos] = (uint16_t)d;
         }
       }
       __syncthreads();  // (C)
       writeout_tag(out, s_buf, s_tag, s_delta, n);
-      zero_u32(s_cnt, round4(D * WP));
+      zero_u32(s_cnt, round4(D * WH));
       for (int d = tid; d < D; d += T) s_gcur[d] += s_dtot[d];
       fence_proxy_async_smem();
       __syncthreads();  // (D)
@@ -862,7 +942,8 @@ struct P3Args {
 };
 
 inline size_t smem_p3(int mode) {
-  return (size_t)2 * CAP3P * 4 + (size_t)round4(ML3 * W3P) * 4 * (mode == kRankSafe ? 2 : 1) + (size_t)ML3 * 8 + 40 * 4;
+  return (size_t)2 * CAP3P * 4 + ((size_t)round4(ML3 * WH3) + (mode == kRankSafe ? (size_t)round4(ML3 * W3P) : 0)) * 4 +
+         (size_t)ML3 * 8 + 40 * 4;
 }
 
 template <int kMode>
@@ -870,8 +951,8 @@ __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
   constexpr int TT = W3 * 32;
   extern __shared__ __align__(128) unsigned char smem[];
   uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem);       // 2 * CAP3P
-  uint32_t* s_cnt = s_buf + 2 * CAP3P;                       // ML3 * W3P (digit-major)
-  uint32_t* s_scr = s_cnt + round4(ML3 * W3P);               // (safe)
+  uint32_t* s_cnt = s_buf + 2 * CAP3P;                       // ML3 * WH3 (packed, digit-major)
+  uint32_t* s_scr = s_cnt + round4(ML3 * WH3);               // ML3 * W3P (safe)
   uint32_t* s_dstart = s_scr + (kMode == kRankSafe ? round4(ML3 * W3P) : 0);
   uint32_t* s_dtot = s_dstart + ML3;
   uint32_t* s_tmp = s_dtot + ML3;
@@ -879,8 +960,9 @@ __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
   __shared__ uint32_t s_uidx[2];
 
   const uint32_t tid = threadIdx.x, lane = lane_id(), w = warp_id();
+  const uint32_t sh = (w & 1) << 4;
   const uint32_t nun = *a.n_units;
-  zero_u32(s_cnt, round4(ML3 * W3P) * (kMode == kRankSafe ? 2 : 1));
+  zero_u32(s_cnt, round4(ML3 * WH3) + (kMode == kRankSafe ? round4(ML3 * W3P) : 0));
   if (tid == 0) {
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
@@ -937,21 +1019,21 @@ __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
       const bool valid = i < n;
       const uint32_t r = valid ? buf[o + i] : 0u;
       const uint32_t lv = valid ? (((r >> a.nbs) & a.lvmask) - lvoff) : 0u;
-      pk[s] = (lv << 16) | rank_at<kMode>(s_cnt + lv * W3P + w, s_scr + lv * W3P + w, valid);
+      pk[s] = (lv << 16) | rank_pk<kMode>(s_cnt + lv * WH3 + (w >> 1), s_scr + lv * W3P + w, sh, valid);
       rr[s] = r & a.src_mask;
     }
     __syncthreads();  // (B)
-    flat_bases<W3>(s_cnt, (int)nloc, nullptr, s_dstart, s_dtot, nullptr, s_tmp);
+    flat_bases_pk<WH3>(s_cnt, (int)nloc, nullptr, nullptr, nullptr, s_tmp);
     {
       const uint64_t v0 = (uint64_t)u.f0 << a.c;
       for (uint32_t v = tid; v < nloc; v += TT)
-        if (v0 + v < a.V) a.t_offsets[v0 + v] = u.start + s_dstart[v];
+        if (v0 + v < a.V) a.t_offsets[v0 + v] = u.start + (s_cnt[v * WH3] & 0xffffu);
     }
     uint32_t* t_e = a.t_edges + u.start;
     const uint32_t oo = align_items_u32(t_e);  // staging offset matching the output's 16B alignment
 #pragma unroll
     for (int s = 0; s < K3; ++s)
-      if (seg0 + s * 32 + lane < n) buf[oo + s_cnt[(pk[s] >> 16) * W3P + w] + (pk[s] & 0xffffu)] = rr[s];
+      if (seg0 + s * 32 + lane < n) buf[oo + ((s_cnt[(pk[s] >> 16) * WH3 + (w >> 1)] >> sh) & 0xffffu) + (pk[s] & 0xffffu)] = rr[s];
     fence_proxy_async_smem();
     __syncthreads();  // (C)
     {
@@ -965,7 +1047,7 @@ __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
       const uint32_t tl = head + mid + tid;
       if (tl < n && tid < 4) t_e[tl] = buf[oo + tl];
     }
-    zero_u32(s_cnt, round4(ML3 * W3P));
+    zero_u32(s_cnt, round4(ML3 * WH3));
     __syncthreads();  // (D)
   }
   if (tid == 0) bulk_wait_read<0>();
