@@ -780,7 +780,7 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
     dec.nbs = p.nbs;
     dec.nh = nh;
     dec.seg_hi = seghi;
-    if (env_int("GT_K2", 32) == 32) {
+    if (env_int("GT_K2", 16) == 32) {
       const size_t sm = smem_p2(Db, kMode, 32);
       if ((rc = set_smem(k_p2<kMode, DecR1, 32>, sm))) return rc;
       const unsigned g = persistent_grid(k_p2<kMode, DecR1, 32>, T, sm, q.max_t2);
@@ -807,7 +807,7 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
     const unsigned gt3 = (unsigned)std::min<uint64_t>(q.max_t3, (uint64_t)sms * 8);
     k_cnt_rec<<<gt3, 512, (size_t)Dc * 4, st>>>(r2, tiles3, cnt + 2, Dc, DigSM{p.nbs, (uint32_t)(Dc - 1)}, cnt3);
     GT_LAUNCH_CHECK();
-    k_segscan<<<(unsigned)std::min<uint64_t>(q.max_big, (uint64_t)sms * 4), 512, (size_t)Dc * 8, st>>>(
+    k_segscan<<<(unsigned)std::min<uint64_t>(q.max_big, (uint64_t)sms * 16), 128, (size_t)Dc * 8, st>>>(
         seg3, cnt + 1, Dc, cnt3, base3, t_offsets, V, err);
     GT_LAUNCH_CHECK();
     DecR2 dec;

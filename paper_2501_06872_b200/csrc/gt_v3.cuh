@@ -40,7 +40,7 @@ constexpr int G1 = 8;            // count tiles per k_c1 CTA
 constexpr int CT2 = 32768;       // L2 / L3-big count tile (records of one segment)
 constexpr int kWin = 1024;       // offsets window (entries) per L1 place tile
 constexpr int kMaxBnd = 512;     // source-high boundaries of an L2 tile held in smem
-constexpr int W3 = 8, K3 = 32;
+constexpr int W3 = 16, K3 = 16;
 constexpr int CAP3 = W3 * K3 * 32;  // 8192 records per L3 unit
 constexpr int CAP3P = CAP3 + 8;
 constexpr int ML3 = 256;            // local vertices per L3 unit
