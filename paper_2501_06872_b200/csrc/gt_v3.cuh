@@ -424,8 +424,8 @@ struct P1Args {
 };
 
 inline size_t smem_p1(int D, int mode) {
-  return (size_t)PTP * 4 + (size_t)kWin * 8 + (size_t)PT * 4 + ((size_t)round4(D * WH) + (mode == kRankSafe ? (size_t)round4(D * WP) : 0)) * 4 +
-         (size_t)D * 4 * 5 + 40 * 4 + (CT1 / PT + 4) * 4;
+  return (size_t)PTP * 4 + (size_t)kWin * 8 + (size_t)PT * 2 + ((size_t)round4(D * WH) + (mode == kRankSafe ? (size_t)round4(D * WP) : 0)) * 4 +
+         (size_t)D * 4 * 3 + 40 * 4 + (CT1 / PT + 4) * 4;
 }
 
 __device__ __forceinline__ void bulk_prefetch_l2(const void* g, uint32_t bytes) {
@@ -482,24 +482,24 @@ __device__ __forceinline__ void writeout_tag(uint32_t* __restrict__ out, const u
 // by the coarse digit; stage payload + global index by digit; vectorised
 // write-out of the runs.  Requires E < 2^32 (u32 indices).
 template <int kMode>
-__global__ void __launch_bounds__(T, 3) k_p1(const P1Args a) {
+__global__ void __launch_bounds__(T, 4) k_p1(const P1Args a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int D = a.D;
   uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem);                         // PTP (landing, then stage)
   uint64_t* s_win = reinterpret_cast<uint64_t*>(s_buf + PTP);                  // kWin
-  uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_win + kWin);                 // PT (source-boundary marks)
+  // source-boundary marks: u16 (v - s0) of the non-empty source whose list starts at the item
+  uint16_t* s_mark = reinterpret_cast<uint16_t*>(s_win + kWin);                // PT
   // digit of each staged slot: aliases the offsets window (dead after ranking;
   // the next window lands by TMA after the end-of-tile barrier + proxy fence)
   static_assert(kWin * 8 >= PT * 2, "tag array must fit in the window");
   uint16_t* s_tag = reinterpret_cast<uint16_t*>(s_win);
-  uint32_t* s_cnt = s_idx + PT;                                                // D * WH (packed, digit-major)
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_mark + PT);                  // D * WH (packed, digit-major)
   uint32_t* s_scr = s_cnt + round4(D * WH);                                    // D * WP (safe)
   uint32_t* s_gcur = s_scr + (kMode == kRankSafe ? round4(D * WP) : 0);        // D
   uint32_t* s_delta = s_gcur + D;                                              // D
-  uint32_t* s_dstart = s_delta + D;                                            // D
-  uint32_t* s_dtot = s_dstart + D;                                             // D
-  uint32_t* s_bh = s_dtot + D;                                                 // D
-  uint32_t* s_tmp = s_bh + D;                                                  // 40
+  uint32_t* s_dtot = s_delta + D;                                              // D
+  uint32_t* s_bh = reinterpret_cast<uint32_t*>(s_mark);                        // D (aliases the marks, dead after ranking)
+  uint32_t* s_tmp = s_dtot + D;                                                // 40
   uint32_t* s_psrc = s_tmp + 40;                                               // CT1/PT + 2
   __shared__ __align__(8) uint64_t s_bar;
   __shared__ uint64_t s_wlo;
@@ -515,7 +515,7 @@ __global__ void __launch_bounds__(T, 3) k_p1(const P1Args a) {
   for (int d = tid; d < D; d += T) s_gcur[d] = (uint32_t)a.tbase[(uint64_t)d * a.ntiles + k];
   for (int j = tid; j <= nplace; j += T) s_psrc[j] = a.psrc[gp0 + j];
   zero_u32(s_cnt, round4(D * WH) + (kMode == kRankSafe ? round4(D * WP) : 0));
-  zero_u32(s_idx, PT);
+  zero_u32(reinterpret_cast<uint32_t*>(s_mark), PT / 2);
   if (tid == 0) {
     mbar_init(&s_bar, 1);
     fence_mbar_init();
@@ -578,10 +578,14 @@ __global__ void __launch_bounds__(T, 3) k_p1(const P1Args a) {
       return (q < nw) ? s_win[q] : __ldg(offs + v);
     };
     const uint32_t s0 = s_psrc[j], s1 = max(s_psrc[j + 1], s0);
-    // mark the first item of every source that starts inside the tile
-    for (uint32_t v = s0 + 1 + tid; v <= s1; v += T) {
-      const uint64_t p = off_at(v) - gi0;
-      if (p < n) atomicMax(&s_idx[p], v + 1);
+    // mark the first item of every non-empty source that starts inside the tile
+    // (one per item; the owner of an item is the last source starting at or before it)
+    const bool wide = s1 - s0 > 65535u;  // marks cannot encode the span: per-lane search below
+    if (!wide) {
+      for (uint32_t v = s0 + 1 + tid; v <= s1; v += T) {
+        const uint64_t p = off_at(v) - gi0;
+        if (p < n && off_at((uint64_t)v + 1) > off_at(v)) s_mark[p] = (uint16_t)(v - s0);
+      }
     }
     __syncthreads();  // (A) tile landed, marks placed
 
@@ -592,13 +596,18 @@ __global__ void __launch_bounds__(T, 3) k_p1(const P1Args a) {
     auto slot = [&](int s, bool valid) {
       const uint32_t i = iw + s * 32 + lane;
       const uint32_t dst = valid ? s_buf[o + i] : 0u;
-      const uint32_t m = s_idx[i];
-      const uint32_t bal = __ballot_sync(kFull, m != 0);
       uint32_t src = carry;
-      if (bal) {  // a source starts inside this slot (warp-uniform)
-        const uint32_t bm = bal & le;
-        const uint32_t ms = __shfl_sync(kFull, m, 31 - __clz(bm | 1u));
-        src = bm ? ms - 1 : carry;
+      if (!wide) {
+        const uint32_t m = s_mark[i];
+        const uint32_t bal = __ballot_sync(kFull, m != 0);
+        if (bal) {  // a source starts inside this slot (warp-uniform)
+          const uint32_t bm = bal & le;
+          const uint32_t ms = __shfl_sync(kFull, m, 31 - __clz(bm | 1u));
+          src = bm ? s0 + ms : carry;
+          carry = __shfl_sync(kFull, src, 31);
+        }
+      } else {
+        src = owner_search(carry, s1, gi0 + i, off_at);
         carry = __shfl_sync(kFull, src, 31);
       }
       if (valid && i == n - 1) s_last_src = src;
@@ -643,7 +652,7 @@ __global__ void __launch_bounds__(T, 3) k_p1(const P1Args a) {
     }
     __syncthreads();  // (C)
     writeout_tag(a.out, s_buf, s_tag, s_delta, n);
-    zero_u32(s_idx, PT);
+    zero_u32(reinterpret_cast<uint32_t*>(s_mark), PT / 2);
     zero_u32(s_cnt, round4(D * WH));
     for (int d = tid; d < D; d += T) s_gcur[d] += s_dtot[d];
     fence_proxy_async_smem();
