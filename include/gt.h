@@ -139,6 +139,19 @@ int gt_gen_rmat(uint64_t scale, uint64_t num_edges, uint64_t seed, int permute,
                 uint32_t *src, uint32_t *dst, void *stream);
 int gt_gen_er(uint64_t num_vertices, uint64_t num_edges, uint64_t seed,
               uint32_t *src, uint32_t *dst, void *stream);
+/* Web-like graph (config C4), two calls.  gt_gen_web_degrees draws every
+ * vertex's out-degree from the Zipf inverse-CDF thresholds deg_cdf (ndeg u64
+ * entries, device), scales it by deg_scale_q16 / 65536 (rounded, >= 1) and
+ * writes the exclusive scan into offsets[0..V] (device) and the edge count to
+ * *num_edges (host).  gt_gen_web_edges writes the pairs in generation order:
+ * with probability p_local_q32 / 2^32 the destination is uniform within
+ * +-window of the source (mod V), otherwise hubs[rank] with rank drawn from
+ * hub_cdf (nhub u64 thresholds, device).  Same draws as gen.web_pairs_np. */
+int gt_gen_web_degrees(uint64_t num_vertices, uint64_t seed, const uint64_t *deg_cdf, uint32_t ndeg,
+                       uint32_t deg_scale_q16, uint64_t *offsets, uint64_t *num_edges, void *stream);
+int gt_gen_web_edges(uint64_t num_vertices, uint64_t seed, const uint64_t *offsets, const uint64_t *hub_cdf,
+                     uint32_t nhub, const uint32_t *hubs, uint32_t window, uint32_t p_local_q32,
+                     uint32_t *src, uint32_t *dst, void *stream);
 /* COO pairs -> CSR with every list ascending by destination (duplicates kept).
  * Consumes src/dst (they are overwritten as scratch). */
 int gt_build_csr(uint32_t *src, uint32_t *dst, uint64_t num_vertices, uint64_t num_edges,

@@ -75,7 +75,9 @@ struct Plan {
       o_status, o_ctr, o_counters, o_err, o_seghi, o_prev, o_cinfo, total;
 };
 
-int make_plan(uint64_t V, uint64_t E, Plan& p, uint64_t Vsrc = 0) {
+// wide_b: the level-2 digit may take 10 bits (v3 kernels only; the older
+// compact kernels size their shared memory for <= 9).
+int make_plan(uint64_t V, uint64_t E, Plan& p, uint64_t Vsrc = 0, bool wide_b = false) {
   p.V = V;
   p.E = E;
   p.nb = bits_for(V);
@@ -91,13 +93,14 @@ int make_plan(uint64_t V, uint64_t E, Plan& p, uint64_t Vsrc = 0) {
     cc = std::min(cc, p.nb);
     const int rem = p.nb - cc;
     int ca = rem, cb = 0;
+    const int bmax = wide_b ? 10 : 9;
     if (rem > 9) {
-      cb = std::min(9, rem / 2);
+      cb = std::min(bmax, rem / 2);
       ca = rem - cb;
     }
     const int L = 32 - (cb + cc);
     const int nsh = std::max(0, p.nbs - L);
-    p.compact = (cc >= 1 && p.nbs + cc <= 32 && ca <= 10 && cb <= 9 && nsh <= 12 &&
+    p.compact = (cc >= 1 && p.nbs + cc <= 32 && ca <= 10 && cb <= bmax && nsh <= 12 &&
                  getenv("GT_FORCE_FULL") == nullptr);
     if (p.compact) {
       a = ca;
@@ -632,7 +635,8 @@ struct Plan3 {
       o_base2, o_seg2, o_fbase, o_units, o_bigs, o_tiles3, o_cnt3, o_base3, o_seg3, o_cnt, o_err, total;
 };
 
-bool use_v3(const Plan& p) { return p.compact && p.E < (1ull << 32) && getenv("GT_V2") == nullptr; }
+bool v3_capable(uint64_t E) { return E < (1ull << 32) && getenv("GT_V2") == nullptr; }
+bool use_v3(const Plan& p) { return p.compact && v3_capable(p.E); }
 
 void make_plan3(const Plan& p, Plan3& q) {
   const uint64_t E = p.E;
@@ -911,7 +915,7 @@ int gt_workspace_size(uint64_t V, uint64_t E, uint64_t* bytes) {
     return GT_OK;
   }
   Plan p;
-  int rc = make_plan(V, E, p);
+  int rc = make_plan(V, E, p, 0, v3_capable(E));
   if (rc) return rc;
   *bytes = workspace_bytes(p, false);
   return GT_OK;
@@ -948,7 +952,7 @@ int gt_transpose(const uint64_t* offsets, const uint32_t* edges, uint64_t V, uin
     return GT_OK;
   }
   Plan p;
-  if ((rc = make_plan(V, E, p))) return rc;
+  if ((rc = make_plan(V, E, p, 0, v3_capable(E)))) return rc;
   unsigned char* ws = static_cast<unsigned char*>(workspace);
   const uint64_t need = workspace_bytes(p, false);
   if (!ws) {
@@ -982,47 +986,33 @@ int gt_transpose_host(const uint64_t* h_offsets, const uint32_t* h_edges, uint64
   int n = 0;
   cudaError_t e = cudaGetDeviceCount(&n);
   if (e != cudaSuccess || n == 0) return set_err(GT_ENODEV, "no CUDA device");
-  if (device < 0 || device >= n) return set_err(GT_EINVAL, "bad device %d", device);
+  if (device < 0 || device >= n || device >= 64) return set_err(GT_EINVAL, "bad device %d", device);
   GT_CUDA(cudaSetDevice(device));
-  cudaStream_t st;
-  GT_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  uint64_t *d_off = nullptr, *d_toff = nullptr;
-  uint32_t *d_e = nullptr, *d_te = nullptr;
-  int rc = GT_OK;
-  auto cleanup = [&]() {
-    cudaFreeAsync(d_off, st);
-    cudaFreeAsync(d_toff, st);
-    if (d_e) cudaFreeAsync(d_e, st);
-    if (d_te) cudaFreeAsync(d_te, st);
-    cudaStreamSynchronize(st);
-    cudaStreamDestroy(st);
-  };
-  do {
-    cudaError_t ce;
-    if ((ce = cudaMallocAsync(&d_off, (V + 1) * 8, st)) != cudaSuccess ||
-        (ce = cudaMallocAsync(&d_toff, (V + 1) * 8, st)) != cudaSuccess ||
-        (E && (ce = cudaMallocAsync(&d_e, E * 4, st)) != cudaSuccess) ||
-        (E && (ce = cudaMallocAsync(&d_te, E * 4, st)) != cudaSuccess)) {
-      rc = set_err(ce == cudaErrorMemoryAllocation ? GT_ENOMEM : GT_ECUDA, "device allocation: %s",
-                   cudaGetErrorString(ce));
-      break;
-    }
-    if ((ce = cudaMemcpyAsync(d_off, h_offsets, (V + 1) * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
-        (E && (ce = cudaMemcpyAsync(d_e, h_edges, E * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess)) {
-      rc = set_err(GT_ECUDA, "H2D: %s", cudaGetErrorString(ce));
-      break;
-    }
-    rc = gt_transpose(d_off, d_e, V, E, d_toff, d_te, nullptr, 0, st, stats);
-    if (rc) break;
-    if ((ce = cudaMemcpyAsync(h_t_offsets, d_toff, (V + 1) * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
-        (E && (ce = cudaMemcpyAsync(h_t_edges, d_te, E * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) ||
-        (ce = cudaStreamSynchronize(st)) != cudaSuccess) {
-      rc = set_err(GT_ECUDA, "D2H: %s", cudaGetErrorString(ce));
-      break;
-    }
-  } while (0);
-  cleanup();
-  return rc;
+  // device copies of input and output live in a per-device cache (grow-only),
+  // like the workspace: repeated calls do not re-map gigabytes of memory
+  static Cache s_io[64];
+  static cudaStream_t s_st[64];
+  static std::mutex s_io_mu;  // (g_mu is taken inside gt_transpose)
+  std::lock_guard<std::mutex> lk(s_io_mu);
+  if (!s_st[device]) GT_CUDA(cudaStreamCreateWithFlags(&s_st[device], cudaStreamNonBlocking));
+  cudaStream_t st = s_st[device];
+  const uint64_t b_off = align_up((V + 1) * 8, 256), b_e = align_up(std::max<uint64_t>(E, 1) * 4, 256);
+  void* base = nullptr;
+  int rc = cache_get(s_io[device], 2 * b_off + 2 * b_e, &base);
+  if (rc) return rc;
+  unsigned char* b = static_cast<unsigned char*>(base);
+  uint64_t* d_off = reinterpret_cast<uint64_t*>(b);
+  uint64_t* d_toff = reinterpret_cast<uint64_t*>(b + b_off);
+  uint32_t* d_e = reinterpret_cast<uint32_t*>(b + 2 * b_off);
+  uint32_t* d_te = reinterpret_cast<uint32_t*>(b + 2 * b_off + b_e);
+  GT_CUDA(cudaMemcpyAsync(d_off, h_offsets, (V + 1) * 8, cudaMemcpyHostToDevice, st));
+  if (E) GT_CUDA(cudaMemcpyAsync(d_e, h_edges, E * 4, cudaMemcpyHostToDevice, st));
+  rc = gt_transpose(d_off, d_e, V, E, d_toff, d_te, nullptr, 0, st, stats);
+  if (rc) return rc;
+  GT_CUDA(cudaMemcpyAsync(h_t_offsets, d_toff, (V + 1) * 8, cudaMemcpyDeviceToHost, st));
+  if (E) GT_CUDA(cudaMemcpyAsync(h_t_edges, d_te, E * 4, cudaMemcpyDeviceToHost, st));
+  GT_CUDA(cudaStreamSynchronize(st));
+  return GT_OK;
 }
 
 int gt_prefix_sum(const uint32_t* counts, uint64_t n, uint64_t* out, void* stream) {

@@ -13,7 +13,7 @@ namespace gtgen {
 
 constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
 constexpr uint64_t kSeedMul = 0xD1B54A32D192ED03ull;
-constexpr uint64_t kStreamRmat = 1, kStreamPerm = 2, kStreamEr = 3;
+constexpr uint64_t kStreamRmat = 1, kStreamPerm = 2, kStreamEr = 3, kStreamWdeg = 4, kStreamWedge = 5;
 // floor(p * 2^32) for the R-MAT quadrant CDF a=.57, a+b=.76, a+b+c=.95
 constexpr uint32_t kRmatA = 2448131358u, kRmatAB = 3264175144u, kRmatABC = 4080218931u;
 
@@ -90,6 +90,49 @@ __global__ void k_er(uint64_t V, uint64_t E, uint64_t key, uint32_t* __restrict_
   }
 }
 
+// first index i with u < cdf[i] (cdf non-decreasing, cdf[n-1] = 2^64-1)
+__device__ __forceinline__ uint32_t cdf_rank(const uint64_t* __restrict__ cdf, uint32_t n, uint64_t u) {
+  uint32_t lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (u < cdf[mid]) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
+__global__ void k_web_deg(uint64_t V, uint64_t key, const uint64_t* __restrict__ cdf, uint32_t n, uint32_t sq,
+                          uint32_t* __restrict__ deg) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < V; v += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = (uint64_t)cdf_rank(cdf, n, hash_at(key, v)) + 1;
+    const uint64_t d = (k * sq + 32768) >> 16;
+    deg[v] = (uint32_t)(d ? d : 1);
+  }
+}
+
+// one warp per source: its edges in generation order
+__global__ void k_web_edges(uint64_t V, uint64_t key, const uint64_t* __restrict__ offs,
+                            const uint64_t* __restrict__ hcdf, uint32_t nh, const uint32_t* __restrict__ hubs,
+                            uint32_t window, uint32_t plocal, uint32_t* __restrict__ src, uint32_t* __restrict__ dst) {
+  const uint64_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t span = 2ull * window + 1;
+  for (uint64_t v = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; v < V; v += nwarps) {
+    const uint64_t e0 = offs[v], e1 = offs[v + 1];
+    for (uint64_t e = e0 + lane; e < e1; e += 32) {
+      const uint64_t ha = hash_at(key, 2 * e), hb = hash_at(key, 2 * e + 1);
+      uint32_t d;
+      if ((uint32_t)ha < plocal) {
+        const uint64_t off = ((ha >> 32) * span) >> 32;
+        d = (uint32_t)((v + V - window + off) % V);
+      } else {
+        d = hubs[cdf_rank(hcdf, nh, hb)];
+      }
+      src[e] = (uint32_t)v;
+      dst[e] = d;
+    }
+  }
+}
+
 __global__ void k_hist(const uint32_t* __restrict__ key, uint64_t E, uint32_t* __restrict__ cnt) {
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < E; e += (uint64_t)gridDim.x * blockDim.x)
     atomicAdd(&cnt[key[e]], 1u);
@@ -139,6 +182,34 @@ int gt_gen_er(uint64_t V, uint64_t E, uint64_t seed, uint32_t* src, uint32_t* ds
   if (V < 1 || V > (1ull << 32) || (E && (!src || !dst))) return GT_EINVAL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (E) k_er<<<148 * 16, 256, 0, st>>>(V, E, stream_key(seed, kStreamEr), src, dst);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? GT_OK : gen_fail(e);
+}
+
+int gt_gen_web_degrees(uint64_t V, uint64_t seed, const uint64_t* deg_cdf, uint32_t ndeg, uint32_t sq,
+                       uint64_t* offsets, uint64_t* num_edges, void* stream) {
+  if (V < 1 || V > (1ull << 32) || !deg_cdf || ndeg < 1 || !offsets || !num_edges) return GT_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint32_t* deg = nullptr;
+  cudaError_t e = cudaMallocAsync(&deg, V * 4, st);
+  if (e != cudaSuccess) return gen_fail(e);
+  k_web_deg<<<148 * 16, 256, 0, st>>>(V, stream_key(seed, kStreamWdeg), deg_cdf, ndeg, sq, deg);
+  int rc = gt_prefix_sum(deg, V, offsets, st);
+  if (rc == GT_OK) {
+    if ((e = cudaMemcpyAsync(num_edges, offsets + V, 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess) rc = gen_fail(e);
+  }
+  cudaFreeAsync(deg, st);
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess && rc == GT_OK) rc = gen_fail(e);
+  return rc;
+}
+
+int gt_gen_web_edges(uint64_t V, uint64_t seed, const uint64_t* offsets, const uint64_t* hub_cdf, uint32_t nhub,
+                     const uint32_t* hubs, uint32_t window, uint32_t plocal, uint32_t* src, uint32_t* dst,
+                     void* stream) {
+  if (V < 1 || V > (1ull << 32) || !offsets || !hub_cdf || nhub < 1 || !hubs || !src || !dst) return GT_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  k_web_edges<<<148 * 32, 256, 0, st>>>(V, stream_key(seed, kStreamWedge), offsets, hub_cdf, nhub, hubs, window,
+                                        plocal, src, dst);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? GT_OK : gen_fail(e);
 }

@@ -468,9 +468,18 @@ __device__ __forceinline__ void bases_delta(uint32_t* cnt, int D, const uint32_t
 // Write-out of a staged tile: slot i holds payload buf[i] of digit tag[i],
 // global index delta[tag] + i.  Consecutive lanes take consecutive slots, so a
 // warp store covers a few digit runs (coalesced sectors).
+template <int NT, int TILE>
 __device__ __forceinline__ void writeout_tag(uint32_t* __restrict__ out, const uint32_t* buf, const uint16_t* tag,
                                              const uint32_t* delta, uint32_t n) {
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) out[delta[tag[i]] + i] = buf[i];
+  if (n == (uint32_t)TILE) {
+#pragma unroll
+    for (int k = 0; k < TILE / NT; ++k) {
+      const uint32_t i = threadIdx.x + k * NT;
+      out[delta[tag[i]] + i] = buf[i];
+    }
+  } else {
+    for (uint32_t i = threadIdx.x; i < n; i += NT) out[delta[tag[i]] + i] = buf[i];
+  }
 }
 
 // L1 place.  One CTA per count tile (CT1 edges), place tiles of PT edges in
@@ -610,7 +619,7 @@ __global__ void __launch_bounds__(T, 4) k_p1(const P1Args a) {
         src = owner_search(carry, s1, gi0 + i, off_at);
         carry = __shfl_sync(kFull, src, 31);
       }
-      if (valid && i == n - 1) s_last_src = src;
+      if ((n == (uint32_t)PT) ? (s == K - 1 && i == PT - 1) : (valid && i == n - 1)) s_last_src = src;
       const uint32_t d = dst >> a.shift;
       pk[s] = (d << 16) | rank_pk<kMode>(s_cnt + d * WH + (w >> 1), s_scr + d * WP + w, sh, valid);
       pay[s] = ((dst & a.low_mask) << a.L) | (src & a.src_mask);
@@ -651,7 +660,7 @@ __global__ void __launch_bounds__(T, 4) k_p1(const P1Args a) {
       }
     }
     __syncthreads();  // (C)
-    writeout_tag(a.out, s_buf, s_tag, s_delta, n);
+    writeout_tag<T, PT>(a.out, s_buf, s_tag, s_delta, n);
     zero_u32(reinterpret_cast<uint32_t*>(s_mark), PT / 2);
     zero_u32(s_cnt, round4(D * WH));
     for (int d = tid; d < D; d += T) s_gcur[d] += s_dtot[d];
@@ -927,7 +936,7 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __r
         }
       }
       __syncthreads();  // (C)
-      writeout_tag(out, s_buf, s_tag, s_delta, n);
+      writeout_tag<T, PT>(out, s_buf, s_tag, s_delta, n);
       zero_u32(s_cnt, round4(D * WH));
       for (int d = tid; d < D; d += T) s_gcur[d] += s_dtot[d];
       fence_proxy_async_smem();

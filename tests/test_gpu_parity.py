@@ -227,3 +227,66 @@ def test_full_size_configs(cfg_name):
     o, e = oracle.transpose_c(off, edg, cfg.num_vertices)
     assert np.array_equal(got_off, o)
     assert np.array_equal(got_edg, e)
+
+
+def _web_cfg(V, target, hubs=1 << 10, window=256, seed=11):
+    from paper_2501_06872_b200 import gen
+
+    scale = V.bit_length() - 1
+    return gen.GraphConfig(f"web-v2^{scale}", "web", V, target, scale=scale, seed=seed,
+                           web=gen.WebParams(hubs=hubs, window=window))
+
+
+def test_web_generator_device_matches_numpy():
+    from paper_2501_06872_b200 import gen
+
+    cfg = _web_cfg(1 << 16, 1 << 20)
+    s_d, d_d = gen.web_pairs_device(cfg)
+    s_n, d_n = gen.web_pairs_np(cfg.num_vertices, cfg.num_edges, cfg.seed, cfg.web)
+    assert np.array_equal(s_d.cpu().numpy().view(np.uint32), s_n)
+    assert np.array_equal(d_d.cpu().numpy().view(np.uint32), d_n)
+
+
+@pytest.mark.parametrize("V,target", [(1 << 16, 1 << 20), (1 << 26, 1 << 26)])
+def test_web_graph_transpose(V, target, rank_mode):
+    """Web-like graphs; |V| = 2^26 takes the 10|10|6 digit split (1024-digit
+    level-2 pass) of config C4 at a small edge count."""
+    from paper_2501_06872_b200 import gen, transpose_device
+
+    cfg = _web_cfg(V, target, hubs=min(1 << 16, V >> 6), window=4096 if V > 1 << 20 else 256)
+    off_d, edg_d = gen.generate_device(cfg)
+    t_off, t_edg, st = transpose_device(off_d, edg_d, V, want_stats=True)
+    if V == 1 << 26:
+        assert list(st.bits) == [10, 10, 6]
+    off = off_d.cpu().numpy().view(np.uint64)
+    edg = edg_d.cpu().numpy().view(np.uint32)
+    o, e = oracle.transpose_c(off, edg, V)
+    assert np.array_equal(t_off.cpu().numpy().view(np.uint64), o)
+    assert np.array_equal(t_edg.cpu().numpy().view(np.uint32), e)
+
+
+@pytest.mark.slow
+def test_full_size_c4():
+    """Config C4 (web-like, |V| = 2^26, |E| ~ 2^30) generated on the device,
+    transposed, and checked against the C oracle bit for bit."""
+    import torch
+
+    from paper_2501_06872_b200 import gen, transpose_device
+
+    if os.environ.get("GT_SKIP_FULL") == "1":
+        pytest.skip("GT_SKIP_FULL=1")
+    cfg = gen.CONFIGS["C4"]
+    off_d, edg_d = gen.generate_device(cfg)
+    E = int(edg_d.numel())
+    t_off, t_edg, st = transpose_device(off_d, edg_d, cfg.num_vertices, want_stats=True)
+    torch.cuda.synchronize()
+    off = off_d.cpu().numpy().view(np.uint64)
+    edg = edg_d.cpu().numpy().view(np.uint32)
+    got_off = t_off.cpu().numpy().view(np.uint64)
+    got_edg = t_edg.cpu().numpy().view(np.uint32)
+    del off_d, edg_d, t_off, t_edg
+    torch.cuda.empty_cache()
+    assert got_off[-1] == E and abs(E / (1 << 30) - 1) < 0.1
+    o, e = oracle.transpose_c(off, edg, cfg.num_vertices)
+    assert np.array_equal(got_off, o)
+    assert np.array_equal(got_edg, e)
