@@ -721,6 +721,13 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
   int rc;
   int launches = 0;
   const int sms = num_sms();
+  // level-3 units are aligned groups of 2^sbits fine buckets (<= ML3 local
+  // vertices); R2 carries g3 = sbits fine-digit bits when it has room, else
+  // the unit decodes the fine bucket from the record's position
+  int sbits = 0;
+  while ((ML3 >> p.c) >> (sbits + 1)) ++sbits;
+  const bool pos_fine = p.gbits < sbits;
+  const int g3 = pos_fine ? 0 : sbits;
 
   GT_CUDA(cudaMemsetAsync(cnt, 0, 64, st));
   GT_CUDA(cudaMemsetAsync(err, 0, 4, st));
@@ -780,7 +787,7 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
     dec.src_mask = (uint32_t)((1ull << p.L) - 1);
     dec.shB = p.L + p.c;
     dec.maskB = (uint32_t)(Db - 1);
-    dec.lvmask = (uint32_t)((1ull << (p.c + p.gbits)) - 1);
+    dec.lvmask = (uint32_t)((1ull << (p.c + g3)) - 1);  // R2: low digit + g3 fine-digit bits (0: L3 uses positions)
     dec.nbs = p.nbs;
     dec.nh = nh;
     dec.seg_hi = seghi;
@@ -802,7 +809,7 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
   // ---- step 3: level 3 (units of small fine buckets; tiled count/scan/place for big ones)
   k_set_u64<<<1, 1, 0, st>>>(fbase + q.nfine, E);
   GT_LAUNCH_CHECK();
-  k_plan3<<<(unsigned)((q.nfine / (1u << p.gbits) + 255) / 256 + 1), 256, 0, st>>>(fbase, (uint32_t)q.nfine, p.gbits,
+  k_plan3<<<(unsigned)((q.nfine / (1u << sbits) + 255) / 256 + 1), 256, 0, st>>>(fbase, (uint32_t)q.nfine, sbits,
                                                                                    units, cnt + 0, bigs, cnt + 1);
   GT_LAUNCH_CHECK();
   k_big_tiles<<<1, 1024, 0, st>>>(bigs, cnt + 1, p.c, tiles3, cnt + 2, seg3);
@@ -832,16 +839,24 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
     a.ctr = cnt + 3;
     a.c = p.c;
     a.nbs = p.nbs;
-    a.gbits = p.gbits;
     a.src_mask = (p.nbs >= 32) ? 0xffffffffu : (uint32_t)((1ull << p.nbs) - 1);
-    a.lvmask = (uint32_t)((1ull << (p.c + p.gbits)) - 1);
+    a.mask_c = (uint32_t)(Dc - 1);
+    a.fbase = fbase;
+    a.gbits = g3;
+    a.lvmask = (uint32_t)((1ull << (p.c + g3)) - 1);
     a.V = V;
     a.t_offsets = t_offsets;
     a.t_edges = t_edges;
     const size_t sm = smem_p3(kMode);
-    if ((rc = set_smem(k_p3<kMode>, sm))) return rc;
-    const unsigned g = persistent_grid(k_p3<kMode>, W3 * 32, sm, q.nfine);
-    k_p3<kMode><<<g, W3 * 32, sm, st>>>(a);
+    auto go3 = [&](auto kern) -> int {
+      int r;
+      if ((r = set_smem(kern, sm))) return r;
+      const unsigned g = persistent_grid(kern, W3 * 32, sm, q.nfine);
+      kern<<<g, W3 * 32, sm, st>>>(a);
+      return GT_OK;
+    };
+    rc = pos_fine ? go3(k_p3<kMode, true>) : go3(k_p3<kMode, false>);
+    if (rc) return rc;
     GT_LAUNCH_CHECK();
   }
   k_set_u64<<<1, 1, 0, st>>>(t_offsets + V, E);

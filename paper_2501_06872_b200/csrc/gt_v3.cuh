@@ -952,8 +952,11 @@ struct P3Args {
   const Unit3* units;
   const uint32_t* n_units;
   unsigned int* ctr;
-  int c, nbs, gbits;
-  uint32_t src_mask, lvmask;
+  int c, nbs;
+  uint32_t src_mask, mask_c;
+  const uint64_t* fbase;  // CSC start of every fine bucket (+ total)
+  int gbits;              // kPosFine == false: R2 keeps (fine & (2^gbits - 1)) << c | low digit
+  uint32_t lvmask;        //   = (1 << (c + gbits)) - 1
   uint64_t V;
   uint64_t* t_offsets;
   uint32_t* t_edges;
@@ -964,7 +967,9 @@ inline size_t smem_p3(int mode) {
          (size_t)ML3 * 8 + 40 * 4;
 }
 
-template <int kMode>
+// kPosFine: the record's fine bucket inside the unit comes from its position
+// (R2 has no room for fine-digit bits); else from the record's bits.
+template <int kMode, bool kPosFine>
 __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
   constexpr int TT = W3 * 32;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -976,6 +981,7 @@ __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
   uint32_t* s_tmp = s_dtot + ML3;
   __shared__ __align__(8) uint64_t s_bar[2];
   __shared__ uint32_t s_uidx[2];
+  __shared__ uint32_t s_fb[ML3];  // fine-bucket boundaries of the unit (relative positions)
 
   const uint32_t tid = threadIdx.x, lane = lane_id(), w = warp_id();
   const uint32_t sh = (w & 1) << 4;
@@ -1001,7 +1007,6 @@ __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
     if (u0 < nun) issue(u0, 0);
   }
   __syncthreads();
-  const uint32_t lvoff_mask = (1u << a.gbits) - 1;
   uint32_t ph0 = 0, ph1 = 0;
   for (int it = 0;; ++it) {
     const int b = it & 1;
@@ -1026,17 +1031,34 @@ __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
     if (b == 0) { mbar_wait_parity(&s_bar[0], ph0); ph0 ^= 1; }
     else { mbar_wait_parity(&s_bar[1], ph1); ph1 ^= 1; }
     if (tail) buf[ti] = tv;
+    const uint32_t nbt = kPosFine ? u.nf - 1 : 0u;  // fine-bucket boundaries inside the unit
+    if constexpr (kPosFine)
+      for (uint32_t q = tid; q < nbt; q += TT) s_fb[q] = (uint32_t)(a.fbase[u.f0 + 1 + q] - u.start);
     __syncthreads();  // (A)
     const uint32_t nloc = u.nf << a.c;
-    const uint32_t lvoff = (u.f0 & lvoff_mask) << a.c;
     const uint32_t seg0 = w * (K3 * 32);
+    // local vertex = (fine bucket inside the unit, from the record's position) << c | low digit
+    auto bnd_at = [&](uint32_t kk) -> uint32_t { return s_fb[kk - 1]; };
+    uint32_t fcur = 0, fnb = 0xffffffffu;
+    if (nbt) {
+      fcur = owner_search(0u, nbt, (uint64_t)seg0, [&](uint64_t kk) -> uint64_t { return s_fb[kk - 1]; });
+      fnb = (fcur + 1 <= nbt) ? s_fb[fcur] : 0xffffffffu;
+    }
+    const bool wbnd = fnb <= seg0 + (K3 * 32 - 1);
+    const uint32_t lvoff = (u.f0 & ((1u << a.gbits) - 1)) << a.c;
     uint32_t rr[K3], pk[K3];
 #pragma unroll
     for (int s = 0; s < K3; ++s) {
       const uint32_t i = seg0 + s * 32 + lane;
       const bool valid = i < n;
       const uint32_t r = valid ? buf[o + i] : 0u;
-      const uint32_t lv = valid ? (((r >> a.nbs) & a.lvmask) - lvoff) : 0u;
+      uint32_t lv;
+      if constexpr (kPosFine) {
+        const uint32_t j = wbnd ? slot_owner32(fcur, fnb, seg0 + s * 32, nbt, bnd_at) : fcur;
+        lv = valid ? ((j << a.c) | ((r >> a.nbs) & a.mask_c)) : 0u;
+      } else {
+        lv = valid ? (((r >> a.nbs) & a.lvmask) - lvoff) : 0u;
+      }
       pk[s] = (lv << 16) | rank_pk<kMode>(s_cnt + lv * WH3 + (w >> 1), s_scr + lv * W3P + w, sh, valid);
       rr[s] = r & a.src_mask;
     }
@@ -1131,8 +1153,8 @@ __global__ void k_l2_tiles(const uint64_t* __restrict__ cstart, const uint32_t* 
   }
 }
 
-// L3 plan: one thread per aligned group of G fine buckets.  Small fine
-// buckets are packed into units (<= CAP3 records, one group); fine buckets
+// L3 plan: one thread per aligned group of G = ML3 >> c fine buckets.  Small
+// fine buckets are packed into units (<= CAP3 records, one group); fine buckets
 // above CAP3 become big buckets.  fbase[f] = CSC start of fine bucket f,
 // fbase[nfine] = E.
 struct Big3 {
@@ -1141,9 +1163,9 @@ struct Big3 {
   uint32_t f;
   uint32_t pad;
 };
-__global__ void k_plan3(const uint64_t* __restrict__ fbase, uint32_t nfine, int gbits, Unit3* __restrict__ units,
+__global__ void k_plan3(const uint64_t* __restrict__ fbase, uint32_t nfine, int sbits, Unit3* __restrict__ units,
                         uint32_t* __restrict__ n_units, Big3* __restrict__ bigs, uint32_t* __restrict__ n_big) {
-  const uint32_t G = 1u << gbits;
+  const uint32_t G = 1u << sbits;
   const uint32_t grp = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t f_begin = grp * G;
   if (f_begin >= nfine) return;
