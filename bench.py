@@ -253,26 +253,34 @@ def main():
     if not dist_on:
         t_off = torch.empty(V + 1, dtype=torch.int64, device=dev)
         t_edg = torch.empty(E, dtype=torch.int32, device=dev)
-        # one instrumented step (per-level device times, launch count, big buckets)
-        _, _, st = transpose_device(off_d, edg_d, V, t_offsets=t_off, t_edges=t_edg, want_stats=True)
         for _ in range(args.warmup):
             transpose_device(off_d, edg_d, V, t_offsets=t_off, t_edges=t_edg)
         torch.cuda.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         sampler.start()
         torch.cuda.synchronize()
+        # every timed step records CUDA events on the launching stream around the
+        # levels and the main kernels (gt_stats), summed below
+        acc = {"step1": 0.0, "step2": 0.0, "step3": 0.0, "k": [0.0, 0.0, 0.0, 0.0]}
         ev0.record(stream)
         for _ in range(args.steps):
-            transpose_device(off_d, edg_d, V, t_offsets=t_off, t_edges=t_edg)
+            _, _, st = transpose_device(off_d, edg_d, V, t_offsets=t_off, t_edges=t_edg, want_stats=True)
+            acc["step1"] += st.ms_step1
+            acc["step2"] += st.ms_step2
+            acc["step3"] += st.ms_step3
+            for i in range(4):
+                acc["k"][i] += st.ms_kernel[i]
         ev1.record(stream)
         torch.cuda.synchronize()
         clocks = sampler.stop()
         ms = ev0.elapsed_time(ev1) / args.steps
         launches = int(st.n_launches) * args.steps
-        kern = {"step1_ms": st.ms_step1, "step2_ms": st.ms_step2, "step3_ms": st.ms_step3,
+        K = args.steps
+        kern = {"step1_ms": acc["step1"] / K, "step2_ms": acc["step2"] / K, "step3_ms": acc["step3"] / K,
                 "digit_bits": list(st.bits), "big_buckets": int(st.n_big_buckets),
                 "rank_mode": "smem-atomic" if st.rank_mode == 0 else "or-mask",
                 "workspace_bytes": int(st.workspace_bytes)}
+        kernel_ms = [x / K for x in acc["k"]]
         n_gpus = 1
     else:
         import torch.distributed as dist
@@ -311,13 +319,41 @@ def main():
     abytes = algo_bytes(V, E)
     achieved = abytes / (ms / 1e3) / 1e9
     agg_peak = peak * n_gpus
-    traffic = None
+    traffic, ktraffic = None, {}
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
         try:
-            traffic = json.loads(tf.read_text()).get(cfg.name)
+            tj = json.loads(tf.read_text()).get(cfg.name) or {}
+            traffic = tj.get("step_bytes")
+            ktraffic = tj.get("kernels", {})
         except Exception:
-            traffic = None
+            traffic, ktraffic = None, {}
+    if not dist_on:
+        # per-kernel roofline: algorithmic bytes of each main kernel over its
+        # CUDA-event time inside the timed region; traffic = its ncu DRAM bytes per launch
+        kspec = [("k_p1 level-1 place (CSR -> R1)", 8 * E + 8 * (V + 1)),
+                 ("k_p2 level-2 place (R1 -> R2)", 8 * E),
+                 ("k_p3 level-3 units (R2 -> CSC)", None),
+                 ("k_p2 level-3 big buckets (R2 -> CSC)", None)]
+        kernels_rf = []
+        for (name, kb), kms in zip(kspec, kernel_ms):
+            if kms <= 0:
+                continue
+            ent = {"name": name, "ms": kms}
+            if kb is not None:
+                ent.update({"algorithmic_bytes": kb, "achieved_gbs": kb / (kms / 1e3) / 1e9,
+                            "frac": kb / (kms / 1e3) / 1e9 / peak})
+            key = name.split()[0] + ("_big" if "big" in name else "")
+            if key in ktraffic:
+                ent["traffic"] = ktraffic[key]
+            kernels_rf.append(ent)
+        l3 = sum(kernel_ms[2:4])
+        if l3 > 0:
+            kernels_rf.append({"name": "level 3 total (units + big buckets)", "ms": l3,
+                               "algorithmic_bytes": 8 * E + 8 * (V + 1),
+                               "achieved_gbs": (8 * E + 8 * (V + 1)) / (l3 / 1e3) / 1e9,
+                               "frac": (8 * E + 8 * (V + 1)) / (l3 / 1e3) / 1e9 / peak})
+        kern["per_kernel"] = kernels_rf
 
     e2e = None
     cpu = None

@@ -52,7 +52,7 @@ extern "C" {
 #define GT_EFORMAT (-6) /* GraphFormatError (errors.py:4-14): a POTG file violates the format */
 #define GT_EIO (-7)     /* OSError: a file could not be opened, read or written */
 
-#define GT_ABI_VERSION 1
+#define GT_ABI_VERSION 2
 
 /* Per-call accounting; mirrors TransposeOutput.phase_times / aux_footprint_bytes
  * (baselines.py:39-53).  Times are device time from CUDA events, in ms, filled
@@ -67,6 +67,9 @@ typedef struct gt_stats {
     int32_t rank_mode;     /* 0 = lane-ordered smem atomics, 1 = safe OR-mask  */
     uint64_t n_big_buckets;/* final buckets that took the multi-CTA path       */
     uint64_t n_launches;   /* kernels this call launched                       */
+    double ms_kernel[4];   /* device time of the main kernels: level-1 place,  */
+                           /* level-2 place, level-3 units, level-3 big place  */
+                           /* (0 when a kernel did not run on this path)       */
 } gt_stats;
 
 /* Library / device info. */

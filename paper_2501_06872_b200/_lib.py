@@ -33,6 +33,7 @@ class GtStats(ctypes.Structure):
         ("rank_mode", ctypes.c_int32),
         ("n_big_buckets", ctypes.c_uint64),
         ("n_launches", ctypes.c_uint64),
+        ("ms_kernel", ctypes.c_double * 4),
     ]
 
 
@@ -47,6 +48,7 @@ class PotgHeader(ctypes.Structure):
     ]
 
 
+ABI_VERSION = 2  # include/gt.h GT_ABI_VERSION
 _u64, _i64, _int, _vp = ctypes.c_uint64, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
 _stats_p = ctypes.POINTER(GtStats)
 _hdr_p = ctypes.POINTER(PotgHeader)
@@ -102,7 +104,7 @@ def load():
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args
-        if handle.gt_abi_version() != 1:
+        if handle.gt_abi_version() != ABI_VERSION:
             raise GpuUnavailableError("libgt.so ABI version mismatch")
         _lib = handle
         return _lib

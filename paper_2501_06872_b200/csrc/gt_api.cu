@@ -317,25 +317,48 @@ int scan_u64_to_u64(const unsigned long long* in, uint64_t n, uint64_t* out, uin
   return GT_OK;
 }
 
+// CUDA-event timing of a call (stats != NULL): step marks plus begin/end of
+// the main kernels.  Events are created once per thread and reused.
 struct Timer {
+  static constexpr int kSteps = 6, kKern = 4;
   bool on = false;
   cudaStream_t st = nullptr;
-  cudaEvent_t ev[5] = {};
+  cudaEvent_t* ev = nullptr;   // kSteps step marks
+  cudaEvent_t* kev = nullptr;  // 2 * kKern kernel begin/end
   int n = 0;
+  bool kset[kKern] = {};
   int init(bool enable, cudaStream_t s) {
     on = enable;
     st = s;
     if (!on) return GT_OK;
-    for (auto& e : ev) GT_CUDA(cudaEventCreate(&e));
+    thread_local cudaEvent_t t_ev[kSteps + 2 * kKern];
+    thread_local bool t_init = false;
+    thread_local int t_dev = -1;
+    int dev = 0;
+    GT_CUDA(cudaGetDevice(&dev));
+    if (!t_init || t_dev != dev) {
+      for (auto& e : t_ev) GT_CUDA(cudaEventCreate(&e));
+      t_init = true;
+      t_dev = dev;
+    }
+    ev = t_ev;
+    kev = t_ev + kSteps;
     return GT_OK;
   }
   int mark() {
-    if (on) GT_CUDA(cudaEventRecord(ev[n++], st));
+    if (on && n < kSteps) GT_CUDA(cudaEventRecord(ev[n++], st));
     return GT_OK;
   }
-  ~Timer() {
-    if (on)
-      for (auto& e : ev) cudaEventDestroy(e);
+  int kbegin(int k) {
+    if (on) GT_CUDA(cudaEventRecord(kev[2 * k], st));
+    return GT_OK;
+  }
+  int kend(int k) {
+    if (on) {
+      GT_CUDA(cudaEventRecord(kev[2 * k + 1], st));
+      kset[k] = true;
+    }
+    return GT_OK;
   }
 };
 
@@ -765,8 +788,10 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
     a.out = t_edges;
     const size_t sm = smem_p1(D1, kMode);
     if ((rc = set_smem(k_p1<kMode>, sm))) return rc;
+    if ((rc = tm.kbegin(0))) return rc;
     k_p1<kMode><<<(unsigned)q.ntiles1, T, sm, st>>>(a);
     GT_LAUNCH_CHECK();
+    if ((rc = tm.kend(0))) return rc;
   }
   launches += 6;
   if ((rc = tm.mark())) return rc;
@@ -791,6 +816,7 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
     dec.nbs = p.nbs;
     dec.nh = nh;
     dec.seg_hi = seghi;
+    if ((rc = tm.kbegin(1))) return rc;
     if (env_int("GT_K2", 16) == 32) {
       const size_t sm = smem_p2(Db, kMode, 32);
       if ((rc = set_smem(k_p2<kMode, DecR1, 32>, sm))) return rc;
@@ -803,6 +829,7 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
       k_p2<kMode, DecR1, 16><<<g, T, sm, st>>>(t_edges, tiles2, cfirst + D1, Db, dec, base2, r2);
     }
     GT_LAUNCH_CHECK();
+    if ((rc = tm.kend(1))) return rc;
   }
   launches += 5;
   if ((rc = tm.mark())) return rc;
@@ -828,8 +855,10 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
     const size_t sm = smem_p2(Dc, kMode, 16);
     if ((rc = set_smem(k_p2<kMode, DecR2, 16>, sm))) return rc;
     const unsigned g = persistent_grid(k_p2<kMode, DecR2, 16>, T, sm, q.max_t3);
+    if ((rc = tm.kbegin(3))) return rc;
     k_p2<kMode, DecR2, 16><<<g, T, sm, st>>>(r2, tiles3, cnt + 2, Dc, dec, base3, t_edges);
     GT_LAUNCH_CHECK();
+    if ((rc = tm.kend(3))) return rc;
   }
   {
     P3Args a;
@@ -855,9 +884,11 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
       kern<<<g, W3 * 32, sm, st>>>(a);
       return GT_OK;
     };
+    if ((rc = tm.kbegin(2))) return rc;
     rc = pos_fine ? go3(k_p3<kMode, true>) : go3(k_p3<kMode, false>);
     if (rc) return rc;
     GT_LAUNCH_CHECK();
+    if ((rc = tm.kend(2))) return rc;
   }
   k_set_u64<<<1, 1, 0, st>>>(t_offsets + V, E);
   GT_LAUNCH_CHECK();
@@ -913,6 +944,11 @@ int fill_stats(const Plan& p, int mode, Timer& tm, gt_stats* stats) {
   stats->rank_mode = mode;
   stats->n_big_buckets = big;
   stats->n_launches = launches;
+  for (int k = 0; k < Timer::kKern; ++k) {
+    float x = 0;
+    if (tm.kset[k]) GT_CUDA(cudaEventElapsedTime(&x, tm.kev[2 * k], tm.kev[2 * k + 1]));
+    stats->ms_kernel[k] = x;
+  }
   return GT_OK;
 }
 

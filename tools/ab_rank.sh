@@ -1,0 +1,4 @@
+for cfg in "GT_RK1=0 GT_RK3=0 GT_RKB=0" "GT_RK1=1 GT_RK3=0 GT_RKB=0" "GT_RK1=2 GT_RK3=0 GT_RKB=0" "GT_RK1=0 GT_RK3=1 GT_RKB=0" "GT_RK1=0 GT_RK3=2 GT_RKB=0" "GT_RK1=0 GT_RK3=0 GT_RKB=2"; do
+  r=$(env $cfg timeout 200 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 | python3 -c "import json,sys; d=json.loads(sys.stdin.read()); k=d['roofline']['kernels']; print(round(d['ms_per_step'],3), round(k['step1_ms'],3), round(k['step2_ms'],3), round(k['step3_ms'],3))")
+  echo "$cfg : $r"
+done
