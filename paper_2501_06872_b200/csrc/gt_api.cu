@@ -826,7 +826,22 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
       const size_t sm = smem_p2(Db, kMode, 16);
       if ((rc = set_smem(k_p2<kMode, DecR1, 16>, sm))) return rc;
       const unsigned g = persistent_grid(k_p2<kMode, DecR1, 16>, T, sm, q.max_t2);
-      k_p2<kMode, DecR1, 16><<<g, T, sm, st>>>(t_edges, tiles2, cfirst + D1, Db, dec, base2, r2);
+      unsigned long long* prof = nullptr;
+      if (getenv("GT_PROF2")) {
+        GT_CUDA(cudaMallocAsync(&prof, 64, st));
+        GT_CUDA(cudaMemsetAsync(prof, 0, 64, st));
+      }
+      k_p2<kMode, DecR1, 16><<<g, T, sm, st>>>(t_edges, tiles2, cfirst + D1, Db, dec, base2, r2, prof);
+      if (prof) {
+        unsigned long long h[6];
+        GT_CUDA(cudaMemcpyAsync(h, prof, 48, cudaMemcpyDeviceToHost, st));
+        GT_CUDA(cudaStreamSynchronize(st));
+        double tot = 0;
+        for (int i = 0; i < 6; ++i) tot += (double)h[i];
+        fprintf(stderr, "[gt_prof2] grid=%u setup=%.3f wait=%.3f rank=%.3f bases=%.3f stage=%.3f write=%.3f (fractions of %.3g CTA-cycles)\n",
+                g, h[0] / tot, h[1] / tot, h[2] / tot, h[3] / tot, h[4] / tot, h[5] / tot, tot);
+        cudaFreeAsync(prof, st);
+      }
     }
     GT_LAUNCH_CHECK();
     if ((rc = tm.kend(1))) return rc;
