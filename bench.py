@@ -413,7 +413,7 @@ def main():
             "dtype": "u32",
             "data": "synthetic",
             "config": {"workload": cfg.name, "num_vertices": V, "num_edges": E,
-                       "l2": "inputs (2.3 GB) larger than L2 (126 MB); no flush",
+                       "l2": f"inputs ({((V + 1) * 8 + E * 4) / 1e9:.2f} GB) larger than L2 (126 MB); no flush",
                        "parallelism": f"sharded{n_gpus}" if dist_on else "single-gpu"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": agg_peak, "unit": "GB/s",
                          "frac": achieved / agg_peak, "traffic": traffic,

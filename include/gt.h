@@ -142,6 +142,13 @@ int gt_gen_rmat(uint64_t scale, uint64_t num_edges, uint64_t seed, int permute,
                 uint32_t *src, uint32_t *dst, void *stream);
 int gt_gen_er(uint64_t num_vertices, uint64_t num_edges, uint64_t seed,
               uint32_t *src, uint32_t *dst, void *stream);
+/* R-MAT straight into CSR form (memory-lean, for config C5): the same
+ * counter-based stream as gt_gen_rmat regenerated twice (out-degree count,
+ * then placement), so only offsets[V+1] (device) and edges[E] (device) are
+ * materialised.  Lists are in an arbitrary order; sort them (gt_sort_lists or
+ * two transposes) to get the config's CSR. */
+int gt_gen_rmat_csr(uint64_t scale, uint64_t num_edges, uint64_t seed, int permute,
+                    uint64_t *offsets, uint32_t *edges, void *stream);
 /* Web-like graph (config C4), two calls.  gt_gen_web_degrees draws every
  * vertex's out-degree from the Zipf inverse-CDF thresholds deg_cdf (ndeg u64
  * entries, device), scales it by deg_scale_q16 / 65536 (rounded, >= 1) and

@@ -69,6 +69,7 @@ SYMBOLS = {
     "gt_shard_transpose": (_int, [_vp, _u64, _u64, _u64, _u64, _u64, _vp, _vp, _vp, _stats_p]),
     "gt_gen_rmat": (_int, [_u64, _u64, _u64, _int, _vp, _vp, _vp]),
     "gt_gen_er": (_int, [_u64, _u64, _u64, _vp, _vp, _vp]),
+    "gt_gen_rmat_csr": (_int, [_u64, _u64, _u64, _int, _vp, _vp, _vp]),
     "gt_gen_web_degrees": (_int, [_u64, _u64, _vp, ctypes.c_uint32, ctypes.c_uint32, _vp, _u64p, _vp]),
     "gt_gen_web_edges": (_int, [_u64, _u64, _vp, _vp, ctypes.c_uint32, _vp, ctypes.c_uint32, ctypes.c_uint32, _vp, _vp,
                                 _vp]),

@@ -52,32 +52,59 @@ __device__ __forceinline__ uint64_t feistel_perm(const Feistel& f, uint64_t x) {
   return y;
 }
 
+__device__ __forceinline__ void rmat_edge(uint64_t e, uint64_t scale, uint64_t key, int permute, const Feistel& fp,
+                                          uint64_t& s, uint64_t& d) {
+  s = 0;
+  d = 0;
+  for (uint64_t l = 0; l < scale; l += 2) {
+    const uint64_t h = hash_at(key, e * 16 + (l >> 1));
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (l + q >= scale) break;
+      const uint32_t u = (uint32_t)(h >> (32 * q));
+      const uint64_t bit = 1ull << (scale - 1 - (l + q));
+      if (u < kRmatA) {
+      } else if (u < kRmatAB) {
+        d |= bit;
+      } else if (u < kRmatABC) {
+        s |= bit;
+      } else {
+        s |= bit;
+        d |= bit;
+      }
+    }
+  }
+  if (permute) {
+    s = feistel_perm(fp, s);
+    d = feistel_perm(fp, d);
+  }
+}
+
+// Two passes of the same counter-based R-MAT stream straight into a CSR
+// (lists in generation order, not sorted): out-degree count, then placement.
+__global__ void k_rmat_count(uint64_t scale, uint64_t E, uint64_t key, int permute, Feistel fp,
+                             uint32_t* __restrict__ cnt) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < E; e += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t s, d;
+    rmat_edge(e, scale, key, permute, fp, s, d);
+    atomicAdd(&cnt[s], 1u);
+  }
+}
+__global__ void k_rmat_place(uint64_t scale, uint64_t E, uint64_t key, int permute, Feistel fp,
+                             const uint64_t* __restrict__ offs, uint32_t* __restrict__ fill,
+                             uint32_t* __restrict__ edges) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < E; e += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t s, d;
+    rmat_edge(e, scale, key, permute, fp, s, d);
+    edges[offs[s] + atomicAdd(&fill[s], 1u)] = (uint32_t)d;
+  }
+}
+
 __global__ void k_rmat(uint64_t scale, uint64_t E, uint64_t key, int permute, Feistel fp, uint32_t* __restrict__ src,
                        uint32_t* __restrict__ dst) {
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < E; e += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t s = 0, d = 0;
-    for (uint64_t l = 0; l < scale; l += 2) {
-      const uint64_t h = hash_at(key, e * 16 + (l >> 1));
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        if (l + q >= scale) break;
-        const uint32_t u = (uint32_t)(h >> (32 * q));
-        const uint64_t bit = 1ull << (scale - 1 - (l + q));
-        if (u < kRmatA) {
-        } else if (u < kRmatAB) {
-          d |= bit;
-        } else if (u < kRmatABC) {
-          s |= bit;
-        } else {
-          s |= bit;
-          d |= bit;
-        }
-      }
-    }
-    if (permute) {
-      s = feistel_perm(fp, s);
-      d = feistel_perm(fp, d);
-    }
+    uint64_t s, d;
+    rmat_edge(e, scale, key, permute, fp, s, d);
     src[e] = (uint32_t)s;
     dst[e] = (uint32_t)d;
   }
@@ -176,6 +203,41 @@ int gt_gen_rmat(uint64_t scale, uint64_t E, uint64_t seed, int permute, uint32_t
   if (E) k_rmat<<<148 * 16, 256, 0, st>>>(scale, E, stream_key(seed, kStreamRmat), permute, fp, src, dst);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? GT_OK : gen_fail(e);
+}
+
+static Feistel make_feistel(uint64_t scale, uint64_t seed) {
+  Feistel fp{};
+  const int width = (int)(scale + (scale & 1));
+  fp.half = width / 2;
+  fp.mask = (1ull << fp.half) - 1;
+  fp.n = 1ull << scale;
+  const uint64_t pk = stream_key(seed, kStreamPerm);
+  for (int r = 0; r < 4; ++r) fp.keys[r] = hash_at(pk, (uint64_t)r);
+  return fp;
+}
+
+int gt_gen_rmat_csr(uint64_t scale, uint64_t E, uint64_t seed, int permute, uint64_t* offsets, uint32_t* edges,
+                    void* stream) {
+  if (scale < 1 || scale > 32 || !offsets || (E && !edges)) return GT_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint64_t V = 1ull << scale;
+  const Feistel fp = make_feistel(scale, seed);
+  const uint64_t key = stream_key(seed, kStreamRmat);
+  uint32_t* cnt = nullptr;
+  cudaError_t e = cudaMallocAsync(&cnt, V * 4, st);
+  if (e != cudaSuccess) return gen_fail(e);
+  int rc = GT_OK;
+  cudaMemsetAsync(cnt, 0, V * 4, st);
+  if (E) k_rmat_count<<<148 * 16, 256, 0, st>>>(scale, E, key, permute, fp, cnt);
+  rc = gt_prefix_sum(cnt, V, offsets, st);
+  if (rc == GT_OK && E) {
+    cudaMemsetAsync(cnt, 0, V * 4, st);
+    k_rmat_place<<<148 * 16, 256, 0, st>>>(scale, E, key, permute, fp, offsets, cnt, edges);
+    if ((e = cudaGetLastError()) != cudaSuccess) rc = gen_fail(e);
+  }
+  cudaFreeAsync(cnt, st);
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess && rc == GT_OK) rc = gen_fail(e);
+  return rc;
 }
 
 int gt_gen_er(uint64_t V, uint64_t E, uint64_t seed, uint32_t* src, uint32_t* dst, void* stream) {

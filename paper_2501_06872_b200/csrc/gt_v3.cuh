@@ -818,7 +818,18 @@ __device__ __forceinline__ uint32_t slot_owner32(uint32_t& cur, uint32_t& nb, ui
 template <int kMode, class Dec, int KK>
 __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __restrict__ rec, const RTile* __restrict__ tiles,
                                              const uint32_t* __restrict__ n_tiles, int D, Dec dec,
-                                             const uint64_t* __restrict__ base, uint32_t* __restrict__ out) {
+                                             const uint64_t* __restrict__ base, uint32_t* __restrict__ out,
+                                             unsigned long long* __restrict__ prof = nullptr) {
+  // optional phase profile (thread 0, clock64): 0 tile setup, 1 wait, 2 rank, 3 bases, 4 stage, 5 write
+  unsigned long long pacc[6] = {0, 0, 0, 0, 0, 0};
+  long long tprev = clock64();
+  auto tick = [&](int ph) {
+    if (prof && threadIdx.x == 0) {
+      const long long t = clock64();
+      pacc[ph] += (unsigned long long)(t - tprev);
+      tprev = t;
+    }
+  };
   constexpr int PT = W * KK * 32, PTP = PT + 8, K = KK;
   extern __shared__ __align__(128) unsigned char smem[];
   uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem);                         // PTP
@@ -885,10 +896,12 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __r
       const bool tail = tid < 4 && ti < o + n;
       uint32_t tv = 0;
       if (tail) tv = ldg_u32(gp - o + ti);
+      tick(0);
       mbar_wait_parity(&s_bar, ph);
       ph ^= 1;
       if (tail) s_buf[ti] = tv;
       __syncthreads();  // (A)
+      tick(1);
 
       const uint32_t iw = w * (K * 32);
       const uint32_t rel0 = (uint32_t)jj * PT;  // tile-relative position of item 0
@@ -925,7 +938,9 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __r
         for (int s = 0; s < K; ++s) slot(s, iw + s * 32 + lane < n);
       }
       __syncthreads();  // (B)
+      tick(2);
       flat_bases_pk<WH>(s_cnt, D, s_gcur, s_dtot, s_delta, s_tmp);
+      tick(3);
 #pragma unroll
       for (int s = 0; s < K; ++s) {
         if (n == (uint32_t)PT || iw + s * 32 + lane < n) {
@@ -936,14 +951,18 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __r
         }
       }
       __syncthreads();  // (C)
+      tick(4);
       writeout_tag<T, PT>(out, s_buf, s_tag, s_delta, n);
       zero_u32(s_cnt, round4(D * WH));
       for (int d = tid; d < D; d += T) s_gcur[d] += s_dtot[d];
       fence_proxy_async_smem();
       __syncthreads();  // (D)
+      tick(5);
       if (tid == 0 && jj + 1 < nplace) issue(jj + 1);
     }
   }
+  if (prof && threadIdx.x == 0)
+    for (int q = 0; q < 6; ++q) atomicAdd(&prof[q], pacc[q]);
 }
 
 // ---------------------------------------------------------------- L3 units

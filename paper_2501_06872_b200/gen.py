@@ -272,14 +272,24 @@ def generate_np(cfg: GraphConfig):
     return csr_from_pairs_np(s, d, cfg.num_vertices)
 
 
-def generate_device(cfg: GraphConfig, device="cuda", num_edges: int | None = None):
+def generate_device(cfg: GraphConfig, device="cuda", num_edges: int | None = None, lean: bool | None = None):
     """Generate the config's CSR directly in HBM with libgt.so.  Returns torch
-    tensors (offsets int64[V+1], edges int32[E]) holding uint64/uint32 bits."""
+    tensors (offsets int64[V+1], edges int32[E]) holding uint64/uint32 bits.
+
+    ``lean`` (default: R-MAT with more than 2^31 edges, i.e. config C5) never
+    materialises the edge pairs: gt_gen_rmat_csr writes the CSR with lists in
+    generation order and two transposes sort the lists (T(T(g)) has g's
+    offsets and every list ascending), so the peak is input + output + the
+    transpose workspace."""
     import torch
 
     from . import _lib
 
     E = cfg.num_edges if num_edges is None else int(num_edges)
+    if lean is None:
+        lean = cfg.kind == "rmat" and E > (1 << 31)
+    if lean and cfg.kind == "rmat":
+        return _rmat_lean_device(cfg, E, torch.device(device))
     V = cfg.num_vertices
     dev = torch.device(device)
     stream = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
@@ -340,3 +350,27 @@ def web_pairs_device(cfg: GraphConfig, device="cuda"):
                                        ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(dst.data_ptr()), stream)
         _lib.check(rc, "gt_gen_web_edges")
     return src, dst
+
+
+def _rmat_lean_device(cfg: GraphConfig, E: int, dev):
+    import torch
+
+    from . import _lib
+    from .transpose import transpose_device
+
+    V = cfg.num_vertices
+    with torch.cuda.device(dev):
+        stream = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+        offsets = torch.empty(V + 1, dtype=torch.int64, device=dev)
+        raw = torch.empty(E, dtype=torch.int32, device=dev)
+        rc = _lib.lib.gt_gen_rmat_csr(cfg.scale, E, cfg.seed, int(cfg.permute), ctypes.c_void_p(offsets.data_ptr()),
+                                      ctypes.c_void_p(raw.data_ptr()), stream)
+        _lib.check(rc, "gt_gen_rmat_csr")
+        t_off, t_edg, _ = transpose_device(offsets, raw, V)  # lists of T(g): ascending sources
+        del raw
+        torch.cuda.empty_cache()
+        edges = torch.empty(E, dtype=torch.int32, device=dev)
+        transpose_device(t_off, t_edg, V, t_offsets=offsets, t_edges=edges)  # T(T(g)): g with sorted lists
+        del t_off, t_edg
+        torch.cuda.empty_cache()
+    return offsets, edges

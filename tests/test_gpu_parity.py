@@ -290,3 +290,82 @@ def test_full_size_c4():
     o, e = oracle.transpose_c(off, edg, cfg.num_vertices)
     assert np.array_equal(got_off, o)
     assert np.array_equal(got_edg, e)
+
+
+@pytest.mark.parametrize("path_env", ["GT_FORCE_FULL", "GT_V2"], ids=["8-byte-records", "v2-compact"])
+def test_alternate_pipelines(path_env, monkeypatch, golden_cases):
+    """The 8-byte-record pipeline (taken when compact records cannot hold a
+    graph: E >= 2^32 or wide IDs, e.g. config C5) and the previous compact
+    kernels (multi-GPU receiver) against the goldens and random graphs."""
+    from paper_2501_06872_b200 import transpose_gpu
+
+    monkeypatch.setenv(path_env, "1")
+    for name, c in golden_cases.items():
+        out = transpose_gpu(_graph(c["nv"], c["off"], c["edg"]))
+        assert np.array_equal(out.graph.offsets, c["toff"]), name
+        assert np.array_equal(out.graph.edges, c["tedg"]), name
+    rng = np.random.default_rng(99)
+    for i in range(20):
+        g = random_graph(rng, max_vertices=3000, max_edges=40_000)
+        out = transpose_gpu(g)
+        toff, tedg = oracle.transpose_c(g.offsets, g.edges, g.num_vertices)
+        assert np.array_equal(out.graph.offsets, toff) and np.array_equal(out.graph.edges, tedg), i
+    from paper_2501_06872_b200 import gen, transpose_device
+
+    cfg = gen.CONFIGS["C1"]
+    off_d, edg_d = gen.generate_device(cfg)
+    t_off, t_edg, _ = transpose_device(off_d, edg_d, cfg.num_vertices)
+    o, e = oracle.transpose_c(off_d.cpu().numpy().view(np.uint64), edg_d.cpu().numpy().view(np.uint32), cfg.num_vertices)
+    assert np.array_equal(t_off.cpu().numpy().view(np.uint64), o)
+    assert np.array_equal(t_edg.cpu().numpy().view(np.uint32), e)
+
+
+def test_rmat_lean_generator_matches_pairs_path():
+    """gt_gen_rmat_csr + two transposes (the C5 generation path) gives the same
+    CSR as the pair generator + CSR build (and as the numpy generator)."""
+    from paper_2501_06872_b200 import gen
+
+    cfg = gen.GraphConfig("rmat-s16-perm", "rmat", 1 << 16, 1 << 20, scale=16, permute=True, seed=21)
+    o1, e1 = gen.generate_device(cfg, lean=True)
+    o2, e2 = gen.generate_device(cfg, lean=False)
+    assert np.array_equal(o1.cpu().numpy(), o2.cpu().numpy())
+    assert np.array_equal(e1.cpu().numpy(), e2.cpu().numpy())
+    on, en = gen.generate_np(cfg)
+    assert np.array_equal(o1.cpu().numpy().view(np.uint64), on)
+    assert np.array_equal(e1.cpu().numpy().view(np.uint32), en)
+
+
+@pytest.mark.slow
+def test_full_size_c5():
+    """Config C5 (R-MAT scale 29, edge factor 16, IDs permuted: 8.6e9 edges, E >= 2^32)
+    on one GPU: lean generation, transpose (8-byte-record pipeline), and the C
+    oracle on the host, bit for bit."""
+    import gc
+
+    import torch
+
+    from paper_2501_06872_b200 import gen, transpose_device
+
+    if os.environ.get("GT_SKIP_FULL") == "1" or os.environ.get("GT_SKIP_C5") == "1":
+        pytest.skip("GT_SKIP_FULL / GT_SKIP_C5")
+    free, total = torch.cuda.mem_get_info()
+    if total < 150 * (1 << 30):
+        pytest.skip("C5 needs a 180 GB-class GPU")
+    cfg = gen.CONFIGS["C5"]
+    V, E = cfg.num_vertices, cfg.num_edges
+    off_d, edg_d = gen.generate_device(cfg)
+    t_off, t_edg, st = transpose_device(off_d, edg_d, V, want_stats=True)
+    torch.cuda.synchronize()
+    off = off_d.cpu().numpy().view(np.uint64)
+    edg = edg_d.cpu().numpy().view(np.uint32)
+    del off_d, edg_d
+    got_off = t_off.cpu().numpy().view(np.uint64)
+    got_edg = t_edg.cpu().numpy().view(np.uint32)
+    del t_off, t_edg
+    torch.cuda.empty_cache()
+    assert off[-1] == E and got_off[-1] == E
+    o, e = oracle.transpose_c(off, edg, V)
+    del off, edg
+    gc.collect()
+    assert np.array_equal(got_off, o)
+    assert np.array_equal(got_edg, e)
