@@ -680,7 +680,9 @@ void make_plan3(const Plan& p, Plan3& q) {
   q.o_r2 = take(E * 4 + 64);
   q.o_tcnt = take(n1 * 4);
   q.o_tbase = take((n1 + 1) * 8);
-  q.o_status = take(((n1 + 1 + kScanTile - 1) / kScanTile + 1) * 8);
+  const uint64_t nscan = std::max<uint64_t>(n1 + 1, std::max<uint64_t>(q.max_t2 * (uint64_t)p.Db,
+                                                                        q.max_t3 * (uint64_t)p.Dc));
+  q.o_status = take(((nscan + kScanTile - 1) / kScanTile + 1) * 8);
   q.o_ctr = take(64);
   q.o_psrc = take((q.nplace + 2) * 4);
   q.o_prev = take((q.ntiles1 + 1) * 4);
@@ -801,10 +803,15 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
   k_l2_tiles<<<D1, 128, 0, st>>>(cstart, cfirst, Db, seghi, nh, tiles2, seg2);
   GT_LAUNCH_CHECK();
   const unsigned gt2 = (unsigned)std::min<uint64_t>(q.max_t2, (uint64_t)sms * 8);
+  GT_CUDA(cudaMemsetAsync(cnt2, 0, q.max_t2 * (uint64_t)Db * 4, st));  // the scan covers the unused tail too
   k_cnt_rec<<<gt2, 512, (size_t)Db * 4, st>>>(t_edges, tiles2, cfirst + D1, Db, DigSM{p.L + p.c, (uint32_t)(Db - 1)},
                                               cnt2);
   GT_LAUNCH_CHECK();
-  k_segscan<<<(unsigned)D1, 512, (size_t)Db * 8, st>>>(seg2, cnt + 4, Db, cnt2, base2, fbase, q.nfine, err);
+  // bases of every (chunk, fine digit): one device-wide exclusive scan of the
+  // per-bucket digit-major count tables (concatenated in bucket order, so the
+  // scan value already includes the bucket start), then the fine-bucket starts
+  if ((rc = scan_u32_to_u64(cnt2, (uint64_t)q.max_t2 * Db, base2, 0, false, status, ctr, st))) return rc;
+  k_segfix<<<(unsigned)D1, 512, 0, st>>>(seg2, cnt + 4, Db, base2, fbase, q.nfine, err);
   GT_LAUNCH_CHECK();
   {
     DecR1 dec;
@@ -858,10 +865,12 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
   GT_LAUNCH_CHECK();
   {
     const unsigned gt3 = (unsigned)std::min<uint64_t>(q.max_t3, (uint64_t)sms * 8);
+    GT_CUDA(cudaMemsetAsync(cnt3, 0, q.max_t3 * (uint64_t)Dc * 4, st));
     k_cnt_rec<<<gt3, 512, (size_t)Dc * 4, st>>>(r2, tiles3, cnt + 2, Dc, DigSM{p.nbs, (uint32_t)(Dc - 1)}, cnt3);
     GT_LAUNCH_CHECK();
-    k_segscan<<<(unsigned)std::min<uint64_t>(q.max_big, (uint64_t)sms * 16), 128, (size_t)Dc * 8, st>>>(
-        seg3, cnt + 1, Dc, cnt3, base3, t_offsets, V, err);
+    if ((rc = scan_u32_to_u64(cnt3, q.max_t3 * (uint64_t)Dc, base3, 0, false, status, ctr, st))) return rc;
+    k_segfix<<<(unsigned)std::min<uint64_t>(q.max_big, (uint64_t)sms * 8), 512, 0, st>>>(seg3, cnt + 1, Dc, base3,
+                                                                                      t_offsets, V, err);
     GT_LAUNCH_CHECK();
     DecR2 dec;
     dec.nbs = p.nbs;

@@ -7,7 +7,7 @@
 namespace gt {
 
 constexpr int kScanThreads = 512;
-constexpr int kScanItems = 8;  // per thread
+constexpr int kScanItems = 16;  // per thread
 constexpr int kScanTile = kScanThreads * kScanItems;
 constexpr uint64_t kFlagAgg = 1ull << 62;
 constexpr uint64_t kFlagInc = 2ull << 62;
@@ -38,12 +38,34 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_lookback(const In* __rest
   const uint64_t base = tile * kScanTile + (uint64_t)threadIdx.x * kScanItems;
   uint64_t v[kScanItems];
   uint64_t tsum = 0;
+  if constexpr (sizeof(In) == 4) {
+    // 16-byte loads when the thread's items are in range and aligned
+    const bool vec = base + kScanItems <= n && ((reinterpret_cast<uintptr_t>(in + base) & 15) == 0);
+    if (vec) {
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    const uint64_t i = base + k;
-    v[k] = (i < n) ? (uint64_t)in[i] : 0;
-    tsum += v[k];
+      for (int k = 0; k < kScanItems; k += 4) {
+        const uint4 q = *reinterpret_cast<const uint4*>(in + base + k);
+        v[k] = q.x;
+        v[k + 1] = q.y;
+        v[k + 2] = q.z;
+        v[k + 3] = q.w;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < kScanItems; ++k) {
+        const uint64_t i = base + k;
+        v[k] = (i < n) ? (uint64_t)in[i] : 0;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      const uint64_t i = base + k;
+      v[k] = (i < n) ? (uint64_t)in[i] : 0;
+    }
   }
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) tsum += v[k];
   // block inclusive scan of tsum
   const uint32_t lane = lane_id(), w = warp_id();
   uint64_t x = tsum;

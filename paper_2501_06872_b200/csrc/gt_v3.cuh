@@ -756,6 +756,40 @@ __global__ void __launch_bounds__(512) k_segscan(const SegDesc* __restrict__ seg
   }
 }
 
+// After one device-wide exclusive scan of all segments' count tables
+// (concatenated in segment order, k_scan_lookback): rebase each segment to its
+// output position (base += S.base - base[g0 * D]), write the digit starts
+// out[out_off + d] (when < out_limit) and flag digit totals >= 2^32.  Threads
+// of a CTA stride over one segment's D * nt entries (grid-stride over
+// segments); large segments are cheap because the scan already did the work.
+__global__ void __launch_bounds__(512) k_segfix(const SegDesc* __restrict__ segs, const uint32_t* __restrict__ n_segs,
+                                                int D, uint64_t* __restrict__ base, uint64_t* __restrict__ out,
+                                                uint64_t out_limit, unsigned int* __restrict__ err) {
+  const uint32_t ns = *n_segs;
+  for (uint32_t sg = blockIdx.x; sg < ns; sg += gridDim.x) {
+    const SegDesc S = segs[sg];
+    const uint64_t t0 = (uint64_t)S.g0 * D, n = (uint64_t)D * S.nt;
+    if (n == 0) {  // empty segment (empty coarse bucket): every digit starts at S.base
+      for (int d = threadIdx.x; d < D; d += blockDim.x)
+        if (S.out_off + d < out_limit) out[S.out_off + d] = S.base;
+      continue;
+    }
+    const uint64_t v0 = base[t0];
+    __syncthreads();  // every thread has read v0 before any entry changes
+    const uint64_t adj = S.base - v0;
+    if (adj)
+      for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) base[t0 + i] += adj;
+    __syncthreads();
+    for (int d = threadIdx.x; d < D; d += blockDim.x) {
+      const uint64_t st = base[t0 + (uint64_t)d * S.nt];
+      if (S.out_off + d < out_limit) out[S.out_off + d] = st;
+      const uint64_t nx = (d + 1 < D) ? base[t0 + (uint64_t)(d + 1) * S.nt] : ~0ull;
+      if (nx != ~0ull && nx - st >= (1ull << 32)) atomicExch(err, 1u);
+    }
+    __syncthreads();
+  }
+}
+
 // Record decoders for k_p2.
 // DecR1 (level 2): R1 -> R2; digit = fine digit B; source high bits from the
 // coarse bucket's seg_hi row (h = h0 + #boundaries <= position).
