@@ -810,9 +810,14 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
   // bases of every (chunk, fine digit): one device-wide exclusive scan of the
   // per-bucket digit-major count tables (concatenated in bucket order, so the
   // scan value already includes the bucket start), then the fine-bucket starts
-  if ((rc = scan_u32_to_u64(cnt2, (uint64_t)q.max_t2 * Db, base2, 0, false, status, ctr, st))) return rc;
-  k_segfix<<<(unsigned)D1, 512, 0, st>>>(seg2, cnt + 4, Db, base2, fbase, q.nfine, err);
-  GT_LAUNCH_CHECK();
+  if (env_int("GT_SEGSCAN", 0)) {
+    k_segscan<<<(unsigned)D1, 512, (size_t)Db * 8, st>>>(seg2, cnt + 4, Db, cnt2, base2, fbase, q.nfine, err);
+    GT_LAUNCH_CHECK();
+  } else {
+    if ((rc = scan_u32_to_u64(cnt2, (uint64_t)q.max_t2 * Db, base2, 0, false, status, ctr, st))) return rc;
+    k_segfix<<<(unsigned)D1, 512, 0, st>>>(seg2, cnt + 4, Db, base2, fbase, q.nfine, err);
+    GT_LAUNCH_CHECK();
+  }
   {
     DecR1 dec;
     dec.L = p.L;
@@ -824,7 +829,12 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
     dec.nh = nh;
     dec.seg_hi = seghi;
     if ((rc = tm.kbegin(1))) return rc;
-    if (env_int("GT_K2", 16) == 32) {
+    if (env_int("GT_K2", 16) == 8) {
+      const size_t sm = smem_p2(Db, kMode, 8);
+      if ((rc = set_smem(k_p2<kMode, DecR1, 8>, sm))) return rc;
+      const unsigned g = persistent_grid(k_p2<kMode, DecR1, 8>, T, sm, q.max_t2);
+      k_p2<kMode, DecR1, 8><<<g, T, sm, st>>>(t_edges, tiles2, cfirst + D1, Db, dec, base2, r2);
+    } else if (env_int("GT_K2", 16) == 32) {
       const size_t sm = smem_p2(Db, kMode, 32);
       if ((rc = set_smem(k_p2<kMode, DecR1, 32>, sm))) return rc;
       const unsigned g = persistent_grid(k_p2<kMode, DecR1, 32>, T, sm, q.max_t2);
@@ -838,7 +848,12 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
         GT_CUDA(cudaMallocAsync(&prof, 64, st));
         GT_CUDA(cudaMemsetAsync(prof, 0, 64, st));
       }
-      k_p2<kMode, DecR1, 16><<<g, T, sm, st>>>(t_edges, tiles2, cfirst + D1, Db, dec, base2, r2, prof);
+      if (prof) {
+        if ((rc = set_smem(k_p2<kMode, DecR1, 16, true>, sm))) return rc;
+        k_p2<kMode, DecR1, 16, true><<<g, T, sm, st>>>(t_edges, tiles2, cfirst + D1, Db, dec, base2, r2, prof);
+      } else {
+        k_p2<kMode, DecR1, 16><<<g, T, sm, st>>>(t_edges, tiles2, cfirst + D1, Db, dec, base2, r2);
+      }
       if (prof) {
         unsigned long long h[6];
         GT_CUDA(cudaMemcpyAsync(h, prof, 48, cudaMemcpyDeviceToHost, st));

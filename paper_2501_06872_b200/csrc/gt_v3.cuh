@@ -849,19 +849,22 @@ __device__ __forceinline__ uint32_t slot_owner32(uint32_t& cur, uint32_t& nb, ui
 
 // Place: per tile, place tiles of PT records are ranked by digit, staged with
 // their global indices, and written out (persistent, grid-stride over tiles).
-template <int kMode, class Dec, int KK>
-__global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __restrict__ rec, const RTile* __restrict__ tiles,
+template <int kMode, class Dec, int KK, bool kProf = false>
+__global__ void __launch_bounds__(T, (KK > 16 ? 2 : (KK < 16 ? 6 : 4))) k_p2(const uint32_t* __restrict__ rec, const RTile* __restrict__ tiles,
                                              const uint32_t* __restrict__ n_tiles, int D, Dec dec,
                                              const uint64_t* __restrict__ base, uint32_t* __restrict__ out,
                                              unsigned long long* __restrict__ prof = nullptr) {
-  // optional phase profile (thread 0, clock64): 0 tile setup, 1 wait, 2 rank, 3 bases, 4 stage, 5 write
-  unsigned long long pacc[6] = {0, 0, 0, 0, 0, 0};
-  long long tprev = clock64();
+  // phase profile (kProf builds only; thread 0, clock64): 0 tile setup, 1 wait,
+  // 2 rank, 3 bases, 4 stage, 5 write
+  unsigned long long pacc[kProf ? 6 : 1] = {};
+  long long tprev = kProf ? clock64() : 0;
   auto tick = [&](int ph) {
-    if (prof && threadIdx.x == 0) {
-      const long long t = clock64();
-      pacc[ph] += (unsigned long long)(t - tprev);
-      tprev = t;
+    if constexpr (kProf) {
+      if (threadIdx.x == 0) {
+        const long long t = clock64();
+        pacc[ph] += (unsigned long long)(t - tprev);
+        tprev = t;
+      }
     }
   };
   constexpr int PT = W * KK * 32, PTP = PT + 8, K = KK;
@@ -995,8 +998,10 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __r
       if (tid == 0 && jj + 1 < nplace) issue(jj + 1);
     }
   }
-  if (prof && threadIdx.x == 0)
-    for (int q = 0; q < 6; ++q) atomicAdd(&prof[q], pacc[q]);
+  if constexpr (kProf) {
+    if (threadIdx.x == 0)
+      for (int q = 0; q < 6; ++q) atomicAdd(&prof[q], pacc[q]);
+  }
 }
 
 // ---------------------------------------------------------------- L3 units
