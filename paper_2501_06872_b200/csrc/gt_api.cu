@@ -749,9 +749,13 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
   // level-3 units are aligned groups of 2^sbits fine buckets (<= ML3 local
   // vertices); R2 carries g3 = sbits fine-digit bits when it has room, else
   // the unit decodes the fine bucket from the record's position
-  int sbits = 0;
-  while ((ML3 >> p.c) >> (sbits + 1)) ++sbits;
-  const bool pos_fine = p.gbits < sbits;
+  auto log2_groups = [&](int ml) {
+    int b = 0;
+    while ((ml >> p.c) >> (b + 1)) ++b;
+    return b;
+  };
+  const bool pos_fine = p.gbits < log2_groups(256);   // R2 cannot name 256 / 2^c fine buckets
+  const int sbits = pos_fine ? log2_groups(ML3) : log2_groups(256);
   const int g3 = pos_fine ? 0 : sbits;
 
   GT_CUDA(cudaMemsetAsync(cnt, 0, 64, st));
@@ -924,7 +928,22 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
       return GT_OK;
     };
     if ((rc = tm.kbegin(2))) return rc;
-    rc = pos_fine ? go3(k_p3<kMode, true>) : go3(k_p3<kMode, false>);
+    a.prof = nullptr;
+    if (getenv("GT_PROF3")) {
+      GT_CUDA(cudaMallocAsync(&a.prof, 64, st));
+      GT_CUDA(cudaMemsetAsync(a.prof, 0, 64, st));
+      rc = pos_fine ? go3(k_p3<kMode, true, true>) : go3(k_p3<kMode, false, true>);
+      unsigned long long h[6];
+      GT_CUDA(cudaMemcpyAsync(h, a.prof, 48, cudaMemcpyDeviceToHost, st));
+      GT_CUDA(cudaStreamSynchronize(st));
+      double tot = 0;
+      for (int i = 0; i < 6; ++i) tot += (double)h[i];
+      fprintf(stderr, "[gt_prof3] fetch=%.3f wait=%.3f rank=%.3f bases=%.3f stage=%.3f store=%.3f (of %.3g CTA-cycles)\n",
+              h[0] / tot, h[1] / tot, h[2] / tot, h[3] / tot, h[4] / tot, h[5] / tot, tot);
+      cudaFreeAsync(a.prof, st);
+    } else {
+      rc = pos_fine ? go3(k_p3<kMode, true>) : go3(k_p3<kMode, false>);
+    }
     if (rc) return rc;
     GT_LAUNCH_CHECK();
     if ((rc = tm.kend(2))) return rc;

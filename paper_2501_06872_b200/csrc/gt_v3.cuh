@@ -43,7 +43,7 @@ constexpr int kMaxBnd = 512;     // source-high boundaries of an L2 tile held in
 constexpr int W3 = 16, K3 = 16;
 constexpr int CAP3 = W3 * K3 * 32;  // 8192 records per L3 unit
 constexpr int CAP3P = CAP3 + 8;
-constexpr int ML3 = 256;            // local vertices per L3 unit
+constexpr int ML3 = 512;            // local vertices per L3 unit (256 when R2 carries the fine bits)
 
 // One count tile of a record pass (L2: a chunk of a coarse bucket; L3-big: a
 // chunk of a big fine bucket).
@@ -1015,6 +1015,7 @@ struct P3Args {
   const uint64_t* fbase;  // CSC start of every fine bucket (+ total)
   int gbits;              // kPosFine == false: R2 keeps (fine & (2^gbits - 1)) << c | low digit
   uint32_t lvmask;        //   = (1 << (c + gbits)) - 1
+  unsigned long long* prof;  // kProf builds: 6 phase-cycle accumulators
   uint64_t V;
   uint64_t* t_offsets;
   uint32_t* t_edges;
@@ -1027,8 +1028,20 @@ inline size_t smem_p3(int mode) {
 
 // kPosFine: the record's fine bucket inside the unit comes from its position
 // (R2 has no room for fine-digit bits); else from the record's bits.
-template <int kMode, bool kPosFine>
+template <int kMode, bool kPosFine, bool kProf = false>
 __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
+  // phase profile (kProf builds only; thread 0, clock64): 0 fetch/issue, 1 wait, 2 rank, 3 bases+offsets, 4 stage, 5 store
+  unsigned long long pacc[kProf ? 6 : 1] = {};
+  long long tprev = kProf ? clock64() : 0;
+  auto tick = [&](int ph) {
+    if constexpr (kProf) {
+      if (threadIdx.x == 0) {
+        const long long t = clock64();
+        pacc[ph] += (unsigned long long)(t - tprev);
+        tprev = t;
+      }
+    }
+  };
   constexpr int TT = W3 * 32;
   extern __shared__ __align__(128) unsigned char smem[];
   uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem);       // 2 * CAP3P
@@ -1059,20 +1072,17 @@ __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
     mbar_arrive_expect_tx(&s_bar[b], full * 4);
     if (full) bulk_g2s(s_buf + b * CAP3P, gp - o, full * 4, &s_bar[b]);
   };
-  if (tid == 0) {
-    const uint32_t u0 = atomicAdd(a.ctr, 1u);
-    s_uidx[0] = u0;
-    if (u0 < nun) issue(u0, 0);
-  }
+  // static round-robin over the units (they are many and bounded in size):
+  // the next unit is known without a global atomic on the critical path
+  if (tid == 0 && blockIdx.x < nun) issue(blockIdx.x, 0);
   __syncthreads();
   uint32_t ph0 = 0, ph1 = 0;
   for (int it = 0;; ++it) {
     const int b = it & 1;
-    const uint32_t ui = s_uidx[b];
+    const uint32_t ui = blockIdx.x + (uint32_t)it * gridDim.x;
     if (ui >= nun) break;
     if (tid == 0) {  // prefetch the next unit into the other buffer (its last bulk store must have read it)
-      const uint32_t un = atomicAdd(a.ctr, 1u);
-      s_uidx[b ^ 1] = un;
+      const uint32_t un = ui + gridDim.x;
       bulk_wait_read<0>();
       if (un < nun) issue(un, b ^ 1);
     }
@@ -1086,6 +1096,7 @@ __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
     const bool tail = tid < 4 && ti < o + n;
     uint32_t tv = 0;
     if (tail) tv = ldg_u32(gp - o + ti);
+    tick(0);
     if (b == 0) { mbar_wait_parity(&s_bar[0], ph0); ph0 ^= 1; }
     else { mbar_wait_parity(&s_bar[1], ph1); ph1 ^= 1; }
     if (tail) buf[ti] = tv;
@@ -1093,6 +1104,7 @@ __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
     if constexpr (kPosFine)
       for (uint32_t q = tid; q < nbt; q += TT) s_fb[q] = (uint32_t)(a.fbase[u.f0 + 1 + q] - u.start);
     __syncthreads();  // (A)
+    tick(1);
     const uint32_t nloc = u.nf << a.c;
     const uint32_t seg0 = w * (K3 * 32);
     // local vertex = (fine bucket inside the unit, from the record's position) << c | low digit
@@ -1121,12 +1133,14 @@ __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
       rr[s] = r & a.src_mask;
     }
     __syncthreads();  // (B)
+    tick(2);
     flat_bases_pk<WH3>(s_cnt, (int)nloc, nullptr, nullptr, nullptr, s_tmp);
     {
       const uint64_t v0 = (uint64_t)u.f0 << a.c;
       for (uint32_t v = tid; v < nloc; v += TT)
         if (v0 + v < a.V) a.t_offsets[v0 + v] = u.start + (s_cnt[v * WH3] & 0xffffu);
     }
+    tick(3);
     uint32_t* t_e = a.t_edges + u.start;
     const uint32_t oo = align_items_u32(t_e);  // staging offset matching the output's 16B alignment
 #pragma unroll
@@ -1134,6 +1148,7 @@ __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
       if (seg0 + s * 32 + lane < n) buf[oo + ((s_cnt[(pk[s] >> 16) * WH3 + (w >> 1)] >> sh) & 0xffffu) + (pk[s] & 0xffffu)] = rr[s];
     fence_proxy_async_smem();
     __syncthreads();  // (C)
+    tick(4);
     {
       const uint32_t head = min(n, (4 - oo) & 3);
       const uint32_t mid = (n - head) & ~3u;
@@ -1145,10 +1160,15 @@ __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
       const uint32_t tl = head + mid + tid;
       if (tl < n && tid < 4) t_e[tl] = buf[oo + tl];
     }
-    zero_u32(s_cnt, round4(ML3 * WH3));
+    zero_u32(s_cnt, round4((int)nloc * WH3));  // rows >= nloc were never touched
     __syncthreads();  // (D)
+    tick(5);
   }
   if (tid == 0) bulk_wait_read<0>();
+  if constexpr (kProf) {
+    if (threadIdx.x == 0 && a.prof)
+      for (int q = 0; q < 6; ++q) atomicAdd(&a.prof[q], pacc[q]);
+  }
 }
 
 // ---------------------------------------------------------------- planning
