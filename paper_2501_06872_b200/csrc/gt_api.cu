@@ -765,7 +765,10 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
   GT_LAUNCH_CHECK();
   if ((rc = tm.mark())) return rc;
   // ---- step 1: level-1 partition of the CSR stream into R1 (in t_edges)
-  k_tile_src<<<(unsigned)((q.nplace + 1 + 255) / 256), 256, 0, st>>>(in, E, PT, q.nplace + 1, psrc);
+  // wide digit sets (>= 1024) use 8192-edge place tiles: half the per-digit work per record
+  const int k1 = env_int("GT_K1", D1 >= 1024 ? 32 : 16);
+  const uint64_t pt1 = (uint64_t)W * k1 * 32, nplace1 = (E + pt1 - 1) / pt1;
+  k_tile_src<<<(unsigned)((nplace1 + 1 + 255) / 256), 256, 0, st>>>(in, E, pt1, nplace1 + 1, psrc);
   GT_LAUNCH_CHECK();
   k_prev_src<<<(unsigned)((q.ntiles1 + 255) / 256), 256, 0, st>>>(in, E, CT1, q.ntiles1, prev);
   GT_LAUNCH_CHECK();
@@ -792,10 +795,16 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
     a.nh = nh;
     a.seg_hi = seghi;
     a.out = t_edges;
-    const size_t sm = smem_p1(D1, kMode);
-    if ((rc = set_smem(k_p1<kMode>, sm))) return rc;
     if ((rc = tm.kbegin(0))) return rc;
-    k_p1<kMode><<<(unsigned)q.ntiles1, T, sm, st>>>(a);
+    if (k1 == 32) {
+      const size_t sm = smem_p1(D1, kMode, 32);
+      if ((rc = set_smem(k_p1<kMode, 32>, sm))) return rc;
+      k_p1<kMode, 32><<<(unsigned)q.ntiles1, T, sm, st>>>(a);
+    } else {
+      const size_t sm = smem_p1(D1, kMode, 16);
+      if ((rc = set_smem(k_p1<kMode, 16>, sm))) return rc;
+      k_p1<kMode, 16><<<(unsigned)q.ntiles1, T, sm, st>>>(a);
+    }
     GT_LAUNCH_CHECK();
     if ((rc = tm.kend(0))) return rc;
   }
@@ -833,12 +842,13 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
     dec.nh = nh;
     dec.seg_hi = seghi;
     if ((rc = tm.kbegin(1))) return rc;
-    if (env_int("GT_K2", 16) == 8) {
+    const int k2 = env_int("GT_K2", Db >= 1024 ? 32 : 16);
+    if (k2 == 8) {
       const size_t sm = smem_p2(Db, kMode, 8);
       if ((rc = set_smem(k_p2<kMode, DecR1, 8>, sm))) return rc;
       const unsigned g = persistent_grid(k_p2<kMode, DecR1, 8>, T, sm, q.max_t2);
       k_p2<kMode, DecR1, 8><<<g, T, sm, st>>>(t_edges, tiles2, cfirst + D1, Db, dec, base2, r2);
-    } else if (env_int("GT_K2", 16) == 32) {
+    } else if (k2 == 32) {
       const size_t sm = smem_p2(Db, kMode, 32);
       if ((rc = set_smem(k_p2<kMode, DecR1, 32>, sm))) return rc;
       const unsigned g = persistent_grid(k_p2<kMode, DecR1, 32>, T, sm, q.max_t2);

@@ -24,6 +24,8 @@
 // shared atomics or the safe OR-mask mode); stability composes over levels, so
 // each CSC list ends in CSR order = ascending source.
 #pragma once
+#include <algorithm>
+
 #include "gt_common.cuh"
 #include "gt_scan.cuh"
 
@@ -423,9 +425,10 @@ struct P1Args {
   uint32_t* out;           // R1
 };
 
-inline size_t smem_p1(int D, int mode) {
-  return (size_t)PTP * 4 + (size_t)kWin * 8 + (size_t)PT * 2 + ((size_t)round4(D * WH) + (mode == kRankSafe ? (size_t)round4(D * WP) : 0)) * 4 +
-         (size_t)D * 4 * 3 + 40 * 4 + (CT1 / PT + 4) * 4;
+inline size_t smem_p1(int D, int mode, int KK = K) {
+  const size_t pt = (size_t)W * KK * 32, win = std::max<size_t>(1024, pt / 4);
+  return (pt + 8) * 4 + win * 8 + pt * 2 + ((size_t)round4(D * WH) + (mode == kRankSafe ? (size_t)round4(D * WP) : 0)) * 4 +
+         (size_t)D * 4 * 3 + 40 * 4 + (CT1 / pt + 4) * 4;
 }
 
 __device__ __forceinline__ void bulk_prefetch_l2(const void* g, uint32_t bytes) {
@@ -490,8 +493,11 @@ __device__ __forceinline__ void writeout_tag(uint32_t* __restrict__ out, const u
 // at or before the lane, else the carry from the previous slot); stable rank
 // by the coarse digit; stage payload + global index by digit; vectorised
 // write-out of the runs.  Requires E < 2^32 (u32 indices).
-template <int kMode>
-__global__ void __launch_bounds__(T, 4) k_p1(const P1Args a) {
+template <int kMode, int KK = K>
+__global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p1(const P1Args a) {
+  // place tiles of PT = W * KK * 32 edges; the offsets window doubles as the
+  // tag array, so it holds max(1024, PT / 4) entries
+  constexpr int K = KK, PT = W * KK * 32, PTP = PT + 8, kWin = (PT / 4 > 1024) ? PT / 4 : 1024;
   extern __shared__ __align__(128) unsigned char smem[];
   const int D = a.D;
   uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem);                         // PTP (landing, then stage)
