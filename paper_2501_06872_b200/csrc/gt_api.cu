@@ -843,12 +843,7 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
     dec.seg_hi = seghi;
     if ((rc = tm.kbegin(1))) return rc;
     const int k2 = env_int("GT_K2", Db >= 1024 ? 32 : 16);
-    if (k2 == 8) {
-      const size_t sm = smem_p2(Db, kMode, 8);
-      if ((rc = set_smem(k_p2<kMode, DecR1, 8>, sm))) return rc;
-      const unsigned g = persistent_grid(k_p2<kMode, DecR1, 8>, T, sm, q.max_t2);
-      k_p2<kMode, DecR1, 8><<<g, T, sm, st>>>(t_edges, tiles2, cfirst + D1, Db, dec, base2, r2);
-    } else if (k2 == 32) {
+    if (k2 == 32) {
       const size_t sm = smem_p2(Db, kMode, 32);
       if ((rc = set_smem(k_p2<kMode, DecR1, 32>, sm))) return rc;
       const unsigned g = persistent_grid(k_p2<kMode, DecR1, 32>, T, sm, q.max_t2);

@@ -856,7 +856,7 @@ __device__ __forceinline__ uint32_t slot_owner32(uint32_t& cur, uint32_t& nb, ui
 // Place: per tile, place tiles of PT records are ranked by digit, staged with
 // their global indices, and written out (persistent, grid-stride over tiles).
 template <int kMode, class Dec, int KK, bool kProf = false>
-__global__ void __launch_bounds__(T, (KK > 16 ? 2 : (KK < 16 ? 6 : 4))) k_p2(const uint32_t* __restrict__ rec, const RTile* __restrict__ tiles,
+__global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __restrict__ rec, const RTile* __restrict__ tiles,
                                              const uint32_t* __restrict__ n_tiles, int D, Dec dec,
                                              const uint64_t* __restrict__ base, uint32_t* __restrict__ out,
                                              unsigned long long* __restrict__ prof = nullptr) {
