@@ -781,7 +781,7 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
     a.offsets = in.offsets;
     a.edges = in.edges;
     a.e_begin = in.e_begin;
-    a.V = V;
+    a.V = in.V;  // source IDs (differ from destinations on the multi-GPU receiver)
     a.E = E;
     a.ntiles = q.ntiles1;
     a.D = D1;
@@ -1144,6 +1144,19 @@ int gt_prefix_sum(const uint32_t* counts, uint64_t n, uint64_t* out, void* strea
   return scan_u32_to_u64(counts, n, out, 0, true, status, ctr, st);
 }
 
+// Source-ordered (src, dst) records -> CSR over the source IDs: offsets from
+// the source changes (every ID gets its entry, empty sources included) and
+// destinations rebased to the local range.
+__global__ void k_rec_to_csr(const uint2* __restrict__ rec, uint64_t R, uint64_t Vs, uint32_t dst_base,
+                             uint64_t* __restrict__ offsets, uint32_t* __restrict__ edges) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= R; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t s = (i < R) ? rec[i].x : Vs;                   // sentinel past the end
+    const uint64_t prev = (i > 0) ? (uint64_t)rec[i - 1].x + 1 : 0;  // first source not yet started
+    for (uint64_t v = prev; v <= s && v <= Vs; ++v) offsets[v] = i;  // sources prev..s start at record i
+    if (i < R) edges[i] = rec[i].y - dst_base;
+  }
+}
+
 __global__ void k_add_base(uint64_t* a, uint64_t n, uint64_t base) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
     a[i] += base;
@@ -1245,7 +1258,42 @@ int gt_shard_transpose(const uint32_t* records, uint64_t R, uint64_t src_num_ver
   Plan p;
   if (src_num_vertices == 0 || src_num_vertices > (1ull << 32))
     return set_err(GT_EINVAL, "gt_shard_transpose: bad src_num_vertices");
-  if ((rc = make_plan(V, R, p, src_num_vertices))) return rc;
+  if ((rc = make_plan(V, R, p, src_num_vertices, v3_capable(R)))) return rc;
+  if (use_v3(p)) {
+    // the received stream is source-ordered: rebuild it as a CSR over the
+    // source IDs (offsets from the source changes, local destination IDs) and
+    // run the v3 pipeline with separate source / destination ID spaces
+    const uint64_t Vs = src_num_vertices;
+    const uint64_t b_off = align_up((Vs + 1) * 8, 256), b_e = align_up(R * 4, 256);
+    Plan3 q;
+    make_plan3(p, q);
+    void* w = nullptr;
+    if ((rc = cache_get(g_ws[dev], q.total + b_off + b_e, &w))) return rc;
+    unsigned char* ws = static_cast<unsigned char*>(w);
+    uint64_t* s_off = reinterpret_cast<uint64_t*>(ws + q.total);
+    uint32_t* s_edg = reinterpret_cast<uint32_t*>(ws + q.total + b_off);
+    k_rec_to_csr<<<(unsigned)std::min<uint64_t>((R + 255) / 256, 148 * 64), 256, 0, st>>>(
+        reinterpret_cast<const uint2*>(records), R, Vs, (uint32_t)dst_begin, s_off, s_edg);
+    GT_LAUNCH_CHECK();
+    int mode;
+    if ((rc = rank_mode_for(dev, st, &mode))) return rc;
+    Timer tm;
+    if ((rc = tm.init(stats != nullptr, st))) return rc;
+    const InCsr in{s_off, s_edg, 0, Vs};
+    rc = (mode == kRankAtomic) ? transpose_v3<kRankAtomic>(p, in, t_offsets_local, t_edges_local, ws, st, stats, tm)
+                               : transpose_v3<kRankSafe>(p, in, t_offsets_local, t_edges_local, ws, st, stats, tm);
+    if (rc) return rc;
+    if (global_base) {
+      k_add_base<<<148, 256, 0, st>>>(t_offsets_local, V + 1, global_base);
+      GT_LAUNCH_CHECK();
+    }
+    if (stats) {
+      GT_CUDA(cudaStreamSynchronize(st));
+      fill_stats(p, mode, tm, stats);
+      stats->workspace_bytes = q.total + b_off + b_e;
+    }
+    return GT_OK;
+  }
   void* w = nullptr;
   if ((rc = cache_get(g_ws[dev], p.total, &w))) return rc;
   unsigned char* ws = static_cast<unsigned char*>(w);
