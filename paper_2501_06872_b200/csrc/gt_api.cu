@@ -666,7 +666,8 @@ int transpose_core_c(const Plan& p, In in, uint64_t* t_offsets, uint32_t* t_edge
 struct Plan3 {
   uint64_t ntiles1 = 0, nplace = 0, nh = 0, max_t2 = 0, nfine = 0, max_big = 0, max_t3 = 0;
   uint64_t o_r2, o_tcnt, o_tbase, o_status, o_ctr, o_psrc, o_prev, o_seghi, o_cstart, o_cfirst, o_tiles2, o_cnt2,
-      o_base2, o_seg2, o_fbase, o_units, o_bigs, o_tiles3, o_cnt3, o_base3, o_seg3, o_cnt, o_err, total;
+      o_base2, o_seg2, o_fbase, o_units, o_bigs, o_tiles3, o_cnt3, o_base3, o_seg3, o_cnt, o_err, o_bnt, o_bfirst,
+      total;
 };
 
 bool v3_capable(uint64_t E) { return E < (1ull << 32) && getenv("GT_V2") == nullptr; }
@@ -713,6 +714,8 @@ void make_plan3(const Plan& p, Plan3& q) {
   q.o_seg3 = take(q.max_big * sizeof(v3::SegDesc));
   q.o_cnt = take(64);
   q.o_err = take(4);
+  q.o_bnt = take((q.max_big + 1) * 4);
+  q.o_bfirst = take((q.max_big + 2) * 8);
   q.total = off;
 }
 
@@ -896,14 +899,35 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
   k_plan3<<<(unsigned)((q.nfine / (1u << sbits) + 255) / 256 + 1), 256, 0, st>>>(fbase, (uint32_t)q.nfine, sbits,
                                                                                    units, cnt + 0, bigs, cnt + 1);
   GT_LAUNCH_CHECK();
-  k_big_tiles<<<1, 1024, 0, st>>>(bigs, cnt + 1, p.c, tiles3, cnt + 2, seg3);
-  GT_LAUNCH_CHECK();
+  {
+    uint32_t* bnt = reinterpret_cast<uint32_t*>(ws + q.o_bnt);
+    uint64_t* bfirst = reinterpret_cast<uint64_t*>(ws + q.o_bfirst);
+    const unsigned gb = (unsigned)std::min<uint64_t>((q.max_big + 255) / 256, (uint64_t)sms * 4);
+    // exclusive scan over the real buckets (device count) -> bfirst[0..n_big]
+    const uint64_t tiles = std::max<uint64_t>(1, (q.max_big + 1 + kScanTile - 1) / kScanTile);
+    GT_CUDA(cudaMemsetAsync(status, 0, tiles * 8, st));
+    GT_CUDA(cudaMemsetAsync(ctr, 0, 4, st));
+    GT_CUDA(cudaMemsetAsync(bnt, 0, (q.max_big + 1) * 4, st));
+    k_big_nt<<<gb, 256, 0, st>>>(bigs, cnt + 1, bnt);
+    k_scan_lookback<uint32_t><<<(unsigned)tiles, kScanThreads, 0, st>>>(bnt, q.max_big + 1, bfirst, 0, 1, status, ctr,
+                                                                         cnt + 1, 1);
+    GT_LAUNCH_CHECK();
+    k_big_write<<<gb, 256, 0, st>>>(bigs, cnt + 1, bfirst, p.c, tiles3, cnt + 2, seg3);
+    GT_LAUNCH_CHECK();
+  }
   {
     const unsigned gt3 = (unsigned)std::min<uint64_t>(q.max_t3, (uint64_t)sms * 8);
-    GT_CUDA(cudaMemsetAsync(cnt3, 0, q.max_t3 * (uint64_t)Dc * 4, st));
     k_cnt_rec<<<gt3, 512, (size_t)Dc * 4, st>>>(r2, tiles3, cnt + 2, Dc, DigSM{p.nbs, (uint32_t)(Dc - 1)}, cnt3);
     GT_LAUNCH_CHECK();
-    if ((rc = scan_u32_to_u64(cnt3, q.max_t3 * (uint64_t)Dc, base3, 0, false, status, ctr, st))) return rc;
+    {  // scan only the real tiles' rows: n = n_tiles3 * Dc (device count)
+      const uint64_t n3 = q.max_t3 * (uint64_t)Dc;
+      const uint64_t tiles = std::max<uint64_t>(1, (n3 + kScanTile - 1) / kScanTile);
+      GT_CUDA(cudaMemsetAsync(status, 0, tiles * 8, st));
+      GT_CUDA(cudaMemsetAsync(ctr, 0, 4, st));
+      k_scan_lookback<uint32_t><<<(unsigned)tiles, kScanThreads, 0, st>>>(cnt3, n3, base3, 0, 0, status, ctr, cnt + 2,
+                                                                           (uint64_t)Dc);
+      GT_LAUNCH_CHECK();
+    }
     k_segfix<<<(unsigned)std::min<uint64_t>(q.max_big, (uint64_t)sms * 8), 512, 0, st>>>(seg3, cnt + 1, Dc, base3,
                                                                                       t_offsets, V, err);
     GT_LAUNCH_CHECK();

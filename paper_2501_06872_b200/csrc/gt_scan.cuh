@@ -28,7 +28,11 @@ template <typename In>
 __global__ void __launch_bounds__(kScanThreads) k_scan_lookback(const In* __restrict__ in, uint64_t n,
                                                                  uint64_t* __restrict__ out, uint64_t init,
                                                                  int write_total, uint64_t* status,
-                                                                 unsigned int* tile_ctr) {
+                                                                 unsigned int* tile_ctr,
+                                                                 const uint32_t* __restrict__ n_dev = nullptr,
+                                                                 uint64_t n_unit = 1) {
+  // optional device-side length: n = min(n, *n_dev * n_unit) (the grid is sized for n)
+  if (n_dev) n = umin64(n, (uint64_t)(*n_dev) * n_unit);
   __shared__ uint64_t s_warp[kScanThreads / 32];
   __shared__ uint64_t s_excl;
   __shared__ unsigned int s_tile;

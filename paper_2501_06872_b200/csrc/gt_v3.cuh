@@ -1287,6 +1287,42 @@ __global__ void k_plan3(const uint64_t* __restrict__ fbase, uint32_t nfine, int 
   }
 }
 
+// Big fine buckets -> L3 tiles, in parallel: k_big_nt writes each bucket's
+// tile count, a scan gives the first tile of each, k_big_write writes the
+// tiles, the segments and the tile total.
+__global__ void k_big_nt(const Big3* __restrict__ bigs, const uint32_t* __restrict__ n_big, uint32_t* __restrict__ bnt) {
+  const uint32_t nb = *n_big;
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nb; q += gridDim.x * blockDim.x)
+    bnt[q] = (uint32_t)((bigs[q].n + CT2 - 1) / CT2);
+}
+__global__ void k_big_write(const Big3* __restrict__ bigs, const uint32_t* __restrict__ n_big,
+                            const uint64_t* __restrict__ tfirst, int c, RTile* __restrict__ tiles,
+                            uint32_t* __restrict__ n_tiles, SegDesc* __restrict__ segs) {
+  const uint32_t nb = *n_big;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *n_tiles = (uint32_t)tfirst[nb];
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nb; q += gridDim.x * blockDim.x) {
+    const Big3 bg = bigs[q];
+    const uint32_t g0 = (uint32_t)tfirst[q], nt = (uint32_t)(tfirst[q + 1] - tfirst[q]);
+    SegDesc S;
+    S.base = bg.start;
+    S.out_off = (uint64_t)bg.f << c;
+    S.g0 = g0;
+    S.nt = nt;
+    segs[q] = S;
+    for (uint32_t j = 0; j < nt; ++j) {
+      RTile t;
+      t.start = bg.start + (uint64_t)j * CT2;
+      t.n = (uint32_t)umin64(CT2, bg.n - (uint64_t)j * CT2);
+      t.seg = q;
+      t.j = j;
+      t.nt = nt;
+      t.h0 = 0;
+      t.nbnd = 0;
+      tiles[g0 + j] = t;
+    }
+  }
+}
+
 // Big fine buckets -> L3 tiles and segments (one CTA).  The biggest buckets go
 // first in the tile order (persistent CTAs then start on them).
 __global__ void __launch_bounds__(1024) k_big_tiles(const Big3* __restrict__ bigs, const uint32_t* __restrict__ n_big,
