@@ -37,7 +37,8 @@ constexpr int T = W * 32;
 constexpr int K = 16;            // items per thread per place tile
 constexpr int PT = W * K * 32;   // 4096 records per place tile
 constexpr int PTP = PT + 8;      // landing buffer (alignment slack)
-constexpr int CT1 = 32768;       // L1 count tile (edges)
+constexpr int CT1_SHIFT = 16;
+constexpr int CT1 = 1 << CT1_SHIFT;  // L1 count tile (edges)
 constexpr int G1 = 8;            // count tiles per k_c1 CTA
 constexpr int CT2 = 32768;       // L2 / L3-big count tile (records of one segment)
 constexpr int kWin = 1024;       // offsets window (entries) per L1 place tile
@@ -387,7 +388,7 @@ __global__ void __launch_bounds__(512) k_c1(const uint32_t* __restrict__ edges, 
   const uint64_t b = k0 * CT1, n = umin64(E, b + (uint64_t)nt * CT1) - b;
   const uint32_t* p = edges + b;
   const uint32_t head = (uint32_t)umin64(n, (4 - align_items_u32(p)) & 3);
-  for (uint32_t i = threadIdx.x; i < head; i += blockDim.x) smem_inc(&s_h[(i >> 15) * D + (p[i] >> shift)]);
+  for (uint32_t i = threadIdx.x; i < head; i += blockDim.x) smem_inc(&s_h[(i >> CT1_SHIFT) * D + (p[i] >> shift)]);
   const uint4* p4 = reinterpret_cast<const uint4*>(p + head);
   const uint64_t n4 = (n - head) >> 2;
   for (uint64_t q = threadIdx.x; q < n4; q += blockDim.x) {
@@ -395,13 +396,13 @@ __global__ void __launch_bounds__(512) k_c1(const uint32_t* __restrict__ edges, 
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p4 + q));
     const uint32_t i = head + (uint32_t)q * 4;
-    smem_inc(&s_h[(i >> 15) * D + (v.x >> shift)]);
-    smem_inc(&s_h[((i + 1) >> 15) * D + (v.y >> shift)]);
-    smem_inc(&s_h[((i + 2) >> 15) * D + (v.z >> shift)]);
-    smem_inc(&s_h[((i + 3) >> 15) * D + (v.w >> shift)]);
+    smem_inc(&s_h[(i >> CT1_SHIFT) * D + (v.x >> shift)]);
+    smem_inc(&s_h[((i + 1) >> CT1_SHIFT) * D + (v.y >> shift)]);
+    smem_inc(&s_h[((i + 2) >> CT1_SHIFT) * D + (v.z >> shift)]);
+    smem_inc(&s_h[((i + 3) >> CT1_SHIFT) * D + (v.w >> shift)]);
   }
   for (uint64_t i = head + n4 * 4 + threadIdx.x; i < n; i += blockDim.x)
-    smem_inc(&s_h[((uint32_t)i >> 15) * D + (p[i] >> shift)]);
+    smem_inc(&s_h[((uint32_t)i >> CT1_SHIFT) * D + (p[i] >> shift)]);
   __syncthreads();
   for (int i = threadIdx.x; i < G1 * D; i += blockDim.x) {
     const int d = i / G1, t = i - d * G1;
