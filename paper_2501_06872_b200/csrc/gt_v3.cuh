@@ -37,7 +37,7 @@ constexpr int T = W * 32;
 constexpr int K = 16;            // items per thread per place tile
 constexpr int PT = W * K * 32;   // 4096 records per place tile
 constexpr int PTP = PT + 8;      // landing buffer (alignment slack)
-constexpr int CT1_SHIFT = 16;
+constexpr int CT1_SHIFT = 17;
 constexpr int CT1 = 1 << CT1_SHIFT;  // L1 count tile (edges)
 constexpr int G1 = 8;            // count tiles per k_c1 CTA
 constexpr int CT2 = 32768;       // L2 / L3-big count tile (records of one segment)
