@@ -65,6 +65,7 @@ inline int bits_for(uint64_t V) {  // bits to address IDs 0..V-1 (>= 1)
 struct Plan {
   uint64_t V = 0, E = 0;
   bool compact = false;  // 4-byte records (R1/R2), see gt_kernels.cuh
+  bool wide = false;     // v3 with 64-bit positions and R2 = source (u32) + low digit (u8): E >= 2^32 or nbs + c > 32
   int L = 0, nsh = 0;    // compact R1: source low bits, source high bits
   int gbits = 0;         // compact R2: fine-digit bits kept (final units = aligned groups of 2^gbits)
   int nb = 0, nbs = 0, a = 0, b = 0, c = 0;
@@ -124,7 +125,42 @@ int make_plan(uint64_t V, uint64_t E, Plan& p, uint64_t Vsrc = 0, bool wide_b = 
       p.gbits = std::max(0, gb);
     }
   }
-  if (!p.compact) {
+  // wide v3 form: graphs with E >= 2^32, or whose source IDs leave no room for
+  // the low digit in a 4-byte R2 (nbs + c > 32); GT_WIDE=1 forces it (tests)
+  const bool v3ok = getenv("GT_V2") == nullptr && getenv("GT_FORCE_FULL") == nullptr;
+  if (v3ok && (!p.compact || E >= (1ull << 32) || getenv("GT_WIDE") != nullptr)) {
+    int cc = 1;
+    while (cc < 8 && (double)(1u << (cc + 1)) * std::max(avg, 1.0) <= (double)kFCapC / 2.0) ++cc;
+    cc = std::min(cc, p.nb);
+    const int rem = p.nb - cc;
+    int ca = rem, cb = 0;
+    if (rem > 10) {
+      cb = std::min(10, std::max(8, rem - 11));
+      ca = rem - cb;
+    }
+    if (const char* sp = getenv("GT_SPLIT")) {
+      int xa = 0, xb = 0, xc = 0;
+      if (sscanf(sp, "%d,%d,%d", &xa, &xb, &xc) == 3 && xa + xb + xc == p.nb && xc >= 1 && xc <= 8 && xa >= 0 &&
+          xb >= 0) {
+        ca = xa;
+        cb = xb;
+        cc = xc;
+      }
+    }
+    const int L = 32 - (cb + cc);
+    const int nsh = std::max(0, p.nbs - L);
+    if (cc >= 1 && cc <= 8 && ca <= 11 && cb <= 10 && L >= 1 && nsh <= 16) {
+      p.compact = false;
+      p.wide = true;
+      a = ca;
+      b = cb;
+      c = cc;
+      p.L = L;
+      p.nsh = nsh;
+      p.gbits = 0;
+    }
+  }
+  if (!p.compact && !p.wide) {
     // final digit: fine buckets of 2^c vertices averaging <= kFCap/2 records
     while (c < 8 && (double)(1u << (c + 1)) * std::max(avg, 1.0) <= (double)kFCap / 2.0) ++c;
     c = std::min(c, p.nb);
@@ -667,11 +703,11 @@ struct Plan3 {
   uint64_t ntiles1 = 0, nplace = 0, nh = 0, max_t2 = 0, nfine = 0, max_big = 0, max_t3 = 0;
   uint64_t o_r2, o_tcnt, o_tbase, o_status, o_ctr, o_psrc, o_prev, o_seghi, o_cstart, o_cfirst, o_tiles2, o_cnt2,
       o_base2, o_seg2, o_fbase, o_units, o_bigs, o_tiles3, o_cnt3, o_base3, o_seg3, o_cnt, o_err, o_bnt, o_bfirst,
-      total;
+      o_r2lv, total;
 };
 
 bool v3_capable(uint64_t E) { return E < (1ull << 32) && getenv("GT_V2") == nullptr; }
-bool use_v3(const Plan& p) { return p.compact && v3_capable(p.E); }
+bool use_v3(const Plan& p) { return p.wide || (p.compact && v3_capable(p.E)); }
 
 void make_plan3(const Plan& p, Plan3& q) {
   const uint64_t E = p.E;
@@ -690,6 +726,7 @@ void make_plan3(const Plan& p, Plan3& q) {
   };
   const uint64_t n1 = (uint64_t)p.D1 * q.ntiles1;
   q.o_r2 = take(E * 4 + 64);
+  q.o_r2lv = take(p.wide ? E + 64 : 0);  // wide: low digit of every R2 record (+ padding for 16-byte block loads)
   q.o_tcnt = take(n1 * 4);
   q.o_tbase = take((n1 + 1) * 8);
   const uint64_t nscan = std::max<uint64_t>(n1 + 1, std::max<uint64_t>(q.max_t2 * (uint64_t)p.Db,
@@ -734,6 +771,7 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
   const uint64_t V = p.V, E = p.E;
   const int D1 = p.D1, Db = p.Db, Dc = p.Dc;
   uint32_t* r2 = reinterpret_cast<uint32_t*>(ws + q.o_r2);
+  uint8_t* r2lv = p.wide ? reinterpret_cast<uint8_t*>(ws + q.o_r2lv) : nullptr;  // wide: R2 low digits
   uint32_t* tcnt = reinterpret_cast<uint32_t*>(ws + q.o_tcnt);
   uint64_t* tbase = reinterpret_cast<uint64_t*>(ws + q.o_tbase);
   uint64_t* status = reinterpret_cast<uint64_t*>(ws + q.o_status);
@@ -768,7 +806,7 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
     while ((ml >> p.c) >> (b + 1)) ++b;
     return b;
   };
-  const bool pos_fine = p.gbits < log2_groups(256);   // R2 cannot name 256 / 2^c fine buckets
+  const bool pos_fine = p.wide || p.gbits < log2_groups(256);   // R2 cannot name 256 / 2^c fine buckets
   const int sbits = pos_fine ? log2_groups(ML3) : log2_groups(256);
   const int g3 = pos_fine ? 0 : sbits;
 
@@ -780,12 +818,14 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
   if ((rc = tm.mark())) return rc;
   // ---- step 1: level-1 partition of the CSR stream into R1 (in t_edges)
   // level 1 uses 8192-edge place tiles (measured: C3 k_p1 2.82 -> 2.79 ms, C4 8.75 -> 7.56 ms)
-  const int k1 = env_int("GT_K1", 32);
+  // (wide graphs: 4096-edge tiles keep 2 CTAs/SM with 2048 coarse digits)
+  const int k1 = env_int("GT_K1", p.wide ? 16 : 32);
   const uint64_t pt1 = (uint64_t)W * k1 * 32, nplace1 = (E + pt1 - 1) / pt1;
   k_tile_src<<<(unsigned)((nplace1 + 1 + 255) / 256), 256, 0, st>>>(in, E, pt1, nplace1 + 1, psrc);
   GT_LAUNCH_CHECK();
   k_prev_src<<<(unsigned)((q.ntiles1 + 255) / 256), 256, 0, st>>>(in, E, CT1, q.ntiles1, prev);
   GT_LAUNCH_CHECK();
+  if ((rc = set_smem(k_c1, (size_t)G1 * D1 * 4))) return rc;
   k_c1<<<(unsigned)((q.ntiles1 + G1 - 1) / G1), 512, (size_t)G1 * D1 * 4, st>>>(in.edges, E, q.ntiles1, D1,
                                                                                 p.b + p.c, tcnt);
   GT_LAUNCH_CHECK();
@@ -810,7 +850,16 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
     a.seg_hi = seghi;
     a.out = t_edges;
     if ((rc = tm.kbegin(0))) return rc;
-    if (k1 == 32) {
+    auto go1 = [&](auto kern, int kk) -> int {
+      const size_t sm = smem_p1(D1, kMode, kk);
+      int r;
+      if ((r = set_smem(kern, sm))) return r;
+      kern<<<(unsigned)q.ntiles1, T, sm, st>>>(a);
+      return GT_OK;
+    };
+    if (p.wide) {  // 64-bit R1 positions
+      if ((rc = (k1 == 32) ? go1(k_p1<kMode, 32, true>, 32) : go1(k_p1<kMode, 16, true>, 16))) return rc;
+    } else if (k1 == 32) {
       const size_t sm = smem_p1(D1, kMode, 32);
       if ((rc = set_smem(k_p1<kMode, 32>, sm))) return rc;
       k_p1<kMode, 32><<<(unsigned)q.ntiles1, T, sm, st>>>(a);
@@ -857,7 +906,19 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
     dec.seg_hi = seghi;
     if ((rc = tm.kbegin(1))) return rc;
     const int k2 = env_int("GT_K2", Db >= 1024 ? 32 : 16);
-    if (k2 == 32) {
+    if (p.wide) {  // R2 = source array + low-digit bytes, 64-bit positions
+      auto go2 = [&](auto kern, int kk) -> int {
+        const size_t sm = smem_p2(Db, kMode, kk, kIoSplit);
+        int r;
+        if ((r = set_smem(kern, sm))) return r;
+        const unsigned g = persistent_grid(kern, T, sm, q.max_t2);
+        kern<<<g, T, sm, st>>>(t_edges, tiles2, cfirst + D1, Db, dec, base2, r2, nullptr, nullptr, r2lv);
+        return GT_OK;
+      };
+      if ((rc = (k2 == 32) ? go2(k_p2<kMode, DecR1, 32, false, kIoSplit>, 32)
+                           : go2(k_p2<kMode, DecR1, 16, false, kIoSplit>, 16)))
+        return rc;
+    } else if (k2 == 32) {
       const size_t sm = smem_p2(Db, kMode, 32);
       if ((rc = set_smem(k_p2<kMode, DecR1, 32>, sm))) return rc;
       const unsigned g = persistent_grid(k_p2<kMode, DecR1, 32>, T, sm, q.max_t2);
@@ -917,7 +978,8 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
   }
   {
     const unsigned gt3 = (unsigned)std::min<uint64_t>(q.max_t3, (uint64_t)sms * 8);
-    k_cnt_rec<<<gt3, 512, (size_t)Dc * 4, st>>>(r2, tiles3, cnt + 2, Dc, DigSM{p.nbs, (uint32_t)(Dc - 1)}, cnt3);
+    if (p.wide) k_cnt_lv<<<gt3, 512, (size_t)Dc * 4, st>>>(r2lv, tiles3, cnt + 2, Dc, cnt3);
+    else k_cnt_rec<<<gt3, 512, (size_t)Dc * 4, st>>>(r2, tiles3, cnt + 2, Dc, DigSM{p.nbs, (uint32_t)(Dc - 1)}, cnt3);
     GT_LAUNCH_CHECK();
     {  // scan only the real tiles' rows: n = n_tiles3 * Dc (device count)
       const uint64_t n3 = q.max_t3 * (uint64_t)Dc;
@@ -933,13 +995,21 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
     GT_LAUNCH_CHECK();
     DecR2 dec;
     dec.nbs = p.nbs;
-    dec.src_mask = (p.nbs >= 32) ? 0xffffffffu : (uint32_t)((1ull << p.nbs) - 1);
+    dec.src_mask = (p.nbs >= 32 || p.wide) ? 0xffffffffu : (uint32_t)((1ull << p.nbs) - 1);
     dec.maskC = (uint32_t)(Dc - 1);
-    const size_t sm = smem_p2(Dc, kMode, 16);
-    if ((rc = set_smem(k_p2<kMode, DecR2, 16>, sm))) return rc;
-    const unsigned g = persistent_grid(k_p2<kMode, DecR2, 16>, T, sm, q.max_t3);
     if ((rc = tm.kbegin(3))) return rc;
-    k_p2<kMode, DecR2, 16><<<g, T, sm, st>>>(r2, tiles3, cnt + 2, Dc, dec, base3, t_edges);
+    if (p.wide) {
+      const size_t sm = smem_p2(Dc, kMode, 16, kIoLv);
+      if ((rc = set_smem(k_p2<kMode, DecR2, 16, false, kIoLv>, sm))) return rc;
+      const unsigned g = persistent_grid(k_p2<kMode, DecR2, 16, false, kIoLv>, T, sm, q.max_t3);
+      k_p2<kMode, DecR2, 16, false, kIoLv><<<g, T, sm, st>>>(r2, tiles3, cnt + 2, Dc, dec, base3, t_edges, nullptr,
+                                                              r2lv, nullptr);
+    } else {
+      const size_t sm = smem_p2(Dc, kMode, 16);
+      if ((rc = set_smem(k_p2<kMode, DecR2, 16>, sm))) return rc;
+      const unsigned g = persistent_grid(k_p2<kMode, DecR2, 16>, T, sm, q.max_t3);
+      k_p2<kMode, DecR2, 16><<<g, T, sm, st>>>(r2, tiles3, cnt + 2, Dc, dec, base3, t_edges);
+    }
     GT_LAUNCH_CHECK();
     if ((rc = tm.kend(3))) return rc;
   }
@@ -951,15 +1021,16 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
     a.ctr = cnt + 3;
     a.c = p.c;
     a.nbs = p.nbs;
-    a.src_mask = (p.nbs >= 32) ? 0xffffffffu : (uint32_t)((1ull << p.nbs) - 1);
+    a.src_mask = (p.nbs >= 32 || p.wide) ? 0xffffffffu : (uint32_t)((1ull << p.nbs) - 1);
     a.mask_c = (uint32_t)(Dc - 1);
+    a.lv = r2lv;
     a.fbase = fbase;
     a.gbits = g3;
     a.lvmask = (uint32_t)((1ull << (p.c + g3)) - 1);
     a.V = V;
     a.t_offsets = t_offsets;
     a.t_edges = t_edges;
-    const size_t sm = smem_p3(kMode);
+    const size_t sm = smem_p3(kMode, p.wide);
     auto go3 = [&](auto kern) -> int {
       int r;
       if ((r = set_smem(kern, sm))) return r;
@@ -969,7 +1040,7 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
     };
     if ((rc = tm.kbegin(2))) return rc;
     a.prof = nullptr;
-    if (getenv("GT_PROF3")) {
+    if (getenv("GT_PROF3") && !p.wide) {
       GT_CUDA(cudaMallocAsync(&a.prof, 64, st));
       GT_CUDA(cudaMemsetAsync(a.prof, 0, 64, st));
       rc = pos_fine ? go3(k_p3<kMode, true, true>) : go3(k_p3<kMode, false, true>);
@@ -981,6 +1052,8 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
       fprintf(stderr, "[gt_prof3] fetch=%.3f wait=%.3f rank=%.3f bases=%.3f stage=%.3f store=%.3f (of %.3g CTA-cycles)\n",
               h[0] / tot, h[1] / tot, h[2] / tot, h[3] / tot, h[4] / tot, h[5] / tot, tot);
       cudaFreeAsync(a.prof, st);
+    } else if (p.wide) {
+      rc = go3(k_p3<kMode, true, false, true>);
     } else {
       rc = pos_fine ? go3(k_p3<kMode, true>) : go3(k_p3<kMode, false>);
     }

@@ -235,12 +235,12 @@ __device__ __forceinline__ uint32_t rank_pk(uint32_t* c, uint32_t* sc, uint32_t 
 }
 // After ranking: tab[d * WHN + k] holds (warp 2k, warp 2k+1) tile positions of
 // their first digit-d item; dtot per digit; delta[d] = gcur[d] - digit start.
-template <int WHN>
-__device__ __forceinline__ void flat_bases_pk(uint32_t* tab, int D, const uint32_t* gcur, uint32_t* dtot,
-                                              uint32_t* delta, uint32_t* tmp) {
+// Epilogue form: epi(d, b, e) per digit with its tile-local start b and end e.
+template <int WHN, class Epi>
+__device__ __forceinline__ void flat_bases_epi(uint32_t* tab, int D, uint32_t* tmp, Epi epi) {
   const int n = D * WHN;
   const int Tn = blockDim.x, t = threadIdx.x, lane = t & 31, w = t >> 5, nw = (Tn + 31) >> 5;
-  const int per = (n + Tn - 1) / Tn;
+  const int per = ((n + Tn - 1) / Tn) | 1;  // odd chunk length: the 32 lanes start in 32 distinct banks
   const int lo = min(n, t * per), hi = min(n, lo + per);
   uint32_t s = 0;
   for (int i = lo; i < hi; ++i) {
@@ -273,18 +273,22 @@ __device__ __forceinline__ void flat_bases_pk(uint32_t* tab, int D, const uint32
     run += l + (v >> 16);
   }
   __syncthreads();
-  for (int d = threadIdx.x; d < D; d += blockDim.x) {
-    const uint32_t b = tab[d * WHN] & 0xffffu;
-    if (dtot) dtot[d] = (tab[d * WHN + WHN - 1] & 0xffffu) - b;
-    if (gcur) delta[d] = gcur[d] - b;
-  }
+  for (int d = threadIdx.x; d < D; d += blockDim.x) epi(d, tab[d * WHN] & 0xffffu, tab[d * WHN + WHN - 1] & 0xffffu);
   __syncthreads();
+}
+template <int WHN>
+__device__ __forceinline__ void flat_bases_pk(uint32_t* tab, int D, const uint32_t* gcur, uint32_t* dtot,
+                                              uint32_t* delta, uint32_t* tmp) {
+  flat_bases_epi<WHN>(tab, D, tmp, [&](int d, uint32_t b, uint32_t e) {
+    if (dtot) dtot[d] = e - b;
+    if (gcur) delta[d] = gcur[d] - b;
+  });
 }
 
 // In-place exclusive scan of a[0..n) (thread-contiguous chunks, one block scan).
 __device__ __forceinline__ void flat_excl_scan(uint32_t* a, int n, uint32_t* tmp /* >= 33 */) {
   const int Tn = blockDim.x, t = threadIdx.x, lane = t & 31, w = t >> 5, nw = (Tn + 31) >> 5;
-  const int per = (n + Tn - 1) / Tn;
+  const int per = ((n + Tn - 1) / Tn) | 1;  // odd chunk length: the 32 lanes start in 32 distinct banks
   const int lo = min(n, t * per), hi = min(n, lo + per);
   uint32_t s = 0;
   for (int i = lo; i < hi; ++i) s += a[i];
@@ -472,9 +476,9 @@ __device__ __forceinline__ void bases_delta(uint32_t* cnt, int D, const uint32_t
 // Write-out of a staged tile: slot i holds payload buf[i] of digit tag[i],
 // global index delta[tag] + i.  Consecutive lanes take consecutive slots, so a
 // warp store covers a few digit runs (coalesced sectors).
-template <int NT, int TILE>
+template <int NT, int TILE, class G>
 __device__ __forceinline__ void writeout_tag(uint32_t* __restrict__ out, const uint32_t* buf, const uint16_t* tag,
-                                             const uint32_t* delta, uint32_t n) {
+                                             const G* delta, uint32_t n) {
   if (n == (uint32_t)TILE) {
 #pragma unroll
     for (int k = 0; k < TILE / NT; ++k) {
@@ -494,8 +498,12 @@ __device__ __forceinline__ void writeout_tag(uint32_t* __restrict__ out, const u
 // at or before the lane, else the carry from the previous slot); stable rank
 // by the coarse digit; stage payload + global index by digit; vectorised
 // write-out of the runs.  Requires E < 2^32 (u32 indices).
-template <int kMode, int KK = K>
-__global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p1(const P1Args a) {
+// kW64 (graphs with E >= 2^32): 64-bit R1 positions.  The per-digit cursor
+// array holds the cursor between tiles and the index delta during a tile
+// (delta = cursor - tile start, restored from the digit end after the tile),
+// so the shared-memory footprint matches the 32-bit form.
+template <int kMode, int KK = K, bool kW64 = false>
+__global__ void __launch_bounds__(T, (KK > 16 || kW64 ? 2 : 4)) k_p1(const P1Args a) {
   // place tiles of PT = W * KK * 32 edges; the offsets window doubles as the
   // tag array, so it holds max(1024, PT / 4) entries
   constexpr int K = KK, PT = W * KK * 32, PTP = PT + 8, kWin = (PT / 4 > 1024) ? PT / 4 : 1024;
@@ -517,6 +525,9 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p1(const P1Args a) {
   uint32_t* s_bh = reinterpret_cast<uint32_t*>(s_mark);                        // D (aliases the marks, dead after ranking)
   uint32_t* s_tmp = s_dtot + D;                                                // 40
   uint32_t* s_psrc = s_tmp + 40;                                               // CT1/PT + 2
+  // kW64: s_g64 (D u64) spans s_gcur + s_delta (8-byte aligned: every region
+  // before it is a multiple of 8 bytes), s_dtot holds the digit's tile end
+  uint64_t* s_g64 = reinterpret_cast<uint64_t*>(s_gcur);
   __shared__ __align__(8) uint64_t s_bar;
   __shared__ uint64_t s_wlo;
   __shared__ uint32_t s_wn;
@@ -528,7 +539,10 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p1(const P1Args a) {
   const uint64_t tb = k * CT1, te = umin64(a.E, tb + CT1);
   const int nplace = (int)((te - tb + PT - 1) / PT);
   const uint64_t gp0 = tb / PT;
-  for (int d = tid; d < D; d += T) s_gcur[d] = (uint32_t)a.tbase[(uint64_t)d * a.ntiles + k];
+  for (int d = tid; d < D; d += T) {
+    if constexpr (kW64) s_g64[d] = a.tbase[(uint64_t)d * a.ntiles + k];
+    else s_gcur[d] = (uint32_t)a.tbase[(uint64_t)d * a.ntiles + k];
+  }
   for (int j = tid; j <= nplace; j += T) s_psrc[j] = a.psrc[gp0 + j];
   zero_u32(s_cnt, round4(D * WH) + (kMode == kRankSafe ? round4(D * WP) : 0));
   zero_u32(reinterpret_cast<uint32_t*>(s_mark), PT / 2);
@@ -573,6 +587,10 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p1(const P1Args a) {
   uint32_t ph = 0;
   if (tid == 0 && nplace > 0) issue(0);
   for (int j = 0; j < nplace; ++j) {
+    if constexpr (kW64) {  // delta -> cursor of the next tile (after barrier (D): the write-out is done)
+      if (j > 0)
+        for (int d = tid; d < D; d += T) s_g64[d] += s_dtot[d];
+    }
     const uint64_t pt = tb + (uint64_t)j * PT;
     const uint32_t n = (uint32_t)umin64(PT, te - pt);
     const uint32_t* gp = a.edges + pt;
@@ -639,7 +657,13 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p1(const P1Args a) {
       for (int s = 0; s < K; ++s) slot(s, iw + s * 32 + lane < n);
     }
     __syncthreads();  // (B) ranks done; landing buffer and marks consumed
-    flat_bases_pk<WH>(s_cnt, D, s_gcur, s_dtot, s_delta, s_tmp);
+    if constexpr (kW64)
+      flat_bases_epi<WH>(s_cnt, D, s_tmp, [&](int d, uint32_t b, uint32_t e) {
+        s_g64[d] -= b;
+        s_dtot[d] = e;
+      });
+    else
+      flat_bases_pk<WH>(s_cnt, D, s_gcur, s_dtot, s_delta, s_tmp);
     // source-high boundaries inside this tile (compact R1 decode table)
     const uint32_t h_last = s_last_src >> a.L;
     for (uint32_t h = (h_prev == 0xffffffffu) ? 0u : h_prev + 1; h <= h_last; ++h) {
@@ -652,7 +676,10 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p1(const P1Args a) {
         if (i < n && i < q) smem_inc(&s_bh[pk[s] >> 16]);
       }
       __syncthreads();
-      for (int d = tid; d < D; d += T) a.seg_hi[(uint64_t)d * (a.nh + 1) + h] = (uint64_t)s_gcur[d] + s_bh[d];
+      for (int d = tid; d < D; d += T) {
+        const uint64_t g0 = kW64 ? s_g64[d] + (s_cnt[d * WH] & 0xffffu) : (uint64_t)s_gcur[d];
+        a.seg_hi[(uint64_t)d * (a.nh + 1) + h] = g0 + s_bh[d];
+      }
       __syncthreads();
     }
     h_prev = h_last;
@@ -667,10 +694,12 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p1(const P1Args a) {
       }
     }
     __syncthreads();  // (C)
-    writeout_tag<T, PT>(a.out, s_buf, s_tag, s_delta, n);
+    if constexpr (kW64) writeout_tag<T, PT>(a.out, s_buf, s_tag, s_g64, n);
+    else writeout_tag<T, PT>(a.out, s_buf, s_tag, s_delta, n);
     zero_u32(reinterpret_cast<uint32_t*>(s_mark), PT / 2);
     zero_u32(s_cnt, round4(D * WH));
-    for (int d = tid; d < D; d += T) s_gcur[d] += s_dtot[d];
+    if constexpr (!kW64)
+      for (int d = tid; d < D; d += T) s_gcur[d] += s_dtot[d];
     fence_proxy_async_smem();
     __syncthreads();  // (D)
     if (tid == 0 && j + 1 < nplace) issue(j + 1);
@@ -705,6 +734,40 @@ __global__ void __launch_bounds__(512) k_cnt_rec(const uint32_t* __restrict__ re
       smem_inc(&s_h[dig(v.w)]);
     }
     for (uint32_t i = head + n4 * 4 + threadIdx.x; i < n; i += blockDim.x) smem_inc(&s_h[dig(p[i])]);
+    __syncthreads();
+    const uint64_t row0 = (uint64_t)(g - t.j) * D + t.j;
+    for (int d = threadIdx.x; d < D; d += blockDim.x) cnt[row0 + (uint64_t)d * t.nt] = s_h[d];
+    __syncthreads();
+  }
+}
+
+// Count over digit bytes (level-3 big buckets of wide graphs): same tables as k_cnt_rec.
+__global__ void __launch_bounds__(512) k_cnt_lv(const uint8_t* __restrict__ lv, const RTile* __restrict__ tiles,
+                                                const uint32_t* __restrict__ n_tiles, int D,
+                                                uint32_t* __restrict__ cnt) {
+  extern __shared__ __align__(16) uint32_t s_h[];
+  const uint32_t nt_all = *n_tiles;
+  for (uint32_t g = blockIdx.x; g < nt_all; g += gridDim.x) {
+    const RTile t = tiles[g];
+    for (int d = threadIdx.x; d < D; d += blockDim.x) s_h[d] = 0;
+    __syncthreads();
+    const uint8_t* p = lv + t.start;
+    const uint32_t n = t.n;
+    const uint32_t head = min(n, (uint32_t)((16 - (reinterpret_cast<uintptr_t>(p) & 15)) & 15));
+    for (uint32_t i = threadIdx.x; i < head; i += blockDim.x) smem_inc(&s_h[p[i]]);
+    const uint4* p4 = reinterpret_cast<const uint4*>(p + head);
+    const uint32_t n16 = (n - head) >> 4;
+    for (uint32_t q = threadIdx.x; q < n16; q += blockDim.x) {
+      uint4 v;
+      asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p4 + q));
+      const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int bb = 0; bb < 32; bb += 8) smem_inc(&s_h[(wd[k] >> bb) & 0xffu]);
+    }
+    for (uint32_t i = head + n16 * 16 + threadIdx.x; i < n; i += blockDim.x) smem_inc(&s_h[p[i]]);
     __syncthreads();
     const uint64_t row0 = (uint64_t)(g - t.j) * D + t.j;
     for (int d = threadIdx.x; d < D; d += blockDim.x) cnt[row0 + (uint64_t)d * t.nt] = s_h[d];
@@ -827,10 +890,18 @@ struct DecR2 {
   __device__ __forceinline__ uint32_t payload(uint32_t r, uint32_t) const { return r & src_mask; }
 };
 
-inline size_t smem_p2(int D, int mode, int KK = K) {
+// k_p2 record I/O forms.  Wide graphs (E >= 2^32 or 29+-bit sources) keep R2
+// as two arrays at CSC positions: the source (u32) and the low digit (u8).
+constexpr int kIoPlain = 0;  // u32 records in, u32 out (absolute u32 positions)
+constexpr int kIoSplit = 1;  // level 2 of wide graphs: R1 in; source + low-digit byte out
+constexpr int kIoLv = 2;     // level 3 big buckets of wide graphs: source + digit byte in, source out
+// Wide forms use 64-bit output positions: the per-digit cursor array holds the
+// cursor between place tiles and the index delta during one (as in k_p1 kW64).
+
+inline size_t smem_p2(int D, int mode, int KK = K, int io = kIoPlain) {
   const size_t pt = (size_t)W * KK * 32;
   return (pt + 8) * 4 + pt * 2 + ((size_t)round4(D * WH) + (mode == kRankSafe ? (size_t)round4(D * WP) : 0)) * 4 + (size_t)D * 4 * 4 +
-         40 * 4 + (size_t)kMaxBnd * 4;
+         40 * 4 + (size_t)kMaxBnd * 4 + (io != kIoPlain ? pt + 16 : 0);
 }
 
 // Owner search over a u32 boundary list (positions relative to the tile):
@@ -856,11 +927,13 @@ __device__ __forceinline__ uint32_t slot_owner32(uint32_t& cur, uint32_t& nb, ui
 
 // Place: per tile, place tiles of PT records are ranked by digit, staged with
 // their global indices, and written out (persistent, grid-stride over tiles).
-template <int kMode, class Dec, int KK, bool kProf = false>
+template <int kMode, class Dec, int KK, bool kProf = false, int kIO = kIoPlain>
 __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __restrict__ rec, const RTile* __restrict__ tiles,
                                              const uint32_t* __restrict__ n_tiles, int D, Dec dec,
                                              const uint64_t* __restrict__ base, uint32_t* __restrict__ out,
-                                             unsigned long long* __restrict__ prof = nullptr) {
+                                             unsigned long long* __restrict__ prof = nullptr,
+                                             const uint8_t* __restrict__ lv_in = nullptr,
+                                             uint8_t* __restrict__ lv_out = nullptr) {
   // phase profile (kProf builds only; thread 0, clock64): 0 tile setup, 1 wait,
   // 2 rank, 3 bases, 4 stage, 5 write
   unsigned long long pacc[kProf ? 6 : 1] = {};
@@ -886,6 +959,10 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __r
   uint32_t* s_dtot = s_dstart + D;                                             // D
   uint32_t* s_tmp = s_dtot + D;                                                // 40
   uint32_t* s_bnd = s_tmp + 40;                                                // kMaxBnd
+  constexpr bool kW64 = (kIO != kIoPlain);
+  uint64_t* s_g64 = reinterpret_cast<uint64_t*>(s_gcur);  // kW64: spans s_gcur + s_delta; s_dtot = digit end
+  // kIoSplit: low-digit byte of each staged slot; kIoLv: landing of the digit bytes (16B aligned)
+  uint8_t* s_lvx = reinterpret_cast<uint8_t*>(s_bnd + kMaxBnd);                // PT + 16
   __shared__ __align__(8) uint64_t s_bar;
 
   const uint32_t tid = threadIdx.x, lane = lane_id(), w = warp_id();
@@ -902,7 +979,10 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __r
   for (uint32_t g = blockIdx.x; g < ntall; g += gridDim.x) {
     const RTile t = tiles[g];
     const uint64_t row0 = (uint64_t)(g - t.j) * D + t.j;
-    for (int d = tid; d < D; d += T) s_gcur[d] = (uint32_t)base[row0 + (uint64_t)d * t.nt];
+    for (int d = tid; d < D; d += T) {
+      if constexpr (kW64) s_g64[d] = base[row0 + (uint64_t)d * t.nt];
+      else s_gcur[d] = (uint32_t)base[row0 + (uint64_t)d * t.nt];
+    }
     const uint32_t nbt = Dec::kSrcHigh ? t.nbnd : 0u;
     const uint64_t* hrow = nullptr;
     if constexpr (Dec::kSrcHigh) {
@@ -918,7 +998,15 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __r
       const uint32_t o = align_items_u32(gp);
       const uint32_t full = (o + n) & ~3u;
       fence_proxy_async_smem();
-      mbar_arrive_expect_tx(&s_bar, full * 4);
+      if constexpr (kIO == kIoLv) {  // the digit bytes: whole 16-byte blocks (the array is padded)
+        const uint8_t* gl = lv_in + pt;
+        const uint32_t o8 = (uint32_t)(reinterpret_cast<uintptr_t>(gl) & 15);
+        const uint32_t nb8 = (o8 + n + 15) & ~15u;
+        mbar_arrive_expect_tx(&s_bar, full * 4 + nb8);
+        bulk_g2s(s_lvx, gl - o8, nb8, &s_bar);
+      } else {
+        mbar_arrive_expect_tx(&s_bar, full * 4);
+      }
       if (full) bulk_g2s(s_buf, gp - o, full * 4, &s_bar);
       if (jj + 1 < nplace) {
         const uint32_t* gn = gp + PT;
@@ -931,6 +1019,10 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __r
     __syncthreads();  // s_gcur / s_bnd visible; the previous tile's buffers are free
     if (tid == 0 && nplace > 0) issue(0);
     for (int jj = 0; jj < nplace; ++jj) {
+      if constexpr (kW64) {  // delta -> cursor of this place tile (after barrier (D))
+        if (jj > 0)
+          for (int d = tid; d < D; d += T) s_g64[d] += s_dtot[d];
+      }
       const uint64_t pt = t.start + (uint64_t)jj * PT;
       const uint32_t n = min((uint32_t)PT, t.n - jj * PT);
       const uint32_t* gp = rec + pt;
@@ -961,18 +1053,28 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __r
       }
       // warps whose 512 items hold no source-high boundary keep h constant
       const bool wbnd = nb <= rel0 + iw + (K * 32 - 1);
+      const uint32_t o8 = (kIO == kIoLv) ? (uint32_t)(reinterpret_cast<uintptr_t>(lv_in + pt) & 15) : 0u;
+      // pk = digit << 16 | rank; kIoSplit: low-digit byte << 24 | digit << 13 | rank (rank < 8192, digit < 2048)
+      constexpr int kDS = (kIO == kIoSplit) ? 13 : 16;
       uint32_t pay[K], pk[K];
       auto slot = [&](int s, bool valid) {
         const uint32_t i0 = iw + s * 32, i = i0 + lane;
         const uint32_t r = valid ? s_buf[o + i] : 0u;
         uint32_t h = t.h0;
         if constexpr (Dec::kSrcHigh) h += wbnd ? slot_owner32(cur, nb, rel0 + i0, nbt, bnd_at) : cur;
-        const uint32_t d = dec.digit(r);
+        uint32_t d;
+        if constexpr (kIO == kIoLv) d = valid ? (uint32_t)s_lvx[o8 + i] : 0u;
+        else d = dec.digit(r);
         uint32_t rk;
         if constexpr (Dec::kMatchRank) rk = rank_match(s_cnt + d * WH + (w >> 1), sh, d, valid);
         else rk = rank_pk<kMode>(s_cnt + d * WH + (w >> 1), s_scr + d * WP + w, sh, valid);
-        pk[s] = (d << 16) | rk;
-        pay[s] = dec.payload(r, h);
+        if constexpr (kIO == kIoSplit) {
+          pk[s] = (((r >> dec.L) & dec.lvmask) << 24) | (d << 13) | rk;
+          pay[s] = (h << dec.L) | (r & dec.src_mask);
+        } else {
+          pk[s] = (d << 16) | rk;
+          pay[s] = dec.payload(r, h);
+        }
       };
       if (n == (uint32_t)PT) {
 #pragma unroll
@@ -983,22 +1085,44 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __r
       }
       __syncthreads();  // (B)
       tick(2);
-      flat_bases_pk<WH>(s_cnt, D, s_gcur, s_dtot, s_delta, s_tmp);
+      if constexpr (kW64)
+        flat_bases_epi<WH>(s_cnt, D, s_tmp, [&](int d, uint32_t b, uint32_t e) {
+          s_g64[d] -= b;
+          s_dtot[d] = e;
+        });
+      else
+        flat_bases_pk<WH>(s_cnt, D, s_gcur, s_dtot, s_delta, s_tmp);
       tick(3);
 #pragma unroll
       for (int s = 0; s < K; ++s) {
         if (n == (uint32_t)PT || iw + s * 32 + lane < n) {
-          const uint32_t d = pk[s] >> 16;
-          const uint32_t pos = ((s_cnt[d * WH + (w >> 1)] >> sh) & 0xffffu) + (pk[s] & 0xffffu);
+          const uint32_t d = (pk[s] >> kDS) & ((kIO == kIoSplit) ? 0x7ffu : 0xffffu);
+          const uint32_t pos = ((s_cnt[d * WH + (w >> 1)] >> sh) & 0xffffu) + (pk[s] & ((1u << kDS) - 1));
           s_buf[pos] = pay[s];
           s_tag[pos] = (uint16_t)d;
+          if constexpr (kIO == kIoSplit) s_lvx[pos] = (uint8_t)(pk[s] >> 24);
         }
       }
       __syncthreads();  // (C)
       tick(4);
-      writeout_tag<T, PT>(out, s_buf, s_tag, s_delta, n);
+      if constexpr (kIO == kIoPlain) {
+        writeout_tag<T, PT>(out, s_buf, s_tag, s_delta, n);
+      } else {  // 64-bit positions
+        auto put = [&](uint32_t i) {
+          const uint64_t q = s_g64[s_tag[i]] + i;
+          out[q] = s_buf[i];
+          if constexpr (kIO == kIoSplit) lv_out[q] = s_lvx[i];
+        };
+        if (n == (uint32_t)PT) {
+#pragma unroll
+          for (int q = 0; q < PT / T; ++q) put(threadIdx.x + q * T);
+        } else {
+          for (uint32_t i = threadIdx.x; i < n; i += T) put(i);
+        }
+      }
       zero_u32(s_cnt, round4(D * WH));
-      for (int d = tid; d < D; d += T) s_gcur[d] += s_dtot[d];
+      if constexpr (!kW64)
+        for (int d = tid; d < D; d += T) s_gcur[d] += s_dtot[d];
       fence_proxy_async_smem();
       __syncthreads();  // (D)
       tick(5);
@@ -1026,16 +1150,19 @@ struct P3Args {
   uint64_t V;
   uint64_t* t_offsets;
   uint32_t* t_edges;
+  const uint8_t* lv;  // kLv: low digit of every R2 record (wide graphs; rec then holds the bare source)
 };
 
-inline size_t smem_p3(int mode) {
+constexpr int CAP3L = CAP3 + 16;  // digit-byte landing per buffer (whole 16-byte blocks)
+inline size_t smem_p3(int mode, bool lv = false) {
   return (size_t)2 * CAP3P * 4 + ((size_t)round4(ML3 * WH3) + (mode == kRankSafe ? (size_t)round4(ML3 * W3P) : 0)) * 4 +
-         (size_t)ML3 * 8 + 40 * 4;
+         (size_t)ML3 * 8 + 40 * 4 + (lv ? (size_t)2 * CAP3L : 0);
 }
 
 // kPosFine: the record's fine bucket inside the unit comes from its position
 // (R2 has no room for fine-digit bits); else from the record's bits.
-template <int kMode, bool kPosFine, bool kProf = false>
+// kLv (requires kPosFine): the low digit comes from the separate byte array.
+template <int kMode, bool kPosFine, bool kProf = false, bool kLv = false>
 __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
   // phase profile (kProf builds only; thread 0, clock64): 0 fetch/issue, 1 wait, 2 rank, 3 bases+offsets, 4 stage, 5 store
   unsigned long long pacc[kProf ? 6 : 1] = {};
@@ -1057,6 +1184,8 @@ __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
   uint32_t* s_dstart = s_scr + (kMode == kRankSafe ? round4(ML3 * W3P) : 0);
   uint32_t* s_dtot = s_dstart + ML3;
   uint32_t* s_tmp = s_dtot + ML3;
+  uint8_t* s_lvb = reinterpret_cast<uint8_t*>(s_tmp + 40);  // kLv: 2 * CAP3L (16B aligned)
+  static_assert(!kLv || kPosFine, "digit bytes imply position-derived fine buckets");
   __shared__ __align__(8) uint64_t s_bar[2];
   __shared__ uint32_t s_uidx[2];
   __shared__ uint32_t s_fb[ML3];  // fine-bucket boundaries of the unit (relative positions)
@@ -1076,7 +1205,15 @@ __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
     const uint32_t o = align_items_u32(gp);
     const uint32_t full = (o + u.n) & ~3u;
     fence_proxy_async_smem();
-    mbar_arrive_expect_tx(&s_bar[b], full * 4);
+    if constexpr (kLv) {
+      const uint8_t* gl = a.lv + u.start;
+      const uint32_t o8 = (uint32_t)(reinterpret_cast<uintptr_t>(gl) & 15);
+      const uint32_t nb8 = (o8 + u.n + 15) & ~15u;
+      mbar_arrive_expect_tx(&s_bar[b], full * 4 + nb8);
+      bulk_g2s(s_lvb + b * CAP3L, gl - o8, nb8, &s_bar[b]);
+    } else {
+      mbar_arrive_expect_tx(&s_bar[b], full * 4);
+    }
     if (full) bulk_g2s(s_buf + b * CAP3P, gp - o, full * 4, &s_bar[b]);
   };
   // static round-robin over the units (they are many and bounded in size):
@@ -1123,6 +1260,7 @@ __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
     }
     const bool wbnd = fnb <= seg0 + (K3 * 32 - 1);
     const uint32_t lvoff = (u.f0 & ((1u << a.gbits) - 1)) << a.c;
+    const uint8_t* lvb = s_lvb + b * CAP3L + (kLv ? (uint32_t)(reinterpret_cast<uintptr_t>(a.lv + u.start) & 15) : 0u);
     uint32_t rr[K3], pk[K3];
 #pragma unroll
     for (int s = 0; s < K3; ++s) {
@@ -1132,7 +1270,8 @@ __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
       uint32_t lv;
       if constexpr (kPosFine) {
         const uint32_t j = wbnd ? slot_owner32(fcur, fnb, seg0 + s * 32, nbt, bnd_at) : fcur;
-        lv = valid ? ((j << a.c) | ((r >> a.nbs) & a.mask_c)) : 0u;
+        if constexpr (kLv) lv = valid ? ((j << a.c) | lvb[i]) : 0u;
+        else lv = valid ? ((j << a.c) | ((r >> a.nbs) & a.mask_c)) : 0u;
       } else {
         lv = valid ? (((r >> a.nbs) & a.lvmask) - lvoff) : 0u;
       }

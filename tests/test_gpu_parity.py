@@ -320,6 +320,46 @@ def test_alternate_pipelines(path_env, monkeypatch, golden_cases):
     assert np.array_equal(t_edg.cpu().numpy().view(np.uint32), e)
 
 
+def test_wide_pipeline(monkeypatch, golden_cases, rank_mode):
+    """The wide v3 form (64-bit positions, R2 = source array + low-digit bytes;
+    taken by graphs with E >= 2^32 or 29-bit IDs such as C5), forced on small
+    graphs: goldens, random graphs, hub graphs (big-bucket path), skewed medium
+    graphs, and a 2^29-vertex graph with the C5 digit split (11|10|8, 15
+    source-high bits per coarse bucket)."""
+    from paper_2501_06872_b200 import CsrGraph, transpose_gpu
+
+    monkeypatch.setenv("GT_WIDE", "1")
+    for name, c in golden_cases.items():
+        out = transpose_gpu(_graph(c["nv"], c["off"], c["edg"]))
+        assert np.array_equal(out.graph.offsets, c["toff"]), name
+        assert np.array_equal(out.graph.edges, c["tedg"]), name
+    rng = np.random.default_rng(515 + rank_mode)
+    for i in range(30):
+        g = random_graph(rng, max_vertices=3000, max_edges=40_000)
+        out = transpose_gpu(g)
+        toff, tedg = oracle.transpose_c(g.offsets, g.edges, g.num_vertices)
+        assert np.array_equal(out.graph.offsets, toff) and np.array_equal(out.graph.edges, tedg), i
+    cases = []
+    for nv, ne, skew in ((1 << 16, 1 << 22, 3.0), (1 << 21, 1 << 24, 6.0), (1_000_003, 1 << 23, 1.0)):
+        src = rng.integers(0, nv, ne)
+        dst = np.minimum((nv * rng.random(ne) ** skew).astype(np.int64), nv - 1)
+        cases.append((nv, src, rng.permutation(nv)[dst]))
+    src = np.sort(rng.integers(0, 50, 2_000_000))
+    cases.append((50, src, np.full(src.size, 17)))  # every edge to one vertex
+    nv = 1 << 29  # C5's ID width and digit split at 2^25 edges
+    src = rng.integers(0, nv, 1 << 25)
+    dst = np.minimum((nv * rng.random(1 << 25) ** 2.0).astype(np.int64), nv - 1)
+    cases.append((nv, src, (dst * 2654435761) % nv))  # odd multiplier: a bijection of [0, 2^29)
+    for nv, s, d in cases:
+        g = CsrGraph.from_edge_pairs(s, d, nv)
+        out = transpose_gpu(g)
+        toff, tedg = oracle.transpose_c(g.offsets, g.edges, nv)
+        assert np.array_equal(out.graph.offsets, toff), nv
+        assert np.array_equal(out.graph.edges, tedg), nv
+        if nv == 1 << 29:
+            assert tuple(out.details["digit_bits"]) == (11, 10, 8)
+
+
 def test_rmat_lean_generator_matches_pairs_path():
     """gt_gen_rmat_csr + two transposes (the C5 generation path) gives the same
     CSR as the pair generator + CSR build (and as the numpy generator)."""
