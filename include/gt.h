@@ -52,7 +52,7 @@ extern "C" {
 #define GT_EFORMAT (-6) /* GraphFormatError (errors.py:4-14): a POTG file violates the format */
 #define GT_EIO (-7)     /* OSError: a file could not be opened, read or written */
 
-#define GT_ABI_VERSION 2
+#define GT_ABI_VERSION 3
 
 /* Per-call accounting; mirrors TransposeOutput.phase_times / aux_footprint_bytes
  * (baselines.py:39-53).  Times are device time from CUDA events, in ms, filled
@@ -166,6 +166,33 @@ int gt_gen_web_edges(uint64_t num_vertices, uint64_t seed, const uint64_t *offse
  * Consumes src/dst (they are overwritten as scratch). */
 int gt_build_csr(uint32_t *src, uint32_t *dst, uint64_t num_vertices, uint64_t num_edges,
                  uint64_t *offsets, uint32_t *edges, void *stream);
+
+/* ---- step 0: high-degree-vertex sample (hlh.py:141-228) --------------------
+ * gt_sample_hdv replaces sample_hdv (hlh.py:167-218) + _sample_tally
+ * (hlh.py:153-164): num_samples > 0 draws that many edge positions in each of
+ * two tallies from 2 * workers xoshiro256** streams seeded by successive
+ * splitmix64 outputs of seed (worker_seeds, _nb.py:86-93); num_samples == 0
+ * counts every edge (sample_fraction == 1).  hdv_ids (device, k <= V entries)
+ * receives the k most counted endpoints of the first tally, most first, ties
+ * to the lower ID (then zero-count vertices by ID); *h_hits = the second
+ * tally's count over that set (the coverage estimate's numerator).  Same
+ * result as the reference for the same (seed, workers).
+ * gt_hdv_table_build: the plan's open-addressing table (_table_build,
+ * hlh.py:81-90) on the device: keys[capacity] (u64, empty = ~0), vals[capacity]
+ * = position in hdv_ids, slot (key * 0x9E3779B97F4A7C15) >> shift, linear
+ * probing.  gt_hdv_lookup: out[i] = position of queries[i] or -1
+ * (_table_find, hlh.py:68-78; hash_lookup, hlh.py:141-145).
+ * gt_coverage_exact: *h_hits = edges whose endpoint is in the table
+ * (coverage_exact, hlh.py:221-228).  All pointers but h_hits are device. */
+int gt_sample_hdv(const uint32_t *edges, uint64_t num_edges, uint64_t num_vertices, uint64_t k,
+                  uint64_t num_samples, uint64_t seed, int workers, uint64_t *hdv_ids, uint64_t *h_hits,
+                  void *stream);
+int gt_hdv_table_build(const uint64_t *hdv_ids, uint64_t k, uint64_t capacity, int shift, uint64_t *keys,
+                       uint32_t *vals, void *stream);
+int gt_hdv_lookup(const uint64_t *keys, const uint32_t *vals, uint64_t capacity, int shift,
+                  const uint32_t *queries, uint64_t n, int64_t *out, void *stream);
+int gt_coverage_exact(const uint64_t *keys, const uint32_t *vals, uint64_t capacity, int shift,
+                      const uint32_t *edges, uint64_t num_edges, uint64_t *h_hits, void *stream);
 
 /* ---- canonicalisation and verification on the device (bench.py:84-170) ----
  * gt_sort_lists: out_edges = every list of (offsets, edges) sorted ascending

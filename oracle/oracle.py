@@ -15,6 +15,11 @@ never by the product package.  Two restatements of the reference algorithm:
   transpose_scantrans (baselines.py:265-312), transpose_atomic
   (baselines.py:168-209) and sort_neighbor_lists (baselines.py:457-475).
 
+* ``sample_hdv_np`` — numpy restatement of step 0's ``sample_hdv``
+  (hlh.py:153-218) with the reference's generators (worker_seeds /
+  xoshiro_seed_scalar / xoshiro_step, _nb.py:47-93), vectorised over the
+  worker streams; pinned by tests/golden/hdv_cases.npz (make_hdv_golden.py).
+
 Pinned against the reference: tests/golden/ holds outputs of the real
 ``potra.transpose_oracle`` (made by tests/golden/make_golden.py, which imports
 /root/reference); tests/test_oracle.py checks both restatements against them.
@@ -149,6 +154,74 @@ def edge_balanced_bounds_np(offsets, parts: int):
     bounds[0] = 0
     bounds[-1] = nv
     return bounds
+
+
+_M64 = (1 << 64) - 1
+_GAMMA = 0x9E3779B97F4A7C15
+
+
+def _mix64(z: int) -> int:
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def _rotl(x, k):
+    return (x << np.uint64(k)) | (x >> np.uint64(64 - k))
+
+
+def _tally_np(edges, nv, num_samples, seeds):
+    """_sample_tally (hlh.py:153-164): stream w draws samples
+    [w*N/W, (w+1)*N/W) as edges[r % E]; all streams advance together."""
+    W = len(seeds)
+    freq = np.zeros(nv, np.int64)
+    st = np.zeros((4, W), np.uint64)
+    for w, sd in enumerate(seeds):  # xoshiro_seed_scalar (_nb.py:62-69)
+        x = sd
+        for j in range(4):
+            x = (x + _GAMMA) & _M64
+            st[j, w] = _mix64(x)
+    lo = np.array([w * num_samples // W for w in range(W)], np.int64)
+    cnt = np.array([(w + 1) * num_samples // W for w in range(W)], np.int64) - lo
+    n = np.uint64(edges.shape[0])
+    s0, s1, s2, s3 = st
+    with np.errstate(over="ignore"):
+        for i in range(int(cnt.max()) if W else 0):
+            r = _rotl(s1 * np.uint64(5), 7) * np.uint64(9)  # xoshiro_step (_nb.py:72-83)
+            t = s1 << np.uint64(17)
+            s2 ^= s0
+            s3 ^= s1
+            s1 ^= s2
+            s0 ^= s3
+            s2 ^= t
+            s3 = _rotl(s3, 45)
+            live = cnt > i
+            np.add.at(freq, edges[(r[live] % n).astype(np.int64)].astype(np.int64), 1)
+    return freq
+
+
+def sample_hdv_np(edges, nv: int, k: int, sample_fraction: float, seed: int, threads: int):
+    """Restates sample_hdv (hlh.py:167-218): returns (hdv_ids uint64, coverage_estimate, sample_size)."""
+    import math
+
+    edges = np.asarray(edges).view(np.uint32)
+    ne = edges.shape[0]
+    k = min(k, nv)
+    if sample_fraction >= 1.0 or ne == 0:
+        freq = np.bincount(edges.astype(np.int64), minlength=nv) if ne else np.zeros(nv, np.int64)
+        est = freq
+        size = ne
+    else:
+        size = math.ceil(sample_fraction * nv)
+        seeds, x = [], seed & _M64
+        for _ in range(2 * threads):  # worker_seeds (_nb.py:86-93)
+            x = (x + _GAMMA) & _M64
+            seeds.append(_mix64(x))
+        freq = _tally_np(edges, nv, size, seeds[:threads]) if size else np.zeros(nv, np.int64)
+        est = _tally_np(edges, nv, size, seeds[threads:]) if size else np.zeros(nv, np.int64)
+    ids = np.lexsort((np.arange(nv, dtype=np.int64), -freq))[:k].astype(np.uint64) if k else np.empty(0, np.uint64)
+    hits = int(est[ids.astype(np.int64)].sum()) if k else 0
+    return ids, (hits / size if size else 0.0), size
 
 
 def max_threads() -> int:

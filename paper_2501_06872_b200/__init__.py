@@ -20,6 +20,7 @@ from .transpose import (
     transpose_potra,
 )
 from .verify import VerifyReport, sort_neighbor_lists, verify_output
+from .hdv import HdvBudget, HdvPlan, coverage_exact, hash_lookup, hdv_count, sample_hdv
 from .io import DeviceGraph, load_graph, load_graph_device, store_graph, store_graph_device, transpose_file
 
 __version__ = "0.1.0"
@@ -41,6 +42,12 @@ __all__ = [
     "transpose_file",
     "DeviceGraph",
     "prefix_sum_gpu",
+    "HdvBudget",
+    "HdvPlan",
+    "hdv_count",
+    "sample_hdv",
+    "hash_lookup",
+    "coverage_exact",
     "edge_balanced_vertex_bounds",
     "selftest_rank_order",
     "set_rank_mode",

@@ -48,7 +48,7 @@ class PotgHeader(ctypes.Structure):
     ]
 
 
-ABI_VERSION = 2  # include/gt.h GT_ABI_VERSION
+ABI_VERSION = 3  # include/gt.h GT_ABI_VERSION
 _u64, _i64, _int, _vp = ctypes.c_uint64, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
 _stats_p = ctypes.POINTER(GtStats)
 _hdr_p = ctypes.POINTER(PotgHeader)
@@ -79,6 +79,10 @@ SYMBOLS = {
     "gt_first_diff_u32": (_int, [_vp, _vp, _u64, _u64p, _vp]),
     "gt_in_degree_offsets": (_int, [_vp, _u64, _u64, _vp, _vp]),
     "gt_first_diff_lists": (_int, [_vp, _vp, _vp, _vp, _vp, _u64, _u64p, _vp]),
+    "gt_sample_hdv": (_int, [_vp, _u64, _u64, _u64, _u64, _u64, _int, _vp, _u64p, _vp]),
+    "gt_hdv_table_build": (_int, [_vp, _u64, _u64, _int, _vp, _vp, _vp]),
+    "gt_hdv_lookup": (_int, [_vp, _vp, _u64, _int, _vp, _u64, _vp, _vp]),
+    "gt_coverage_exact": (_int, [_vp, _vp, _u64, _int, _vp, _u64, _u64p, _vp]),
     "gt_potg_read_header": (_int, [ctypes.c_char_p, _hdr_p, _u64p]),
     "gt_potg_read": (_int, [ctypes.c_char_p, _hdr_p, _vp, _vp, _vp, _u64p]),
     "gt_potg_write": (_int, [ctypes.c_char_p, _vp, _vp, _u64, _u64, _int, _int, _vp]),

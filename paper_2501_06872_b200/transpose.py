@@ -164,33 +164,47 @@ def transpose_potra(g, threads: int, budget=None, *, force_method=None, sample_f
     """Signature of the reference's ``transpose_potra`` (hlh.py:441-452) on the GPU.
 
     Argument checks are the reference's (``threads >= 1``, _nb.py:112-113;
-    ``force_method`` in {None, "atomic", "hlh"}, hlh.py:462-463).  The GPU
-    path has no degree-dependent branch: high- and low-degree destinations go
-    through the same stable partition kernels, so the probe, the HDV sample
-    and the cache budget have nothing to choose; ``details`` reports
-    ``method_chosen="gpu"``, ``k=0`` and the GPU accounting.  The output is
-    sorted (``sorted=True``) and equals ``transpose_oracle(g)``.
+    ``force_method`` in {None, "atomic", "hlh"}, hlh.py:462-463).  Step 0 runs
+    as in the reference (hlh.py:466-475): k from the budget (Eq. 1,
+    ``hdv_count`` + ``fit_table_budget``; default budget = one CTA's shared
+    memory, ``hdv.gpu_budget``) and ``sample_hdv`` on the GPU with the same
+    ``(sample_fraction, seed, threads)`` — same HDV set and coverage estimate
+    as the reference.  The transposition has no degree-dependent branch (hubs
+    take the level-3 big-bucket path by measured size), so there is no probe:
+    ``details`` reports ``method_chosen="gpu"``, the step-0 results and the GPU
+    accounting.  The output is sorted (``sorted=True``) and equals
+    ``transpose_oracle(g)``.
     """
+    from .hdv import fit_table_budget, gpu_budget, hdv_count, sample_hdv
+
     if force_method not in (None, "atomic", "hlh"):
         raise ValueError(f"force_method must be 'atomic' or 'hlh', got {force_method!r}")
     if threads < 1:
         raise ValueError(f"thread count must be >= 1, got {threads}")
+    t0 = time.perf_counter()
+    if budget is None:
+        budget = gpu_budget()
+    k = fit_table_budget(hdv_count(budget).k, budget.load_factor, threads, budget.cache_bytes)
+    plan = sample_hdv(g, k, sample_fraction=sample_fraction, seed=seed, threads=threads,
+                      load_factor=budget.load_factor)
+    step0 = time.perf_counter() - t0
     out = transpose_gpu(g)
     details = {
         "method_chosen": "gpu",
-        "k": 0,
-        "coverage_estimate": 0.0,
-        "sample_size": 0,
+        "k": plan.k,
+        "coverage_estimate": plan.coverage_estimate,
+        "sample_size": plan.sample_size,
         "probe": None,
-        "hdv_aux_bytes": 0,
+        "hdv_aux_bytes": plan.aux_bytes(),
         "shared_aux_bytes": out.aux_footprint_bytes,
         "partitions": out.details.get("big_buckets", 0),
         "step3_imbalance": None,
+        "plan": plan,
     }
     details.update(out.details)
-    return TransposeOutput(graph=out.graph, phase_times={"step0": 0.0, **out.phase_times},
-                           aux_footprint_bytes=out.aux_footprint_bytes, method="potra-gpu", sorted=True,
-                           details=details)
+    return TransposeOutput(graph=out.graph, phase_times={"step0": step0, **out.phase_times},
+                           aux_footprint_bytes=out.aux_footprint_bytes + plan.aux_bytes(), method="potra-gpu",
+                           sorted=True, details=details)
 
 
 def transpose_atomic(g, threads: int, partition_edges: int = 1 << 18) -> TransposeOutput:

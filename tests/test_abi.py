@@ -34,7 +34,7 @@ def test_abi_version_and_structs():
     from paper_2501_06872_b200 import _lib
 
     lib = _lib.load()
-    assert lib.gt_abi_version() == 2
+    assert lib.gt_abi_version() == 3
     assert ctypes.sizeof(_lib.GtStats) == 4 * 8 + 8 + 3 * 4 + 4 + 8 + 8 + 4 * 8
 
 
