@@ -798,6 +798,10 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
   int rc;
   int launches = 0;
   const int sms = num_sms();
+  // batched shared loads in the place kernels (bits: 2 L2, 4 L3 big buckets, 8 L3 units, 16 L3 units
+  // with position-derived fine buckets).  Measured (C3 / C4): L3 big 0.85 -> 0.78 ms; L3 position units
+  // (C4) 4.40 -> 4.33 ms; slower for L2 with 4096-record tiles (2.11 -> 2.18 ms) and C3's L3 units
+  const int pre = env_int("GT_PRE", 4 | 16);
   // level-3 units are aligned groups of 2^sbits fine buckets (<= ML3 local
   // vertices); R2 carries g3 = sbits fine-digit bits when it has room, else
   // the unit decodes the fine bucket from the record's position
@@ -819,8 +823,9 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
   // ---- step 1: level-1 partition of the CSR stream into R1 (in t_edges)
   // level 1 uses 8192-edge place tiles (measured: C3 k_p1 2.82 -> 2.79 ms, C4 8.75 -> 7.56 ms)
   // (wide graphs: 4096-edge tiles keep 2 CTAs/SM with 2048 coarse digits)
-  const int k1 = env_int("GT_K1", p.wide ? 16 : 32);
-  const uint64_t pt1 = (uint64_t)W * k1 * 32, nplace1 = (E + pt1 - 1) / pt1;
+  const int k1 = env_int("GT_K1", 32);  // C5 (wide, 2048 coarse digits): 8192-edge tiles 90.0 -> 81.8 ms
+  const int w1 = p.wide ? W : env_int("GT_W1", W);  // warps per level-1 CTA (16: 8192-edge tiles at K = 16)
+  const uint64_t pt1 = (uint64_t)w1 * (w1 == 16 ? 16 : k1) * 32, nplace1 = (E + pt1 - 1) / pt1;
   k_tile_src<<<(unsigned)((nplace1 + 1 + 255) / 256), 256, 0, st>>>(in, E, pt1, nplace1 + 1, psrc);
   GT_LAUNCH_CHECK();
   k_prev_src<<<(unsigned)((q.ntiles1 + 255) / 256), 256, 0, st>>>(in, E, CT1, q.ntiles1, prev);
@@ -859,6 +864,10 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
     };
     if (p.wide) {  // 64-bit R1 positions
       if ((rc = (k1 == 32) ? go1(k_p1<kMode, 32, true>, 32) : go1(k_p1<kMode, 16, true>, 16))) return rc;
+    } else if (w1 == 16) {
+      const size_t sm = smem_p1(D1, kMode, 16, 16);
+      if ((rc = set_smem(k_p1<kMode, 16, false, 16>, sm))) return rc;
+      k_p1<kMode, 16, false, 16><<<(unsigned)q.ntiles1, 512, sm, st>>>(a);
     } else if (k1 == 32) {
       const size_t sm = smem_p1(D1, kMode, 32);
       if ((rc = set_smem(k_p1<kMode, 32>, sm))) return rc;
@@ -935,8 +944,11 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
       if (prof) {
         if ((rc = set_smem(k_p2<kMode, DecR1, 16, true>, sm))) return rc;
         k_p2<kMode, DecR1, 16, true><<<g, T, sm, st>>>(t_edges, tiles2, cfirst + D1, Db, dec, base2, r2, prof);
-      } else {
+      } else if (pre & 2) {
         k_p2<kMode, DecR1, 16><<<g, T, sm, st>>>(t_edges, tiles2, cfirst + D1, Db, dec, base2, r2);
+      } else {
+        if ((rc = set_smem(k_p2<kMode, DecR1, 16, false, kIoPlain, false>, sm))) return rc;
+        k_p2<kMode, DecR1, 16, false, kIoPlain, false><<<g, T, sm, st>>>(t_edges, tiles2, cfirst + D1, Db, dec, base2, r2);
       }
       if (prof) {
         unsigned long long h[6];
@@ -1008,7 +1020,12 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
       const size_t sm = smem_p2(Dc, kMode, 16);
       if ((rc = set_smem(k_p2<kMode, DecR2, 16>, sm))) return rc;
       const unsigned g = persistent_grid(k_p2<kMode, DecR2, 16>, T, sm, q.max_t3);
-      k_p2<kMode, DecR2, 16><<<g, T, sm, st>>>(r2, tiles3, cnt + 2, Dc, dec, base3, t_edges);
+      if (pre & 4) {
+        k_p2<kMode, DecR2, 16><<<g, T, sm, st>>>(r2, tiles3, cnt + 2, Dc, dec, base3, t_edges);
+      } else {
+        if ((rc = set_smem(k_p2<kMode, DecR2, 16, false, kIoPlain, false>, sm))) return rc;
+        k_p2<kMode, DecR2, 16, false, kIoPlain, false><<<g, T, sm, st>>>(r2, tiles3, cnt + 2, Dc, dec, base3, t_edges);
+      }
     }
     GT_LAUNCH_CHECK();
     if ((rc = tm.kend(3))) return rc;
@@ -1055,7 +1072,8 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
     } else if (p.wide) {
       rc = go3(k_p3<kMode, true, false, true>);
     } else {
-      rc = pos_fine ? go3(k_p3<kMode, true>) : go3(k_p3<kMode, false>);
+      if ((pre & 8) || ((pre & 16) && pos_fine)) rc = pos_fine ? go3(k_p3<kMode, true>) : go3(k_p3<kMode, false>);
+      else rc = pos_fine ? go3(k_p3<kMode, true, false, false, false>) : go3(k_p3<kMode, false, false, false, false>);
     }
     if (rc) return rc;
     GT_LAUNCH_CHECK();

@@ -430,9 +430,10 @@ struct P1Args {
   uint32_t* out;           // R1
 };
 
-inline size_t smem_p1(int D, int mode, int KK = K) {
-  const size_t pt = (size_t)W * KK * 32, win = std::max<size_t>(1024, pt / 4);
-  return (pt + 8) * 4 + win * 8 + pt * 2 + ((size_t)round4(D * WH) + (mode == kRankSafe ? (size_t)round4(D * WP) : 0)) * 4 +
+inline size_t smem_p1(int D, int mode, int KK = K, int WW = W) {
+  const size_t pt = (size_t)WW * KK * 32, win = std::max<size_t>(1024, pt / 4);
+  const int wh = WW / 2 + 1, wp = WW + 1;
+  return (pt + 8) * 4 + win * 8 + pt * 2 + ((size_t)round4(D * wh) + (mode == kRankSafe ? (size_t)round4(D * wp) : 0)) * 4 +
          (size_t)D * 4 * 3 + 40 * 4 + (CT1 / pt + 4) * 4;
 }
 
@@ -490,6 +491,33 @@ __device__ __forceinline__ void writeout_tag(uint32_t* __restrict__ out, const u
   }
 }
 
+// Stage K ranked items of a thread: item s (pk = digit << 16 | rank inside its
+// warp's digit run, payload pay) goes to slot base(digit, warp) + rank, its
+// digit to tag[slot].  The base words of G items are loaded before their
+// stores: shared stores would otherwise order every following load behind
+// them.  lim = valid items of the tile (0xffffffff: all), i0 = position of
+// item 0 (items at i0 + 32 s).
+constexpr int kStageG = 8;
+template <int G, int K_, class Tag>
+__device__ __forceinline__ void stage_tag(const uint32_t (&pk)[K_], const uint32_t (&pay)[K_], const uint32_t* cnt,
+                                          int whn, uint32_t w, uint32_t sh, uint32_t* buf, Tag* tag, uint32_t lim,
+                                          uint32_t i0) {
+#pragma unroll
+  for (int c = 0; c < K_; c += G) {
+    uint32_t bw[G];
+#pragma unroll
+    for (int q = 0; q < G; ++q) bw[q] = cnt[(pk[c + q] >> 16) * whn + (w >> 1)];
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      if (lim == 0xffffffffu || i0 + (c + q) * 32 < lim) {
+        const uint32_t pos = ((bw[q] >> sh) & 0xffffu) + (pk[c + q] & 0xffffu);
+        buf[pos] = pay[c + q];
+        tag[pos] = (Tag)(pk[c + q] >> 16);
+      }
+    }
+  }
+}
+
 // L1 place.  One CTA per count tile (CT1 edges), place tiles of PT edges in
 // order with running per-digit cursors.  Per place tile: TMA bulk load of the
 // edges and of the offsets window; every source boundary inside the tile is
@@ -502,11 +530,12 @@ __device__ __forceinline__ void writeout_tag(uint32_t* __restrict__ out, const u
 // array holds the cursor between tiles and the index delta during a tile
 // (delta = cursor - tile start, restored from the digit end after the tile),
 // so the shared-memory footprint matches the 32-bit form.
-template <int kMode, int KK = K, bool kW64 = false>
-__global__ void __launch_bounds__(T, (KK > 16 || kW64 ? 2 : 4)) k_p1(const P1Args a) {
-  // place tiles of PT = W * KK * 32 edges; the offsets window doubles as the
+template <int kMode, int KK = K, bool kW64 = false, int WW = W>
+__global__ void __launch_bounds__(WW * 32, (KK > 16 || kW64 || WW > 8 ? 2 : 4)) k_p1(const P1Args a) {
+  constexpr int W1_ = WW, T1_ = WW * 32, WH1_ = WW / 2 + 1, WP1_ = WW + 1;
+  // place tiles of PT = W1_ * KK * 32 edges; the offsets window doubles as the
   // tag array, so it holds max(1024, PT / 4) entries
-  constexpr int K = KK, PT = W * KK * 32, PTP = PT + 8, kWin = (PT / 4 > 1024) ? PT / 4 : 1024;
+  constexpr int K = KK, PT = W1_ * KK * 32, PTP = PT + 8, kWin = (PT / 4 > 1024) ? PT / 4 : 1024;
   extern __shared__ __align__(128) unsigned char smem[];
   const int D = a.D;
   uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem);                         // PTP (landing, then stage)
@@ -517,9 +546,9 @@ __global__ void __launch_bounds__(T, (KK > 16 || kW64 ? 2 : 4)) k_p1(const P1Arg
   // the next window lands by TMA after the end-of-tile barrier + proxy fence)
   static_assert(kWin * 8 >= PT * 2, "tag array must fit in the window");
   uint16_t* s_tag = reinterpret_cast<uint16_t*>(s_win);
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_mark + PT);                  // D * WH (packed, digit-major)
-  uint32_t* s_scr = s_cnt + round4(D * WH);                                    // D * WP (safe)
-  uint32_t* s_gcur = s_scr + (kMode == kRankSafe ? round4(D * WP) : 0);        // D
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_mark + PT);                  // D * WH1_ (packed, digit-major)
+  uint32_t* s_scr = s_cnt + round4(D * WH1_);                                    // D * WP1_ (safe)
+  uint32_t* s_gcur = s_scr + (kMode == kRankSafe ? round4(D * WP1_) : 0);        // D
   uint32_t* s_delta = s_gcur + D;                                              // D
   uint32_t* s_dtot = s_delta + D;                                              // D
   uint32_t* s_bh = reinterpret_cast<uint32_t*>(s_mark);                        // D (aliases the marks, dead after ranking)
@@ -539,12 +568,12 @@ __global__ void __launch_bounds__(T, (KK > 16 || kW64 ? 2 : 4)) k_p1(const P1Arg
   const uint64_t tb = k * CT1, te = umin64(a.E, tb + CT1);
   const int nplace = (int)((te - tb + PT - 1) / PT);
   const uint64_t gp0 = tb / PT;
-  for (int d = tid; d < D; d += T) {
+  for (int d = tid; d < D; d += T1_) {
     if constexpr (kW64) s_g64[d] = a.tbase[(uint64_t)d * a.ntiles + k];
     else s_gcur[d] = (uint32_t)a.tbase[(uint64_t)d * a.ntiles + k];
   }
-  for (int j = tid; j <= nplace; j += T) s_psrc[j] = a.psrc[gp0 + j];
-  zero_u32(s_cnt, round4(D * WH) + (kMode == kRankSafe ? round4(D * WP) : 0));
+  for (int j = tid; j <= nplace; j += T1_) s_psrc[j] = a.psrc[gp0 + j];
+  zero_u32(s_cnt, round4(D * WH1_) + (kMode == kRankSafe ? round4(D * WP1_) : 0));
   zero_u32(reinterpret_cast<uint32_t*>(s_mark), PT / 2);
   if (tid == 0) {
     mbar_init(&s_bar, 1);
@@ -589,7 +618,7 @@ __global__ void __launch_bounds__(T, (KK > 16 || kW64 ? 2 : 4)) k_p1(const P1Arg
   for (int j = 0; j < nplace; ++j) {
     if constexpr (kW64) {  // delta -> cursor of the next tile (after barrier (D): the write-out is done)
       if (j > 0)
-        for (int d = tid; d < D; d += T) s_g64[d] += s_dtot[d];
+        for (int d = tid; d < D; d += T1_) s_g64[d] += s_dtot[d];
     }
     const uint64_t pt = tb + (uint64_t)j * PT;
     const uint32_t n = (uint32_t)umin64(PT, te - pt);
@@ -616,7 +645,7 @@ __global__ void __launch_bounds__(T, (KK > 16 || kW64 ? 2 : 4)) k_p1(const P1Arg
     // (one per item; the owner of an item is the last source starting at or before it)
     const bool wide = s1 - s0 > 65535u;  // marks cannot encode the span: per-lane search below
     if (!wide) {
-      for (uint32_t v = s0 + 1 + tid; v <= s1; v += T) {
+      for (uint32_t v = s0 + 1 + tid; v <= s1; v += T1_) {
         const uint64_t p = off_at(v) - gi0;
         if (p < n && off_at((uint64_t)v + 1) > off_at(v)) s_mark[p] = (uint16_t)(v - s0);
       }
@@ -627,12 +656,15 @@ __global__ void __launch_bounds__(T, (KK > 16 || kW64 ? 2 : 4)) k_p1(const P1Arg
     uint32_t carry = owner_search(s0, s1, gi0 + iw, off_at);
     const uint32_t le = lanemask_le();
     uint32_t pay[K], pk[K];
+    // pay[s] / pk[s] first hold the slot's destination and mark: all loads of
+    // the tile are issued before the first rank atomic (the compiler keeps
+    // shared loads behind earlier shared atomics)
     auto slot = [&](int s, bool valid) {
       const uint32_t i = iw + s * 32 + lane;
-      const uint32_t dst = valid ? s_buf[o + i] : 0u;
+      const uint32_t dst = valid ? pay[s] : 0u;
       uint32_t src = carry;
       if (!wide) {
-        const uint32_t m = s_mark[i];
+        const uint32_t m = pk[s];
         const uint32_t bal = __ballot_sync(kFull, m != 0);
         if (bal) {  // a source starts inside this slot (warp-uniform)
           const uint32_t bm = bal & le;
@@ -646,9 +678,15 @@ __global__ void __launch_bounds__(T, (KK > 16 || kW64 ? 2 : 4)) k_p1(const P1Arg
       }
       if ((n == (uint32_t)PT) ? (s == K - 1 && i == PT - 1) : (valid && i == n - 1)) s_last_src = src;
       const uint32_t d = dst >> a.shift;
-      pk[s] = (d << 16) | rank_pk<kMode>(s_cnt + d * WH + (w >> 1), s_scr + d * WP + w, sh, valid);
+      pk[s] = (d << 16) | rank_pk<kMode>(s_cnt + d * WH1_ + (w >> 1), s_scr + d * WP1_ + w, sh, valid);
       pay[s] = ((dst & a.low_mask) << a.L) | (src & a.src_mask);
     };
+#pragma unroll
+    for (int s = 0; s < K; ++s) {
+      const uint32_t i = iw + s * 32 + lane;
+      pay[s] = s_buf[o + i];
+      pk[s] = s_mark[i];
+    }
     if (n == (uint32_t)PT) {
 #pragma unroll
       for (int s = 0; s < K; ++s) slot(s, true);
@@ -658,17 +696,17 @@ __global__ void __launch_bounds__(T, (KK > 16 || kW64 ? 2 : 4)) k_p1(const P1Arg
     }
     __syncthreads();  // (B) ranks done; landing buffer and marks consumed
     if constexpr (kW64)
-      flat_bases_epi<WH>(s_cnt, D, s_tmp, [&](int d, uint32_t b, uint32_t e) {
+      flat_bases_epi<WH1_>(s_cnt, D, s_tmp, [&](int d, uint32_t b, uint32_t e) {
         s_g64[d] -= b;
         s_dtot[d] = e;
       });
     else
-      flat_bases_pk<WH>(s_cnt, D, s_gcur, s_dtot, s_delta, s_tmp);
+      flat_bases_pk<WH1_>(s_cnt, D, s_gcur, s_dtot, s_delta, s_tmp);
     // source-high boundaries inside this tile (compact R1 decode table)
     const uint32_t h_last = s_last_src >> a.L;
     for (uint32_t h = (h_prev == 0xffffffffu) ? 0u : h_prev + 1; h <= h_last; ++h) {
       const uint64_t q = __ldg(offs + ((uint64_t)h << a.L)) - gi0;  // first item with src >= h << L
-      for (int d = tid; d < D; d += T) s_bh[d] = 0;
+      for (int d = tid; d < D; d += T1_) s_bh[d] = 0;
       __syncthreads();
 #pragma unroll
       for (int s = 0; s < K; ++s) {
@@ -676,30 +714,23 @@ __global__ void __launch_bounds__(T, (KK > 16 || kW64 ? 2 : 4)) k_p1(const P1Arg
         if (i < n && i < q) smem_inc(&s_bh[pk[s] >> 16]);
       }
       __syncthreads();
-      for (int d = tid; d < D; d += T) {
-        const uint64_t g0 = kW64 ? s_g64[d] + (s_cnt[d * WH] & 0xffffu) : (uint64_t)s_gcur[d];
+      for (int d = tid; d < D; d += T1_) {
+        const uint64_t g0 = kW64 ? s_g64[d] + (s_cnt[d * WH1_] & 0xffffu) : (uint64_t)s_gcur[d];
         a.seg_hi[(uint64_t)d * (a.nh + 1) + h] = g0 + s_bh[d];
       }
       __syncthreads();
     }
     h_prev = h_last;
-    // stage payloads and global indices by digit
-#pragma unroll
-    for (int s = 0; s < K; ++s) {
-      if (n == (uint32_t)PT || iw + s * 32 + lane < n) {
-        const uint32_t d = pk[s] >> 16;
-        const uint32_t pos = ((s_cnt[d * WH + (w >> 1)] >> sh) & 0xffffu) + (pk[s] & 0xffffu);
-        s_buf[pos] = pay[s];
-        s_tag[pos] = (uint16_t)d;
-      }
-    }
+    // stage payloads and global indices by digit (base words loaded in groups
+    // of kStageG before their stores)
+    stage_tag<kStageG, K>(pk, pay, s_cnt, WH1_, w, sh, s_buf, s_tag, (n == (uint32_t)PT) ? 0xffffffffu : n, iw + lane);
     __syncthreads();  // (C)
-    if constexpr (kW64) writeout_tag<T, PT>(a.out, s_buf, s_tag, s_g64, n);
-    else writeout_tag<T, PT>(a.out, s_buf, s_tag, s_delta, n);
+    if constexpr (kW64) writeout_tag<T1_, PT>(a.out, s_buf, s_tag, s_g64, n);
+    else writeout_tag<T1_, PT>(a.out, s_buf, s_tag, s_delta, n);
     zero_u32(reinterpret_cast<uint32_t*>(s_mark), PT / 2);
-    zero_u32(s_cnt, round4(D * WH));
+    zero_u32(s_cnt, round4(D * WH1_));
     if constexpr (!kW64)
-      for (int d = tid; d < D; d += T) s_gcur[d] += s_dtot[d];
+      for (int d = tid; d < D; d += T1_) s_gcur[d] += s_dtot[d];
     fence_proxy_async_smem();
     __syncthreads();  // (D)
     if (tid == 0 && j + 1 < nplace) issue(j + 1);
@@ -927,7 +958,7 @@ __device__ __forceinline__ uint32_t slot_owner32(uint32_t& cur, uint32_t& nb, ui
 
 // Place: per tile, place tiles of PT records are ranked by digit, staged with
 // their global indices, and written out (persistent, grid-stride over tiles).
-template <int kMode, class Dec, int KK, bool kProf = false, int kIO = kIoPlain>
+template <int kMode, class Dec, int KK, bool kProf = false, int kIO = kIoPlain, bool kPre = true>
 __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __restrict__ rec, const RTile* __restrict__ tiles,
                                              const uint32_t* __restrict__ n_tiles, int D, Dec dec,
                                              const uint64_t* __restrict__ base, uint32_t* __restrict__ out,
@@ -1057,9 +1088,9 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __r
       // pk = digit << 16 | rank; kIoSplit: low-digit byte << 24 | digit << 13 | rank (rank < 8192, digit < 2048)
       constexpr int kDS = (kIO == kIoSplit) ? 13 : 16;
       uint32_t pay[K], pk[K];
-      auto slot = [&](int s, bool valid) {
+      auto slot = [&](int s, bool valid) {  // pay[s] holds the slot's record (loaded below)
         const uint32_t i0 = iw + s * 32, i = i0 + lane;
-        const uint32_t r = valid ? s_buf[o + i] : 0u;
+        const uint32_t r = valid ? (kPre ? pay[s] : s_buf[o + i]) : 0u;
         uint32_t h = t.h0;
         if constexpr (Dec::kSrcHigh) h += wbnd ? slot_owner32(cur, nb, rel0 + i0, nbt, bnd_at) : cur;
         uint32_t d;
@@ -1076,6 +1107,10 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __r
           pay[s] = dec.payload(r, h);
         }
       };
+      if constexpr (kPre) {
+#pragma unroll
+        for (int s = 0; s < K; ++s) pay[s] = s_buf[o + iw + s * 32 + lane];
+      }
       if (n == (uint32_t)PT) {
 #pragma unroll
         for (int s = 0; s < K; ++s) slot(s, true);
@@ -1093,6 +1128,9 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __r
       else
         flat_bases_pk<WH>(s_cnt, D, s_gcur, s_dtot, s_delta, s_tmp);
       tick(3);
+      if constexpr (kIO != kIoSplit) {
+        stage_tag<kPre ? kStageG : 1, K>(pk, pay, s_cnt, WH, w, sh, s_buf, s_tag, (n == (uint32_t)PT) ? 0xffffffffu : n, iw + lane);
+      } else {
 #pragma unroll
       for (int s = 0; s < K; ++s) {
         if (n == (uint32_t)PT || iw + s * 32 + lane < n) {
@@ -1102,6 +1140,7 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __r
           s_tag[pos] = (uint16_t)d;
           if constexpr (kIO == kIoSplit) s_lvx[pos] = (uint8_t)(pk[s] >> 24);
         }
+      }
       }
       __syncthreads();  // (C)
       tick(4);
@@ -1162,7 +1201,7 @@ inline size_t smem_p3(int mode, bool lv = false) {
 // kPosFine: the record's fine bucket inside the unit comes from its position
 // (R2 has no room for fine-digit bits); else from the record's bits.
 // kLv (requires kPosFine): the low digit comes from the separate byte array.
-template <int kMode, bool kPosFine, bool kProf = false, bool kLv = false>
+template <int kMode, bool kPosFine, bool kProf = false, bool kLv = false, bool kPre = true>
 __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
   // phase profile (kProf builds only; thread 0, clock64): 0 fetch/issue, 1 wait, 2 rank, 3 bases+offsets, 4 stage, 5 store
   unsigned long long pacc[kProf ? 6 : 1] = {};
@@ -1262,11 +1301,16 @@ __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
     const uint32_t lvoff = (u.f0 & ((1u << a.gbits) - 1)) << a.c;
     const uint8_t* lvb = s_lvb + b * CAP3L + (kLv ? (uint32_t)(reinterpret_cast<uintptr_t>(a.lv + u.start) & 15) : 0u);
     uint32_t rr[K3], pk[K3];
+    constexpr int kG3 = kPre ? kStageG : 1;
+    if constexpr (kPre) {
+#pragma unroll
+      for (int s = 0; s < K3; ++s) rr[s] = buf[o + seg0 + s * 32 + lane];  // all loads before the first rank atomic
+    }
 #pragma unroll
     for (int s = 0; s < K3; ++s) {
       const uint32_t i = seg0 + s * 32 + lane;
       const bool valid = i < n;
-      const uint32_t r = valid ? buf[o + i] : 0u;
+      const uint32_t r = valid ? (kPre ? rr[s] : buf[o + i]) : 0u;
       uint32_t lv;
       if constexpr (kPosFine) {
         const uint32_t j = wbnd ? slot_owner32(fcur, fnb, seg0 + s * 32, nbt, bnd_at) : fcur;
@@ -1290,8 +1334,14 @@ __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
     uint32_t* t_e = a.t_edges + u.start;
     const uint32_t oo = align_items_u32(t_e);  // staging offset matching the output's 16B alignment
 #pragma unroll
-    for (int s = 0; s < K3; ++s)
-      if (seg0 + s * 32 + lane < n) buf[oo + ((s_cnt[(pk[s] >> 16) * WH3 + (w >> 1)] >> sh) & 0xffffu) + (pk[s] & 0xffffu)] = rr[s];
+    for (int c = 0; c < K3; c += kG3) {  // base words of kG3 items loaded before their stores
+      uint32_t bw[kG3];
+#pragma unroll
+      for (int q = 0; q < kG3; ++q) bw[q] = s_cnt[(pk[c + q] >> 16) * WH3 + (w >> 1)];
+#pragma unroll
+      for (int q = 0; q < kG3; ++q)
+        if (seg0 + (c + q) * 32 + lane < n) buf[oo + ((bw[q] >> sh) & 0xffffu) + (pk[c + q] & 0xffffu)] = rr[c + q];
+    }
     fence_proxy_async_smem();
     __syncthreads();  // (C)
     tick(4);
