@@ -334,6 +334,7 @@ template <typename Kern>
 unsigned persistent_grid(Kern kernel, int threads, size_t smem, uint64_t work) {
   int occ = 1;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem) != cudaSuccess || occ < 1) occ = 1;
+  if (const char* e = getenv("GT_OCC")) occ = std::max(1, std::min(occ, atoi(e)));  // experiments: CTAs per SM cap
   const uint64_t g = (uint64_t)num_sms() * occ;
   return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g, std::max<uint64_t>(work, 1)));
 }

@@ -929,9 +929,10 @@ constexpr int kIoLv = 2;     // level 3 big buckets of wide graphs: source + dig
 // Wide forms use 64-bit output positions: the per-digit cursor array holds the
 // cursor between place tiles and the index delta during one (as in k_p1 kW64).
 
-inline size_t smem_p2(int D, int mode, int KK = K, int io = kIoPlain) {
-  const size_t pt = (size_t)W * KK * 32;
-  return (pt + 8) * 4 + pt * 2 + ((size_t)round4(D * WH) + (mode == kRankSafe ? (size_t)round4(D * WP) : 0)) * 4 + (size_t)D * 4 * 4 +
+inline size_t smem_p2(int D, int mode, int KK = K, int io = kIoPlain, int WW = W) {
+  const size_t pt = (size_t)WW * KK * 32;
+  const int wh = WW / 2 + 1, wp = WW + 1;
+  return (pt + 8) * 4 + pt * 2 + ((size_t)round4(D * wh) + (mode == kRankSafe ? (size_t)round4(D * wp) : 0)) * 4 + (size_t)D * 4 * 4 +
          40 * 4 + (size_t)kMaxBnd * 4 + (io != kIoPlain ? pt + 16 : 0);
 }
 
@@ -958,8 +959,8 @@ __device__ __forceinline__ uint32_t slot_owner32(uint32_t& cur, uint32_t& nb, ui
 
 // Place: per tile, place tiles of PT records are ranked by digit, staged with
 // their global indices, and written out (persistent, grid-stride over tiles).
-template <int kMode, class Dec, int KK, bool kProf = false, int kIO = kIoPlain, bool kPre = true>
-__global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __restrict__ rec, const RTile* __restrict__ tiles,
+template <int kMode, class Dec, int KK, bool kProf = false, int kIO = kIoPlain, bool kPre = true, int WW = W, int kMinB = (KK > 16 ? 2 : 4)>
+__global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restrict__ rec, const RTile* __restrict__ tiles,
                                              const uint32_t* __restrict__ n_tiles, int D, Dec dec,
                                              const uint64_t* __restrict__ base, uint32_t* __restrict__ out,
                                              unsigned long long* __restrict__ prof = nullptr,
@@ -978,13 +979,14 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __r
       }
     }
   };
-  constexpr int PT = W * KK * 32, PTP = PT + 8, K = KK;
+  constexpr int W2_ = WW, T2_ = WW * 32, WH2_ = WW / 2 + 1, WP2_ = WW + 1;
+  constexpr int PT = W2_ * KK * 32, PTP = PT + 8, K = KK;
   extern __shared__ __align__(128) unsigned char smem[];
   uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem);                         // PTP
   uint16_t* s_tag = reinterpret_cast<uint16_t*>(s_buf + PTP);                 // PT (digit of each staged slot)
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_tag + PT);                   // D * WH (packed, digit-major)
-  uint32_t* s_scr = s_cnt + round4(D * WH);                                    // D * WP (safe)
-  uint32_t* s_gcur = s_scr + (kMode == kRankSafe ? round4(D * WP) : 0);        // D
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_tag + PT);                   // D * WH2_ (packed, digit-major)
+  uint32_t* s_scr = s_cnt + round4(D * WH2_);                                    // D * WP2_ (safe)
+  uint32_t* s_gcur = s_scr + (kMode == kRankSafe ? round4(D * WP2_) : 0);        // D
   uint32_t* s_delta = s_gcur + D;                                              // D
   uint32_t* s_dstart = s_delta + D;                                            // D
   uint32_t* s_dtot = s_dstart + D;                                             // D
@@ -999,7 +1001,7 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __r
   const uint32_t tid = threadIdx.x, lane = lane_id(), w = warp_id();
   const uint32_t sh = (w & 1) << 4;
   const uint32_t ntall = *n_tiles;
-  zero_u32(s_cnt, round4(D * WH) + (kMode == kRankSafe ? round4(D * WP) : 0));
+  zero_u32(s_cnt, round4(D * WH2_) + (kMode == kRankSafe ? round4(D * WP2_) : 0));
   if (tid == 0) {
     mbar_init(&s_bar, 1);
     fence_mbar_init();
@@ -1010,7 +1012,7 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __r
   for (uint32_t g = blockIdx.x; g < ntall; g += gridDim.x) {
     const RTile t = tiles[g];
     const uint64_t row0 = (uint64_t)(g - t.j) * D + t.j;
-    for (int d = tid; d < D; d += T) {
+    for (int d = tid; d < D; d += T2_) {
       if constexpr (kW64) s_g64[d] = base[row0 + (uint64_t)d * t.nt];
       else s_gcur[d] = (uint32_t)base[row0 + (uint64_t)d * t.nt];
     }
@@ -1019,7 +1021,7 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __r
     if constexpr (Dec::kSrcHigh) {
       hrow = dec.seg_hi + (uint64_t)t.seg * (dec.nh + 1) + t.h0 + 1;  // boundary k (1-based) = hrow[k - 1]
       if (nbt <= (uint32_t)kMaxBnd)
-        for (uint32_t q = tid; q < nbt; q += T) s_bnd[q] = (uint32_t)(hrow[q] - t.start);
+        for (uint32_t q = tid; q < nbt; q += T2_) s_bnd[q] = (uint32_t)(hrow[q] - t.start);
     }
     const int nplace = (int)((t.n + PT - 1) / PT);
     auto issue = [&](int jj) {  // thread 0
@@ -1052,7 +1054,7 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __r
     for (int jj = 0; jj < nplace; ++jj) {
       if constexpr (kW64) {  // delta -> cursor of this place tile (after barrier (D))
         if (jj > 0)
-          for (int d = tid; d < D; d += T) s_g64[d] += s_dtot[d];
+          for (int d = tid; d < D; d += T2_) s_g64[d] += s_dtot[d];
       }
       const uint64_t pt = t.start + (uint64_t)jj * PT;
       const uint32_t n = min((uint32_t)PT, t.n - jj * PT);
@@ -1097,8 +1099,8 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __r
         if constexpr (kIO == kIoLv) d = valid ? (uint32_t)s_lvx[o8 + i] : 0u;
         else d = dec.digit(r);
         uint32_t rk;
-        if constexpr (Dec::kMatchRank) rk = rank_match(s_cnt + d * WH + (w >> 1), sh, d, valid);
-        else rk = rank_pk<kMode>(s_cnt + d * WH + (w >> 1), s_scr + d * WP + w, sh, valid);
+        if constexpr (Dec::kMatchRank) rk = rank_match(s_cnt + d * WH2_ + (w >> 1), sh, d, valid);
+        else rk = rank_pk<kMode>(s_cnt + d * WH2_ + (w >> 1), s_scr + d * WP2_ + w, sh, valid);
         if constexpr (kIO == kIoSplit) {
           pk[s] = (((r >> dec.L) & dec.lvmask) << 24) | (d << 13) | rk;
           pay[s] = (h << dec.L) | (r & dec.src_mask);
@@ -1121,21 +1123,21 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __r
       __syncthreads();  // (B)
       tick(2);
       if constexpr (kW64)
-        flat_bases_epi<WH>(s_cnt, D, s_tmp, [&](int d, uint32_t b, uint32_t e) {
+        flat_bases_epi<WH2_>(s_cnt, D, s_tmp, [&](int d, uint32_t b, uint32_t e) {
           s_g64[d] -= b;
           s_dtot[d] = e;
         });
       else
-        flat_bases_pk<WH>(s_cnt, D, s_gcur, s_dtot, s_delta, s_tmp);
+        flat_bases_pk<WH2_>(s_cnt, D, s_gcur, s_dtot, s_delta, s_tmp);
       tick(3);
       if constexpr (kIO != kIoSplit) {
-        stage_tag<kPre ? kStageG : 1, K>(pk, pay, s_cnt, WH, w, sh, s_buf, s_tag, (n == (uint32_t)PT) ? 0xffffffffu : n, iw + lane);
+        stage_tag<kPre ? kStageG : 1, K>(pk, pay, s_cnt, WH2_, w, sh, s_buf, s_tag, (n == (uint32_t)PT) ? 0xffffffffu : n, iw + lane);
       } else {
 #pragma unroll
       for (int s = 0; s < K; ++s) {
         if (n == (uint32_t)PT || iw + s * 32 + lane < n) {
           const uint32_t d = (pk[s] >> kDS) & ((kIO == kIoSplit) ? 0x7ffu : 0xffffu);
-          const uint32_t pos = ((s_cnt[d * WH + (w >> 1)] >> sh) & 0xffffu) + (pk[s] & ((1u << kDS) - 1));
+          const uint32_t pos = ((s_cnt[d * WH2_ + (w >> 1)] >> sh) & 0xffffu) + (pk[s] & ((1u << kDS) - 1));
           s_buf[pos] = pay[s];
           s_tag[pos] = (uint16_t)d;
           if constexpr (kIO == kIoSplit) s_lvx[pos] = (uint8_t)(pk[s] >> 24);
@@ -1145,7 +1147,7 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __r
       __syncthreads();  // (C)
       tick(4);
       if constexpr (kIO == kIoPlain) {
-        writeout_tag<T, PT>(out, s_buf, s_tag, s_delta, n);
+        writeout_tag<T2_, PT>(out, s_buf, s_tag, s_delta, n);
       } else {  // 64-bit positions
         auto put = [&](uint32_t i) {
           const uint64_t q = s_g64[s_tag[i]] + i;
@@ -1154,14 +1156,14 @@ __global__ void __launch_bounds__(T, (KK > 16 ? 2 : 4)) k_p2(const uint32_t* __r
         };
         if (n == (uint32_t)PT) {
 #pragma unroll
-          for (int q = 0; q < PT / T; ++q) put(threadIdx.x + q * T);
+          for (int q = 0; q < PT / T2_; ++q) put(threadIdx.x + q * T2_);
         } else {
-          for (uint32_t i = threadIdx.x; i < n; i += T) put(i);
+          for (uint32_t i = threadIdx.x; i < n; i += T2_) put(i);
         }
       }
-      zero_u32(s_cnt, round4(D * WH));
+      zero_u32(s_cnt, round4(D * WH2_));
       if constexpr (!kW64)
-        for (int d = tid; d < D; d += T) s_gcur[d] += s_dtot[d];
+        for (int d = tid; d < D; d += T2_) s_gcur[d] += s_dtot[d];
       fence_proxy_async_smem();
       __syncthreads();  // (D)
       tick(5);
