@@ -825,8 +825,12 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
   // level 1 uses 8192-edge place tiles (measured: C3 k_p1 2.82 -> 2.79 ms, C4 8.75 -> 7.56 ms)
   // (wide graphs: 4096-edge tiles keep 2 CTAs/SM with 2048 coarse digits)
   const int k1 = env_int("GT_K1", 32);  // C5 (wide, 2048 coarse digits): 8192-edge tiles 90.0 -> 81.8 ms
-  const int w1 = p.wide ? W : env_int("GT_W1", W);  // warps per level-1 CTA (16: 8192-edge tiles at K = 16)
-  const uint64_t pt1 = (uint64_t)w1 * (w1 == 16 ? 16 : k1) * 32, nplace1 = (E + pt1 - 1) / pt1;
+  // warps per level-1 CTA: compact graphs 16 = 8192-edge tiles at K = 16; wide graphs 16 = 16384-edge tiles at K = 32
+  // (GT_W1 = 32: compact graphs with 16384-edge tiles, 16 warps at K = 32)
+  // wide graphs (C5): 16384-edge tiles 81.8 -> 58.0 ms
+  const int w1x = p.wide ? (env_int("GT_W1W", 16) == 16 ? 32 : W) : env_int("GT_W1", W);
+  const int w1 = w1x == 32 ? 16 : w1x;
+  const uint64_t pt1 = (uint64_t)w1 * ((w1x == 16) ? 16 : k1) * 32, nplace1 = (E + pt1 - 1) / pt1;
   k_tile_src<<<(unsigned)((nplace1 + 1 + 255) / 256), 256, 0, st>>>(in, E, pt1, nplace1 + 1, psrc);
   GT_LAUNCH_CHECK();
   k_prev_src<<<(unsigned)((q.ntiles1 + 255) / 256), 256, 0, st>>>(in, E, CT1, q.ntiles1, prev);
@@ -863,7 +867,15 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
       kern<<<(unsigned)q.ntiles1, T, sm, st>>>(a);
       return GT_OK;
     };
-    if (p.wide) {  // 64-bit R1 positions
+    if (!p.wide && w1x == 32) {
+      const size_t sm = smem_p1(D1, kMode, 32, 16);
+      if ((rc = set_smem(k_p1<kMode, 32, false, 16, 1>, sm))) return rc;
+      k_p1<kMode, 32, false, 16, 1><<<(unsigned)q.ntiles1, 512, sm, st>>>(a);
+    } else if (p.wide && w1 == 16) {  // 16384-edge tiles, one 16-warp CTA per SM
+      const size_t sm = smem_p1(D1, kMode, 32, 16);
+      if ((rc = set_smem(k_p1<kMode, 32, true, 16, 1>, sm))) return rc;
+      k_p1<kMode, 32, true, 16, 1><<<(unsigned)q.ntiles1, 512, sm, st>>>(a);
+    } else if (p.wide) {  // 64-bit R1 positions
       if ((rc = (k1 == 32) ? go1(k_p1<kMode, 32, true>, 32) : go1(k_p1<kMode, 16, true>, 16))) return rc;
     } else if (w1 == 16) {
       const size_t sm = smem_p1(D1, kMode, 16, 16);
@@ -925,9 +937,22 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
         kern<<<g, T, sm, st>>>(t_edges, tiles2, cfirst + D1, Db, dec, base2, r2, nullptr, nullptr, r2lv);
         return GT_OK;
       };
-      if ((rc = (k2 == 32) ? go2(k_p2<kMode, DecR1, 32, false, kIoSplit>, 32)
-                           : go2(k_p2<kMode, DecR1, 16, false, kIoSplit>, 16)))
+      if (env_int("GT_W2W", 16) == 16) {  // 16384-record tiles, one 16-warp CTA per SM (C5: 88.4 -> 65.9 ms)
+        const size_t sm = smem_p2(Db, kMode, 32, kIoSplit, 16);
+        using K16 = decltype(&k_p2<kMode, DecR1, 32, false, kIoSplit, true, 16, 1>);
+        K16 kern = k_p2<kMode, DecR1, 32, false, kIoSplit, true, 16, 1>;
+        if ((rc = set_smem(kern, sm))) return rc;
+        const unsigned g = persistent_grid(kern, 512, sm, q.max_t2);
+        kern<<<g, 512, sm, st>>>(t_edges, tiles2, cfirst + D1, Db, dec, base2, r2, nullptr, nullptr, r2lv);
+      } else if ((rc = (k2 == 32) ? go2(k_p2<kMode, DecR1, 32, false, kIoSplit>, 32)
+                                  : go2(k_p2<kMode, DecR1, 16, false, kIoSplit>, 16))) {
         return rc;
+      }
+    } else if (k2 == 32 && env_int("GT_W2", 8) == 16) {
+      const size_t sm = smem_p2(Db, kMode, 32, kIoPlain, 16);
+      if ((rc = set_smem(k_p2<kMode, DecR1, 32, false, kIoPlain, true, 16, 1>, sm))) return rc;
+      const unsigned g = persistent_grid(k_p2<kMode, DecR1, 32, false, kIoPlain, true, 16, 1>, 512, sm, q.max_t2);
+      k_p2<kMode, DecR1, 32, false, kIoPlain, true, 16, 1><<<g, 512, sm, st>>>(t_edges, tiles2, cfirst + D1, Db, dec, base2, r2);
     } else if (k2 == 32) {
       const size_t sm = smem_p2(Db, kMode, 32);
       if ((rc = set_smem(k_p2<kMode, DecR1, 32>, sm))) return rc;

@@ -530,8 +530,8 @@ __device__ __forceinline__ void stage_tag(const uint32_t (&pk)[K_], const uint32
 // array holds the cursor between tiles and the index delta during a tile
 // (delta = cursor - tile start, restored from the digit end after the tile),
 // so the shared-memory footprint matches the 32-bit form.
-template <int kMode, int KK = K, bool kW64 = false, int WW = W>
-__global__ void __launch_bounds__(WW * 32, (KK > 16 || kW64 || WW > 8 ? 2 : 4)) k_p1(const P1Args a) {
+template <int kMode, int KK = K, bool kW64 = false, int WW = W, int kMinB = (KK > 16 || kW64 || WW > 8 ? 2 : 4)>
+__global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
   constexpr int W1_ = WW, T1_ = WW * 32, WH1_ = WW / 2 + 1, WP1_ = WW + 1;
   // place tiles of PT = W1_ * KK * 32 edges; the offsets window doubles as the
   // tag array, so it holds max(1024, PT / 4) entries
