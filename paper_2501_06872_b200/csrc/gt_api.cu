@@ -339,6 +339,14 @@ unsigned persistent_grid(Kern kernel, int threads, size_t smem, uint64_t work) {
   return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g, std::max<uint64_t>(work, 1)));
 }
 
+// Largest dynamic shared memory a block may opt into on the current device.
+size_t max_smem_optin() {
+  int dev = 0, v = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+    return 0;
+  return (size_t)v;
+}
+
 template <typename K>
 int set_smem(K kernel, size_t bytes) {
   GT_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
@@ -828,7 +836,10 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
   // warps per level-1 CTA: compact graphs 16 = 8192-edge tiles at K = 16; wide graphs 16 = 16384-edge tiles at K = 32
   // (GT_W1 = 32: compact graphs with 16384-edge tiles, 16 warps at K = 32)
   // wide graphs (C5): 16384-edge tiles 81.8 -> 58.0 ms
-  const int w1x = p.wide ? (env_int("GT_W1W", 16) == 16 ? 32 : W) : env_int("GT_W1", W);
+  // (the 16-warp forms need their larger tables to fit: the safe rank mode's scratch table may not)
+  int w1x = p.wide ? (env_int("GT_W1W", 16) == 16 ? 32 : W) : env_int("GT_W1", W);
+  if (w1x == 32 && smem_p1(D1, kMode, 32, 16) + 64 > max_smem_optin()) w1x = W;
+  if (w1x == 16 && smem_p1(D1, kMode, 16, 16) + 64 > max_smem_optin()) w1x = W;
   const int w1 = w1x == 32 ? 16 : w1x;
   const uint64_t pt1 = (uint64_t)w1 * ((w1x == 16) ? 16 : k1) * 32, nplace1 = (E + pt1 - 1) / pt1;
   k_tile_src<<<(unsigned)((nplace1 + 1 + 255) / 256), 256, 0, st>>>(in, E, pt1, nplace1 + 1, psrc);
@@ -937,7 +948,7 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
         kern<<<g, T, sm, st>>>(t_edges, tiles2, cfirst + D1, Db, dec, base2, r2, nullptr, nullptr, r2lv);
         return GT_OK;
       };
-      if (env_int("GT_W2W", 16) == 16) {  // 16384-record tiles, one 16-warp CTA per SM (C5: 88.4 -> 65.9 ms)
+      if (env_int("GT_W2W", 16) == 16 && smem_p2(Db, kMode, 32, kIoSplit, 16) + 64 <= max_smem_optin()) {  // 16384-record tiles, one 16-warp CTA per SM (C5: 88.4 -> 65.9 ms)
         const size_t sm = smem_p2(Db, kMode, 32, kIoSplit, 16);
         using K16 = decltype(&k_p2<kMode, DecR1, 32, false, kIoSplit, true, 16, 1>);
         K16 kern = k_p2<kMode, DecR1, 32, false, kIoSplit, true, 16, 1>;
@@ -948,7 +959,7 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
                                   : go2(k_p2<kMode, DecR1, 16, false, kIoSplit>, 16))) {
         return rc;
       }
-    } else if (k2 == 32 && env_int("GT_W2", 8) == 16) {
+    } else if (k2 == 32 && env_int("GT_W2", 8) == 16 && smem_p2(Db, kMode, 32, kIoPlain, 16) + 64 <= max_smem_optin()) {
       const size_t sm = smem_p2(Db, kMode, 32, kIoPlain, 16);
       if ((rc = set_smem(k_p2<kMode, DecR1, 32, false, kIoPlain, true, 16, 1>, sm))) return rc;
       const unsigned g = persistent_grid(k_p2<kMode, DecR1, 32, false, kIoPlain, true, 16, 1>, 512, sm, q.max_t2);
@@ -995,8 +1006,11 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
   // ---- step 3: level 3 (units of small fine buckets; tiled count/scan/place for big ones)
   k_set_u64<<<1, 1, 0, st>>>(fbase + q.nfine, E);
   GT_LAUNCH_CHECK();
+  // level-3 unit width: 16 warps (8192-record units, 2 CTAs/SM) or 32 warps (16384-record units, 1 CTA/SM)
+  const int w3 = (env_int("GT_W3", 16) == 32 && smem_p3(kMode, p.wide, 32) + 64 <= max_smem_optin()) ? 32 : 16;
   k_plan3<<<(unsigned)((q.nfine / (1u << sbits) + 255) / 256 + 1), 256, 0, st>>>(fbase, (uint32_t)q.nfine, sbits,
-                                                                                   units, cnt + 0, bigs, cnt + 1);
+                                                                                   units, cnt + 0, bigs, cnt + 1,
+                                                                                   (uint32_t)(w3 * K3 * 32));
   GT_LAUNCH_CHECK();
   {
     uint32_t* bnt = reinterpret_cast<uint32_t*>(ws + q.o_bnt);
@@ -1073,12 +1087,12 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
     a.V = V;
     a.t_offsets = t_offsets;
     a.t_edges = t_edges;
-    const size_t sm = smem_p3(kMode, p.wide);
+    const size_t sm = smem_p3(kMode, p.wide, w3);
     auto go3 = [&](auto kern) -> int {
       int r;
       if ((r = set_smem(kern, sm))) return r;
-      const unsigned g = persistent_grid(kern, W3 * 32, sm, q.nfine);
-      kern<<<g, W3 * 32, sm, st>>>(a);
+      const unsigned g = persistent_grid(kern, w3 * 32, sm, q.nfine);
+      kern<<<g, w3 * 32, sm, st>>>(a);
       return GT_OK;
     };
     if ((rc = tm.kbegin(2))) return rc;
@@ -1096,7 +1110,12 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
               h[0] / tot, h[1] / tot, h[2] / tot, h[3] / tot, h[4] / tot, h[5] / tot, tot);
       cudaFreeAsync(a.prof, st);
     } else if (p.wide) {
-      rc = go3(k_p3<kMode, true, false, true>);
+      rc = (w3 == 32) ? go3(k_p3<kMode, true, false, true, true, 32>) : go3(k_p3<kMode, true, false, true>);
+    } else if (w3 == 32) {
+      if ((pre & 8) || ((pre & 16) && pos_fine))
+        rc = pos_fine ? go3(k_p3<kMode, true, false, false, true, 32>) : go3(k_p3<kMode, false, false, false, true, 32>);
+      else
+        rc = pos_fine ? go3(k_p3<kMode, true, false, false, false, 32>) : go3(k_p3<kMode, false, false, false, false, 32>);
     } else {
       if ((pre & 8) || ((pre & 16) && pos_fine)) rc = pos_fine ? go3(k_p3<kMode, true>) : go3(k_p3<kMode, false>);
       else rc = pos_fine ? go3(k_p3<kMode, true, false, false, false>) : go3(k_p3<kMode, false, false, false, false>);

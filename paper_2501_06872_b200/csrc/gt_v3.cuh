@@ -1195,16 +1195,18 @@ struct P3Args {
 };
 
 constexpr int CAP3L = CAP3 + 16;  // digit-byte landing per buffer (whole 16-byte blocks)
-inline size_t smem_p3(int mode, bool lv = false) {
-  return (size_t)2 * CAP3P * 4 + ((size_t)round4(ML3 * WH3) + (mode == kRankSafe ? (size_t)round4(ML3 * W3P) : 0)) * 4 +
-         (size_t)ML3 * 8 + 40 * 4 + (lv ? (size_t)2 * CAP3L : 0);
+inline size_t smem_p3(int mode, bool lv = false, int ww = W3) {
+  const size_t cap = (size_t)ww * K3 * 32;
+  const int wh = ww / 2 + 1, wp = ww + 1;
+  return (size_t)2 * (cap + 8) * 4 + ((size_t)round4(ML3 * wh) + (mode == kRankSafe ? (size_t)round4(ML3 * wp) : 0)) * 4 +
+         (size_t)ML3 * 8 + 40 * 4 + (lv ? (size_t)2 * (cap + 16) : 0);
 }
 
 // kPosFine: the record's fine bucket inside the unit comes from its position
 // (R2 has no room for fine-digit bits); else from the record's bits.
 // kLv (requires kPosFine): the low digit comes from the separate byte array.
-template <int kMode, bool kPosFine, bool kProf = false, bool kLv = false, bool kPre = true>
-__global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
+template <int kMode, bool kPosFine, bool kProf = false, bool kLv = false, bool kPre = true, int WW3 = W3>
+__global__ void __launch_bounds__(WW3 * 32, WW3 > 16 ? 1 : 2) k_p3(const P3Args a) {
   // phase profile (kProf builds only; thread 0, clock64): 0 fetch/issue, 1 wait, 2 rank, 3 bases+offsets, 4 stage, 5 store
   unsigned long long pacc[kProf ? 6 : 1] = {};
   long long tprev = kProf ? clock64() : 0;
@@ -1217,15 +1219,16 @@ __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
       }
     }
   };
-  constexpr int TT = W3 * 32;
+  constexpr int W3_ = WW3, TT = W3_ * 32, CAP3_ = W3_ * K3 * 32, CAP3P_ = CAP3_ + 8, CAP3L_ = CAP3_ + 16;
+  constexpr int WH3_ = W3_ / 2 + 1, W3P_ = W3_ + 1;
   extern __shared__ __align__(128) unsigned char smem[];
-  uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem);       // 2 * CAP3P
-  uint32_t* s_cnt = s_buf + 2 * CAP3P;                       // ML3 * WH3 (packed, digit-major)
-  uint32_t* s_scr = s_cnt + round4(ML3 * WH3);               // ML3 * W3P (safe)
-  uint32_t* s_dstart = s_scr + (kMode == kRankSafe ? round4(ML3 * W3P) : 0);
+  uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem);       // 2 * CAP3P_
+  uint32_t* s_cnt = s_buf + 2 * CAP3P_;                       // ML3 * WH3_ (packed, digit-major)
+  uint32_t* s_scr = s_cnt + round4(ML3 * WH3_);               // ML3 * W3P_ (safe)
+  uint32_t* s_dstart = s_scr + (kMode == kRankSafe ? round4(ML3 * W3P_) : 0);
   uint32_t* s_dtot = s_dstart + ML3;
   uint32_t* s_tmp = s_dtot + ML3;
-  uint8_t* s_lvb = reinterpret_cast<uint8_t*>(s_tmp + 40);  // kLv: 2 * CAP3L (16B aligned)
+  uint8_t* s_lvb = reinterpret_cast<uint8_t*>(s_tmp + 40);  // kLv: 2 * CAP3L_ (16B aligned)
   static_assert(!kLv || kPosFine, "digit bytes imply position-derived fine buckets");
   __shared__ __align__(8) uint64_t s_bar[2];
   __shared__ uint32_t s_uidx[2];
@@ -1234,7 +1237,7 @@ __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
   const uint32_t tid = threadIdx.x, lane = lane_id(), w = warp_id();
   const uint32_t sh = (w & 1) << 4;
   const uint32_t nun = *a.n_units;
-  zero_u32(s_cnt, round4(ML3 * WH3) + (kMode == kRankSafe ? round4(ML3 * W3P) : 0));
+  zero_u32(s_cnt, round4(ML3 * WH3_) + (kMode == kRankSafe ? round4(ML3 * W3P_) : 0));
   if (tid == 0) {
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
@@ -1251,11 +1254,11 @@ __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
       const uint32_t o8 = (uint32_t)(reinterpret_cast<uintptr_t>(gl) & 15);
       const uint32_t nb8 = (o8 + u.n + 15) & ~15u;
       mbar_arrive_expect_tx(&s_bar[b], full * 4 + nb8);
-      bulk_g2s(s_lvb + b * CAP3L, gl - o8, nb8, &s_bar[b]);
+      bulk_g2s(s_lvb + b * CAP3L_, gl - o8, nb8, &s_bar[b]);
     } else {
       mbar_arrive_expect_tx(&s_bar[b], full * 4);
     }
-    if (full) bulk_g2s(s_buf + b * CAP3P, gp - o, full * 4, &s_bar[b]);
+    if (full) bulk_g2s(s_buf + b * CAP3P_, gp - o, full * 4, &s_bar[b]);
   };
   // static round-robin over the units (they are many and bounded in size):
   // the next unit is known without a global atomic on the critical path
@@ -1276,7 +1279,7 @@ __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
     const uint32_t* gp = a.rec + u.start;
     const uint32_t o = align_items_u32(gp);
     const uint32_t full = (o + n) & ~3u;
-    uint32_t* buf = s_buf + b * CAP3P;
+    uint32_t* buf = s_buf + b * CAP3P_;
     const uint32_t ti = full + tid;
     const bool tail = tid < 4 && ti < o + n;
     uint32_t tv = 0;
@@ -1301,7 +1304,7 @@ __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
     }
     const bool wbnd = fnb <= seg0 + (K3 * 32 - 1);
     const uint32_t lvoff = (u.f0 & ((1u << a.gbits) - 1)) << a.c;
-    const uint8_t* lvb = s_lvb + b * CAP3L + (kLv ? (uint32_t)(reinterpret_cast<uintptr_t>(a.lv + u.start) & 15) : 0u);
+    const uint8_t* lvb = s_lvb + b * CAP3L_ + (kLv ? (uint32_t)(reinterpret_cast<uintptr_t>(a.lv + u.start) & 15) : 0u);
     uint32_t rr[K3], pk[K3];
     constexpr int kG3 = kPre ? kStageG : 1;
     if constexpr (kPre) {
@@ -1321,16 +1324,16 @@ __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
       } else {
         lv = valid ? (((r >> a.nbs) & a.lvmask) - lvoff) : 0u;
       }
-      pk[s] = (lv << 16) | rank_pk<kMode>(s_cnt + lv * WH3 + (w >> 1), s_scr + lv * W3P + w, sh, valid);
+      pk[s] = (lv << 16) | rank_pk<kMode>(s_cnt + lv * WH3_ + (w >> 1), s_scr + lv * W3P_ + w, sh, valid);
       rr[s] = r & a.src_mask;
     }
     __syncthreads();  // (B)
     tick(2);
-    flat_bases_pk<WH3>(s_cnt, (int)nloc, nullptr, nullptr, nullptr, s_tmp);
+    flat_bases_pk<WH3_>(s_cnt, (int)nloc, nullptr, nullptr, nullptr, s_tmp);
     {
       const uint64_t v0 = (uint64_t)u.f0 << a.c;
       for (uint32_t v = tid; v < nloc; v += TT)
-        if (v0 + v < a.V) a.t_offsets[v0 + v] = u.start + (s_cnt[v * WH3] & 0xffffu);
+        if (v0 + v < a.V) a.t_offsets[v0 + v] = u.start + (s_cnt[v * WH3_] & 0xffffu);
     }
     tick(3);
     uint32_t* t_e = a.t_edges + u.start;
@@ -1339,7 +1342,7 @@ __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
     for (int c = 0; c < K3; c += kG3) {  // base words of kG3 items loaded before their stores
       uint32_t bw[kG3];
 #pragma unroll
-      for (int q = 0; q < kG3; ++q) bw[q] = s_cnt[(pk[c + q] >> 16) * WH3 + (w >> 1)];
+      for (int q = 0; q < kG3; ++q) bw[q] = s_cnt[(pk[c + q] >> 16) * WH3_ + (w >> 1)];
 #pragma unroll
       for (int q = 0; q < kG3; ++q)
         if (seg0 + (c + q) * 32 + lane < n) buf[oo + ((bw[q] >> sh) & 0xffffu) + (pk[c + q] & 0xffffu)] = rr[c + q];
@@ -1358,7 +1361,7 @@ __global__ void __launch_bounds__(W3 * 32, 2) k_p3(const P3Args a) {
       const uint32_t tl = head + mid + tid;
       if (tl < n && tid < 4) t_e[tl] = buf[oo + tl];
     }
-    zero_u32(s_cnt, round4((int)nloc * WH3));  // rows >= nloc were never touched
+    zero_u32(s_cnt, round4((int)nloc * WH3_));  // rows >= nloc were never touched
     __syncthreads();  // (D)
     tick(5);
   }
@@ -1440,7 +1443,8 @@ struct Big3 {
   uint32_t pad;
 };
 __global__ void k_plan3(const uint64_t* __restrict__ fbase, uint32_t nfine, int sbits, Unit3* __restrict__ units,
-                        uint32_t* __restrict__ n_units, Big3* __restrict__ bigs, uint32_t* __restrict__ n_big) {
+                        uint32_t* __restrict__ n_units, Big3* __restrict__ bigs, uint32_t* __restrict__ n_big,
+                        uint32_t cap = CAP3) {
   const uint32_t G = 1u << sbits;
   const uint32_t grp = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t f_begin = grp * G;
@@ -1449,7 +1453,7 @@ __global__ void k_plan3(const uint64_t* __restrict__ fbase, uint32_t nfine, int 
   uint32_t f = f_begin;
   while (f < f_end) {
     const uint64_t s = fbase[f], sz = fbase[f + 1] - s;
-    if (sz > (uint64_t)CAP3) {
+    if (sz > (uint64_t)cap) {
       const uint32_t q = atomicAdd(n_big, 1u);
       Big3 bg;
       bg.start = s;
@@ -1464,7 +1468,7 @@ __global__ void k_plan3(const uint64_t* __restrict__ fbase, uint32_t nfine, int 
     uint32_t e = f + 1;
     while (e < f_end) {
       const uint64_t z = fbase[e + 1] - fbase[e];
-      if (z > (uint64_t)CAP3 || tot + z > (uint64_t)CAP3) break;
+      if (z > (uint64_t)cap || tot + z > (uint64_t)cap) break;
       tot += z;
       ++e;
     }
