@@ -375,6 +375,24 @@ int scan_u64_to_u64(const unsigned long long* in, uint64_t n, uint64_t* out, uin
 
 // CUDA-event timing of a call (stats != NULL): step marks plus begin/end of
 // the main kernels.  Events are created once per thread and reused.
+// Per-thread, per-device side stream and fork/join events (created once).
+int side_stream(cudaStream_t* s, cudaEvent_t* fork, cudaEvent_t* join) {
+  thread_local cudaStream_t t_s[64] = {};
+  thread_local cudaEvent_t t_f[64] = {}, t_j[64] = {};
+  int dev = 0;
+  GT_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return set_err(GT_ECUDA, "device ordinal %d out of range", dev);
+  if (!t_s[dev]) {
+    GT_CUDA(cudaStreamCreateWithFlags(&t_s[dev], cudaStreamNonBlocking));
+    GT_CUDA(cudaEventCreateWithFlags(&t_f[dev], cudaEventDisableTiming));
+    GT_CUDA(cudaEventCreateWithFlags(&t_j[dev], cudaEventDisableTiming));
+  }
+  *s = t_s[dev];
+  *fork = t_f[dev];
+  *join = t_j[dev];
+  return GT_OK;
+}
+
 struct Timer {
   static constexpr int kSteps = 6, kKern = 4;
   bool on = false;
@@ -405,13 +423,13 @@ struct Timer {
     if (on && n < kSteps) GT_CUDA(cudaEventRecord(ev[n++], st));
     return GT_OK;
   }
-  int kbegin(int k) {
-    if (on) GT_CUDA(cudaEventRecord(kev[2 * k], st));
+  int kbegin(int k, cudaStream_t s = nullptr) {
+    if (on) GT_CUDA(cudaEventRecord(kev[2 * k], s ? s : st));
     return GT_OK;
   }
-  int kend(int k) {
+  int kend(int k, cudaStream_t s = nullptr) {
     if (on) {
-      GT_CUDA(cudaEventRecord(kev[2 * k + 1], st));
+      GT_CUDA(cudaEventRecord(kev[2 * k + 1], s ? s : st));
       kset[k] = true;
     }
     return GT_OK;
@@ -1012,63 +1030,73 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
                                                                                    units, cnt + 0, bigs, cnt + 1,
                                                                                    (uint32_t)(w3 * K3 * 32));
   GT_LAUNCH_CHECK();
+  // the big-bucket chain (count / scans / place of fine buckets above the unit
+  // capacity) runs on a side stream, concurrently with the level-3 units:
+  // they touch disjoint fine buckets; its short scans overlap the units kernel
+  cudaStream_t sb = st;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  if (env_int("GT_FORK", 1)) {
+    if ((rc = side_stream(&sb, &ev_fork, &ev_join))) return rc;
+    GT_CUDA(cudaEventRecord(ev_fork, st));
+    GT_CUDA(cudaStreamWaitEvent(sb, ev_fork, 0));
+  }
   {
     uint32_t* bnt = reinterpret_cast<uint32_t*>(ws + q.o_bnt);
     uint64_t* bfirst = reinterpret_cast<uint64_t*>(ws + q.o_bfirst);
     const unsigned gb = (unsigned)std::min<uint64_t>((q.max_big + 255) / 256, (uint64_t)sms * 4);
     // exclusive scan over the real buckets (device count) -> bfirst[0..n_big]
     const uint64_t tiles = std::max<uint64_t>(1, (q.max_big + 1 + kScanTile - 1) / kScanTile);
-    GT_CUDA(cudaMemsetAsync(status, 0, tiles * 8, st));
-    GT_CUDA(cudaMemsetAsync(ctr, 0, 4, st));
-    GT_CUDA(cudaMemsetAsync(bnt, 0, (q.max_big + 1) * 4, st));
-    k_big_nt<<<gb, 256, 0, st>>>(bigs, cnt + 1, bnt);
-    k_scan_lookback<uint32_t><<<(unsigned)tiles, kScanThreads, 0, st>>>(bnt, q.max_big + 1, bfirst, 0, 1, status, ctr,
+    GT_CUDA(cudaMemsetAsync(status, 0, tiles * 8, sb));
+    GT_CUDA(cudaMemsetAsync(ctr, 0, 4, sb));
+    GT_CUDA(cudaMemsetAsync(bnt, 0, (q.max_big + 1) * 4, sb));
+    k_big_nt<<<gb, 256, 0, sb>>>(bigs, cnt + 1, bnt);
+    k_scan_lookback<uint32_t><<<(unsigned)tiles, kScanThreads, 0, sb>>>(bnt, q.max_big + 1, bfirst, 0, 1, status, ctr,
                                                                          cnt + 1, 1);
     GT_LAUNCH_CHECK();
-    k_big_write<<<gb, 256, 0, st>>>(bigs, cnt + 1, bfirst, p.c, tiles3, cnt + 2, seg3);
+    k_big_write<<<gb, 256, 0, sb>>>(bigs, cnt + 1, bfirst, p.c, tiles3, cnt + 2, seg3);
     GT_LAUNCH_CHECK();
   }
   {
     const unsigned gt3 = (unsigned)std::min<uint64_t>(q.max_t3, (uint64_t)sms * 8);
-    if (p.wide) k_cnt_lv<<<gt3, 512, (size_t)Dc * 4, st>>>(r2lv, tiles3, cnt + 2, Dc, cnt3);
-    else k_cnt_rec<<<gt3, 512, (size_t)Dc * 4, st>>>(r2, tiles3, cnt + 2, Dc, DigSM{p.nbs, (uint32_t)(Dc - 1)}, cnt3);
+    if (p.wide) k_cnt_lv<<<gt3, 512, (size_t)Dc * 4, sb>>>(r2lv, tiles3, cnt + 2, Dc, cnt3);
+    else k_cnt_rec<<<gt3, 512, (size_t)Dc * 4, sb>>>(r2, tiles3, cnt + 2, Dc, DigSM{p.nbs, (uint32_t)(Dc - 1)}, cnt3);
     GT_LAUNCH_CHECK();
     {  // scan only the real tiles' rows: n = n_tiles3 * Dc (device count)
       const uint64_t n3 = q.max_t3 * (uint64_t)Dc;
       const uint64_t tiles = std::max<uint64_t>(1, (n3 + kScanTile - 1) / kScanTile);
-      GT_CUDA(cudaMemsetAsync(status, 0, tiles * 8, st));
-      GT_CUDA(cudaMemsetAsync(ctr, 0, 4, st));
-      k_scan_lookback<uint32_t><<<(unsigned)tiles, kScanThreads, 0, st>>>(cnt3, n3, base3, 0, 0, status, ctr, cnt + 2,
+      GT_CUDA(cudaMemsetAsync(status, 0, tiles * 8, sb));
+      GT_CUDA(cudaMemsetAsync(ctr, 0, 4, sb));
+      k_scan_lookback<uint32_t><<<(unsigned)tiles, kScanThreads, 0, sb>>>(cnt3, n3, base3, 0, 0, status, ctr, cnt + 2,
                                                                            (uint64_t)Dc);
       GT_LAUNCH_CHECK();
     }
-    k_segfix<<<(unsigned)std::min<uint64_t>(q.max_big, (uint64_t)sms * 8), 512, 0, st>>>(seg3, cnt + 1, Dc, base3,
+    k_segfix<<<(unsigned)std::min<uint64_t>(q.max_big, (uint64_t)sms * 8), 512, 0, sb>>>(seg3, cnt + 1, Dc, base3,
                                                                                       t_offsets, V, err);
     GT_LAUNCH_CHECK();
     DecR2 dec;
     dec.nbs = p.nbs;
     dec.src_mask = (p.nbs >= 32 || p.wide) ? 0xffffffffu : (uint32_t)((1ull << p.nbs) - 1);
     dec.maskC = (uint32_t)(Dc - 1);
-    if ((rc = tm.kbegin(3))) return rc;
+    if ((rc = tm.kbegin(3, sb))) return rc;
     if (p.wide) {
       const size_t sm = smem_p2(Dc, kMode, 16, kIoLv);
       if ((rc = set_smem(k_p2<kMode, DecR2, 16, false, kIoLv>, sm))) return rc;
       const unsigned g = persistent_grid(k_p2<kMode, DecR2, 16, false, kIoLv>, T, sm, q.max_t3);
-      k_p2<kMode, DecR2, 16, false, kIoLv><<<g, T, sm, st>>>(r2, tiles3, cnt + 2, Dc, dec, base3, t_edges, nullptr,
+      k_p2<kMode, DecR2, 16, false, kIoLv><<<g, T, sm, sb>>>(r2, tiles3, cnt + 2, Dc, dec, base3, t_edges, nullptr,
                                                               r2lv, nullptr);
     } else {
       const size_t sm = smem_p2(Dc, kMode, 16);
       if ((rc = set_smem(k_p2<kMode, DecR2, 16>, sm))) return rc;
       const unsigned g = persistent_grid(k_p2<kMode, DecR2, 16>, T, sm, q.max_t3);
       if (pre & 4) {
-        k_p2<kMode, DecR2, 16><<<g, T, sm, st>>>(r2, tiles3, cnt + 2, Dc, dec, base3, t_edges);
+        k_p2<kMode, DecR2, 16><<<g, T, sm, sb>>>(r2, tiles3, cnt + 2, Dc, dec, base3, t_edges);
       } else {
         if ((rc = set_smem(k_p2<kMode, DecR2, 16, false, kIoPlain, false>, sm))) return rc;
-        k_p2<kMode, DecR2, 16, false, kIoPlain, false><<<g, T, sm, st>>>(r2, tiles3, cnt + 2, Dc, dec, base3, t_edges);
+        k_p2<kMode, DecR2, 16, false, kIoPlain, false><<<g, T, sm, sb>>>(r2, tiles3, cnt + 2, Dc, dec, base3, t_edges);
       }
     }
     GT_LAUNCH_CHECK();
-    if ((rc = tm.kend(3))) return rc;
+    if ((rc = tm.kend(3, sb))) return rc;
   }
   {
     P3Args a;
@@ -1123,6 +1151,10 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
     if (rc) return rc;
     GT_LAUNCH_CHECK();
     if ((rc = tm.kend(2))) return rc;
+  }
+  if (sb != st) {
+    GT_CUDA(cudaEventRecord(ev_join, sb));
+    GT_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
   }
   k_set_u64<<<1, 1, 0, st>>>(t_offsets + V, E);
   GT_LAUNCH_CHECK();
