@@ -2,13 +2,20 @@
 """Per-step and per-kernel DRAM traffic (ncu dram__bytes_read.sum + write.sum)
 from an ncu --csv launch list of `bench.py --steps 1`: the last complete
 transpose in the list (launches from one k_set_u32 to the next).
-Usage: make_traffic.py launches.csv config_name [profiles/ncu_traffic.json]"""
+Usage: make_traffic.py launches.csv config [profiles/ncu_traffic.json]; config = C1..C5 or the
+workload name bench.py looks up (gen.CONFIGS[...].name)."""
 import json
 import sys
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parent))
 from launches_summary import load  # noqa: E402
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+from paper_2501_06872_b200 import gen  # noqa: E402
+
+if sys.argv[2] in gen.CONFIGS:
+    sys.argv[2] = gen.CONFIGS[sys.argv[2]].name
 
 out = load(sys.argv[1])
 keys = list(out.keys())
