@@ -378,7 +378,7 @@ def test_rmat_lean_generator_matches_pairs_path():
 @pytest.mark.slow
 def test_full_size_c5():
     """Config C5 (R-MAT scale 29, edge factor 16, IDs permuted: 8.6e9 edges, E >= 2^32)
-    on one GPU: lean generation, transpose (8-byte-record pipeline), and the C
+    on one GPU: lean generation, transpose (wide v3 form), and the C
     oracle on the host, bit for bit."""
     import gc
 
