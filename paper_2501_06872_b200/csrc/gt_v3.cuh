@@ -561,6 +561,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
   __shared__ uint64_t s_wlo;
   __shared__ uint32_t s_wn;
   __shared__ uint32_t s_last_src;
+  __shared__ uint32_t s_lastm[32];
 
   const uint32_t tid = threadIdx.x, lane = lane_id(), w = warp_id();
   const uint32_t sh = (w & 1) << 4;
@@ -575,6 +576,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
   for (int j = tid; j <= nplace; j += T1_) s_psrc[j] = a.psrc[gp0 + j];
   zero_u32(s_cnt, round4(D * WH1_) + (kMode == kRankSafe ? round4(D * WP1_) : 0));
   zero_u32(reinterpret_cast<uint32_t*>(s_mark), PT / 2);
+  if (tid < 32) s_lastm[tid] = 0;
   if (tid == 0) {
     mbar_init(&s_bar, 1);
     fence_mbar_init();
@@ -647,13 +649,24 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
     if (!wide) {
       for (uint32_t v = s0 + 1 + tid; v <= s1; v += T1_) {
         const uint64_t p = off_at(v) - gi0;
-        if (p < n && off_at((uint64_t)v + 1) > off_at(v)) s_mark[p] = (uint16_t)(v - s0);
+        if (p < n && off_at((uint64_t)v + 1) > off_at(v)) {
+          s_mark[p] = (uint16_t)(v - s0);
+          atomicMax(&s_lastm[p / (K * 32)], v - s0);  // last source starting in each warp's segment
+        }
       }
     }
     __syncthreads();  // (A) tile landed, marks placed
 
     const uint32_t iw = w * (K * 32);
-    uint32_t carry = owner_search(s0, s1, gi0 + iw, off_at);
+    // owner of the warp's first item: the last source starting in an earlier segment (else s0)
+    uint32_t carry;
+    if (!wide) {
+      uint32_t mx = 0;
+      for (uint32_t k = 0; k < w; ++k) mx = max(mx, s_lastm[k]);
+      carry = s0 + mx;
+    } else {
+      carry = owner_search(s0, s1, gi0 + iw, off_at);
+    }
     const uint32_t le = lanemask_le();
     uint32_t pay[K], pk[K];
     // pay[s] / pk[s] first hold the slot's destination and mark: all loads of
@@ -728,6 +741,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
     if constexpr (kW64) writeout_tag<T1_, PT>(a.out, s_buf, s_tag, s_g64, n);
     else writeout_tag<T1_, PT>(a.out, s_buf, s_tag, s_delta, n);
     zero_u32(reinterpret_cast<uint32_t*>(s_mark), PT / 2);
+    if (tid < 32) s_lastm[tid] = 0;
     zero_u32(s_cnt, round4(D * WH1_));
     if constexpr (!kW64)
       for (int d = tid; d < D; d += T1_) s_gcur[d] += s_dtot[d];
