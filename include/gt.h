@@ -12,6 +12,7 @@
  *                        hlh.py:441-588, baselines.py:457-475); output equals
  *                        transpose_oracle (graph.py:136-148) bit for bit.
  *   gt_transpose_host    same, host buffers in and out (H2D + kernels + D2H).
+ *   gt_transpose_host_many  a batch of host transposes, copies overlapped with the kernels.
  *   gt_prefix_sum        prefix_sum_parallel (baselines.py:116-127).
  *   gt_edge_balanced_bounds  edge_balanced_vertex_bounds (_nb.py:118-132),
  *                        the source-range sharding rule for multi-GPU runs.
@@ -93,6 +94,18 @@ int gt_transpose_host(const uint64_t *h_offsets, const uint32_t *h_edges,
                       uint64_t num_vertices, uint64_t num_edges,
                       uint64_t *h_t_offsets, uint32_t *h_t_edges,
                       int device, gt_stats *stats);
+
+/* A batch of `count` host-resident transposes on `device`, pipelined: graph i+1's
+ * H2D copy runs while graph i is transposed and graph i-1's result is copied
+ * back (three streams, two device buffer sets sized for the largest graph), so
+ * with pinned host buffers both PCIe directions and the kernels overlap.  Same
+ * per-graph contract and results as gt_transpose_host; `stats` describes the
+ * last graph.  Replaces a loop of transpose_atomic / transpose_potra calls over
+ * several graphs (baselines.py:168-209, hlh.py:441-588). */
+int gt_transpose_host_many(int count, const uint64_t *const *h_offsets, const uint32_t *const *h_edges,
+                           const uint64_t *num_vertices, const uint64_t *num_edges,
+                           uint64_t *const *h_t_offsets, uint32_t *const *h_t_edges,
+                           int device, gt_stats *stats);
 
 /* Exclusive prefix sum of uint32 counts into uint64[n+1] (out[n] = total). */
 int gt_prefix_sum(const uint32_t *counts, uint64_t n, uint64_t *out, void *stream);

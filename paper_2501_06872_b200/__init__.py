@@ -17,6 +17,7 @@ from .transpose import (
     transpose_atomic,
     transpose_device,
     transpose_gpu,
+    transpose_gpu_many,
     transpose_potra,
 )
 from .verify import VerifyReport, sort_neighbor_lists, verify_output
@@ -29,6 +30,7 @@ __all__ = [
     "CsrGraph",
     "TransposeOutput",
     "transpose_gpu",
+    "transpose_gpu_many",
     "transpose_potra",
     "transpose_atomic",
     "transpose_device",

@@ -61,6 +61,7 @@ SYMBOLS = {
     "gt_workspace_size": (_int, [_u64, _u64, ctypes.POINTER(_u64)]),
     "gt_transpose": (_int, [_vp, _vp, _u64, _u64, _vp, _vp, _vp, _u64, _vp, _stats_p]),
     "gt_transpose_host": (_int, [_vp, _vp, _u64, _u64, _vp, _vp, _int, _stats_p]),
+    "gt_transpose_host_many": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _int, _stats_p]),
     "gt_prefix_sum": (_int, [_vp, _u64, _vp, _vp]),
     "gt_edge_balanced_bounds": (_int, [_vp, _u64, _i64, _vp]),
     "gt_selftest_rank_order": (_int, [_u64, ctypes.POINTER(_u64)]),

@@ -1332,6 +1332,89 @@ int gt_transpose_host(const uint64_t* h_offsets, const uint32_t* h_edges, uint64
   return GT_OK;
 }
 
+int gt_transpose_host_many(int count, const uint64_t* const* h_offsets, const uint32_t* const* h_edges,
+                           const uint64_t* Vs, const uint64_t* Es, uint64_t* const* h_t_offsets,
+                           uint32_t* const* h_t_edges, int device, gt_stats* stats) {
+  if (count < 0) return set_err(GT_EINVAL, "negative batch size %d", count);
+  if (count == 0) return GT_OK;
+  if (!h_offsets || !h_edges || !Vs || !Es || !h_t_offsets || !h_t_edges) return set_err(GT_EINVAL, "NULL array");
+  uint64_t vmax = 0, emax = 0;
+  for (int i = 0; i < count; ++i) {
+    if (!h_offsets[i] || !h_t_offsets[i] || (Es[i] && (!h_edges[i] || !h_t_edges[i])))
+      return set_err(GT_EINVAL, "NULL host array in graph %d", i);
+    vmax = std::max(vmax, Vs[i]);
+    emax = std::max(emax, Es[i]);
+  }
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) return set_err(GT_ENODEV, "no CUDA device");
+  if (device < 0 || device >= n || device >= 64) return set_err(GT_EINVAL, "bad device %d", device);
+  GT_CUDA(cudaSetDevice(device));
+  // two device buffer sets (input + output of one graph each), cached per device
+  static Cache s_io2[64];
+  static cudaStream_t s_sin[64], s_scmp[64], s_sout[64];
+  static cudaEvent_t s_ev[64][6];  // in_done[2], cmp_done[2], out_done[2]
+  static std::mutex s_mu;
+  std::lock_guard<std::mutex> lk(s_mu);
+  if (!s_sin[device]) {
+    GT_CUDA(cudaStreamCreateWithFlags(&s_sin[device], cudaStreamNonBlocking));
+    GT_CUDA(cudaStreamCreateWithFlags(&s_scmp[device], cudaStreamNonBlocking));
+    GT_CUDA(cudaStreamCreateWithFlags(&s_sout[device], cudaStreamNonBlocking));
+    for (auto& ev : s_ev[device]) GT_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  }
+  cudaStream_t sin = s_sin[device], scmp = s_scmp[device], sout = s_sout[device];
+  cudaEvent_t* ev = s_ev[device];
+  const uint64_t b_off = align_up((vmax + 1) * 8, 256), b_e = align_up(std::max<uint64_t>(emax, 1) * 4, 256);
+  const uint64_t set_bytes = 2 * b_off + 2 * b_e;
+  void* base = nullptr;
+  int rc = cache_get(s_io2[device], 2 * set_bytes, &base);
+  if (rc) return rc;
+  auto buf = [&](int slot, int which) -> unsigned char* {  // 0 off, 1 toff, 2 edges, 3 t_edges
+    unsigned char* b = static_cast<unsigned char*>(base) + slot * set_bytes;
+    const uint64_t o[4] = {0, b_off, 2 * b_off, 2 * b_off + b_e};
+    return b + o[which];
+  };
+  // H2D of graph i (input set i & 1 is free once graph i-2's transpose has read it)
+  auto h2d = [&](int i) -> int {
+    const int slot = i & 1;
+    if (i >= 2) GT_CUDA(cudaStreamWaitEvent(sin, ev[2 + slot], 0));
+    GT_CUDA(cudaMemcpyAsync(buf(slot, 0), h_offsets[i], (Vs[i] + 1) * 8, cudaMemcpyHostToDevice, sin));
+    if (Es[i]) GT_CUDA(cudaMemcpyAsync(buf(slot, 2), h_edges[i], Es[i] * 4, cudaMemcpyHostToDevice, sin));
+    GT_CUDA(cudaEventRecord(ev[slot], sin));
+    return GT_OK;
+  };
+  if ((rc = h2d(0))) return rc;
+  for (int i = 0; i < count; ++i) {
+    const int slot = i & 1;
+    const uint64_t V = Vs[i], E = Es[i];
+    // one graph ahead: graph i+1's copy-in overlaps graph i's kernels and graph i-1's copy-out
+    // (gt_transpose returns after its kernels, so graph i-1's transpose is done here)
+    if (i + 1 < count && (rc = h2d(i + 1))) return rc;
+    uint64_t* d_off = reinterpret_cast<uint64_t*>(buf(slot, 0));
+    uint64_t* d_toff = reinterpret_cast<uint64_t*>(buf(slot, 1));
+    uint32_t* d_e = reinterpret_cast<uint32_t*>(buf(slot, 2));
+    uint32_t* d_te = reinterpret_cast<uint32_t*>(buf(slot, 3));
+    // output set free once graph i-2's result has been copied back
+    GT_CUDA(cudaStreamWaitEvent(scmp, ev[slot], 0));
+    if (i >= 2) GT_CUDA(cudaStreamWaitEvent(scmp, ev[4 + slot], 0));
+    rc = gt_transpose(d_off, d_e, V, E, d_toff, d_te, nullptr, 0, scmp, (i == count - 1) ? stats : nullptr);
+    if (rc) {
+      cudaStreamSynchronize(sin);
+      cudaStreamSynchronize(sout);
+      return rc;
+    }
+    GT_CUDA(cudaEventRecord(ev[2 + slot], scmp));
+    GT_CUDA(cudaStreamWaitEvent(sout, ev[2 + slot], 0));
+    GT_CUDA(cudaMemcpyAsync(h_t_offsets[i], d_toff, (V + 1) * 8, cudaMemcpyDeviceToHost, sout));
+    if (E) GT_CUDA(cudaMemcpyAsync(h_t_edges[i], d_te, E * 4, cudaMemcpyDeviceToHost, sout));
+    GT_CUDA(cudaEventRecord(ev[4 + slot], sout));
+  }
+  GT_CUDA(cudaStreamSynchronize(sin));
+  GT_CUDA(cudaStreamSynchronize(scmp));
+  GT_CUDA(cudaStreamSynchronize(sout));
+  return GT_OK;
+}
+
 int gt_prefix_sum(const uint32_t* counts, uint64_t n, uint64_t* out, void* stream) {
   if (!out || (n && !counts)) return set_err(GT_EINVAL, "NULL array");
   cudaStream_t st = static_cast<cudaStream_t>(stream);

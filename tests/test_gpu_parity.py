@@ -183,6 +183,28 @@ def test_host_entry_point_e2e():
     assert np.array_equal(toff, o) and np.array_equal(tedg, e)
 
 
+def test_host_batch_entry_point():
+    """gt_transpose_host_many: a batch of host graphs of different sizes (an
+    empty one and a hub-heavy one included), copies overlapped with kernels;
+    every result equals the oracle."""
+    from paper_2501_06872_b200 import CsrGraph, transpose_gpu_many
+
+    rng = np.random.default_rng(12)
+    gs = [random_graph(rng, max_vertices=20_000, max_edges=300_000) for _ in range(3)]
+    gs.append(CsrGraph(17, 0, np.zeros(18, np.uint64), np.zeros(0, np.uint32)))
+    src = rng.integers(0, 50_000, 1_500_000)
+    dst = np.minimum((50_000 * rng.random(1_500_000) ** 5).astype(np.int64), 49_999)
+    gs.append(CsrGraph.from_edge_pairs(src, dst, 50_000))
+    gs.append(gs[0])
+    outs = transpose_gpu_many(gs)
+    assert len(outs) == len(gs)
+    for i, (g, out) in enumerate(zip(gs, outs)):
+        o, e = oracle.transpose_c(g.offsets, g.edges, g.num_vertices)
+        assert np.array_equal(out.graph.offsets, o) and np.array_equal(out.graph.edges, e), i
+        assert out.sorted and out.method == "gpu"
+    assert transpose_gpu_many([]) == []
+
+
 @pytest.mark.parametrize("parts", [1, 2, 3, 8])
 def test_shard_pipeline_single_gpu(parts):
     """The multi-GPU building blocks, run for every rank on one GPU in sequence
