@@ -1144,6 +1144,11 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
         rc = pos_fine ? go3(k_p3<kMode, true, false, false, true, 32>) : go3(k_p3<kMode, false, false, false, true, 32>);
       else
         rc = pos_fine ? go3(k_p3<kMode, true, false, false, false, 32>) : go3(k_p3<kMode, false, false, false, false, 32>);
+    } else if (env_int("GT_BAL3", 1) == 0) {  // A/B: fixed 512 positions per warp
+      if ((pre & 8) || ((pre & 16) && pos_fine))
+        rc = pos_fine ? go3(k_p3<kMode, true, false, false, true, W3, false>) : go3(k_p3<kMode, false, false, false, true, W3, false>);
+      else
+        rc = pos_fine ? go3(k_p3<kMode, true, false, false, false, W3, false>) : go3(k_p3<kMode, false, false, false, false, W3, false>);
     } else {
       if ((pre & 8) || ((pre & 16) && pos_fine)) rc = pos_fine ? go3(k_p3<kMode, true>) : go3(k_p3<kMode, false>);
       else rc = pos_fine ? go3(k_p3<kMode, true, false, false, false>) : go3(k_p3<kMode, false, false, false, false>);

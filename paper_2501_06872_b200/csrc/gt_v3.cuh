@@ -1219,7 +1219,11 @@ inline size_t smem_p3(int mode, bool lv = false, int ww = W3) {
 // kPosFine: the record's fine bucket inside the unit comes from its position
 // (R2 has no room for fine-digit bits); else from the record's bits.
 // kLv (requires kPosFine): the low digit comes from the separate byte array.
-template <int kMode, bool kPosFine, bool kProf = false, bool kLv = false, bool kPre = true, int WW3 = W3>
+// kBal: a unit's n records are split evenly over the warps (ceil(n / 512) slots
+// each, consecutive ranges in warp order) and warps skip their empty slots;
+// otherwise every warp owns 512 positions and partial units run predicated slots.
+template <int kMode, bool kPosFine, bool kProf = false, bool kLv = false, bool kPre = true, int WW3 = W3,
+          bool kBal = true>
 __global__ void __launch_bounds__(WW3 * 32, WW3 > 16 ? 1 : 2) k_p3(const P3Args a) {
   // phase profile (kProf builds only; thread 0, clock64): 0 fetch/issue, 1 wait, 2 rank, 3 bases+offsets, 4 stage, 5 store
   unsigned long long pacc[kProf ? 6 : 1] = {};
@@ -1308,7 +1312,8 @@ __global__ void __launch_bounds__(WW3 * 32, WW3 > 16 ? 1 : 2) k_p3(const P3Args 
     __syncthreads();  // (A)
     tick(1);
     const uint32_t nloc = u.nf << a.c;
-    const uint32_t seg0 = w * (K3 * 32);
+    const uint32_t per = kBal ? ((n + TT - 1) / TT) * 32 : (uint32_t)(K3 * 32);  // positions per warp
+    const uint32_t seg0 = w * per;
     // local vertex = (fine bucket inside the unit, from the record's position) << c | low digit
     auto bnd_at = [&](uint32_t kk) -> uint32_t { return s_fb[kk - 1]; };
     uint32_t fcur = 0, fnb = 0xffffffffu;
@@ -1316,17 +1321,21 @@ __global__ void __launch_bounds__(WW3 * 32, WW3 > 16 ? 1 : 2) k_p3(const P3Args 
       fcur = owner_search(0u, nbt, (uint64_t)seg0, [&](uint64_t kk) -> uint64_t { return s_fb[kk - 1]; });
       fnb = (fcur + 1 <= nbt) ? s_fb[fcur] : 0xffffffffu;
     }
-    const bool wbnd = fnb <= seg0 + (K3 * 32 - 1);
+    const bool wbnd = fnb <= seg0 + (per - 1);
     const uint32_t lvoff = (u.f0 & ((1u << a.gbits) - 1)) << a.c;
     const uint8_t* lvb = s_lvb + b * CAP3L_ + (kLv ? (uint32_t)(reinterpret_cast<uintptr_t>(a.lv + u.start) & 15) : 0u);
     uint32_t rr[K3], pk[K3];
     constexpr int kG3 = kPre ? kStageG : 1;
     if constexpr (kPre) {
 #pragma unroll
-      for (int s = 0; s < K3; ++s) rr[s] = buf[o + seg0 + s * 32 + lane];  // all loads before the first rank atomic
+      for (int s = 0; s < K3; ++s) {  // all loads before the first rank atomic
+        if (kBal && (uint32_t)s * 32 >= per) break;
+        rr[s] = buf[o + seg0 + s * 32 + lane];
+      }
     }
 #pragma unroll
     for (int s = 0; s < K3; ++s) {
+      if (kBal && (uint32_t)s * 32 >= per) break;
       const uint32_t i = seg0 + s * 32 + lane;
       const bool valid = i < n;
       const uint32_t r = valid ? (kPre ? rr[s] : buf[o + i]) : 0u;
@@ -1354,12 +1363,15 @@ __global__ void __launch_bounds__(WW3 * 32, WW3 > 16 ? 1 : 2) k_p3(const P3Args 
     const uint32_t oo = align_items_u32(t_e);  // staging offset matching the output's 16B alignment
 #pragma unroll
     for (int c = 0; c < K3; c += kG3) {  // base words of kG3 items loaded before their stores
+      if (kBal && (uint32_t)c * 32 >= per) break;
       uint32_t bw[kG3];
 #pragma unroll
-      for (int q = 0; q < kG3; ++q) bw[q] = s_cnt[(pk[c + q] >> 16) * WH3_ + (w >> 1)];
+      for (int q = 0; q < kG3; ++q)
+        if (!kBal || (uint32_t)(c + q) * 32 < per) bw[q] = s_cnt[(pk[c + q] >> 16) * WH3_ + (w >> 1)];
 #pragma unroll
       for (int q = 0; q < kG3; ++q)
-        if (seg0 + (c + q) * 32 + lane < n) buf[oo + ((bw[q] >> sh) & 0xffffu) + (pk[c + q] & 0xffffu)] = rr[c + q];
+        if ((!kBal || (uint32_t)(c + q) * 32 < per) && seg0 + (c + q) * 32 + lane < n)
+          buf[oo + ((bw[q] >> sh) & 0xffffu) + (pk[c + q] & 0xffffu)] = rr[c + q];
     }
     fence_proxy_async_smem();
     __syncthreads();  // (C)
