@@ -501,15 +501,16 @@ constexpr int kStageG = 8;
 template <int G, int K_, class Tag>
 __device__ __forceinline__ void stage_tag(const uint32_t (&pk)[K_], const uint32_t (&pay)[K_], const uint32_t* cnt,
                                           int whn, uint32_t w, uint32_t sh, uint32_t* buf, Tag* tag, uint32_t lim,
-                                          uint32_t i0) {
+                                          uint32_t i0, uint32_t per = K_ * 32) {
 #pragma unroll
   for (int c = 0; c < K_; c += G) {
+    if ((uint32_t)c * 32 >= per) break;  // per: positions of this warp (slots beyond hold nothing)
     uint32_t bw[G];
 #pragma unroll
-    for (int q = 0; q < G; ++q) bw[q] = cnt[(pk[c + q] >> 16) * whn + (w >> 1)];
+    for (int q = 0; q < G; ++q) bw[q] = cnt[(pk[c + q] >> 16) * whn + (w >> 1)];  // (unused slots: pk = 0)
 #pragma unroll
     for (int q = 0; q < G; ++q) {
-      if (lim == 0xffffffffu || i0 + (c + q) * 32 < lim) {
+      if ((uint32_t)(c + q) * 32 < per && (lim == 0xffffffffu || i0 + (c + q) * 32 < lim)) {
         const uint32_t pos = ((bw[q] >> sh) & 0xffffu) + (pk[c + q] & 0xffffu);
         buf[pos] = pay[c + q];
         tag[pos] = (Tag)(pk[c + q] >> 16);
@@ -1086,7 +1087,12 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
       __syncthreads();  // (A)
       tick(1);
 
-      const uint32_t iw = w * (K * 32);
+      // level-3 big buckets (many partial tiles): a partial tile's records are split evenly over
+      // the warps (consecutive ranges in warp order) and warps skip the slots beyond their range
+      // (measured: big buckets 0.778 -> 0.765 ms on C3; level 2 slower with it, 2.11 -> 2.16 ms)
+      constexpr bool kBal2 = Dec::kMatchRank;
+      const uint32_t per = (!kBal2 || n == (uint32_t)PT) ? (uint32_t)(K * 32) : ((n + T2_ - 1) / T2_) * 32;
+      const uint32_t iw = w * per;
       const uint32_t rel0 = (uint32_t)jj * PT;  // tile-relative position of item 0
       uint32_t cur = 0, nb = 0xffffffffu;
       auto bnd_at = [&](uint32_t kk) -> uint32_t {  // kk in [1, nbt]
@@ -1098,12 +1104,16 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
           nb = (cur + 1 <= nbt) ? bnd_at(cur + 1) : 0xffffffffu;
         }
       }
-      // warps whose 512 items hold no source-high boundary keep h constant
-      const bool wbnd = nb <= rel0 + iw + (K * 32 - 1);
+      // warps whose items hold no source-high boundary keep h constant
+      const bool wbnd = nb <= rel0 + iw + (per - 1);
       const uint32_t o8 = (kIO == kIoLv) ? (uint32_t)(reinterpret_cast<uintptr_t>(lv_in + pt) & 15) : 0u;
       // pk = digit << 16 | rank; kIoSplit: low-digit byte << 24 | digit << 13 | rank (rank < 8192, digit < 2048)
       constexpr int kDS = (kIO == kIoSplit) ? 13 : 16;
       uint32_t pay[K], pk[K];
+      if (kBal2 && n != (uint32_t)PT) {
+#pragma unroll
+        for (int s = 0; s < K; ++s) pk[s] = 0;  // slots a warp skips stage nothing
+      }
       auto slot = [&](int s, bool valid) {  // pay[s] holds the slot's record (loaded below)
         const uint32_t i0 = iw + s * 32, i = i0 + lane;
         const uint32_t r = valid ? (kPre ? pay[s] : s_buf[o + i]) : 0u;
@@ -1125,14 +1135,17 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
       };
       if constexpr (kPre) {
 #pragma unroll
-        for (int s = 0; s < K; ++s) pay[s] = s_buf[o + iw + s * 32 + lane];
+        for (int s = 0; s < K; ++s) pay[s] = s_buf[o + iw + s * 32 + lane];  // in bounds: iw + K * 32 <= PT
       }
       if (n == (uint32_t)PT) {
 #pragma unroll
         for (int s = 0; s < K; ++s) slot(s, true);
       } else {
 #pragma unroll
-        for (int s = 0; s < K; ++s) slot(s, iw + s * 32 + lane < n);
+        for (int s = 0; s < K; ++s) {
+          if (kBal2 && (uint32_t)s * 32 >= per) break;
+          slot(s, iw + s * 32 + lane < n);
+        }
       }
       __syncthreads();  // (B)
       tick(2);
@@ -1145,11 +1158,12 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
         flat_bases_pk<WH2_>(s_cnt, D, s_gcur, s_dtot, s_delta, s_tmp);
       tick(3);
       if constexpr (kIO != kIoSplit) {
-        stage_tag<kPre ? kStageG : 1, K>(pk, pay, s_cnt, WH2_, w, sh, s_buf, s_tag, (n == (uint32_t)PT) ? 0xffffffffu : n, iw + lane);
+        stage_tag<kPre ? kStageG : 1, K>(pk, pay, s_cnt, WH2_, w, sh, s_buf, s_tag, (n == (uint32_t)PT) ? 0xffffffffu : n, iw + lane,
+                                         per);
       } else {
 #pragma unroll
       for (int s = 0; s < K; ++s) {
-        if (n == (uint32_t)PT || iw + s * 32 + lane < n) {
+        if (n == (uint32_t)PT || ((uint32_t)s * 32 < per && iw + s * 32 + lane < n)) {
           const uint32_t d = (pk[s] >> kDS) & ((kIO == kIoSplit) ? 0x7ffu : 0xffffu);
           const uint32_t pos = ((s_cnt[d * WH2_ + (w >> 1)] >> sh) & 0xffffu) + (pk[s] & ((1u << kDS) - 1));
           s_buf[pos] = pay[s];
