@@ -431,3 +431,37 @@ def test_full_size_c5():
     gc.collect()
     assert np.array_equal(got_off, o)
     assert np.array_equal(got_edg, e)
+
+
+@pytest.mark.parametrize("env", [
+    {"GT_W1": "16"}, {"GT_W1": "32"}, {"GT_K1": "16"}, {"GT_W3": "32"}, {"GT_PRE": "30"}, {"GT_PRE": "0"},
+    {"GT_FORK": "0"}, {"GT_BAL3": "0"}, {"GT_OCC": "1"}, {"GT_K2": "32", "GT_W2": "16"},
+    {"GT_SPLIT": "6,6,6"}, {"GT_WIDE": "1", "GT_W1W": "8", "GT_W2W": "8"},
+])
+def test_kernel_variants(monkeypatch, golden_cases, env):
+    """Every tile-shape / occupancy / scheduling variant kept as a measured
+    alternative stays bit-exact: goldens, random graphs and a
+    hub-heavy graph (level-3 big-bucket path), against the oracle."""
+    from paper_2501_06872_b200 import CsrGraph, transpose_gpu
+
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    for name in sorted(golden_cases)[:20]:
+        c = golden_cases[name]
+        out = transpose_gpu(_graph(c["nv"], c["off"], c["edg"]))
+        assert np.array_equal(out.graph.offsets, c["toff"]), name
+        assert np.array_equal(out.graph.edges, c["tedg"]), name
+    rng = np.random.default_rng(77)
+    for i in range(6):
+        g = random_graph(rng, max_vertices=50_000, max_edges=400_000)
+        out = transpose_gpu(g)
+        o, e = oracle.transpose_c(g.offsets, g.edges, g.num_vertices)
+        assert np.array_equal(out.graph.offsets, o) and np.array_equal(out.graph.edges, e), i
+    nv, ne = 1 << 18, 1 << 23
+    src = np.sort(rng.integers(0, nv, ne))
+    dst = np.minimum((nv * rng.random(ne) ** 6).astype(np.int64), nv - 1)
+    g = CsrGraph.from_edge_pairs(src, dst, nv)
+    out = transpose_gpu(g)
+    o, e = oracle.transpose_c(g.offsets, g.edges, nv)
+    assert np.array_equal(out.graph.offsets, o) and np.array_equal(out.graph.edges, e)
+    assert out.details["big_buckets"] > 0 or env.get("GT_WIDE") == "1"
