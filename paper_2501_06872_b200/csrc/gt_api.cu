@@ -1019,7 +1019,7 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
     GT_LAUNCH_CHECK();
     if ((rc = tm.kend(1))) return rc;
   }
-  launches += 5;
+  launches += 6;  // coarse tiles, l2 tiles, count, scan, segfix, place
   if ((rc = tm.mark())) return rc;
   // ---- step 3: level 3 (units of small fine buckets; tiled count/scan/place for big ones)
   k_set_u64<<<1, 1, 0, st>>>(fbase + q.nfine, E);
@@ -1163,7 +1163,7 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
   }
   k_set_u64<<<1, 1, 0, st>>>(t_offsets + V, E);
   GT_LAUNCH_CHECK();
-  launches += 8;
+  launches += 10;  // set, plan, big nt / scan / write, count, scan, segfix, big place, units (+ the final set below)
   if ((rc = tm.mark())) return rc;
   uint32_t h_cnt[3] = {0, 0, 0};
   unsigned int h_err = 0;
