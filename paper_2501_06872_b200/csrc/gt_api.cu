@@ -855,7 +855,8 @@ int transpose_v3(const Plan& p, InCsr in, uint64_t* t_offsets, uint32_t* t_edges
   // (GT_W1 = 32: compact graphs with 16384-edge tiles, 16 warps at K = 32)
   // wide graphs (C5): 16384-edge tiles 81.8 -> 58.0 ms
   // (the 16-warp forms need their larger tables to fit: the safe rank mode's scratch table may not)
-  int w1x = p.wide ? (env_int("GT_W1W", 16) == 16 ? 32 : W) : env_int("GT_W1", W);
+  // compact graphs with <= 512 coarse digits: 16 warps x K = 16 (C3 k_p1 2.70 -> 2.64 ms; C4, 1024 digits: slower)
+  int w1x = p.wide ? (env_int("GT_W1W", 16) == 16 ? 32 : W) : env_int("GT_W1", D1 <= 512 ? 16 : W);
   if (w1x == 32 && smem_p1(D1, kMode, 32, 16) + 64 > max_smem_optin()) w1x = W;
   if (w1x == 16 && smem_p1(D1, kMode, 16, 16) + 64 > max_smem_optin()) w1x = W;
   const int w1 = w1x == 32 ? 16 : w1x;

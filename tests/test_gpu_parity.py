@@ -434,7 +434,7 @@ def test_full_size_c5():
 
 
 @pytest.mark.parametrize("env", [
-    {"GT_W1": "16"}, {"GT_W1": "32"}, {"GT_K1": "16"}, {"GT_W3": "32"}, {"GT_PRE": "30"}, {"GT_PRE": "0"},
+    {"GT_W1": "8"}, {"GT_W1": "16"}, {"GT_W1": "32"}, {"GT_W1": "8", "GT_K1": "16"}, {"GT_W3": "32"}, {"GT_PRE": "30"}, {"GT_PRE": "0"},
     {"GT_FORK": "0"}, {"GT_BAL3": "0"}, {"GT_OCC": "1"}, {"GT_K2": "32", "GT_W2": "16"},
     {"GT_SPLIT": "6,6,6"}, {"GT_WIDE": "1", "GT_W1W": "8", "GT_W2W": "8"},
 ])
