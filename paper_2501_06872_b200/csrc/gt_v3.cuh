@@ -236,7 +236,8 @@ __device__ __forceinline__ uint32_t rank_pk(uint32_t* c, uint32_t* sc, uint32_t 
 // After ranking: tab[d * WHN + k] holds (warp 2k, warp 2k+1) tile positions of
 // their first digit-d item; dtot per digit; delta[d] = gcur[d] - digit start.
 // Epilogue form: epi(d, b, e) per digit with its tile-local start b and end e.
-template <int WHN, class Epi>
+// kEpi = false: no per-digit epilogue (and no barrier after the rewrite's barrier).
+template <int WHN, bool kEpi = true, class Epi>
 __device__ __forceinline__ void flat_bases_epi(uint32_t* tab, int D, uint32_t* tmp, Epi epi) {
   const int n = D * WHN;
   const int Tn = blockDim.x, t = threadIdx.x, lane = t & 31, w = t >> 5, nw = (Tn + 31) >> 5;
@@ -273,8 +274,10 @@ __device__ __forceinline__ void flat_bases_epi(uint32_t* tab, int D, uint32_t* t
     run += l + (v >> 16);
   }
   __syncthreads();
-  for (int d = threadIdx.x; d < D; d += blockDim.x) epi(d, tab[d * WHN] & 0xffffu, tab[d * WHN + WHN - 1] & 0xffffu);
-  __syncthreads();
+  if constexpr (kEpi) {
+    for (int d = threadIdx.x; d < D; d += blockDim.x) epi(d, tab[d * WHN] & 0xffffu, tab[d * WHN + WHN - 1] & 0xffffu);
+    __syncthreads();
+  }
 }
 template <int WHN>
 __device__ __forceinline__ void flat_bases_pk(uint32_t* tab, int D, const uint32_t* gcur, uint32_t* dtot,
@@ -1366,7 +1369,7 @@ __global__ void __launch_bounds__(WW3 * 32, WW3 > 16 ? 1 : 2) k_p3(const P3Args 
     }
     __syncthreads();  // (B)
     tick(2);
-    flat_bases_pk<WH3_>(s_cnt, (int)nloc, nullptr, nullptr, nullptr, s_tmp);
+    flat_bases_epi<WH3_, false>(s_cnt, (int)nloc, s_tmp, [](int, uint32_t, uint32_t) {});
     {
       const uint64_t v0 = (uint64_t)u.f0 << a.c;
       for (uint32_t v = tid; v < nloc; v += TT)
