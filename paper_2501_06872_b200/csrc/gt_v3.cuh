@@ -494,6 +494,25 @@ __device__ __forceinline__ void writeout_tag(uint32_t* __restrict__ out, const u
   }
 }
 
+// Write-out of (payload, digit) pairs: slot i goes to delta[digit] + i.
+template <int NT, int TILE>
+__device__ __forceinline__ void writeout_pair(uint32_t* __restrict__ out, const uint2* st, const uint32_t* delta,
+                                              uint32_t n) {
+  if (n == (uint32_t)TILE) {
+#pragma unroll
+    for (int k = 0; k < TILE / NT; ++k) {
+      const uint32_t i = threadIdx.x + k * NT;
+      const uint2 v = st[i];
+      out[delta[v.y] + i] = v.x;
+    }
+  } else {
+    for (uint32_t i = threadIdx.x; i < n; i += NT) {
+      const uint2 v = st[i];
+      out[delta[v.y] + i] = v.x;
+    }
+  }
+}
+
 // Stage K ranked items of a thread: item s (pk = digit << 16 | rank inside its
 // warp's digit run, payload pay) goes to slot base(digit, warp) + rank, its
 // digit to tag[slot].  The base words of G items are loaded before their
@@ -517,6 +536,27 @@ __device__ __forceinline__ void stage_tag(const uint32_t (&pk)[K_], const uint32
         const uint32_t pos = ((bw[q] >> sh) & 0xffffu) + (pk[c + q] & 0xffffu);
         buf[pos] = pay[c + q];
         tag[pos] = (Tag)(pk[c + q] >> 16);
+      }
+    }
+  }
+}
+
+// stage_tag with one 8-byte (payload, digit) store per item.
+template <int G, int K_>
+__device__ __forceinline__ void stage_pair(const uint32_t (&pk)[K_], const uint32_t (&pay)[K_], const uint32_t* cnt,
+                                           int whn, uint32_t w, uint32_t sh, uint2* st, uint32_t lim, uint32_t i0,
+                                           uint32_t per = K_ * 32) {
+#pragma unroll
+  for (int c = 0; c < K_; c += G) {
+    if ((uint32_t)c * 32 >= per) break;
+    uint32_t bw[G];
+#pragma unroll
+    for (int q = 0; q < G; ++q) bw[q] = cnt[(pk[c + q] >> 16) * whn + (w >> 1)];
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      if ((uint32_t)(c + q) * 32 < per && (lim == 0xffffffffu || i0 + (c + q) * 32 < lim)) {
+        const uint32_t pos = ((bw[q] >> sh) & 0xffffu) + (pk[c + q] & 0xffffu);
+        st[pos] = make_uint2(pay[c + q], pk[c + q] >> 16);
       }
     }
   }
@@ -947,10 +987,11 @@ constexpr int kIoLv = 2;     // level 3 big buckets of wide graphs: source + dig
 // Wide forms use 64-bit output positions: the per-digit cursor array holds the
 // cursor between place tiles and the index delta during one (as in k_p1 kW64).
 
-inline size_t smem_p2(int D, int mode, int KK = K, int io = kIoPlain, int WW = W) {
+inline size_t smem_p2(int D, int mode, int KK = K, int io = kIoPlain, int WW = W, int s64 = -1) {
   const size_t pt = (size_t)WW * KK * 32;
   const int wh = WW / 2 + 1, wp = WW + 1;
-  return (pt + 8) * 4 + pt * 2 + ((size_t)round4(D * wh) + (mode == kRankSafe ? (size_t)round4(D * wp) : 0)) * 4 + (size_t)D * 4 * 4 +
+  if (s64 < 0) s64 = (io == kIoPlain && KK <= 16);  // measured: C3 level 2 2.115 -> 2.075 ms; 8192-record tiles slower
+  return (s64 ? pt * 8 : (pt + 8) * 4 + pt * 2) + ((size_t)round4(D * wh) + (mode == kRankSafe ? (size_t)round4(D * wp) : 0)) * 4 + (size_t)D * 4 * 4 +
          40 * 4 + (size_t)kMaxBnd * 4 + (io != kIoPlain ? pt + 16 : 0);
 }
 
@@ -977,7 +1018,10 @@ __device__ __forceinline__ uint32_t slot_owner32(uint32_t& cur, uint32_t& nb, ui
 
 // Place: per tile, place tiles of PT records are ranked by digit, staged with
 // their global indices, and written out (persistent, grid-stride over tiles).
-template <int kMode, class Dec, int KK, bool kProf = false, int kIO = kIoPlain, bool kPre = true, int WW = W, int kMinB = (KK > 16 ? 2 : 4)>
+// kS64: staged items as (payload, digit) pairs, one 8-byte store / load each (the
+// landing buffer is dead after ranking and the pair array overlays it).
+template <int kMode, class Dec, int KK, bool kProf = false, int kIO = kIoPlain, bool kPre = true, int WW = W,
+          int kMinB = (KK > 16 ? 2 : 4), bool kS64 = (kIO == kIoPlain && KK <= 16)>
 __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restrict__ rec, const RTile* __restrict__ tiles,
                                              const uint32_t* __restrict__ n_tiles, int D, Dec dec,
                                              const uint64_t* __restrict__ base, uint32_t* __restrict__ out,
@@ -1000,9 +1044,11 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
   constexpr int W2_ = WW, T2_ = WW * 32, WH2_ = WW / 2 + 1, WP2_ = WW + 1;
   constexpr int PT = W2_ * KK * 32, PTP = PT + 8, K = KK;
   extern __shared__ __align__(128) unsigned char smem[];
-  uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem);                         // PTP
+  uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem);                         // PTP (kS64: PT pairs overlay it)
+  uint2* s_st64 = reinterpret_cast<uint2*>(smem);                              // kS64: PT staged (payload, digit)
   uint16_t* s_tag = reinterpret_cast<uint16_t*>(s_buf + PTP);                 // PT (digit of each staged slot)
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_tag + PT);                   // D * WH2_ (packed, digit-major)
+  uint32_t* s_cnt = kS64 ? reinterpret_cast<uint32_t*>(smem + (size_t)PT * 8)
+                         : reinterpret_cast<uint32_t*>(s_tag + PT);            // D * WH2_ (packed, digit-major)
   uint32_t* s_scr = s_cnt + round4(D * WH2_);                                    // D * WP2_ (safe)
   uint32_t* s_gcur = s_scr + (kMode == kRankSafe ? round4(D * WP2_) : 0);        // D
   uint32_t* s_delta = s_gcur + D;                                              // D
@@ -1160,7 +1206,10 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
       else
         flat_bases_pk<WH2_>(s_cnt, D, s_gcur, s_dtot, s_delta, s_tmp);
       tick(3);
-      if constexpr (kIO != kIoSplit) {
+      if constexpr (kS64) {
+        stage_pair<kPre ? kStageG : 1, K>(pk, pay, s_cnt, WH2_, w, sh, s_st64, (n == (uint32_t)PT) ? 0xffffffffu : n,
+                                          iw + lane, per);
+      } else if constexpr (kIO != kIoSplit) {
         stage_tag<kPre ? kStageG : 1, K>(pk, pay, s_cnt, WH2_, w, sh, s_buf, s_tag, (n == (uint32_t)PT) ? 0xffffffffu : n, iw + lane,
                                          per);
       } else {
@@ -1177,7 +1226,9 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
       }
       __syncthreads();  // (C)
       tick(4);
-      if constexpr (kIO == kIoPlain) {
+      if constexpr (kS64) {
+        writeout_pair<T2_, PT>(out, s_st64, s_delta, n);
+      } else if constexpr (kIO == kIoPlain) {
         writeout_tag<T2_, PT>(out, s_buf, s_tag, s_delta, n);
       } else {  // 64-bit positions
         auto put = [&](uint32_t i) {
