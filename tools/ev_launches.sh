@@ -12,7 +12,7 @@ for c in C3 C2 C4; do
   echo "$c launches rc=$?"
 done
 for k in k_p1 k_p2 k_p3; do
-  timeout 240 ncu --set full --clock-control none -k regex:"$k" -s 2 -c 1 -o /tmp/full_$k python bench.py --config C3 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $D/ncu_full_$k.log 2>&1
+  timeout 240 ncu -f --set full --clock-control none -k regex:"$k" -s 2 -c 1 -o /tmp/full_$k python bench.py --config C3 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $D/ncu_full_$k.log 2>&1
   echo "$k full rc=$?"
   ncu -i /tmp/full_$k.ncu-rep --page raw --csv > $D/raw_${R}_C3_$k.csv 2>/dev/null
 done
