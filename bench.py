@@ -423,6 +423,15 @@ def main():
                    "sample": f"full {cfg.name} graph, median of {reps} (after 1 warm-up); OpenMP port of "
                              "transpose_scantrans (baselines.py:265-312), sorted by construction"}
 
+    # the dominant kernel (longest per-launch time among the place kernels with algorithmic bytes)
+    dominant = None
+    for ent in (kern or {}).get("per_kernel", []) if isinstance(kern, dict) else []:
+        if "algorithmic_bytes" in ent and "level 3 total" not in ent["name"]:
+            if dominant is None or ent["ms"] > dominant["ms_per_launch"]:
+                dominant = {"name": ent["name"], "ms_per_launch": ent["ms"], "algorithmic_bytes": ent["algorithmic_bytes"],
+                            "achieved": ent["achieved_gbs"], "peak": peak, "unit": "GB/s", "frac": ent["frac"],
+                            "traffic": ent.get("traffic")}
+
     if rank == 0:
         line = {
             "metric": METRIC,
@@ -443,7 +452,8 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": agg_peak, "unit": "GB/s",
                          "frac": achieved / agg_peak, "traffic": traffic,
                          "scope": "whole transpose step (all kernels); algorithmic bytes 24(V+1)+12E per step",
-                         "peak_source": peak_src, "algorithmic_bytes_per_step": abytes, "kernels": kern},
+                         "peak_source": peak_src, "algorithmic_bytes_per_step": abytes,
+                         "dominant_kernel": dominant, "kernels": kern},
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks,
