@@ -813,15 +813,28 @@ __global__ void __launch_bounds__(512) k_cnt_rec(const uint32_t* __restrict__ re
     for (uint32_t i = threadIdx.x; i < head; i += blockDim.x) smem_inc(&s_h[dig(p[i])]);
     const uint4* p4 = reinterpret_cast<const uint4*>(p + head);
     const uint32_t n4 = (n - head) >> 2;
-    for (uint32_t q = threadIdx.x; q < n4; q += blockDim.x) {
+    auto ld4 = [](const uint4* a) {
       uint4 v;
       asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                   : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p4 + q));
+                   : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(a));
+      return v;
+    };
+    auto inc4 = [&](const uint4& v) {
       smem_inc(&s_h[dig(v.x)]);
       smem_inc(&s_h[dig(v.y)]);
       smem_inc(&s_h[dig(v.z)]);
       smem_inc(&s_h[dig(v.w)]);
+    };
+    const uint32_t bd = blockDim.x;
+    uint32_t q = threadIdx.x;
+    for (; q + 3 * bd < n4; q += 4 * bd) {  // four 16-byte loads in flight per thread
+      const uint4 v0 = ld4(p4 + q), v1 = ld4(p4 + q + bd), v2 = ld4(p4 + q + 2 * bd), v3 = ld4(p4 + q + 3 * bd);
+      inc4(v0);
+      inc4(v1);
+      inc4(v2);
+      inc4(v3);
     }
+    for (; q < n4; q += bd) inc4(ld4(p4 + q));
     for (uint32_t i = head + n4 * 4 + threadIdx.x; i < n; i += blockDim.x) smem_inc(&s_h[dig(p[i])]);
     __syncthreads();
     const uint64_t row0 = (uint64_t)(g - t.j) * D + t.j;
