@@ -5,5 +5,5 @@ set -u
 mkdir -p gpurun_out/ev
 timeout 1200 python -m pytest tests -x -q -m gpu > gpurun_out/ev/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/ev/pytest_gpu.log
 timeout 300 python -c 'import __graft_entry__ as g; g.smoke()' > gpurun_out/ev/smoke.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/ev/smoke.log
-bash tools/ev_launches.sh ${1:-r01j}
+bash tools/ev_launches.sh ${1:-r01m}
 bash tools/ev_bench.sh | grep rc=

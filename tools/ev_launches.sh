@@ -3,7 +3,7 @@
 # `ncu --set full` capture per main C3 kernel, each after a plain run of the same command.
 # Usage (on the GPU box): bash tools/ev_launches.sh r01h
 set -u
-R=${1:-r01l}
+R=${1:-r01m}
 D=gpurun_out/ev; mkdir -p $D
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__warps_active.avg.pct_of_peak_sustained_active,smsp__inst_executed.sum,l1tex__throughput.avg.pct_of_peak_sustained_active,lts__t_sector_hit_rate.pct
 for c in C3 C2 C4; do
