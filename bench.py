@@ -250,6 +250,7 @@ def main():
     peak, peak_src = _peaks()
     sampler = ClockSampler(local_rank)
 
+    e2e_dist = None
     if not dist_on:
         t_off = torch.empty(V + 1, dtype=torch.int64, device=dev)
         t_edg = torch.empty(E, dtype=torch.int32, device=dev)
@@ -314,6 +315,45 @@ def main():
         launches = 11 * args.steps  # partition (4) + receiver pipeline (~7+) per step, lower bound
         kern = {"dst_bounds": plan.dst_bounds.tolist(), "src_bounds": plan.src_bounds.tolist()}
         n_gpus = world
+        e2e_dist = None
+        if not args.no_e2e:
+            # end to end per rank: H2D of the offsets and this rank's edge slice from pinned
+            # host memory, the sharded step, D2H of this rank's CSC slice into pinned memory;
+            # CUDA events on the launching stream (the copies are on it), max over ranks
+            h_off = off_d.cpu().pin_memory()
+            h_edg = edg_slice.cpu().pin_memory()
+            t_off_s, t_edg_s, _ = distributed_step(off_d, edg_slice, V, plan, rank, backend)
+            h_toff = torch.empty(t_off_s.shape, dtype=t_off_s.dtype).pin_memory()
+            h_tedg = torch.empty(t_edg_s.shape, dtype=t_edg_s.dtype).pin_memory()
+
+            def e2e_step():
+                off_d.copy_(h_off, non_blocking=True)
+                edg_slice.copy_(h_edg, non_blocking=True)
+                to, te, _ = distributed_step(off_d, edg_slice, V, plan, rank, backend)
+                h_toff.copy_(to, non_blocking=True)
+                h_tedg.copy_(te, non_blocking=True)
+
+            e2e_step()
+            torch.cuda.synchronize()
+            dist.barrier()
+            ne = max(3, min(args.steps, 10))
+            e0v, e1v = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0v.record(stream)
+            for _ in range(ne):
+                e2e_step()
+            e1v.record(stream)
+            torch.cuda.synchronize()
+            dist.barrier()
+            te_ms = torch.tensor([e0v.elapsed_time(e1v) / ne], device=dev, dtype=torch.float64)
+            dist.all_reduce(te_ms, op=dist.ReduceOp.MAX)
+            nb = torch.tensor([h_off.numel() * 8 + h_edg.numel() * 4, h_toff.numel() * 8 + h_tedg.numel() * 4],
+                              device=dev, dtype=torch.int64)
+            dist.all_reduce(nb)  # whole-job bytes per step
+            te = float(te_ms.item()) / 1e3
+            e2e_dist = {"value": E / te, "unit": "edges/s", "h2d_bytes_per_step": int(nb[0]),
+                        "d2h_bytes_per_step": int(nb[1]), "ms_per_step": te * 1e3, "steps": ne,
+                        "api": "per rank: pinned H2D of offsets + its edge slice, distributed_step "
+                               "(multi.py), pinned D2H of its CSC slice; max over ranks"}
 
     value = E / (ms / 1e3)
     abytes = algo_bytes(V, E)
@@ -355,7 +395,7 @@ def main():
                                "frac": (8 * E + 8 * (V + 1)) / (l3 / 1e3) / 1e9 / peak})
         kern["per_kernel"] = kernels_rf
 
-    e2e = None
+    e2e = e2e_dist if dist_on else None
     cpu = None
     if rank == 0 and not dist_on:
         if not args.no_e2e:
