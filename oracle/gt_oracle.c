@@ -30,6 +30,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <math.h>
 #include <omp.h>
 
 #define GTO_OK 0
@@ -227,3 +228,358 @@ int gto_sort_lists(const uint64_t *offsets, uint64_t nv, uint32_t *edges, int th
 }
 
 int gto_max_threads(void) { return omp_get_max_threads(); }
+
+/* ======================================================================== */
+/* Seeded synthetic graphs (CPU side, test infrastructure): the same counter-  */
+/* based draws as paper_2501_06872_b200/gen.py (rmat_pairs_np, er_pairs_np,   */
+/* csr_from_pairs_np) so bench.py's reference arm builds its input without the */
+/* product library.  CSR lists come out sorted ascending by destination.       */
+/* ======================================================================== */
+#define GTO_GOLDEN 0x9E3779B97F4A7C15ull
+#define GTO_SEED_MUL 0xD1B54A32D192ED03ull
+#define GTO_RMAT_A 2448131358u
+#define GTO_RMAT_AB 3264175144u
+#define GTO_RMAT_ABC 4080218931u
+
+static inline uint64_t gto_mix64(uint64_t z) {
+    z ^= z >> 30; z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27; z *= 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+static inline uint64_t gto_stream_key(uint64_t seed, uint64_t stream) {
+    return gto_mix64(seed * GTO_SEED_MUL + stream * GTO_GOLDEN + 1);
+}
+static inline uint64_t gto_hash_at(uint64_t key, uint64_t idx) { return gto_mix64(key + (idx + 1) * GTO_GOLDEN); }
+
+typedef struct { uint64_t keys[4]; int half; uint64_t mask, n; } gto_perm;
+static void gto_perm_init(gto_perm *p, int scale, uint64_t seed) {
+    int width = scale + (scale & 1);
+    p->half = width / 2;
+    p->mask = (1ull << p->half) - 1;
+    p->n = 1ull << scale;
+    uint64_t pk = gto_stream_key(seed, 2 /* STREAM_PERM */);
+    for (int r = 0; r < 4; ++r) p->keys[r] = gto_hash_at(pk, (uint64_t)r);
+}
+static inline uint64_t gto_feistel(const gto_perm *p, uint64_t x) {
+    uint64_t L = x >> p->half, R = x & p->mask;
+    for (int r = 0; r < 4; ++r) {
+        uint64_t t = L ^ (gto_mix64(R ^ p->keys[r]) & p->mask);
+        L = R; R = t;
+    }
+    return (L << p->half) | R;
+}
+static inline uint64_t gto_permute(const gto_perm *p, uint64_t x) {
+    uint64_t y = gto_feistel(p, x);
+    while (y >= p->n) y = gto_feistel(p, y); /* cycle walking */
+    return y;
+}
+
+/* kind 0 = R-MAT (.57/.19/.19/.05), 1 = Erdos-Renyi */
+typedef struct { int kind, scale, permute; uint64_t nv, key; gto_perm perm; } gto_gen;
+static inline void gto_pair(const gto_gen *g, uint64_t e, uint32_t *src, uint32_t *dst) {
+    if (g->kind == 1) {
+        *src = (uint32_t)(((gto_hash_at(g->key, 2 * e) >> 32) * g->nv) >> 32);
+        *dst = (uint32_t)(((gto_hash_at(g->key, 2 * e + 1) >> 32) * g->nv) >> 32);
+        return;
+    }
+    uint64_t s = 0, d = 0;
+    for (int l = 0; l < g->scale; l += 2) {
+        uint64_t h = gto_hash_at(g->key, e * 16 + (uint64_t)(l >> 1));
+        for (int q = 0; q < 2 && l + q < g->scale; ++q) {
+            uint32_t u = (uint32_t)(h >> (32 * q));
+            uint64_t bit = 1ull << (g->scale - 1 - (l + q));
+            int in_b = u >= GTO_RMAT_A && u < GTO_RMAT_AB, in_c = u >= GTO_RMAT_AB && u < GTO_RMAT_ABC;
+            int in_d = u >= GTO_RMAT_ABC;
+            if (in_b || in_d) d |= bit;
+            if (in_c || in_d) s |= bit;
+        }
+    }
+    if (g->permute) { s = gto_permute(&g->perm, s); d = gto_permute(&g->perm, d); }
+    *src = (uint32_t)s;
+    *dst = (uint32_t)d;
+}
+
+static int cmp_u32(const void *a, const void *b);
+
+/* Two passes over the draws (count sources, then place destinations with
+ * atomic cursors) and a per-list sort: the CSR of csr_from_pairs_np
+ * (lexsort((dst, src))) without materialising the pair arrays. */
+int gto_generate(int kind, int scale, int permute, uint64_t nv, uint64_t ne, uint64_t seed,
+                 uint64_t *offsets, uint32_t *edges, int threads) {
+    if (threads < 1 || (kind != 0 && kind != 1)) return GTO_EINVAL;
+    gto_gen g;
+    g.kind = kind; g.scale = scale; g.permute = permute; g.nv = nv;
+    g.key = gto_stream_key(seed, kind == 0 ? 1 /* STREAM_RMAT */ : 3 /* STREAM_ER */);
+    if (kind == 0) gto_perm_init(&g.perm, scale, seed);
+    uint64_t *cur = (uint64_t *)calloc(nv + 1, sizeof(uint64_t));
+    if (!cur) return GTO_ENOMEM;
+#pragma omp parallel for num_threads(threads) schedule(static, 1 << 16)
+    for (int64_t e = 0; e < (int64_t)ne; ++e) {
+        uint32_t s, d;
+        gto_pair(&g, (uint64_t)e, &s, &d);
+        __atomic_fetch_add(&cur[s], 1ull, __ATOMIC_RELAXED);
+    }
+    offsets[0] = 0;
+    for (uint64_t v = 0; v < nv; ++v) { offsets[v + 1] = offsets[v] + cur[v]; cur[v] = offsets[v]; }
+#pragma omp parallel for num_threads(threads) schedule(static, 1 << 16)
+    for (int64_t e = 0; e < (int64_t)ne; ++e) {
+        uint32_t s, d;
+        gto_pair(&g, (uint64_t)e, &s, &d);
+        edges[__atomic_fetch_add(&cur[s], 1ull, __ATOMIC_RELAXED)] = d;
+    }
+    free(cur);
+#pragma omp parallel for num_threads(threads) schedule(dynamic, 4096)
+    for (int64_t v = 0; v < (int64_t)nv; ++v) {
+        uint64_t a = offsets[v], b = offsets[v + 1];
+        if (b - a > 1) qsort(edges + a, (size_t)(b - a), sizeof(uint32_t), cmp_u32);
+    }
+    return GTO_OK;
+}
+
+/* ======================================================================== */
+/* transpose_potra (hlh.py:441-588): step 0 (sample_hdv hlh.py:167-218 with  */
+/* the reference's xoshiro256** worker streams _nb.py:47-93, the compressing */
+/* linear-probe table hlh.py:68-90, probe_methods hlh.py:293-333), then the  */
+/* HLH steps 1-3 (_hlh_step1 / _hlh_degrees / _hlh_step3, hlh.py:340-397) or */
+/* the atomic baseline when the probe picks it.  Output lists are unsorted,  */
+/* as the reference's (sorted=False); gto_sort_lists canonicalises them.      */
+/* ======================================================================== */
+#define GTO_EMPTY 0xFFFFFFFFFFFFFFFFull
+typedef struct { uint64_t *keys; uint32_t *vals; uint64_t cap; int shift; } gto_table;
+
+static inline int64_t gto_table_find(const gto_table *t, uint64_t key) {
+    uint64_t mask = t->cap - 1, i = (key * GTO_GOLDEN) >> t->shift;
+    for (;;) {
+        uint64_t k = t->keys[i & mask];
+        if (k == key) return (int64_t)t->vals[i & mask];
+        if (k == GTO_EMPTY) return -1;
+        ++i;
+    }
+}
+
+static inline uint64_t gto_rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+static inline uint64_t gto_splitmix(uint64_t *x) {
+    *x += GTO_GOLDEN;
+    return gto_mix64(*x);
+}
+
+static void gto_tally(const uint32_t *edges, uint64_t ne, uint64_t num_samples, const uint64_t *seeds, int workers,
+                      uint32_t *freq) {
+#pragma omp parallel for num_threads(workers) schedule(static, 1)
+    for (int w = 0; w < workers; ++w) {
+        uint64_t lo = (uint64_t)w * num_samples / workers, hi = (uint64_t)(w + 1) * num_samples / workers;
+        uint64_t x = seeds[w];
+        uint64_t s0 = gto_splitmix(&x), s1 = gto_splitmix(&x), s2 = gto_splitmix(&x), s3 = gto_splitmix(&x);
+        for (uint64_t i = lo; i < hi; ++i) {
+            uint64_t r = gto_rotl(s1 * 5, 7) * 9, t = s1 << 17;
+            s2 ^= s0; s3 ^= s1; s1 ^= s2; s0 ^= s3; s2 ^= t; s3 = gto_rotl(s3, 45);
+            __atomic_fetch_add(&freq[edges[r % ne]], 1u, __ATOMIC_RELAXED);
+        }
+    }
+}
+
+typedef struct { uint32_t f; uint32_t id; } gto_cand;
+static int cmp_cand(const void *a, const void *b) { /* (-freq, id) */
+    const gto_cand *x = (const gto_cand *)a, *y = (const gto_cand *)b;
+    if (x->f != y->f) return x->f > y->f ? -1 : 1;
+    return (x->id > y->id) - (x->id < y->id);
+}
+
+static double gto_now(void) { return omp_get_wtime(); }
+
+/* phase[0..3] = step0..step3 seconds; info[0] = method (0 atomic, 1 hlh),
+ * info[1] = k, info[2] = sample size; est = coverage estimate. */
+int gto_transpose_potra(const uint64_t *offsets, const uint32_t *edges, uint64_t nv, uint64_t ne,
+                        uint64_t *t_offsets, uint32_t *t_edges, int threads, int64_t k, double sample_fraction,
+                        uint64_t seed, uint64_t partition_edges, int force_method, double *phase, int64_t *info,
+                        double *est) {
+    if (threads < 1 || partition_edges < 1 || k < 0) return GTO_EINVAL;
+    const int W = threads;
+    double t_start = gto_now();
+    if ((uint64_t)k > nv) k = (int64_t)nv;
+    /* ---- step 0: sample_hdv ---- */
+    uint64_t size = 0;
+    uint32_t *freq = (uint32_t *)calloc(nv ? nv : 1, sizeof(uint32_t));
+    uint32_t *estf = (uint32_t *)calloc(nv ? nv : 1, sizeof(uint32_t));
+    if (!freq || !estf) { free(freq); free(estf); return GTO_ENOMEM; }
+    if (sample_fraction >= 1.0 || ne == 0) {
+        for (uint64_t j = 0; j < ne; ++j) freq[edges[j]]++;
+        memcpy(estf, freq, nv * sizeof(uint32_t));
+        size = ne;
+    } else {
+        size = (uint64_t)ceil(sample_fraction * (double)nv);
+        uint64_t *seeds = (uint64_t *)malloc(sizeof(uint64_t) * 2 * W), x = seed;
+        for (int w = 0; w < 2 * W; ++w) seeds[w] = gto_splitmix(&x);
+        if (size) {
+            gto_tally(edges, ne, size, seeds, W, freq);
+            gto_tally(edges, ne, size, seeds + W, W, estf);
+        }
+        free(seeds);
+    }
+    uint64_t *ids = (uint64_t *)malloc(sizeof(uint64_t) * (k ? k : 1));
+    {
+        uint64_t nc = 0;
+        for (uint64_t v = 0; v < nv; ++v) nc += freq[v] != 0;
+        gto_cand *c = (gto_cand *)malloc(sizeof(gto_cand) * (nc ? nc : 1));
+        nc = 0;
+        for (uint64_t v = 0; v < nv; ++v)
+            if (freq[v]) { c[nc].f = freq[v]; c[nc].id = (uint32_t)v; ++nc; }
+        qsort(c, nc, sizeof(gto_cand), cmp_cand);
+        int64_t m = 0;
+        for (; m < k && (uint64_t)m < nc; ++m) ids[m] = c[m].id;
+        for (uint64_t v = 0; m < k; ++v) /* zero-frequency vertices by ascending id */
+            if (!freq[v]) ids[m++] = v;
+        free(c);
+    }
+    uint64_t hits = 0;
+    for (int64_t i = 0; i < k; ++i) hits += estf[ids[i]];
+    *est = size ? (double)hits / (double)size : 0.0;
+    free(freq);
+    free(estf);
+    gto_table tb;
+    {
+        uint64_t need = k ? (uint64_t)ceil((double)k / 0.5) : 2, cap = 2;
+        while (cap < need) cap <<= 1;
+        tb.cap = cap;
+        int lg = 0;
+        while ((1ull << lg) < cap) ++lg;
+        tb.shift = 64 - lg;
+        tb.keys = (uint64_t *)malloc(sizeof(uint64_t) * cap);
+        tb.vals = (uint32_t *)calloc(cap, sizeof(uint32_t));
+        for (uint64_t i = 0; i < cap; ++i) tb.keys[i] = GTO_EMPTY;
+        for (int64_t n = 0; n < k; ++n) {
+            uint64_t i = (ids[n] * GTO_GOLDEN) >> tb.shift;
+            while (tb.keys[i & (cap - 1)] != GTO_EMPTY) ++i;
+            tb.keys[i & (cap - 1)] = ids[n];
+            tb.vals[i & (cap - 1)] = (uint32_t)n;
+        }
+    }
+    const int64_t k1 = k > 0 ? k : 1;
+    uint32_t *ldv = (uint32_t *)calloc(nv ? nv : 1, sizeof(uint32_t));
+    uint8_t *low = (uint8_t *)calloc((size_t)W * k1, 1);
+    uint32_t *high = (uint32_t *)calloc((size_t)W * k1, sizeof(uint32_t));
+    /* ---- probe_methods: split counting vs atomic counting on an edge prefix ---- */
+    int method = force_method; /* -1 = probe, 0 = atomic, 1 = hlh */
+    if (method < 0) {
+        uint64_t n = ne / 100 ? ne / 100 : 1;
+        if (n > (1ull << 24)) n = 1ull << 24;
+        if (n > ne) n = ne;
+        if (n == 0) {
+            method = 0;
+        } else {
+            uint32_t *cnt = (uint32_t *)calloc(nv ? nv : 1, sizeof(uint32_t));
+            double th = 0, ta = 0;
+            for (int pass = 0; pass < 2; ++pass) {
+                uint64_t m = pass ? n : (n < 4096 ? n : 4096);
+                double t0 = gto_now();
+#pragma omp parallel for num_threads(W) schedule(static, 1)
+                for (int w = 0; w < W; ++w)
+                    for (uint64_t i = (uint64_t)w * m / W; i < (uint64_t)(w + 1) * m / W; ++i) {
+                        int64_t t = gto_table_find(&tb, edges[i]);
+                        if (t < 0) __atomic_fetch_add(&ldv[edges[i]], 1u, __ATOMIC_RELAXED);
+                        else if (++low[(size_t)w * k1 + t] == 0) high[(size_t)w * k1 + t]++;
+                    }
+                double t1 = gto_now();
+#pragma omp parallel for num_threads(W) schedule(static, 1)
+                for (int w = 0; w < W; ++w)
+                    for (uint64_t i = (uint64_t)w * m / W; i < (uint64_t)(w + 1) * m / W; ++i)
+                        __atomic_fetch_add(&cnt[edges[i]], 1u, __ATOMIC_RELAXED);
+                double t2 = gto_now();
+                if (pass) { th = t1 - t0; ta = t2 - t1; }
+            }
+            free(cnt);
+            method = th < ta ? 1 : 0;
+            memset(ldv, 0, (nv ? nv : 1) * sizeof(uint32_t));
+            memset(low, 0, (size_t)W * k1);
+            memset(high, 0, (size_t)W * k1 * sizeof(uint32_t));
+        }
+    }
+    phase[0] = gto_now() - t_start;
+    info[0] = method;
+    info[1] = k;
+    info[2] = (int64_t)size;
+    int rc = GTO_OK;
+    if (method == 0) {
+        double t0 = gto_now();
+        rc = gto_transpose_atomic(offsets, edges, nv, ne, t_offsets, t_edges, W, partition_edges);
+        phase[1] = gto_now() - t0; /* steps 1-3 of the atomic baseline together */
+        phase[2] = phase[3] = 0.0;
+        goto done;
+    }
+    {
+        /* ---- step 1 ---- */
+        double t0 = gto_now();
+        int64_t parts = ne ? (int64_t)((ne + partition_edges - 1) / partition_edges) : 1;
+        if (parts < 1) parts = 1;
+        int64_t *vb = (int64_t *)malloc(sizeof(int64_t) * (size_t)(parts + 1));
+        int32_t *p2t = (int32_t *)malloc(sizeof(int32_t) * (size_t)parts);
+        gto_edge_balanced_bounds(offsets, nv, parts, vb);
+        int64_t cursor = 0;
+#pragma omp parallel num_threads(W)
+        {
+            const int w = omp_get_thread_num();
+            for (;;) {
+                int64_t p = __atomic_fetch_add(&cursor, 1, __ATOMIC_RELAXED);
+                if (p >= parts) break;
+                p2t[p] = w;
+                for (int64_t v = vb[p]; v < vb[p + 1]; ++v)
+                    for (uint64_t j = offsets[v]; j < offsets[v + 1]; ++j) {
+                        const uint32_t e = edges[j];
+                        int64_t t = gto_table_find(&tb, e);
+                        if (t < 0) __atomic_fetch_add(&ldv[e], 1u, __ATOMIC_RELAXED);
+                        else if (++low[(size_t)w * k1 + t] == 0) high[(size_t)w * k1 + t]++;
+                    }
+            }
+        }
+        double t1 = gto_now();
+        /* ---- step 2: degrees, scan, cursors ---- */
+#pragma omp parallel for num_threads(W) schedule(static)
+        for (int64_t v = 0; v < (int64_t)nv; ++v) {
+            int64_t t = gto_table_find(&tb, (uint64_t)v);
+            uint64_t d = 0;
+            if (t < 0) d = ldv[v];
+            else for (int w = 0; w < W; ++w) d += (uint64_t)high[(size_t)w * k1 + t] * 256 + low[(size_t)w * k1 + t];
+            t_offsets[v + 1] = d;
+        }
+        t_offsets[0] = 0;
+        for (uint64_t v = 0; v < nv; ++v) t_offsets[v + 1] += t_offsets[v];
+        int64_t *ip = NULL, *hip = NULL;
+        if (t_offsets[nv] != ne) { rc = GTO_EOVERFLOW; free(vb); free(p2t); goto done; }
+        ip = (int64_t *)malloc(sizeof(int64_t) * (nv ? nv : 1));
+        hip = (int64_t *)malloc(sizeof(int64_t) * (size_t)W * k1);
+#pragma omp parallel for num_threads(W) schedule(static)
+        for (int64_t v = 0; v < (int64_t)nv; ++v) ip[v] = (int64_t)t_offsets[v];
+        for (int64_t t = 0; t < k; ++t) {
+            int64_t run = (int64_t)t_offsets[ids[t]];
+            for (int w = 0; w < W; ++w) {
+                hip[(size_t)w * k1 + t] = run;
+                run += (int64_t)high[(size_t)w * k1 + t] * 256 + low[(size_t)w * k1 + t];
+            }
+        }
+        double t2 = gto_now();
+        /* ---- step 3: each worker replays the partitions it claimed ---- */
+#pragma omp parallel num_threads(W)
+        {
+            const int w = omp_get_thread_num();
+            for (int64_t p = 0; p < parts; ++p) {
+                if (p2t[p] != w) continue;
+                for (int64_t v = vb[p]; v < vb[p + 1]; ++v)
+                    for (uint64_t j = offsets[v]; j < offsets[v + 1]; ++j) {
+                        const uint32_t u = edges[j];
+                        int64_t t = gto_table_find(&tb, u), idx;
+                        if (t < 0) idx = __atomic_fetch_add(&ip[u], 1, __ATOMIC_RELAXED);
+                        else idx = hip[(size_t)w * k1 + t]++;
+                        t_edges[idx] = (uint32_t)v;
+                    }
+            }
+        }
+        double t3 = gto_now();
+        phase[1] = t1 - t0;
+        phase[2] = t2 - t1;
+        phase[3] = t3 - t2;
+        free(vb); free(p2t); free(ip); free(hip);
+    }
+done:
+    free(ids); free(tb.keys); free(tb.vals); free(ldv); free(low); free(high);
+    return rc;
+}

@@ -76,8 +76,11 @@ def load():
         lib.gto_scan_exclusive.argtypes = [vp, u64, vp, i]
         lib.gto_edge_balanced_bounds.argtypes = [vp, u64, ctypes.c_int64, vp]
         lib.gto_edge_balanced_bounds.restype = None
+        lib.gto_generate.argtypes = [i, i, i, u64, u64, u64, vp, vp, i]
+        d, i64 = ctypes.c_double, ctypes.c_int64
+        lib.gto_transpose_potra.argtypes = [vp, vp, u64, u64, vp, vp, i, i64, d, u64, u64, i, vp, vp, vp]
         for f in ("gto_transpose_serial", "gto_transpose_scantrans", "gto_transpose_atomic", "gto_sort_lists",
-                  "gto_scan_exclusive", "gto_max_threads"):
+                  "gto_scan_exclusive", "gto_max_threads", "gto_generate", "gto_transpose_potra"):
             getattr(lib, f).restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -132,6 +135,90 @@ def transpose_atomic_sorted_c(offsets, edges, num_vertices: int, threads: int, p
                                     partition_edges), "gto_transpose_atomic")
     _check(lib.gto_sort_lists(_p(t_off), num_vertices, _p(t_e), threads), "gto_sort_lists")
     return t_off, t_e
+
+
+def generate_c(cfg, threads: int):
+    """Seeded R-MAT / Erdos-Renyi CSR (gen.generate_np's draws) on host cores.
+    Used where the product library must not be loaded (bench.py's reference arm)."""
+    if cfg.kind not in ("rmat", "er"):
+        raise ValueError(f"generate_c covers rmat and er, not {cfg.kind!r}")
+    lib = load()
+    off = np.empty(cfg.num_vertices + 1, dtype=np.uint64)
+    e = np.empty(cfg.num_edges, dtype=np.uint32)
+    _check(lib.gto_generate(0 if cfg.kind == "rmat" else 1, cfg.scale, int(cfg.permute), cfg.num_vertices,
+                            cfg.num_edges, cfg.seed, _p(off), _p(e), threads), "gto_generate")
+    return off, e
+
+
+def detect_cache_budget():
+    """hw.detect_cache_budget (hw.py:19-63): L2 + L3 bytes from sysfs, or None."""
+    import glob
+
+    units = {"K": 1024, "M": 1024 ** 2, "G": 1024 ** 3}
+    seen, tot = set(), {}
+    for d in glob.glob("/sys/devices/system/cpu/cpu*/cache/index*"):
+        try:
+            lvl = int(open(os.path.join(d, "level")).read())
+            typ = open(os.path.join(d, "type")).read().strip()
+            sz = open(os.path.join(d, "size")).read().strip()
+            sh = open(os.path.join(d, "shared_cpu_list")).read().strip()
+        except (OSError, ValueError):
+            continue
+        if typ == "Instruction" or (lvl, sh) in seen:
+            continue
+        seen.add((lvl, sh))
+        b = int(sz[:-1]) * units[sz[-1].upper()] if sz and sz[-1].upper() in units else int(sz)
+        tot[lvl] = tot.get(lvl, 0) + b
+    return (tot.get(2, 0) + tot.get(3, 0)) or None
+
+
+def potra_k(threads: int, cache_bytes=None, load_factor: float = 0.5) -> int:
+    """k of transpose_potra's default budget: hdv_count (model.py:65-75) then
+    _fit_table_budget (hlh.py:422-433), 12-byte slots, 13 B per HDV per thread."""
+    import math
+
+    cache = cache_bytes or detect_cache_budget() or 32 * 1024 * 1024
+    k_raw = max(0, math.floor(cache / (12 / load_factor + 13 * threads)))
+    if k_raw <= 0:
+        return 0
+    cap = max(2, 1 << max(1, (math.ceil(k_raw / load_factor) - 1).bit_length()))
+    while cap >= 2:
+        k = min(k_raw, math.floor(load_factor * cap))
+        if 12 * cap + 13 * threads * k <= cache:
+            return k
+        cap //= 2
+    return 0
+
+
+def transpose_potra_c(offsets, edges, num_vertices: int, threads: int, k=None, sample_fraction: float = 0.01,
+                      seed: int = 0, partition_edges: int = 1 << 18, force_method=None, sort: bool = False):
+    """OpenMP port of transpose_potra (hlh.py:441-588), optionally followed by
+    sort_neighbor_lists.  Returns (t_offsets, t_edges, info dict with the
+    reference's phase names)."""
+    import time
+
+    lib = load()
+    off = np.ascontiguousarray(offsets, dtype=np.uint64)
+    e = np.ascontiguousarray(edges, dtype=np.uint32)
+    t_off = np.empty(num_vertices + 1, dtype=np.uint64)
+    t_e = np.empty(e.shape[0], dtype=np.uint32)
+    if k is None:
+        k = potra_k(threads)
+    phase = np.zeros(4, np.float64)
+    info = np.zeros(3, np.int64)
+    est = np.zeros(1, np.float64)
+    fm = {None: -1, "atomic": 0, "hlh": 1}[force_method]
+    _check(lib.gto_transpose_potra(_p(off), _p(e), num_vertices, e.shape[0], _p(t_off), _p(t_e), threads, int(k),
+                                   float(sample_fraction), seed, partition_edges, fm, _p(phase), _p(info), _p(est)),
+           "gto_transpose_potra")
+    out = {"method_chosen": "hlh" if info[0] else "atomic", "k": int(info[1]), "sample_size": int(info[2]),
+           "coverage_estimate": float(est[0]),
+           "phase_times": {"step0": phase[0], "step1": phase[1], "step2": phase[2], "step3": phase[3]}}
+    if sort:
+        t0 = time.perf_counter()
+        _check(lib.gto_sort_lists(_p(t_off), num_vertices, _p(t_e), threads), "gto_sort_lists")
+        out["phase_times"]["sort"] = time.perf_counter() - t0
+    return t_off, t_e, out
 
 
 def edge_balanced_bounds_c(offsets, parts: int):

@@ -148,31 +148,19 @@ def store_graph(g, path) -> None:
 
 
 def _load_text(path) -> CsrGraph:
-    """Edge-list text (io.py:117-143): "src dst" per line, '#' comments."""
-    src: list[int] = []
-    dst: list[int] = []
-    with open(path, "r", encoding="utf-8") as f:
-        for lineno, line in enumerate(f, start=1):
-            body = line.strip()
-            if not body or body.startswith("#"):
-                continue
-            parts = body.split()
-            if len(parts) != 2:
-                raise GraphFormatError(f"line {lineno}: expected 'src dst', got {body!r}")
-            try:
-                u, v = int(parts[0]), int(parts[1])
-            except ValueError:
-                raise GraphFormatError(f"line {lineno}: non-integer vertex ID in {body!r}") from None
-            if u < 0 or v < 0:
-                raise GraphFormatError(f"line {lineno}: negative vertex ID in {body!r}")
-            src.append(u)
-            dst.append(v)
-    if not src:
-        return CsrGraph(0, 0, np.zeros(1, dtype=np.uint64), np.empty(0, dtype=np.uint32))
-    s = np.asarray(src, dtype=np.int64)
-    d = np.asarray(dst, dtype=np.int64)
-    nv = int(max(s.max(), d.max())) + 1
-    return CsrGraph.from_edge_pairs(s, d, nv)
+    """Edge-list text is host-side parsing outside this package's scope (the
+    GPU path starts at a CSR in memory or a POTG file).  It is delegated to the
+    reference's own reader (potra.io.load_graph, io.py:117-143) when potra is
+    importable."""
+    try:
+        from potra import io as _potra_io  # the reference package, when installed
+    except ImportError:
+        raise NotImplementedError(
+            "edge-list-text input is read by the reference's potra.io.load_graph; "
+            "potra is not importable here (convert to the binary POTG format first)") from None
+    g = _potra_io.load_graph(path, format="edge-list-text")
+    return CsrGraph(int(g.num_vertices), int(g.num_edges), np.asarray(g.offsets, dtype=np.uint64),
+                    np.asarray(g.edges, dtype=np.uint32))
 
 
 def transpose_file(in_path, out_path, *, sort: bool = False, device=None) -> dict:

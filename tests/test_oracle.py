@@ -99,3 +99,46 @@ def test_reference_importable_cross_check():
         t = potra.transpose_oracle(g)
         toff, tedg = oracle.transpose_c(g.offsets, g.edges, nv)
         assert np.array_equal(toff, t.offsets) and np.array_equal(tedg, t.edges)
+
+
+@pytest.mark.parametrize("threads", [1, 3, 8])
+@pytest.mark.parametrize("method", [None, "atomic", "hlh"])
+def test_potra_port_sorted_matches_goldens(golden_cases, threads, method):
+    """OpenMP port of transpose_potra (hlh.py:441-588) + sort_neighbor_lists == transpose_oracle."""
+    for name, c in golden_cases.items():
+        if c["nv"] == 0:
+            continue
+        toff, tedg, info = oracle.transpose_potra_c(c["off"], c["edg"], c["nv"], threads, k=min(64, c["nv"]),
+                                                    force_method=method, sort=True)
+        assert np.array_equal(toff, c["toff"]) and np.array_equal(tedg, c["tedg"]), (name, method)
+        if method is not None:
+            assert info["method_chosen"] == method
+
+
+def test_potra_port_step0_matches_sample_restatement():
+    """The port's HDV selection = sample_hdv_np (pinned by tests/golden/hdv_cases.npz)."""
+    from paper_2501_06872_b200 import gen
+
+    off, edg = gen.generate_np(gen.CONFIGS["C1"])
+    for k, frac, seed, thr in [(100, 0.01, 0, 4), (1000, 0.05, 7, 3), (50, 1.0, 0, 2)]:
+        ids, est, size = oracle.sample_hdv_np(edg, 1 << 16, k, frac, seed, thr)
+        _, _, info = oracle.transpose_potra_c(off, edg, 1 << 16, thr, k=k, sample_fraction=frac, seed=seed,
+                                              force_method="hlh")
+        assert info["k"] == len(ids) and info["sample_size"] == size
+        assert abs(info["coverage_estimate"] - est) < 1e-12
+
+
+@pytest.mark.parametrize("name", ["C1"])
+def test_host_generator_matches_numpy_generator(name):
+    """oracle.generate_c (bench.py's reference-arm input) == gen.generate_np, bit for bit."""
+    import dataclasses
+
+    from paper_2501_06872_b200 import gen
+
+    cfgs = [gen.CONFIGS[name],
+            dataclasses.replace(gen.CONFIGS["C2"], num_vertices=1 << 14, num_edges=1 << 18),
+            dataclasses.replace(gen.CONFIGS["C3"], num_vertices=1 << 13, num_edges=1 << 17, scale=13)]
+    for cfg in cfgs:
+        o1, e1 = gen.generate_np(cfg)
+        o2, e2 = oracle.generate_c(cfg, 4)
+        assert np.array_equal(o1, o2) and np.array_equal(e1, e2), cfg.name
