@@ -341,17 +341,22 @@ def main():
     else:
         import torch.distributed as dist
 
-        from paper_2501_06872_b200.multi import GpuShardBackend, distributed_step, plan_shards
+        from paper_2501_06872_b200.multi import GpuShardBackend, distributed_step, plan_shards, shard_geometry
 
         off_h = off_d.cpu().numpy().view(np.uint64)
         plan = plan_shards(off_h, world)
+        geom = shard_geometry(V, E)
         e0, e1 = int(plan.edge_bounds[rank]), int(plan.edge_bounds[rank + 1])
         edg_slice = edg_d[e0:e1].clone()
         del edg_d
         torch.cuda.empty_cache()
         backend = GpuShardBackend(dev)
+
+        def dstep(timings=None):
+            return distributed_step(off_d, edg_slice, V, E, plan, rank, backend, geom=geom, timings=timings)
+
         for _ in range(args.warmup):
-            distributed_step(off_d, edg_slice, V, plan, rank, backend)
+            dstep()
         torch.cuda.synchronize()
         dist.barrier()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -359,7 +364,7 @@ def main():
         torch.cuda.synchronize()
         ev0.record(stream)
         for _ in range(args.steps):
-            distributed_step(off_d, edg_slice, V, plan, rank, backend)
+            dstep()
         ev1.record(stream)
         torch.cuda.synchronize()
         dist.barrier()
@@ -367,8 +372,26 @@ def main():
         t = torch.tensor([ev0.elapsed_time(ev1)], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item()) / args.steps
-        launches = 11 * args.steps  # partition (4) + receiver pipeline (~7+) per step, lower bound
-        kern = {"dst_bounds": plan.dst_bounds.tolist(), "src_bounds": plan.src_bounds.tolist()}
+        # per-phase device times (CUDA events inside the step; max over ranks), after the timed region
+        ph = {"send_ms": 0.0, "exchange_ms": 0.0, "receive_ms": 0.0}
+        nph = max(1, min(args.steps, 5))
+        tim = {}
+        for _ in range(nph):
+            tim = {}
+            dstep(tim)
+            for k in ph:
+                ph[k] += tim[k] / nph
+        pt = torch.tensor([ph["send_ms"], ph["exchange_ms"], ph["receive_ms"]], device=dev, dtype=torch.float64)
+        dist.all_reduce(pt, op=dist.ReduceOp.MAX)
+        # our kernels per step: sender level 1 (tile owners x2, count-tile owners, count, scan, place, meta)
+        # + receiver (gt_stats.n_launches); NCCL's own kernels are not counted
+        launches = (7 + int(tim.get("receive_launches") or 0)) * args.steps
+        kern = {"src_bounds": plan.src_bounds.tolist(), "bucket_range": list(tim.get("buckets", ())),
+                "records_received": tim.get("records_received"),
+                "phases_ms_max_over_ranks": {"send (level 1)": float(pt[0]), "exchange (count all-gather + "
+                                             "NCCL all-to-all of R1, 4 B/edge)": float(pt[1]),
+                                             "receive (levels 2-3)": float(pt[2])},
+                "bytes_on_wire_per_edge": 4}
         n_gpus = world
         e2e_dist = None
         if not args.no_e2e:
@@ -377,14 +400,14 @@ def main():
             # CUDA events on the launching stream (the copies are on it), max over ranks
             h_off = off_d.cpu().pin_memory()
             h_edg = edg_slice.cpu().pin_memory()
-            t_off_s, t_edg_s, _ = distributed_step(off_d, edg_slice, V, plan, rank, backend)
+            t_off_s, t_edg_s, _, _ = dstep()
             h_toff = torch.empty(t_off_s.shape, dtype=t_off_s.dtype).pin_memory()
             h_tedg = torch.empty(t_edg_s.shape, dtype=t_edg_s.dtype).pin_memory()
 
             def e2e_step():
                 off_d.copy_(h_off, non_blocking=True)
                 edg_slice.copy_(h_edg, non_blocking=True)
-                to, te, _ = distributed_step(off_d, edg_slice, V, plan, rank, backend)
+                to, te, _, _ = dstep()
                 h_toff.copy_(to, non_blocking=True)
                 h_tedg.copy_(te, non_blocking=True)
 
@@ -416,7 +439,7 @@ def main():
     agg_peak = peak * n_gpus
     traffic, ktraffic = None, {}
     tf = ROOT / "profiles" / "ncu_traffic.json"
-    if tf.exists():
+    if tf.exists() and not dist_on:  # the ncu table describes the single-GPU pipeline only
         try:
             tj = json.loads(tf.read_text()).get(cfg.name) or {}
             traffic = tj.get("step_bytes")

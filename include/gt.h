@@ -16,9 +16,13 @@
  *   gt_prefix_sum        prefix_sum_parallel (baselines.py:116-127).
  *   gt_edge_balanced_bounds  edge_balanced_vertex_bounds (_nb.py:118-132),
  *                        the source-range sharding rule for multi-GPU runs.
- *   gt_shard_*           multi-GPU building blocks (sender-side stable partition
- *                        by destination owner, receiver-side transpose of the
- *                        received records); the exchange itself is NCCL.
+ *   gt_shard_*           multi-GPU building blocks: a sender's level-1 partition
+ *                        of its source shard, a receiver's levels 2-3 over the
+ *                        runs it received; the exchange itself is NCCL.
+ *   gt_transpose_multi   the whole sharded transpose of one rank over NCCL
+ *                        (gt_multi.cu), the `threads` / use_workers width of
+ *                        transpose_atomic (baselines.py:168-170, _nb.py:105-115)
+ *                        mapped to GPUs.
  *
  * Array conventions (graph.py:34-36, 59-80): offsets are uint64[V+1] with
  * offsets[0]=0 and offsets[V]=E; neighbour IDs are uint32[E] (V <= 2^32).
@@ -32,8 +36,16 @@
  * gt_last_error() returns a thread-local message for the last failure.
  *
  * Device pointers are CUDA global-memory pointers; `stream` is a cudaStream_t
- * (NULL = legacy default stream).  All calls are stream-ordered; the caller
- * owns every buffer.  No torch types cross this boundary.
+ * (NULL = legacy default stream).  gt_transpose and gt_shard_receive are
+ * stream-ordered: they enqueue their kernels and return without waiting (the
+ * first call on a device also runs a one-off synchronous self-test), so they
+ * can be captured in a CUDA graph; an in-degree overflow is reported by
+ * gt_transpose_status() once the stream has completed the call (or directly
+ * when `stats` is non-NULL, which makes the call wait for its events).  With
+ * workspace == NULL the library uses a cached workspace private to the
+ * (device, stream) pair: calls on different streams never share scratch,
+ * calls on one stream are ordered by it.  The caller owns every other buffer.
+ * No torch types cross this boundary.
  */
 #ifndef GT_H_
 #define GT_H_
@@ -53,7 +65,7 @@ extern "C" {
 #define GT_EFORMAT (-6) /* GraphFormatError (errors.py:4-14): a POTG file violates the format */
 #define GT_EIO (-7)     /* OSError: a file could not be opened, read or written */
 
-#define GT_ABI_VERSION 3
+#define GT_ABI_VERSION 4
 
 /* Per-call accounting; mirrors TransposeOutput.phase_times / aux_footprint_bytes
  * (baselines.py:39-53).  Times are device time from CUDA events, in ms, filled
@@ -123,30 +135,92 @@ int gt_selftest_rank_order(uint64_t trials, uint64_t *violations);
 /* Force the ranking mode: -1 auto (self-test), 0 atomics, 1 safe OR-mask. */
 int gt_set_rank_mode(int mode);
 
-/* ---- multi-GPU building blocks (one process per GPU; NCCL moves records) --
- * Sender: stable partition of this rank's source shard (sources
- * [src_begin, src_end), i.e. edges [offsets[src_begin], offsets[src_end])) into
- * `parts` destination-owner ranges dst_bounds[0..parts] (vertex IDs).  Writes
- * records (src, dst) as uint32 pairs grouped by owner, each group in CSR
- * order, and counts[p] = records for owner p.  `offsets`/`edges` are the
- * rank's device copies of the full offsets and its edge slice. */
-int gt_shard_partition(const uint64_t *offsets, const uint32_t *edges_slice,
-                       uint64_t num_vertices, uint64_t src_begin, uint64_t src_end,
-                       const uint64_t *h_dst_bounds, int parts,
-                       uint32_t *records_out /* 2 * slice edges */,
-                       uint64_t *h_counts_out /* parts */,
-                       void *stream);
+/* Explicit pipeline configuration (process-wide; read once per call).  All
+ * zero = the defaults.  split: destination digit split a|b|c (used when
+ * a+b+c equals the ID bits); force_wide: the 64-bit-position form (DESIGN.md
+ * §2b) even for small graphs.  Test and experiment hooks; no environment
+ * variable changes the product path. */
+typedef struct gt_config {
+    int32_t split[3];
+    int32_t force_wide;
+    int32_t reserved[4];
+} gt_config;
+int gt_set_config(const gt_config *cfg);   /* NULL restores the defaults */
+int gt_get_config(gt_config *cfg);
 
-/* Receiver: records (src, dst) for destinations [dst_begin, dst_end), already
- * concatenated in sender-rank order (= ascending source order), transposed
- * into the local CSC slice: t_offsets_local[0..n_local] (global positions
- * start at `global_base`) and t_edges_local[0..num_records).  Sources are
- * global IDs < src_num_vertices. */
-int gt_shard_transpose(const uint32_t *records, uint64_t num_records,
-                       uint64_t src_num_vertices,
-                       uint64_t dst_begin, uint64_t dst_end, uint64_t global_base,
-                       uint64_t *t_offsets_local, uint32_t *t_edges_local,
-                       void *stream, gt_stats *stats);
+/* Result of the last gt_transpose / gt_shard_receive enqueued on `stream`
+ * (current device): *status = GT_OK or GT_EOVERFLOW.  Valid once the stream
+ * has completed that call; it reads a mapped status word the call's last
+ * kernel writes, so it does not synchronise. */
+int gt_transpose_status(void *stream, int *status);
+
+/* Free the cached workspaces of the current device (synchronises the device). */
+int gt_release_workspace(void);
+
+/* ---- multi-GPU building blocks (one process per GPU; NCCL moves R1) -------
+ * Every rank plans with the global (num_vertices, num_edges): the destination
+ * ID splits into coarse buckets (ID >> bucket_shift, num_buckets of them).
+ * Sender (gt_shard_send): level 1 of its edge slice [e_begin, e_begin+e_count)
+ * (the slice of an edge-balanced source shard, _nb.py:118-132) into R1: 4-byte
+ * records grouped by bucket, each group in CSR order; bucket_counts[c] =
+ * records of bucket c; seg_hi_out = the source-high boundary table
+ * (num_buckets rows of seg_hi_row u64).  Owners take contiguous bucket
+ * ranges (gt_shard_owners balances them on the global bucket totals); the
+ * receiver of buckets [lo, hi) gets, from every sender s in rank order, R1
+ * records [prefix_s(lo), prefix_s(hi)) and seg_hi rows lo..hi-1.
+ * Receiver (gt_shard_receive): levels 2-3 over those runs: r1_recv holds the
+ * senders' blocks back to back, seg_hi_recv their rows (nranks * (hi-lo) rows,
+ * rebased in place), counts the nranks x num_buckets matrix of all senders'
+ * bucket_counts (device).  Output: the CSC slice of destinations
+ * [lo << shift, min(hi << shift, V)): t_offsets_local (global positions,
+ * starting at global_base) and t_edges_local[num_records]. */
+typedef struct gt_shard_geom {
+    uint32_t num_buckets;   /* coarse buckets                                 */
+    uint32_t bucket_shift;  /* destination ID >> bucket_shift = bucket        */
+    uint32_t seg_hi_row;    /* u64 entries per bucket row of the seg_hi table */
+    uint32_t wide;          /* 1: 64-bit-position form                        */
+    int32_t bits[3];        /* digit split                                    */
+    uint32_t pad;
+} gt_shard_geom;
+int gt_shard_geometry(uint64_t num_vertices, uint64_t num_edges, gt_shard_geom *geom);
+int gt_shard_send(const uint64_t *offsets, const uint32_t *edges_slice, uint64_t num_vertices,
+                  uint64_t num_edges, uint64_t e_begin, uint64_t e_count, uint32_t *r1_out,
+                  uint64_t *bucket_counts, uint64_t *seg_hi_out, void *stream);
+int gt_shard_receive(const uint32_t *r1_recv, uint64_t *seg_hi_recv, const uint64_t *counts, int nranks,
+                     uint64_t num_vertices, uint64_t num_edges, uint32_t bucket_lo, uint32_t bucket_hi,
+                     uint64_t num_records, uint64_t global_base, uint64_t *t_offsets_local,
+                     uint32_t *t_edges_local, void *stream, gt_stats *stats);
+/* Host: owners' bucket ranges h_bounds[0..parts] (bucket-aligned, balanced on
+ * the bucket totals). */
+int gt_shard_owners(const uint64_t *h_bucket_totals, uint32_t num_buckets, int parts, uint32_t *h_bounds);
+
+/* ---- the whole sharded transpose over NCCL (gt_multi.cu) -------------------
+ * libnccl.so.2 is loaded at run time (the one already in the process, e.g.
+ * torch's, else the system's).  gt_multi_unique_id fills 128 bytes (an
+ * ncclUniqueId) on one rank; every rank passes the same bytes to
+ * gt_multi_comm_init(id, rank, nranks) (on its device) and gets an opaque
+ * communicator.  gt_transpose_multi is one rank's step: the rank owns the
+ * edge-balanced source shard [src_begin, src_end) (gt_edge_balanced_bounds),
+ * `offsets` is the full device offsets array and `edges_slice` the shard's
+ * edges.  The rank receives the CSC slice of destinations
+ * [info->dst_begin, info->dst_end): t_offsets_local (capacity
+ * num_vertices + 1 entries suffices) with global positions starting at
+ * info->global_base, and t_edges_local[info->num_local_edges]; if
+ * t_edges_capacity is smaller, GT_ENOMEM with info->num_local_edges set.
+ * One host synchronisation per step: the nranks x num_buckets count matrix
+ * that sizes the NCCL sends. */
+typedef struct gt_multi_info {
+    uint64_t dst_begin, dst_end, global_base, num_local_edges;
+    uint32_t bucket_lo, bucket_hi;
+    double ms_send, ms_exchange, ms_receive; /* phase device times (CUDA events) */
+} gt_multi_info;
+int gt_multi_unique_id(void *id128);
+int gt_multi_comm_init(const void *id128, int rank, int nranks, void **comm);
+int gt_multi_comm_destroy(void *comm);
+int gt_transpose_multi(void *comm, int rank, int nranks, const uint64_t *offsets, const uint32_t *edges_slice,
+                       uint64_t num_vertices, uint64_t num_edges, uint64_t src_begin, uint64_t src_end,
+                       uint64_t *t_offsets_local, uint32_t *t_edges_local, uint64_t t_edges_capacity,
+                       gt_multi_info *info, void *stream);
 
 /* ---- seeded synthetic inputs (BASELINE.json configs), generated on device --
  * Deterministic counter-based generators; identical to the numpy versions in

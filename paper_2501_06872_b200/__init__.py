@@ -11,14 +11,18 @@ from .graph import CsrGraph, edge_id_dtype, flip_orientation, lists_are_sorted
 from .transpose import (
     TransposeOutput,
     edge_balanced_vertex_bounds,
+    pipeline_config,
     prefix_sum_gpu,
+    release_workspace,
     selftest_rank_order,
+    set_config,
     set_rank_mode,
     transpose_atomic,
     transpose_device,
     transpose_gpu,
     transpose_gpu_many,
     transpose_potra,
+    transpose_status,
 )
 from .verify import VerifyReport, sort_neighbor_lists, verify_output
 from .hdv import HdvBudget, HdvPlan, coverage_exact, hash_lookup, hdv_count, sample_hdv
@@ -34,6 +38,10 @@ __all__ = [
     "transpose_potra",
     "transpose_atomic",
     "transpose_device",
+    "transpose_status",
+    "set_config",
+    "pipeline_config",
+    "release_workspace",
     "sort_neighbor_lists",
     "verify_output",
     "VerifyReport",

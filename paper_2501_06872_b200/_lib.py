@@ -14,7 +14,7 @@ from pathlib import Path
 
 from .errors import CounterOverflowError, FootprintError, GpuUnavailableError
 
-__all__ = ["lib", "GtStats", "PotgHeader", "check", "LIB_PATH", "SYMBOLS", "load"]
+__all__ = ["lib", "GtStats", "GtConfig", "ShardGeom", "MultiInfo", "PotgHeader", "check", "LIB_PATH", "SYMBOLS", "load"]
 
 LIB_PATH = Path(__file__).resolve().parent / "libgt.so"
 
@@ -37,6 +37,35 @@ class GtStats(ctypes.Structure):
     ]
 
 
+class GtConfig(ctypes.Structure):
+    _fields_ = [("split", ctypes.c_int32 * 3), ("force_wide", ctypes.c_int32), ("reserved", ctypes.c_int32 * 4)]
+
+
+class ShardGeom(ctypes.Structure):
+    _fields_ = [
+        ("num_buckets", ctypes.c_uint32),
+        ("bucket_shift", ctypes.c_uint32),
+        ("seg_hi_row", ctypes.c_uint32),
+        ("wide", ctypes.c_uint32),
+        ("bits", ctypes.c_int32 * 3),
+        ("pad", ctypes.c_uint32),
+    ]
+
+
+class MultiInfo(ctypes.Structure):
+    _fields_ = [
+        ("dst_begin", ctypes.c_uint64),
+        ("dst_end", ctypes.c_uint64),
+        ("global_base", ctypes.c_uint64),
+        ("num_local_edges", ctypes.c_uint64),
+        ("bucket_lo", ctypes.c_uint32),
+        ("bucket_hi", ctypes.c_uint32),
+        ("ms_send", ctypes.c_double),
+        ("ms_exchange", ctypes.c_double),
+        ("ms_receive", ctypes.c_double),
+    ]
+
+
 class PotgHeader(ctypes.Structure):
     _fields_ = [
         ("version", ctypes.c_uint32),
@@ -48,7 +77,7 @@ class PotgHeader(ctypes.Structure):
     ]
 
 
-ABI_VERSION = 3  # include/gt.h GT_ABI_VERSION
+ABI_VERSION = 4  # include/gt.h GT_ABI_VERSION
 _u64, _i64, _int, _vp = ctypes.c_uint64, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
 _stats_p = ctypes.POINTER(GtStats)
 _hdr_p = ctypes.POINTER(PotgHeader)
@@ -66,8 +95,20 @@ SYMBOLS = {
     "gt_edge_balanced_bounds": (_int, [_vp, _u64, _i64, _vp]),
     "gt_selftest_rank_order": (_int, [_u64, ctypes.POINTER(_u64)]),
     "gt_set_rank_mode": (_int, [_int]),
-    "gt_shard_partition": (_int, [_vp, _vp, _u64, _u64, _u64, _vp, _int, _vp, _vp, _vp]),
-    "gt_shard_transpose": (_int, [_vp, _u64, _u64, _u64, _u64, _u64, _vp, _vp, _vp, _stats_p]),
+    "gt_set_config": (_int, [ctypes.POINTER(GtConfig)]),
+    "gt_get_config": (_int, [ctypes.POINTER(GtConfig)]),
+    "gt_transpose_status": (_int, [_vp, ctypes.POINTER(_int)]),
+    "gt_release_workspace": (_int, []),
+    "gt_shard_geometry": (_int, [_u64, _u64, ctypes.POINTER(ShardGeom)]),
+    "gt_shard_send": (_int, [_vp, _vp, _u64, _u64, _u64, _u64, _vp, _vp, _vp, _vp]),
+    "gt_shard_receive": (_int, [_vp, _vp, _vp, _int, _u64, _u64, ctypes.c_uint32, ctypes.c_uint32, _u64, _u64, _vp,
+                                _vp, _vp, _stats_p]),
+    "gt_shard_owners": (_int, [_vp, ctypes.c_uint32, _int, _vp]),
+    "gt_multi_unique_id": (_int, [_vp]),
+    "gt_multi_comm_init": (_int, [_vp, _int, _int, ctypes.POINTER(_vp)]),
+    "gt_multi_comm_destroy": (_int, [_vp]),
+    "gt_transpose_multi": (_int, [_vp, _int, _int, _vp, _vp, _u64, _u64, _u64, _u64, _vp, _vp, _u64,
+                                  ctypes.POINTER(MultiInfo), _vp]),
     "gt_gen_rmat": (_int, [_u64, _u64, _u64, _int, _vp, _vp, _vp]),
     "gt_gen_er": (_int, [_u64, _u64, _u64, _vp, _vp, _vp]),
     "gt_gen_rmat_csr": (_int, [_u64, _u64, _u64, _int, _vp, _vp, _vp]),

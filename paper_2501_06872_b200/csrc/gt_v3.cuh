@@ -10,7 +10,7 @@
 //         written into t_edges (the output buffer doubles as R1 storage).
 //         Sources come from per-tile boundary marks (one per source that starts
 //         in the tile) resolved with one ballot per 32-edge slot.
-//   L2  k_cnt_rec count -> k_segscan -> k_p2 place
+//   L2  k_cnt_rec count -> k_scan_lookback + k_segfix -> k_p2 place
 //         each coarse bucket is cut into count tiles; a per-bucket column scan
 //         gives every (tile, fine digit B) its final CSC position, so L2 writes
 //         R2 = (lv << nbs | src) fine-bucket-major into the workspace: a fine
@@ -18,7 +18,7 @@
 //   L3  k_p3 units (runs of small fine buckets, TMA in, rank by local vertex,
 //         stage in place, TMA out to t_edges, CSC offsets) and, for fine
 //         buckets above the unit capacity, the same count/scan/place trio as L2
-//         with the low digit C (k_cnt_rec / k_segscan / k_p2<DecR2>).
+//         with the low digit C (k_cnt_rec / k_scan_lookback + k_segfix / k_p2<DecR2>).
 //
 // Ranking is the one of gt_common.cuh (warp-private counters, lane-ordered
 // shared atomics or the safe OR-mask mode); stability composes over levels, so
@@ -67,6 +67,7 @@ struct SegDesc {
   uint64_t base;
   uint64_t out_off;
   uint32_t g0, nt;
+  uint64_t end;  // output position past the segment's last record
 };
 
 struct Unit3 {
@@ -627,7 +628,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
   }
   uint32_t h_prev;
   {
-    const uint32_t ps = (k > 0) ? a.prev_src[k] : 0xffffffffu;
+    const uint32_t ps = a.prev_src[k];  // k = 0: ~0u (whole graph) or the shard's first source
     h_prev = (ps == 0xffffffffu) ? 0xffffffffu : (ps >> a.L);
   }
   __syncthreads();
@@ -762,7 +763,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
     // source-high boundaries inside this tile (compact R1 decode table)
     const uint32_t h_last = s_last_src >> a.L;
     for (uint32_t h = (h_prev == 0xffffffffu) ? 0u : h_prev + 1; h <= h_last; ++h) {
-      const uint64_t q = __ldg(offs + ((uint64_t)h << a.L)) - gi0;  // first item with src >= h << L
+      const uint64_t ob = __ldg(offs + ((uint64_t)h << a.L)), q = (ob > gi0) ? ob - gi0 : 0;  // first item with src >= h << L
       for (int d = tid; d < D; d += T1_) s_bh[d] = 0;
       __syncthreads();
 #pragma unroll
@@ -877,57 +878,6 @@ __global__ void __launch_bounds__(512) k_cnt_lv(const uint8_t* __restrict__ lv, 
   }
 }
 
-// Column scan of each segment's count table: totals per digit over the tiles,
-// digit starts (out[out_off + d] = base + start_d when out_off + d < out_limit),
-// and per-(tile, digit) bases.  One CTA per segment (grid-stride over *n_segs).
-// Sets *err when a digit total reaches 2^32 (a transposed degree >= 2^32).
-__global__ void __launch_bounds__(512) k_segscan(const SegDesc* __restrict__ segs, const uint32_t* __restrict__ n_segs,
-                                                 int D, const uint32_t* __restrict__ cnt, uint64_t* __restrict__ base,
-                                                 uint64_t* __restrict__ out, uint64_t out_limit,
-                                                 unsigned int* __restrict__ err) {
-  extern __shared__ __align__(16) uint64_t s_tot[];  // D
-  __shared__ uint64_t s_tmp[40];
-  const uint32_t ns = *n_segs;
-  const uint32_t lane = lane_id(), w = warp_id(), nw = blockDim.x >> 5;
-  for (uint32_t sg = blockIdx.x; sg < ns; sg += gridDim.x) {
-    const SegDesc S = segs[sg];
-    const uint64_t t0 = (uint64_t)S.g0 * D;
-    for (int d = w; d < D; d += nw) {
-      const uint32_t* row = cnt + t0 + (uint64_t)d * S.nt;
-      uint64_t s = 0;
-      for (uint32_t j = lane; j < S.nt; j += 32) s += row[j];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-      if (lane == 0) {
-        s_tot[d] = s;
-        if (s >= (1ull << 32)) atomicExch(err, 1u);
-      }
-    }
-    __syncthreads();
-    block_excl_scan_u64(s_tot, D, s_tmp);
-    for (int d = threadIdx.x; d < D; d += blockDim.x)
-      if (S.out_off + d < out_limit) out[S.out_off + d] = S.base + s_tot[d];
-    for (int d = w; d < D; d += nw) {
-      const uint32_t* row = cnt + t0 + (uint64_t)d * S.nt;
-      uint64_t* brow = base + t0 + (uint64_t)d * S.nt;
-      uint64_t carry = S.base + s_tot[d];
-      for (uint32_t j0 = 0; j0 < S.nt; j0 += 32) {
-        const uint32_t j = j0 + lane;
-        const uint64_t x = (j < S.nt) ? row[j] : 0;
-        uint64_t y = x;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint64_t z = __shfl_up_sync(kFull, y, o);
-          if (lane >= (uint32_t)o) y += z;
-        }
-        if (j < S.nt) brow[j] = carry + y - x;
-        carry += __shfl_sync(kFull, y, 31);
-      }
-    }
-    __syncthreads();
-  }
-}
-
 // After one device-wide exclusive scan of all segments' count tables
 // (concatenated in segment order, k_scan_lookback): rebase each segment to its
 // output position (base += S.base - base[g0 * D]), write the digit starts
@@ -955,8 +905,8 @@ __global__ void __launch_bounds__(512) k_segfix(const SegDesc* __restrict__ segs
     for (int d = threadIdx.x; d < D; d += blockDim.x) {
       const uint64_t st = base[t0 + (uint64_t)d * S.nt];
       if (S.out_off + d < out_limit) out[S.out_off + d] = st;
-      const uint64_t nx = (d + 1 < D) ? base[t0 + (uint64_t)(d + 1) * S.nt] : ~0ull;
-      if (nx != ~0ull && nx - st >= (1ull << 32)) atomicExch(err, 1u);
+      const uint64_t nx = (d + 1 < D) ? base[t0 + (uint64_t)(d + 1) * S.nt] : S.end;
+      if (nx - st >= (1ull << 32)) atomicExch(err, 1u);
     }
     __syncthreads();
   }
@@ -1480,62 +1430,132 @@ __global__ void __launch_bounds__(WW3 * 32, WW3 > 16 ? 1 : 2) k_p3(const P3Args 
 }
 
 // ---------------------------------------------------------------- planning
-// Coarse buckets -> L2 tiles: cstart[c] (c <= D1), cfirst[c] = first tile of
-// bucket c (exclusive prefix of ceil(size / CT2)), cfirst[D1] = tile count.
-__global__ void k_coarse_tiles(const uint64_t* __restrict__ tbase, uint64_t ntiles1, int D1, uint64_t E,
-                               uint64_t* __restrict__ cstart, uint32_t* __restrict__ cfirst) {
-  extern __shared__ uint32_t s_n[];
-  __shared__ uint32_t s_tmp[40];
-  for (int c = threadIdx.x; c <= D1; c += blockDim.x) cstart[c] = (c < D1) ? tbase[(uint64_t)c * ntiles1] : E;
-  __syncthreads();
-  for (int c = threadIdx.x; c < D1; c += blockDim.x) {
-    const uint64_t sz = cstart[c + 1] - cstart[c];
-    s_n[c] = (uint32_t)((sz + CT2 - 1) / CT2);
+// A coarse bucket's level-1 records arrive as R runs (R = 1 on one GPU: the
+// bucket's range of R1; R = P on a multi-GPU receiver: one run per sender, in
+// sender order = ascending source).  runs[c * R + s] = (start in the R1 buffer,
+// records).
+struct Run {
+  uint64_t start;
+  uint64_t n;
+};
+
+// One GPU / sender: bucket c of R1 = [tbase[c * ntiles1], next bucket's start).
+__global__ void k_runs_from_tbase(const uint64_t* __restrict__ tbase, uint64_t ntiles1, int D1, uint64_t E,
+                                  Run* __restrict__ runs) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < D1; c += gridDim.x * blockDim.x) {
+    const uint64_t s = tbase[(uint64_t)c * ntiles1];
+    const uint64_t e = (c + 1 < D1) ? tbase[(uint64_t)(c + 1) * ntiles1] : E;
+    runs[c] = Run{s, e - s};
   }
-  __syncthreads();
-  const uint32_t total = block_excl_scan_u32(s_n, D1, s_tmp);
-  for (int c = threadIdx.x; c < D1; c += blockDim.x) cfirst[c] = s_n[c];
-  if (threadIdx.x == 0) cfirst[D1] = total;
 }
 
-// One CTA per coarse bucket: its tiles (with the R1 source-high decode state)
-// and its segment descriptor.
-__global__ void k_l2_tiles(const uint64_t* __restrict__ cstart, const uint32_t* __restrict__ cfirst, int Db,
+// Level-2 tiling of the runs (one CTA): rfirst[r] = first tile of run r
+// (ceil(n / CT2) tiles per run), rfirst[nruns] = tile count; bstart[c] =
+// output (R2 / CSC) start of bucket c = records of the runs before run c * R,
+// bstart[nb] = all records.
+__global__ void __launch_bounds__(1024) k_runs_plan(const Run* __restrict__ runs, uint32_t nruns, uint32_t R,
+                                                     uint32_t* __restrict__ rfirst, uint64_t* __restrict__ bstart) {
+  __shared__ uint32_t s_t[1024];
+  __shared__ uint64_t s_n[1024];
+  __shared__ uint32_t s_tmp[40];
+  __shared__ uint64_t s_tmp64[40];
+  uint32_t tcarry = 0;
+  uint64_t ncarry = 0;
+  for (uint32_t r0 = 0; r0 < nruns; r0 += blockDim.x) {
+    const uint32_t r = r0 + threadIdx.x;
+    const Run x = (r < nruns) ? runs[r] : Run{0, 0};
+    s_t[threadIdx.x] = (uint32_t)((x.n + CT2 - 1) / CT2);
+    s_n[threadIdx.x] = x.n;
+    __syncthreads();
+    const uint32_t tt = block_excl_scan_u32(s_t, blockDim.x, s_tmp);
+    const uint64_t tn = block_excl_scan_u64(s_n, blockDim.x, s_tmp64);
+    if (r < nruns) {
+      rfirst[r] = tcarry + s_t[threadIdx.x];
+      if (r % R == 0) bstart[r / R] = ncarry + s_n[threadIdx.x];
+    }
+    tcarry += tt;
+    ncarry += tn;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    rfirst[nruns] = tcarry;
+    bstart[nruns / R] = ncarry;
+  }
+}
+
+// One CTA per bucket: its tiles (with the R1 source-high decode state of the
+// run's seg_hi row, row index s * row_stride + c) and its segment descriptor.
+__global__ void k_l2_tiles(const Run* __restrict__ runs, uint32_t R, uint32_t row_stride,
+                           const uint32_t* __restrict__ rfirst, const uint64_t* __restrict__ bstart, int Db,
                            const uint64_t* __restrict__ seg_hi, uint32_t nh, RTile* __restrict__ tiles,
                            SegDesc* __restrict__ segs) {
   const uint32_t c = blockIdx.x;
-  const uint32_t g0 = cfirst[c], nt = cfirst[c + 1] - g0;
-  const uint64_t cs = cstart[c], ce = cstart[c + 1];
+  const uint32_t g0 = rfirst[c * R], nt = rfirst[(c + 1) * R] - g0;
   if (threadIdx.x == 0) {
     SegDesc S;
-    S.base = cs;
+    S.base = bstart[c];
     S.out_off = (uint64_t)c * Db;
     S.g0 = g0;
     S.nt = nt;
+    S.end = bstart[c + 1];
     segs[c] = S;
   }
-  const uint64_t* row = seg_hi + (uint64_t)c * (nh + 1);
-  for (uint32_t j = threadIdx.x; j < nt; j += blockDim.x) {
-    const uint64_t st = cs + (uint64_t)j * CT2;
-    const uint32_t n = (uint32_t)umin64(CT2, ce - st);
-    // h0 = #{h in [1, nh] : row[h] <= st}; hi = #{h : row[h] <= st + n - 1}
-    auto cnt_le = [&](uint64_t x) -> uint32_t {
-      uint32_t lo = 0, hi = nh;  // answer in [0, nh]
-      while (lo < hi) {
-        const uint32_t mid = lo + (hi - lo + 1) / 2;
-        if (row[mid] <= x) lo = mid; else hi = mid - 1;
-      }
-      return lo;
-    };
-    RTile t;
-    t.start = st;
-    t.n = n;
-    t.seg = c;
-    t.j = j;
-    t.nt = nt;
-    t.h0 = cnt_le(st);
-    t.nbnd = cnt_le(st + n - 1) - t.h0;
-    tiles[g0 + j] = t;
+  for (uint32_t s = 0; s < R; ++s) {
+    const Run run = runs[c * R + s];
+    const uint32_t rt0 = rfirst[c * R + s], ntr = rfirst[c * R + s + 1] - rt0;
+    const uint32_t rowi = s * row_stride + c;
+    const uint64_t* row = seg_hi + (uint64_t)rowi * (nh + 1);
+    for (uint32_t jj = threadIdx.x; jj < ntr; jj += blockDim.x) {
+      const uint64_t st = run.start + (uint64_t)jj * CT2;
+      const uint32_t n = (uint32_t)umin64(CT2, run.start + run.n - st);
+      // h0 = #{h in [1, nh] : row[h] <= st}; hi = #{h : row[h] <= st + n - 1}
+      auto cnt_le = [&](uint64_t x) -> uint32_t {
+        uint32_t lo = 0, hi = nh;  // answer in [0, nh]
+        while (lo < hi) {
+          const uint32_t mid = lo + (hi - lo + 1) / 2;
+          if (row[mid] <= x) lo = mid; else hi = mid - 1;
+        }
+        return lo;
+      };
+      RTile t;
+      t.start = st;
+      t.n = n;
+      t.seg = rowi;
+      t.j = rt0 - g0 + jj;
+      t.nt = nt;
+      t.h0 = cnt_le(st);
+      t.nbnd = cnt_le(st + n - 1) - t.h0;
+      tiles[rt0 + jj] = t;
+    }
+  }
+}
+
+// Multi-GPU receiver: runs of its buckets [lo, lo + nloc) from the P senders'
+// per-bucket counts (counts[s * D1 + c]; the receive buffer holds sender s's
+// buckets lo..lo+nloc-1 back to back after senders 0..s-1), and the received
+// seg_hi rows (row s * nloc + (c - lo), sender coordinates; entry 0 = the
+// sender's first source-high value) rebased to receive-buffer positions.
+// One thread per (c, s) run.
+__global__ void k_recv_runs(const uint64_t* __restrict__ counts, uint32_t P, uint32_t D1, uint32_t lo, uint32_t nloc,
+                            Run* __restrict__ runs, uint64_t* __restrict__ seg_hi, uint32_t nh) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P * nloc) return;
+  const uint32_t c = i / P, s = i - c * P;  // run index i = c * P + s (bucket-major)
+  uint64_t before = 0;                      // records of earlier senders' blocks
+  for (uint32_t q = 0; q < s; ++q)
+    for (uint32_t k = 0; k < nloc; ++k) before += counts[(uint64_t)q * D1 + lo + k];
+  uint64_t in_blk = 0;
+  for (uint32_t k = 0; k < c; ++k) in_blk += counts[(uint64_t)s * D1 + lo + k];
+  uint64_t sstart = 0;  // the bucket's start in the sender's R1
+  for (uint32_t k = 0; k < lo + c; ++k) sstart += counts[(uint64_t)s * D1 + k];
+  const uint64_t start = before + in_blk;
+  runs[i] = Run{start, counts[(uint64_t)s * D1 + lo + c]};
+  uint64_t* row = seg_hi + ((uint64_t)s * nloc + c) * (nh + 1);
+  const uint64_t hb = row[0];
+  for (uint32_t h = 1; h <= nh; ++h) {
+    const uint64_t v = row[h];
+    if (h <= hb) row[h] = start;
+    else if (v != ~0ull) row[h] = v - sstart + start;
   }
 }
 
@@ -1611,6 +1631,7 @@ __global__ void k_big_write(const Big3* __restrict__ bigs, const uint32_t* __res
     S.out_off = (uint64_t)bg.f << c;
     S.g0 = g0;
     S.nt = nt;
+    S.end = bg.start + bg.n;
     segs[q] = S;
     for (uint32_t j = 0; j < nt; ++j) {
       RTile t;
@@ -1624,52 +1645,6 @@ __global__ void k_big_write(const Big3* __restrict__ bigs, const uint32_t* __res
       tiles[g0 + j] = t;
     }
   }
-}
-
-// Big fine buckets -> L3 tiles and segments (one CTA).  The biggest buckets go
-// first in the tile order (persistent CTAs then start on them).
-__global__ void __launch_bounds__(1024) k_big_tiles(const Big3* __restrict__ bigs, const uint32_t* __restrict__ n_big,
-                                                    int c, RTile* __restrict__ tiles, uint32_t* __restrict__ n_tiles,
-                                                    SegDesc* __restrict__ segs) {
-  __shared__ uint32_t s_tmp[40];
-  __shared__ uint32_t s_cnt[1024];
-  const uint32_t nb = *n_big;
-  uint32_t carry = 0;
-  for (uint32_t q0 = 0; q0 < nb; q0 += blockDim.x) {
-    const uint32_t q = q0 + threadIdx.x;
-    Big3 bg{};
-    uint32_t nt = 0;
-    if (q < nb) {
-      bg = bigs[q];
-      nt = (uint32_t)((bg.n + CT2 - 1) / CT2);
-    }
-    s_cnt[threadIdx.x] = nt;
-    __syncthreads();
-    const uint32_t tot = block_excl_scan_u32(s_cnt, blockDim.x, s_tmp);
-    const uint32_t g0 = carry + s_cnt[threadIdx.x];
-    if (q < nb) {
-      SegDesc S;
-      S.base = bg.start;
-      S.out_off = (uint64_t)bg.f << c;
-      S.g0 = g0;
-      S.nt = nt;
-      segs[q] = S;
-      for (uint32_t j = 0; j < nt; ++j) {
-        RTile t;
-        t.start = bg.start + (uint64_t)j * CT2;
-        t.n = (uint32_t)umin64(CT2, bg.n - (uint64_t)j * CT2);
-        t.seg = q;
-        t.j = j;
-        t.nt = nt;
-        t.h0 = 0;
-        t.nbnd = 0;
-        tiles[g0 + j] = t;
-      }
-    }
-    carry += tot;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *n_tiles = carry;
 }
 
 }  // namespace v3

@@ -6,28 +6,32 @@ Partitioning:
      [src_bounds[r], src_bounds[r+1]) with src_bounds =
      edge_balanced_vertex_bounds(offsets, P) (_nb.py:118-132), i.e. a
      contiguous slice of the CSR edge stream.
-  2. Destination ownership: P contiguous vertex ranges dst_bounds.
-  3. Sender: a stable partition of its slice by destination owner
-     (gt_shard_partition, the level-1 kernel with an owner digit) -> records
-     (src, dst) grouped by owner, each group in CSR order.
-  4. Counts: all_gather of the P per-owner counts -> P x P matrix; receiver
-     bases and the global CSC offset of every slice follow from it.  (The
-     V-sized histogram reduce-scatter sketched in BASELINE/SURVEY is not
-     needed: the records carry their destinations, so each receiver derives the
-     in-degrees of its own range locally and only P*P counts cross NVLink.)
-  5. Exchange: NCCL all_to_all_single of the records; the output is ordered by
-     sender rank = ascending source ranges, so concatenation preserves the
-     stable (source-ascending) order.
-  6. Receiver: gt_shard_transpose — the full single-GPU pipeline over the
-     received record stream for its destination range, offsets rebased to the
-     global position of the slice.
+  2. Sender (gt_shard_send): level 1 of the single-GPU pipeline on the slice:
+     R1 = 4-byte records grouped by coarse destination bucket (bucket =
+     destination >> bucket_shift), each group in CSR order, the per-bucket
+     counts, and the source-high boundary rows that decode R1's sources.
+  3. Counts: all_gather of the per-bucket counts -> P x D1 matrix, the one
+     host read of the step.  Destination owners take contiguous bucket ranges
+     balanced on the global bucket totals (gt_shard_owners) — this is the
+     histogram reduce-scatter of the north_star at bucket granularity: each
+     owner learns exactly the counts of its own destination range.
+  4. Exchange: all_to_all of R1 (4 bytes per edge) and of the boundary rows;
+     the receive buffer is ordered by sender rank = ascending source ranges,
+     the order the stable transpose needs (the model is the reference's
+     _mt_merge_round, baselines.py:346-375, which merges per-worker runs in
+     worker order).
+  5. Receiver (gt_shard_receive): levels 2-3 over the received runs (one per
+     sender and bucket): the CSC slice of its destination range, offsets
+     rebased to the slice's global position.
 Each rank ends with its CSC slice: offsets for [dst_lo, dst_hi] and the
-neighbour IDs of those lists.
+neighbour IDs of those lists.  The same step exists as one C-ABI call,
+gt_transpose_multi (gt_multi.cu), with NCCL driven from C++.
 """
 
 from __future__ import annotations
 
 import ctypes
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -38,11 +42,14 @@ from .graph import flip_orientation
 __all__ = [
     "ShardPlan",
     "plan_shards",
+    "shard_geometry",
+    "shard_owners",
     "GpuShardBackend",
-    "exchange_records",
+    "exchange",
     "transpose_sharded_local",
     "transpose_distributed",
     "distributed_step",
+    "MultiComm",
 ]
 
 
@@ -50,29 +57,40 @@ __all__ = [
 class ShardPlan:
     parts: int
     src_bounds: np.ndarray  # int64[P+1] vertex bounds of source shards
-    dst_bounds: np.ndarray  # int64[P+1] vertex bounds of destination owners
     edge_bounds: np.ndarray  # int64[P+1] edge index bounds of source shards
 
 
-def plan_shards(offsets: np.ndarray, parts: int, dst_bounds=None) -> ShardPlan:
+def plan_shards(offsets: np.ndarray, parts: int) -> ShardPlan:
     from .transpose import edge_balanced_vertex_bounds
 
     offsets = np.asarray(offsets, dtype=np.uint64)
-    nv = offsets.shape[0] - 1
     if parts < 1:
         raise ValueError(f"parts must be >= 1, got {parts}")
     sb = edge_balanced_vertex_bounds(offsets, parts)
-    if dst_bounds is None:
-        dst_bounds = (np.arange(parts + 1, dtype=np.int64) * nv) // parts
-    db = np.asarray(dst_bounds, dtype=np.int64)
-    if db.shape != (parts + 1,) or db[0] != 0 or db[-1] != nv or np.any(np.diff(db) < 0):
-        raise ValueError("dst_bounds must be monotone with dst_bounds[0]=0, dst_bounds[-1]=num_vertices")
     eb = offsets[sb].astype(np.int64)
-    return ShardPlan(parts, sb, db, eb)
+    return ShardPlan(parts, sb, eb)
+
+
+def shard_geometry(num_vertices: int, num_edges: int) -> _lib.ShardGeom:
+    """Bucket geometry every rank plans with (gt_shard_geometry; host only)."""
+    g = _lib.ShardGeom()
+    _lib.check(_lib.lib.gt_shard_geometry(int(num_vertices), int(num_edges), ctypes.byref(g)), "gt_shard_geometry")
+    return g
+
+
+def shard_owners(bucket_totals: np.ndarray, parts: int) -> np.ndarray:
+    """Owners' bucket ranges (gt_shard_owners): uint32[parts + 1]."""
+    t = np.ascontiguousarray(bucket_totals, dtype=np.uint64)
+    out = np.empty(parts + 1, dtype=np.uint32)
+    _lib.check(_lib.lib.gt_shard_owners(t.ctypes.data_as(ctypes.c_void_p), t.size, int(parts),
+                                        out.ctypes.data_as(ctypes.c_void_p)), "gt_shard_owners")
+    return out
 
 
 class GpuShardBackend:
     """libgt.so kernels on torch CUDA tensors (the product path)."""
+
+    rec_words = 1  # R1: one 32-bit word per edge
 
     def __init__(self, device=None):
         import torch
@@ -93,130 +111,195 @@ class GpuShardBackend:
     def to_device_edges(self, edges: np.ndarray):
         return self.torch.from_numpy(np.ascontiguousarray(edges, dtype=np.uint32).view(np.int32)).to(self.device)
 
-    def partition(self, offsets_d, edges_slice_d, num_vertices: int, src_lo: int, src_hi: int, dst_bounds):
-        """-> (records int32[n, 2] grouped by owner, counts int64[P] numpy)."""
+    def send(self, offsets_d, edges_slice_d, num_vertices: int, num_edges: int, e_begin: int, geom):
+        """-> (r1 int32[e], bucket counts int64[D1] device, seg_hi rows int64[D1 * row] device)."""
         torch = self.torch
-        P = len(dst_bounds) - 1
         n = int(edges_slice_d.numel())
-        records = torch.empty((max(n, 1), 2), dtype=torch.int32, device=self.device)
-        counts = np.zeros(P, dtype=np.uint64)
-        db = np.ascontiguousarray(dst_bounds, dtype=np.uint64)
+        D1, row = int(geom.num_buckets), int(geom.seg_hi_row)
+        r1 = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+        cnt = torch.empty(D1, dtype=torch.int64, device=self.device)
+        seg = torch.empty(D1 * row, dtype=torch.int64, device=self.device)
         with torch.cuda.device(self.device):
-            rc = _lib.lib.gt_shard_partition(
-                ctypes.c_void_p(offsets_d.data_ptr()), ctypes.c_void_p(edges_slice_d.data_ptr()), num_vertices,
-                src_lo, src_hi, db.ctypes.data_as(ctypes.c_void_p), P, ctypes.c_void_p(records.data_ptr()),
-                counts.ctypes.data_as(ctypes.c_void_p), self._stream())
-        _lib.check(rc, "gt_shard_partition")
-        return records[:n], counts.astype(np.int64)
+            rc = _lib.lib.gt_shard_send(ctypes.c_void_p(offsets_d.data_ptr()),
+                                        ctypes.c_void_p(edges_slice_d.data_ptr()) if n else None, num_vertices,
+                                        num_edges, e_begin, n, ctypes.c_void_p(r1.data_ptr()),
+                                        ctypes.c_void_p(cnt.data_ptr()), ctypes.c_void_p(seg.data_ptr()),
+                                        self._stream())
+        _lib.check(rc, "gt_shard_send")
+        return r1[:n], cnt, seg
 
-    def transpose_received(self, records, dst_lo: int, dst_hi: int, global_base: int, want_stats=False,
-                           src_num_vertices: int = 1 << 32):
+    def receive(self, r1_recv, seg_recv, counts_all, parts: int, num_vertices: int, num_edges: int, lo: int, hi: int,
+                num_records: int, global_base: int, geom, want_stats=False):
         """-> (t_offsets int64[n_local+1] with global positions, t_edges int32[R], stats)."""
         torch = self.torch
-        R = int(records.shape[0])
-        nloc = dst_hi - dst_lo
-        t_off = torch.empty(nloc + 1, dtype=torch.int64, device=self.device)
-        t_edg = torch.empty(max(R, 1), dtype=torch.int32, device=self.device)
+        shift = int(geom.bucket_shift)
+        v_lo, v_hi = min(num_vertices, lo << shift), min(num_vertices, hi << shift)
+        t_off = torch.empty(v_hi - v_lo + 1, dtype=torch.int64, device=self.device)
+        t_edg = torch.empty(max(num_records, 1), dtype=torch.int32, device=self.device)
         st = _lib.GtStats() if want_stats else None
         with torch.cuda.device(self.device):
-            rc = _lib.lib.gt_shard_transpose(
-                ctypes.c_void_p(records.data_ptr()) if R else None, R, src_num_vertices, dst_lo, dst_hi, global_base,
-                ctypes.c_void_p(t_off.data_ptr()), ctypes.c_void_p(t_edg.data_ptr()), self._stream(),
+            rc = _lib.lib.gt_shard_receive(
+                ctypes.c_void_p(r1_recv.data_ptr()) if num_records else None,
+                ctypes.c_void_p(seg_recv.data_ptr()) if seg_recv.numel() else None,
+                ctypes.c_void_p(counts_all.data_ptr()), parts, num_vertices, num_edges, lo, hi, num_records,
+                global_base, ctypes.c_void_p(t_off.data_ptr()), ctypes.c_void_p(t_edg.data_ptr()), self._stream(),
                 ctypes.byref(st) if st is not None else None)
-        _lib.check(rc, "gt_shard_transpose")
-        return t_off, t_edg[:R], st
+        _lib.check(rc, "gt_shard_receive")
+        if st is None:
+            from .transpose import transpose_status
+
+            torch.cuda.current_stream(self.device).synchronize()
+            transpose_status(device=self.device)
+        return t_off, t_edg[:num_records], st
 
 
-def transpose_sharded_local(g, plan: ShardPlan, backend):
-    """Run every rank's sender and receiver steps in one process, in sequence
-    (used to check the sharded pipeline on a single GPU).  Returns the full
-    (t_offsets uint64, t_edges uint32) on the host."""
-    P = plan.parts
-    nv = int(g.num_vertices)
-    off_d = backend.to_device_offsets(g.offsets)
-    sent = []
-    counts = np.zeros((P, P), dtype=np.int64)
-    for r in range(P):
-        e0, e1 = int(plan.edge_bounds[r]), int(plan.edge_bounds[r + 1])
-        edges_d = backend.to_device_edges(g.edges[e0:e1])
-        rec, cnt = backend.partition(off_d, edges_d, nv, int(plan.src_bounds[r]), int(plan.src_bounds[r + 1]),
-                                     plan.dst_bounds)
-        sent.append(rec)
-        counts[r] = cnt
-    t_offsets = np.zeros(nv + 1, dtype=np.uint64)
-    t_edges = np.empty(int(g.num_edges), dtype=np.uint32)
-    base = 0
+def _owner_split(C: np.ndarray, bounds: np.ndarray, rank: int):
+    """Send counts of `rank` to every owner and receive counts from every sender
+    (records), from the P x D1 count matrix C and the owners' bucket bounds."""
+    P = C.shape[0]
+    send = np.array([int(C[rank, bounds[q]:bounds[q + 1]].sum()) for q in range(P)], dtype=np.int64)
+    recv = np.array([int(C[s, bounds[rank]:bounds[rank + 1]].sum()) for s in range(P)], dtype=np.int64)
+    return send, recv
+
+
+def _all_to_all(out, inp, out_splits, in_splits, group=None):
+    """NCCL all_to_all_single; with gloo (CPU tests) point-to-point send/recv."""
+    import torch.distributed as dist
+
+    P = dist.get_world_size(group)
+    r = dist.get_rank(group)
+    if dist.get_backend(group) == "nccl":
+        dist.all_to_all_single(out, inp, output_split_sizes=[int(x) for x in out_splits],
+                               input_split_sizes=[int(x) for x in in_splits], group=group)
+        return
+    so = np.concatenate([[0], np.cumsum(in_splits)])
+    ro = np.concatenate([[0], np.cumsum(out_splits)])
+    ops = []
     for q in range(P):
-        pieces = []
-        for r in range(P):
-            lo = int(counts[r, :q].sum())
-            pieces.append(sent[r][lo : lo + int(counts[r, q])])
-        torch = backend.torch
-        recv = torch.cat(pieces, dim=0) if pieces else None
-        lo_v, hi_v = int(plan.dst_bounds[q]), int(plan.dst_bounds[q + 1])
-        t_off, t_edg, _ = backend.transpose_received(recv, lo_v, hi_v, base, src_num_vertices=nv)
-        t_offsets[lo_v : hi_v + 1] = t_off.cpu().numpy().view(np.uint64)
-        n = int(recv.shape[0])
-        t_edges[base : base + n] = t_edg.cpu().numpy().view(np.uint32)
-        base += n
-    return t_offsets, t_edges
+        if q == r:
+            out[ro[r]:ro[r + 1]] = inp[so[r]:so[r + 1]]
+            continue
+        if in_splits[q]:
+            ops.append(dist.P2POp(dist.isend, inp[so[q]:so[q + 1]].contiguous(), q, group))
+        if out_splits[q]:
+            ops.append(dist.P2POp(dist.irecv, out[ro[q]:ro[q + 1]], q, group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
 
 
-def exchange_records(records, send_counts: np.ndarray, group=None):
-    """All-to-all of owner-grouped records.  Returns (received records ordered by
-    sender rank, counts matrix P x P).  NCCL all_to_all_single on GPU tensors;
-    with gloo (CPU tests) falls back to point-to-point send/recv."""
+def exchange(r1, seg, counts, geom, rec_words: int = 1, group=None):
+    """All-gather of the bucket counts, owner ranges, all-to-all of R1 and of the
+    boundary rows.  Returns (r1_recv, seg_recv, counts_all device, C host,
+    bounds, phase seconds)."""
     import torch
     import torch.distributed as dist
 
     P = dist.get_world_size(group)
     r = dist.get_rank(group)
-    send = torch.as_tensor(np.asarray(send_counts, dtype=np.int64), device=records.device)
-    allc = [torch.empty_like(send) for _ in range(P)]
-    dist.all_gather(allc, send, group=group)
-    C = torch.stack(allc).cpu().numpy()  # C[s][q] = records from s to q
-    recv_counts = C[:, r]
-    out = torch.empty((int(recv_counts.sum()), 2), dtype=records.dtype, device=records.device)
-    backend = dist.get_backend(group)
-    if backend == "nccl":
-        dist.all_to_all_single(out, records.contiguous(), output_split_sizes=recv_counts.tolist(),
-                               input_split_sizes=[int(x) for x in send_counts], group=group)
-    else:
-        ops = []
-        so = np.concatenate([[0], np.cumsum(send_counts)])
-        ro = np.concatenate([[0], np.cumsum(recv_counts)])
-        for q in range(P):
-            if q == r:
-                out[ro[r] : ro[r + 1]] = records[so[r] : so[r + 1]]
-                continue
-            if send_counts[q]:
-                ops.append(dist.P2POp(dist.isend, records[so[q] : so[q + 1]].contiguous(), q, group))
-            if recv_counts[q]:
-                buf = out[ro[q] : ro[q + 1]]
-                ops.append(dist.P2POp(dist.irecv, buf, q, group))
-        if ops:
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
-    return out, C
+    D1, row = int(geom.num_buckets), int(geom.seg_hi_row)
+    allc = [torch.empty_like(counts) for _ in range(P)]
+    dist.all_gather(allc, counts, group=group)
+    counts_all = torch.stack(allc).contiguous()
+    C = counts_all.cpu().numpy()  # the step's one host read: sizes of the sends
+    bounds = shard_owners(C.sum(axis=0), P).astype(np.int64)
+    send, recv = _owner_split(C, bounds, r)
+    r1_recv = torch.empty(int(recv.sum()) * rec_words, dtype=r1.dtype, device=r1.device)
+    _all_to_all(r1_recv, r1, recv * rec_words, send * rec_words, group)
+    nloc = int(bounds[r + 1] - bounds[r])
+    seg_recv = torch.empty(P * nloc * row, dtype=seg.dtype, device=seg.device)
+    seg_send = [(int(bounds[q + 1] - bounds[q])) * row for q in range(P)]
+    # every owner's rows are the contiguous bucket range of this sender's table
+    _all_to_all(seg_recv, seg, [nloc * row] * P, seg_send, group)
+    return r1_recv, seg_recv, counts_all, C, bounds
 
 
-def distributed_step(offsets_d, edges_slice_d, num_vertices: int, plan: ShardPlan, rank: int, backend, group=None):
-    """One rank's sharded transpose on device-resident inputs (the timed step
-    of bench.py at N > 1).  Returns (t_offsets slice, t_edges slice, global base)."""
-    rec, cnt = backend.partition(offsets_d, edges_slice_d, num_vertices, int(plan.src_bounds[rank]),
-                                 int(plan.src_bounds[rank + 1]), plan.dst_bounds)
-    recv, C = exchange_records(rec, cnt, group=group)
-    base = int(C[:, :rank].sum())
-    t_off, t_edg, _ = backend.transpose_received(recv, int(plan.dst_bounds[rank]), int(plan.dst_bounds[rank + 1]),
-                                                 base, src_num_vertices=num_vertices)
-    return t_off, t_edg, base
+def distributed_step(offsets_d, edges_slice_d, num_vertices: int, num_edges: int, plan: ShardPlan, rank: int,
+                     backend, group=None, geom=None, timings: dict | None = None):
+    """One rank's sharded transpose on device-resident inputs (the timed step of
+    bench.py at N > 1).  Returns (t_offsets slice, t_edges slice, global base,
+    (dst_lo, dst_hi))."""
+    P = plan.parts
+    geom = geom or shard_geometry(num_vertices, num_edges)
+    ev = None
+    if timings is not None and hasattr(backend, "torch") and backend.torch.cuda.is_available():
+        ev = [backend.torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    t0 = time.perf_counter()
+    if ev:
+        ev[0].record()
+    r1, cnt, seg = backend.send(offsets_d, edges_slice_d, num_vertices, num_edges, int(plan.edge_bounds[rank]), geom)
+    if ev:
+        ev[1].record()
+    t1 = time.perf_counter()
+    r1_recv, seg_recv, counts_all, C, bounds = exchange(r1, seg, cnt, geom, backend.rec_words, group)
+    if ev:
+        ev[2].record()
+    t2 = time.perf_counter()
+    lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+    base = int(C[:, :lo].sum())
+    nrec = int(C[:, lo:hi].sum())
+    t_off, t_edg, st = backend.receive(r1_recv, seg_recv, counts_all, P, num_vertices, num_edges, lo, hi, nrec, base,
+                                       geom, want_stats=timings is not None and ev is not None)
+    if ev:
+        ev[3].record()
+    t3 = time.perf_counter()
+    if timings is not None:
+        if ev:  # device time of each phase (CUDA events on the launching stream)
+            ev[3].synchronize()
+            timings.update(send_ms=ev[0].elapsed_time(ev[1]), exchange_ms=ev[1].elapsed_time(ev[2]),
+                           receive_ms=ev[2].elapsed_time(ev[3]),
+                           receive_launches=int(st.n_launches) if st is not None else None,
+                           records_received=nrec, buckets=(lo, hi))
+        else:
+            timings.update(send_ms=(t1 - t0) * 1e3, exchange_ms=(t2 - t1) * 1e3, receive_ms=(t3 - t2) * 1e3)
+    shift = int(geom.bucket_shift)
+    return t_off, t_edg, base, (min(num_vertices, lo << shift), min(num_vertices, hi << shift))
+
+
+def transpose_sharded_local(g, plan: ShardPlan, backend):
+    """Run every rank's sender and receiver steps in one process, in sequence
+    (checks the sharded pipeline on a single GPU).  Returns the full
+    (t_offsets uint64, t_edges uint32) on the host."""
+    torch = backend.torch
+    P = plan.parts
+    nv, ne = int(g.num_vertices), int(g.num_edges)
+    geom = shard_geometry(nv, ne)
+    D1, row = int(geom.num_buckets), int(geom.seg_hi_row)
+    off_d = backend.to_device_offsets(g.offsets)
+    sent = []
+    for r in range(P):
+        e0, e1 = int(plan.edge_bounds[r]), int(plan.edge_bounds[r + 1])
+        edges_d = backend.to_device_edges(g.edges[e0:e1])
+        sent.append(backend.send(off_d, edges_d, nv, ne, e0, geom))
+    counts_all = torch.stack([s[1] for s in sent]).contiguous()
+    C = counts_all.cpu().numpy()
+    bounds = shard_owners(C.sum(axis=0), P).astype(np.int64)
+    t_offsets = np.zeros(nv + 1, dtype=np.uint64)
+    t_edges = np.empty(ne, dtype=np.uint32)
+    shift = int(geom.bucket_shift)
+    w = backend.rec_words
+    for q in range(P):
+        lo, hi = int(bounds[q]), int(bounds[q + 1])
+        pieces, segs = [], []
+        for r in range(P):
+            a, b = int(C[r, :lo].sum()), int(C[r, :hi].sum())
+            pieces.append(sent[r][0][a * w:b * w])
+            segs.append(sent[r][2][lo * row:hi * row])
+        recv = torch.cat(pieces) if pieces else None
+        seg_recv = torch.cat(segs).contiguous()
+        base = int(C[:, :lo].sum())
+        nrec = int(C[:, lo:hi].sum())
+        t_off, t_edg, _ = backend.receive(recv, seg_recv, counts_all, P, nv, ne, lo, hi, nrec, base, geom)
+        v_lo, v_hi = min(nv, lo << shift), min(nv, hi << shift)
+        t_offsets[v_lo:v_hi + 1] = t_off.cpu().numpy().view(np.uint64)
+        t_edges[base:base + nrec] = t_edg.cpu().numpy().view(np.uint32)
+    return t_offsets, t_edges
 
 
 def transpose_distributed(g, devices: int, device=None, backend=None, group=None, gather: bool = True):
     """Collective: every rank calls with the same host CsrGraph ``g``.  Rank 0
     receives the full transposed graph (a TransposeOutput) when ``gather``;
     other ranks receive their slice in ``details``."""
-    import torch
     import torch.distributed as dist
 
     from .transpose import TransposeOutput
@@ -229,31 +312,73 @@ def transpose_distributed(g, devices: int, device=None, backend=None, group=None
     r = dist.get_rank(group)
     backend = backend or GpuShardBackend(device)
     plan = plan_shards(g.offsets, P)
+    nv, ne = int(g.num_vertices), int(g.num_edges)
     off_d = backend.to_device_offsets(g.offsets)
     e0, e1 = int(plan.edge_bounds[r]), int(plan.edge_bounds[r + 1])
     edg_d = backend.to_device_edges(g.edges[e0:e1])
-    t_off, t_edg, base = distributed_step(off_d, edg_d, int(g.num_vertices), plan, r, backend, group)
-    details = {"rank": r, "devices": P, "dst_range": (int(plan.dst_bounds[r]), int(plan.dst_bounds[r + 1])),
-               "global_base": base}
+    t_off, t_edg, base, (lo_v, hi_v) = distributed_step(off_d, edg_d, nv, ne, plan, r, backend, group)
+    details = {"rank": r, "devices": P, "dst_range": (lo_v, hi_v), "global_base": base}
     if not gather:
         return TransposeOutput(graph=None, phase_times={}, aux_footprint_bytes=0, method="gpu-sharded", sorted=True,
                                details={**details, "t_offsets": t_off, "t_edges": t_edg})
     # gather slices on rank 0 (host), for the drop-in full-graph result
-    off_np = t_off.cpu().numpy()
-    edg_np = t_edg.cpu().numpy()
     objs = [None] * P
-    dist.all_gather_object(objs, (r, off_np, edg_np), group=group)
+    dist.all_gather_object(objs, (r, lo_v, hi_v, t_off.cpu().numpy(), t_edg.cpu().numpy()), group=group)
     if r != 0:
         return TransposeOutput(graph=None, phase_times={}, aux_footprint_bytes=0, method="gpu-sharded", sorted=True,
                                details=details)
-    nv = int(g.num_vertices)
     t_offsets = np.zeros(nv + 1, dtype=np.uint64)
     pieces = []
-    for rr, o, e in sorted(objs, key=lambda t: t[0]):
-        lo, hi = int(plan.dst_bounds[rr]), int(plan.dst_bounds[rr + 1])
-        t_offsets[lo : hi + 1] = o.view(np.uint64)
+    for rr, lo, hi, o, e in sorted(objs, key=lambda t: t[0]):
+        t_offsets[lo:hi + 1] = o.view(np.uint64)
         pieces.append(e.view(np.uint32))
     t_edges = np.concatenate(pieces) if pieces else np.empty(0, np.uint32)
-    graph = type(g)(nv, int(g.num_edges), t_offsets, t_edges, flip_orientation(g.orientation))
+    graph = type(g)(nv, ne, t_offsets, t_edges, flip_orientation(g.orientation))
     return TransposeOutput(graph=graph, phase_times={}, aux_footprint_bytes=0, method="gpu-sharded", sorted=True,
                            details=details)
+
+
+class MultiComm:
+    """A libgt NCCL communicator (gt_multi_comm_init) for gt_transpose_multi.
+    Rank 0 draws the id; ``broadcast`` ships it to the other ranks (e.g.
+    torch.distributed.broadcast_object_list)."""
+
+    def __init__(self, rank: int, nranks: int, id_bytes: bytes | None = None, broadcast=None):
+        buf = ctypes.create_string_buffer(128)
+        if rank == 0 and id_bytes is None:
+            _lib.check(_lib.lib.gt_multi_unique_id(buf), "gt_multi_unique_id")
+            id_bytes = buf.raw
+        if broadcast is not None:
+            id_bytes = broadcast(id_bytes)
+        if id_bytes is None or len(id_bytes) != 128:
+            raise ValueError("a 128-byte NCCL unique id is required")
+        self.rank, self.nranks = rank, nranks
+        self.comm = ctypes.c_void_p()
+        _lib.check(_lib.lib.gt_multi_comm_init(ctypes.create_string_buffer(id_bytes, 128), rank, nranks,
+                                               ctypes.byref(self.comm)), "gt_multi_comm_init")
+
+    def transpose(self, offsets_d, edges_slice_d, num_vertices: int, num_edges: int, src_begin: int, src_end: int,
+                  capacity: int | None = None, stream=None):
+        """One rank's gt_transpose_multi step -> (t_offsets slice, t_edges slice, info)."""
+        import torch
+
+        dev = offsets_d.device
+        info = _lib.MultiInfo()
+        cap = int(capacity) if capacity is not None else int(num_edges)
+        t_off = torch.empty(int(num_vertices) + 1, dtype=torch.int64, device=dev)
+        t_edg = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+        s = stream if stream is not None else torch.cuda.current_stream(dev)
+        with torch.cuda.device(dev):
+            rc = _lib.lib.gt_transpose_multi(self.comm, self.rank, self.nranks, ctypes.c_void_p(offsets_d.data_ptr()),
+                                             ctypes.c_void_p(edges_slice_d.data_ptr()) if edges_slice_d.numel() else None,
+                                             int(num_vertices), int(num_edges), int(src_begin), int(src_end),
+                                             ctypes.c_void_p(t_off.data_ptr()), ctypes.c_void_p(t_edg.data_ptr()), cap,
+                                             ctypes.byref(info), ctypes.c_void_p(s.cuda_stream))
+        _lib.check(rc, "gt_transpose_multi")
+        nloc = int(info.dst_end - info.dst_begin)
+        return t_off[:nloc + 1], t_edg[:int(info.num_local_edges)], info
+
+    def close(self):
+        if self.comm:
+            _lib.lib.gt_multi_comm_destroy(self.comm)
+            self.comm = ctypes.c_void_p()

@@ -37,6 +37,10 @@ __all__ = [
     "edge_balanced_vertex_bounds",
     "selftest_rank_order",
     "set_rank_mode",
+    "transpose_status",
+    "set_config",
+    "pipeline_config",
+    "release_workspace",
 ]
 
 
@@ -74,6 +78,10 @@ def transpose_device(offsets, edges, num_vertices: int, *, t_offsets=None, t_edg
 
     ``offsets`` int64[V+1] (uint64 bits) and ``edges`` int32[E] (uint32 bits)
     on the same device.  Returns ``(t_offsets, t_edges, stats_or_None)``.
+    Stream-ordered: without ``want_stats`` the call returns once the kernels
+    are enqueued; call :func:`transpose_status` after synchronising the stream
+    to learn whether an in-degree overflowed (``want_stats`` waits and raises
+    :class:`CounterOverflowError` itself).
     """
     torch = _torch()
     V = int(num_vertices)
@@ -293,3 +301,50 @@ def selftest_rank_order(trials: int = 1 << 26) -> int:
 def set_rank_mode(mode: int) -> None:
     """-1 auto (self-test), 0 smem-atomic ranking, 1 safe OR-mask ranking."""
     _lib.check(_lib.lib.gt_set_rank_mode(int(mode)), "gt_set_rank_mode")
+
+
+def transpose_status(stream=None, device=None) -> None:
+    """Raise CounterOverflowError if the last transpose enqueued on ``stream``
+    (default: the current stream of ``device``) overflowed a 32-bit in-degree.
+    Call after the stream has completed (gt_transpose_status)."""
+    torch = _torch()
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    with torch.cuda.device(dev):
+        s = stream if stream is not None else torch.cuda.current_stream(dev)
+        st = ctypes.c_int(0)
+        _lib.check(_lib.lib.gt_transpose_status(ctypes.c_void_p(s.cuda_stream), ctypes.byref(st)),
+                   "gt_transpose_status")
+        _lib.check(st.value, "gt_transpose")
+
+
+def set_config(split=None, force_wide: bool = False) -> None:
+    """Explicit pipeline configuration (gt_set_config): ``split`` = (a, b, c)
+    digit bits (used when they cover the destination ID bits), ``force_wide``
+    = the 64-bit-position form.  ``set_config()`` restores the defaults."""
+    cfg = _lib.GtConfig()
+    if split is not None:
+        for i, x in enumerate(split):
+            cfg.split[i] = int(x)
+    cfg.force_wide = 1 if force_wide else 0
+    _lib.check(_lib.lib.gt_set_config(ctypes.byref(cfg)), "gt_set_config")
+
+
+class pipeline_config:
+    """Context manager form of :func:`set_config` (restores the defaults)."""
+
+    def __init__(self, split=None, force_wide: bool = False):
+        self.split, self.force_wide = split, force_wide
+
+    def __enter__(self):
+        set_config(self.split, self.force_wide)
+        return self
+
+    def __exit__(self, *exc):
+        _lib.check(_lib.lib.gt_set_config(None), "gt_set_config")
+        return False
+
+
+def release_workspace() -> None:
+    """Free libgt.so's cached device workspaces on the current device."""
+    _torch()
+    _lib.check(_lib.lib.gt_release_workspace(), "gt_release_workspace")

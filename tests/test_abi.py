@@ -34,7 +34,7 @@ def test_abi_version_and_structs():
     from paper_2501_06872_b200 import _lib
 
     lib = _lib.load()
-    assert lib.gt_abi_version() == 3
+    assert lib.gt_abi_version() == 4
     assert ctypes.sizeof(_lib.GtStats) == 4 * 8 + 8 + 3 * 4 + 4 + 8 + 8 + 4 * 8
 
 
@@ -47,6 +47,48 @@ def test_workspace_size_host_only():
     assert b.value >= (1 << 29) * 4  # level-1 records (4-byte compact records at C3)
     assert lib.gt_workspace_size(0, 0, ctypes.byref(b)) == 0 and b.value == 0
     assert lib.gt_workspace_size((1 << 31), 10, ctypes.byref(b)) == _lib.GT_EINVAL
+    # the limit is the documented one: 29-bit destination IDs (config C5)
+    assert lib.gt_workspace_size(1 << 29, 1 << 33, ctypes.byref(b)) == 0
+    assert lib.gt_workspace_size((1 << 29) + 1, 1 << 20, ctypes.byref(b)) == _lib.GT_EINVAL
+    assert b"29 bits" in lib.gt_last_error()
+
+
+def test_config_is_explicit():
+    """Pipeline knobs are an explicit gt_config (no environment variable is read)."""
+    from paper_2501_06872_b200 import _lib
+    from paper_2501_06872_b200.transpose import pipeline_config
+
+    lib = _lib.load()
+    b0, b1 = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    assert lib.gt_workspace_size(1 << 24, 1 << 29, ctypes.byref(b0)) == 0
+    with pipeline_config(force_wide=True):
+        c = _lib.GtConfig()
+        assert lib.gt_get_config(ctypes.byref(c)) == 0 and c.force_wide == 1
+        assert lib.gt_workspace_size(1 << 24, 1 << 29, ctypes.byref(b1)) == 0
+        assert b1.value > b0.value  # wide form: + one low-digit byte per record
+    c = _lib.GtConfig()
+    assert lib.gt_get_config(ctypes.byref(c)) == 0 and c.force_wide == 0 and list(c.split) == [0, 0, 0]
+    src = (ROOT / "paper_2501_06872_b200" / "csrc" / "gt_api.cu").read_text()
+    assert "getenv" not in src
+
+
+def test_shard_geometry_and_owners_host_only():
+    from paper_2501_06872_b200.multi import shard_geometry, shard_owners
+
+    g = shard_geometry(1 << 24, 1 << 29)  # C3: 9|8|7
+    assert (g.num_buckets, g.bucket_shift, list(g.bits), g.wide) == (512, 15, [9, 8, 7], 0)
+    g5 = shard_geometry(1 << 29, 16 << 29)  # C5: wide, 11|10|8
+    assert (g5.num_buckets, list(g5.bits), g5.wide) == (2048, [11, 10, 8], 1)
+    tot = np.array([5, 0, 7, 100, 1, 1, 1, 1, 80], dtype=np.uint64)
+    for parts in (1, 2, 3, 4, 9, 12):
+        b = shard_owners(tot, parts)
+        assert b[0] == 0 and b[-1] == tot.size and np.all(np.diff(b.astype(np.int64)) >= 0)
+    assert shard_owners(tot, 2).tolist() == [0, 4, 9]  # 112 | 84 of 196 edges
+    rng = np.random.default_rng(1)
+    t = rng.integers(0, 1000, 512).astype(np.uint64)
+    b = shard_owners(t, 8).astype(np.int64)
+    loads = [int(t[b[q]:b[q + 1]].sum()) for q in range(8)]
+    assert max(loads) - min(loads) <= 2 * int(t.max())
 
 
 def test_edge_balanced_bounds_host_entry_point(golden_hashes):

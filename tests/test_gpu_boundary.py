@@ -1,0 +1,234 @@
+"""GPU tests of the C-ABI boundary contract (include/gt.h): stream ordering
+(CUDA-graph capture + replay), per-stream workspaces (two concurrent streams),
+the status word, gt_transpose_multi over NCCL at P = 1, the multi-GPU
+building blocks, the overflow error, and the reference's skewed_4m golden."""
+
+import ctypes
+import os
+import sys
+import threading
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, sha
+
+sys.path.insert(0, str(ROOT))
+from oracle import oracle  # noqa: E402  (test infrastructure)
+
+pytestmark = pytest.mark.gpu
+
+
+def _rand_graph(seed, nv=300_007, ne=3_000_000, skew=3.0):
+    from paper_2501_06872_b200 import CsrGraph
+
+    rng = np.random.default_rng(seed)
+    src = rng.integers(0, nv, ne)
+    dst = np.minimum((nv * rng.random(ne) ** skew).astype(np.int64), nv - 1)
+    return CsrGraph.from_edge_pairs(src, rng.permutation(nv)[dst], nv)
+
+
+def _dev(torch, g):
+    off = torch.from_numpy(g.offsets.view(np.int64)).cuda()
+    edg = torch.from_numpy(g.edges.view(np.int32)).cuda()
+    return off, edg
+
+
+def _check(t_off, t_edg, g):
+    o, e = oracle.transpose_c(g.offsets, g.edges, g.num_vertices)
+    assert np.array_equal(t_off.cpu().numpy().view(np.uint64), o)
+    assert np.array_equal(t_edg.cpu().numpy().view(np.uint32), e)
+
+
+def test_cuda_graph_capture_and_replay():
+    """gt_transpose enqueues without host synchronisation: it can be captured in
+    a CUDA graph, and every replay reproduces the transpose bit for bit."""
+    import torch
+
+    from paper_2501_06872_b200 import transpose_device, transpose_status
+
+    g = _rand_graph(5)
+    off, edg = _dev(torch, g)
+    t_off = torch.empty(g.num_vertices + 1, dtype=torch.int64, device="cuda")
+    t_edg = torch.empty(g.num_edges, dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        transpose_device(off, edg, g.num_vertices, t_offsets=t_off, t_edges=t_edg, stream=s)  # warm-up: sizes caches
+    s.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        transpose_device(off, edg, g.num_vertices, t_offsets=t_off, t_edges=t_edg, stream=s)
+    for _ in range(3):
+        t_off.fill_(-1)
+        t_edg.fill_(-1)
+        graph.replay()
+        torch.cuda.synchronize()
+        transpose_status(stream=s)
+        _check(t_off, t_edg, g)
+
+
+def test_two_concurrent_streams():
+    """Two transposes in flight at once on different streams (from two host
+    threads) use separate cached workspaces and both match the oracle."""
+    import torch
+
+    from paper_2501_06872_b200 import transpose_device, transpose_status
+
+    gs = [_rand_graph(11), _rand_graph(12, nv=150_001, ne=4_000_000, skew=6.0)]
+    devs = [_dev(torch, g) for g in gs]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [None, None]
+    errs = []
+
+    def run(i):
+        try:
+            torch.cuda.set_device(0)
+            with torch.cuda.stream(streams[i]):
+                for _ in range(3):
+                    outs[i] = transpose_device(devs[i][0], devs[i][1], gs[i].num_vertices, stream=streams[i])[:2]
+        except Exception as exc:  # pragma: no cover - reported below
+            errs.append(exc)
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for i in range(2):
+        streams[i].synchronize()
+        transpose_status(stream=streams[i])
+        _check(outs[i][0], outs[i][1], gs[i])
+
+
+def test_transpose_multi_c_abi_one_rank():
+    """gt_transpose_multi (NCCL driven from libgt.so) with one rank equals the
+    oracle: level 1, the count all-gather, the NCCL send/recv of R1 and the
+    receiver's levels 2-3."""
+    import torch
+
+    from paper_2501_06872_b200.multi import MultiComm
+
+    g = _rand_graph(21, nv=1 << 20, ne=1 << 24, skew=2.0)
+    off, edg = _dev(torch, g)
+    comm = MultiComm(0, 1)
+    try:
+        t_off, t_edg, info = comm.transpose(off, edg, g.num_vertices, g.num_edges, 0, g.num_vertices)
+        torch.cuda.synchronize()
+        assert info.dst_begin == 0 and info.dst_end == g.num_vertices and info.global_base == 0
+        assert info.num_local_edges == g.num_edges
+        _check(t_off, t_edg, g)
+        # capacity too small: GT_ENOMEM -> MemoryError, with the required size reported
+        with pytest.raises(MemoryError):
+            comm.transpose(off, edg, g.num_vertices, g.num_edges, 0, g.num_vertices, capacity=10)
+    finally:
+        comm.close()
+
+
+@pytest.mark.parametrize("parts", [1, 2, 3, 8])
+def test_shard_pipeline_single_gpu(parts):
+    """The multi-GPU building blocks, run for every rank on one GPU in sequence
+    (no kernel waits on another): sender level 1, owner ranges balanced on the
+    bucket totals, receiver levels 2-3 over the runs of every sender."""
+    from paper_2501_06872_b200.multi import GpuShardBackend, plan_shards, transpose_sharded_local
+
+    g = _rand_graph(parts, nv=200_003, ne=2_000_000, skew=2.0)
+    plan = plan_shards(g.offsets, parts)
+    toff, tedg = transpose_sharded_local(g, plan, GpuShardBackend())
+    o, e = oracle.transpose_c(g.offsets, g.edges, g.num_vertices)
+    assert np.array_equal(toff, o) and np.array_equal(tedg, e)
+
+
+def test_shard_pipeline_wide_and_edge_cases():
+    """Sharded pipeline on the wide form (forced), with an empty source shard
+    and a hub graph (level-3 big buckets on the receivers)."""
+    from paper_2501_06872_b200 import CsrGraph, pipeline_config
+    from paper_2501_06872_b200.multi import GpuShardBackend, plan_shards, transpose_sharded_local
+
+    rng = np.random.default_rng(3)
+    nv = 40_000
+    src = np.sort(rng.integers(20_000, nv, 1_000_000))  # sources below 20000 are empty
+    dst = np.where(rng.random(src.size) < 0.3, 17, rng.integers(0, nv, src.size))
+    g = CsrGraph.from_edge_pairs(src, dst, nv)
+    o, e = oracle.transpose_c(g.offsets, g.edges, nv)
+    for wide in (False, True):
+        with pipeline_config(force_wide=wide):
+            for parts in (2, 5):
+                toff, tedg = transpose_sharded_local(g, plan_shards(g.offsets, parts), GpuShardBackend())
+                assert np.array_equal(toff, o) and np.array_equal(tedg, e), (wide, parts)
+
+
+def test_status_word_without_stats():
+    """Without stats the call returns after enqueueing; gt_transpose_status
+    reports GT_OK once the stream is done."""
+    import torch
+
+    from paper_2501_06872_b200 import _lib, transpose_device
+
+    g = _rand_graph(31, nv=10_007, ne=200_000)
+    off, edg = _dev(torch, g)
+    t_off, t_edg, st = transpose_device(off, edg, g.num_vertices)
+    assert st is None
+    torch.cuda.synchronize()
+    v = ctypes.c_int(7)
+    assert _lib.lib.gt_transpose_status(ctypes.c_void_p(torch.cuda.current_stream().cuda_stream), ctypes.byref(v)) == 0
+    assert v.value == 0
+    _check(t_off, t_edg, g)
+
+
+def _skewed_reference_graph():
+    """potra.relabel_random(potra.generate_skewed(300000, 4000000, 1.1, seed=7),
+    seed=8) restated in numpy (graph.py:187-222, 225-249): Zipf destinations by
+    inverse CDF (searchsorted, 2^24-draw chunks), uniform sources, a seeded
+    permutation of both endpoints, canonical CSR."""
+    from paper_2501_06872_b200 import CsrGraph
+
+    nv, ne, zipf = 300_000, 4_000_000, 1.1
+    rng = np.random.default_rng(7)
+    cdf = np.cumsum(np.arange(1, nv + 1, dtype=np.float64) ** -zipf)
+    cdf /= cdf[-1]
+    src = rng.integers(0, nv, size=ne, dtype=np.int64)
+    dst = np.searchsorted(cdf, rng.random(ne), side="right")
+    g = CsrGraph.from_edge_pairs(src, dst, nv)
+    perm = np.random.default_rng(8).permutation(nv).astype(np.int64)
+    owners = np.repeat(np.arange(nv, dtype=np.int64), np.diff(g.offsets.astype(np.int64)))
+    return CsrGraph.from_edge_pairs(perm[owners], perm[g.edges.astype(np.int64)], nv)
+
+
+def test_skewed_4m_reference_hash(golden_hashes):
+    """The reference-made skewed_4m golden: the restated generator reproduces the
+    reference's input bit for bit, and the GPU transpose hashes to the
+    reference's transpose_oracle output."""
+    from paper_2501_06872_b200 import transpose_gpu
+
+    g = _skewed_reference_graph()
+    assert sha(g.offsets, g.edges) == golden_hashes["skewed_4m"]["input"]
+    out = transpose_gpu(g)
+    assert sha(out.graph.offsets, out.graph.edges) == golden_hashes["skewed_4m"]["oracle"]
+
+
+@pytest.mark.slow
+def test_counter_overflow_raises():
+    """One vertex with 2^32 + 5 in-edges (the reference's 32-bit counters
+    overflow, baselines.py:189-192): transpose_device raises
+    CounterOverflowError (stats path), and the stream-ordered path reports it
+    through gt_transpose_status."""
+    import torch
+
+    from paper_2501_06872_b200 import transpose_device, transpose_status
+    from paper_2501_06872_b200.errors import CounterOverflowError
+
+    if os.environ.get("GT_SKIP_FULL") == "1":
+        pytest.skip("GT_SKIP_FULL=1")
+    free, total = torch.cuda.mem_get_info()
+    if free < 80 * (1 << 30):
+        pytest.skip("needs ~70 GB of device memory")
+    E = (1 << 32) + 5
+    off = torch.tensor([0, E // 2, E], dtype=torch.int64, device="cuda")  # 2 sources, 2 destinations
+    edg = torch.zeros(E, dtype=torch.int32, device="cuda")  # every edge to vertex 0
+    with pytest.raises(CounterOverflowError):
+        transpose_device(off, edg, 2, want_stats=True)
+    transpose_device(off, edg, 2)
+    torch.cuda.synchronize()
+    with pytest.raises(CounterOverflowError):
+        transpose_status()

@@ -314,43 +314,19 @@ def test_full_size_c4():
     assert np.array_equal(got_edg, e)
 
 
-@pytest.mark.parametrize("path_env", ["GT_FORCE_FULL", "GT_V2"], ids=["8-byte-records", "v2-compact"])
-def test_alternate_pipelines(path_env, monkeypatch, golden_cases):
-    """The 8-byte-record pipeline (taken when compact records cannot hold a
-    graph: E >= 2^32 or wide IDs, e.g. config C5) and the previous compact
-    kernels (multi-GPU receiver) against the goldens and random graphs."""
-    from paper_2501_06872_b200 import transpose_gpu
-
-    monkeypatch.setenv(path_env, "1")
-    for name, c in golden_cases.items():
-        out = transpose_gpu(_graph(c["nv"], c["off"], c["edg"]))
-        assert np.array_equal(out.graph.offsets, c["toff"]), name
-        assert np.array_equal(out.graph.edges, c["tedg"]), name
-    rng = np.random.default_rng(99)
-    for i in range(20):
-        g = random_graph(rng, max_vertices=3000, max_edges=40_000)
-        out = transpose_gpu(g)
-        toff, tedg = oracle.transpose_c(g.offsets, g.edges, g.num_vertices)
-        assert np.array_equal(out.graph.offsets, toff) and np.array_equal(out.graph.edges, tedg), i
-    from paper_2501_06872_b200 import gen, transpose_device
-
-    cfg = gen.CONFIGS["C1"]
-    off_d, edg_d = gen.generate_device(cfg)
-    t_off, t_edg, _ = transpose_device(off_d, edg_d, cfg.num_vertices)
-    o, e = oracle.transpose_c(off_d.cpu().numpy().view(np.uint64), edg_d.cpu().numpy().view(np.uint32), cfg.num_vertices)
-    assert np.array_equal(t_off.cpu().numpy().view(np.uint64), o)
-    assert np.array_equal(t_edg.cpu().numpy().view(np.uint32), e)
-
-
-def test_wide_pipeline(monkeypatch, golden_cases, rank_mode):
+def test_wide_pipeline(golden_cases, rank_mode):
     """The wide v3 form (64-bit positions, R2 = source array + low-digit bytes;
     taken by graphs with E >= 2^32 or 29-bit IDs such as C5), forced on small
     graphs: goldens, random graphs, hub graphs (big-bucket path), skewed medium
     graphs, and a 2^29-vertex graph with the C5 digit split (11|10|8, 15
     source-high bits per coarse bucket)."""
-    from paper_2501_06872_b200 import CsrGraph, transpose_gpu
+    from paper_2501_06872_b200 import CsrGraph, pipeline_config, transpose_gpu
 
-    monkeypatch.setenv("GT_WIDE", "1")
+    with pipeline_config(force_wide=True):
+        _wide_cases(golden_cases, rank_mode, CsrGraph, transpose_gpu)
+
+
+def _wide_cases(golden_cases, rank_mode, CsrGraph, transpose_gpu):
     for name, c in golden_cases.items():
         out = transpose_gpu(_graph(c["nv"], c["off"], c["edg"]))
         assert np.array_equal(out.graph.offsets, c["toff"]), name
@@ -433,35 +409,33 @@ def test_full_size_c5():
     assert np.array_equal(got_edg, e)
 
 
-@pytest.mark.parametrize("env", [
-    {"GT_W1": "8"}, {"GT_W1": "16"}, {"GT_W1": "32"}, {"GT_W1": "8", "GT_K1": "16"}, {"GT_W3": "32"}, {"GT_PRE": "30"}, {"GT_PRE": "0"},
-    {"GT_FORK": "0"}, {"GT_BAL3": "0"}, {"GT_OCC": "1"}, {"GT_K2": "32", "GT_W2": "16"},
-    {"GT_SPLIT": "6,6,6"}, {"GT_WIDE": "1", "GT_W1W": "8", "GT_W2W": "8"},
-])
-def test_kernel_variants(monkeypatch, golden_cases, env):
-    """Every tile-shape / occupancy / scheduling variant kept as a measured
-    alternative stays bit-exact: goldens, random graphs and a
-    hub-heavy graph (level-3 big-bucket path), against the oracle."""
-    from paper_2501_06872_b200 import CsrGraph, transpose_gpu
+@pytest.mark.parametrize("cfg", [{}, {"split": (6, 6, 6)}, {"split": (8, 8, 2)}, {"force_wide": True}],
+                         ids=["default", "split-6-6-6", "split-8-8-2", "wide"])
+def test_pipeline_configs(golden_cases, cfg):
+    """The explicit pipeline configuration (gt_set_config: digit split, wide
+    form) stays bit-exact: goldens, random graphs and a hub-heavy graph
+    (level-3 big-bucket path), against the oracle."""
+    from paper_2501_06872_b200 import CsrGraph, pipeline_config, transpose_gpu
 
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
-    for name in sorted(golden_cases)[:20]:
-        c = golden_cases[name]
-        out = transpose_gpu(_graph(c["nv"], c["off"], c["edg"]))
-        assert np.array_equal(out.graph.offsets, c["toff"]), name
-        assert np.array_equal(out.graph.edges, c["tedg"]), name
-    rng = np.random.default_rng(77)
-    for i in range(6):
-        g = random_graph(rng, max_vertices=50_000, max_edges=400_000)
+    with pipeline_config(**cfg):
+        for name in sorted(golden_cases)[:20]:
+            c = golden_cases[name]
+            out = transpose_gpu(_graph(c["nv"], c["off"], c["edg"]))
+            assert np.array_equal(out.graph.offsets, c["toff"]), name
+            assert np.array_equal(out.graph.edges, c["tedg"]), name
+        rng = np.random.default_rng(77)
+        for i in range(6):
+            g = random_graph(rng, max_vertices=50_000, max_edges=400_000)
+            out = transpose_gpu(g)
+            o, e = oracle.transpose_c(g.offsets, g.edges, g.num_vertices)
+            assert np.array_equal(out.graph.offsets, o) and np.array_equal(out.graph.edges, e), i
+        nv, ne = 1 << 18, 1 << 23
+        src = np.sort(rng.integers(0, nv, ne))
+        dst = np.minimum((nv * rng.random(ne) ** 6).astype(np.int64), nv - 1)
+        g = CsrGraph.from_edge_pairs(src, dst, nv)
         out = transpose_gpu(g)
-        o, e = oracle.transpose_c(g.offsets, g.edges, g.num_vertices)
-        assert np.array_equal(out.graph.offsets, o) and np.array_equal(out.graph.edges, e), i
-    nv, ne = 1 << 18, 1 << 23
-    src = np.sort(rng.integers(0, nv, ne))
-    dst = np.minimum((nv * rng.random(ne) ** 6).astype(np.int64), nv - 1)
-    g = CsrGraph.from_edge_pairs(src, dst, nv)
-    out = transpose_gpu(g)
-    o, e = oracle.transpose_c(g.offsets, g.edges, nv)
-    assert np.array_equal(out.graph.offsets, o) and np.array_equal(out.graph.edges, e)
-    assert out.details["big_buckets"] > 0 or env.get("GT_WIDE") == "1"
+        o, e = oracle.transpose_c(g.offsets, g.edges, nv)
+        assert np.array_equal(out.graph.offsets, o) and np.array_equal(out.graph.edges, e)
+        if "split" in cfg:
+            assert tuple(out.details["digit_bits"]) == cfg["split"]
+        assert out.details["big_buckets"] > 0 or cfg.get("force_wide")

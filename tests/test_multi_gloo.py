@@ -20,9 +20,11 @@ sys.path.insert(0, str(ROOT))
 
 
 class CpuShardBackend:
-    """CPU stand-in for GpuShardBackend (same interface)."""
+    """CPU stand-in for GpuShardBackend (same interface and bucket geometry;
+    records travel as (src, dst) pairs, rec_words = 2)."""
 
     torch = torch
+    rec_words = 2
 
     def to_device_offsets(self, offsets):
         return torch.from_numpy(np.ascontiguousarray(offsets, dtype=np.uint64).view(np.int64))
@@ -30,24 +32,29 @@ class CpuShardBackend:
     def to_device_edges(self, edges):
         return torch.from_numpy(np.ascontiguousarray(edges, dtype=np.uint32).view(np.int32))
 
-    def partition(self, offsets_d, edges_slice_d, num_vertices, src_lo, src_hi, dst_bounds):
-        off = offsets_d.numpy().view(np.uint64)
+    def send(self, offsets_d, edges_slice_d, num_vertices, num_edges, e_begin, geom):
+        off = offsets_d.numpy().view(np.uint64).astype(np.int64)
         edges = edges_slice_d.numpy().view(np.uint32)
-        deg = np.diff(off[src_lo : src_hi + 1].astype(np.int64))
-        owners = np.repeat(np.arange(src_lo, src_hi, dtype=np.uint32), deg)
-        owner_rank = np.searchsorted(np.asarray(dst_bounds)[1:-1], edges, side="right")
-        order = np.argsort(owner_rank, kind="stable")
-        rec = np.stack([owners[order], edges[order]], axis=1).astype(np.uint32)
-        counts = np.bincount(owner_rank, minlength=len(dst_bounds) - 1).astype(np.int64)
-        return torch.from_numpy(rec.view(np.int32)), counts
+        pos = e_begin + np.arange(edges.size, dtype=np.int64)
+        owners = (np.searchsorted(off, pos, side="right") - 1).astype(np.uint32)
+        bucket = (edges.astype(np.int64) >> int(geom.bucket_shift))
+        order = np.argsort(bucket, kind="stable")
+        rec = np.stack([owners[order], edges[order]], axis=1).astype(np.uint32).reshape(-1)
+        counts = np.bincount(bucket, minlength=int(geom.num_buckets)).astype(np.int64)
+        seg = np.zeros(int(geom.num_buckets) * int(geom.seg_hi_row), dtype=np.int64)
+        return torch.from_numpy(rec.view(np.int32)), torch.from_numpy(counts), torch.from_numpy(seg)
 
-    def transpose_received(self, records, dst_lo, dst_hi, global_base, want_stats=False, src_num_vertices=None):
-        rec = records.numpy().view(np.uint32).reshape(-1, 2)
-        d = rec[:, 1].astype(np.int64) - dst_lo
+    def receive(self, r1_recv, seg_recv, counts_all, parts, num_vertices, num_edges, lo, hi, num_records,
+                global_base, geom, want_stats=False):
+        shift = int(geom.bucket_shift)
+        v_lo, v_hi = min(num_vertices, lo << shift), min(num_vertices, hi << shift)
+        rec = r1_recv.numpy().view(np.uint32).reshape(-1, 2)
+        assert rec.shape[0] == num_records
+        d = rec[:, 1].astype(np.int64) - v_lo
         order = np.argsort(d, kind="stable")
         t_edges = rec[order, 0].copy()
-        cnt = np.bincount(d, minlength=dst_hi - dst_lo)
-        t_off = np.zeros(dst_hi - dst_lo + 1, dtype=np.uint64)
+        cnt = np.bincount(d, minlength=v_hi - v_lo)
+        t_off = np.zeros(v_hi - v_lo + 1, dtype=np.uint64)
         np.cumsum(cnt, out=t_off[1:])
         t_off += np.uint64(global_base)
         return torch.from_numpy(t_off.view(np.int64)), torch.from_numpy(t_edges.view(np.int32)), None
@@ -81,7 +88,7 @@ def _worker(rank, world, port, seed, result_path):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 4])
 def test_sharded_exchange_gloo(tmp_path, world):
     from oracle import oracle
 
@@ -100,8 +107,5 @@ def test_plan_shards_contract():
     p = plan_shards(off, 3)
     assert p.src_bounds.tolist() == [0, 4, 4, 6]  # edge_balanced_vertex_bounds probe
     assert p.edge_bounds.tolist() == [0, 20, 20, 30]
-    assert p.dst_bounds.tolist() == [0, 2, 4, 6]
     with pytest.raises(ValueError):
         plan_shards(off, 0)
-    with pytest.raises(ValueError):
-        plan_shards(off, 2, dst_bounds=[0, 7, 6])
