@@ -1231,7 +1231,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
       __syncthreads();  // (C)
       tick(4);
       if constexpr (kS64) {
-        writeout_pair<T2_, PT>(out, s_st64, s_delta, n);
+        writeout_pair<T2_, PT>(out, s_st64, s_delta, n - ddtot);  // kDD: the staged items exclude the dominant digit
       } else if constexpr (kIO == kIoPlain) {
         writeout_tag<T2_, PT>(out, s_buf, s_tag, s_delta, n);
       } else {  // 64-bit positions
