@@ -268,6 +268,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--force-dist", action="store_true", help="use the sharded path even at N=1")
+    ap.add_argument("--experiment", type=int, default=0, help="A/B experiment bits (gt_config.reserved[0]); 0 = product")
+    ap.add_argument("--rank-mode", type=int, default=-1, help="-1 auto, 0 smem-atomic, 1 safe OR-mask ranking")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3  # timing rule: >= 3 warm-up steps
@@ -294,7 +296,12 @@ def main():
         os.environ.setdefault("MASTER_PORT", "29511")
         dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local_rank))
 
-    from paper_2501_06872_b200 import _lib, transpose_device
+    from paper_2501_06872_b200 import _lib, set_config, set_rank_mode, transpose_device
+
+    if args.experiment:
+        set_config(experiment=args.experiment)
+    if args.rank_mode >= 0:
+        set_rank_mode(args.rank_mode)
 
     V = cfg.num_vertices
     dev = torch.device("cuda", local_rank)
@@ -564,7 +571,9 @@ def main():
             "data": "synthetic",
             "config": {"workload": cfg.name, "num_vertices": V, "num_edges": E,
                        "l2": f"inputs ({((V + 1) * 8 + E * 4) / 1e9:.2f} GB) larger than L2 (126 MB); no flush",
-                       "parallelism": f"sharded{n_gpus}" if dist_on else "single-gpu"},
+                       "parallelism": f"sharded{n_gpus}" if dist_on else "single-gpu",
+                       **({"experiment": args.experiment} if args.experiment else {}),
+                       **({"rank_mode_forced": args.rank_mode} if args.rank_mode >= 0 else {})},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": agg_peak, "unit": "GB/s",
                          "frac": achieved / agg_peak, "traffic": traffic,
                          "scope": "whole transpose step (all kernels); algorithmic bytes 24(V+1)+12E per step",

@@ -90,6 +90,7 @@ struct Plan {
   int L = 0, nsh = 0;  // R1: source low bits, source high bits (decoded from seg_hi)
   int gbits = 0;       // compact R2: fine-digit bits kept beside the low digit
   int D1 = 1, Db = 1, Dc = 1;
+  int exp = 0;  // gt_config.reserved[0]: experiment bits (A/B measurements; 0 = product path)
 };
 
 // Digit split of the destination ID for a graph of V destinations, E edges,
@@ -170,6 +171,7 @@ int make_plan(uint64_t V, uint64_t E, uint64_t Vsrc, const gt_config& cfg, Plan&
   p.D1 = 1 << p.a;
   p.Db = 1 << p.b;
   p.Dc = 1 << p.c;
+  p.exp = cfg.reserved[0];
   return GT_OK;
 }
 
@@ -722,7 +724,7 @@ int level23(const Plan& p, const Layout& q, Ws& w, const uint32_t* r1, uint32_t 
       const size_t sm = smem_p2(Dc, kMode, 16);
       if ((rc = set_smem(kern, sm))) return rc;
       kern<<<persistent_grid(kern, T, sm, q.max_t3), T, sm, sb>>>(w.r2, w.tiles3, w.cnt + 2, Dc, dec, w.base3, t_edges,
-                                                                   nullptr, nullptr, nullptr, w.segdd);
+                                                                   nullptr, nullptr, nullptr, (p.exp & 1) ? nullptr : w.segdd);
     }
     GT_LAUNCH_CHECK();
     if ((rc = tm.kend(3, sb))) return rc;

@@ -317,11 +317,13 @@ def transpose_status(stream=None, device=None) -> None:
         _lib.check(st.value, "gt_transpose")
 
 
-def set_config(split=None, force_wide: bool = False) -> None:
+def set_config(split=None, force_wide: bool = False, experiment: int = 0) -> None:
     """Explicit pipeline configuration (gt_set_config): ``split`` = (a, b, c)
     digit bits (used when they cover the destination ID bits), ``force_wide``
-    = the 64-bit-position form.  ``set_config()`` restores the defaults."""
+    = the 64-bit-position form, ``experiment`` = A/B bits for measurements
+    (0 = the product path).  ``set_config()`` restores the defaults."""
     cfg = _lib.GtConfig()
+    cfg.reserved[0] = int(experiment)
     if split is not None:
         for i, x in enumerate(split):
             cfg.split[i] = int(x)
@@ -332,11 +334,11 @@ def set_config(split=None, force_wide: bool = False) -> None:
 class pipeline_config:
     """Context manager form of :func:`set_config` (restores the defaults)."""
 
-    def __init__(self, split=None, force_wide: bool = False):
-        self.split, self.force_wide = split, force_wide
+    def __init__(self, split=None, force_wide: bool = False, experiment: int = 0):
+        self.split, self.force_wide, self.experiment = split, force_wide, experiment
 
     def __enter__(self):
-        set_config(self.split, self.force_wide)
+        set_config(self.split, self.force_wide, self.experiment)
         return self
 
     def __exit__(self, *exc):
