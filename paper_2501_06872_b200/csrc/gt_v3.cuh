@@ -1154,9 +1154,15 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
         else d = dec.digit(r);
         const bool isdd = kDD && valid && d == dd;
         if constexpr (kDD) nddw += __popc(__ballot_sync(kFull, isdd));
-        uint32_t rk = 0;
-        if constexpr (kDD) {  // slots holding only the dominant digit skip the match
-          if (__ballot_sync(kFull, valid && !isdd)) rk = rank_match(s_cnt + (isdd ? 0u : d) * WH2_ + (w >> 1), sh, d, valid && !isdd);
+        uint32_t rk;
+        // kDD: with the hub's items taken out the remaining digits are spread, so the
+        // lane-ordered counter atomics apply again (match peers only when no hub digit is known)
+        if constexpr (kDD) {
+          if (dd != 0xffffffffu)
+            rk = rank_pk<kMode>(s_cnt + (isdd ? 0u : d) * WH2_ + (w >> 1), s_scr + (isdd ? 0u : d) * WP2_ + w, sh,
+                                valid && !isdd);
+          else
+            rk = rank_match(s_cnt + d * WH2_ + (w >> 1), sh, d, valid);
         } else if constexpr (Dec::kMatchRank) rk = rank_match(s_cnt + d * WH2_ + (w >> 1), sh, d, valid);
         else rk = rank_pk<kMode>(s_cnt + d * WH2_ + (w >> 1), s_scr + d * WP2_ + w, sh, valid);
         if constexpr (kIO == kIoSplit) {
