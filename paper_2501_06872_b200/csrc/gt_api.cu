@@ -182,7 +182,7 @@ struct Layout {
   uint64_t ntiles1 = 0, nplace = 0, nh = 0, nruns = 0, max_t2 = 0, nfine = 0, max_big = 0, max_t3 = 0;
   uint64_t o_r2, o_r2lv, o_tcnt, o_tbase, o_status, o_ctr, o_psrc, o_prev, o_seghi, o_runs, o_rfirst, o_bstart,
       o_tiles2, o_cnt2, o_base2, o_seg2, o_fbase, o_units, o_bigs, o_tiles3, o_cnt3, o_base3, o_seg3, o_cnt, o_err,
-      o_bnt, o_bfirst, o_segdd, total;
+      o_bnt, o_bfirst, total;
 };
 
 // E1: level-1 edges (0: no level 1 here); E23: records of levels 2-3; D1: local buckets; R: runs per bucket.
@@ -232,7 +232,6 @@ void make_layout(const Plan& p, uint64_t E1, uint64_t E23, uint32_t R, Layout& q
   q.o_err = take(4);
   q.o_bnt = take((q.max_big + 1) * 4);
   q.o_bfirst = take((q.max_big + 2) * 8);
-  q.o_segdd = take((q.max_big + 1) * 4);
   q.total = off;
 }
 
@@ -469,7 +468,6 @@ struct Ws {
   unsigned int* err;
   uint32_t* bnt;
   uint64_t* bfirst;
-  uint32_t* segdd;
 };
 Ws ws_ptrs(const Layout& q, unsigned char* ws, const Plan& p) {
   Ws w;
@@ -500,7 +498,6 @@ Ws ws_ptrs(const Layout& q, unsigned char* ws, const Plan& p) {
   w.err = reinterpret_cast<unsigned int*>(ws + q.o_err);
   w.bnt = reinterpret_cast<uint32_t*>(ws + q.o_bnt);
   w.bfirst = reinterpret_cast<uint64_t*>(ws + q.o_bfirst);
-  w.segdd = reinterpret_cast<uint32_t*>(ws + q.o_segdd);
   return w;
 }
 
@@ -639,24 +636,24 @@ int level23(const Plan& p, const Layout& q, Ws& w, const uint32_t* r1, uint32_t 
         auto kern = k_p2<kMode, DecR1, 32, false, kIoSplit, true, 16, 1>;
         if ((rc = set_smem(kern, sm16))) return rc;
         kern<<<persistent_grid(kern, 512, sm16, q.max_t2), 512, sm16, st>>>(r1, w.tiles2, n_t2, Db, dec, w.base2,
-                                                                              w.r2, nullptr, nullptr, w.r2lv, nullptr);
+                                                                              w.r2, nullptr, nullptr, w.r2lv);
       } else {
         auto kern = k_p2<kMode, DecR1, 32, false, kIoSplit>;
         const size_t sm = smem_p2(Db, kMode, 32, kIoSplit);
         if ((rc = set_smem(kern, sm))) return rc;
         kern<<<persistent_grid(kern, T, sm, q.max_t2), T, sm, st>>>(r1, w.tiles2, n_t2, Db, dec, w.base2, w.r2,
-                                                                     nullptr, nullptr, w.r2lv, nullptr);
+                                                                     nullptr, nullptr, w.r2lv);
       }
     } else if (Db >= 1024) {  // 8192-record tiles (C4 level 2: 5.70 ms vs 5.89 at 4096)
       auto kern = k_p2<kMode, DecR1, 32>;
       const size_t sm = smem_p2(Db, kMode, 32);
       if ((rc = set_smem(kern, sm))) return rc;
-      kern<<<persistent_grid(kern, T, sm, q.max_t2), T, sm, st>>>(r1, w.tiles2, n_t2, Db, dec, w.base2, w.r2, nullptr, nullptr, nullptr, nullptr);
+      kern<<<persistent_grid(kern, T, sm, q.max_t2), T, sm, st>>>(r1, w.tiles2, n_t2, Db, dec, w.base2, w.r2, nullptr, nullptr, nullptr);
     } else {  // 4096-record tiles, 4 CTAs/SM, no batched landing loads (C3 2.11 vs 2.18 ms)
       auto kern = k_p2<kMode, DecR1, 16, false, kIoPlain, false>;
       const size_t sm = smem_p2(Db, kMode, 16);
       if ((rc = set_smem(kern, sm))) return rc;
-      kern<<<persistent_grid(kern, T, sm, q.max_t2), T, sm, st>>>(r1, w.tiles2, n_t2, Db, dec, w.base2, w.r2, nullptr, nullptr, nullptr, nullptr);
+      kern<<<persistent_grid(kern, T, sm, q.max_t2), T, sm, st>>>(r1, w.tiles2, n_t2, Db, dec, w.base2, w.r2, nullptr, nullptr, nullptr);
     }
     GT_LAUNCH_CHECK();
     if ((rc = tm.kend(1))) return rc;
@@ -706,7 +703,7 @@ int level23(const Plan& p, const Layout& q, Ws& w, const uint32_t* r1, uint32_t 
       GT_LAUNCH_CHECK();
     }
     k_segfix<<<(unsigned)std::min<uint64_t>(q.max_big, (uint64_t)sms * 8), 512, 0, sb>>>(w.seg3, w.cnt + 1, Dc, w.base3,
-                                                                                      t_offsets, V, w.err, w.segdd);
+                                                                                      t_offsets, V, w.err);
     GT_LAUNCH_CHECK();
     DecR2 dec;
     dec.nbs = p.nbs;
@@ -718,13 +715,13 @@ int level23(const Plan& p, const Layout& q, Ws& w, const uint32_t* r1, uint32_t 
       const size_t sm = smem_p2(Dc, kMode, 16, kIoLv);
       if ((rc = set_smem(kern, sm))) return rc;
       kern<<<persistent_grid(kern, T, sm, q.max_t3), T, sm, sb>>>(w.r2, w.tiles3, w.cnt + 2, Dc, dec, w.base3, t_edges,
-                                                                   nullptr, w.r2lv, nullptr, nullptr);
+                                                                   nullptr, w.r2lv, nullptr);
     } else {  // batched landing loads (C3 big buckets 0.85 -> 0.78 ms)
       auto kern = k_p2<kMode, DecR2, 16>;
       const size_t sm = smem_p2(Dc, kMode, 16);
       if ((rc = set_smem(kern, sm))) return rc;
       kern<<<persistent_grid(kern, T, sm, q.max_t3), T, sm, sb>>>(w.r2, w.tiles3, w.cnt + 2, Dc, dec, w.base3, t_edges,
-                                                                   nullptr, nullptr, nullptr, (p.exp & 1) ? nullptr : w.segdd);
+                                                                   nullptr, nullptr, nullptr);
     }
     GT_LAUNCH_CHECK();
     if ((rc = tm.kend(3, sb))) return rc;

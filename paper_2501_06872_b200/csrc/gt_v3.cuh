@@ -543,9 +543,7 @@ __device__ __forceinline__ void stage_tag(const uint32_t (&pk)[K_], const uint32
 }
 
 // stage_tag with one 8-byte (payload, digit) store per item.
-// kSkip: items with pk == ~0u (a dominant digit's items, written straight to
-// their output run) are not staged.
-template <int G, int K_, bool kSkip = false>
+template <int G, int K_>
 __device__ __forceinline__ void stage_pair(const uint32_t (&pk)[K_], const uint32_t (&pay)[K_], const uint32_t* cnt,
                                            int whn, uint32_t w, uint32_t sh, uint2* st, uint32_t lim, uint32_t i0,
                                            uint32_t per = K_ * 32) {
@@ -554,11 +552,10 @@ __device__ __forceinline__ void stage_pair(const uint32_t (&pk)[K_], const uint3
     if ((uint32_t)c * 32 >= per) break;
     uint32_t bw[G];
 #pragma unroll
-    for (int q = 0; q < G; ++q) bw[q] = cnt[((kSkip && pk[c + q] == 0xffffffffu) ? 0u : (pk[c + q] >> 16)) * whn + (w >> 1)];
+    for (int q = 0; q < G; ++q) bw[q] = cnt[(pk[c + q] >> 16) * whn + (w >> 1)];
 #pragma unroll
     for (int q = 0; q < G; ++q) {
-      if ((uint32_t)(c + q) * 32 < per && (lim == 0xffffffffu || i0 + (c + q) * 32 < lim) &&
-          (!kSkip || pk[c + q] != 0xffffffffu)) {
+      if ((uint32_t)(c + q) * 32 < per && (lim == 0xffffffffu || i0 + (c + q) * 32 < lim)) {
         const uint32_t pos = ((bw[q] >> sh) & 0xffffu) + (pk[c + q] & 0xffffu);
         st[pos] = make_uint2(pay[c + q], pk[c + q] >> 16);
       }
@@ -889,9 +886,7 @@ __global__ void __launch_bounds__(512) k_cnt_lv(const uint8_t* __restrict__ lv, 
 // segments); large segments are cheap because the scan already did the work.
 __global__ void __launch_bounds__(512) k_segfix(const SegDesc* __restrict__ segs, const uint32_t* __restrict__ n_segs,
                                                 int D, uint64_t* __restrict__ base, uint64_t* __restrict__ out,
-                                                uint64_t out_limit, unsigned int* __restrict__ err,
-                                                uint32_t* __restrict__ seg_dd = nullptr) {
-  __shared__ unsigned long long s_best;
+                                                uint64_t out_limit, unsigned int* __restrict__ err) {
   const uint32_t ns = *n_segs;
   for (uint32_t sg = blockIdx.x; sg < ns; sg += gridDim.x) {
     const SegDesc S = segs[sg];
@@ -902,7 +897,6 @@ __global__ void __launch_bounds__(512) k_segfix(const SegDesc* __restrict__ segs
       continue;
     }
     const uint64_t v0 = base[t0];
-    if (threadIdx.x == 0) s_best = 0;
     __syncthreads();  // every thread has read v0 before any entry changes
     const uint64_t adj = S.base - v0;
     if (adj)
@@ -913,11 +907,8 @@ __global__ void __launch_bounds__(512) k_segfix(const SegDesc* __restrict__ segs
       if (S.out_off + d < out_limit) out[S.out_off + d] = st;
       const uint64_t nx = (d + 1 < D) ? base[t0 + (uint64_t)(d + 1) * S.nt] : S.end;
       if (nx - st >= (1ull << 32)) atomicExch(err, 1u);
-      // dominant digit of the segment (most records, lowest digit on ties)
-      if (seg_dd) atomicMax(&s_best, ((unsigned long long)umin64(nx - st, 0xffffffffull) << 32) | (0xffffffffu - d));
     }
     __syncthreads();
-    if (seg_dd && threadIdx.x == 0) seg_dd[sg] = 0xffffffffu - (uint32_t)(s_best & 0xffffffffull);
   }
 }
 
@@ -999,15 +990,9 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
                                              const uint64_t* __restrict__ base, uint32_t* __restrict__ out,
                                              unsigned long long* __restrict__ prof = nullptr,
                                              const uint8_t* __restrict__ lv_in = nullptr,
-                                             uint8_t* __restrict__ lv_out = nullptr,
-                                             const uint32_t* __restrict__ seg_dd = nullptr) {
+                                             uint8_t* __restrict__ lv_out = nullptr) {
   // phase profile (kProf builds only; thread 0, clock64): 0 tile setup, 1 wait,
   // 2 rank, 3 bases, 4 stage, 5 write
-  // kDD (level-3 big buckets, compact form): the segment's dominant digit
-  // (seg_dd[tile.seg], a hub vertex) is not ranked or staged: its items are
-  // compacted with one ballot per slot and written straight to the digit's
-  // output run, contiguous and in record order (PoTra's high-degree split).
-  constexpr bool kDD = Dec::kMatchRank && kIO == kIoPlain && kS64;
   unsigned long long pacc[kProf ? 6 : 1] = {};
   long long tprev = kProf ? clock64() : 0;
   auto tick = [&](int ph) {
@@ -1039,7 +1024,6 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
   // kIoSplit: low-digit byte of each staged slot; kIoLv: landing of the digit bytes (16B aligned)
   uint8_t* s_lvx = reinterpret_cast<uint8_t*>(s_bnd + kMaxBnd);                // PT + 16
   __shared__ __align__(8) uint64_t s_bar;
-  __shared__ uint32_t s_ddw[kDD ? WW : 1];  // kDD: dominant-digit items per warp in this place tile
 
   const uint32_t tid = threadIdx.x, lane = lane_id(), w = warp_id();
   const uint32_t sh = (w & 1) << 4;
@@ -1060,7 +1044,6 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
       else s_gcur[d] = (uint32_t)base[row0 + (uint64_t)d * t.nt];
     }
     const uint32_t nbt = Dec::kSrcHigh ? t.nbnd : 0u;
-    const uint32_t dd = (kDD && seg_dd) ? seg_dd[t.seg] : 0xffffffffu;
     const uint64_t* hrow = nullptr;
     if constexpr (Dec::kSrcHigh) {
       hrow = dec.seg_hi + (uint64_t)t.seg * (dec.nh + 1) + t.h0 + 1;  // boundary k (1-based) = hrow[k - 1]
@@ -1143,7 +1126,6 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
 #pragma unroll
         for (int s = 0; s < K; ++s) pk[s] = 0;  // slots a warp skips stage nothing
       }
-      uint32_t nddw = 0;  // kDD: this warp's dominant-digit items
       auto slot = [&](int s, bool valid) {  // pay[s] holds the slot's record (loaded below)
         const uint32_t i0 = iw + s * 32, i = i0 + lane;
         const uint32_t r = valid ? (kPre ? pay[s] : s_buf[o + i]) : 0u;
@@ -1152,24 +1134,14 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
         uint32_t d;
         if constexpr (kIO == kIoLv) d = valid ? (uint32_t)s_lvx[o8 + i] : 0u;
         else d = dec.digit(r);
-        const bool isdd = kDD && valid && d == dd;
-        if constexpr (kDD) nddw += __popc(__ballot_sync(kFull, isdd));
         uint32_t rk;
-        // kDD: with the hub's items taken out the remaining digits are spread, so the
-        // lane-ordered counter atomics apply again (match peers only when no hub digit is known)
-        if constexpr (kDD) {
-          if (dd != 0xffffffffu)
-            rk = rank_pk<kMode>(s_cnt + (isdd ? 0u : d) * WH2_ + (w >> 1), s_scr + (isdd ? 0u : d) * WP2_ + w, sh,
-                                valid && !isdd);
-          else
-            rk = rank_match(s_cnt + d * WH2_ + (w >> 1), sh, d, valid);
-        } else if constexpr (Dec::kMatchRank) rk = rank_match(s_cnt + d * WH2_ + (w >> 1), sh, d, valid);
+        if constexpr (Dec::kMatchRank) rk = rank_match(s_cnt + d * WH2_ + (w >> 1), sh, d, valid);
         else rk = rank_pk<kMode>(s_cnt + d * WH2_ + (w >> 1), s_scr + d * WP2_ + w, sh, valid);
         if constexpr (kIO == kIoSplit) {
           pk[s] = (((r >> dec.L) & dec.lvmask) << 24) | (d << 13) | rk;
           pay[s] = (h << dec.L) | (r & dec.src_mask);
         } else {
-          pk[s] = isdd ? 0xffffffffu : ((d << 16) | rk);
+          pk[s] = (d << 16) | rk;
           pay[s] = dec.payload(r, h);
         }
       };
@@ -1187,27 +1159,8 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
           slot(s, iw + s * 32 + lane < n);
         }
       }
-      if (kDD && lane == 0) s_ddw[w] = nddw;
       __syncthreads();  // (B)
       tick(2);
-      uint32_t ddtot = 0;
-      if constexpr (kDD) {
-        if (dd != 0xffffffffu) {  // the dominant digit's items, compacted in record order
-          uint32_t run = s_gcur[dd];
-          for (uint32_t q = 0; q < (uint32_t)WW; ++q) {
-            if (q == w) run += ddtot;
-            ddtot += s_ddw[q];
-          }
-#pragma unroll
-          for (int s = 0; s < K; ++s) {
-            if (kBal2 && (uint32_t)s * 32 >= per) break;
-            const bool mine = pk[s] == 0xffffffffu;
-            const uint32_t m = __ballot_sync(kFull, mine);
-            if (mine) out[run + __popc(m & lanemask_lt())] = pay[s];
-            run += __popc(m);
-          }
-        }
-      }
       if constexpr (kW64)
         flat_bases_epi<WH2_>(s_cnt, D, s_tmp, [&](int d, uint32_t b, uint32_t e) {
           s_g64[d] -= b;
@@ -1217,8 +1170,8 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
         flat_bases_pk<WH2_>(s_cnt, D, s_gcur, s_dtot, s_delta, s_tmp);
       tick(3);
       if constexpr (kS64) {
-        stage_pair<kPre ? kStageG : 1, K, kDD>(pk, pay, s_cnt, WH2_, w, sh, s_st64, (n == (uint32_t)PT) ? 0xffffffffu : n,
-                                               iw + lane, per);
+        stage_pair<kPre ? kStageG : 1, K>(pk, pay, s_cnt, WH2_, w, sh, s_st64, (n == (uint32_t)PT) ? 0xffffffffu : n,
+                                          iw + lane, per);
       } else if constexpr (kIO != kIoSplit) {
         stage_tag<kPre ? kStageG : 1, K>(pk, pay, s_cnt, WH2_, w, sh, s_buf, s_tag, (n == (uint32_t)PT) ? 0xffffffffu : n, iw + lane,
                                          per);
@@ -1237,7 +1190,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
       __syncthreads();  // (C)
       tick(4);
       if constexpr (kS64) {
-        writeout_pair<T2_, PT>(out, s_st64, s_delta, n - ddtot);  // kDD: the staged items exclude the dominant digit
+        writeout_pair<T2_, PT>(out, s_st64, s_delta, n);
       } else if constexpr (kIO == kIoPlain) {
         writeout_tag<T2_, PT>(out, s_buf, s_tag, s_delta, n);
       } else {  // 64-bit positions
@@ -1255,7 +1208,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
       }
       zero_u32(s_cnt, round4(D * WH2_));
       if constexpr (!kW64)
-        for (int d = tid; d < D; d += T2_) s_gcur[d] += s_dtot[d] + (((uint32_t)d == dd) ? ddtot : 0u);
+        for (int d = tid; d < D; d += T2_) s_gcur[d] += s_dtot[d];
       fence_proxy_async_smem();
       __syncthreads();  // (D)
       tick(5);
