@@ -293,6 +293,12 @@ int gt_coverage_exact(const uint64_t *keys, const uint32_t *vals, uint64_t capac
  * canonical lists). */
 int gt_sort_lists(const uint64_t *offsets, const uint32_t *edges, uint64_t num_vertices, uint64_t num_edges,
                   uint32_t *out_edges, void *stream);
+/* An independent transpose for verification (verify_output full-oracle):
+ * offsets from the in-degree histogram, lists from a global radix sort of
+ * (destination << 32 | source) keys (CUB) — transpose_oracle's lexsort
+ * (graph.py:136-148) with none of the partition kernels it checks.  E < 2^32. */
+int gt_verify_transpose(const uint64_t *offsets, const uint32_t *edges, uint64_t num_vertices, uint64_t num_edges,
+                        uint64_t *t_offsets, uint32_t *t_edges, void *stream);
 int gt_first_diff_u64(const uint64_t *a, const uint64_t *b, uint64_t n, uint64_t *first, void *stream);
 int gt_first_diff_u32(const uint32_t *a, const uint32_t *b, uint64_t n, uint64_t *first, void *stream);
 int gt_in_degree_offsets(const uint32_t *edges, uint64_t num_edges, uint64_t num_vertices, uint64_t *offsets,

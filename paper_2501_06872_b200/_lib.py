@@ -117,6 +117,7 @@ SYMBOLS = {
                                 _vp]),
     "gt_build_csr": (_int, [_vp, _vp, _u64, _u64, _vp, _vp, _vp]),
     "gt_sort_lists": (_int, [_vp, _vp, _u64, _u64, _vp, _vp]),
+    "gt_verify_transpose": (_int, [_vp, _vp, _u64, _u64, _vp, _vp, _vp]),
     "gt_first_diff_u64": (_int, [_vp, _vp, _u64, _u64p, _vp]),
     "gt_first_diff_u32": (_int, [_vp, _vp, _u64, _u64p, _vp]),
     "gt_in_degree_offsets": (_int, [_vp, _u64, _u64, _vp, _vp]),

@@ -5,6 +5,11 @@
 //   twice: T(g) lists sources ascending per destination, and T(T(g)) lists,
 //   for every vertex, its neighbours ascending with multiplicity — the same
 //   offsets as g and each list sorted, by the stable kernels of gt_api.cu.
+// * gt_verify_transpose: an independent GPU transpose for verify_output's
+//   full-oracle mode — the exact offsets (bincount + cumsum) and a global radix
+//   sort (CUB, library code) of destination << 32 | source keys, i.e.
+//   transpose_oracle's lexsort (graph.py:136-148) with none of the partition
+//   kernels it checks.
 // * gt_first_diff_* / gt_in_degree_offsets / gt_first_diff_lists are the
 //   device halves of verify_output (bench.py:91-170): first differing offset
 //   or edge index (_first_mismatch_vertex, bench.py:91-99), the exact
@@ -15,6 +20,7 @@
 #include <algorithm>
 #include <cstdint>
 
+#include <cub/device/device_radix_sort.cuh>
 #include <cuda_runtime.h>
 
 #include "../../include/gt.h"
@@ -53,6 +59,25 @@ __global__ void k_first_diff_lists(const uint64_t* __restrict__ oa, const uint32
       if (lane == 0) atomicMin(first, (unsigned long long)j);
     }
   }
+}
+
+// key of edge i (stream position): destination << 32 | source, the source by
+// binary search over the offsets (largest v with offsets[v] <= i)
+__global__ void k_edge_keys(const uint64_t* __restrict__ off, const uint32_t* __restrict__ e, uint64_t V, uint64_t E,
+                            uint64_t* __restrict__ keys) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < E; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t lo = 0, hi = V;
+    while (hi - lo > 1) {
+      const uint64_t mid = lo + (hi - lo) / 2;
+      if (off[mid] <= i) lo = mid; else hi = mid;
+    }
+    keys[i] = ((uint64_t)e[i] << 32) | lo;
+  }
+}
+
+__global__ void k_low_words(const uint64_t* __restrict__ keys, uint64_t E, uint32_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < E; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = (uint32_t)keys[i];
 }
 
 int cuda_fail(cudaError_t e) {
@@ -103,6 +128,38 @@ int gt_sort_lists(const uint64_t* offsets, const uint32_t* edges, uint64_t V, ui
   cudaFreeAsync(tt_off, st);
   if (rc == GT_OK && (e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e);
   return rc;
+}
+
+int gt_verify_transpose(const uint64_t* offsets, const uint32_t* edges, uint64_t V, uint64_t E, uint64_t* t_offsets,
+                        uint32_t* t_edges, void* stream) {
+  if (!offsets || !t_offsets || (E && (!edges || !t_edges))) return gt_internal_set_err(GT_EINVAL, "null argument");
+  if (V == 0 || V >= (1ull << 32)) return gt_internal_set_err(GT_EINVAL, "num_vertices must be in [1, 2^32)");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int rc = gt_in_degree_offsets(edges, E, V, t_offsets, st);
+  if (rc != GT_OK || E == 0) return rc;
+  uint64_t *k0 = nullptr, *k1 = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  cudaError_t e;
+  int bits = 1;
+  while (bits < 32 && (1ull << bits) < V) ++bits;
+  if ((e = cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, k0, k1, E, 0, 32 + bits, st)) != cudaSuccess)
+    return cuda_fail(e);
+  if ((e = cudaMallocAsync(&k0, E * 8, st)) != cudaSuccess || (e = cudaMallocAsync(&k1, E * 8, st)) != cudaSuccess ||
+      (e = cudaMallocAsync(&tmp, tmp_bytes, st)) != cudaSuccess) {
+    cudaFreeAsync(k0, st);
+    cudaFreeAsync(k1, st);
+    return cuda_fail(e);
+  }
+  k_edge_keys<<<148 * 16, 256, 0, st>>>(offsets, edges, V, E, k0);
+  e = cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, k0, k1, E, 0, 32 + bits, st);
+  if (e == cudaSuccess) k_low_words<<<148 * 16, 256, 0, st>>>(k1, E, t_edges);
+  cudaFreeAsync(k0, st);
+  cudaFreeAsync(k1, st);
+  cudaFreeAsync(tmp, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e);
+  return GT_OK;
 }
 
 int gt_first_diff_u64(const uint64_t* a, const uint64_t* b, uint64_t n, uint64_t* first, void* stream) {

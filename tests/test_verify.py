@@ -108,3 +108,34 @@ def test_transpose_potra_shape(golden_cases):
     for out in (p, a):
         assert out.sorted and np.array_equal(out.graph.offsets, c["toff"]) and np.array_equal(out.graph.edges, c["tedg"])
     assert p.details["method_chosen"] == "gpu" and "step0" in p.phase_times
+
+
+@pytest.mark.gpu
+def test_full_oracle_is_independent_of_the_pipeline(golden_cases):
+    """verify_output(full-oracle) builds its expected CSC with gt_verify_transpose
+    (histogram + global key sort), which equals the reference goldens, accepts
+    the product's output and rejects a corrupted copy of it."""
+    import torch
+
+    from paper_2501_06872_b200 import CsrGraph, transpose_gpu, verify_output
+    from paper_2501_06872_b200.verify import reference_transpose_device
+
+    for name, c in golden_cases.items():
+        off = torch.from_numpy(c["off"].astype(np.uint64).view(np.int64)).cuda()
+        edg = torch.from_numpy(c["edg"].astype(np.uint32).view(np.int32)).cuda()
+        o, e = reference_transpose_device(off, edg, c["nv"])
+        assert np.array_equal(o.cpu().numpy().view(np.uint64), c["toff"]), name
+        assert np.array_equal(e.cpu().numpy().view(np.uint32), c["tedg"]), name
+    rng = np.random.default_rng(8)
+    src = rng.integers(0, 3000, 100_000)
+    dst = np.minimum((3000 * rng.random(100_000) ** 3).astype(np.int64), 2999)
+    g = CsrGraph.from_edge_pairs(src, dst, 3000)
+    out = transpose_gpu(g)
+    assert verify_output(g, out, mode="full-oracle").passed
+    bad = out.graph.edges.copy()
+    i = int(out.graph.offsets[0])  # vertex 0 (the hub): swap two of its sources
+    bad[i], bad[i + 1] = bad[i + 1], bad[i] if bad[i] != bad[i + 1] else bad[i] + 1
+    t = CsrGraph(3000, g.num_edges, out.graph.offsets, bad, "CSC")
+    out.graph = t
+    r = verify_output(g, out, mode="full-oracle")
+    assert not r.passed and r.mismatch_vertex == 0
