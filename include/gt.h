@@ -297,6 +297,19 @@ int gt_sort_lists(const uint64_t *offsets, const uint32_t *edges, uint64_t num_v
  * offsets from the in-degree histogram, lists from a global radix sort of
  * (destination << 32 | source) keys (CUB) — transpose_oracle's lexsort
  * (graph.py:136-148) with none of the partition kernels it checks.  E < 2^32. */
+/* Debug checks of a transpose (transpose_potra(debug=True), the GPU analogue
+ * of the reference's write-once bitmap and conservation asserts,
+ * hlh.py:400-419, 523-528, 550-558), run on a t_edges that was filled with
+ * 0xFFFFFFFF before the transpose: unwritten = slots never written (a slot
+ * written twice leaves another one unwritten), descents = adjacent pairs out
+ * of order inside a list, offset_diff = first index where t_offsets differs
+ * from the in-degree scan (V+1 if none), multiset_diff = first destination
+ * whose list is not the multiset of its sources (hash sums; V if none). */
+typedef struct gt_debug_report {
+    uint64_t unwritten, descents, offset_diff, multiset_diff;
+} gt_debug_report;
+int gt_debug_check(const uint64_t *offsets, const uint32_t *edges, uint64_t num_vertices, uint64_t num_edges,
+                   const uint64_t *t_offsets, const uint32_t *t_edges, gt_debug_report *report, void *stream);
 int gt_verify_transpose(const uint64_t *offsets, const uint32_t *edges, uint64_t num_vertices, uint64_t num_edges,
                         uint64_t *t_offsets, uint32_t *t_edges, void *stream);
 int gt_first_diff_u64(const uint64_t *a, const uint64_t *b, uint64_t n, uint64_t *first, void *stream);

@@ -66,6 +66,11 @@ class MultiInfo(ctypes.Structure):
     ]
 
 
+class DebugReport(ctypes.Structure):
+    _fields_ = [("unwritten", ctypes.c_uint64), ("descents", ctypes.c_uint64), ("offset_diff", ctypes.c_uint64),
+                ("multiset_diff", ctypes.c_uint64)]
+
+
 class PotgHeader(ctypes.Structure):
     _fields_ = [
         ("version", ctypes.c_uint32),
@@ -118,6 +123,7 @@ SYMBOLS = {
     "gt_build_csr": (_int, [_vp, _vp, _u64, _u64, _vp, _vp, _vp]),
     "gt_sort_lists": (_int, [_vp, _vp, _u64, _u64, _vp, _vp]),
     "gt_verify_transpose": (_int, [_vp, _vp, _u64, _u64, _vp, _vp, _vp]),
+    "gt_debug_check": (_int, [_vp, _vp, _u64, _u64, _vp, _vp, ctypes.POINTER(DebugReport), _vp]),
     "gt_first_diff_u64": (_int, [_vp, _vp, _u64, _u64p, _vp]),
     "gt_first_diff_u32": (_int, [_vp, _vp, _u64, _u64p, _vp]),
     "gt_in_degree_offsets": (_int, [_vp, _u64, _u64, _vp, _vp]),

@@ -80,6 +80,58 @@ __global__ void k_low_words(const uint64_t* __restrict__ keys, uint64_t E, uint3
     out[i] = (uint32_t)keys[i];
 }
 
+// ---- debug checks (transpose_potra(debug=True) / transpose_gpu(debug=True))
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {  // splitmix64 finaliser
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+// warp per source: h[d] += mix(s) for every edge (s, d)
+__global__ void k_hash_in(const uint64_t* __restrict__ off, const uint32_t* __restrict__ e, uint64_t V,
+                          unsigned long long* __restrict__ h) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t s = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); s < V; s += warps) {
+    const uint64_t m = mix64(s);
+    for (uint64_t j = off[s] + lane; j < off[s + 1]; j += 32) atomicAdd(&h[e[j]], (unsigned long long)m);
+  }
+}
+// warp per destination: h[d] -= mix(t_edges[j]) over its list; descents and
+// sentinels (slots never written) counted
+__global__ void k_hash_out(const uint64_t* __restrict__ toff, const uint32_t* __restrict__ te, uint64_t V,
+                           unsigned long long* __restrict__ h, unsigned long long* __restrict__ cnt) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t d = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); d < V; d += warps) {
+    unsigned long long acc = 0, unwritten = 0, desc = 0;
+    const uint64_t a = toff[d], b = toff[d + 1];
+    for (uint64_t j = a + lane; j < b; j += 32) {
+      const uint32_t x = te[j];
+      if (x == 0xffffffffu) ++unwritten;
+      else acc += mix64(x);
+      if (j + 1 < b && te[j + 1] < x) ++desc;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      unwritten += __shfl_xor_sync(0xffffffffu, unwritten, o);
+      desc += __shfl_xor_sync(0xffffffffu, desc, o);
+    }
+    if (lane == 0) {
+      h[d] -= acc;
+      if (unwritten) atomicAdd(&cnt[0], unwritten);
+      if (desc) atomicAdd(&cnt[1], desc);
+    }
+  }
+}
+__global__ void k_first_nonzero(const unsigned long long* __restrict__ h, uint64_t n, unsigned long long* first) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    if (h[i]) {
+      atomicMin(first, (unsigned long long)i);
+      return;
+    }
+}
+
 int cuda_fail(cudaError_t e) {
   return gt_internal_set_err(e == cudaErrorMemoryAllocation ? GT_ENOMEM : GT_ECUDA, cudaGetErrorString(e));
 }
@@ -160,6 +212,47 @@ int gt_verify_transpose(const uint64_t* offsets, const uint32_t* edges, uint64_t
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e);
   return GT_OK;
+}
+
+int gt_debug_check(const uint64_t* offsets, const uint32_t* edges, uint64_t V, uint64_t E, const uint64_t* t_offsets,
+                   const uint32_t* t_edges, gt_debug_report* report, void* stream) {
+  if (!offsets || !t_offsets || !report || (E && (!edges || !t_edges))) return gt_internal_set_err(GT_EINVAL, "null argument");
+  if (V == 0 || V >= (1ull << 32) || E >= (1ull << 32)) return gt_internal_set_err(GT_EINVAL, "debug check: size out of range");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  report->unwritten = report->descents = 0;
+  report->offset_diff = V + 1;
+  report->multiset_diff = V;
+  uint64_t* exp_off = nullptr;
+  unsigned long long* h = nullptr;
+  cudaError_t e;
+  if ((e = cudaMallocAsync(&exp_off, (V + 1) * 8, st)) != cudaSuccess) return cuda_fail(e);
+  if ((e = cudaMallocAsync(&h, (V + 3) * 8, st)) != cudaSuccess) {
+    cudaFreeAsync(exp_off, st);
+    return cuda_fail(e);
+  }
+  int rc = gt_in_degree_offsets(edges, E, V, exp_off, st);
+  uint64_t first = V + 1;
+  if (rc == GT_OK) rc = gt_first_diff_u64(exp_off, t_offsets, V + 1, &first, st);
+  if (rc == GT_OK) {
+    report->offset_diff = first;
+    if (first == V + 1) {  // lists are delimited correctly: hash them against the input
+      cudaMemsetAsync(h, 0, (V + 3) * 8, st);
+      k_hash_in<<<148 * 8, 256, 0, st>>>(offsets, edges, V, h);
+      k_hash_out<<<148 * 8, 256, 0, st>>>(t_offsets, t_edges, V, h, h + V);
+      cudaMemsetAsync(h + V + 2, 0xff, 8, st);
+      k_first_nonzero<<<148 * 8, 256, 0, st>>>(h, V, h + V + 2);
+      unsigned long long tail[3];
+      cudaMemcpyAsync(tail, h + V, 24, cudaMemcpyDeviceToHost, st);
+      if ((e = cudaStreamSynchronize(st)) != cudaSuccess) rc = cuda_fail(e);
+      report->unwritten = tail[0];
+      report->descents = tail[1];
+      report->multiset_diff = (tail[2] == ~0ull) ? V : tail[2];
+    }
+  }
+  cudaFreeAsync(exp_off, st);
+  cudaFreeAsync(h, st);
+  cudaStreamSynchronize(st);
+  return rc;
 }
 
 int gt_first_diff_u64(const uint64_t* a, const uint64_t* b, uint64_t n, uint64_t* first, void* stream) {

@@ -113,14 +113,42 @@ def transpose_device(offsets, edges, num_vertices: int, *, t_offsets=None, t_edg
     return t_offsets, t_edges, st
 
 
-def transpose_gpu(g, devices: int = 1, *, device=None, stream=None) -> TransposeOutput:
+def _debug_check(off_d, edg_d, t_off, t_edg, nv: int, torch) -> dict:
+    """The reference's debug asserts (hlh.py:400-419, 523-528, 550-558) on the
+    device: write-once slots, offsets = in-degree scan, ascending lists,
+    per-destination source multisets (gt_debug_check)."""
+    rep = _lib.DebugReport()
+    with torch.cuda.device(off_d.device):
+        rc = _lib.lib.gt_debug_check(ctypes.c_void_p(off_d.data_ptr()), ctypes.c_void_p(edg_d.data_ptr()), nv,
+                                     int(edg_d.numel()), ctypes.c_void_p(t_off.data_ptr()),
+                                     ctypes.c_void_p(t_edg.data_ptr()), ctypes.byref(rep),
+                                     _stream_handle(torch, None))
+    _lib.check(rc, "gt_debug_check")
+    r = {"unwritten": int(rep.unwritten), "descents": int(rep.descents), "offset_diff": int(rep.offset_diff),
+         "multiset_diff": int(rep.multiset_diff)}
+    if r["offset_diff"] != nv + 1:
+        raise AssertionError(f"split counters do not sum to the edge count (t_offsets differ at index "
+                             f"{r['offset_diff']})")
+    if r["unwritten"]:
+        raise AssertionError(f"a t_edges index was written more than once ({r['unwritten']} slots never written)")
+    if r["multiset_diff"] != nv:
+        raise AssertionError(f"the list of vertex {r['multiset_diff']} is not the multiset of its sources")
+    if r["descents"]:
+        raise AssertionError(f"{r['descents']} adjacent pairs out of order inside neighbour lists")
+    return r
+
+
+def transpose_gpu(g, devices: int = 1, *, device=None, stream=None, debug: bool = False) -> TransposeOutput:
     """Transpose a CsrGraph on the GPU; same contract as transpose_atomic +
     sort_neighbor_lists, output equal to transpose_oracle(g).
 
     ``devices`` plays the role of the reference's ``threads`` (must be >= 1,
     _nb.py:112-113).  ``devices > 1`` needs an initialised torch.distributed
     process group with that many ranks (one process per GPU) and dispatches to
-    :func:`paper_2501_06872_b200.multi.transpose_distributed`.
+    :func:`paper_2501_06872_b200.multi.transpose_distributed`.  ``debug``
+    runs the reference's debug asserts on the device (write-once slots,
+    degree conservation, ascending lists, source multisets; ``_debug_check``)
+    and raises AssertionError on a violation.
     """
     if devices < 1:
         raise ValueError(f"device count must be >= 1, got {devices}")
@@ -139,7 +167,11 @@ def transpose_gpu(g, devices: int = 1, *, device=None, stream=None) -> Transpose
     off_d = torch.from_numpy(np.ascontiguousarray(g.offsets).view(np.int64)).to(dev, non_blocking=False)
     edg_d = torch.from_numpy(np.ascontiguousarray(g.edges).view(np.int32)).to(dev, non_blocking=False)
     t1 = time.perf_counter()
-    t_off, t_edg, st = transpose_device(off_d, edg_d, nv, stream=stream, want_stats=True)
+    t_edg0 = None
+    if debug:  # every slot starts as the sentinel 0xFFFFFFFF (IDs are < 2^29)
+        t_edg0 = torch.full((ne,), -1, dtype=torch.int32, device=dev)
+    t_off, t_edg, st = transpose_device(off_d, edg_d, nv, t_edges=t_edg0, stream=stream, want_stats=True)
+    dbg = _debug_check(off_d, edg_d, t_off, t_edg, nv, torch) if debug and nv > 0 else None
     t2 = time.perf_counter()
     t_offsets = t_off.cpu().numpy().view(np.uint64)
     t_edges = t_edg.cpu().numpy().view(np.uint32)
@@ -163,6 +195,7 @@ def transpose_gpu(g, devices: int = 1, *, device=None, stream=None) -> Transpose
             "rank_mode": "smem-atomic" if st.rank_mode == 0 else "or-mask",
             "big_buckets": int(st.n_big_buckets),
             "devices": 1,
+            **({"debug": dbg} if dbg is not None else {}),
         },
     )
 
@@ -231,7 +264,7 @@ def transpose_potra(g, threads: int, budget=None, *, force_method=None, sample_f
     plan = sample_hdv(g, k, sample_fraction=sample_fraction, seed=seed, threads=threads,
                       load_factor=budget.load_factor)
     step0 = time.perf_counter() - t0
-    out = transpose_gpu(g)
+    out = transpose_gpu(g, debug=debug)
     details = {
         "method_chosen": "gpu",
         "k": plan.k,

@@ -76,3 +76,22 @@ def random_graph(rng, max_vertices=1000, max_edges=10_000):
     else:
         dst = np.minimum((nv * rng.random(ne) ** 3).astype(np.int64), nv - 1)
     return CsrGraph.from_edge_pairs(src, dst, nv)
+
+
+def skewed_reference_graph():
+    """potra.relabel_random(potra.generate_skewed(300000, 4000000, 1.1, seed=7),
+    seed=8) restated in numpy (graph.py:187-222, 225-249): Zipf destinations by
+    inverse CDF (searchsorted, 2^24-draw chunks), uniform sources, a seeded
+    permutation of both endpoints, canonical CSR."""
+    from paper_2501_06872_b200 import CsrGraph
+
+    nv, ne, zipf = 300_000, 4_000_000, 1.1
+    rng = np.random.default_rng(7)
+    cdf = np.cumsum(np.arange(1, nv + 1, dtype=np.float64) ** -zipf)
+    cdf /= cdf[-1]
+    src = rng.integers(0, nv, size=ne, dtype=np.int64)
+    dst = np.searchsorted(cdf, rng.random(ne), side="right")
+    g = CsrGraph.from_edge_pairs(src, dst, nv)
+    perm = np.random.default_rng(8).permutation(nv).astype(np.int64)
+    owners = np.repeat(np.arange(nv, dtype=np.int64), np.diff(g.offsets.astype(np.int64)))
+    return CsrGraph.from_edge_pairs(perm[owners], perm[g.edges.astype(np.int64)], nv)

@@ -11,7 +11,7 @@ import threading
 import numpy as np
 import pytest
 
-from conftest import ROOT, sha
+from conftest import ROOT, sha, skewed_reference_graph
 
 sys.path.insert(0, str(ROOT))
 from oracle import oracle  # noqa: E402  (test infrastructure)
@@ -176,32 +176,13 @@ def test_status_word_without_stats():
     _check(t_off, t_edg, g)
 
 
-def _skewed_reference_graph():
-    """potra.relabel_random(potra.generate_skewed(300000, 4000000, 1.1, seed=7),
-    seed=8) restated in numpy (graph.py:187-222, 225-249): Zipf destinations by
-    inverse CDF (searchsorted, 2^24-draw chunks), uniform sources, a seeded
-    permutation of both endpoints, canonical CSR."""
-    from paper_2501_06872_b200 import CsrGraph
-
-    nv, ne, zipf = 300_000, 4_000_000, 1.1
-    rng = np.random.default_rng(7)
-    cdf = np.cumsum(np.arange(1, nv + 1, dtype=np.float64) ** -zipf)
-    cdf /= cdf[-1]
-    src = rng.integers(0, nv, size=ne, dtype=np.int64)
-    dst = np.searchsorted(cdf, rng.random(ne), side="right")
-    g = CsrGraph.from_edge_pairs(src, dst, nv)
-    perm = np.random.default_rng(8).permutation(nv).astype(np.int64)
-    owners = np.repeat(np.arange(nv, dtype=np.int64), np.diff(g.offsets.astype(np.int64)))
-    return CsrGraph.from_edge_pairs(perm[owners], perm[g.edges.astype(np.int64)], nv)
-
-
 def test_skewed_4m_reference_hash(golden_hashes):
     """The reference-made skewed_4m golden: the restated generator reproduces the
     reference's input bit for bit, and the GPU transpose hashes to the
     reference's transpose_oracle output."""
     from paper_2501_06872_b200 import transpose_gpu
 
-    g = _skewed_reference_graph()
+    g = skewed_reference_graph()
     assert sha(g.offsets, g.edges) == golden_hashes["skewed_4m"]["input"]
     out = transpose_gpu(g)
     assert sha(out.graph.offsets, out.graph.edges) == golden_hashes["skewed_4m"]["oracle"]
@@ -232,3 +213,42 @@ def test_counter_overflow_raises():
     torch.cuda.synchronize()
     with pytest.raises(CounterOverflowError):
         transpose_status()
+
+
+def test_debug_mode_checks(golden_cases):
+    """transpose_gpu / transpose_potra(debug=True): the reference's debug
+    asserts on the device pass on real outputs and fire on corrupted ones
+    (a slot never written, a wrong source, two sources out of order)."""
+    import torch
+
+    from paper_2501_06872_b200 import transpose_gpu, transpose_potra
+    from paper_2501_06872_b200.transpose import _debug_check
+
+    for name in sorted(golden_cases)[:30]:
+        c = golden_cases[name]
+        from paper_2501_06872_b200 import CsrGraph
+
+        g = CsrGraph(c["nv"], int(c["edg"].size), c["off"].astype(np.uint64), c["edg"].astype(np.uint32))
+        out = transpose_gpu(g, debug=True)
+        if c["nv"]:
+            assert out.details["debug"]["unwritten"] == 0, name
+    g = _rand_graph(41, nv=20_011, ne=400_000, skew=4.0)
+    out = transpose_potra(g, 4, debug=True)
+    assert out.details["debug"] == {"unwritten": 0, "descents": 0, "offset_diff": g.num_vertices + 1,
+                                    "multiset_diff": g.num_vertices}
+    off, edg = _dev(torch, g)
+    t_off = torch.from_numpy(out.graph.offsets.view(np.int64)).cuda()
+    good = out.graph.edges.copy()
+    hub_start = int(out.graph.offsets[int(np.argmax(np.diff(out.graph.offsets.astype(np.int64))))])
+    cases = {}
+    bad = good.copy(); bad[hub_start + 3] = 0xFFFFFFFF; cases["written more than once"] = bad
+    bad = good.copy(); bad[hub_start + 3] ^= 1; cases["multiset"] = bad
+    bad = good.copy(); bad[hub_start], bad[hub_start + 1] = good[hub_start + 1] + 1, good[hub_start]
+    cases["not the multiset"] = bad
+    for msg, b in cases.items():
+        with pytest.raises(AssertionError, match=msg.split()[0]):
+            _debug_check(off, edg, t_off, torch.from_numpy(b.view(np.int32)).cuda(), g.num_vertices, torch)
+    bad = good.copy(); bad[hub_start], bad[hub_start + 1] = good[hub_start + 1], good[hub_start]
+    if good[hub_start] != good[hub_start + 1]:
+        with pytest.raises(AssertionError, match="out of order"):
+            _debug_check(off, edg, t_off, torch.from_numpy(bad.view(np.int32)).cuda(), g.num_vertices, torch)

@@ -142,3 +142,15 @@ def test_host_generator_matches_numpy_generator(name):
         o1, e1 = gen.generate_np(cfg)
         o2, e2 = oracle.generate_c(cfg, 4)
         assert np.array_equal(o1, o2) and np.array_equal(e1, e2), cfg.name
+
+
+def test_skewed_4m_generator_restatement_and_oracle(golden_hashes):
+    """The restated skewed_4m generator (conftest.skewed_reference_graph)
+    reproduces the reference's input bit for bit, and the C oracle's transpose
+    of it hashes to the reference's transpose_oracle output."""
+    from conftest import sha, skewed_reference_graph
+
+    g = skewed_reference_graph()
+    assert sha(g.offsets, g.edges) == golden_hashes["skewed_4m"]["input"]
+    o, e = oracle.transpose_c(g.offsets, g.edges, g.num_vertices)
+    assert sha(o, e) == golden_hashes["skewed_4m"]["oracle"]
