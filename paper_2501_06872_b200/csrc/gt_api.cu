@@ -91,12 +91,7 @@ struct Plan {
   int gbits = 0;       // compact R2: fine-digit bits kept beside the low digit
   int D1 = 1, Db = 1, Dc = 1;
   int exp = 0;  // gt_config.reserved[0]: experiment bits (A/B measurements; 0 = product path)
-  bool hubs = false;  // level-2 hub segments
-  int D2 = 1;         // level-2 digits per bucket: Db, or Db + 2 * kHubMax in hub mode
 };
-constexpr int kHubMax = 128;        // hubs per coarse bucket
-constexpr uint32_t kHubStride = 2048;  // hub sample: 256 of every 2048 level-1 records
-constexpr uint32_t kHubThr = 64;    // sampled records of a hub (~512 in-edges)
 
 // Digit split of the destination ID for a graph of V destinations, E edges,
 // Vsrc source IDs.  Compact form: 4-byte R1 and R2 records; wide form: E >=
@@ -177,10 +172,6 @@ int make_plan(uint64_t V, uint64_t E, uint64_t Vsrc, const gt_config& cfg, Plan&
   p.Db = 1 << p.b;
   p.Dc = 1 << p.c;
   p.exp = cfg.reserved[0];
-  // hub segments: compact form, <= 256 fine buckets per coarse bucket, and a
-  // coarse bucket's vertex histogram fits in shared memory (b + c <= 15)
-  p.hubs = !p.wide && p.Db <= 256 && p.b + p.c <= 15 && !(p.exp & 2);
-  p.D2 = p.hubs ? p.Db + 2 * kHubMax : p.Db;
   return GT_OK;
 }
 
@@ -189,10 +180,9 @@ int make_plan(uint64_t V, uint64_t E, uint64_t Vsrc, const gt_config& cfg, Plan&
 // R2 (4E, + E low-digit bytes for the wide form) is the bulk.
 struct Layout {
   uint64_t ntiles1 = 0, nplace = 0, nh = 0, nruns = 0, max_t2 = 0, nfine = 0, max_big = 0, max_t3 = 0;
-  uint64_t njobs = 0;
   uint64_t o_r2, o_r2lv, o_tcnt, o_tbase, o_status, o_ctr, o_psrc, o_prev, o_seghi, o_runs, o_rfirst, o_bstart,
       o_tiles2, o_cnt2, o_base2, o_seg2, o_fbase, o_units, o_bigs, o_tiles3, o_cnt3, o_base3, o_seg3, o_cnt, o_err,
-      o_bnt, o_bfirst, o_htab, o_hdig, o_jobs, total;
+      o_bnt, o_bfirst, total;
 };
 
 // E1: level-1 edges (0: no level 1 here); E23: records of levels 2-3; D1: local buckets; R: runs per bucket.
@@ -203,8 +193,7 @@ void make_layout(const Plan& p, uint64_t E1, uint64_t E23, uint32_t R, Layout& q
   q.nh = 1ull << p.nsh;
   q.nruns = (uint64_t)p.D1 * R;
   q.max_t2 = (E23 + v3::CT2 - 1) / v3::CT2 + q.nruns;
-  q.nfine = (uint64_t)p.D1 * p.D2;  // level-2 digits (fine buckets, or segments in hub mode)
-  q.njobs = p.hubs ? (uint64_t)p.D1 * kHubMax + E23 / v3::kHubChunk + 1 : 0;
+  q.nfine = (uint64_t)p.D1 * p.Db;
   q.max_big = std::min<uint64_t>(q.nfine, E23 / v3::CAP3 + 1);
   q.max_t3 = (E23 + v3::CT2 - 1) / v3::CT2 + q.max_big;
   uint64_t off = 0;
@@ -219,7 +208,7 @@ void make_layout(const Plan& p, uint64_t E1, uint64_t E23, uint32_t R, Layout& q
   q.o_tcnt = take(n1 * 4);
   q.o_tbase = take((n1 + 1) * 8);
   const uint64_t nscan = std::max<uint64_t>(std::max<uint64_t>(n1 + 1, q.max_big + 1),
-                                            std::max<uint64_t>(q.max_t2 * (uint64_t)p.D2, q.max_t3 * (uint64_t)p.Dc));
+                                            std::max<uint64_t>(q.max_t2 * (uint64_t)p.Db, q.max_t3 * (uint64_t)p.Dc));
   q.o_status = take(((nscan + kScanTile - 1) / kScanTile + 1) * 8);
   q.o_ctr = take(64);
   q.o_psrc = take((q.nplace + 2) * 4);
@@ -229,8 +218,8 @@ void make_layout(const Plan& p, uint64_t E1, uint64_t E23, uint32_t R, Layout& q
   q.o_rfirst = take((q.nruns + 1) * 4);
   q.o_bstart = take(((uint64_t)p.D1 + 1) * 8);
   q.o_tiles2 = take(q.max_t2 * sizeof(v3::RTile));
-  q.o_cnt2 = take(q.max_t2 * (uint64_t)p.D2 * 4);
-  q.o_base2 = take(q.max_t2 * (uint64_t)p.D2 * 8);
+  q.o_cnt2 = take(q.max_t2 * (uint64_t)p.Db * 4);
+  q.o_base2 = take(q.max_t2 * (uint64_t)p.Db * 8);
   q.o_seg2 = take((uint64_t)p.D1 * sizeof(v3::SegDesc));
   q.o_fbase = take((q.nfine + 1) * 8);
   q.o_units = take(q.nfine * sizeof(v3::Unit3));
@@ -243,9 +232,6 @@ void make_layout(const Plan& p, uint64_t E1, uint64_t E23, uint32_t R, Layout& q
   q.o_err = take(4);
   q.o_bnt = take((q.max_big + 1) * 4);
   q.o_bfirst = take((q.max_big + 2) * 8);
-  q.o_htab = take(p.hubs ? (uint64_t)p.D1 * p.Db * 8 : 0);
-  q.o_hdig = take(p.hubs ? (uint64_t)p.D1 * 4 : 0);
-  q.o_jobs = take(q.njobs * sizeof(v3::HubJob));
   q.total = off;
 }
 
@@ -482,9 +468,6 @@ struct Ws {
   unsigned int* err;
   uint32_t* bnt;
   uint64_t* bfirst;
-  uint64_t* htab;
-  uint32_t* hdig;
-  v3::HubJob* jobs;
 };
 Ws ws_ptrs(const Layout& q, unsigned char* ws, const Plan& p) {
   Ws w;
@@ -515,9 +498,6 @@ Ws ws_ptrs(const Layout& q, unsigned char* ws, const Plan& p) {
   w.err = reinterpret_cast<unsigned int*>(ws + q.o_err);
   w.bnt = reinterpret_cast<uint32_t*>(ws + q.o_bnt);
   w.bfirst = reinterpret_cast<uint64_t*>(ws + q.o_bfirst);
-  w.htab = reinterpret_cast<uint64_t*>(ws + q.o_htab);
-  w.hdig = reinterpret_cast<uint32_t*>(ws + q.o_hdig);
-  w.jobs = reinterpret_cast<v3::HubJob*>(ws + q.o_jobs);
   return w;
 }
 
@@ -614,8 +594,7 @@ int level23(const Plan& p, const Layout& q, Ws& w, const uint32_t* r1, uint32_t 
     while ((ml >> p.c) >> (b + 1)) ++b;
     return b;
   };
-  const bool pos_fine = p.wide || p.hubs || p.gbits < log2_groups(256);
-  const int D2 = p.D2;  // level-2 digits per bucket (Db, or Db + 2 * kHubMax with hub segments)
+  const bool pos_fine = p.wide || p.gbits < log2_groups(256);
   const int sbits = pos_fine ? log2_groups(ML3) : log2_groups(256);
   const int g3 = pos_fine ? 0 : sbits;
 
@@ -623,47 +602,22 @@ int level23(const Plan& p, const Layout& q, Ws& w, const uint32_t* r1, uint32_t 
   // ---- level 2: tiles of every run, count, per-bucket bases, place into R2
   k_runs_plan<<<1, 1024, 0, st>>>(w.runs, nruns, R, w.rfirst, w.bstart);
   GT_LAUNCH_CHECK();
-  k_l2_tiles<<<D1, 128, 0, st>>>(w.runs, R, row_stride, w.rfirst, w.bstart, D2, seg_hi, nh, w.tiles2, w.seg2);
+  k_l2_tiles<<<D1, 128, 0, st>>>(w.runs, R, row_stride, w.rfirst, w.bstart, Db, seg_hi, nh, w.tiles2, w.seg2);
   GT_LAUNCH_CHECK();
   const uint32_t* n_t2 = w.rfirst + nruns;
   const unsigned gt2 = (unsigned)std::min<uint64_t>(q.max_t2, (uint64_t)sms * 8);
-  GT_CUDA(cudaMemsetAsync(w.cnt2, 0, q.max_t2 * (uint64_t)D2 * 4, st));  // the scan covers the unused tail too
-  DecR1H dech;  // hub mode decoder (its DecR1 part is filled below)
-  if (p.hubs) {
-    // hub segments: per bucket the heaviest sampled vertices (<= 3 per fine
-    // bucket, <= kHubMax per bucket) get level-2 digits of their own
-    const size_t hsm = (size_t)4 << (p.b + p.c);
-    if ((rc = set_smem(k_hub_select, hsm))) return rc;
-    k_hub_select<<<D1, 1024, hsm, st>>>(w.runs, R, r1, p.L, p.b, p.c, kHubStride, kHubThr, kHubMax, w.htab, w.hdig);
-    GT_LAUNCH_CHECK();
-    dech.L = p.L;
-    dech.src_mask = (uint32_t)((1ull << p.L) - 1);
-    dech.shB = p.L + p.c;
-    dech.maskB = (uint32_t)(Db - 1);
-    dech.lvmask = (uint32_t)((1ull << p.c) - 1);
-    dech.nbs = p.nbs;
-    dech.nh = nh;
-    dech.seg_hi = seg_hi;
-    dech.htab = w.htab;
-    dech.row_stride = row_stride;
-    dech.c = p.c;
-    dech.tab = nullptr;
-    if ((rc = set_smem(k_cnt_hub, (size_t)D2 * 4))) return rc;
-    k_cnt_hub<<<gt2, 512, (size_t)D2 * 4, st>>>(r1, w.tiles2, n_t2, D2, dech, w.cnt2);
-    *launches += 1;
-  } else {
-    if ((rc = set_smem(k_cnt_rec, (size_t)Db * 4))) return rc;
-    k_cnt_rec<<<gt2, 512, (size_t)Db * 4, st>>>(r1, w.tiles2, n_t2, Db, DigSM{p.L + p.c, (uint32_t)(Db - 1)}, w.cnt2);
-  }
+  GT_CUDA(cudaMemsetAsync(w.cnt2, 0, q.max_t2 * (uint64_t)Db * 4, st));  // the scan covers the unused tail too
+  if ((rc = set_smem(k_cnt_rec, (size_t)Db * 4))) return rc;
+  k_cnt_rec<<<gt2, 512, (size_t)Db * 4, st>>>(r1, w.tiles2, n_t2, Db, DigSM{p.L + p.c, (uint32_t)(Db - 1)}, w.cnt2);
   GT_LAUNCH_CHECK();
   // bases of every (tile, fine digit): one device-wide exclusive scan of the
   // per-bucket digit-major count tables (concatenated in bucket order), then a
   // per-bucket rebase to its output start, which also writes the fine-bucket starts
-  if ((rc = scan_u32_to_u64(w.cnt2, (uint64_t)q.max_t2 * D2, w.base2, 0, false, w.status, w.ctr, st))) return rc;
+  if ((rc = scan_u32_to_u64(w.cnt2, (uint64_t)q.max_t2 * Db, w.base2, 0, false, w.status, w.ctr, st))) return rc;
   GT_CUDA(cudaMemsetAsync(w.cnt + 4, 0, 4, st));
   k_set_u32<<<1, 1, 0, st>>>(w.cnt + 4, (uint32_t)D1);
   GT_LAUNCH_CHECK();
-  k_segfix<<<(unsigned)D1, 512, 0, st>>>(w.seg2, w.cnt + 4, D2, w.base2, w.fbase, q.nfine, w.err);
+  k_segfix<<<(unsigned)D1, 512, 0, st>>>(w.seg2, w.cnt + 4, Db, w.base2, w.fbase, q.nfine, w.err);
   GT_LAUNCH_CHECK();
   {
     DecR1 dec;
@@ -676,13 +630,7 @@ int level23(const Plan& p, const Layout& q, Ws& w, const uint32_t* r1, uint32_t 
     dec.nh = nh;
     dec.seg_hi = seg_hi;
     if ((rc = tm.kbegin(1))) return rc;
-    if (p.hubs) {  // 4096-record tiles over the segment digits
-      auto kern = k_p2<kMode, DecR1H, 16, false, kIoPlain, false>;
-      const size_t sm = smem_p2(D2, kMode, 16);
-      if ((rc = set_smem(kern, sm))) return rc;
-      kern<<<persistent_grid(kern, T, sm, q.max_t2), T, sm, st>>>(r1, w.tiles2, n_t2, D2, dech, w.base2, w.r2, nullptr,
-                                                                   nullptr, nullptr);
-    } else if (p.wide) {  // R2 = source array + low-digit bytes, 64-bit positions
+    if (p.wide) {  // R2 = source array + low-digit bytes, 64-bit positions
       const size_t sm16 = smem_p2(Db, kMode, 32, kIoSplit, 16);
       if (sm16 + 64 <= max_smem_optin()) {  // 16384-record tiles, one 16-warp CTA per SM (C5: 88.4 -> 65.9 ms)
         auto kern = k_p2<kMode, DecR1, 32, false, kIoSplit, true, 16, 1>;
@@ -715,13 +663,8 @@ int level23(const Plan& p, const Layout& q, Ws& w, const uint32_t* r1, uint32_t 
   // ---- level 3: units of small fine buckets; tiled count / scan / place for big ones
   k_set_u64<<<1, 1, 0, st>>>(w.fbase + q.nfine, E);
   GT_LAUNCH_CHECK();
-  if (p.hubs)  // segments: units between hubs, hub lists final (copy jobs), hub offsets
-    k_plan3h<<<(unsigned)((D1 + 127) / 128), 128, 0, st>>>(w.fbase, w.bstart, w.htab, w.hdig, (uint32_t)D1, p.b, p.c,
-                                                            (uint32_t)D2, (uint32_t)CAP3, w.units, w.cnt + 0, w.bigs,
-                                                            w.cnt + 1, w.jobs, w.cnt + 5, t_offsets, V);
-  else
-    k_plan3<<<(unsigned)((q.nfine / (1u << sbits) + 255) / 256 + 1), 256, 0, st>>>(
-        w.fbase, (uint32_t)q.nfine, sbits, w.units, w.cnt + 0, w.bigs, w.cnt + 1, (uint32_t)CAP3);
+  k_plan3<<<(unsigned)((q.nfine / (1u << sbits) + 255) / 256 + 1), 256, 0, st>>>(
+      w.fbase, (uint32_t)q.nfine, sbits, w.units, w.cnt + 0, w.bigs, w.cnt + 1, (uint32_t)CAP3);
   GT_LAUNCH_CHECK();
   // the big-bucket chain runs on a side stream, concurrently with the units
   // (disjoint fine buckets); its short scans overlap the units kernel
@@ -730,12 +673,6 @@ int level23(const Plan& p, const Layout& q, Ws& w, const uint32_t* r1, uint32_t 
   if ((rc = side_stream(&sb, &ev_fork, &ev_join))) return rc;
   GT_CUDA(cudaEventRecord(ev_fork, st));
   GT_CUDA(cudaStreamWaitEvent(sb, ev_fork, 0));
-  if (p.hubs) {  // hub lists R2 -> t_edges (memory-bound, overlaps the units kernel)
-    const uint32_t src_mask = (p.nbs >= 32) ? 0xffffffffu : (uint32_t)((1ull << p.nbs) - 1);
-    k_hub_copy<<<(unsigned)(sms * 4), 256, 0, sb>>>(w.jobs, w.cnt + 5, w.r2, src_mask, t_edges);
-    GT_LAUNCH_CHECK();
-    *launches += 1;
-  }
   {
     const unsigned gb = (unsigned)std::min<uint64_t>((q.max_big + 255) / 256, (uint64_t)sms * 4);
     const uint64_t tiles = std::max<uint64_t>(1, (q.max_big + 1 + kScanTile - 1) / kScanTile);

@@ -67,38 +67,16 @@ struct SegDesc {
   uint64_t base;
   uint64_t out_off;
   uint32_t g0, nt;
-  uint64_t end;        // output position past the segment's last record
-  uint32_t dlo, dhi;   // out[out_off + d] written for d in [dlo, dhi) (dhi == 0: every digit)
+  uint64_t end;  // output position past the segment's last record
 };
 
 struct Unit3 {
   uint64_t start;  // CSC position of the first record
   uint32_t n;      // records (<= CAP3)
-  uint32_t f0;     // first fine bucket (global index A * Db + B); hub mode: first segment (digit) index
-  uint32_t nf;     // fine buckets (hub mode: segments, one per consecutive fine bucket)
-  uint32_t fb0;    // fine bucket of the first segment (hub mode; else f0)
-  uint32_t vlo, vhi;  // local vertices whose offsets the unit writes: [vlo, vhi) (hub mode; else all)
+  uint32_t f0;     // first fine bucket (global index A * Db + B)
+  uint32_t nf;     // fine buckets
+  uint32_t pad;
 };
-static_assert(sizeof(Unit3) == 32, "Unit3 layout");
-
-// Level-2 hub table (hub mode): per coarse bucket and fine
-// bucket B one word: bits 0-9 segbase (the first level-2 digit of B), 10-11
-// nh (hubs of B, <= 3), 12+8i the low digit C of hub i (ascending).  Fine
-// bucket B's records split into segments in vertex order: [C < h0], hub h0,
-// [h0 < C < h1], hub h1, ...; each segment is one level-2 digit, so digit order
-// is CSC order and a hub's digit run is its final CSC list.
-__device__ __forceinline__ uint32_t hub_digit(uint64_t e, uint32_t C) {
-  const uint32_t nh = (uint32_t)(e >> 10) & 3u;
-  uint32_t k = (uint32_t)e & 1023u;
-#pragma unroll
-  for (uint32_t i = 0; i < 3; ++i) {
-    if (i < nh) {
-      const uint32_t h = (uint32_t)(e >> (12 + 8 * i)) & 255u;
-      k += (C > h) ? 2u : ((C == h) ? 1u : 0u);
-    }
-  }
-  return k;
-}
 
 struct DigSM {  // (r >> shift) & mask
   int shift;
@@ -915,8 +893,7 @@ __global__ void __launch_bounds__(512) k_segfix(const SegDesc* __restrict__ segs
     const uint64_t t0 = (uint64_t)S.g0 * D, n = (uint64_t)D * S.nt;
     if (n == 0) {  // empty segment (empty coarse bucket): every digit starts at S.base
       for (int d = threadIdx.x; d < D; d += blockDim.x)
-        if (S.out_off + d < out_limit && (S.dhi == 0 || ((uint32_t)d >= S.dlo && (uint32_t)d < S.dhi)))
-          out[S.out_off + d] = S.base;
+        if (S.out_off + d < out_limit) out[S.out_off + d] = S.base;
       continue;
     }
     const uint64_t v0 = base[t0];
@@ -927,8 +904,7 @@ __global__ void __launch_bounds__(512) k_segfix(const SegDesc* __restrict__ segs
     __syncthreads();
     for (int d = threadIdx.x; d < D; d += blockDim.x) {
       const uint64_t st = base[t0 + (uint64_t)d * S.nt];
-      if (S.out_off + d < out_limit && (S.dhi == 0 || ((uint32_t)d >= S.dlo && (uint32_t)d < S.dhi)))
-        out[S.out_off + d] = st;
+      if (S.out_off + d < out_limit) out[S.out_off + d] = st;
       const uint64_t nx = (d + 1 < D) ? base[t0 + (uint64_t)(d + 1) * S.nt] : S.end;
       if (nx - st >= (1ull << 32)) atomicExch(err, 1u);
     }
@@ -955,25 +931,6 @@ struct DecR1 {
     return (((r >> L) & lvmask) << nbs) | (h << L) | (r & src_mask);
   }
 };
-// DecR1H: DecR1 with hub segments: digit = hub_digit(table[B], C); the
-// bucket's table is staged in shared memory per tile (tab).
-struct DecR1H : DecR1 {
-  const uint64_t* htab;  // Db words per local bucket
-  uint32_t row_stride;   // seg_hi row -> bucket: c = row_stride ? row % row_stride : row
-  int c;
-  const uint64_t* tab;   // shared-memory copy (set in the kernel)
-  static constexpr bool kHub = true;
-  __device__ __forceinline__ uint32_t bucket(uint32_t row) const { return row_stride ? row % row_stride : row; }
-  __device__ __forceinline__ uint32_t digit(uint32_t r) const {
-    const uint32_t B = (r >> shB) & maskB;
-    return hub_digit(tab[B], (r >> L) & ((1u << c) - 1u));
-  }
-};
-template <class Dec, class = void>
-struct HasHub { static constexpr bool value = false; };
-template <class Dec>
-struct HasHub<Dec, decltype((void)Dec::kHub)> { static constexpr bool value = Dec::kHub; };
-
 // DecR2 (level 3, big fine buckets): R2 -> source; digit = low digit C.
 struct DecR2 {
   int nbs;
@@ -1067,10 +1024,6 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
   // kIoSplit: low-digit byte of each staged slot; kIoLv: landing of the digit bytes (16B aligned)
   uint8_t* s_lvx = reinterpret_cast<uint8_t*>(s_bnd + kMaxBnd);                // PT + 16
   __shared__ __align__(8) uint64_t s_bar;
-  constexpr bool kHubD = HasHub<Dec>::value;
-  __shared__ uint64_t s_htab[kHubD ? 256 : 1];  // hub mode: the bucket's table (Db <= 256)
-  Dec dl = dec;
-  if constexpr (kHubD) dl.tab = s_htab;
 
   const uint32_t tid = threadIdx.x, lane = lane_id(), w = warp_id();
   const uint32_t sh = (w & 1) << 4;
@@ -1091,10 +1044,6 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
       else s_gcur[d] = (uint32_t)base[row0 + (uint64_t)d * t.nt];
     }
     const uint32_t nbt = Dec::kSrcHigh ? t.nbnd : 0u;
-    if constexpr (kHubD) {
-      const uint32_t c = dec.bucket(t.seg);
-      for (uint32_t i = tid; i <= dec.maskB; i += T2_) s_htab[i] = dec.htab[(uint64_t)c * (dec.maskB + 1) + i];
-    }
     const uint64_t* hrow = nullptr;
     if constexpr (Dec::kSrcHigh) {
       hrow = dec.seg_hi + (uint64_t)t.seg * (dec.nh + 1) + t.h0 + 1;  // boundary k (1-based) = hrow[k - 1]
@@ -1184,7 +1133,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
         if constexpr (Dec::kSrcHigh) h += wbnd ? slot_owner32(cur, nb, rel0 + i0, nbt, bnd_at) : cur;
         uint32_t d;
         if constexpr (kIO == kIoLv) d = valid ? (uint32_t)s_lvx[o8 + i] : 0u;
-        else d = dl.digit(r);
+        else d = dec.digit(r);
         uint32_t rk;
         if constexpr (Dec::kMatchRank) rk = rank_match(s_cnt + d * WH2_ + (w >> 1), sh, d, valid);
         else rk = rank_pk<kMode>(s_cnt + d * WH2_ + (w >> 1), s_scr + d * WP2_ + w, sh, valid);
@@ -1436,9 +1385,9 @@ __global__ void __launch_bounds__(WW3 * 32, WW3 > 16 ? 1 : 2) k_p3(const P3Args 
     tick(2);
     flat_bases_epi<WH3_, false>(s_cnt, (int)nloc, s_tmp, [](int, uint32_t, uint32_t) {});
     {
-      const uint64_t v0 = (uint64_t)u.fb0 << a.c;
+      const uint64_t v0 = (uint64_t)u.f0 << a.c;
       for (uint32_t v = tid; v < nloc; v += TT)
-        if (v0 + v < a.V && v >= u.vlo && v < u.vhi) a.t_offsets[v0 + v] = u.start + (s_cnt[v * WH3_] & 0xffffu);
+        if (v0 + v < a.V) a.t_offsets[v0 + v] = u.start + (s_cnt[v * WH3_] & 0xffffu);
     }
     tick(3);
     uint32_t* t_e = a.t_edges + u.start;
@@ -1537,7 +1486,7 @@ __global__ void __launch_bounds__(1024) k_runs_plan(const Run* __restrict__ runs
 // One CTA per bucket: its tiles (with the R1 source-high decode state of the
 // run's seg_hi row, row index s * row_stride + c) and its segment descriptor.
 __global__ void k_l2_tiles(const Run* __restrict__ runs, uint32_t R, uint32_t row_stride,
-                           const uint32_t* __restrict__ rfirst, const uint64_t* __restrict__ bstart, int Db /* digits */,
+                           const uint32_t* __restrict__ rfirst, const uint64_t* __restrict__ bstart, int Db,
                            const uint64_t* __restrict__ seg_hi, uint32_t nh, RTile* __restrict__ tiles,
                            SegDesc* __restrict__ segs) {
   const uint32_t c = blockIdx.x;
@@ -1549,7 +1498,6 @@ __global__ void k_l2_tiles(const Run* __restrict__ runs, uint32_t R, uint32_t ro
     S.g0 = g0;
     S.nt = nt;
     S.end = bstart[c + 1];
-    S.dlo = S.dhi = 0;
     segs[c] = S;
   }
   for (uint32_t s = 0; s < R; ++s) {
@@ -1656,9 +1604,7 @@ __global__ void k_plan3(const uint64_t* __restrict__ fbase, uint32_t nfine, int 
     u.n = (uint32_t)tot;
     u.f0 = f;
     u.nf = e - f;
-    u.fb0 = f;
-    u.vlo = 0;
-    u.vhi = 0xffffffffu;
+    u.pad = 0;
     units[atomicAdd(n_units, 1u)] = u;
     f = e;
   }
@@ -1686,8 +1632,6 @@ __global__ void k_big_write(const Big3* __restrict__ bigs, const uint32_t* __res
     S.g0 = g0;
     S.nt = nt;
     S.end = bg.start + bg.n;
-    S.dlo = bg.pad & 0xffffu;  // hub mode: the segment's low-digit range (0, 0: the whole fine bucket)
-    S.dhi = bg.pad >> 16;
     segs[q] = S;
     for (uint32_t j = 0; j < nt; ++j) {
       RTile t;
@@ -1700,238 +1644,6 @@ __global__ void k_big_write(const Big3* __restrict__ bigs, const uint32_t* __res
       t.nbnd = 0;
       tiles[g0 + j] = t;
     }
-  }
-}
-
-
-// ------------------------------------------------------------ hub mode (§2c)
-// Level-2 count with hub digits (the bucket's table staged per tile).
-__global__ void __launch_bounds__(512) k_cnt_hub(const uint32_t* __restrict__ rec, const RTile* __restrict__ tiles,
-                                                 const uint32_t* __restrict__ n_tiles, int D, DecR1H dec,
-                                                 uint32_t* __restrict__ cnt) {
-  extern __shared__ __align__(16) uint32_t s_h[];
-  __shared__ uint64_t s_tab[256];
-  dec.tab = s_tab;
-  const uint32_t nt_all = *n_tiles;
-  for (uint32_t g = blockIdx.x; g < nt_all; g += gridDim.x) {
-    const RTile t = tiles[g];
-    const uint32_t c = dec.bucket(t.seg);
-    for (int d = threadIdx.x; d < D; d += blockDim.x) s_h[d] = 0;
-    for (uint32_t i = threadIdx.x; i <= dec.maskB; i += blockDim.x) s_tab[i] = dec.htab[(uint64_t)c * (dec.maskB + 1) + i];
-    __syncthreads();
-    const uint32_t* p = rec + t.start;
-    const uint32_t n = t.n;
-    const uint32_t head = min(n, (4 - align_items_u32(p)) & 3);
-    for (uint32_t i = threadIdx.x; i < head; i += blockDim.x) smem_inc(&s_h[dec.digit(p[i])]);
-    const uint4* p4 = reinterpret_cast<const uint4*>(p + head);
-    const uint32_t n4 = (n - head) >> 2;
-    for (uint32_t q = threadIdx.x; q < n4; q += blockDim.x) {
-      uint4 v;
-      asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                   : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p4 + q));
-      smem_inc(&s_h[dec.digit(v.x)]);
-      smem_inc(&s_h[dec.digit(v.y)]);
-      smem_inc(&s_h[dec.digit(v.z)]);
-      smem_inc(&s_h[dec.digit(v.w)]);
-    }
-    for (uint32_t i = head + n4 * 4 + threadIdx.x; i < n; i += blockDim.x) smem_inc(&s_h[dec.digit(p[i])]);
-    __syncthreads();
-    const uint64_t row0 = (uint64_t)(g - t.j) * D + t.j;
-    for (int d = threadIdx.x; d < D; d += blockDim.x) cnt[row0 + (uint64_t)d * t.nt] = s_h[d];
-    __syncthreads();
-  }
-}
-
-// Hub selection, one CTA per coarse bucket (HDV sampling, the role of PoTra's
-// step 0, hlh.py:153-228, taken from the level-1 records themselves): a
-// histogram of the local vertex over a sample of the bucket's records (256 of
-// every `stride` records of each run; all of them when the bucket is small),
-// then per fine bucket the up-to-3 heaviest vertices with >= thr sampled
-// records, then the count threshold doubled until <= hmax hubs remain.
-// Writes the bucket's table (htab[c * Db + B], see hub_digit) and its digit
-// count hdig[c] = Db + 2 * hubs.  Requires 2^(b+c) * 4 bytes of shared memory.
-__global__ void __launch_bounds__(1024) k_hub_select(const Run* __restrict__ runs, uint32_t R,
-                                                     const uint32_t* __restrict__ r1, int L, int bits_b, int bits_c,
-                                                     uint32_t stride, uint32_t thr, uint32_t hmax,
-                                                     uint64_t* __restrict__ htab, uint32_t* __restrict__ hdig) {
-  extern __shared__ __align__(16) uint32_t s_hist[];  // 2^(b+c)
-  __shared__ uint32_t s_nh[256], s_tmp[40], s_tot;
-  __shared__ uint32_t s_hc[256][3], s_hv[256][3];  // chosen hubs per fine bucket: sampled count, low digit
-  const uint32_t c = blockIdx.x, Db = 1u << bits_b, nloc = 1u << (bits_b + bits_c);
-  const uint32_t lmask = nloc - 1;
-  for (uint32_t i = threadIdx.x; i < nloc; i += blockDim.x) s_hist[i] = 0;
-  __syncthreads();
-  uint64_t total = 0;
-  for (uint32_t s = 0; s < R; ++s) total += runs[c * R + s].n;
-  const bool all = total <= (uint64_t)stride * 16;  // small bucket: count every record
-  for (uint32_t s = 0; s < R; ++s) {
-    const Run run = runs[c * R + s];
-    const uint32_t* p = r1 + run.start;
-    if (all) {
-      for (uint64_t i = threadIdx.x; i < run.n; i += blockDim.x) atomicAdd(&s_hist[(p[i] >> L) & lmask], 1u);
-    } else {
-      const uint64_t nblk = (run.n + stride - 1) / stride;
-      for (uint64_t q = threadIdx.x; q < nblk * 256; q += blockDim.x) {
-        const uint64_t i = (q >> 8) * stride + (q & 255);
-        if (i < run.n) atomicAdd(&s_hist[(p[i] >> L) & lmask], 1u);
-      }
-    }
-  }
-  const uint32_t th = all ? max(1u, thr * 8u) : thr;  // thresholds in sampled records (1/8 sample)
-  __syncthreads();
-  // per fine bucket: up to 3 heaviest vertices above the threshold
-  for (uint32_t B = threadIdx.x; B < Db; B += blockDim.x) {
-    uint32_t hc[3] = {0, 0, 0}, hv[3] = {0, 0, 0};
-    for (uint32_t C = 0; C < (1u << bits_c); ++C) {
-      const uint32_t x = s_hist[(B << bits_c) | C];
-      if (x < th || x <= hc[2]) continue;
-      if (x > hc[0]) { hc[2] = hc[1]; hv[2] = hv[1]; hc[1] = hc[0]; hv[1] = hv[0]; hc[0] = x; hv[0] = C; }
-      else if (x > hc[1]) { hc[2] = hc[1]; hv[2] = hv[1]; hc[1] = x; hv[1] = C; }
-      else { hc[2] = x; hv[2] = C; }
-    }
-    for (int i = 0; i < 3; ++i) { s_hc[B][i] = hc[i]; s_hv[B][i] = hv[i]; }
-  }
-  __syncthreads();
-  // raise the threshold until at most hmax hubs remain
-  uint32_t t = th;
-  while (true) {
-    if (threadIdx.x == 0) s_tot = 0;
-    __syncthreads();
-    uint32_t mine = 0;
-    for (uint32_t B = threadIdx.x; B < Db; B += blockDim.x)
-      for (int i = 0; i < 3; ++i) mine += (s_hc[B][i] >= t) ? 1u : 0u;
-    if (mine) atomicAdd(&s_tot, mine);
-    __syncthreads();
-    const uint32_t tot = s_tot;
-    __syncthreads();
-    if (tot <= hmax) break;
-    t = (t > 0x7fffffffu) ? 0xffffffffu : t * 2;
-  }
-  // the table: hubs of B ascending by low digit; segbase = B + 2 * hubs before B
-  for (uint32_t B = threadIdx.x; B < Db; B += blockDim.x) {
-    uint32_t v[3], n = 0;
-    for (int i = 0; i < 3; ++i)
-      if (s_hc[B][i] >= t && s_hc[B][i] > 0) v[n++] = s_hv[B][i];
-    for (uint32_t i = 1; i < n; ++i)  // insertion sort (<= 3)
-      for (uint32_t j = i; j > 0 && v[j - 1] > v[j]; --j) { const uint32_t x = v[j]; v[j] = v[j - 1]; v[j - 1] = x; }
-    s_nh[B] = n;
-    for (uint32_t i = n; i < 3; ++i) v[i] = 0;
-    s_hv[B][0] = v[0]; s_hv[B][1] = v[1]; s_hv[B][2] = v[2];
-  }
-  __syncthreads();
-  const uint32_t nh_all = block_excl_scan_u32(s_nh, (int)Db, s_tmp);
-  for (uint32_t B = threadIdx.x; B < Db; B += blockDim.x) {
-    const uint32_t nhB = ((B + 1 < Db) ? s_nh[B + 1] : nh_all) - s_nh[B];
-    const uint64_t e = (uint64_t)(B + 2 * s_nh[B]) | ((uint64_t)nhB << 10) | ((uint64_t)s_hv[B][0] << 12) |
-                       ((uint64_t)s_hv[B][1] << 20) | ((uint64_t)s_hv[B][2] << 28);
-    htab[(uint64_t)c * Db + B] = e;
-  }
-  if (threadIdx.x == 0) hdig[c] = Db + 2 * nh_all;
-}
-
-// Hub-mode level-3 plan, one thread per coarse bucket: walk its segments
-// (level-2 digits) in CSC order.  Hub segments are final: the hub vertex's
-// CSC offset is written here and its list becomes copy jobs (R2 -> t_edges).
-// Non-hub segments pack into units (runs of segments in consecutive fine
-// buckets with no hub between them, <= cap records, <= ML3 local vertices);
-// segments above cap become big buckets restricted to their low-digit range.
-struct HubJob {
-  uint64_t start;
-  uint32_t n;
-  uint32_t pad;
-};
-constexpr uint32_t kHubChunk = 1u << 16;  // records per copy job
-__global__ void k_plan3h(const uint64_t* __restrict__ fbase, const uint64_t* __restrict__ bstart,
-                         const uint64_t* __restrict__ htab, const uint32_t* __restrict__ hdig, uint32_t D1, int bits_b,
-                         int bits_c, uint32_t D2, uint32_t cap, Unit3* __restrict__ units, uint32_t* __restrict__ n_units,
-                         Big3* __restrict__ bigs, uint32_t* __restrict__ n_big, HubJob* __restrict__ jobs,
-                         uint32_t* __restrict__ n_jobs, uint64_t* __restrict__ t_offsets, uint64_t V) {
-  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= D1) return;
-  const uint32_t Db = 1u << bits_b, Cn = 1u << bits_c, nd = hdig[c];
-  const uint32_t maxf = (uint32_t)ML3 >> bits_c;  // fine buckets per unit
-  bool open = false;
-  Unit3 u{};
-  auto flush = [&]() {
-    if (open) units[atomicAdd(n_units, 1u)] = u;
-    open = false;
-  };
-  for (uint32_t B = 0; B < Db; ++B) {
-    const uint64_t e = htab[(uint64_t)c * Db + B];
-    const uint32_t sb = (uint32_t)e & 1023u, nh = (uint32_t)(e >> 10) & 3u;
-    const uint32_t fine = c * Db + B;
-    for (uint32_t k = 0; k <= 2 * nh; ++k) {
-      const uint32_t d = sb + k, gd = c * D2 + d;
-      const uint64_t st = fbase[gd];
-      const uint64_t en = (d + 1 < nd) ? fbase[gd + 1] : bstart[c + 1];
-      const uint64_t sz = en - st;
-      if (k & 1) {  // hub segment: final list
-        const uint32_t h = (uint32_t)(e >> (12 + 8 * (k >> 1))) & 255u;
-        const uint64_t v = ((uint64_t)fine << bits_c) | h;
-        if (v < V) t_offsets[v] = st;
-        for (uint64_t o = 0; o < sz; o += kHubChunk) {
-          HubJob j;
-          j.start = st + o;
-          j.n = (uint32_t)min(sz - o, (uint64_t)kHubChunk);
-          j.pad = 0;
-          jobs[atomicAdd(n_jobs, 1u)] = j;
-        }
-        flush();
-        continue;
-      }
-      const uint32_t i = k >> 1;
-      const uint32_t lo = (i == 0) ? 0u : ((uint32_t)(e >> (12 + 8 * (i - 1))) & 255u) + 1u;
-      const uint32_t hi = (i < nh) ? ((uint32_t)(e >> (12 + 8 * i)) & 255u) : Cn;
-      if (sz > cap) {
-        flush();
-        Big3 bg;
-        bg.start = st;
-        bg.n = sz;
-        bg.f = fine;
-        bg.pad = lo | (hi << 16);
-        bigs[atomicAdd(n_big, 1u)] = bg;
-        continue;
-      }
-      // extend the open unit: a non-hub segment starting the next fine bucket (k == 0)
-      if (open && k == 0 && u.n + sz <= cap && (fine - u.fb0) < maxf) {
-        u.n += (uint32_t)sz;
-        u.nf += 1;
-        u.vhi = ((fine - u.fb0) << bits_c) + hi;
-        continue;
-      }
-      flush();
-      u.start = st;
-      u.n = (uint32_t)sz;
-      u.f0 = gd;
-      u.nf = 1;
-      u.fb0 = fine;
-      u.vlo = lo;
-      u.vhi = hi;
-      open = true;
-    }
-  }
-  flush();
-}
-
-// Hub lists: R2 (workspace, at CSC positions) -> t_edges, source bits only.
-__global__ void k_hub_copy(const HubJob* __restrict__ jobs, const uint32_t* __restrict__ n_jobs,
-                           const uint32_t* __restrict__ r2, uint32_t src_mask, uint32_t* __restrict__ t_edges) {
-  const uint32_t nj = *n_jobs;
-  for (uint32_t q = blockIdx.x; q < nj; q += gridDim.x) {
-    const HubJob j = jobs[q];
-    const uint32_t* src = r2 + j.start;
-    uint32_t* dst = t_edges + j.start;
-    const uint32_t head = min(j.n, (4 - align_items_u32(src)) & 3);  // same alignment on both sides
-    for (uint32_t i = threadIdx.x; i < head; i += blockDim.x) dst[i] = src[i] & src_mask;
-    const uint32_t n4 = (j.n - head) >> 2;
-    const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
-    uint4* d4 = reinterpret_cast<uint4*>(dst + head);
-    for (uint32_t i = threadIdx.x; i < n4; i += blockDim.x) {
-      uint4 v = s4[i];
-      v.x &= src_mask; v.y &= src_mask; v.z &= src_mask; v.w &= src_mask;
-      d4[i] = v;
-    }
-    for (uint32_t i = head + n4 * 4 + threadIdx.x; i < j.n; i += blockDim.x) dst[i] = src[i] & src_mask;
   }
 }
 
