@@ -332,19 +332,20 @@ def main():
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph, stream=s):
                 transpose_device(off_d, edg_d, V, t_offsets=t_off, t_edges=t_edg, stream=s)
-            graph.replay()
+            with torch.cuda.stream(s):
+                graph.replay()
             s.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         sampler.start()
         torch.cuda.synchronize()
-        ev0.record(s)
-        for _ in range(args.steps):
-            if graph is not None:
-                graph.replay()
-            else:
-                with torch.cuda.stream(s):
+        with torch.cuda.stream(s):  # graph replays launch on the current stream
+            ev0.record(s)
+            for _ in range(args.steps):
+                if graph is not None:
+                    graph.replay()
+                else:
                     transpose_device(off_d, edg_d, V, t_offsets=t_off, t_edges=t_edg, stream=s)
-        ev1.record(s)
+            ev1.record(s)
         torch.cuda.synchronize()
         clocks = sampler.stop()
         transpose_status(stream=s)

@@ -59,9 +59,10 @@ def test_cuda_graph_capture_and_replay():
     with torch.cuda.graph(graph, stream=s):
         transpose_device(off, edg, g.num_vertices, t_offsets=t_off, t_edges=t_edg, stream=s)
     for _ in range(3):
-        t_off.fill_(-1)
-        t_edg.fill_(-1)
-        graph.replay()
+        with torch.cuda.stream(s):
+            t_off.fill_(-1)
+            t_edg.fill_(-1)
+            graph.replay()
         torch.cuda.synchronize()
         transpose_status(stream=s)
         _check(t_off, t_edg, g)
