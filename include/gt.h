@@ -190,6 +190,12 @@ int gt_shard_receive(const uint32_t *r1_recv, uint64_t *seg_hi_recv, const uint6
                      uint64_t num_vertices, uint64_t num_edges, uint32_t bucket_lo, uint32_t bucket_hi,
                      uint64_t num_records, uint64_t global_base, uint64_t *t_offsets_local,
                      uint32_t *t_edges_local, void *stream, gt_stats *stats);
+/* Host: library workspace of a sender (level-1 tables for e_count edges) and of
+ * a receiver (num_buckets_local buckets, num_records records from nranks
+ * senders: R2 + tables), for memory planning. */
+int gt_shard_workspace_size(uint64_t num_vertices, uint64_t num_edges, uint64_t e_count,
+                            uint32_t num_buckets_local, int nranks, uint64_t num_records,
+                            uint64_t *send_bytes, uint64_t *recv_bytes);
 /* Host: owners' bucket ranges h_bounds[0..parts] (bucket-aligned, balanced on
  * the bucket totals). */
 int gt_shard_owners(const uint64_t *h_bucket_totals, uint32_t num_buckets, int parts, uint32_t *h_bounds);

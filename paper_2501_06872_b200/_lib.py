@@ -109,6 +109,7 @@ SYMBOLS = {
     "gt_shard_receive": (_int, [_vp, _vp, _vp, _int, _u64, _u64, ctypes.c_uint32, ctypes.c_uint32, _u64, _u64, _vp,
                                 _vp, _vp, _stats_p]),
     "gt_shard_owners": (_int, [_vp, ctypes.c_uint32, _int, _vp]),
+    "gt_shard_workspace_size": (_int, [_u64, _u64, _u64, ctypes.c_uint32, _int, _u64, _u64p, _u64p]),
     "gt_multi_unique_id": (_int, [_vp]),
     "gt_multi_comm_init": (_int, [_vp, _int, _int, ctypes.POINTER(_vp)]),
     "gt_multi_comm_destroy": (_int, [_vp]),

@@ -1259,6 +1259,25 @@ int gt_shard_receive(const uint32_t* r1_recv, uint64_t* seg_hi_recv, const uint6
   return GT_OK;
 }
 
+int gt_shard_workspace_size(uint64_t V, uint64_t E_total, uint64_t e_count, uint32_t num_buckets_local, int nranks,
+                            uint64_t num_records, uint64_t* send_bytes, uint64_t* recv_bytes) {
+  if (!send_bytes || !recv_bytes || nranks < 1) return set_err(GT_EINVAL, "bad arguments");
+  Plan p;
+  int rc = make_plan(V, E_total, V, config_snapshot(), p);
+  if (rc) return rc;
+  Layout qs, qr;
+  Plan ps = p;
+  ps.E = e_count;
+  make_layout(ps, e_count, 0, 1, qs);
+  Plan pr = p;
+  pr.D1 = (int)num_buckets_local;
+  pr.E = num_records;
+  make_layout(pr, 0, num_records, (uint32_t)nranks, qr);
+  *send_bytes = e_count ? qs.total : 0;
+  *recv_bytes = num_records ? qr.total : 0;
+  return GT_OK;
+}
+
 int gt_shard_owners(const uint64_t* h_bucket_totals, uint32_t num_buckets, int parts, uint32_t* h_bounds) {
   if (!h_bucket_totals || !h_bounds || parts < 1) return set_err(GT_EINVAL, "gt_shard_owners: bad arguments");
   uint64_t total = 0;

@@ -50,6 +50,7 @@ __all__ = [
     "transpose_distributed",
     "distributed_step",
     "MultiComm",
+    "memory_plan",
 ]
 
 
@@ -383,3 +384,29 @@ class MultiComm:
         if self.comm:
             _lib.lib.gt_multi_comm_destroy(self.comm)
             self.comm = ctypes.c_void_p()
+
+
+def memory_plan(num_vertices: int, num_edges: int, parts: int, imbalance: float = 1.02) -> dict:
+    """Per-rank device bytes of one sharded step (balanced shards; the receive
+    side scaled by ``imbalance``): inputs (full offsets + the edge slice), the
+    sender's R1 and library workspace, the exchange buffers, the receiver's
+    workspace, and its CSC slice (torch-allocated buffers of multi.py included)."""
+    V, E, P = int(num_vertices), int(num_edges), int(parts)
+    g = shard_geometry(V, E)
+    e_rank = -(-E // P)
+    rec = int(e_rank * imbalance)
+    nloc = -(-int(g.num_buckets) // P)
+    sb, rb = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    _lib.check(_lib.lib.gt_shard_workspace_size(V, E, e_rank, nloc, P, rec, ctypes.byref(sb), ctypes.byref(rb)),
+               "gt_shard_workspace_size")
+    row = int(g.seg_hi_row) * 8
+    plan = {
+        "inputs (offsets + edge slice)": (V + 1) * 8 + e_rank * 4,
+        "sender R1": e_rank * 4,
+        "sender workspace + boundary rows": int(sb.value) + int(g.num_buckets) * row,
+        "receive buffer (R1 runs + rows)": rec * 4 + P * nloc * row,
+        "receiver workspace (R2 + tables)": int(rb.value),
+        "CSC slice (offsets + edges)": (-(-V // P) + 1) * 8 + rec * 4,
+    }
+    plan["total"] = sum(plan.values())
+    return plan

@@ -109,3 +109,15 @@ def test_plan_shards_contract():
     assert p.edge_bounds.tolist() == [0, 20, 20, 30]
     with pytest.raises(ValueError):
         plan_shards(off, 0)
+
+
+def test_c5_memory_plan_fits():
+    """Per-rank device memory of the sharded C5 step (8.6e9 edges): it fits a
+    180 GB B200 from P = 2 on and shrinks ~1/P; at P = 1 the
+    single-GPU path (R1 inside t_edges, no exchange buffers) is the one used."""
+    from paper_2501_06872_b200.multi import memory_plan
+
+    V, E = 1 << 29, 16 << 29
+    tot = {P: memory_plan(V, E, P)["total"] for P in (1, 2, 4, 8)}
+    assert tot[2] < 120e9 and tot[4] < 60e9 and tot[8] < 35e9
+    assert tot[8] < tot[4] < tot[2] < tot[1]
