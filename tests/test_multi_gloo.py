@@ -45,7 +45,7 @@ class CpuShardBackend:
         return torch.from_numpy(rec.view(np.int32)), torch.from_numpy(counts), torch.from_numpy(seg)
 
     def receive(self, r1_recv, seg_recv, counts_all, parts, num_vertices, num_edges, lo, hi, num_records,
-                global_base, geom, want_stats=False):
+                global_base, geom, want_stats=False, check_status=True):
         shift = int(geom.bucket_shift)
         v_lo, v_hi = min(num_vertices, lo << shift), min(num_vertices, hi << shift)
         rec = r1_recv.numpy().view(np.uint32).reshape(-1, 2)
