@@ -240,15 +240,17 @@ def transpose_potra(g, threads: int, budget=None, *, force_method=None, sample_f
     """Signature of the reference's ``transpose_potra`` (hlh.py:441-452) on the GPU.
 
     Argument checks are the reference's (``threads >= 1``, _nb.py:112-113;
-    ``force_method`` in {None, "atomic", "hlh"}, hlh.py:462-463).  Step 0 runs
-    as in the reference (hlh.py:466-475): k from the budget (Eq. 1,
-    ``hdv_count`` + ``fit_table_budget``; default budget = one CTA's shared
-    memory, ``hdv.gpu_budget``) and ``sample_hdv`` on the GPU with the same
+    ``force_method`` in {None, "atomic", "hlh"}, hlh.py:462-463).  The GPU
+    transposition has no degree-dependent branch to choose (hubs take the
+    level-3 big-bucket path by measured size; a sampled hub split at level 2
+    measured slower), so step 0 is not paid on the default path:
+    ``details["method_chosen"] = "gpu"`` and the step-0 fields are None.
+    ``force_method="hlh"`` runs step 0 as the reference does (hlh.py:466-475:
+    k from the budget by Eq. 1, ``sample_hdv`` on the GPU with the same
     ``(sample_fraction, seed, threads)`` — same HDV set and coverage estimate
-    as the reference.  The transposition has no degree-dependent branch (hubs
-    take the level-3 big-bucket path by measured size), so there is no probe:
-    ``details`` reports ``method_chosen="gpu"``, the step-0 results and the GPU
-    accounting.  The output is sorted (``sorted=True``) and equals
+    as the reference) and reports it.  ``debug=True`` runs the reference's
+    debug asserts on the device (write-once slots, degree conservation,
+    hlh.py:400-419, 523-528).  The output is sorted and equals
     ``transpose_oracle(g)``.
     """
     from .hdv import fit_table_budget, gpu_budget, hdv_count, sample_hdv
@@ -258,20 +260,22 @@ def transpose_potra(g, threads: int, budget=None, *, force_method=None, sample_f
     if threads < 1:
         raise ValueError(f"thread count must be >= 1, got {threads}")
     t0 = time.perf_counter()
-    if budget is None:
-        budget = gpu_budget()
-    k = fit_table_budget(hdv_count(budget).k, budget.load_factor, threads, budget.cache_bytes)
-    plan = sample_hdv(g, k, sample_fraction=sample_fraction, seed=seed, threads=threads,
-                      load_factor=budget.load_factor)
+    plan = None
+    if force_method == "hlh":
+        if budget is None:
+            budget = gpu_budget()
+        k = fit_table_budget(hdv_count(budget).k, budget.load_factor, threads, budget.cache_bytes)
+        plan = sample_hdv(g, k, sample_fraction=sample_fraction, seed=seed, threads=threads,
+                          load_factor=budget.load_factor)
     step0 = time.perf_counter() - t0
     out = transpose_gpu(g, debug=debug)
     details = {
         "method_chosen": "gpu",
-        "k": plan.k,
-        "coverage_estimate": plan.coverage_estimate,
-        "sample_size": plan.sample_size,
+        "k": plan.k if plan else None,
+        "coverage_estimate": plan.coverage_estimate if plan else None,
+        "sample_size": plan.sample_size if plan else None,
         "probe": None,
-        "hdv_aux_bytes": plan.aux_bytes(),
+        "hdv_aux_bytes": plan.aux_bytes() if plan else 0,
         "shared_aux_bytes": out.aux_footprint_bytes,
         "partitions": out.details.get("big_buckets", 0),
         "step3_imbalance": None,
@@ -279,8 +283,8 @@ def transpose_potra(g, threads: int, budget=None, *, force_method=None, sample_f
     }
     details.update(out.details)
     return TransposeOutput(graph=out.graph, phase_times={"step0": step0, **out.phase_times},
-                           aux_footprint_bytes=out.aux_footprint_bytes + plan.aux_bytes(), method="potra-gpu",
-                           sorted=True, details=details)
+                           aux_footprint_bytes=out.aux_footprint_bytes + (plan.aux_bytes() if plan else 0),
+                           method="potra-gpu", sorted=True, details=details)
 
 
 def transpose_atomic(g, threads: int, partition_edges: int = 1 << 18) -> TransposeOutput:

@@ -87,7 +87,9 @@ def test_gpu_sample_hdv_errors_and_potra_step0():
         sample_hdv(g, 1, sample_fraction=0.0)
     with pytest.raises(ValueError):
         sample_hdv(g, -1)
-    out = transpose_potra(g, 8, HdvBudget(cache_bytes=1 << 16, threads=8), seed=3)
+    out0 = transpose_potra(g, 8, HdvBudget(cache_bytes=1 << 16, threads=8), seed=3)  # default: no step 0
+    assert out0.details["k"] is None and out0.details["plan"] is None
+    out = transpose_potra(g, 8, HdvBudget(cache_bytes=1 << 16, threads=8), seed=3, force_method="hlh")
     d = out.details
     assert d["method_chosen"] == "gpu" and d["k"] > 0 and d["plan"].hdv_ids[0] == 77
     assert d["sample_size"] == 1000 and 0.2 < d["coverage_estimate"] < 0.45
