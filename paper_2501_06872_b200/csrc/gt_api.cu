@@ -756,7 +756,6 @@ int level23(const Plan& p, const Layout& q, Ws& w, const uint32_t* r1, uint32_t 
     // batched landing loads where fine buckets come from positions (C4 4.40 -> 4.33 ms)
     if (p.wide) rc = go3(k_p3<kMode, true, false, true>);
     else if (pos_fine) rc = go3(k_p3<kMode, true>);
-    else if (p.exp & 4) rc = go3(k_p3<kMode, false, false, false, false, W3, true, true>);  // A/B: match ranking
     else rc = go3(k_p3<kMode, false, false, false, false>);
     if (rc) return rc;
     GT_LAUNCH_CHECK();

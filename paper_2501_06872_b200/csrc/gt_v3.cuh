@@ -1254,7 +1254,7 @@ inline size_t smem_p3(int mode, bool lv = false, int ww = W3) {
 // each, consecutive ranges in warp order) and warps skip their empty slots;
 // otherwise every warp owns 512 positions and partial units run predicated slots.
 template <int kMode, bool kPosFine, bool kProf = false, bool kLv = false, bool kPre = true, int WW3 = W3,
-          bool kBal = true, bool kMatch = false>
+          bool kBal = true>
 __global__ void __launch_bounds__(WW3 * 32, WW3 > 16 ? 1 : 2) k_p3(const P3Args a) {
   // phase profile (kProf builds only; thread 0, clock64): 0 fetch/issue, 1 wait, 2 rank, 3 bases+offsets, 4 stage, 5 store
   unsigned long long pacc[kProf ? 6 : 1] = {};
@@ -1378,10 +1378,7 @@ __global__ void __launch_bounds__(WW3 * 32, WW3 > 16 ? 1 : 2) k_p3(const P3Args 
       } else {
         lv = valid ? (((r >> a.nbs) & a.lvmask) - lvoff) : 0u;
       }
-      if constexpr (kMatch)  // one counter atomic per distinct local vertex of the slot
-        pk[s] = (lv << 16) | rank_match(s_cnt + lv * WH3_ + (w >> 1), sh, lv, valid);
-      else
-        pk[s] = (lv << 16) | rank_pk<kMode>(s_cnt + lv * WH3_ + (w >> 1), s_scr + lv * W3P_ + w, sh, valid);
+      pk[s] = (lv << 16) | rank_pk<kMode>(s_cnt + lv * WH3_ + (w >> 1), s_scr + lv * W3P_ + w, sh, valid);
       rr[s] = r & a.src_mask;
     }
     __syncthreads();  // (B)
