@@ -560,10 +560,7 @@ int level1(const Plan& p, const Layout& q, Ws& w, InCsr in, uint64_t E, bool sen
     return GT_OK;
   };
   switch (form) {
-    case kC16x16:
-      if (p.exp & 8) rc = go(k_p1<kMode, 16, false, 16, 2, true>, 512, smem_p1(D1, kMode, 16, 16));  // A/B: run ranks
-      else rc = go(k_p1<kMode, 16, false, 16>, 512, smem_p1(D1, kMode, 16, 16));
-      break;
+    case kC16x16: rc = go(k_p1<kMode, 16, false, 16>, 512, smem_p1(D1, kMode, 16, 16)); break;
     case kC8x32: rc = go(k_p1<kMode, 32>, T, smem_p1(D1, kMode, 32)); break;
     case kW16x32: rc = go(k_p1<kMode, 32, true, 16, 1>, 512, smem_p1(D1, kMode, 32, 16)); break;
     case kW8x32: rc = go(k_p1<kMode, 32, true>, T, smem_p1(D1, kMode, 32)); break;
@@ -650,11 +647,6 @@ int level23(const Plan& p, const Layout& q, Ws& w, const uint32_t* r1, uint32_t 
     } else if (Db >= 1024) {  // 8192-record tiles (C4 level 2: 5.70 ms vs 5.89 at 4096)
       auto kern = k_p2<kMode, DecR1, 32>;
       const size_t sm = smem_p2(Db, kMode, 32);
-      if ((rc = set_smem(kern, sm))) return rc;
-      kern<<<persistent_grid(kern, T, sm, q.max_t2), T, sm, st>>>(r1, w.tiles2, n_t2, Db, dec, w.base2, w.r2, nullptr, nullptr, nullptr);
-    } else if (p.exp & 16) {  // A/B: run ranks
-      auto kern = k_p2<kMode, DecR1, 16, false, kIoPlain, false, W, 4, true, true>;
-      const size_t sm = smem_p2(Db, kMode, 16);
       if ((rc = set_smem(kern, sm))) return rc;
       kern<<<persistent_grid(kern, T, sm, q.max_t2), T, sm, st>>>(r1, w.tiles2, n_t2, Db, dec, w.base2, w.r2, nullptr, nullptr, nullptr);
     } else {  // 4096-record tiles, 4 CTAs/SM, no batched landing loads (C3 2.11 vs 2.18 ms)

@@ -94,12 +94,6 @@ __device__ __forceinline__ uint32_t ldg_u32(const uint32_t* p) {
   return v;
 }
 
-__device__ __forceinline__ uint32_t lanemask_le_u() {
-  uint32_t m;
-  asm("mov.u32 %0, %%lanemask_le;" : "=r"(m));
-  return m;
-}
-
 // Number of lanes' positions: for lane l, #{j in [0,32) : rel_j <= l}, rel
 // non-decreasing across lanes (a shuffle binary search, 6 rounds).
 __device__ __forceinline__ uint32_t count_le_lane(uint32_t rel, uint32_t lane) {
@@ -240,31 +234,6 @@ __device__ __forceinline__ uint32_t rank_pk(uint32_t* c, uint32_t* sc, uint32_t 
     return ((old >> sh) & 0xffffu) + __popc(peers & lanemask_lt());
   }
 }
-// Run-aggregated rank (kRankAtomic): equal digits in adjacent lanes (CSR lists
-// are sorted, so a dense source's consecutive edges share coarse and fine
-// digits) form one run; the run head adds the run length with one atomic and
-// the others take head's old value + their offset.  Same-address lanes of one
-// atomic become rare, which is what serialises the shared-memory atomic unit.
-// Valid lanes must be a prefix of the warp.  The old-value order of the
-// remaining same-address heads is the lane order of gt_common.cuh.
-__device__ __forceinline__ uint32_t rank_run(uint32_t* c, uint32_t sh, uint32_t d, bool valid) {
-  const uint32_t lane = lane_id();
-  const uint32_t dp = __shfl_up_sync(kFull, d, 1);
-  const uint32_t vm = __ballot_sync(kFull, valid);
-  const bool head = valid && (lane == 0 || d != dp);
-  const uint32_t hm = __ballot_sync(kFull, head);
-  const uint32_t le = hm & lanemask_le_u();
-  const uint32_t st = le ? 31u - __clz(le) : 0u;
-  uint32_t old = 0;
-  if (head) {
-    const uint32_t above = hm & ~lanemask_le_u();
-    const uint32_t nxt = above ? (uint32_t)(__ffs(above) - 1) : (uint32_t)__popc(vm);
-    old = atomicAdd(c, (nxt - lane) << sh);
-  }
-  old = __shfl_sync(kFull, old, st);
-  return ((old >> sh) & 0xffffu) + (lane - st);
-}
-
 // After ranking: tab[d * WHN + k] holds (warp 2k, warp 2k+1) tile positions of
 // their first digit-d item; dtot per digit; delta[d] = gcur[d] - digit start.
 // Epilogue form: epi(d, b, e) per digit with its tile-local start b and end e.
@@ -606,8 +575,7 @@ __device__ __forceinline__ void stage_pair(const uint32_t (&pk)[K_], const uint3
 // array holds the cursor between tiles and the index delta during a tile
 // (delta = cursor - tile start, restored from the digit end after the tile),
 // so the shared-memory footprint matches the 32-bit form.
-template <int kMode, int KK = K, bool kW64 = false, int WW = W, int kMinB = (KK > 16 || kW64 || WW > 8 ? 2 : 4),
-          bool kRun = false>
+template <int kMode, int KK = K, bool kW64 = false, int WW = W, int kMinB = (KK > 16 || kW64 || WW > 8 ? 2 : 4)>
 __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
   constexpr int W1_ = WW, T1_ = WW * 32, WH1_ = WW / 2 + 1, WP1_ = WW + 1;
   // place tiles of PT = W1_ * KK * 32 edges; the offsets window doubles as the
@@ -768,10 +736,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
       }
       if ((n == (uint32_t)PT) ? (s == K - 1 && i == PT - 1) : (valid && i == n - 1)) s_last_src = src;
       const uint32_t d = dst >> a.shift;
-      if constexpr (kRun && kMode == kRankAtomic)
-        pk[s] = (d << 16) | rank_run(s_cnt + d * WH1_ + (w >> 1), sh, d, valid);
-      else
-        pk[s] = (d << 16) | rank_pk<kMode>(s_cnt + d * WH1_ + (w >> 1), s_scr + d * WP1_ + w, sh, valid);
+      pk[s] = (d << 16) | rank_pk<kMode>(s_cnt + d * WH1_ + (w >> 1), s_scr + d * WP1_ + w, sh, valid);
       pay[s] = ((dst & a.low_mask) << a.L) | (src & a.src_mask);
     };
 #pragma unroll
@@ -1019,7 +984,7 @@ __device__ __forceinline__ uint32_t slot_owner32(uint32_t& cur, uint32_t& nb, ui
 // kS64: staged items as (payload, digit) pairs, one 8-byte store / load each (the
 // landing buffer is dead after ranking and the pair array overlays it).
 template <int kMode, class Dec, int KK, bool kProf = false, int kIO = kIoPlain, bool kPre = true, int WW = W,
-          int kMinB = (KK > 16 ? 2 : 4), bool kS64 = (kIO == kIoPlain && KK <= 16), bool kRun = false>
+          int kMinB = (KK > 16 ? 2 : 4), bool kS64 = (kIO == kIoPlain && KK <= 16)>
 __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restrict__ rec, const RTile* __restrict__ tiles,
                                              const uint32_t* __restrict__ n_tiles, int D, Dec dec,
                                              const uint64_t* __restrict__ base, uint32_t* __restrict__ out,
@@ -1171,7 +1136,6 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
         else d = dec.digit(r);
         uint32_t rk;
         if constexpr (Dec::kMatchRank) rk = rank_match(s_cnt + d * WH2_ + (w >> 1), sh, d, valid);
-        else if constexpr (kRun && kMode == kRankAtomic) rk = rank_run(s_cnt + d * WH2_ + (w >> 1), sh, d, valid);
         else rk = rank_pk<kMode>(s_cnt + d * WH2_ + (w >> 1), s_scr + d * WP2_ + w, sh, valid);
         if constexpr (kIO == kIoSplit) {
           pk[s] = (((r >> dec.L) & dec.lvmask) << 24) | (d << 13) | rk;
