@@ -253,3 +253,63 @@ def test_debug_mode_checks(golden_cases):
     if good[hub_start] != good[hub_start + 1]:
         with pytest.raises(AssertionError, match="out of order"):
             _debug_check(off, edg, t_off, torch.from_numpy(bad.view(np.int32)).cuda(), g.num_vertices, torch)
+
+
+@pytest.mark.slow
+def test_c5_one_rank_share_at_p8():
+    """Config C5 (8.6e9 edges) sharded over 8 ranks: all eight senders' level 1
+    on this GPU, then one rank's receiver (its bucket range, runs from every
+    sender) — its CSC slice equals the corresponding slice of the C oracle's
+    full transpose, bit for bit."""
+    import gc
+
+    import torch
+
+    from paper_2501_06872_b200 import gen, release_workspace
+    from paper_2501_06872_b200.multi import GpuShardBackend, plan_shards, shard_geometry, shard_owners
+
+    if os.environ.get("GT_SKIP_FULL") == "1" or os.environ.get("GT_SKIP_C5") == "1":
+        pytest.skip("GT_SKIP_FULL / GT_SKIP_C5")
+    free, total = torch.cuda.mem_get_info()
+    if total < 150 * (1 << 30):
+        pytest.skip("C5 needs a 180 GB-class GPU")
+    cfg = gen.CONFIGS["C5"]
+    V, E, P, r = cfg.num_vertices, cfg.num_edges, 8, 3
+    off_d, edg_d = gen.generate_device(cfg)
+    release_workspace()
+    torch.cuda.empty_cache()
+    off_h = off_d.cpu().numpy().view(np.uint64)
+    plan = plan_shards(off_h, P)
+    geom = shard_geometry(V, E)
+    row = int(geom.seg_hi_row)
+    be = GpuShardBackend()
+    sent = []
+    for s in range(P):
+        e0, e1 = int(plan.edge_bounds[s]), int(plan.edge_bounds[s + 1])
+        sent.append(be.send(off_d, edg_d[e0:e1], V, E, e0, geom))
+    counts_all = torch.stack([x[1] for x in sent]).contiguous()
+    C = counts_all.cpu().numpy()
+    bounds = shard_owners(C.sum(axis=0), P).astype(np.int64)
+    lo, hi = int(bounds[r]), int(bounds[r + 1])
+    recv = torch.cat([x[0][int(C[s, :lo].sum()):int(C[s, :hi].sum())] for s, x in enumerate(sent)])
+    seg = torch.cat([x[2][lo * row:hi * row] for x in sent]).contiguous()
+    del sent
+    gc.collect()
+    torch.cuda.empty_cache()
+    base, nrec = int(C[:, :lo].sum()), int(C[:, lo:hi].sum())
+    assert abs(nrec / (E / P) - 1) < 0.05  # owners balanced on the bucket totals
+    t_off, t_edg, _ = be.receive(recv, seg, counts_all, P, V, E, lo, hi, nrec, base, geom)
+    got_off = t_off.cpu().numpy().view(np.uint64)
+    got_edg = t_edg.cpu().numpy().view(np.uint32)
+    del recv, seg, t_off, t_edg
+    release_workspace()
+    edg_h = edg_d.cpu().numpy().view(np.uint32)
+    del off_d, edg_d
+    torch.cuda.empty_cache()
+    o, e = oracle.transpose_c(off_h, edg_h, V)
+    del edg_h
+    gc.collect()
+    shift = int(geom.bucket_shift)
+    v_lo, v_hi = min(V, lo << shift), min(V, hi << shift)
+    assert np.array_equal(got_off, o[v_lo:v_hi + 1])
+    assert np.array_equal(got_edg, e[base:base + nrec])
