@@ -269,6 +269,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--force-dist", action="store_true", help="use the sharded path even at N=1")
     ap.add_argument("--no-graph", action="store_true", help="time plain launches instead of CUDA-graph replays")
+    ap.add_argument("--no-capi", action="store_true", help="sharded runs: skip the gt_transpose_multi (C ABI) leg")
     ap.add_argument("--experiment", type=int, default=0, help="A/B experiment bits (gt_config.reserved[0]); 0 = product")
     ap.add_argument("--rank-mode", type=int, default=-1, help="-1 auto, 0 smem-atomic, 1 safe OR-mask ranking")
     args = ap.parse_args()
@@ -428,6 +429,41 @@ def main():
                                              "NCCL all-to-all of R1, 4 B/edge)": float(pt[1]),
                                              "receive (levels 2-3)": float(pt[2])},
                 "bytes_on_wire_per_edge": 4}
+        if not args.no_capi:
+            # the same step as one C-ABI call per rank (gt_transpose_multi: NCCL driven from
+            # libgt.so); its slice must equal the torch.distributed orchestration's
+            from paper_2501_06872_b200.multi import MultiComm
+
+            def bcast(b):
+                obj = [b]
+                dist.broadcast_object_list(obj, src=0)
+                return obj[0]
+
+            comm = MultiComm(rank, world, broadcast=bcast)
+            src0, src1 = int(plan.src_bounds[rank]), int(plan.src_bounds[rank + 1])
+            cap = int(1.1 * E / world) + (1 << 20)
+            to_c, te_c, info = comm.transpose(off_d, edg_slice, V, E, src0, src1, capacity=cap)
+            to_p, te_p, _, _ = dstep()
+            same = bool(torch.equal(to_c, to_p) and torch.equal(te_c, te_p))
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0c, e1c = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            nc = max(3, min(args.steps, 10))
+            e0c.record(stream)
+            for _ in range(nc):
+                comm.transpose(off_d, edg_slice, V, E, src0, src1, capacity=cap)
+            e1c.record(stream)
+            torch.cuda.synchronize()
+            tc = torch.tensor([e0c.elapsed_time(e1c) / nc, info.ms_send, info.ms_exchange, info.ms_receive],
+                              device=dev, dtype=torch.float64)
+            dist.all_reduce(tc, op=dist.ReduceOp.MAX)
+            okt = torch.tensor([1 if same else 0], device=dev)
+            dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+            kern["c_abi_gt_transpose_multi"] = {"ms_per_step": float(tc[0]), "send_ms": float(tc[1]),
+                                                "exchange_ms": float(tc[2]), "receive_ms": float(tc[3]),
+                                                "equals_torch_distributed_step": bool(okt.item()),
+                                                "steps": nc}
+            comm.close()
         n_gpus = world
         e2e_dist = None
         if not args.no_e2e:
