@@ -246,6 +246,8 @@ struct WsEntry {
   void* ptr = nullptr;
   uint64_t bytes = 0;
   int* status = nullptr;  // mapped pinned (host pointer == device pointer under UVA)
+  std::mutex call_mu;     // held by a call from its workspace lookup to its last launch: two host
+                          // threads on one stream cannot free each other's buffer before use
 };
 std::mutex g_ws_mu;
 std::map<std::pair<int, cudaStream_t>, WsEntry> g_ws;
@@ -922,6 +924,7 @@ int gt_transpose(const uint64_t* offsets, const uint32_t* edges, uint64_t V, uin
   if (rc) return rc;
   WsEntry* ent;
   if ((rc = ws_entry(dev, st, &ent))) return rc;
+  std::lock_guard<std::mutex> call(ent->call_mu);
   if (E == 0) {
     GT_CUDA(cudaMemsetAsync(t_offsets, 0, (V + 1) * 8, st));
     GT_CUDA(cudaMemsetAsync(ent->status, 0, sizeof(int), st));
@@ -973,12 +976,18 @@ int gt_release_workspace(void) {
   int rc = current_device(&dev);
   if (rc) return rc;
   GT_CUDA(cudaDeviceSynchronize());
-  std::lock_guard<std::mutex> lk(g_ws_mu);
-  for (auto& kv : g_ws) {
-    if (kv.first.first != dev) continue;
-    if (kv.second.ptr) GT_CUDA(cudaFree(kv.second.ptr));
-    kv.second.ptr = nullptr;
-    kv.second.bytes = 0;
+  std::vector<WsEntry*> mine;
+  {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    for (auto& kv : g_ws)
+      if (kv.first.first == dev) mine.push_back(&kv.second);  // entries are never erased
+  }
+  for (WsEntry* e : mine) {  // lock order of the calls: call_mu, then g_ws_mu
+    std::lock_guard<std::mutex> call(e->call_mu);
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    if (e->ptr) GT_CUDA(cudaFree(e->ptr));
+    e->ptr = nullptr;
+    e->bytes = 0;
   }
   return GT_OK;
 }
@@ -1134,6 +1143,9 @@ int gt_prefix_sum(const uint32_t* counts, uint64_t n, uint64_t* out, void* strea
   int rc = current_device(&dev);
   if (rc) return rc;
   const uint64_t tiles = std::max<uint64_t>(1, (n + kScanTile - 1) / kScanTile);
+  WsEntry* ent;
+  if ((rc = ws_entry(dev, st, &ent))) return rc;
+  std::lock_guard<std::mutex> call(ent->call_mu);
   unsigned char* w = nullptr;
   if ((rc = ws_get(dev, st, tiles * 8 + 256, &w, nullptr))) return rc;
   uint64_t* status = reinterpret_cast<uint64_t*>(w);
@@ -1171,6 +1183,9 @@ int gt_shard_send(const uint64_t* offsets, const uint32_t* edges_slice, uint64_t
   ps.E = e_count;
   Layout q;
   make_layout(ps, e_count, 0, 1, q);
+  WsEntry* ent;
+  if ((rc = ws_entry(dev, st, &ent))) return rc;
+  std::lock_guard<std::mutex> call(ent->call_mu);
   unsigned char* ws;
   if ((rc = ws_get(dev, st, q.total, &ws, nullptr))) return rc;
   Ws w = ws_ptrs(q, ws, ps);
@@ -1211,6 +1226,7 @@ int gt_shard_receive(const uint32_t* r1_recv, uint64_t* seg_hi_recv, const uint6
   const uint64_t Vloc = v_hi - v_lo;
   WsEntry* ent;
   if ((rc = ws_entry(dev, st, &ent))) return rc;
+  std::lock_guard<std::mutex> call(ent->call_mu);
   if (num_records == 0 || Vloc == 0) {
     if (num_records) return set_err(GT_EINVAL, "gt_shard_receive: records for an empty destination range");
     GT_CUDA(cudaMemsetAsync(t_offsets_local, 0, (Vloc + 1) * 8, st));
