@@ -570,7 +570,7 @@ int level1(const Plan& p, const Layout& q, Ws& w, InCsr in, uint64_t E, bool sen
   if (rc) return rc;
   GT_LAUNCH_CHECK();
   if ((rc = tm.kend(0))) return rc;
-  *launches += 6;
+  *launches += sender ? 6 : 5;  // tile owners (x2 for a shard), count-tile owners, count, scan, place
   return GT_OK;
 }
 
@@ -660,7 +660,7 @@ int level23(const Plan& p, const Layout& q, Ws& w, const uint32_t* r1, uint32_t 
     GT_LAUNCH_CHECK();
     if ((rc = tm.kend(1))) return rc;
   }
-  *launches += 9;
+  *launches += 7;  // runs plan, tiles, count, scan, set, segfix, place
   if ((rc = tm.mark())) return rc;
   // ---- level 3: units of small fine buckets; tiled count / scan / place for big ones
   k_set_u64<<<1, 1, 0, st>>>(w.fbase + q.nfine, E);
@@ -767,7 +767,7 @@ int level23(const Plan& p, const Layout& q, Ws& w, const uint32_t* r1, uint32_t 
   GT_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
   k_set_u64<<<1, 1, 0, st>>>(t_offsets + V, E);
   GT_LAUNCH_CHECK();
-  *launches += 14;
+  *launches += 11;  // set, plan, big: tiles count / scan / write, count, scan, segfix, place; units; set
   return GT_OK;
 }
 
@@ -839,6 +839,7 @@ int transpose_one(const Plan& p, const Layout& q, unsigned char* ws, InCsr in, u
   if ((rc = tm.mark())) return rc;
   v3::k_runs_from_tbase<<<(p.D1 + 255) / 256, 256, 0, st>>>(w.tbase, q.ntiles1, p.D1, p.E, w.runs);
   GT_LAUNCH_CHECK();
+  *launches += 1;
   if ((rc = level23<kMode>(p, q, w, t_edges, 1, 0, w.seghi, t_offsets, t_edges, st, tm, launches))) return rc;
   if ((rc = tm.mark())) return rc;
   return GT_OK;
