@@ -269,7 +269,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--force-dist", action="store_true", help="use the sharded path even at N=1")
     ap.add_argument("--no-graph", action="store_true", help="time plain launches instead of CUDA-graph replays")
-    ap.add_argument("--no-capi", action="store_true", help="sharded runs: skip the gt_transpose_multi (C ABI) leg")
+    ap.add_argument("--capi", action="store_true",
+                    help="sharded runs: also time the step as one gt_transpose_multi (C ABI, NCCL from libgt.so) call")
     ap.add_argument("--experiment", type=int, default=0, help="A/B experiment bits (gt_config.reserved[0]); 0 = product")
     ap.add_argument("--rank-mode", type=int, default=-1, help="-1 auto, 0 smem-atomic, 1 safe OR-mask ranking")
     args = ap.parse_args()
@@ -429,7 +430,7 @@ def main():
                                              "NCCL all-to-all of R1, 4 B/edge)": float(pt[1]),
                                              "receive (levels 2-3)": float(pt[2])},
                 "bytes_on_wire_per_edge": 4}
-        if not args.no_capi:
+        if args.capi:
             # the same step as one C-ABI call per rank (gt_transpose_multi: NCCL driven from
             # libgt.so); its slice must equal the torch.distributed orchestration's
             from paper_2501_06872_b200.multi import MultiComm
