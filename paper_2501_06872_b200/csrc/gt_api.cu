@@ -155,10 +155,9 @@ int make_plan(uint64_t V, uint64_t E, uint64_t Vsrc, const gt_config& cfg, Plan&
     }
     const int L = 32 - (cb + cc);
     const int nsh = std::max(0, p.nbs - L);
-    if (!(cc >= 1 && cc <= 8 && ca >= 0 && ca <= 11 && cb >= 0 && cb <= 10 && L >= 1 && nsh <= 16))
+    if (!(cc >= 1 && cc <= 8 && ca >= 0 && ca <= 11 && cb >= 0 && cb <= 10 && L >= 1 && nsh <= 18))
       return set_err(GT_EINVAL,
-                     "num_vertices = %llu (%d-bit IDs) with %llu edges has no digit split in this build "
-                     "(destination IDs up to 29 bits are supported)",
+                     "num_vertices = %llu (%d-bit IDs) with %llu edges has no digit split in this build",
                      (unsigned long long)V, p.nb, (unsigned long long)E);
     p.wide = true;
     p.a = ca;
@@ -511,7 +510,10 @@ Ws ws_ptrs(const Layout& q, unsigned char* ws, const Plan& p) {
 // source-high value instead of 0.
 template <int kMode>
 int level1(const Plan& p, const Layout& q, Ws& w, InCsr in, uint64_t E, bool sender, uint32_t* r1, cudaStream_t st,
-           Timer& tm, int* launches) {
+           Timer& tm, int* launches, uint32_t slab_mask = 0, uint32_t slab_val = 0) {
+  // slab_mask != 0: slab mode (num_vertices > 2^29, wide form only): only the
+  // destinations with (dst & slab_mask) == slab_val are partitioned
+  const bool slab = slab_mask != 0;
   using namespace v3;
   const int D1 = p.D1;
   int rc;
@@ -533,7 +535,7 @@ int level1(const Plan& p, const Layout& q, Ws& w, InCsr in, uint64_t E, bool sen
   }
   if ((rc = set_smem(k_c1, (size_t)G1 * D1 * 4))) return rc;
   k_c1<<<(unsigned)((q.ntiles1 + G1 - 1) / G1), 512, (size_t)G1 * D1 * 4, st>>>(in.edges, E, q.ntiles1, D1, p.b + p.c,
-                                                                                w.tcnt);
+                                                                                w.tcnt, slab_mask, slab_val);
   GT_LAUNCH_CHECK();
   if ((rc = scan_u32_to_u64(w.tcnt, (uint64_t)D1 * q.ntiles1, w.tbase, 0, true, w.status, w.ctr, st))) return rc;
   P1Args a;
@@ -554,6 +556,8 @@ int level1(const Plan& p, const Layout& q, Ws& w, InCsr in, uint64_t E, bool sen
   a.nh = (uint32_t)q.nh;
   a.seg_hi = w.seghi;
   a.out = r1;
+  a.slab_mask = slab_mask;
+  a.slab_val = slab_val;
   if ((rc = tm.kbegin(0))) return rc;
   auto go = [&](auto kern, int threads, size_t sm) -> int {
     int r;
@@ -564,9 +568,16 @@ int level1(const Plan& p, const Layout& q, Ws& w, InCsr in, uint64_t E, bool sen
   switch (form) {
     case kC16x16: rc = go(k_p1<kMode, 16, false, 16>, 512, smem_p1(D1, kMode, 16, 16)); break;
     case kC8x32: rc = go(k_p1<kMode, 32>, T, smem_p1(D1, kMode, 32)); break;
-    case kW16x32: rc = go(k_p1<kMode, 32, true, 16, 1>, 512, smem_p1(D1, kMode, 32, 16)); break;
-    case kW8x32: rc = go(k_p1<kMode, 32, true>, T, smem_p1(D1, kMode, 32)); break;
+    case kW16x32:
+      if (slab) rc = go(k_p1<kMode, 32, true, 16, 1, true>, 512, smem_p1(D1, kMode, 32, 16));
+      else rc = go(k_p1<kMode, 32, true, 16, 1>, 512, smem_p1(D1, kMode, 32, 16));
+      break;
+    case kW8x32:
+      if (slab) rc = go(k_p1<kMode, 32, true, W, 2, true>, T, smem_p1(D1, kMode, 32));
+      else rc = go(k_p1<kMode, 32, true>, T, smem_p1(D1, kMode, 32));
+      break;
   }
+  if (slab && !p.wide) return set_err(GT_EINVAL, "slab mode needs the wide form");
   if (rc) return rc;
   GT_LAUNCH_CHECK();
   if ((rc = tm.kend(0))) return rc;
@@ -845,6 +856,71 @@ int transpose_one(const Plan& p, const Layout& q, unsigned char* ws, InCsr in, u
   return GT_OK;
 }
 
+// ---------------------------------------------------------------- slab mode
+// num_vertices > 2^29: the destinations split into slabs of 2^29 IDs; slab s
+// runs level 1 over the whole edge stream keeping only its destinations
+// (k_c1 / k_p1 kSlab), writing R1 into t_edges at the slab's CSC start, then
+// levels 2-3 with the slab's local IDs, offsets rebased.  One host read (the
+// per-slab edge counts) per call.
+constexpr int kSlabBits = 29;
+__global__ void k_fill_u64(uint64_t* a, uint64_t n, uint64_t v) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    a[i] = v;
+}
+
+// Plan and layout every slab uses (the split from the whole edge count, so it
+// does not depend on the slab sizes; tables sized for all E records).
+int slab_plan(uint64_t V, uint64_t E, uint32_t s, const gt_config& cfg, Plan& p, Layout& q) {
+  const uint64_t Vs = std::min<uint64_t>(1ull << kSlabBits, V - ((uint64_t)s << kSlabBits));
+  gt_config c = cfg;
+  c.force_wide = 1;  // 64-bit positions and source-array R2 for 30-32-bit source IDs
+  int rc = make_plan(Vs, E, V, c, p);
+  if (rc) return rc;
+  if (!p.wide) return set_err(GT_EINVAL, "slab mode needs the wide form");
+  make_layout(p, E, E, 1, q);
+  return GT_OK;
+}
+
+template <int kMode>
+int transpose_slabs(uint64_t V, uint64_t E, const gt_config& cfg, unsigned char* ws, InCsr in, uint64_t* t_offsets,
+                    uint32_t* t_edges, const uint64_t* slab_counts, cudaStream_t st, int* launches, Ws* wlast) {
+  const uint32_t S = (uint32_t)((V + (1ull << kSlabBits) - 1) >> kSlabBits);
+  uint64_t before = 0;
+  int rc;
+  Timer tm;
+  tm.init(false, st);
+  for (uint32_t s = 0; s < S; ++s) {
+    Plan p;
+    Layout q;
+    if ((rc = slab_plan(V, E, s, cfg, p, q))) return rc;
+    Ws w = ws_ptrs(q, ws, p);
+    if (s == 0) GT_CUDA(cudaMemsetAsync(w.err, 0, 4, st));
+    *wlast = w;
+    const uint64_t v0 = (uint64_t)s << kSlabBits, Es = slab_counts[s];
+    if (Es == 0) {  // no destination in the slab: every offset is the slab's start
+      k_fill_u64<<<64, 256, 0, st>>>(t_offsets + v0, p.V + 1, before);
+      GT_LAUNCH_CHECK();
+      *launches += 1;
+      continue;
+    }
+    p.E = Es;
+    const uint32_t mask = ~((1u << kSlabBits) - 1u), val = s << kSlabBits;
+    if ((rc = level1<kMode>(p, q, w, in, E, false, t_edges + before, st, tm, launches, mask, val))) return rc;
+    v3::k_runs_from_tbase<<<(p.D1 + 255) / 256, 256, 0, st>>>(w.tbase, q.ntiles1, p.D1, Es, w.runs);
+    GT_LAUNCH_CHECK();
+    if ((rc = level23<kMode>(p, q, w, t_edges + before, 1, 0, w.seghi, t_offsets + v0, t_edges + before, st, tm,
+                             launches)))
+      return rc;
+    if (before) {
+      k_add_base<<<148, 256, 0, st>>>(t_offsets + v0, p.V + 1, before);
+      GT_LAUNCH_CHECK();
+    }
+    *launches += 2;
+    before += Es;
+  }
+  return GT_OK;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------- internal API (gt_multi.cu)
@@ -886,6 +962,18 @@ int gt_workspace_size(uint64_t V, uint64_t E, uint64_t* bytes) {
   if (!bytes) return set_err(GT_EINVAL, "bytes is NULL");
   if (E == 0 || V == 0) {
     *bytes = 0;
+    return GT_OK;
+  }
+  if (bits_for(V) > kSlabBits) {  // slab mode: the largest slab layout
+    uint64_t mx = 0;
+    for (uint32_t s = 0; ((uint64_t)s << kSlabBits) < V; ++s) {
+      Plan p;
+      Layout q;
+      int rc = slab_plan(V, E, s, config_snapshot(), p, q);
+      if (rc) return rc;
+      mx = std::max(mx, q.total);
+    }
+    *bytes = mx;
     return GT_OK;
   }
   Plan p;
@@ -930,6 +1018,50 @@ int gt_transpose(const uint64_t* offsets, const uint32_t* edges, uint64_t V, uin
     GT_CUDA(cudaMemsetAsync(t_offsets, 0, (V + 1) * 8, st));
     GT_CUDA(cudaMemsetAsync(ent->status, 0, sizeof(int), st));
     if (stats) GT_CUDA(cudaStreamSynchronize(st));
+    return GT_OK;
+  }
+  if (bits_for(V) > kSlabBits) {  // num_vertices > 2^29: slab mode
+    const gt_config cfg = config_snapshot();
+    uint64_t need = 0;
+    if ((rc = gt_workspace_size(V, E, &need))) return rc;
+    unsigned char* ws = static_cast<unsigned char*>(workspace);
+    if (!ws) {
+      if ((rc = ws_get(dev, st, need, &ws, nullptr))) return rc;
+    } else if (ws_bytes < need) {
+      return set_err(GT_ENOMEM, "workspace too small: need %llu bytes, got %llu", (unsigned long long)need,
+                     (unsigned long long)ws_bytes);
+    }
+    unsigned long long* d_cnt = nullptr;
+    unsigned long long h_cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    GT_CUDA(cudaMallocAsync(&d_cnt, 64, st));
+    GT_CUDA(cudaMemsetAsync(d_cnt, 0, 64, st));
+    v3::k_slab_hist<<<(unsigned)(num_sms() * 4), 256, 0, st>>>(edges, E, d_cnt);
+    GT_LAUNCH_CHECK();
+    GT_CUDA(cudaMemcpyAsync(h_cnt, d_cnt, 64, cudaMemcpyDeviceToHost, st));
+    GT_CUDA(cudaFreeAsync(d_cnt, st));
+    GT_CUDA(cudaStreamSynchronize(st));  // the per-slab edge counts size the slabs' passes
+    uint64_t cnt[8];
+    for (int i = 0; i < 8; ++i) cnt[i] = h_cnt[i];
+    int mode;
+    if ((rc = rank_mode_for(dev, st, &mode))) return rc;
+    const InCsr in{offsets, edges, 0, V};
+    int launches = 2;
+    Ws w;
+    rc = (mode == kRankAtomic)
+             ? transpose_slabs<kRankAtomic>(V, E, cfg, ws, in, t_offsets, t_edges, cnt, st, &launches, &w)
+             : transpose_slabs<kRankSafe>(V, E, cfg, ws, in, t_offsets, t_edges, cnt, st, &launches, &w);
+    if (rc) return rc;
+    k_status_out<<<1, 1, 0, st>>>(w.err, ent->status);
+    GT_LAUNCH_CHECK();
+    if (stats) {
+      unsigned int h_err = 0;
+      GT_CUDA(cudaMemcpyAsync(&h_err, w.err, 4, cudaMemcpyDeviceToHost, st));
+      GT_CUDA(cudaStreamSynchronize(st));
+      stats->workspace_bytes = need;
+      stats->rank_mode = mode;
+      stats->n_launches = (uint64_t)launches + 1;
+      if (h_err) return set_err(GT_EOVERFLOW, "32-bit degree counter overflowed (a transposed degree >= 2^32)");
+    }
     return GT_OK;
   }
   Plan p;

@@ -387,8 +387,14 @@ __device__ __forceinline__ uint64_t block_excl_scan_u64(uint64_t* a, int n, uint
 // tcnt is digit-major: tcnt[d * ntiles + k] (consecutive tiles of one digit are
 // written together: full 32-byte sectors).
 __global__ void __launch_bounds__(512) k_c1(const uint32_t* __restrict__ edges, uint64_t E, uint64_t ntiles, int D,
-                                            int shift, uint32_t* __restrict__ tcnt) {
+                                            int shift, uint32_t* __restrict__ tcnt, uint32_t slab_mask = 0,
+                                            uint32_t slab_val = 0) {
   extern __shared__ __align__(16) uint32_t s_h[];  // G1 * D
+  // slab mode (num_vertices > 2^29): only destinations with (dst & slab_mask) == slab_val count
+  const uint32_t dm = (uint32_t)D - 1;
+  auto inc = [&](uint32_t i, uint32_t v) {
+    if ((v & slab_mask) == slab_val) smem_inc(&s_h[(i >> CT1_SHIFT) * D + ((v >> shift) & dm)]);
+  };
   const uint64_t k0 = (uint64_t)blockIdx.x * G1;
   const int nt = (int)umin64(G1, ntiles - k0);
   for (int i = threadIdx.x; i < G1 * D; i += blockDim.x) s_h[i] = 0;
@@ -396,7 +402,7 @@ __global__ void __launch_bounds__(512) k_c1(const uint32_t* __restrict__ edges, 
   const uint64_t b = k0 * CT1, n = umin64(E, b + (uint64_t)nt * CT1) - b;
   const uint32_t* p = edges + b;
   const uint32_t head = (uint32_t)umin64(n, (4 - align_items_u32(p)) & 3);
-  for (uint32_t i = threadIdx.x; i < head; i += blockDim.x) smem_inc(&s_h[(i >> CT1_SHIFT) * D + (p[i] >> shift)]);
+  for (uint32_t i = threadIdx.x; i < head; i += blockDim.x) inc(i, p[i]);
   const uint4* p4 = reinterpret_cast<const uint4*>(p + head);
   const uint64_t n4 = (n - head) >> 2;
   for (uint64_t q = threadIdx.x; q < n4; q += blockDim.x) {
@@ -404,18 +410,31 @@ __global__ void __launch_bounds__(512) k_c1(const uint32_t* __restrict__ edges, 
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p4 + q));
     const uint32_t i = head + (uint32_t)q * 4;
-    smem_inc(&s_h[(i >> CT1_SHIFT) * D + (v.x >> shift)]);
-    smem_inc(&s_h[((i + 1) >> CT1_SHIFT) * D + (v.y >> shift)]);
-    smem_inc(&s_h[((i + 2) >> CT1_SHIFT) * D + (v.z >> shift)]);
-    smem_inc(&s_h[((i + 3) >> CT1_SHIFT) * D + (v.w >> shift)]);
+    inc(i, v.x);
+    inc(i + 1, v.y);
+    inc(i + 2, v.z);
+    inc(i + 3, v.w);
   }
-  for (uint64_t i = head + n4 * 4 + threadIdx.x; i < n; i += blockDim.x)
-    smem_inc(&s_h[((uint32_t)i >> CT1_SHIFT) * D + (p[i] >> shift)]);
+  for (uint64_t i = head + n4 * 4 + threadIdx.x; i < n; i += blockDim.x) inc((uint32_t)i, p[i]);
   __syncthreads();
   for (int i = threadIdx.x; i < G1 * D; i += blockDim.x) {
     const int d = i / G1, t = i - d * G1;
     if (t < nt) tcnt[(uint64_t)d * ntiles + k0 + t] = s_h[t * D + d];
   }
+}
+
+// Destinations per slab of 2^29 IDs (slab mode).
+__global__ void k_slab_hist(const uint32_t* __restrict__ edges, uint64_t E, unsigned long long* __restrict__ cnt) {
+  __shared__ unsigned long long s_c[8];
+  if (threadIdx.x < 8) s_c[threadIdx.x] = 0;
+  __syncthreads();
+  unsigned long long local[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < E; i += (uint64_t)gridDim.x * blockDim.x)
+    ++local[edges[i] >> 29];
+  for (int k = 0; k < 8; ++k)
+    if (local[k]) atomicAdd(&s_c[k], local[k]);
+  __syncthreads();
+  if (threadIdx.x < 8 && s_c[threadIdx.x]) atomicAdd(&cnt[threadIdx.x], s_c[threadIdx.x]);
 }
 
 // ------------------------------------------------------------- L1: place
@@ -432,6 +451,7 @@ struct P1Args {
   uint32_t nh;             // source-high values; seg_hi rows have nh + 1 entries
   uint64_t* seg_hi;
   uint32_t* out;           // R1
+  uint32_t slab_mask, slab_val;  // kSlab: records with (dst & slab_mask) == slab_val only
 };
 
 inline size_t smem_p1(int D, int mode, int KK = K, int WW = W) {
@@ -521,7 +541,8 @@ __device__ __forceinline__ void writeout_pair(uint32_t* __restrict__ out, const 
 // them.  lim = valid items of the tile (0xffffffff: all), i0 = position of
 // item 0 (items at i0 + 32 s).
 constexpr int kStageG = 8;
-template <int G, int K_, class Tag>
+// kSkip: items with pk == ~0u (filtered out) are not staged.
+template <int G, int K_, class Tag, bool kSkip = false>
 __device__ __forceinline__ void stage_tag(const uint32_t (&pk)[K_], const uint32_t (&pay)[K_], const uint32_t* cnt,
                                           int whn, uint32_t w, uint32_t sh, uint32_t* buf, Tag* tag, uint32_t lim,
                                           uint32_t i0, uint32_t per = K_ * 32) {
@@ -530,10 +551,12 @@ __device__ __forceinline__ void stage_tag(const uint32_t (&pk)[K_], const uint32
     if ((uint32_t)c * 32 >= per) break;  // per: positions of this warp (slots beyond hold nothing)
     uint32_t bw[G];
 #pragma unroll
-    for (int q = 0; q < G; ++q) bw[q] = cnt[(pk[c + q] >> 16) * whn + (w >> 1)];  // (unused slots: pk = 0)
+    for (int q = 0; q < G; ++q)  // (unused slots: pk = 0)
+      bw[q] = cnt[((kSkip && pk[c + q] == 0xffffffffu) ? 0u : (pk[c + q] >> 16)) * whn + (w >> 1)];
 #pragma unroll
     for (int q = 0; q < G; ++q) {
-      if ((uint32_t)(c + q) * 32 < per && (lim == 0xffffffffu || i0 + (c + q) * 32 < lim)) {
+      if ((uint32_t)(c + q) * 32 < per && (lim == 0xffffffffu || i0 + (c + q) * 32 < lim) &&
+          (!kSkip || pk[c + q] != 0xffffffffu)) {
         const uint32_t pos = ((bw[q] >> sh) & 0xffffu) + (pk[c + q] & 0xffffu);
         buf[pos] = pay[c + q];
         tag[pos] = (Tag)(pk[c + q] >> 16);
@@ -575,7 +598,11 @@ __device__ __forceinline__ void stage_pair(const uint32_t (&pk)[K_], const uint3
 // array holds the cursor between tiles and the index delta during a tile
 // (delta = cursor - tile start, restored from the digit end after the tile),
 // so the shared-memory footprint matches the 32-bit form.
-template <int kMode, int KK = K, bool kW64 = false, int WW = W, int kMinB = (KK > 16 || kW64 || WW > 8 ? 2 : 4)>
+// kSlab (num_vertices > 2^29, slab mode): only records of one 2^29-ID
+// destination slab are ranked, staged and written (the others pass through
+// source recovery only); the digit is taken modulo D.
+template <int kMode, int KK = K, bool kW64 = false, int WW = W, int kMinB = (KK > 16 || kW64 || WW > 8 ? 2 : 4),
+          bool kSlab = false>
 __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
   constexpr int W1_ = WW, T1_ = WW * 32, WH1_ = WW / 2 + 1, WP1_ = WW + 1;
   // place tiles of PT = W1_ * KK * 32 edges; the offsets window doubles as the
@@ -607,6 +634,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
   __shared__ uint32_t s_wn;
   __shared__ uint32_t s_last_src;
   __shared__ uint32_t s_lastm[32];
+  __shared__ uint32_t s_nst;  // kSlab: staged (kept) items of the place tile
 
   const uint32_t tid = threadIdx.x, lane = lane_id(), w = warp_id();
   const uint32_t sh = (w & 1) << 4;
@@ -622,6 +650,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
   zero_u32(s_cnt, round4(D * WH1_) + (kMode == kRankSafe ? round4(D * WP1_) : 0));
   zero_u32(reinterpret_cast<uint32_t*>(s_mark), PT / 2);
   if (tid < 32) s_lastm[tid] = 0;
+  if (tid == 0) s_nst = 0;
   if (tid == 0) {
     mbar_init(&s_bar, 1);
     fence_mbar_init();
@@ -717,6 +746,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
     // pay[s] / pk[s] first hold the slot's destination and mark: all loads of
     // the tile are issued before the first rank atomic (the compiler keeps
     // shared loads behind earlier shared atomics)
+    uint32_t nkeep = 0;  // kSlab: this warp's kept items
     auto slot = [&](int s, bool valid) {
       const uint32_t i = iw + s * 32 + lane;
       const uint32_t dst = valid ? pay[s] : 0u;
@@ -735,8 +765,16 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
         carry = __shfl_sync(kFull, src, 31);
       }
       if ((n == (uint32_t)PT) ? (s == K - 1 && i == PT - 1) : (valid && i == n - 1)) s_last_src = src;
-      const uint32_t d = dst >> a.shift;
-      pk[s] = (d << 16) | rank_pk<kMode>(s_cnt + d * WH1_ + (w >> 1), s_scr + d * WP1_ + w, sh, valid);
+      if constexpr (kSlab) {
+        const bool keep = valid && (dst & a.slab_mask) == a.slab_val;
+        nkeep += __popc(__ballot_sync(kFull, keep));
+        const uint32_t d = (dst >> a.shift) & (uint32_t)(D - 1);
+        const uint32_t rk = rank_pk<kMode>(s_cnt + d * WH1_ + (w >> 1), s_scr + d * WP1_ + w, sh, keep);
+        pk[s] = keep ? ((d << 16) | rk) : 0xffffffffu;
+      } else {
+        const uint32_t d = dst >> a.shift;
+        pk[s] = (d << 16) | rank_pk<kMode>(s_cnt + d * WH1_ + (w >> 1), s_scr + d * WP1_ + w, sh, valid);
+      }
       pay[s] = ((dst & a.low_mask) << a.L) | (src & a.src_mask);
     };
 #pragma unroll
@@ -752,6 +790,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
 #pragma unroll
       for (int s = 0; s < K; ++s) slot(s, iw + s * 32 + lane < n);
     }
+    if (kSlab && lane == 0) atomicAdd(&s_nst, nkeep);
     __syncthreads();  // (B) ranks done; landing buffer and marks consumed
     if constexpr (kW64)
       flat_bases_epi<WH1_>(s_cnt, D, s_tmp, [&](int d, uint32_t b, uint32_t e) {
@@ -769,7 +808,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
 #pragma unroll
       for (int s = 0; s < K; ++s) {
         const uint32_t i = iw + s * 32 + lane;
-        if (i < n && i < q) smem_inc(&s_bh[pk[s] >> 16]);
+        if (i < n && i < q && (!kSlab || pk[s] != 0xffffffffu)) smem_inc(&s_bh[pk[s] >> 16]);
       }
       __syncthreads();
       for (int d = tid; d < D; d += T1_) {
@@ -781,10 +820,12 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
     h_prev = h_last;
     // stage payloads and global indices by digit (base words loaded in groups
     // of kStageG before their stores)
-    stage_tag<kStageG, K>(pk, pay, s_cnt, WH1_, w, sh, s_buf, s_tag, (n == (uint32_t)PT) ? 0xffffffffu : n, iw + lane);
+    stage_tag<kStageG, K, uint16_t, kSlab>(pk, pay, s_cnt, WH1_, w, sh, s_buf, s_tag,
+                                            (n == (uint32_t)PT) ? 0xffffffffu : n, iw + lane);
     __syncthreads();  // (C)
-    if constexpr (kW64) writeout_tag<T1_, PT>(a.out, s_buf, s_tag, s_g64, n);
-    else writeout_tag<T1_, PT>(a.out, s_buf, s_tag, s_delta, n);
+    const uint32_t nout = kSlab ? s_nst : n;  // staged items
+    if constexpr (kW64) writeout_tag<T1_, PT>(a.out, s_buf, s_tag, s_g64, nout);
+    else writeout_tag<T1_, PT>(a.out, s_buf, s_tag, s_delta, nout);
     zero_u32(reinterpret_cast<uint32_t*>(s_mark), PT / 2);
     if (tid < 32) s_lastm[tid] = 0;
     zero_u32(s_cnt, round4(D * WH1_));
@@ -792,6 +833,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
       for (int d = tid; d < D; d += T1_) s_gcur[d] += s_dtot[d];
     fence_proxy_async_smem();
     __syncthreads();  // (D)
+    if (kSlab && tid == 0) s_nst = 0;  // (read above, before (D); incremented again after the next (A))
     if (tid == 0 && j + 1 < nplace) issue(j + 1);
   }
 }
