@@ -533,9 +533,12 @@ int level1(const Plan& p, const Layout& q, Ws& w, InCsr in, uint64_t E, bool sen
     k_tile_src<<<1, 32, 0, st>>>(in, E, CT1, 1, w.prev);
     GT_LAUNCH_CHECK();
   }
-  if ((rc = set_smem(k_c1, (size_t)G1 * D1 * 4))) return rc;
-  k_c1<<<(unsigned)((q.ntiles1 + G1 - 1) / G1), 512, (size_t)G1 * D1 * 4, st>>>(in.edges, E, q.ntiles1, D1, p.b + p.c,
-                                                                                w.tcnt, slab_mask, slab_val);
+  {
+    auto kc = slab ? k_c1<true> : k_c1<false>;
+    if ((rc = set_smem(kc, (size_t)G1 * D1 * 4))) return rc;
+    kc<<<(unsigned)((q.ntiles1 + G1 - 1) / G1), 512, (size_t)G1 * D1 * 4, st>>>(in.edges, E, q.ntiles1, D1, p.b + p.c,
+                                                                               w.tcnt, slab_mask, slab_val);
+  }
   GT_LAUNCH_CHECK();
   if ((rc = scan_u32_to_u64(w.tcnt, (uint64_t)D1 * q.ntiles1, w.tbase, 0, true, w.status, w.ctr, st))) return rc;
   P1Args a;
@@ -881,10 +884,18 @@ int slab_plan(uint64_t V, uint64_t E, uint32_t s, const gt_config& cfg, Plan& p,
   return GT_OK;
 }
 
+__global__ void k_or_flag(const unsigned int* __restrict__ src, unsigned int* __restrict__ dst) {
+  if (*src) *dst = 1u;
+}
+
+// ws: 256 bytes of slab-mode state (the accumulated overflow flag at ws[0]),
+// then the slab layouts (plans differ per slab, so their offsets do too).
 template <int kMode>
 int transpose_slabs(uint64_t V, uint64_t E, const gt_config& cfg, unsigned char* ws, InCsr in, uint64_t* t_offsets,
-                    uint32_t* t_edges, const uint64_t* slab_counts, cudaStream_t st, int* launches, Ws* wlast) {
+                    uint32_t* t_edges, const uint64_t* slab_counts, cudaStream_t st, int* launches) {
   const uint32_t S = (uint32_t)((V + (1ull << kSlabBits) - 1) >> kSlabBits);
+  unsigned int* err_all = reinterpret_cast<unsigned int*>(ws);
+  GT_CUDA(cudaMemsetAsync(err_all, 0, 4, st));
   uint64_t before = 0;
   int rc;
   Timer tm;
@@ -893,9 +904,8 @@ int transpose_slabs(uint64_t V, uint64_t E, const gt_config& cfg, unsigned char*
     Plan p;
     Layout q;
     if ((rc = slab_plan(V, E, s, cfg, p, q))) return rc;
-    Ws w = ws_ptrs(q, ws, p);
-    if (s == 0) GT_CUDA(cudaMemsetAsync(w.err, 0, 4, st));
-    *wlast = w;
+    Ws w = ws_ptrs(q, ws + 256, p);
+    GT_CUDA(cudaMemsetAsync(w.err, 0, 4, st));
     const uint64_t v0 = (uint64_t)s << kSlabBits, Es = slab_counts[s];
     if (Es == 0) {  // no destination in the slab: every offset is the slab's start
       k_fill_u64<<<64, 256, 0, st>>>(t_offsets + v0, p.V + 1, before);
@@ -915,7 +925,9 @@ int transpose_slabs(uint64_t V, uint64_t E, const gt_config& cfg, unsigned char*
       k_add_base<<<148, 256, 0, st>>>(t_offsets + v0, p.V + 1, before);
       GT_LAUNCH_CHECK();
     }
-    *launches += 2;
+    k_or_flag<<<1, 1, 0, st>>>(w.err, err_all);
+    GT_LAUNCH_CHECK();
+    *launches += 3;
     before += Es;
   }
   return GT_OK;
@@ -973,7 +985,7 @@ int gt_workspace_size(uint64_t V, uint64_t E, uint64_t* bytes) {
       if (rc) return rc;
       mx = std::max(mx, q.total);
     }
-    *bytes = mx;
+    *bytes = mx + 256;  // + the slab-mode state
     return GT_OK;
   }
   Plan p;
@@ -1046,16 +1058,15 @@ int gt_transpose(const uint64_t* offsets, const uint32_t* edges, uint64_t V, uin
     if ((rc = rank_mode_for(dev, st, &mode))) return rc;
     const InCsr in{offsets, edges, 0, V};
     int launches = 2;
-    Ws w;
-    rc = (mode == kRankAtomic)
-             ? transpose_slabs<kRankAtomic>(V, E, cfg, ws, in, t_offsets, t_edges, cnt, st, &launches, &w)
-             : transpose_slabs<kRankSafe>(V, E, cfg, ws, in, t_offsets, t_edges, cnt, st, &launches, &w);
+    rc = (mode == kRankAtomic) ? transpose_slabs<kRankAtomic>(V, E, cfg, ws, in, t_offsets, t_edges, cnt, st, &launches)
+                               : transpose_slabs<kRankSafe>(V, E, cfg, ws, in, t_offsets, t_edges, cnt, st, &launches);
     if (rc) return rc;
-    k_status_out<<<1, 1, 0, st>>>(w.err, ent->status);
+    const unsigned int* err_all = reinterpret_cast<const unsigned int*>(ws);
+    k_status_out<<<1, 1, 0, st>>>(err_all, ent->status);
     GT_LAUNCH_CHECK();
     if (stats) {
       unsigned int h_err = 0;
-      GT_CUDA(cudaMemcpyAsync(&h_err, w.err, 4, cudaMemcpyDeviceToHost, st));
+      GT_CUDA(cudaMemcpyAsync(&h_err, err_all, 4, cudaMemcpyDeviceToHost, st));
       GT_CUDA(cudaStreamSynchronize(st));
       stats->workspace_bytes = need;
       stats->rank_mode = mode;

@@ -386,14 +386,19 @@ __device__ __forceinline__ uint64_t block_excl_scan_u64(uint64_t* a, int n, uint
 // Histogram of the coarse digit per count tile (CT1 edges); G1 tiles per CTA.
 // tcnt is digit-major: tcnt[d * ntiles + k] (consecutive tiles of one digit are
 // written together: full 32-byte sectors).
+template <bool kSlab>
 __global__ void __launch_bounds__(512) k_c1(const uint32_t* __restrict__ edges, uint64_t E, uint64_t ntiles, int D,
-                                            int shift, uint32_t* __restrict__ tcnt, uint32_t slab_mask = 0,
-                                            uint32_t slab_val = 0) {
+                                            int shift, uint32_t* __restrict__ tcnt, uint32_t slab_mask,
+                                            uint32_t slab_val) {
   extern __shared__ __align__(16) uint32_t s_h[];  // G1 * D
-  // slab mode (num_vertices > 2^29): only destinations with (dst & slab_mask) == slab_val count
+  // kSlab (num_vertices > 2^29): only destinations with (dst & slab_mask) == slab_val count
   const uint32_t dm = (uint32_t)D - 1;
   auto inc = [&](uint32_t i, uint32_t v) {
-    if ((v & slab_mask) == slab_val) smem_inc(&s_h[(i >> CT1_SHIFT) * D + ((v >> shift) & dm)]);
+    if constexpr (kSlab) {
+      if ((v & slab_mask) == slab_val) smem_inc(&s_h[(i >> CT1_SHIFT) * D + ((v >> shift) & dm)]);
+    } else {
+      smem_inc(&s_h[(i >> CT1_SHIFT) * D + (v >> shift)]);
+    }
   };
   const uint64_t k0 = (uint64_t)blockIdx.x * G1;
   const int nt = (int)umin64(G1, ntiles - k0);
