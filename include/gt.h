@@ -26,10 +26,10 @@
  *
  * Array conventions (graph.py:34-36, 59-80): offsets are uint64[V+1] with
  * offsets[0]=0 and offsets[V]=E; neighbour IDs are uint32[E].  Every neighbour
- * list of the output is ascending by source ID.  Limit of this build: V <=
- * 2^29 (29-bit destination IDs, config C5's width; three partition levels of
- * <= 11 + 10 + 8 bits); larger V returns GT_EINVAL with that limit in
- * gt_last_error().  E may exceed 2^32 (the wide form).
+ * list of the output is ascending by source ID.  V may be anything up to 2^32
+ * (the uint32 ID range): above 2^29 the destinations are processed in slabs of
+ * 2^29 IDs, which costs one host read of the per-slab edge
+ * counts per call.  E may exceed 2^32 (the wide form).
  *
  * Return codes mirror the reference's exceptions:
  *   GT_OK (0); GT_EINVAL (ValueError: bad arguments, _nb.py:112-113);

@@ -143,8 +143,8 @@ def transpose_gpu(g, devices: int = 1, *, device=None, stream=None, debug: bool 
     sort_neighbor_lists, output equal to transpose_oracle(g).
 
     ``devices`` plays the role of the reference's ``threads`` (must be >= 1,
-    _nb.py:112-113).  Vertex IDs up to 29 bits (num_vertices <= 2^29) are
-    supported; larger graphs raise ValueError naming that limit.  ``devices > 1`` needs an initialised torch.distributed
+    _nb.py:112-113).  The whole uint32 ID range is supported (above 2^29
+    vertices the destinations are transposed in 2^29-ID slabs).  ``devices > 1`` needs an initialised torch.distributed
     process group with that many ranks (one process per GPU) and dispatches to
     :func:`paper_2501_06872_b200.multi.transpose_distributed`.  ``debug``
     runs the reference's debug asserts on the device (write-once slots,
