@@ -273,6 +273,8 @@ def main():
                     help="sharded runs: also time the step as one gt_transpose_multi (C ABI, NCCL from libgt.so) call")
     ap.add_argument("--experiment", type=int, default=0, help="A/B experiment bits (gt_config.reserved[0]); 0 = product")
     ap.add_argument("--rank-mode", type=int, default=-1, help="-1 auto, 0 smem-atomic, 1 safe OR-mask ranking")
+    ap.add_argument("--split", default=None, help="experiment: digit split a,b,c (gt_config.split)")
+    ap.add_argument("--force-wide", action="store_true", help="experiment: the wide form (gt_config.force_wide)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3  # timing rule: >= 3 warm-up steps
@@ -301,8 +303,9 @@ def main():
 
     from paper_2501_06872_b200 import _lib, set_config, set_rank_mode, transpose_device
 
-    if args.experiment:
-        set_config(experiment=args.experiment)
+    if args.experiment or args.split or args.force_wide:
+        set_config(split=tuple(int(x) for x in args.split.split(",")) if args.split else None,
+                   force_wide=args.force_wide, experiment=args.experiment)
     if args.rank_mode >= 0:
         set_rank_mode(args.rank_mode)
 
@@ -641,6 +644,8 @@ def main():
                        "l2": f"inputs ({((V + 1) * 8 + E * 4) / 1e9:.2f} GB) larger than L2 (126 MB); no flush",
                        "parallelism": f"sharded{n_gpus}" if dist_on else "single-gpu",
                        **({"experiment": args.experiment} if args.experiment else {}),
+                       **({"split_forced": args.split} if args.split else {}),
+                       **({"force_wide": True} if args.force_wide else {}),
                        **({"rank_mode_forced": args.rank_mode} if args.rank_mode >= 0 else {})},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": agg_peak, "unit": "GB/s",
                          "frac": achieved / agg_peak, "traffic": traffic,
