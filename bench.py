@@ -651,6 +651,7 @@ def main():
                          "frac": achieved / agg_peak, "traffic": traffic,
                          "scope": "whole transpose step (all kernels); algorithmic bytes 24(V+1)+12E per step",
                          "peak_source": peak_src, "algorithmic_bytes_per_step": abytes,
+                         "frac_vs_datasheet_8tbs": achieved / (8000.0 * n_gpus),
                          "dominant_kernel": dominant, "kernels": kern},
             "e2e": e2e,
             "gpu_launches": launches,
