@@ -391,3 +391,26 @@ def test_slab_mode_full_uint32_range():
     _lib.check(_lib.lib.gt_first_diff_u64(ctypes.c_void_p(exp.data_ptr()), ctypes.c_void_p(t_off.data_ptr()), V + 1,
                                           ctypes.byref(first), s), "gt_first_diff_u64")
     assert first.value == V + 1
+
+
+def test_caller_workspace():
+    """A caller-owned workspace of exactly gt_workspace_size bytes gives the same
+    CSC; one byte less is GT_ENOMEM (MemoryError) before any kernel runs."""
+    import torch
+
+    from paper_2501_06872_b200 import _lib
+
+    g = _rand_graph(51, nv=70_001, ne=1_500_000, skew=4.0)
+    off, edg = _dev(torch, g)
+    need = ctypes.c_uint64(0)
+    _lib.check(_lib.lib.gt_workspace_size(g.num_vertices, g.num_edges, ctypes.byref(need)), "gt_workspace_size")
+    ws = torch.empty(int(need.value), dtype=torch.uint8, device="cuda")
+    t_off = torch.empty(g.num_vertices + 1, dtype=torch.int64, device="cuda")
+    t_edg = torch.empty(g.num_edges, dtype=torch.int32, device="cuda")
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    args = [ctypes.c_void_p(off.data_ptr()), ctypes.c_void_p(edg.data_ptr()), g.num_vertices, g.num_edges,
+            ctypes.c_void_p(t_off.data_ptr()), ctypes.c_void_p(t_edg.data_ptr()), ctypes.c_void_p(ws.data_ptr())]
+    assert _lib.lib.gt_transpose(*args, int(need.value), s, None) == 0
+    torch.cuda.synchronize()
+    _check(t_off, t_edg, g)
+    assert _lib.lib.gt_transpose(*args, int(need.value) - 1, s, None) == _lib.GT_ENOMEM
