@@ -578,10 +578,7 @@ int level1(const Plan& p, const Layout& q, Ws& w, InCsr in, uint64_t E, bool sen
     return GT_OK;
   };
   switch (form) {
-    case kC16x16:
-      if (p.exp & 8) rc = go(k_p1<kMode, 16, false, 16, 2, false, true>, 512, smem_p1(D1, kMode, 16, 16));  // A/B
-      else rc = go(k_p1<kMode, 16, false, 16>, 512, smem_p1(D1, kMode, 16, 16));
-      break;
+    case kC16x16: rc = go(k_p1<kMode, 16, false, 16>, 512, smem_p1(D1, kMode, 16, 16)); break;
     case kC8x32: rc = go(k_p1<kMode, 32>, T, smem_p1(D1, kMode, 32)); break;
     case kW16x32:
       if (slab) rc = go(k_p1<kMode, 32, true, 16, 1, true>, 512, smem_p1(D1, kMode, 32, 16));

@@ -607,7 +607,7 @@ __device__ __forceinline__ void stage_pair(const uint32_t (&pk)[K_], const uint3
 // destination slab are ranked, staged and written (the others pass through
 // source recovery only); the digit is taken modulo D.
 template <int kMode, int KK = K, bool kW64 = false, int WW = W, int kMinB = (KK > 16 || kW64 || WW > 8 ? 2 : 4),
-          bool kSlab = false, bool kRun = false>
+          bool kSlab = false>
 __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
   constexpr int W1_ = WW, T1_ = WW * 32, WH1_ = WW / 2 + 1, WP1_ = WW + 1;
   // place tiles of PT = W1_ * KK * 32 edges; the offsets window doubles as the
@@ -776,23 +776,6 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
         const uint32_t d = (dst >> a.shift) & (uint32_t)(D - 1);
         const uint32_t rk = rank_pk<kMode>(s_cnt + d * WH1_ + (w >> 1), s_scr + d * WP1_ + w, sh, keep);
         pk[s] = keep ? ((d << 16) | rk) : 0xffffffffu;
-      } else if constexpr (kRun && kMode == kRankAtomic) {
-        // equal digits of adjacent lanes (a dense source's sorted list) form runs: the run
-        // head adds the run length with one atomic; members keep (head lane, offset) and take
-        // the head's old value after barrier (B), off the atomic's latency path
-        const uint32_t d = dst >> a.shift;
-        const uint32_t dp = __shfl_up_sync(kFull, d, 1);
-        const bool head = valid && (lane == 0 || d != dp);
-        const uint32_t hm = __ballot_sync(kFull, head), vm = __ballot_sync(kFull, valid);
-        const uint32_t lem = hm & le;
-        const uint32_t hl = lem ? 31u - __clz(lem) : lane;
-        uint32_t val = lane - hl;
-        if (head) {
-          const uint32_t above = hm & ~le;
-          const uint32_t len = (above ? (uint32_t)(__ffs(above) - 1) : (uint32_t)__popc(vm)) - lane;
-          val = (atomicAdd(s_cnt + d * WH1_ + (w >> 1), len << sh) >> sh) & 0xffffu;
-        }
-        pk[s] = (d << 21) | (hl << 16) | val;
       } else {
         const uint32_t d = dst >> a.shift;
         pk[s] = (d << 16) | rank_pk<kMode>(s_cnt + d * WH1_ + (w >> 1), s_scr + d * WP1_ + w, sh, valid);
@@ -814,15 +797,6 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
     }
     if (kSlab && lane == 0) atomicAdd(&s_nst, nkeep);
     __syncthreads();  // (B) ranks done; landing buffer and marks consumed
-    if constexpr (kRun && kMode == kRankAtomic && !kSlab) {  // run members: head's old value + offset
-#pragma unroll
-      for (int s = 0; s < K; ++s) {
-        const uint32_t v = pk[s];
-        const uint32_t hl = (v >> 16) & 31u, head_lane_val = v & 0xffffu;
-        const uint32_t base = __shfl_sync(kFull, head_lane_val, hl);
-        pk[s] = ((v >> 21) << 16) | (hl == lane ? head_lane_val : base + head_lane_val);
-      }
-    }
     if constexpr (kW64)
       flat_bases_epi<WH1_>(s_cnt, D, s_tmp, [&](int d, uint32_t b, uint32_t e) {
         s_g64[d] -= b;
