@@ -517,6 +517,7 @@ int level1(const Plan& p, const Layout& q, Ws& w, InCsr in, uint64_t E, bool sen
   using namespace v3;
   const int D1 = p.D1;
   int rc;
+  GT_CUDA(cudaMemsetAsync(w.seghi, 0xff, (uint64_t)D1 * (q.nh + 1) * 8, st));
   // place-tile shape (measured, DESIGN.md §2 table): compact graphs with <= 512
   // coarse digits: 16 warps x K = 16 (8192 edges, 2 CTAs/SM); more digits: 8 x 32;
   // wide graphs: 16 x 32 (16384 edges, 1 CTA/SM) when its tables fit
@@ -524,23 +525,14 @@ int level1(const Plan& p, const Layout& q, Ws& w, InCsr in, uint64_t E, bool sen
   if (!p.wide) form = (D1 <= 512 && smem_p1(D1, kMode, 16, 16) + 64 <= max_smem_optin()) ? kC16x16 : kC8x32;
   else form = (smem_p1(D1, kMode, 32, 16) + 64 <= max_smem_optin()) ? kW16x32 : kW8x32;
   const uint64_t pt1 = (form == kW16x32) ? 16384 : 8192, nplace1 = (E + pt1 - 1) / pt1;
-  // tile owners and the boundary table's reset only feed the place kernel: a side
-  // stream runs them while the count pass streams the edges
-  cudaStream_t sb;
-  cudaEvent_t ev_fork, ev_join;
-  if ((rc = side_stream(&sb, &ev_fork, &ev_join))) return rc;
-  GT_CUDA(cudaEventRecord(ev_fork, st));
-  GT_CUDA(cudaStreamWaitEvent(sb, ev_fork, 0));
-  GT_CUDA(cudaMemsetAsync(w.seghi, 0xff, (uint64_t)D1 * (q.nh + 1) * 8, sb));
-  k_tile_src<<<(unsigned)((nplace1 + 1 + 255) / 256), 256, 0, sb>>>(in, E, pt1, nplace1 + 1, w.psrc);
+  k_tile_src<<<(unsigned)((nplace1 + 1 + 255) / 256), 256, 0, st>>>(in, E, pt1, nplace1 + 1, w.psrc);
   GT_LAUNCH_CHECK();
-  k_prev_src<<<(unsigned)((q.ntiles1 + 255) / 256), 256, 0, sb>>>(in, E, CT1, q.ntiles1, w.prev);
+  k_prev_src<<<(unsigned)((q.ntiles1 + 255) / 256), 256, 0, st>>>(in, E, CT1, q.ntiles1, w.prev);
   GT_LAUNCH_CHECK();
   if (sender) {  // the first count tile's boundaries start after the shard's first source
-    k_tile_src<<<1, 32, 0, sb>>>(in, E, CT1, 1, w.prev);
+    k_tile_src<<<1, 32, 0, st>>>(in, E, CT1, 1, w.prev);
     GT_LAUNCH_CHECK();
   }
-  GT_CUDA(cudaEventRecord(ev_join, sb));
   {
     auto kc = slab ? k_c1<true> : k_c1<false>;
     if ((rc = set_smem(kc, (size_t)G1 * D1 * 4))) return rc;
@@ -549,7 +541,6 @@ int level1(const Plan& p, const Layout& q, Ws& w, InCsr in, uint64_t E, bool sen
   }
   GT_LAUNCH_CHECK();
   if ((rc = scan_u32_to_u64(w.tcnt, (uint64_t)D1 * q.ntiles1, w.tbase, 0, true, w.status, w.ctr, st))) return rc;
-  GT_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
   P1Args a;
   a.offsets = in.offsets;
   a.edges = in.edges;
