@@ -665,11 +665,6 @@ int level23(const Plan& p, const Layout& q, Ws& w, const uint32_t* r1, uint32_t 
       const size_t sm = smem_p2(Db, kMode, 32);
       if ((rc = set_smem(kern, sm))) return rc;
       kern<<<persistent_grid(kern, T, sm, q.max_t2), T, sm, st>>>(r1, w.tiles2, n_t2, Db, dec, w.base2, w.r2, nullptr, nullptr, nullptr);
-    } else if (p.exp & 32) {  // A/B: staging apart from the landing buffer, next tile's load issued at (B)
-      auto kern = k_p2<kMode, DecR1, 16, false, kIoPlain, false, W, 4, false, true>;
-      const size_t sm = smem_p2(Db, kMode, 16, kIoPlain, W, 0, true);
-      if ((rc = set_smem(kern, sm))) return rc;
-      kern<<<persistent_grid(kern, T, sm, q.max_t2), T, sm, st>>>(r1, w.tiles2, n_t2, Db, dec, w.base2, w.r2, nullptr, nullptr, nullptr);
     } else {  // 4096-record tiles, 4 CTAs/SM, no batched landing loads (C3 2.11 vs 2.18 ms)
       auto kern = k_p2<kMode, DecR1, 16, false, kIoPlain, false>;
       const size_t sm = smem_p2(Db, kMode, 16);

@@ -997,11 +997,11 @@ constexpr int kIoLv = 2;     // level 3 big buckets of wide graphs: source + dig
 // Wide forms use 64-bit output positions: the per-digit cursor array holds the
 // cursor between place tiles and the index delta during one (as in k_p1 kW64).
 
-inline size_t smem_p2(int D, int mode, int KK = K, int io = kIoPlain, int WW = W, int s64 = -1, bool early = false) {
+inline size_t smem_p2(int D, int mode, int KK = K, int io = kIoPlain, int WW = W, int s64 = -1) {
   const size_t pt = (size_t)WW * KK * 32;
   const int wh = WW / 2 + 1, wp = WW + 1;
-  if (s64 < 0) s64 = (io == kIoPlain && KK <= 16) && !early;  // measured: C3 level 2 2.115 -> 2.075 ms; 8192-record tiles slower
-  return (s64 ? pt * 8 : (pt + 8) * 4 + pt * 2 + (early ? pt * 4 : 0)) + ((size_t)round4(D * wh) + (mode == kRankSafe ? (size_t)round4(D * wp) : 0)) * 4 + (size_t)D * 4 * 4 +
+  if (s64 < 0) s64 = (io == kIoPlain && KK <= 16);  // measured: C3 level 2 2.115 -> 2.075 ms; 8192-record tiles slower
+  return (s64 ? pt * 8 : (pt + 8) * 4 + pt * 2) + ((size_t)round4(D * wh) + (mode == kRankSafe ? (size_t)round4(D * wp) : 0)) * 4 + (size_t)D * 4 * 4 +
          40 * 4 + (size_t)kMaxBnd * 4 + (io != kIoPlain ? pt + 16 : 0);
 }
 
@@ -1031,7 +1031,7 @@ __device__ __forceinline__ uint32_t slot_owner32(uint32_t& cur, uint32_t& nb, ui
 // kS64: staged items as (payload, digit) pairs, one 8-byte store / load each (the
 // landing buffer is dead after ranking and the pair array overlays it).
 template <int kMode, class Dec, int KK, bool kProf = false, int kIO = kIoPlain, bool kPre = true, int WW = W,
-          int kMinB = (KK > 16 ? 2 : 4), bool kS64 = (kIO == kIoPlain && KK <= 16), bool kEarly = false>
+          int kMinB = (KK > 16 ? 2 : 4), bool kS64 = (kIO == kIoPlain && KK <= 16)>
 __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restrict__ rec, const RTile* __restrict__ tiles,
                                              const uint32_t* __restrict__ n_tiles, int D, Dec dec,
                                              const uint64_t* __restrict__ base, uint32_t* __restrict__ out,
@@ -1056,11 +1056,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
   extern __shared__ __align__(128) unsigned char smem[];
   uint32_t* s_buf = reinterpret_cast<uint32_t*>(smem);                         // PTP (kS64: PT pairs overlay it)
   uint2* s_st64 = reinterpret_cast<uint2*>(smem);                              // kS64: PT staged (payload, digit)
-  // kEarly: staging apart from the landing buffer, so the next tile's TMA load
-  // is issued as soon as ranking has consumed the landing data (barrier (B))
-  static_assert(!(kEarly && (kS64 || kIO != kIoPlain)), "kEarly: plain u32 staging with tags");
-  uint32_t* s_stg = kEarly ? s_buf + PTP : s_buf;                              // PT staged payloads
-  uint16_t* s_tag = reinterpret_cast<uint16_t*>(s_stg + (kEarly ? PT : PTP));   // PT (digit of each staged slot)
+  uint16_t* s_tag = reinterpret_cast<uint16_t*>(s_buf + PTP);                 // PT (digit of each staged slot)
   uint32_t* s_cnt = kS64 ? reinterpret_cast<uint32_t*>(smem + (size_t)PT * 8)
                          : reinterpret_cast<uint32_t*>(s_tag + PT);            // D * WH2_ (packed, digit-major)
   uint32_t* s_scr = s_cnt + round4(D * WH2_);                                    // D * WP2_ (safe)
@@ -1212,7 +1208,6 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
       }
       __syncthreads();  // (B)
       tick(2);
-      if (kEarly && tid == 0 && jj + 1 < nplace) issue(jj + 1);  // the landing buffer is free
       if constexpr (kW64)
         flat_bases_epi<WH2_>(s_cnt, D, s_tmp, [&](int d, uint32_t b, uint32_t e) {
           s_g64[d] -= b;
@@ -1225,7 +1220,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
         stage_pair<kPre ? kStageG : 1, K>(pk, pay, s_cnt, WH2_, w, sh, s_st64, (n == (uint32_t)PT) ? 0xffffffffu : n,
                                           iw + lane, per);
       } else if constexpr (kIO != kIoSplit) {
-        stage_tag<kPre ? kStageG : 1, K>(pk, pay, s_cnt, WH2_, w, sh, s_stg, s_tag, (n == (uint32_t)PT) ? 0xffffffffu : n, iw + lane,
+        stage_tag<kPre ? kStageG : 1, K>(pk, pay, s_cnt, WH2_, w, sh, s_buf, s_tag, (n == (uint32_t)PT) ? 0xffffffffu : n, iw + lane,
                                          per);
       } else {
 #pragma unroll
@@ -1244,7 +1239,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
       if constexpr (kS64) {
         writeout_pair<T2_, PT>(out, s_st64, s_delta, n);
       } else if constexpr (kIO == kIoPlain) {
-        writeout_tag<T2_, PT>(out, s_stg, s_tag, s_delta, n);
+        writeout_tag<T2_, PT>(out, s_buf, s_tag, s_delta, n);
       } else {  // 64-bit positions
         auto put = [&](uint32_t i) {
           const uint64_t q = s_g64[s_tag[i]] + i;
@@ -1264,7 +1259,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
       fence_proxy_async_smem();
       __syncthreads();  // (D)
       tick(5);
-      if (!kEarly && tid == 0 && jj + 1 < nplace) issue(jj + 1);
+      if (tid == 0 && jj + 1 < nplace) issue(jj + 1);
     }
   }
   if constexpr (kProf) {

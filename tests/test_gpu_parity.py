@@ -409,9 +409,8 @@ def test_full_size_c5():
     assert np.array_equal(got_edg, e)
 
 
-@pytest.mark.parametrize("cfg", [{}, {"split": (6, 6, 6)}, {"split": (8, 8, 2)}, {"force_wide": True},
-                                 {"experiment": 32}],
-                         ids=["default", "split-6-6-6", "split-8-8-2", "wide", "exp32"])
+@pytest.mark.parametrize("cfg", [{}, {"split": (6, 6, 6)}, {"split": (8, 8, 2)}, {"force_wide": True}],
+                         ids=["default", "split-6-6-6", "split-8-8-2", "wide"])
 def test_pipeline_configs(golden_cases, cfg):
     """The explicit pipeline configuration (gt_set_config: digit split, wide
     form) stays bit-exact: goldens, random graphs and a hub-heavy graph
