@@ -224,7 +224,7 @@ int gt_transpose_multi(void* comm, int rank, int nranks, const uint64_t* offsets
   static std::mutex s_rmu;
   static std::map<std::pair<int, cudaStream_t>, Buf> s_recv;
   uint32_t* rr1 = nullptr;
-  {
+  if (P > 1) {
     int dev = 0;
     GT_CU(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lk(s_rmu);
@@ -242,6 +242,10 @@ int gt_transpose_multi(void* comm, int rank, int nranks, const uint64_t* offsets
   // every sender's bucket prefix (its R1 offset of bucket c)
   auto prefix = [&](uint64_t s, uint32_t c) { return cnt_range(s, 0, c); };
   GT_CU(cudaEventRecord(ev[2], st));
+  if (P == 1) {  // one rank owns every bucket: receive straight from the send buffers
+    rr1 = r1;
+    rseg = seg;
+  } else {
   GT_NCCL(nc->GroupStart());
   uint64_t roff = 0;
   for (uint64_t q = 0; q < P; ++q) {
@@ -255,6 +259,7 @@ int gt_transpose_multi(void* comm, int rank, int nranks, const uint64_t* offsets
     if (nloc) GT_NCCL(nc->Recv(rseg + q * nloc * row, (uint64_t)nloc * row, ncclUint64, (int)q, cm, st));
   }
   GT_NCCL(nc->GroupEnd());
+  }
   GT_CU(cudaEventRecord(ev[3], st));
   if ((rc = gt_shard_receive(rr1, rseg, all, nranks, V, E, lo, hi, local, gbase, t_offsets_local, t_edges_local, st,
                              nullptr)))

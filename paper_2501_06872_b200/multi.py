@@ -204,6 +204,8 @@ def exchange(r1, seg, counts, geom, rec_words: int = 1, group=None):
     counts_all = torch.stack(allc).contiguous()
     C = counts_all.cpu().numpy()  # the step's one host read: sizes of the sends
     bounds = shard_owners(C.sum(axis=0), P).astype(np.int64)
+    if P == 1:  # one rank owns every bucket: its R1 and rows are already where the receiver reads them
+        return r1, seg, counts_all, C, bounds
     send, recv = _owner_split(C, bounds, r)
     r1_recv = torch.empty(int(recv.sum()) * rec_words, dtype=r1.dtype, device=r1.device)
     _all_to_all(r1_recv, r1, recv * rec_words, send * rec_words, group)
