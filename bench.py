@@ -598,7 +598,7 @@ def main():
             # (copies of consecutive graphs overlapped with the kernels) is reported beside it
             e2e = {"value": E / t_single, "unit": "edges/s", "h2d_bytes_per_step": (V + 1) * 8 + E * 4,
                    "d2h_bytes_per_step": (V + 1) * 8 + E * 4, "ms_per_step": t_single * 1e3, "steps": n1,
-                   "api": "gt_transpose_host (C ABI), one graph per call: pinned H2D, kernels, D2H",
+                   "api": "gt_transpose_host (C ABI), one graph per call, pinned host buffers: source chunks copy in while earlier chunks run level 1; bucket groups copy back while later groups run levels 2-3",
                    "stream_of_graphs": {"value": E / te, "ms_per_step": te * 1e3, "steps": ne2e,
                                         "api": "gt_transpose_host_many (C ABI): a stream of host graphs, pinned "
                                                "host buffers, copy-in / kernels / copy-out overlapped across "

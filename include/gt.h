@@ -104,7 +104,16 @@ int gt_transpose(const uint64_t *offsets, const uint32_t *edges,
                  void *stream, gt_stats *stats);
 
 /* Host-resident CSR -> CSC on `device` (H2D copy, transpose, D2H copy).  Host
- * buffers may be pageable or pinned. */
+ * buffers may be pageable or pinned; pinned buffers make the copies overlap the
+ * kernels.  Compact graphs of >= 2^24 edges take the pipelined call (DESIGN.md
+ * §7b): the edges copy in as P source chunks, each partitioned (level 1) while
+ * the next one copies; after one host read of the P x num_buckets counts,
+ * levels 2-3 run per group of coarse buckets and each group's CSC range copies
+ * back while the next group is computed.  gt_config.reserved[1] / [2] set P /
+ * the group count (0 = by size; reserved[1] < 0 = the serial call).  `stats`
+ * (pipelined call): ms_step1 = copy-in + level 1, ms_step2 = levels 2-3 of the
+ * groups, ms_step3 = the copy-back tail, ms_total = the call on the device,
+ * ms_kernel zero.  Rejects offsets[num_vertices] != num_edges (GT_EINVAL). */
 int gt_transpose_host(const uint64_t *h_offsets, const uint32_t *h_edges,
                       uint64_t num_vertices, uint64_t num_edges,
                       uint64_t *h_t_offsets, uint32_t *h_t_edges,

@@ -21,6 +21,7 @@ from .transpose import (
     transpose_device,
     transpose_gpu,
     transpose_gpu_many,
+    transpose_host,
     transpose_potra,
     transpose_status,
 )
@@ -35,6 +36,7 @@ __all__ = [
     "TransposeOutput",
     "transpose_gpu",
     "transpose_gpu_many",
+    "transpose_host",
     "transpose_potra",
     "transpose_atomic",
     "transpose_device",

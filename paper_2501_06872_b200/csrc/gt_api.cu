@@ -933,6 +933,273 @@ int transpose_slabs(uint64_t V, uint64_t E, const gt_config& cfg, unsigned char*
   return GT_OK;
 }
 
+// ---------------------------------------------------------------- pipelined host call
+// gt_transpose_host for one graph: the PCIe copies are the floor (H2D then D2H,
+// ~41 + 40 ms for C3), so the kernels hide under them.  The edges arrive in P
+// source chunks; chunk s runs level 1 as a sender (the multi-GPU building
+// block) while chunk s+1 is still copying, writing its R1 at its edge offset of
+// one buffer.  After one host read of the P x D1 bucket counts, levels 2-3 run
+// per group of coarse buckets (balanced on records, the multi-GPU owner rule)
+// with one run per (bucket, sender); group g's CSC range is copied back while
+// group g+1 is computed.  Device buffers are cached per device (grow-only).
+struct HostPipe {
+  cudaEvent_t tev[8] = {};  // timing marks: start, copy-in end, level 1 end, group 0 end, groups end, copy-back end
+  std::vector<cudaEvent_t> gev;  // experiment bit 256: per-group compute end / copy-back end
+  void* io = nullptr;  // offsets, t_offsets, edges, t_edges, R1, seg rows, counts, flag, sender workspace
+  uint64_t io_bytes = 0;
+  void* rws = nullptr;  // receiver workspace (levels 2-3 of one group)
+  uint64_t rws_bytes = 0;
+  uint64_t* h_counts = nullptr;  // pinned P x D1
+  uint64_t h_counts_n = 0;
+  cudaStream_t sin = nullptr, scmp = nullptr, sout = nullptr;
+  std::vector<cudaEvent_t> ev;
+};
+
+int pipe_events(HostPipe& hp, size_t n) {
+  while (hp.ev.size() < n) {
+    cudaEvent_t e;
+    GT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    hp.ev.push_back(e);
+  }
+  return GT_OK;
+}
+
+// Source chunks and bucket groups: config override (reserved[1] / reserved[2];
+// reserved[1] < 0: the serial call), else one per 2^26 edges, 2..8 of each;
+// graphs under 2^24 edges, wide or slab plans take the serial call (P = 0).
+void pipe_shape(const Plan& p, uint64_t V, uint64_t E, const gt_config& cfg, int* P, int* G) {
+  *P = *G = 0;
+  if (p.wide || V > (1ull << kSlabBits) || E == 0 || cfg.reserved[1] < 0) return;
+  const bool forced = cfg.reserved[1] > 0 || cfg.reserved[2] > 0;
+  if (!forced && E < (1ull << 24)) return;
+  const int autoN = (int)std::min<uint64_t>(8, std::max<uint64_t>(2, (E + (1ull << 26) - 1) >> 26));
+  *P = cfg.reserved[1] > 0 ? std::min(cfg.reserved[1], 64) : autoN;
+  *G = cfg.reserved[2] > 0 ? std::min(cfg.reserved[2], p.D1) : std::min(autoN, p.D1);
+}
+
+template <int kMode>
+int host_pipeline(HostPipe& hp, const Plan& p, int P, int G, const uint64_t* h_offsets, const uint32_t* h_edges,
+                  uint64_t V, uint64_t E, uint64_t* h_t_offsets, uint32_t* h_t_edges, int* status_out,
+                  gt_stats* stats) {
+  int rc;
+  const int D1 = p.D1;
+  const uint64_t nh = 1ull << p.nsh;
+  // source chunks: vertex-aligned, edge-balanced (_nb.py:118-132)
+  std::vector<int64_t> vb(P + 1);
+  if ((rc = gt_edge_balanced_bounds(h_offsets, V, P, vb.data()))) return rc;
+  std::vector<uint64_t> es(P + 1);
+  for (int s = 0; s <= P; ++s) es[s] = h_offsets[vb[s]];
+  uint64_t max_chunk = 0;
+  for (int s = 0; s < P; ++s) max_chunk = std::max(max_chunk, es[s + 1] - es[s]);
+  Plan ps = p;
+  ps.E = max_chunk;
+  Layout qs;
+  make_layout(ps, max_chunk, 0, 1, qs);
+  // io buffer
+  const uint64_t b_off = align_up((V + 1) * 8, 256), b_e = align_up(E * 4, 256);
+  const uint64_t b_seg = align_up((uint64_t)P * D1 * (nh + 1) * 8, 256), b_cnt = align_up((uint64_t)P * D1 * 8, 256);
+  const uint64_t need = 2 * b_off + 3 * b_e + b_seg + b_cnt + 256 + qs.total;
+  if (hp.io_bytes < need) {
+    if (hp.io) GT_CUDA(cudaFreeAsync(hp.io, hp.scmp));
+    hp.io = nullptr;
+    hp.io_bytes = 0;
+    GT_CUDA(cudaMallocAsync(&hp.io, need, hp.scmp));
+    hp.io_bytes = need;
+  }
+  unsigned char* b = static_cast<unsigned char*>(hp.io);
+  uint64_t* d_off = reinterpret_cast<uint64_t*>(b);
+  uint64_t* d_toff = reinterpret_cast<uint64_t*>(b + b_off);
+  uint32_t* d_e = reinterpret_cast<uint32_t*>(b + 2 * b_off);
+  uint32_t* d_te = reinterpret_cast<uint32_t*>(b + 2 * b_off + b_e);
+  uint32_t* d_r1 = reinterpret_cast<uint32_t*>(b + 2 * b_off + 2 * b_e);
+  uint64_t* seg_all = reinterpret_cast<uint64_t*>(b + 2 * b_off + 3 * b_e);
+  uint64_t* counts = reinterpret_cast<uint64_t*>(b + 2 * b_off + 3 * b_e + b_seg);
+  unsigned int* err = reinterpret_cast<unsigned int*>(b + 2 * b_off + 3 * b_e + b_seg + b_cnt);
+  unsigned char* sws = b + 2 * b_off + 3 * b_e + b_seg + b_cnt + 256;
+  if ((rc = pipe_events(hp, (size_t)P + G))) return rc;
+  if (!hp.tev[0])
+    for (auto& e : hp.tev) GT_CUDA(cudaEventCreate(&e));
+  while ((p.exp & 256) && hp.gev.size() < 2 * (size_t)G) {
+    cudaEvent_t e;
+    GT_CUDA(cudaEventCreate(&e));
+    hp.gev.push_back(e);
+  }
+  GT_CUDA(cudaMemsetAsync(err, 0, 4, hp.scmp));
+  GT_CUDA(cudaEventRecord(hp.ev[0], hp.scmp));  // the buffers are allocated / free of the previous call
+  GT_CUDA(cudaStreamWaitEvent(hp.sin, hp.ev[0], 0));
+  GT_CUDA(cudaEventRecord(hp.tev[0], hp.sin));
+  GT_CUDA(cudaMemcpyAsync(d_off, h_offsets, (V + 1) * 8, cudaMemcpyHostToDevice, hp.sin));
+  Timer tm;
+  tm.init(false, hp.scmp);
+  int launches = 0;
+  for (int s = 0; s < P; ++s) {  // chunk s copies in while chunk s-1 runs level 1
+    const uint64_t n = es[s + 1] - es[s], ea = es[s] & ~1023ull;  // 4 KB-aligned start (same bytes twice)
+    if (n) GT_CUDA(cudaMemcpyAsync(d_e + ea, h_edges + ea, (es[s + 1] - ea) * 4, cudaMemcpyHostToDevice, hp.sin));
+    GT_CUDA(cudaEventRecord(hp.ev[s], hp.sin));
+    GT_CUDA(cudaStreamWaitEvent(hp.scmp, hp.ev[s], 0));
+    uint64_t* seg = seg_all + (uint64_t)s * D1 * (nh + 1);
+    if (n == 0) {
+      GT_CUDA(cudaMemsetAsync(counts + (uint64_t)s * D1, 0, (uint64_t)D1 * 8, hp.scmp));
+      GT_CUDA(cudaMemsetAsync(seg, 0xff, (uint64_t)D1 * (nh + 1) * 8, hp.scmp));
+      continue;
+    }
+    Plan pc = p;
+    pc.E = n;
+    Layout qc;
+    make_layout(pc, n, 0, 1, qc);
+    Ws w = ws_ptrs(qc, sws, pc);
+    w.seghi = seg;
+    const InCsr in{d_off, d_e + es[s], es[s], V};
+    if ((rc = level1<kMode>(pc, qc, w, in, n, true, d_r1 + es[s], hp.scmp, tm, &launches))) return rc;
+    k_sender_meta<<<(D1 + 255) / 256, 256, 0, hp.scmp>>>(w.tbase, qc.ntiles1, D1, n, w.prev, p.L,
+                                                          counts + (uint64_t)s * D1, seg, nh);
+    GT_LAUNCH_CHECK();
+  }
+  GT_CUDA(cudaEventRecord(hp.tev[1], hp.sin));
+  GT_CUDA(cudaEventRecord(hp.tev[2], hp.scmp));
+  // the one host read: bucket counts -> record-balanced groups of buckets
+  const uint64_t ncnt = (uint64_t)P * D1;
+  if (hp.h_counts_n < ncnt) {
+    if (hp.h_counts) GT_CUDA(cudaFreeHost(hp.h_counts));
+    hp.h_counts = nullptr;
+    hp.h_counts_n = 0;
+    GT_CUDA(cudaMallocHost(reinterpret_cast<void**>(&hp.h_counts), ncnt * 8));
+    hp.h_counts_n = ncnt;
+  }
+  GT_CUDA(cudaMemcpyAsync(hp.h_counts, counts, ncnt * 8, cudaMemcpyDeviceToHost, hp.scmp));
+  GT_CUDA(cudaStreamSynchronize(hp.scmp));
+  std::vector<uint64_t> tot(D1, 0), bstart(D1 + 1, 0);
+  for (int s = 0; s < P; ++s)
+    for (int c = 0; c < D1; ++c) tot[c] += hp.h_counts[(uint64_t)s * D1 + c];
+  for (int c = 0; c < D1; ++c) bstart[c + 1] = bstart[c] + tot[c];
+  if (bstart[D1] != E) return set_err(GT_ECUDA, "pipelined transpose: bucket counts sum to %llu, expected %llu",
+                                      (unsigned long long)bstart[D1], (unsigned long long)E);
+  std::vector<uint32_t> gb(G + 1);
+  if ((rc = gt_shard_owners(tot.data(), (uint32_t)D1, G, gb.data()))) return rc;
+  const int shift = p.b + p.c;
+  uint64_t rneed = 0;
+  for (int g = 0; g < G; ++g) {
+    Plan pl = p;
+    pl.D1 = (int)(gb[g + 1] - gb[g]);
+    pl.E = bstart[gb[g + 1]] - bstart[gb[g]];
+    if (!pl.D1 || !pl.E) continue;
+    Layout q;
+    make_layout(pl, 0, pl.E, (uint32_t)P, q);
+    rneed = std::max(rneed, q.total);
+  }
+  if (hp.rws_bytes < rneed) {
+    if (hp.rws) GT_CUDA(cudaFreeAsync(hp.rws, hp.scmp));
+    hp.rws = nullptr;
+    hp.rws_bytes = 0;
+    GT_CUDA(cudaMallocAsync(&hp.rws, rneed, hp.scmp));
+    hp.rws_bytes = rneed;
+  }
+  // group g's CSC range (t_offsets[v_hi] belongs to the next group) back to the host
+  auto copy_back = [&](int g) -> int {
+    const uint32_t lo = gb[g], nloc = gb[g + 1] - gb[g];
+    const uint64_t v_lo = std::min<uint64_t>(V, (uint64_t)lo << shift);
+    const uint64_t v_hi = (g + 1 == G) ? V : std::min<uint64_t>(V, (uint64_t)gb[g + 1] << shift);
+    const uint64_t e0 = bstart[lo], Eg = bstart[lo + nloc] - e0;
+    const uint64_t noff = (v_hi - v_lo) + (g + 1 == G ? 1 : 0);
+    // copies start on 4 KB boundaries (unaligned DMA measured 52 vs 57 GB/s): the
+    // head re-copies final data of group g-1; copies are ordered on sout, so
+    // nothing earlier can overwrite it
+    const uint64_t ea = e0 & ~1023ull, va = v_lo & ~511ull;
+    GT_CUDA(cudaStreamWaitEvent(hp.sout, hp.ev[P + g], 0));
+    if (Eg) GT_CUDA(cudaMemcpyAsync(h_t_edges + ea, d_te + ea, (e0 + Eg - ea) * 4, cudaMemcpyDeviceToHost, hp.sout));
+    if (noff)
+      GT_CUDA(cudaMemcpyAsync(h_t_offsets + va, d_toff + va, (v_lo + noff - va) * 8, cudaMemcpyDeviceToHost, hp.sout));
+    if (p.exp & 256) GT_CUDA(cudaEventRecord(hp.gev[2 * g + 1], hp.sout));
+    return GT_OK;
+  };
+  auto is_pinned = [](const void* ptr) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+  };
+  const bool pinned_out = is_pinned(h_t_edges) && is_pinned(h_t_offsets);
+  // groups: levels 2-3 on the compute stream, each followed by its copy-back
+  for (int g = 0; g < G; ++g) {
+    const uint32_t lo = gb[g], nloc = gb[g + 1] - gb[g];
+    const uint64_t v_lo = std::min<uint64_t>(V, (uint64_t)lo << shift);
+    const uint64_t v_hi = (g + 1 == G) ? V : std::min<uint64_t>(V, (uint64_t)gb[g + 1] << shift);
+    const uint64_t Vloc = v_hi - v_lo, e0 = bstart[lo], Eg = bstart[lo + nloc] - e0;
+    if (Vloc && !Eg) {
+      k_fill_u64<<<64, 256, 0, hp.scmp>>>(d_toff + v_lo, Vloc + 1, e0);
+      GT_LAUNCH_CHECK();
+    } else if (Vloc) {
+      Plan pl = p;
+      pl.D1 = (int)nloc;
+      pl.V = Vloc;
+      pl.E = Eg;
+      Layout q;
+      make_layout(pl, 0, Eg, (uint32_t)P, q);
+      Ws w = ws_ptrs(q, static_cast<unsigned char*>(hp.rws), pl);
+      w.err = err;
+      v3::k_runs_senders<<<(unsigned)((nloc * P + 127) / 128), 128, 0, hp.scmp>>>(counts, (uint32_t)P, (uint32_t)D1, lo,
+                                                                               nloc, w.runs, seg_all, (uint32_t)nh);
+      GT_LAUNCH_CHECK();
+      if ((rc = level23<kMode>(pl, q, w, d_r1, (uint32_t)P, (uint32_t)D1, seg_all + (uint64_t)lo * (nh + 1),
+                               d_toff + v_lo, d_te + e0, hp.scmp, tm, &launches)))
+        return rc;
+      if (e0) {
+        k_add_base<<<148, 256, 0, hp.scmp>>>(d_toff + v_lo, Vloc + 1, e0);
+        GT_LAUNCH_CHECK();
+      }
+    }
+    GT_CUDA(cudaEventRecord(hp.ev[P + g], hp.scmp));
+    if (g == 0) GT_CUDA(cudaEventRecord(hp.tev[3], hp.scmp));
+    if (p.exp & 256) GT_CUDA(cudaEventRecord(hp.gev[2 * g], hp.scmp));
+    if (pinned_out && (rc = copy_back(g))) return rc;
+  }
+  GT_CUDA(cudaEventRecord(hp.tev[4], hp.scmp));
+  int dev = 0;
+  GT_CUDA(cudaGetDevice(&dev));
+  WsEntry* ent;
+  if ((rc = ws_entry(dev, hp.scmp, &ent))) return rc;
+  k_status_out<<<1, 1, 0, hp.scmp>>>(err, ent->status);
+  GT_LAUNCH_CHECK();
+  // pageable host buffers make the copies synchronous: enqueue them after every
+  // compute launch so that they do not hold back the kernels
+  if (!pinned_out)
+    for (int g = 0; g < G; ++g)
+      if ((rc = copy_back(g))) return rc;
+  GT_CUDA(cudaEventRecord(hp.tev[5], hp.sout));
+  GT_CUDA(cudaStreamSynchronize(hp.sout));
+  GT_CUDA(cudaStreamSynchronize(hp.scmp));
+  *status_out = *reinterpret_cast<volatile int*>(ent->status);
+  float t[6] = {};
+  for (int k = 1; k < 6; ++k) GT_CUDA(cudaEventElapsedTime(&t[k], hp.tev[0], hp.tev[k]));
+  if (stats) {
+    std::memset(stats, 0, sizeof(*stats));
+    stats->ms_total = t[5];
+    stats->ms_step1 = t[2];
+    stats->ms_step2 = t[4] - t[2];
+    stats->ms_step3 = t[5] - t[4];
+    stats->workspace_bytes = hp.io_bytes + hp.rws_bytes;
+    stats->bits[0] = p.a;
+    stats->bits[1] = p.b;
+    stats->bits[2] = p.c;
+    stats->rank_mode = kMode;
+    stats->n_launches = (uint64_t)launches + 1;
+  }
+  if (p.exp & 256)
+    std::fprintf(stderr, "host pipeline P=%d G=%d: copy-in end %.2f, level 1 end %.2f, group 0 end %.2f, groups end %.2f, copy-back end %.2f ms\n",
+                 P, G, t[1], t[2], t[3], t[4], t[5]);
+  if (p.exp & 256) {
+    for (int g = 0; g < G; ++g) {
+      float a = 0, c = 0;
+      GT_CUDA(cudaEventElapsedTime(&a, hp.tev[0], hp.gev[2 * g]));
+      GT_CUDA(cudaEventElapsedTime(&c, hp.tev[0], hp.gev[2 * g + 1]));
+      std::fprintf(stderr, "  group %d: computed %.2f, copied back %.2f ms\n", g, a, c);
+    }
+  }
+  return GT_OK;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------- internal API (gt_multi.cu)
@@ -1145,6 +1412,39 @@ int gt_transpose_host(const uint64_t* h_offsets, const uint32_t* h_edges, uint64
   if (e != cudaSuccess || n == 0) return set_err(GT_ENODEV, "no CUDA device");
   if (device < 0 || device >= n || device >= 64) return set_err(GT_EINVAL, "bad device %d", device);
   GT_CUDA(cudaSetDevice(device));
+  if (h_offsets[V] != E)
+    return set_err(GT_EINVAL, "offsets[num_vertices] = %llu != num_edges = %llu", (unsigned long long)h_offsets[V],
+                   (unsigned long long)E);
+  {  // large compact graphs: the pipelined call (copies overlap the kernels)
+    const gt_config cfg = config_snapshot();
+    Plan p;
+    int P = 0, G = 0;
+    if (make_plan(V, E, V, cfg, p) == GT_OK) pipe_shape(p, V, E, cfg, &P, &G);
+    if (P) {
+      static HostPipe s_pipe[64];
+      static std::mutex s_pipe_mu;
+      std::lock_guard<std::mutex> lk(s_pipe_mu);
+      HostPipe& hp = s_pipe[device];
+      if (!hp.scmp) {
+        GT_CUDA(cudaStreamCreateWithFlags(&hp.sin, cudaStreamNonBlocking));
+        GT_CUDA(cudaStreamCreateWithFlags(&hp.scmp, cudaStreamNonBlocking));
+        GT_CUDA(cudaStreamCreateWithFlags(&hp.sout, cudaStreamNonBlocking));
+      }
+      int mode, rc, status = GT_OK;
+      if ((rc = rank_mode_for(device, hp.scmp, &mode))) return rc;
+      rc = (mode == kRankAtomic)
+               ? host_pipeline<kRankAtomic>(hp, p, P, G, h_offsets, h_edges, V, E, h_t_offsets, h_t_edges, &status, stats)
+               : host_pipeline<kRankSafe>(hp, p, P, G, h_offsets, h_edges, V, E, h_t_offsets, h_t_edges, &status, stats);
+      if (rc) {
+        cudaStreamSynchronize(hp.sin);
+        cudaStreamSynchronize(hp.scmp);
+        cudaStreamSynchronize(hp.sout);
+        return rc;
+      }
+      if (status) return set_err(status, "32-bit degree counter overflowed (a transposed degree >= 2^32)");
+      return GT_OK;
+    }
+  }
   // device copies of input and output live in a per-device cache (grow-only),
   // like the workspace: repeated calls do not re-map gigabytes of memory
   static WsEntry s_io[64];

@@ -1606,6 +1606,34 @@ __global__ void k_recv_runs(const uint64_t* __restrict__ counts, uint32_t P, uin
   }
 }
 
+// Pipelined host entry point (gt_transpose_host): P source chunks of one
+// graph ran level 1 as senders, sender s writing its R1 at its edge offset
+// e_s of one buffer and its seg_hi rows at rows s * D1 + c.  Runs of the
+// buckets [lo, lo + nloc) and their rows rebased to buffer positions
+// (sender-local position v -> v + e_s; boundaries at or below the sender's
+// first source-high value -> the run start).  One thread per (c, s) run;
+// each row belongs to exactly one bucket range, so it is rebased once.
+__global__ void k_runs_senders(const uint64_t* __restrict__ counts, uint32_t P, uint32_t D1, uint32_t lo, uint32_t nloc,
+                               Run* __restrict__ runs, uint64_t* __restrict__ seg_all, uint32_t nh) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P * nloc) return;
+  const uint32_t c = i / P, s = i - c * P;
+  uint64_t es = 0;  // sender s's edge offset = records of the senders before it
+  for (uint32_t q = 0; q < s; ++q)
+    for (uint32_t k = 0; k < D1; ++k) es += counts[(uint64_t)q * D1 + k];
+  uint64_t sstart = 0;  // the bucket's start in sender s's R1
+  for (uint32_t k = 0; k < lo + c; ++k) sstart += counts[(uint64_t)s * D1 + k];
+  const uint64_t start = es + sstart;
+  runs[i] = Run{start, counts[(uint64_t)s * D1 + lo + c]};
+  uint64_t* row = seg_all + ((uint64_t)s * D1 + lo + c) * (nh + 1);
+  const uint64_t hb = row[0];
+  for (uint32_t h = 1; h <= nh; ++h) {
+    const uint64_t v = row[h];
+    if (h <= hb) row[h] = start;
+    else if (v != ~0ull) row[h] = v + es;
+  }
+}
+
 // L3 plan: one thread per aligned group of G = ML3 >> c fine buckets.  Small
 // fine buckets are packed into units (<= CAP3 records, one group); fine buckets
 // above CAP3 become big buckets.  fbase[f] = CSC start of fine bucket f,

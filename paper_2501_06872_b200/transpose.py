@@ -30,6 +30,7 @@ __all__ = [
     "TransposeOutput",
     "transpose_gpu",
     "transpose_gpu_many",
+    "transpose_host",
     "transpose_potra",
     "transpose_atomic",
     "transpose_device",
@@ -235,6 +236,31 @@ def transpose_gpu_many(graphs, device: int = 0) -> list:
             for g, to, te in zip(graphs, t_offs, t_edgs)]
 
 
+def transpose_host(g, device: int = 0, out=None) -> TransposeOutput:
+    """Transpose one host graph through ``gt_transpose_host`` (the drop-in C-ABI
+    call): large graphs take the pipelined call, whose source chunks run level
+    1 while later chunks still copy in and whose bucket groups copy back while
+    later groups are computed (pinned host arrays make the copies asynchronous;
+    pageable ones still give correct results).  ``out`` = optional
+    ``(t_offsets, t_edges)`` host arrays to fill (e.g. pinned)."""
+    if g.edges.dtype != np.uint32 or g.offsets.dtype != np.uint64:
+        raise ValueError("graphs need uint64 offsets and uint32 neighbour IDs")
+    _lib.load()
+    off = np.ascontiguousarray(g.offsets)
+    edg = np.ascontiguousarray(g.edges)
+    if out is None:
+        out = (np.empty(int(g.num_vertices) + 1, np.uint64), np.empty(int(g.num_edges), np.uint32))
+    to, te = out
+    t0 = time.perf_counter()
+    rc = _lib.lib.gt_transpose_host(off.ctypes.data_as(ctypes.c_void_p), edg.ctypes.data_as(ctypes.c_void_p),
+                                    int(g.num_vertices), int(g.num_edges), to.ctypes.data_as(ctypes.c_void_p),
+                                    te.ctypes.data_as(ctypes.c_void_p), int(device), None)
+    _lib.check(rc, "gt_transpose_host")
+    return TransposeOutput(graph=type(g)(int(g.num_vertices), int(g.num_edges), to, te, flip_orientation(g.orientation)),
+                           phase_times={"host_call": time.perf_counter() - t0}, aux_footprint_bytes=0,
+                           method="gpu", sorted=True, details={"devices": 1})
+
+
 def transpose_potra(g, threads: int, budget=None, *, force_method=None, sample_fraction: float = 0.01,
                     probe_edges=None, seed: int = 0, partition_edges: int = 1 << 18,
                     debug: bool = False) -> TransposeOutput:
@@ -355,13 +381,19 @@ def transpose_status(stream=None, device=None) -> None:
         _lib.check(st.value, "gt_transpose")
 
 
-def set_config(split=None, force_wide: bool = False, experiment: int = 0) -> None:
+def set_config(split=None, force_wide: bool = False, experiment: int = 0, host_chunks: int = 0,
+               host_groups: int = 0) -> None:
     """Explicit pipeline configuration (gt_set_config): ``split`` = (a, b, c)
     digit bits (used when they cover the destination ID bits), ``force_wide``
     = the 64-bit-position form, ``experiment`` = A/B bits for measurements
-    (0 = the product path).  ``set_config()`` restores the defaults."""
+    (0 = the product path), ``host_chunks`` / ``host_groups`` = the
+    source chunks and bucket groups of the pipelined ``gt_transpose_host``
+    (0 = by size; either set forces the pipelined call on small graphs).
+    ``set_config()`` restores the defaults."""
     cfg = _lib.GtConfig()
     cfg.reserved[0] = int(experiment)
+    cfg.reserved[1] = int(host_chunks)
+    cfg.reserved[2] = int(host_groups)
     if split is not None:
         for i, x in enumerate(split):
             cfg.split[i] = int(x)
@@ -372,11 +404,13 @@ def set_config(split=None, force_wide: bool = False, experiment: int = 0) -> Non
 class pipeline_config:
     """Context manager form of :func:`set_config` (restores the defaults)."""
 
-    def __init__(self, split=None, force_wide: bool = False, experiment: int = 0):
+    def __init__(self, split=None, force_wide: bool = False, experiment: int = 0, host_chunks: int = 0,
+                 host_groups: int = 0):
         self.split, self.force_wide, self.experiment = split, force_wide, experiment
+        self.host_chunks, self.host_groups = host_chunks, host_groups
 
     def __enter__(self):
-        set_config(self.split, self.force_wide, self.experiment)
+        set_config(self.split, self.force_wide, self.experiment, self.host_chunks, self.host_groups)
         return self
 
     def __exit__(self, *exc):

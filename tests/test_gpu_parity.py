@@ -205,6 +205,89 @@ def test_host_batch_entry_point():
     assert transpose_gpu_many([]) == []
 
 
+def _host_pipeline_cases():
+    from paper_2501_06872_b200 import CsrGraph
+
+    rng = np.random.default_rng(23)
+    cases = [("random", random_graph(rng, max_vertices=20_000, max_edges=300_000))]
+    nv = 70_001  # not a multiple of the coarse bucket width
+    src = np.sort(rng.integers(0, nv, 900_000))
+    dst = np.where(rng.random(src.size) < 0.3, 4242, np.minimum((nv * rng.random(src.size) ** 4).astype(np.int64), nv - 1))
+    cases.append(("hub", CsrGraph.from_edge_pairs(src, dst, nv)))
+    # one source holds almost every edge: the other source chunks are empty
+    src = np.concatenate([np.full(200_000, 5), rng.integers(0, 3000, 50)])
+    cases.append(("star", CsrGraph.from_edge_pairs(src, rng.integers(0, 3000, src.size), 3000)))
+    # destinations only in the first and last coarse buckets: empty bucket groups
+    dst = np.where(rng.random(100_000) < 0.5, rng.integers(0, 50, 100_000), rng.integers(99_900, 100_000, 100_000))
+    cases.append(("two-ends", CsrGraph.from_edge_pairs(rng.integers(0, 100_000, 100_000), dst, 100_000)))
+    return cases
+
+
+@pytest.mark.parametrize("chunks,groups", [(1, 1), (2, 3), (3, 8), (8, 2), (5, 64)])
+def test_host_pipeline(chunks, groups):
+    """The pipelined gt_transpose_host (source chunks run level 1 as senders
+    while later chunks copy in; bucket groups copy back while later groups
+    run levels 2-3), forced on small graphs through gt_config; pageable and
+    pinned host buffers; every result equals the oracle."""
+    import torch
+
+    from paper_2501_06872_b200 import pipeline_config, transpose_host
+
+    for name, g in _host_pipeline_cases():
+        o, e = oracle.transpose_c(g.offsets, g.edges, g.num_vertices)
+        with pipeline_config(host_chunks=chunks, host_groups=groups):
+            out = transpose_host(g)
+            assert np.array_equal(out.graph.offsets, o) and np.array_equal(out.graph.edges, e), name
+            pin_o = torch.empty(g.num_vertices + 1, dtype=torch.int64).pin_memory()
+            pin_e = torch.empty(max(g.num_edges, 1), dtype=torch.int32).pin_memory()
+            to = pin_o.numpy().view(np.uint64)
+            te = pin_e.numpy().view(np.uint32)[: g.num_edges]
+            transpose_host(g, out=(to, te))
+            assert np.array_equal(to, o) and np.array_equal(te, e), name
+
+
+def test_host_pipeline_default_size():
+    """A graph above the pipelined call's size threshold (2^24 edges) takes it
+    by default (2 source chunks, 2 bucket groups) and equals the oracle, with
+    and without stats; the serial call (host_chunks = -1) gives the same."""
+    from paper_2501_06872_b200 import CsrGraph, _lib, pipeline_config, transpose_host
+
+    rng = np.random.default_rng(29)
+    nv, ne = 3_000_000, (1 << 24) + (1 << 25) + 12345
+    src = rng.integers(0, nv, ne)
+    dst = np.minimum((nv * rng.random(ne) ** 2).astype(np.int64), nv - 1)
+    g = CsrGraph.from_edge_pairs(src, dst, nv)
+    del src, dst
+    o, e = oracle.transpose_c(g.offsets, g.edges, g.num_vertices)
+    out = transpose_host(g)
+    assert np.array_equal(out.graph.offsets, o) and np.array_equal(out.graph.edges, e)
+    toff = np.empty(nv + 1, np.uint64)
+    tedg = np.empty(ne, np.uint32)
+    st = _lib.GtStats()
+    rc = _lib.lib.gt_transpose_host(g.offsets.ctypes.data_as(ctypes.c_void_p), g.edges.ctypes.data_as(ctypes.c_void_p),
+                                    nv, ne, toff.ctypes.data_as(ctypes.c_void_p), tedg.ctypes.data_as(ctypes.c_void_p),
+                                    0, ctypes.byref(st))
+    _lib.check(rc, "gt_transpose_host")
+    assert st.n_launches > 0 and st.ms_total > 0
+    assert np.array_equal(toff, o) and np.array_equal(tedg, e)
+    with pipeline_config(host_chunks=-1):
+        out = transpose_host(g)
+    assert np.array_equal(out.graph.offsets, o) and np.array_equal(out.graph.edges, e)
+
+
+def test_host_offsets_mismatch():
+    """gt_transpose_host rejects offsets[V] != num_edges before any copy."""
+    from paper_2501_06872_b200 import _lib
+
+    off = np.array([0, 2, 3], np.uint64)
+    edg = np.array([1, 0, 0, 1], np.uint32)
+    toff = np.empty(3, np.uint64)
+    tedg = np.empty(4, np.uint32)
+    rc = _lib.lib.gt_transpose_host(off.ctypes.data_as(ctypes.c_void_p), edg.ctypes.data_as(ctypes.c_void_p), 2, 4,
+                                    toff.ctypes.data_as(ctypes.c_void_p), tedg.ctypes.data_as(ctypes.c_void_p), 0, None)
+    assert rc == -1  # GT_EINVAL
+
+
 @pytest.mark.parametrize("parts", [1, 2, 3, 8])
 def test_shard_pipeline_single_gpu(parts):
     """The multi-GPU building blocks, run for every rank on one GPU in sequence
