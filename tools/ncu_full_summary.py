@@ -5,11 +5,18 @@ import csv
 import sys
 
 
+SCALE = {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0, "nsecond": 1e-6, "s": 1e3, "second": 1e3,
+         "byte": 1e-9, "Kbyte": 1e-6, "Mbyte": 1e-3, "Gbyte": 1.0, "Tbyte": 1e3}
+UNITS = {}
+
+
 def f(d, k):
+    """Value of metric k in ms (times) / GB (bytes) / as exported (others)."""
     try:
-        return float(str(d.get(k, "nan")).replace(",", ""))
+        x = float(str(d.get(k, "nan")).replace(",", ""))
     except ValueError:
         return float("nan")
+    return x * SCALE.get(UNITS.get(k, ""), 1.0)
 
 
 print("kernel | ms | DRAM GB/s | DRAM GB (R+W) | L2 hit % | L1TEX/smem lsu wavefronts % | smem wavefronts/SM-cycle | "
@@ -17,6 +24,8 @@ print("kernel | ms | DRAM GB/s | DRAM GB (R+W) | L2 hit % | L1TEX/smem lsu wavef
 for path in sys.argv[1:]:
     rows = list(csv.reader(open(path)))
     h, v = rows[0], rows[2]
+    UNITS.clear()
+    UNITS.update(zip(h, rows[1]))
     d = dict(zip(h, v))
     ms = f(d, "gpu__time_duration.sum")  # ms in the raw page
     gb = (f(d, "dram__bytes_read.sum") + f(d, "dram__bytes_write.sum"))
