@@ -569,7 +569,11 @@ int level1(const Plan& p, const Layout& q, Ws& w, InCsr in, uint64_t E, bool sen
     return GT_OK;
   };
   switch (form) {
-    case kC16x16: rc = go(k_p1<kMode, 16, false, 16>, 512, smem_p1(D1, kMode, 16, 16)); break;
+    case kC16x16:
+      if (p.exp & 64) rc = go(k_p1<kMode, 16, false, 16, 2, false, true>, 512, smem_p1(D1, kMode, 16, 16));
+      else if (p.exp & 512) rc = go(k_p1<kMode, 16, false, 16, 2, false, false, true>, 512, smem_p1(D1, kMode, 16, 16));
+      else rc = go(k_p1<kMode, 16, false, 16>, 512, smem_p1(D1, kMode, 16, 16));
+      break;
     case kC8x32: rc = go(k_p1<kMode, 32>, T, smem_p1(D1, kMode, 32)); break;
     case kW16x32:
       if (slab) rc = go(k_p1<kMode, 32, true, 16, 1, true>, 512, smem_p1(D1, kMode, 32, 16));
@@ -666,7 +670,8 @@ int level23(const Plan& p, const Layout& q, Ws& w, const uint32_t* r1, uint32_t 
       if ((rc = set_smem(kern, sm))) return rc;
       kern<<<persistent_grid(kern, T, sm, q.max_t2), T, sm, st>>>(r1, w.tiles2, n_t2, Db, dec, w.base2, w.r2, nullptr, nullptr, nullptr);
     } else {  // 4096-record tiles, 4 CTAs/SM, no batched landing loads (C3 2.11 vs 2.18 ms)
-      auto kern = k_p2<kMode, DecR1, 16, false, kIoPlain, false>;
+      auto kern = (p.exp & 128) ? k_p2<kMode, DecR1, 16, false, kIoPlain, false, W, 4, true, true>
+                                : k_p2<kMode, DecR1, 16, false, kIoPlain, false>;
       const size_t sm = smem_p2(Db, kMode, 16);
       if ((rc = set_smem(kern, sm))) return rc;
       kern<<<persistent_grid(kern, T, sm, q.max_t2), T, sm, st>>>(r1, w.tiles2, n_t2, Db, dec, w.base2, w.r2, nullptr, nullptr, nullptr);

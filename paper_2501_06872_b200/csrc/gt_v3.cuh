@@ -607,7 +607,7 @@ __device__ __forceinline__ void stage_pair(const uint32_t (&pk)[K_], const uint3
 // destination slab are ranked, staged and written (the others pass through
 // source recovery only); the digit is taken modulo D.
 template <int kMode, int KK = K, bool kW64 = false, int WW = W, int kMinB = (KK > 16 || kW64 || WW > 8 ? 2 : 4),
-          bool kSlab = false>
+          bool kSlab = false, bool kPair = false, bool kOpt = false>
 __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
   constexpr int W1_ = WW, T1_ = WW * 32, WH1_ = WW / 2 + 1, WP1_ = WW + 1;
   // place tiles of PT = W1_ * KK * 32 edges; the offsets window doubles as the
@@ -623,6 +623,9 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
   // the next window lands by TMA after the end-of-tile barrier + proxy fence)
   static_assert(kWin * 8 >= PT * 2, "tag array must fit in the window");
   uint16_t* s_tag = reinterpret_cast<uint16_t*>(s_win);
+  // kPair: (payload, digit) pairs staged over landing buffer + window + marks (all dead after ranking)
+  static_assert(!kPair || (!kW64 && !kSlab && PTP * 4 + kWin * 8 + PT * 2 >= PT * 8), "pair staging does not fit");
+  uint2* s_st = reinterpret_cast<uint2*>(smem);
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_mark + PT);                  // D * WH1_ (packed, digit-major)
   uint32_t* s_scr = s_cnt + round4(D * WH1_);                                    // D * WP1_ (safe)
   uint32_t* s_gcur = s_scr + (kMode == kRankSafe ? round4(D * WP1_) : 0);        // D
@@ -667,6 +670,17 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
   }
   __syncthreads();
 
+  // kFast: rank, stage and write-out through 32-bit shared addresses off laundered registers (gt_common.cuh)
+  constexpr bool kFast = kOpt && kMode == kRankAtomic && !kW64 && !kSlab && !kPair;
+  uint32_t f_sb = 0, f_cw = 0, f_inc = 0, f_selr = 0, f_sel16 = 0, f_delta = 0;
+  if constexpr (kFast) {
+    f_sb = launder(smem_u32(smem));
+    f_cw = launder(f_sb + (uint32_t)(PTP * 4 + kWin * 8 + PT * 2) + (w >> 1) * 4);  // this warp's word of every digit row
+    f_inc = launder(1u << sh);
+    f_selr = launder((w & 1) ? 0x5432u : 0x5410u);   // (old field, digit) -> digit << 16 | rank
+    f_sel16 = launder((w & 1) ? 0x4432u : 0x4410u);  // this warp's u16 field of a counter word
+    f_delta = launder(smem_u32(s_delta));
+  }
   auto issue = [&](int j) {  // thread 0
     const uint64_t pt = tb + (uint64_t)j * PT;
     const uint32_t n = (uint32_t)umin64(PT, te - pt);
@@ -782,18 +796,64 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
       }
       pay[s] = ((dst & a.low_mask) << a.L) | (src & a.src_mask);
     };
+    bool fdone = false;
+    if constexpr (kFast) {
+      if (!wide) {
+        fdone = true;
+        const uint32_t a_rec = f_sb + (o + iw + lane) * 4, a_mk = f_sb + (uint32_t)(PTP * 4 + kWin * 8) + (iw + lane) * 2;
 #pragma unroll
-    for (int s = 0; s < K; ++s) {
-      const uint32_t i = iw + s * 32 + lane;
-      pay[s] = s_buf[o + i];
-      pk[s] = s_mark[i];
+        for (int s = 0; s < K; ++s) {
+          pay[s] = lds_u32(a_rec + s * 128);
+          pk[s] = lds_u16(a_mk + s * 64);
+        }
+        const uint32_t shift = a.shift, lowm = a.low_mask, L = a.L, srcm = a.src_mask;
+        auto fslot = [&](int s, bool valid) {
+          const uint32_t dst = valid ? pay[s] : 0u;
+          const uint32_t m = pk[s];
+          uint32_t src = carry;
+          const uint32_t bal = __ballot_sync(kFull, m != 0);
+          if (bal) {  // a source starts inside this slot (warp-uniform)
+            const uint32_t bm = bal & le;
+            const uint32_t ms = __shfl_sync(kFull, m, 31 - __clz(bm | 1u));
+            src = bm ? s0 + ms : carry;
+            carry = __shfl_sync(kFull, src, 31);
+          }
+          const uint32_t d = dst >> shift;
+          uint32_t old = 0;
+          if (valid) old = atoms_add(f_cw + d * (uint32_t)(WH1_ * 4), f_inc);
+          pk[s] = prmt(old, d, f_selr);
+          pay[s] = ((dst & lowm) << L) | (src & srcm);
+          return src;
+        };
+        if (n == (uint32_t)PT) {
+          uint32_t src = 0;
+#pragma unroll
+          for (int s = 0; s < K; ++s) src = fslot(s, true);
+          if (tid == T1_ - 1) s_last_src = src;
+        } else {
+#pragma unroll
+          for (int s = 0; s < K; ++s) {
+            const uint32_t i = iw + s * 32 + lane;
+            const uint32_t src = fslot(s, i < n);
+            if (i == n - 1) s_last_src = src;
+          }
+        }
+      }
     }
-    if (n == (uint32_t)PT) {
+    if (!fdone) {
 #pragma unroll
-      for (int s = 0; s < K; ++s) slot(s, true);
-    } else {
+      for (int s = 0; s < K; ++s) {
+        const uint32_t i = iw + s * 32 + lane;
+        pay[s] = s_buf[o + i];
+        pk[s] = s_mark[i];
+      }
+      if (n == (uint32_t)PT) {
 #pragma unroll
-      for (int s = 0; s < K; ++s) slot(s, iw + s * 32 + lane < n);
+        for (int s = 0; s < K; ++s) slot(s, true);
+      } else {
+#pragma unroll
+        for (int s = 0; s < K; ++s) slot(s, iw + s * 32 + lane < n);
+      }
     }
     if (kSlab && lane == 0) atomicAdd(&s_nst, nkeep);
     __syncthreads();  // (B) ranks done; landing buffer and marks consumed
@@ -825,11 +885,46 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
     h_prev = h_last;
     // stage payloads and global indices by digit (base words loaded in groups
     // of kStageG before their stores)
-    stage_tag<kStageG, K, uint16_t, kSlab>(pk, pay, s_cnt, WH1_, w, sh, s_buf, s_tag,
-                                            (n == (uint32_t)PT) ? 0xffffffffu : n, iw + lane);
+    if constexpr (kFast) {
+      const uint32_t a_tag = f_sb + (uint32_t)(PTP * 4);
+      auto fstage = [&](auto full_c) {
+        constexpr bool kFull_ = decltype(full_c)::value;
+#pragma unroll
+        for (int c = 0; c < K; c += kStageG) {
+          uint32_t bw[kStageG];
+#pragma unroll
+          for (int q = 0; q < kStageG; ++q) bw[q] = lds_u32(f_cw + (pk[c + q] >> 16) * (uint32_t)(WH1_ * 4));
+#pragma unroll
+          for (int q = 0; q < kStageG; ++q)
+            if (kFull_ || iw + (c + q) * 32 + lane < n) {
+              const uint32_t pos = prmt(bw[q], 0u, f_sel16) + (pk[c + q] & 0xffffu);
+              sts_u32(f_sb + pos * 4, pay[c + q]);
+              sts_u16(a_tag + pos * 2, pk[c + q] >> 16);
+            }
+        }
+      };
+      if (n == (uint32_t)PT) fstage(std::true_type{});
+      else fstage(std::false_type{});
+    } else if constexpr (kPair)
+      stage_pair<kStageG, K>(pk, pay, s_cnt, WH1_, w, sh, s_st, (n == (uint32_t)PT) ? 0xffffffffu : n, iw + lane);
+    else
+      stage_tag<kStageG, K, uint16_t, kSlab>(pk, pay, s_cnt, WH1_, w, sh, s_buf, s_tag,
+                                              (n == (uint32_t)PT) ? 0xffffffffu : n, iw + lane);
     __syncthreads();  // (C)
     const uint32_t nout = kSlab ? s_nst : n;  // staged items
-    if constexpr (kW64) writeout_tag<T1_, PT>(a.out, s_buf, s_tag, s_g64, nout);
+    if constexpr (kFast) {
+      const uint32_t a_b = f_sb + tid * 4, a_t = f_sb + (uint32_t)(PTP * 4) + tid * 2;
+      uint32_t* outp = a.out + tid;
+      if (n == (uint32_t)PT) {
+#pragma unroll
+        for (int k = 0; k < PT / T1_; ++k)
+          outp[lds_u32(f_delta + lds_u16(a_t + k * (T1_ * 2)) * 4) + k * T1_] = lds_u32(a_b + k * (T1_ * 4));
+      } else {
+        for (uint32_t i = tid, k = 0; i < n; i += T1_, ++k)
+          outp[lds_u32(f_delta + lds_u16(a_t + k * (T1_ * 2)) * 4) + k * T1_] = lds_u32(a_b + k * (T1_ * 4));
+      }
+    } else if constexpr (kPair) writeout_pair<T1_, PT>(a.out, s_st, s_delta, nout);
+    else if constexpr (kW64) writeout_tag<T1_, PT>(a.out, s_buf, s_tag, s_g64, nout);
     else writeout_tag<T1_, PT>(a.out, s_buf, s_tag, s_delta, nout);
     zero_u32(reinterpret_cast<uint32_t*>(s_mark), PT / 2);
     if (tid < 32) s_lastm[tid] = 0;
@@ -1031,7 +1126,7 @@ __device__ __forceinline__ uint32_t slot_owner32(uint32_t& cur, uint32_t& nb, ui
 // kS64: staged items as (payload, digit) pairs, one 8-byte store / load each (the
 // landing buffer is dead after ranking and the pair array overlays it).
 template <int kMode, class Dec, int KK, bool kProf = false, int kIO = kIoPlain, bool kPre = true, int WW = W,
-          int kMinB = (KK > 16 ? 2 : 4), bool kS64 = (kIO == kIoPlain && KK <= 16)>
+          int kMinB = (KK > 16 ? 2 : 4), bool kS64 = (kIO == kIoPlain && KK <= 16), bool kOpt = false>
 __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restrict__ rec, const RTile* __restrict__ tiles,
                                              const uint32_t* __restrict__ n_tiles, int D, Dec dec,
                                              const uint64_t* __restrict__ base, uint32_t* __restrict__ out,
@@ -1082,6 +1177,22 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
   }
   __syncthreads();
   uint32_t ph = 0;
+  // kFast: rank and stage through 32-bit shared addresses off laundered registers (gt_common.cuh)
+  constexpr bool kFast = kOpt && kMode == kRankAtomic && kS64 && kIO == kIoPlain && !Dec::kMatchRank && Dec::kSrcHigh;
+  uint32_t f_sb = 0, f_cw = 0, f_inc = 0, f_selr = 0, f_sel16 = 0, f_shB = 0, f_maskB = 0, f_himask = 0, f_mul = 0,
+           f_srcm = 0;
+  if constexpr (kFast) {
+    f_sb = launder(smem_u32(smem));
+    f_cw = launder(f_sb + (uint32_t)PT * 8 + (w >> 1) * 4);  // this warp's word of every digit row
+    f_inc = launder(1u << sh);
+    f_selr = launder((w & 1) ? 0x5432u : 0x5410u);   // (old field, digit) -> digit << 16 | rank
+    f_sel16 = launder((w & 1) ? 0x4432u : 0x4410u);  // this warp's u16 field of a counter word
+    f_shB = launder((uint32_t)dec.shB);
+    f_maskB = launder(dec.maskB);
+    f_himask = launder(dec.lvmask << dec.L);
+    f_mul = launder(1u << (dec.nbs - dec.L));
+    f_srcm = launder(dec.src_mask);
+  }
 
   for (uint32_t g = blockIdx.x; g < ntall; g += gridDim.x) {
     const RTile t = tiles[g];
@@ -1196,7 +1307,33 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
 #pragma unroll
         for (int s = 0; s < K; ++s) pay[s] = s_buf[o + iw + s * 32 + lane];  // in bounds: iw + K * 32 <= PT
       }
-      if (n == (uint32_t)PT) {
+      bool fdone = false;
+      if constexpr (kFast) {
+        if (!wbnd) {  // no source-high boundary inside this warp's items: h is constant
+          fdone = true;
+          const uint32_t hl = (t.h0 + cur) << dec.L;
+          const uint32_t a_rec = f_sb + (o + iw + lane) * 4;
+          auto fslot = [&](int s, bool valid) {
+            uint32_t r = 0;
+            if constexpr (kPre) r = valid ? pay[s] : 0u;
+            else if (valid) r = lds_u32(a_rec + s * 128);
+            const uint32_t d = (r >> f_shB) & f_maskB;
+            uint32_t old = 0;
+            if (valid) old = atoms_add(f_cw + d * (uint32_t)(WH2_ * 4), f_inc);
+            pk[s] = prmt(old, d, f_selr);
+            pay[s] = (r & f_himask) * f_mul + ((r & f_srcm) | hl);
+          };
+          if (n == (uint32_t)PT) {
+#pragma unroll
+            for (int s = 0; s < K; ++s) fslot(s, true);
+          } else {
+#pragma unroll
+            for (int s = 0; s < K; ++s) fslot(s, iw + s * 32 + lane < n);
+          }
+        }
+      }
+      if (fdone) {
+      } else if (n == (uint32_t)PT) {
 #pragma unroll
         for (int s = 0; s < K; ++s) slot(s, true);
       } else {
@@ -1216,7 +1353,24 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
       else
         flat_bases_pk<WH2_>(s_cnt, D, s_gcur, s_dtot, s_delta, s_tmp);
       tick(3);
-      if constexpr (kS64) {
+      if constexpr (kFast) {
+        constexpr int G = kPre ? kStageG : 1;
+        auto fstage = [&](auto full_c) {
+          constexpr bool kFull_ = decltype(full_c)::value;
+#pragma unroll
+          for (int c = 0; c < K; c += G) {
+            uint32_t bw[G];
+#pragma unroll
+            for (int q = 0; q < G; ++q) bw[q] = lds_u32(f_cw + (pk[c + q] >> 16) * (uint32_t)(WH2_ * 4));
+#pragma unroll
+            for (int q = 0; q < G; ++q)
+              if (kFull_ || iw + (c + q) * 32 + lane < n)
+                sts_v2(f_sb + (prmt(bw[q], 0u, f_sel16) + (pk[c + q] & 0xffffu)) * 8, pay[c + q], pk[c + q] >> 16);
+          }
+        };
+        if (n == (uint32_t)PT) fstage(std::true_type{});
+        else fstage(std::false_type{});
+      } else if constexpr (kS64) {
         stage_pair<kPre ? kStageG : 1, K>(pk, pay, s_cnt, WH2_, w, sh, s_st64, (n == (uint32_t)PT) ? 0xffffffffu : n,
                                           iw + lane, per);
       } else if constexpr (kIO != kIoSplit) {
