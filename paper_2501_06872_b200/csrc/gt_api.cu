@@ -570,8 +570,8 @@ int level1(const Plan& p, const Layout& q, Ws& w, InCsr in, uint64_t E, bool sen
   };
   switch (form) {
     case kC16x16:
-      if (p.exp & 64) rc = go(k_p1<kMode, 16, false, 16, 2, false, true>, 512, smem_p1(D1, kMode, 16, 16));
-      else if (p.exp & 512) rc = go(k_p1<kMode, 16, false, 16, 2, false, false, true>, 512, smem_p1(D1, kMode, 16, 16));
+      // experiment bit 4096: the pointer-based rank/stage loops (A/B of DESIGN.md §2e)
+      if (p.exp & 4096) rc = go(k_p1<kMode, 16, false, 16, 2, false, false>, 512, smem_p1(D1, kMode, 16, 16));
       else rc = go(k_p1<kMode, 16, false, 16>, 512, smem_p1(D1, kMode, 16, 16));
       break;
     case kC8x32: rc = go(k_p1<kMode, 32>, T, smem_p1(D1, kMode, 32)); break;
@@ -670,8 +670,8 @@ int level23(const Plan& p, const Layout& q, Ws& w, const uint32_t* r1, uint32_t 
       if ((rc = set_smem(kern, sm))) return rc;
       kern<<<persistent_grid(kern, T, sm, q.max_t2), T, sm, st>>>(r1, w.tiles2, n_t2, Db, dec, w.base2, w.r2, nullptr, nullptr, nullptr);
     } else {  // 4096-record tiles, 4 CTAs/SM, no batched landing loads (C3 2.11 vs 2.18 ms)
-      auto kern = (p.exp & 128) ? k_p2<kMode, DecR1, 16, false, kIoPlain, false, W, 4, true, true>
-                                : k_p2<kMode, DecR1, 16, false, kIoPlain, false>;
+      auto kern = (p.exp & 4096) ? k_p2<kMode, DecR1, 16, false, kIoPlain, false, W, 4, true, false>
+                                 : k_p2<kMode, DecR1, 16, false, kIoPlain, false>;
       const size_t sm = smem_p2(Db, kMode, 16);
       if ((rc = set_smem(kern, sm))) return rc;
       kern<<<persistent_grid(kern, T, sm, q.max_t2), T, sm, st>>>(r1, w.tiles2, n_t2, Db, dec, w.base2, w.r2, nullptr, nullptr, nullptr);
@@ -738,7 +738,7 @@ int level23(const Plan& p, const Layout& q, Ws& w, const uint32_t* r1, uint32_t 
       kern<<<persistent_grid(kern, T, sm, q.max_t3), T, sm, sb>>>(w.r2, w.tiles3, w.cnt + 2, Dc, dec, w.base3, t_edges,
                                                                    nullptr, w.r2lv, nullptr);
     } else {  // batched landing loads (C3 big buckets 0.85 -> 0.78 ms)
-      auto kern = k_p2<kMode, DecR2, 16>;
+      auto kern = (p.exp & 4096) ? k_p2<kMode, DecR2, 16, false, kIoPlain, true, W, 4, true, false> : k_p2<kMode, DecR2, 16>;
       const size_t sm = smem_p2(Dc, kMode, 16);
       if ((rc = set_smem(kern, sm))) return rc;
       kern<<<persistent_grid(kern, T, sm, q.max_t3), T, sm, sb>>>(w.r2, w.tiles3, w.cnt + 2, Dc, dec, w.base3, t_edges,
@@ -777,7 +777,8 @@ int level23(const Plan& p, const Layout& q, Ws& w, const uint32_t* r1, uint32_t 
     // batched landing loads where fine buckets come from positions (C4 4.40 -> 4.33 ms)
     if (p.wide) rc = go3(k_p3<kMode, true, false, true>);
     else if (pos_fine) rc = go3(k_p3<kMode, true>);
-    else rc = go3(k_p3<kMode, false, false, false, false>);
+    else rc = (p.exp & 4096) ? go3(k_p3<kMode, false, false, false, false, W3, true, false>)
+                             : go3(k_p3<kMode, false, false, false, false>);
     if (rc) return rc;
     GT_LAUNCH_CHECK();
     if ((rc = tm.kend(2))) return rc;

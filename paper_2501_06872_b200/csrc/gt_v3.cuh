@@ -607,7 +607,7 @@ __device__ __forceinline__ void stage_pair(const uint32_t (&pk)[K_], const uint3
 // destination slab are ranked, staged and written (the others pass through
 // source recovery only); the digit is taken modulo D.
 template <int kMode, int KK = K, bool kW64 = false, int WW = W, int kMinB = (KK > 16 || kW64 || WW > 8 ? 2 : 4),
-          bool kSlab = false, bool kPair = false, bool kOpt = false>
+          bool kSlab = false, bool kOpt = true>
 __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
   constexpr int W1_ = WW, T1_ = WW * 32, WH1_ = WW / 2 + 1, WP1_ = WW + 1;
   // place tiles of PT = W1_ * KK * 32 edges; the offsets window doubles as the
@@ -623,9 +623,6 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
   // the next window lands by TMA after the end-of-tile barrier + proxy fence)
   static_assert(kWin * 8 >= PT * 2, "tag array must fit in the window");
   uint16_t* s_tag = reinterpret_cast<uint16_t*>(s_win);
-  // kPair: (payload, digit) pairs staged over landing buffer + window + marks (all dead after ranking)
-  static_assert(!kPair || (!kW64 && !kSlab && PTP * 4 + kWin * 8 + PT * 2 >= PT * 8), "pair staging does not fit");
-  uint2* s_st = reinterpret_cast<uint2*>(smem);
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_mark + PT);                  // D * WH1_ (packed, digit-major)
   uint32_t* s_scr = s_cnt + round4(D * WH1_);                                    // D * WP1_ (safe)
   uint32_t* s_gcur = s_scr + (kMode == kRankSafe ? round4(D * WP1_) : 0);        // D
@@ -671,7 +668,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
   __syncthreads();
 
   // kFast: rank, stage and write-out through 32-bit shared addresses off laundered registers (gt_common.cuh)
-  constexpr bool kFast = kOpt && kMode == kRankAtomic && !kW64 && !kSlab && !kPair;
+  constexpr bool kFast = kOpt && kMode == kRankAtomic && !kW64 && !kSlab;
   uint32_t f_sb = 0, f_cw = 0, f_inc = 0, f_selr = 0, f_sel16 = 0, f_delta = 0;
   if constexpr (kFast) {
     f_sb = launder(smem_u32(smem));
@@ -905,9 +902,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
       };
       if (n == (uint32_t)PT) fstage(std::true_type{});
       else fstage(std::false_type{});
-    } else if constexpr (kPair)
-      stage_pair<kStageG, K>(pk, pay, s_cnt, WH1_, w, sh, s_st, (n == (uint32_t)PT) ? 0xffffffffu : n, iw + lane);
-    else
+    } else
       stage_tag<kStageG, K, uint16_t, kSlab>(pk, pay, s_cnt, WH1_, w, sh, s_buf, s_tag,
                                               (n == (uint32_t)PT) ? 0xffffffffu : n, iw + lane);
     __syncthreads();  // (C)
@@ -923,7 +918,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
         for (uint32_t i = tid, k = 0; i < n; i += T1_, ++k)
           outp[lds_u32(f_delta + lds_u16(a_t + k * (T1_ * 2)) * 4) + k * T1_] = lds_u32(a_b + k * (T1_ * 4));
       }
-    } else if constexpr (kPair) writeout_pair<T1_, PT>(a.out, s_st, s_delta, nout);
+    }
     else if constexpr (kW64) writeout_tag<T1_, PT>(a.out, s_buf, s_tag, s_g64, nout);
     else writeout_tag<T1_, PT>(a.out, s_buf, s_tag, s_delta, nout);
     zero_u32(reinterpret_cast<uint32_t*>(s_mark), PT / 2);
@@ -1126,7 +1121,7 @@ __device__ __forceinline__ uint32_t slot_owner32(uint32_t& cur, uint32_t& nb, ui
 // kS64: staged items as (payload, digit) pairs, one 8-byte store / load each (the
 // landing buffer is dead after ranking and the pair array overlays it).
 template <int kMode, class Dec, int KK, bool kProf = false, int kIO = kIoPlain, bool kPre = true, int WW = W,
-          int kMinB = (KK > 16 ? 2 : 4), bool kS64 = (kIO == kIoPlain && KK <= 16), bool kOpt = false>
+          int kMinB = (KK > 16 ? 2 : 4), bool kS64 = (kIO == kIoPlain && KK <= 16), bool kOpt = true>
 __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restrict__ rec, const RTile* __restrict__ tiles,
                                              const uint32_t* __restrict__ n_tiles, int D, Dec dec,
                                              const uint64_t* __restrict__ base, uint32_t* __restrict__ out,
@@ -1178,20 +1173,20 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
   __syncthreads();
   uint32_t ph = 0;
   // kFast: rank and stage through 32-bit shared addresses off laundered registers (gt_common.cuh)
-  constexpr bool kFast = kOpt && kMode == kRankAtomic && kS64 && kIO == kIoPlain && !Dec::kMatchRank && Dec::kSrcHigh;
-  uint32_t f_sb = 0, f_cw = 0, f_inc = 0, f_selr = 0, f_sel16 = 0, f_shB = 0, f_maskB = 0, f_himask = 0, f_mul = 0,
-           f_srcm = 0;
+  constexpr bool kFast = kOpt && kMode == kRankAtomic && kS64 && kIO == kIoPlain;
+  uint32_t f_sb = 0, f_cw = 0, f_inc = 0, f_selr = 0, f_sel16 = 0, f_himask = 0, f_mul = 0, f_srcm = 0, f_delta = 0;
   if constexpr (kFast) {
     f_sb = launder(smem_u32(smem));
+    f_delta = launder(smem_u32(s_delta));
     f_cw = launder(f_sb + (uint32_t)PT * 8 + (w >> 1) * 4);  // this warp's word of every digit row
     f_inc = launder(1u << sh);
     f_selr = launder((w & 1) ? 0x5432u : 0x5410u);   // (old field, digit) -> digit << 16 | rank
     f_sel16 = launder((w & 1) ? 0x4432u : 0x4410u);  // this warp's u16 field of a counter word
-    f_shB = launder((uint32_t)dec.shB);
-    f_maskB = launder(dec.maskB);
-    f_himask = launder(dec.lvmask << dec.L);
-    f_mul = launder(1u << (dec.nbs - dec.L));
-    f_srcm = launder(dec.src_mask);
+    if constexpr (Dec::kSrcHigh) {  // R1 -> R2: (r & himask) * mul moves the low-digit field above the source bits
+      f_himask = launder(dec.lvmask << dec.L);
+      f_mul = launder(1u << (dec.nbs - dec.L));
+      f_srcm = launder(dec.src_mask);
+    }
   }
 
   for (uint32_t g = blockIdx.x; g < ntall; g += gridDim.x) {
@@ -1311,24 +1306,38 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
       if constexpr (kFast) {
         if (!wbnd) {  // no source-high boundary inside this warp's items: h is constant
           fdone = true;
-          const uint32_t hl = (t.h0 + cur) << dec.L;
+          uint32_t hl = 0;
+          if constexpr (Dec::kSrcHigh) hl = (t.h0 + cur) << dec.L;
           const uint32_t a_rec = f_sb + (o + iw + lane) * 4;
           auto fslot = [&](int s, bool valid) {
             uint32_t r = 0;
             if constexpr (kPre) r = valid ? pay[s] : 0u;
             else if (valid) r = lds_u32(a_rec + s * 128);
-            const uint32_t d = (r >> f_shB) & f_maskB;
-            uint32_t old = 0;
-            if (valid) old = atoms_add(f_cw + d * (uint32_t)(WH2_ * 4), f_inc);
-            pk[s] = prmt(old, d, f_selr);
-            pay[s] = (r & f_himask) * f_mul + ((r & f_srcm) | hl);
+            const uint32_t d = dec.digit(r);
+            if constexpr (Dec::kMatchRank) {  // one atomic per distinct digit of the slot
+              const uint32_t m = __match_any_sync(kFull, valid ? d : 0xffffffffu);
+              const uint32_t ld = __ffs(m) - 1;
+              uint32_t old = 0;
+              if (valid && lane == ld) old = atoms_add(f_cw + d * (uint32_t)(WH2_ * 4), (uint32_t)__popc(m) << sh);
+              old = __shfl_sync(kFull, old, ld);
+              pk[s] = prmt(old, d, f_selr) + __popc(m & lanemask_lt());
+            } else {
+              uint32_t old = 0;
+              if (valid) old = atoms_add(f_cw + d * (uint32_t)(WH2_ * 4), f_inc);
+              pk[s] = prmt(old, d, f_selr);
+            }
+            if constexpr (Dec::kSrcHigh) pay[s] = (r & f_himask) * f_mul + ((r & f_srcm) | hl);
+            else pay[s] = dec.payload(r, 0u);
           };
           if (n == (uint32_t)PT) {
 #pragma unroll
             for (int s = 0; s < K; ++s) fslot(s, true);
           } else {
 #pragma unroll
-            for (int s = 0; s < K; ++s) fslot(s, iw + s * 32 + lane < n);
+            for (int s = 0; s < K; ++s) {
+              if (kBal2 && (uint32_t)s * 32 >= per) break;
+              fslot(s, iw + s * 32 + lane < n);
+            }
           }
         }
       }
@@ -1364,7 +1373,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
             for (int q = 0; q < G; ++q) bw[q] = lds_u32(f_cw + (pk[c + q] >> 16) * (uint32_t)(WH2_ * 4));
 #pragma unroll
             for (int q = 0; q < G; ++q)
-              if (kFull_ || iw + (c + q) * 32 + lane < n)
+              if (kFull_ || ((uint32_t)(c + q) * 32 < per && iw + (c + q) * 32 + lane < n))
                 sts_v2(f_sb + (prmt(bw[q], 0u, f_sel16) + (pk[c + q] & 0xffffu)) * 8, pay[c + q], pk[c + q] >> 16);
           }
         };
@@ -1390,7 +1399,22 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
       }
       __syncthreads();  // (C)
       tick(4);
-      if constexpr (kS64) {
+      if constexpr (kFast) {
+        const uint32_t a_st = f_sb + tid * 8;
+        uint32_t* outp = out + tid;
+        if (n == (uint32_t)PT) {
+#pragma unroll
+          for (int k = 0; k < PT / T2_; ++k) {
+            const uint2 v = lds_v2(a_st + k * (T2_ * 8));
+            outp[lds_u32(f_delta + v.y * 4) + k * T2_] = v.x;
+          }
+        } else {
+          for (uint32_t i = tid, k = 0; i < n; i += T2_, ++k) {
+            const uint2 v = lds_v2(a_st + k * (T2_ * 8));
+            outp[lds_u32(f_delta + v.y * 4) + k * T2_] = v.x;
+          }
+        }
+      } else if constexpr (kS64) {
         writeout_pair<T2_, PT>(out, s_st64, s_delta, n);
       } else if constexpr (kIO == kIoPlain) {
         writeout_tag<T2_, PT>(out, s_buf, s_tag, s_delta, n);
@@ -1455,7 +1479,7 @@ inline size_t smem_p3(int mode, bool lv = false, int ww = W3) {
 // each, consecutive ranges in warp order) and warps skip their empty slots;
 // otherwise every warp owns 512 positions and partial units run predicated slots.
 template <int kMode, bool kPosFine, bool kProf = false, bool kLv = false, bool kPre = true, int WW3 = W3,
-          bool kBal = true>
+          bool kBal = true, bool kOpt = true>
 __global__ void __launch_bounds__(WW3 * 32, WW3 > 16 ? 1 : 2) k_p3(const P3Args a) {
   // phase profile (kProf builds only; thread 0, clock64): 0 fetch/issue, 1 wait, 2 rank, 3 bases+offsets, 4 stage, 5 store
   unsigned long long pacc[kProf ? 6 : 1] = {};
@@ -1492,6 +1516,16 @@ __global__ void __launch_bounds__(WW3 * 32, WW3 > 16 ? 1 : 2) k_p3(const P3Args 
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
     fence_mbar_init();
+  }
+  // kFast: rank and stage through 32-bit shared addresses off laundered registers (gt_common.cuh)
+  constexpr bool kFast = kOpt && kMode == kRankAtomic && !kLv;
+  uint32_t f_sb = 0, f_cw = 0, f_inc = 0, f_selr = 0, f_sel16 = 0;
+  if constexpr (kFast) {
+    f_sb = launder(smem_u32(smem));
+    f_cw = launder(f_sb + (uint32_t)(2 * CAP3P_ * 4) + (w >> 1) * 4);
+    f_inc = launder(1u << sh);
+    f_selr = launder((w & 1) ? 0x5432u : 0x5410u);
+    f_sel16 = launder((w & 1) ? 0x4432u : 0x4410u);
   }
   auto issue = [&](uint32_t ui, int b) {  // thread 0
     const Unit3 u = a.units[ui];
@@ -1565,8 +1599,31 @@ __global__ void __launch_bounds__(WW3 * 32, WW3 > 16 ? 1 : 2) k_p3(const P3Args 
         rr[s] = buf[o + seg0 + s * 32 + lane];
       }
     }
+    bool fdone = false;
+    if constexpr (kFast) {
+      if (!kPosFine || !wbnd) {  // (kPosFine: no fine-bucket boundary inside this warp's positions)
+        fdone = true;
+        const uint32_t a_rec = f_sb + (uint32_t)b * (CAP3P_ * 4) + (o + seg0 + lane) * 4;
+        const uint32_t nbs = a.nbs, lvm = kPosFine ? a.mask_c : a.lvmask, srcm = a.src_mask;
+        const uint32_t lvadd = kPosFine ? (fcur << a.c) : (0u - lvoff);
+#pragma unroll
+        for (int s = 0; s < K3; ++s) {
+          if (kBal && (uint32_t)s * 32 >= per) break;
+          const bool valid = seg0 + s * 32 + lane < n;
+          uint32_t r = 0;
+          if constexpr (kPre) r = valid ? rr[s] : 0u;
+          else if (valid) r = lds_u32(a_rec + s * 128);
+          const uint32_t lv = valid ? (((r >> nbs) & lvm) + lvadd) : 0u;
+          uint32_t old = 0;
+          if (valid) old = atoms_add(f_cw + lv * (uint32_t)(WH3_ * 4), f_inc);
+          pk[s] = prmt(old, lv, f_selr);
+          rr[s] = r & srcm;
+        }
+      }
+    }
 #pragma unroll
     for (int s = 0; s < K3; ++s) {
+      if (fdone) break;
       if (kBal && (uint32_t)s * 32 >= per) break;
       const uint32_t i = seg0 + s * 32 + lane;
       const bool valid = i < n;
@@ -1593,8 +1650,24 @@ __global__ void __launch_bounds__(WW3 * 32, WW3 > 16 ? 1 : 2) k_p3(const P3Args 
     tick(3);
     uint32_t* t_e = a.t_edges + u.start;
     const uint32_t oo = align_items_u32(t_e);  // staging offset matching the output's 16B alignment
+    if constexpr (kFast) {
+      const uint32_t a_out = f_sb + (uint32_t)b * (CAP3P_ * 4) + oo * 4;
+#pragma unroll
+      for (int c = 0; c < K3; c += kG3) {
+        if (kBal && (uint32_t)c * 32 >= per) break;
+        uint32_t bw[kG3];
+#pragma unroll
+        for (int q = 0; q < kG3; ++q)
+          if (!kBal || (uint32_t)(c + q) * 32 < per) bw[q] = lds_u32(f_cw + (pk[c + q] >> 16) * (uint32_t)(WH3_ * 4));
+#pragma unroll
+        for (int q = 0; q < kG3; ++q)
+          if ((!kBal || (uint32_t)(c + q) * 32 < per) && seg0 + (c + q) * 32 + lane < n)
+            sts_u32(a_out + (prmt(bw[q], 0u, f_sel16) + (pk[c + q] & 0xffffu)) * 4, rr[c + q]);
+      }
+    }
 #pragma unroll
     for (int c = 0; c < K3; c += kG3) {  // base words of kG3 items loaded before their stores
+      if (kFast) break;
       if (kBal && (uint32_t)c * 32 >= per) break;
       uint32_t bw[kG3];
 #pragma unroll
