@@ -289,6 +289,66 @@ __device__ __forceinline__ void flat_bases_pk(uint32_t* tab, int D, const uint32
   });
 }
 
+// flat_bases_epi's scan on 32-bit shared addresses with a compile-time chunk
+// length (PER words per thread, odd: conflict-free) and block size: the words
+// stay in registers between the two passes, every access has an immediate
+// offset, and each warp sums the earlier warps' totals itself (two barriers).
+// Requires n <= NT * PER.  a_tmp: NT / 32 words.
+template <int NT, int PER>
+__device__ __forceinline__ void flat_scan_fast(uint32_t a_tab, uint32_t n, uint32_t a_tmp) {
+  static_assert(PER & 1, "odd chunk length");
+  const uint32_t t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int rem = (int)n - (int)(t * PER);  // words of this thread: i < rem
+  const uint32_t a0 = a_tab + t * (PER * 4);
+  constexpr bool kKeep = PER <= 3;  // longer chunks are re-read (the callers hold 32+ live registers)
+  uint32_t v[PER];
+  uint32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    v[i] = 0;
+    if (i < rem) v[i] = lds_u32(a0 + i * 4);
+  }
+#pragma unroll
+  for (int i = 0; i < PER; ++i) s += (v[i] & 0xffffu) + (v[i] >> 16);
+  uint32_t x = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sts_u32(a_tmp + w * 4, x);
+  __syncthreads();
+  uint32_t p = 0;
+  if (lane < w) p = lds_u32(a_tmp + lane * 4);  // (w < NW <= 32)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(kFull, p, o);
+  uint32_t run = p + x - s;
+  if constexpr (!kKeep) {
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      v[i] = 0;
+      if (i < rem) v[i] = lds_u32(a0 + i * 4);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const uint32_t e = run + (v[i] & 0xffffu);
+    if (i < rem) sts_u32(a0 + i * 4, run | (e << 16));
+    run = e + (v[i] >> 16);
+  }
+  __syncthreads();
+}
+// Chunk length by table size; false if the table is larger than NT * 11 words.
+template <int NT>
+__device__ __forceinline__ bool flat_scan_any(uint32_t a_tab, uint32_t n, uint32_t a_tmp) {
+  if (n <= NT * 3) flat_scan_fast<NT, 3>(a_tab, n, a_tmp);
+  else if (n <= NT * 5) flat_scan_fast<NT, 5>(a_tab, n, a_tmp);
+  else if (n <= NT * 9) flat_scan_fast<NT, 9>(a_tab, n, a_tmp);
+  else if (n <= NT * 11) flat_scan_fast<NT, 11>(a_tab, n, a_tmp);
+  else return false;
+  return true;
+}
+
 // In-place exclusive scan of a[0..n) (thread-contiguous chunks, one block scan).
 __device__ __forceinline__ void flat_excl_scan(uint32_t* a, int n, uint32_t* tmp /* >= 33 */) {
   const int Tn = blockDim.x, t = threadIdx.x, lane = t & 31, w = t >> 5, nw = (Tn + 31) >> 5;
@@ -859,8 +919,23 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
         s_g64[d] -= b;
         s_dtot[d] = e;
       });
-    else
-      flat_bases_pk<WH1_>(s_cnt, D, s_gcur, s_dtot, s_delta, s_tmp);
+    else {
+      bool fscan = false;
+      if constexpr (kFast) {
+        const uint32_t a_cnt = f_sb + (uint32_t)(PTP * 4 + kWin * 8 + PT * 2);
+        fscan = flat_scan_any<T1_>(a_cnt, (uint32_t)(D * WH1_), smem_u32(s_tmp));
+        if (fscan) {  // per digit: tile-local start b and end e (the row's pad word)
+          for (int d = tid; d < D; d += T1_) {
+            const uint32_t ar = a_cnt + d * (WH1_ * 4);
+            const uint32_t b = lds_u32(ar) & 0xffffu, e = lds_u32(ar + (WH1_ - 1) * 4) & 0xffffu;
+            sts_u32(f_delta + (uint32_t)D * 4 + d * 4, e - b);            // s_dtot
+            sts_u32(f_delta + d * 4, lds_u32(f_delta - (uint32_t)D * 4 + d * 4) - b);  // s_delta = s_gcur - b
+          }
+          __syncthreads();
+        }
+      }
+      if (!fscan) flat_bases_pk<WH1_>(s_cnt, D, s_gcur, s_dtot, s_delta, s_tmp);
+    }
     // source-high boundaries inside this tile (compact R1 decode table)
     const uint32_t h_last = s_last_src >> a.L;
     for (uint32_t h = (h_prev == 0xffffffffu) ? 0u : h_prev + 1; h <= h_last; ++h) {
@@ -1175,6 +1250,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
   // kFast: rank and stage through 32-bit shared addresses off laundered registers (gt_common.cuh)
   constexpr bool kFast = kOpt && kMode == kRankAtomic && kS64 && kIO == kIoPlain;
   uint32_t f_sb = 0, f_cw = 0, f_inc = 0, f_selr = 0, f_sel16 = 0, f_himask = 0, f_mul = 0, f_srcm = 0, f_delta = 0;
+  bool f_up = true;
   if constexpr (kFast) {
     f_sb = launder(smem_u32(smem));
     f_delta = launder(smem_u32(s_delta));
@@ -1183,8 +1259,9 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
     f_selr = launder((w & 1) ? 0x5432u : 0x5410u);   // (old field, digit) -> digit << 16 | rank
     f_sel16 = launder((w & 1) ? 0x4432u : 0x4410u);  // this warp's u16 field of a counter word
     if constexpr (Dec::kSrcHigh) {  // R1 -> R2: (r & himask) * mul moves the low-digit field above the source bits
+      f_up = dec.nbs >= dec.L;      // (small graphs: the field moves down instead; they take the generic slots)
       f_himask = launder(dec.lvmask << dec.L);
-      f_mul = launder(1u << (dec.nbs - dec.L));
+      f_mul = launder(1u << (f_up ? dec.nbs - dec.L : 0));
       f_srcm = launder(dec.src_mask);
     }
   }
@@ -1304,7 +1381,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
       }
       bool fdone = false;
       if constexpr (kFast) {
-        if (!wbnd) {  // no source-high boundary inside this warp's items: h is constant
+        if (!wbnd && f_up) {  // no source-high boundary inside this warp's items: h is constant
           fdone = true;
           uint32_t hl = 0;
           if constexpr (Dec::kSrcHigh) hl = (t.h0 + cur) << dec.L;
@@ -1354,13 +1431,30 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
       }
       __syncthreads();  // (B)
       tick(2);
+      bool fscan = false;  // kFast: scanned by flat_scan_any (the cursors advance in its epilogue)
       if constexpr (kW64)
         flat_bases_epi<WH2_>(s_cnt, D, s_tmp, [&](int d, uint32_t b, uint32_t e) {
           s_g64[d] -= b;
           s_dtot[d] = e;
         });
-      else
-        flat_bases_pk<WH2_>(s_cnt, D, s_gcur, s_dtot, s_delta, s_tmp);
+      else {
+        if constexpr (kFast) {
+          const uint32_t a_cnt = f_sb + (uint32_t)PT * 8;
+          fscan = flat_scan_any<T2_>(a_cnt, (uint32_t)(D * WH2_), smem_u32(s_tmp));
+          if (fscan) {  // per digit: index delta of this tile, cursor of the next (s_gcur is not read in between)
+            for (int d = tid; d < D; d += T2_) {
+              const uint32_t ar = a_cnt + d * (WH2_ * 4);
+              const uint32_t b = lds_u32(ar) & 0xffffu, e = lds_u32(ar + (WH2_ - 1) * 4) & 0xffffu;
+              const uint32_t ag = f_delta - (uint32_t)D * 4 + d * 4;  // s_gcur
+              const uint32_t gc = lds_u32(ag);
+              sts_u32(f_delta + d * 4, gc - b);
+              sts_u32(ag, gc + (e - b));
+            }
+            __syncthreads();
+          }
+        }
+        if (!fscan) flat_bases_pk<WH2_>(s_cnt, D, s_gcur, s_dtot, s_delta, s_tmp);
+      }
       tick(3);
       if constexpr (kFast) {
         constexpr int G = kPre ? kStageG : 1;
@@ -1433,7 +1527,8 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
       }
       zero_u32(s_cnt, round4(D * WH2_));
       if constexpr (!kW64)
-        for (int d = tid; d < D; d += T2_) s_gcur[d] += s_dtot[d];
+        if (!fscan)
+          for (int d = tid; d < D; d += T2_) s_gcur[d] += s_dtot[d];
       fence_proxy_async_smem();
       __syncthreads();  // (D)
       tick(5);
@@ -1641,7 +1736,12 @@ __global__ void __launch_bounds__(WW3 * 32, WW3 > 16 ? 1 : 2) k_p3(const P3Args 
     }
     __syncthreads();  // (B)
     tick(2);
-    flat_bases_epi<WH3_, false>(s_cnt, (int)nloc, s_tmp, [](int, uint32_t, uint32_t) {});
+    {
+      bool fscan = false;
+      if constexpr (kFast)
+        fscan = flat_scan_any<TT>(f_sb + (uint32_t)(2 * CAP3P_ * 4), nloc * WH3_, smem_u32(s_tmp));
+      if (!fscan) flat_bases_epi<WH3_, false>(s_cnt, (int)nloc, s_tmp, [](int, uint32_t, uint32_t) {});
+    }
     {
       const uint64_t v0 = (uint64_t)u.f0 << a.c;
       for (uint32_t v = tid; v < nloc; v += TT)
