@@ -185,6 +185,21 @@ __device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
 __device__ __forceinline__ void sts_v2(uint32_t a, uint32_t x, uint32_t y) {
   asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(a), "r"(x), "r"(y));
 }
+__device__ __forceinline__ void sts_v4z(uint32_t a) {  // 16 zero bytes
+  asm volatile("{ .reg .b32 z; mov.b32 z, 0; st.shared.v4.b32 [%0], {z,z,z,z}; }" ::"r"(a));
+}
+// Zero nwords (multiple of 4) 32-bit words at the 16-byte aligned shared address a; tid < NT.
+template <int NT>
+__device__ __forceinline__ void zero_s(uint32_t a, uint32_t nwords, uint32_t tid) {
+  for (uint32_t i = tid * 16; i < nwords * 4; i += NT * 16) sts_v4z(a + i);
+}
+template <int NT, int NWORDS>
+__device__ __forceinline__ void zero_s(uint32_t a, uint32_t tid) {
+  static_assert(NWORDS % 4 == 0, "whole 16-byte blocks");
+#pragma unroll
+  for (int k = 0; k < (NWORDS * 4 + NT * 16 - 1) / (NT * 16); ++k)
+    if ((NWORDS * 4) % (NT * 16) == 0 || tid * 16 + k * (NT * 16) < NWORDS * 4) sts_v4z(a + tid * 16 + k * (NT * 16));
+}
 __device__ __forceinline__ uint32_t atoms_add(uint32_t a, uint32_t v) {
   uint32_t o;
   asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(o) : "r"(a), "r"(v));

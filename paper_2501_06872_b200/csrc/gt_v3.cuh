@@ -701,7 +701,8 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
   __shared__ uint32_t s_lastm[32];
   __shared__ uint32_t s_nst;  // kSlab: staged (kept) items of the place tile
 
-  const uint32_t tid = threadIdx.x, lane = lane_id(), w = warp_id();
+  // (kOpt: the thread index in a laundered register — ptxas otherwise re-reads SR_TID.X all over the kernel)
+  const uint32_t tid = kOpt ? launder(threadIdx.x) : threadIdx.x, lane = tid & 31u, w = tid >> 5;
   const uint32_t sh = (w & 1) << 4;
   const uint64_t k = blockIdx.x;
   const uint64_t tb = k * CT1, te = umin64(a.E, tb + CT1);
@@ -766,6 +767,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
   };
 
   uint32_t ph = 0;
+  const uint32_t o_c = align_items_u32(a.edges + tb);
   if (tid == 0 && nplace > 0) issue(0);
   for (int j = 0; j < nplace; ++j) {
     if constexpr (kW64) {  // delta -> cursor of the next tile (after barrier (D): the write-out is done)
@@ -775,10 +777,11 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
     const uint64_t pt = tb + (uint64_t)j * PT;
     const uint32_t n = (uint32_t)umin64(PT, te - pt);
     const uint32_t* gp = a.edges + pt;
-    const uint32_t o = align_items_u32(gp);
+    static_assert(PT % 4 == 0 && CT1 % 4 == 0, "every place tile starts at the stream's 16-byte phase");
+    const uint32_t o = o_c;
     const uint32_t full = (o + n) & ~3u;
     const uint32_t ti = full + tid;
-    const bool tail = tid < 4 && ti < o + n;
+    const bool tail = ((o + n) & 3u) != 0 && tid < 4 && ti < o + n;  // (first test uniform, rarely true)
     uint32_t tv = 0;
     if (tail) tv = ldg_u32(gp - o + ti);
     mbar_wait_parity(&s_bar, ph);
@@ -811,8 +814,8 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
     // owner of the warp's first item: the last source starting in an earlier segment (else s0)
     uint32_t carry;
     if (!wide) {
-      uint32_t mx = 0;
-      for (uint32_t k = 0; k < w; ++k) mx = max(mx, s_lastm[k]);
+      uint32_t mx = (lane < w) ? s_lastm[lane] : 0u;  // (w < 32)
+      mx = __reduce_max_sync(kFull, mx);
       carry = s0 + mx;
     } else {
       carry = owner_search(s0, s1, gi0 + iw, off_at);
@@ -996,11 +999,20 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
     }
     else if constexpr (kW64) writeout_tag<T1_, PT>(a.out, s_buf, s_tag, s_g64, nout);
     else writeout_tag<T1_, PT>(a.out, s_buf, s_tag, s_delta, nout);
-    zero_u32(reinterpret_cast<uint32_t*>(s_mark), PT / 2);
+    if constexpr (kFast) {
+      zero_s<T1_, PT / 2>(f_sb + (uint32_t)(PTP * 4 + kWin * 8), tid);
+      zero_s<T1_>(f_sb + (uint32_t)(PTP * 4 + kWin * 8 + PT * 2), (uint32_t)round4(D * WH1_), tid);
+      for (uint32_t d = tid; d < (uint32_t)D; d += T1_) {
+        const uint32_t ag = f_delta - (uint32_t)D * 4 + d * 4;  // s_gcur += s_dtot
+        sts_u32(ag, lds_u32(ag) + lds_u32(f_delta + (uint32_t)D * 4 + d * 4));
+      }
+    } else {
+      zero_u32(reinterpret_cast<uint32_t*>(s_mark), PT / 2);
+      zero_u32(s_cnt, round4(D * WH1_));
+      if constexpr (!kW64)
+        for (int d = tid; d < D; d += T1_) s_gcur[d] += s_dtot[d];
+    }
     if (tid < 32) s_lastm[tid] = 0;
-    zero_u32(s_cnt, round4(D * WH1_));
-    if constexpr (!kW64)
-      for (int d = tid; d < D; d += T1_) s_gcur[d] += s_dtot[d];
     fence_proxy_async_smem();
     __syncthreads();  // (D)
     if (kSlab && tid == 0) s_nst = 0;  // (read above, before (D); incremented again after the next (A))
