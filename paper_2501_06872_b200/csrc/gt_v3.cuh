@@ -294,12 +294,12 @@ __device__ __forceinline__ void flat_bases_pk(uint32_t* tab, int D, const uint32
 // stay in registers between the two passes, every access has an immediate
 // offset, and each warp sums the earlier warps' totals itself (two barriers).
 // Requires n <= NT * PER.  a_tmp: NT / 32 words.
+// a0 = this thread's first word (a_tab + t * PER * 4), rem = its word count bound (n - t * PER):
+// computed by the caller from the runtime chunk length, so the instances share that arithmetic.
 template <int NT, int PER>
-__device__ __forceinline__ void flat_scan_fast(uint32_t a_tab, uint32_t n, uint32_t a_tmp) {
+__device__ __forceinline__ void flat_scan_fast(uint32_t a0, int rem, uint32_t a_tmp, uint32_t t) {
   static_assert(PER & 1, "odd chunk length");
-  const uint32_t t = threadIdx.x, lane = t & 31, w = t >> 5;
-  const int rem = (int)n - (int)(t * PER);  // words of this thread: i < rem
-  const uint32_t a0 = a_tab + t * (PER * 4);
+  const uint32_t lane = t & 31, w = t >> 5;
   constexpr bool kKeep = PER <= 3;  // longer chunks are re-read (the callers hold 32+ live registers)
   uint32_t v[PER];
   uint32_t s = 0;
@@ -340,12 +340,15 @@ __device__ __forceinline__ void flat_scan_fast(uint32_t a_tab, uint32_t n, uint3
 }
 // Chunk length by table size; false if the table is larger than NT * 11 words.
 template <int NT>
-__device__ __forceinline__ bool flat_scan_any(uint32_t a_tab, uint32_t n, uint32_t a_tmp) {
-  if (n <= NT * 3) flat_scan_fast<NT, 3>(a_tab, n, a_tmp);
-  else if (n <= NT * 5) flat_scan_fast<NT, 5>(a_tab, n, a_tmp);
-  else if (n <= NT * 9) flat_scan_fast<NT, 9>(a_tab, n, a_tmp);
-  else if (n <= NT * 11) flat_scan_fast<NT, 11>(a_tab, n, a_tmp);
-  else return false;
+__device__ __forceinline__ bool flat_scan_any(uint32_t a_tab, uint32_t n, uint32_t a_tmp, uint32_t t) {
+  if (n > NT * 11) return false;
+  const uint32_t per = (n <= NT * 3) ? 3u : (n <= NT * 5) ? 5u : (n <= NT * 9) ? 9u : 11u;
+  const uint32_t a0 = a_tab + t * per * 4;
+  const int rem = (int)n - (int)(t * per);
+  if (per == 3) flat_scan_fast<NT, 3>(a0, rem, a_tmp, t);
+  else if (per == 5) flat_scan_fast<NT, 5>(a0, rem, a_tmp, t);
+  else if (per == 9) flat_scan_fast<NT, 9>(a0, rem, a_tmp, t);
+  else flat_scan_fast<NT, 11>(a0, rem, a_tmp, t);
   return true;
 }
 
@@ -926,7 +929,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
       bool fscan = false;
       if constexpr (kFast) {
         const uint32_t a_cnt = f_sb + (uint32_t)(PTP * 4 + kWin * 8 + PT * 2);
-        fscan = flat_scan_any<T1_>(a_cnt, (uint32_t)(D * WH1_), smem_u32(s_tmp));
+        fscan = flat_scan_any<T1_>(a_cnt, (uint32_t)(D * WH1_), smem_u32(s_tmp), tid);
         if (fscan) {  // per digit: tile-local start b and end e (the row's pad word)
           for (int d = tid; d < D; d += T1_) {
             const uint32_t ar = a_cnt + d * (WH1_ * 4);
@@ -1452,7 +1455,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
       else {
         if constexpr (kFast) {
           const uint32_t a_cnt = f_sb + (uint32_t)PT * 8;
-          fscan = flat_scan_any<T2_>(a_cnt, (uint32_t)(D * WH2_), smem_u32(s_tmp));
+          fscan = flat_scan_any<T2_>(a_cnt, (uint32_t)(D * WH2_), smem_u32(s_tmp), tid);
           if (fscan) {  // per digit: index delta of this tile, cursor of the next (s_gcur is not read in between)
             for (int d = tid; d < D; d += T2_) {
               const uint32_t ar = a_cnt + d * (WH2_ * 4);
@@ -1537,7 +1540,8 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
           for (uint32_t i = threadIdx.x; i < n; i += T2_) put(i);
         }
       }
-      zero_u32(s_cnt, round4(D * WH2_));
+      if constexpr (kFast) zero_s<T2_>(f_sb + (uint32_t)PT * 8, (uint32_t)round4(D * WH2_), tid);
+      else zero_u32(s_cnt, round4(D * WH2_));
       if constexpr (!kW64)
         if (!fscan)
           for (int d = tid; d < D; d += T2_) s_gcur[d] += s_dtot[d];
@@ -1615,7 +1619,7 @@ __global__ void __launch_bounds__(WW3 * 32, WW3 > 16 ? 1 : 2) k_p3(const P3Args 
   __shared__ uint32_t s_uidx[2];
   __shared__ uint32_t s_fb[ML3];  // fine-bucket boundaries of the unit (relative positions)
 
-  const uint32_t tid = threadIdx.x, lane = lane_id(), w = warp_id();
+  const uint32_t tid = kOpt ? launder(threadIdx.x) : threadIdx.x, lane = tid & 31u, w = tid >> 5;  // (see k_p1)
   const uint32_t sh = (w & 1) << 4;
   const uint32_t nun = *a.n_units;
   zero_u32(s_cnt, round4(ML3 * WH3_) + (kMode == kRankSafe ? round4(ML3 * W3P_) : 0));
@@ -1672,7 +1676,7 @@ __global__ void __launch_bounds__(WW3 * 32, WW3 > 16 ? 1 : 2) k_p3(const P3Args 
     const uint32_t full = (o + n) & ~3u;
     uint32_t* buf = s_buf + b * CAP3P_;
     const uint32_t ti = full + tid;
-    const bool tail = tid < 4 && ti < o + n;
+    const bool tail = ((o + n) & 3u) != 0 && tid < 4 && ti < o + n;  // (first test uniform)
     uint32_t tv = 0;
     if (tail) tv = ldg_u32(gp - o + ti);
     tick(0);
@@ -1751,7 +1755,7 @@ __global__ void __launch_bounds__(WW3 * 32, WW3 > 16 ? 1 : 2) k_p3(const P3Args 
     {
       bool fscan = false;
       if constexpr (kFast)
-        fscan = flat_scan_any<TT>(f_sb + (uint32_t)(2 * CAP3P_ * 4), nloc * WH3_, smem_u32(s_tmp));
+        fscan = flat_scan_any<TT>(f_sb + (uint32_t)(2 * CAP3P_ * 4), nloc * WH3_, smem_u32(s_tmp), tid);
       if (!fscan) flat_bases_epi<WH3_, false>(s_cnt, (int)nloc, s_tmp, [](int, uint32_t, uint32_t) {});
     }
     {
@@ -1804,7 +1808,8 @@ __global__ void __launch_bounds__(WW3 * 32, WW3 > 16 ? 1 : 2) k_p3(const P3Args 
       const uint32_t tl = head + mid + tid;
       if (tl < n && tid < 4) t_e[tl] = buf[oo + tl];
     }
-    zero_u32(s_cnt, round4((int)nloc * WH3_));  // rows >= nloc were never touched
+    if constexpr (kFast) zero_s<TT>(f_sb + (uint32_t)(2 * CAP3P_ * 4), (uint32_t)round4((int)nloc * WH3_), tid);
+    else zero_u32(s_cnt, round4((int)nloc * WH3_));  // rows >= nloc were never touched
     __syncthreads();  // (D)
     tick(5);
   }
