@@ -1154,6 +1154,8 @@ struct DecR1 {
   static constexpr bool kSrcHigh = true;
   static constexpr bool kMatchRank = false;  // fine digits are spread: lane-ordered atomics
   __device__ __forceinline__ uint32_t digit(uint32_t r) const { return (r >> shB) & maskB; }
+  // the same without the mask: B is the top field of R1 (shB = L + c = 32 - b; clamped shift: b = 0 gives 0)
+  __device__ __forceinline__ uint32_t digit_top(uint32_t r) const { return __funnelshift_rc(r, 0u, (uint32_t)shB); }
   __device__ __forceinline__ uint32_t payload(uint32_t r, uint32_t h) const {
     return (((r >> L) & lvmask) << nbs) | (h << L) | (r & src_mask);
   }
@@ -1405,7 +1407,9 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
             uint32_t r = 0;
             if constexpr (kPre) r = valid ? pay[s] : 0u;
             else if (valid) r = lds_u32(a_rec + s * 128);
-            const uint32_t d = dec.digit(r);
+            uint32_t d;
+            if constexpr (Dec::kSrcHigh) d = dec.digit_top(r);
+            else d = dec.digit(r);
             if constexpr (Dec::kMatchRank) {  // one atomic per distinct digit of the slot
               const uint32_t m = __match_any_sync(kFull, valid ? d : 0xffffffffu);
               const uint32_t ld = __ffs(m) - 1;
@@ -1715,7 +1719,7 @@ __global__ void __launch_bounds__(WW3 * 32, WW3 > 16 ? 1 : 2) k_p3(const P3Args 
       if (!kPosFine || !wbnd) {  // (kPosFine: no fine-bucket boundary inside this warp's positions)
         fdone = true;
         const uint32_t a_rec = f_sb + (uint32_t)b * (CAP3P_ * 4) + (o + seg0 + lane) * 4;
-        const uint32_t nbs = a.nbs, lvm = kPosFine ? a.mask_c : a.lvmask, srcm = a.src_mask;
+        const uint32_t nbs = a.nbs, srcm = a.src_mask;
         const uint32_t lvadd = kPosFine ? (fcur << a.c) : (0u - lvoff);
 #pragma unroll
         for (int s = 0; s < K3; ++s) {
@@ -1724,7 +1728,8 @@ __global__ void __launch_bounds__(WW3 * 32, WW3 > 16 ? 1 : 2) k_p3(const P3Args 
           uint32_t r = 0;
           if constexpr (kPre) r = valid ? rr[s] : 0u;
           else if (valid) r = lds_u32(a_rec + s * 128);
-          const uint32_t lv = valid ? (((r >> nbs) & lvm) + lvadd) : 0u;
+          // (no mask: the low-digit field is R2's top field, DecR1::payload keeps c + gbits bits)
+          const uint32_t lv = valid ? ((r >> nbs) + lvadd) : 0u;
           uint32_t old = 0;
           if (valid) old = atoms_add(f_cw + lv * (uint32_t)(WH3_ * 4), f_inc);
           pk[s] = prmt(old, lv, f_selr);
