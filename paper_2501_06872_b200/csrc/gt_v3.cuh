@@ -308,8 +308,12 @@ __device__ __forceinline__ void flat_scan_fast(uint32_t a0, int rem, uint32_t a_
     v[i] = 0;
     if (i < rem) v[i] = lds_u32(a0 + i * 4);
   }
+  {  // both u16 fields summed as a packed pair first (each sum <= the tile size < 2^16)
+    uint32_t acc = 0;
 #pragma unroll
-  for (int i = 0; i < PER; ++i) s += (v[i] & 0xffffu) + (v[i] >> 16);
+    for (int i = 0; i < PER; ++i) acc += v[i];
+    s = (acc & 0xffffu) + (acc >> 16);
+  }
   uint32_t x = s;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
