@@ -690,14 +690,18 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
   // the next window lands by TMA after the end-of-tile barrier + proxy fence)
   static_assert(kWin * 8 >= PT * 2, "tag array must fit in the window");
   uint16_t* s_tag = reinterpret_cast<uint16_t*>(s_win);
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_mark + PT);                  // D * WH1_ (packed, digit-major)
+  // fixed-size scratch first (compile-time offsets from the base), the D-sized tables after it
+  uint32_t* s_tmp = reinterpret_cast<uint32_t*>(s_mark + PT);                  // 40
+  uint32_t* s_psrc = s_tmp + 40;                                               // CT1/PT + 4 (16-byte multiple with s_tmp)
+  static_assert((40 + CT1 / PT + 4) % 4 == 0, "s_cnt stays 16-byte aligned");
+  constexpr uint32_t kOffMark = PTP * 4 + kWin * 8, kOffTmp = kOffMark + PT * 2, kOffPsrc = kOffTmp + 160,
+                     kOffCnt = kOffPsrc + (CT1 / PT + 4) * 4;
+  uint32_t* s_cnt = s_psrc + (CT1 / PT + 4);                                   // D * WH1_ (packed, digit-major)
   uint32_t* s_scr = s_cnt + round4(D * WH1_);                                    // D * WP1_ (safe)
   uint32_t* s_gcur = s_scr + (kMode == kRankSafe ? round4(D * WP1_) : 0);        // D
   uint32_t* s_delta = s_gcur + D;                                              // D
   uint32_t* s_dtot = s_delta + D;                                              // D
   uint32_t* s_bh = reinterpret_cast<uint32_t*>(s_mark);                        // D (aliases the marks, dead after ranking)
-  uint32_t* s_tmp = s_dtot + D;                                                // 40
-  uint32_t* s_psrc = s_tmp + 40;                                               // CT1/PT + 2
   // kW64: s_g64 (D u64) spans s_gcur + s_delta (8-byte aligned: every region
   // before it is a multiple of 8 bytes), s_dtot holds the digit's tile end
   uint64_t* s_g64 = reinterpret_cast<uint64_t*>(s_gcur);
@@ -740,7 +744,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
   uint32_t f_sb = 0, f_cw = 0, f_inc = 0, f_selr = 0, f_sel16 = 0, f_delta = 0;
   if constexpr (kFast) {
     f_sb = launder(smem_u32(smem));
-    f_cw = launder(f_sb + (uint32_t)(PTP * 4 + kWin * 8 + PT * 2) + (w >> 1) * 4);  // this warp's word of every digit row
+    f_cw = launder(f_sb + kOffCnt + (w >> 1) * 4);  // this warp's word of every digit row
     f_inc = launder(1u << sh);
     f_selr = launder((w & 1) ? 0x5432u : 0x5410u);   // (old field, digit) -> digit << 16 | rank
     f_sel16 = launder((w & 1) ? 0x4432u : 0x4410u);  // this warp's u16 field of a counter word
@@ -867,7 +871,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
     if constexpr (kFast) {
       if (!wide) {
         fdone = true;
-        const uint32_t a_rec = f_sb + (o + iw + lane) * 4, a_mk = f_sb + (uint32_t)(PTP * 4 + kWin * 8) + (iw + lane) * 2;
+        const uint32_t a_rec = f_sb + (o + iw + lane) * 4, a_mk = f_sb + kOffMark + (iw + lane) * 2;
 #pragma unroll
         for (int s = 0; s < K; ++s) {
           pay[s] = lds_u32(a_rec + s * 128);
@@ -932,8 +936,8 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
     else {
       bool fscan = false;
       if constexpr (kFast) {
-        const uint32_t a_cnt = f_sb + (uint32_t)(PTP * 4 + kWin * 8 + PT * 2);
-        fscan = flat_scan_any<T1_>(a_cnt, (uint32_t)(D * WH1_), smem_u32(s_tmp), tid);
+        const uint32_t a_cnt = f_sb + kOffCnt;
+        fscan = flat_scan_any<T1_>(a_cnt, (uint32_t)(D * WH1_), f_sb + kOffTmp, tid);
         if (fscan) {  // per digit: tile-local start b and end e (the row's pad word)
           for (int d = tid; d < D; d += T1_) {
             const uint32_t ar = a_cnt + d * (WH1_ * 4);
@@ -1007,8 +1011,8 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
     else if constexpr (kW64) writeout_tag<T1_, PT>(a.out, s_buf, s_tag, s_g64, nout);
     else writeout_tag<T1_, PT>(a.out, s_buf, s_tag, s_delta, nout);
     if constexpr (kFast) {
-      zero_s<T1_, PT / 2>(f_sb + (uint32_t)(PTP * 4 + kWin * 8), tid);
-      zero_s<T1_>(f_sb + (uint32_t)(PTP * 4 + kWin * 8 + PT * 2), (uint32_t)round4(D * WH1_), tid);
+      zero_s<T1_, PT / 2>(f_sb + kOffMark, tid);
+      zero_s<T1_>(f_sb + kOffCnt, (uint32_t)round4(D * WH1_), tid);
       for (uint32_t d = tid; d < (uint32_t)D; d += T1_) {
         const uint32_t ag = f_delta - (uint32_t)D * 4 + d * 4;  // s_gcur += s_dtot
         sts_u32(ag, lds_u32(ag) + lds_u32(f_delta + (uint32_t)D * 4 + d * 4));
