@@ -976,12 +976,13 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
       auto fstage = [&](auto full_c) {
         constexpr bool kFull_ = decltype(full_c)::value;
 #pragma unroll
-        for (int c = 0; c < K; c += kStageG) {
-          uint32_t bw[kStageG];
+        constexpr int kG1 = 1;
+        for (int c = 0; c < K; c += kG1) {
+          uint32_t bw[kG1];
 #pragma unroll
-          for (int q = 0; q < kStageG; ++q) bw[q] = lds_u32(f_cw + (pk[c + q] >> 16) * (uint32_t)(WH1_ * 4));
+          for (int q = 0; q < kG1; ++q) bw[q] = lds_u32(f_cw + (pk[c + q] >> 16) * (uint32_t)(WH1_ * 4));
 #pragma unroll
-          for (int q = 0; q < kStageG; ++q)
+          for (int q = 0; q < kG1; ++q)
             if (kFull_ || iw + (c + q) * 32 + lane < n) {
               const uint32_t pos = prmt(bw[q], 0u, f_sel16) + (pk[c + q] & 0xffffu);
               sts_u32(f_sb + pos * 4, pay[c + q]);
@@ -1484,7 +1485,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
       }
       tick(3);
       if constexpr (kFast) {
-        constexpr int G = kPre ? kStageG : 1;
+        constexpr int G = 1;  // (batched base-word loads measured slower with these loops)
         auto fstage = [&](auto full_c) {
           constexpr bool kFull_ = decltype(full_c)::value;
 #pragma unroll
