@@ -342,17 +342,19 @@ __device__ __forceinline__ void flat_scan_fast(uint32_t a0, int rem, uint32_t a_
   }
   __syncthreads();
 }
-// Chunk length by table size; false if the table is larger than NT * 11 words.
-template <int NT>
+// Chunk length by table size; false if the table is larger than NT * 21 words.
+template <int NT, int kMaxPer = 11>
 __device__ __forceinline__ bool flat_scan_any(uint32_t a_tab, uint32_t n, uint32_t a_tmp, uint32_t t) {
-  if (n > NT * 11) return false;
-  const uint32_t per = (n <= NT * 3) ? 3u : (n <= NT * 5) ? 5u : (n <= NT * 9) ? 9u : 11u;
+  static_assert(kMaxPer == 11 || kMaxPer == 21, "instances: 3, 5, 9, 11 (and 21 for the 1024-digit forms)");
+  if (n > NT * kMaxPer) return false;
+  const uint32_t per = (n <= NT * 3) ? 3u : (n <= NT * 5) ? 5u : (n <= NT * 9) ? 9u : (kMaxPer == 11 || n <= NT * 11) ? 11u : 21u;
   const uint32_t a0 = a_tab + t * per * 4;
   const int rem = (int)n - (int)(t * per);
   if (per == 3) flat_scan_fast<NT, 3>(a0, rem, a_tmp, t);
   else if (per == 5) flat_scan_fast<NT, 5>(a0, rem, a_tmp, t);
   else if (per == 9) flat_scan_fast<NT, 9>(a0, rem, a_tmp, t);
-  else flat_scan_fast<NT, 11>(a0, rem, a_tmp, t);
+  else if (kMaxPer == 11 || per == 11) flat_scan_fast<NT, 11>(a0, rem, a_tmp, t);
+  else if constexpr (kMaxPer == 21) flat_scan_fast<NT, 21>(a0, rem, a_tmp, t);
   return true;
 }
 
@@ -937,7 +939,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
       bool fscan = false;
       if constexpr (kFast) {
         const uint32_t a_cnt = f_sb + kOffCnt;
-        fscan = flat_scan_any<T1_>(a_cnt, (uint32_t)(D * WH1_), f_sb + kOffTmp, tid);
+        fscan = flat_scan_any<T1_, (KK > 16 ? 21 : 11)>(a_cnt, (uint32_t)(D * WH1_), f_sb + kOffTmp, tid);
         if (fscan) {  // per digit: tile-local start b and end e (the row's pad word)
           for (int d = tid; d < D; d += T1_) {
             const uint32_t ar = a_cnt + d * (WH1_ * 4);
@@ -1274,13 +1276,15 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
   __syncthreads();
   uint32_t ph = 0;
   // kFast: rank and stage through 32-bit shared addresses off laundered registers (gt_common.cuh)
-  constexpr bool kFast = kOpt && kMode == kRankAtomic && kS64 && kIO == kIoPlain;
+  constexpr bool kFast = kOpt && kMode == kRankAtomic && kIO == kIoPlain;
+  // byte offset of the counter table: behind the pair array (kS64) or behind landing buffer + tags
+  constexpr uint32_t kOffCnt = kS64 ? (uint32_t)PT * 8 : (uint32_t)(PTP * 4 + PT * 2);
   uint32_t f_sb = 0, f_cw = 0, f_inc = 0, f_selr = 0, f_sel16 = 0, f_himask = 0, f_mul = 0, f_srcm = 0, f_delta = 0;
   bool f_up = true;
   if constexpr (kFast) {
     f_sb = launder(smem_u32(smem));
     f_delta = launder(smem_u32(s_delta));
-    f_cw = launder(f_sb + (uint32_t)PT * 8 + (w >> 1) * 4);  // this warp's word of every digit row
+    f_cw = launder(f_sb + kOffCnt + (w >> 1) * 4);  // this warp's word of every digit row
     f_inc = launder(1u << sh);
     f_selr = launder((w & 1) ? 0x5432u : 0x5410u);   // (old field, digit) -> digit << 16 | rank
     f_sel16 = launder((w & 1) ? 0x4432u : 0x4410u);  // this warp's u16 field of a counter word
@@ -1467,8 +1471,8 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
         });
       else {
         if constexpr (kFast) {
-          const uint32_t a_cnt = f_sb + (uint32_t)PT * 8;
-          fscan = flat_scan_any<T2_>(a_cnt, (uint32_t)(D * WH2_), smem_u32(s_tmp), tid);
+          const uint32_t a_cnt = f_sb + kOffCnt;
+          fscan = flat_scan_any<T2_, (KK > 16 ? 21 : 11)>(a_cnt, (uint32_t)(D * WH2_), smem_u32(s_tmp), tid);
           if (fscan) {  // per digit: index delta of this tile, cursor of the next (s_gcur is not read in between)
             for (int d = tid; d < D; d += T2_) {
               const uint32_t ar = a_cnt + d * (WH2_ * 4);
@@ -1495,8 +1499,15 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
             for (int q = 0; q < G; ++q) bw[q] = lds_u32(f_cw + (pk[c + q] >> 16) * (uint32_t)(WH2_ * 4));
 #pragma unroll
             for (int q = 0; q < G; ++q)
-              if (kFull_ || ((uint32_t)(c + q) * 32 < per && iw + (c + q) * 32 + lane < n))
-                sts_v2(f_sb + (prmt(bw[q], 0u, f_sel16) + (pk[c + q] & 0xffffu)) * 8, pay[c + q], pk[c + q] >> 16);
+              if (kFull_ || ((uint32_t)(c + q) * 32 < per && iw + (c + q) * 32 + lane < n)) {
+                const uint32_t pos = prmt(bw[q], 0u, f_sel16) + (pk[c + q] & 0xffffu);
+                if constexpr (kS64) {
+                  sts_v2(f_sb + pos * 8, pay[c + q], pk[c + q] >> 16);
+                } else {
+                  sts_u32(f_sb + pos * 4, pay[c + q]);
+                  sts_u16(f_sb + (uint32_t)(PTP * 4) + pos * 2, pk[c + q] >> 16);
+                }
+              }
           }
         };
         if (n == (uint32_t)PT) fstage(std::true_type{});
@@ -1522,19 +1533,21 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
       __syncthreads();  // (C)
       tick(4);
       if constexpr (kFast) {
-        const uint32_t a_st = f_sb + tid * 8;
+        const uint32_t a_st = f_sb + tid * (kS64 ? 8 : 4), a_tg = f_sb + (uint32_t)(PTP * 4) + tid * 2;
         uint32_t* outp = out + tid;
+        auto put = [&](uint32_t k) {
+          if constexpr (kS64) {
+            const uint2 v = lds_v2(a_st + k * (T2_ * 8));
+            outp[lds_u32(f_delta + v.y * 4) + k * T2_] = v.x;
+          } else {
+            outp[lds_u32(f_delta + lds_u16(a_tg + k * (T2_ * 2)) * 4) + k * T2_] = lds_u32(a_st + k * (T2_ * 4));
+          }
+        };
         if (n == (uint32_t)PT) {
 #pragma unroll
-          for (int k = 0; k < PT / T2_; ++k) {
-            const uint2 v = lds_v2(a_st + k * (T2_ * 8));
-            outp[lds_u32(f_delta + v.y * 4) + k * T2_] = v.x;
-          }
+          for (int k = 0; k < PT / T2_; ++k) put(k);
         } else {
-          for (uint32_t i = tid, k = 0; i < n; i += T2_, ++k) {
-            const uint2 v = lds_v2(a_st + k * (T2_ * 8));
-            outp[lds_u32(f_delta + v.y * 4) + k * T2_] = v.x;
-          }
+          for (uint32_t i = tid, k = 0; i < n; i += T2_, ++k) put(k);
         }
       } else if constexpr (kS64) {
         writeout_pair<T2_, PT>(out, s_st64, s_delta, n);
@@ -1553,7 +1566,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p2(const uint32_t* __restric
           for (uint32_t i = threadIdx.x; i < n; i += T2_) put(i);
         }
       }
-      if constexpr (kFast) zero_s<T2_>(f_sb + (uint32_t)PT * 8, (uint32_t)round4(D * WH2_), tid);
+      if constexpr (kFast) zero_s<T2_>(f_sb + kOffCnt, (uint32_t)round4(D * WH2_), tid);
       else zero_u32(s_cnt, round4(D * WH2_));
       if constexpr (!kW64)
         if (!fscan)
