@@ -742,9 +742,11 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
   __syncthreads();
 
   // kFast: rank, stage and write-out through 32-bit shared addresses off laundered registers (gt_common.cuh)
-  constexpr bool kFast = kOpt && kMode == kRankAtomic && !kW64 && !kSlab;
+  // (kFastRS: the rank and stage loops, also for 64-bit positions; kFast: scan, write-out and zeroing too)
+  constexpr bool kFastRS = kOpt && kMode == kRankAtomic && !kSlab;
+  constexpr bool kFast = kFastRS && !kW64;
   uint32_t f_sb = 0, f_cw = 0, f_inc = 0, f_selr = 0, f_sel16 = 0, f_delta = 0;
-  if constexpr (kFast) {
+  if constexpr (kFastRS) {
     f_sb = launder(smem_u32(smem));
     f_cw = launder(f_sb + kOffCnt + (w >> 1) * 4);  // this warp's word of every digit row
     f_inc = launder(1u << sh);
@@ -870,7 +872,7 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
       pay[s] = ((dst & a.low_mask) << a.L) | (src & a.src_mask);
     };
     bool fdone = false;
-    if constexpr (kFast) {
+    if constexpr (kFastRS) {
       if (!wide) {
         fdone = true;
         const uint32_t a_rec = f_sb + (o + iw + lane) * 4, a_mk = f_sb + kOffMark + (iw + lane) * 2;
@@ -973,12 +975,12 @@ __global__ void __launch_bounds__(WW * 32, kMinB) k_p1(const P1Args a) {
     h_prev = h_last;
     // stage payloads and global indices by digit (base words loaded in groups
     // of kStageG before their stores)
-    if constexpr (kFast) {
+    if constexpr (kFastRS) {
       const uint32_t a_tag = f_sb + (uint32_t)(PTP * 4);
       auto fstage = [&](auto full_c) {
         constexpr bool kFull_ = decltype(full_c)::value;
+        constexpr int kG1 = 1;  // (batched base-word loads measured slower with these loops)
 #pragma unroll
-        constexpr int kG1 = 1;
         for (int c = 0; c < K; c += kG1) {
           uint32_t bw[kG1];
 #pragma unroll
