@@ -1745,20 +1745,27 @@ __global__ void __launch_bounds__(WW3 * 32, WW3 > 16 ? 1 : 2) k_p3(const P3Args 
         const uint32_t a_rec = f_sb + (uint32_t)b * (CAP3P_ * 4) + (o + seg0 + lane) * 4;
         const uint32_t nbs = a.nbs, srcm = a.src_mask;
         const uint32_t lvadd = kPosFine ? (fcur << a.c) : (0u - lvoff);
+        // all of this warp's positions hold records (every warp but the unit's last one or two):
+        // no per-lane validity tests
+        auto frank = [&](auto all_c) {
+          constexpr bool kAll = decltype(all_c)::value;
 #pragma unroll
-        for (int s = 0; s < K3; ++s) {
-          if (kBal && (uint32_t)s * 32 >= per) break;
-          const bool valid = seg0 + s * 32 + lane < n;
-          uint32_t r = 0;
-          if constexpr (kPre) r = valid ? rr[s] : 0u;
-          else if (valid) r = lds_u32(a_rec + s * 128);
-          // (no mask: the low-digit field is R2's top field, DecR1::payload keeps c + gbits bits)
-          const uint32_t lv = valid ? ((r >> nbs) + lvadd) : 0u;
-          uint32_t old = 0;
-          if (valid) old = atoms_add(f_cw + lv * (uint32_t)(WH3_ * 4), f_inc);
-          pk[s] = prmt(old, lv, f_selr);
-          rr[s] = r & srcm;
-        }
+          for (int s = 0; s < K3; ++s) {
+            if (kBal && (uint32_t)s * 32 >= per) break;
+            const bool valid = kAll || seg0 + s * 32 + lane < n;
+            uint32_t r = 0;
+            if constexpr (kPre) r = valid ? rr[s] : 0u;
+            else if (valid) r = lds_u32(a_rec + s * 128);
+            // (no mask: the low-digit field is R2's top field, DecR1::payload keeps c + gbits bits)
+            const uint32_t lv = valid ? ((r >> nbs) + lvadd) : 0u;
+            uint32_t old = 0;
+            if (valid) old = atoms_add(f_cw + lv * (uint32_t)(WH3_ * 4), f_inc);
+            pk[s] = prmt(old, lv, f_selr);
+            rr[s] = r & srcm;
+          }
+        };
+        if (seg0 + per <= n) frank(std::true_type{});
+        else frank(std::false_type{});
       }
     }
 #pragma unroll
@@ -1797,18 +1804,23 @@ __global__ void __launch_bounds__(WW3 * 32, WW3 > 16 ? 1 : 2) k_p3(const P3Args 
     const uint32_t oo = align_items_u32(t_e);  // staging offset matching the output's 16B alignment
     if constexpr (kFast) {
       const uint32_t a_out = f_sb + (uint32_t)b * (CAP3P_ * 4) + oo * 4;
+      auto fstage3 = [&](auto all_c) {
+        constexpr bool kAll = decltype(all_c)::value;
 #pragma unroll
-      for (int c = 0; c < K3; c += kG3) {
-        if (kBal && (uint32_t)c * 32 >= per) break;
-        uint32_t bw[kG3];
+        for (int c = 0; c < K3; c += kG3) {
+          if (kBal && (uint32_t)c * 32 >= per) break;
+          uint32_t bw[kG3];
 #pragma unroll
-        for (int q = 0; q < kG3; ++q)
-          if (!kBal || (uint32_t)(c + q) * 32 < per) bw[q] = lds_u32(f_cw + (pk[c + q] >> 16) * (uint32_t)(WH3_ * 4));
+          for (int q = 0; q < kG3; ++q)
+            if (!kBal || (uint32_t)(c + q) * 32 < per) bw[q] = lds_u32(f_cw + (pk[c + q] >> 16) * (uint32_t)(WH3_ * 4));
 #pragma unroll
-        for (int q = 0; q < kG3; ++q)
-          if ((!kBal || (uint32_t)(c + q) * 32 < per) && seg0 + (c + q) * 32 + lane < n)
-            sts_u32(a_out + (prmt(bw[q], 0u, f_sel16) + (pk[c + q] & 0xffffu)) * 4, rr[c + q]);
-      }
+          for (int q = 0; q < kG3; ++q)
+            if ((!kBal || (uint32_t)(c + q) * 32 < per) && (kAll || seg0 + (c + q) * 32 + lane < n))
+              sts_u32(a_out + (prmt(bw[q], 0u, f_sel16) + (pk[c + q] & 0xffffu)) * 4, rr[c + q]);
+        }
+      };
+      if (seg0 + per <= n) fstage3(std::true_type{});
+      else fstage3(std::false_type{});
     }
 #pragma unroll
     for (int c = 0; c < K3; c += kG3) {  // base words of kG3 items loaded before their stores
