@@ -1,9 +1,9 @@
 // gt_v3.cuh — lean three-level stable partition (compact 4-byte records).
 //
-// Same contract as gt_kernels.cuh (CSR -> CSC, every list ascending by source =
-// transpose_oracle, graph.py:136-148 = a stable counting sort of the CSR edge
-// stream by destination), re-planned so that every level is one streaming
-// partition pass with a short instruction path per record:
+// Contract: CSR -> CSC, every list ascending by source (= transpose_oracle,
+// graph.py:136-148 = a stable counting sort of the CSR edge stream by
+// destination), planned so that every level is one streaming partition pass
+// with a short instruction path per record:
 //
 //   L1  k_c1 count  -> lookback scan -> k_p1 place
 //         CSR edges -> R1 = (dst_low << L | src_low) grouped by coarse digit A,
@@ -23,6 +23,17 @@
 // Ranking is the one of gt_common.cuh (warp-private counters, lane-ordered
 // shared atomics or the safe OR-mask mode); stability composes over levels, so
 // each CSC list ends in CSR order = ascending source.
+//
+// Hot loops (kOpt, the default with the atomic rank mode): the rank, stage and
+// write-out loops of the three place kernels and their per-tile scan address
+// shared memory through 32-bit shared addresses off registers that went through
+// an identity shuffle (gt_common.cuh: launder, lds_* / sts_* / atoms_add), with
+// immediate offsets.  Plain pointer code made ptxas re-derive the shared window
+// address (S2UR SR_CgaCtaId + UMOV + ULEA), kernel parameters and the thread
+// index in front of every access: two thirds of the instructions between two
+// rank atomics.  The pointer-based loops remain for the safe
+// rank mode, the wide / slab forms' remaining phases, warps that hold a
+// source-high boundary, and as experiment bit 4096 (A/B).
 #pragma once
 #include <algorithm>
 
@@ -1764,8 +1775,13 @@ __global__ void __launch_bounds__(WW3 * 32, WW3 > 16 ? 1 : 2) k_p3(const P3Args 
             rr[s] = r & srcm;
           }
         };
-        if (seg0 + per <= n) frank(std::true_type{});
-        else frank(std::false_type{});
+        // (position-derived fine buckets, C4: one copy — the second one spills)
+        if constexpr (kPosFine) {
+          frank(std::false_type{});
+        } else {
+          if (seg0 + per <= n) frank(std::true_type{});
+          else frank(std::false_type{});
+        }
       }
     }
 #pragma unroll
@@ -1819,8 +1835,12 @@ __global__ void __launch_bounds__(WW3 * 32, WW3 > 16 ? 1 : 2) k_p3(const P3Args 
               sts_u32(a_out + (prmt(bw[q], 0u, f_sel16) + (pk[c + q] & 0xffffu)) * 4, rr[c + q]);
         }
       };
-      if (seg0 + per <= n) fstage3(std::true_type{});
-      else fstage3(std::false_type{});
+      if constexpr (kPosFine) {
+        fstage3(std::false_type{});
+      } else {
+        if (seg0 + per <= n) fstage3(std::true_type{});
+        else fstage3(std::false_type{});
+      }
     }
 #pragma unroll
     for (int c = 0; c < K3; c += kG3) {  // base words of kG3 items loaded before their stores
